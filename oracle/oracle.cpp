@@ -591,6 +591,17 @@ int orc_schedule_depth(int n, const int* id, const int* phase, const int* depth,
   return nb;
 }
 
+uint64_t orc_digest_encoded(const int32_t* toks, int64_t ntok, const float* data, int64_t ndata, int count) {
+  uint64_t h = 1469598103934665603ull;
+  int64_t ti = 0, di = 0;
+  for (int i = 0; i < count; ++i) {
+    HV v;
+    if (!decode(toks, ntok, ti, data, ndata, di, v)) return 0;
+    digest(v, h);
+  }
+  return h;
+}
+
 float orc_unary(int which, float x) {
   switch (which) {
     case 0: return std::exp(x);

@@ -71,6 +71,9 @@ int orc_schedule_depth(int n, const int* id, const int* phase, const int* depth,
                        const int* ghost, const int* nshared, const int64_t* shared_refs,
                        int* batches, int* order, long* ops);
 
+/* FNV-1a digest of `count` encoded values (same layout as the digests above). */
+uint64_t orc_digest_encoded(const int32_t* toks, int64_t ntok, const float* data, int64_t ndata, int count);
+
 /* Scalar restatements of the libm calls on the path, for unit tests: 0 expf, 1 tanhf,
  * 2 sigmoid 1/(1+expf(-x)). */
 float orc_unary(int which, float x);

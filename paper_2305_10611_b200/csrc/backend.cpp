@@ -1,0 +1,784 @@
+// backend.cpp — device arena, plan compiler/registry and the host half of exec_batched.
+//
+// Reference interfaces replaced (proj/include/mbatch/backend.hpp):
+//   Arena (:63-88)            -> HBM arena in one CUDA VMM reservation (stable offsets)
+//   exec_primop (:92-93)      -> one-step plan on the FP32 plan VM (kernels_vm.cu)
+//   exec_batched (:149-150)   -> prepare_batch (validation, gather accounting, allocation in the
+//                                reference's order) + issue_batch (device launch)
+// Error texts are the reference's, so callers matching on them keep working.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdlib>
+#include <cstring>
+#include <sstream>
+
+#include "ctx.h"
+#include "tc.h"
+
+namespace mbx {
+
+std::atomic<int64_t> g_launches{0};
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw mbatch::Error(std::string("cuda error in ") + what + ": " + cudaGetErrorString(e));
+}
+void cu_check(CUresult r, const char* what) {
+  if (r != CUDA_SUCCESS) throw mbatch::Error(std::string("cuda driver error ") + std::to_string(int(r)) + " in " + what);
+}
+
+float* arena_ptr(mbx_ctx* c) { return reinterpret_cast<float*>(c->base); }
+
+// Driver VMM entry points, resolved through the runtime (cudaGetDriverEntryPoint) so the library
+// has no link-time dependency on libcuda and loads on GPU-less hosts.
+struct VmmApi {
+  decltype(&cuMemCreate) create = nullptr;
+  decltype(&cuMemMap) map = nullptr;
+  decltype(&cuMemSetAccess) set_access = nullptr;
+  decltype(&cuMemAddressReserve) reserve = nullptr;
+  decltype(&cuMemAddressFree) addr_free = nullptr;
+  decltype(&cuMemUnmap) unmap = nullptr;
+  decltype(&cuMemRelease) release = nullptr;
+  decltype(&cuMemGetAllocationGranularity) granularity = nullptr;
+};
+
+static const VmmApi& vmm() {
+  static VmmApi api = [] {
+    VmmApi a;
+    auto get = [](const char* name, void** fn) {
+      cudaDriverEntryPointQueryResult q;
+      cuda_check(cudaGetDriverEntryPoint(name, fn, cudaEnableDefault, &q), name);
+      if (q != cudaDriverEntryPointSuccess || !*fn) throw mbatch::Error(std::string("driver entry point missing: ") + name);
+    };
+    get("cuMemCreate", reinterpret_cast<void**>(&a.create));
+    get("cuMemMap", reinterpret_cast<void**>(&a.map));
+    get("cuMemSetAccess", reinterpret_cast<void**>(&a.set_access));
+    get("cuMemAddressReserve", reinterpret_cast<void**>(&a.reserve));
+    get("cuMemAddressFree", reinterpret_cast<void**>(&a.addr_free));
+    get("cuMemUnmap", reinterpret_cast<void**>(&a.unmap));
+    get("cuMemRelease", reinterpret_cast<void**>(&a.release));
+    get("cuMemGetAllocationGranularity", reinterpret_cast<void**>(&a.granularity));
+    return a;
+  }();
+  return api;
+}
+
+void arena_init(mbx_ctx* c) {
+  if (c->dry) return;
+  const VmmApi& api = vmm();
+  CUmemAllocationProp prop{};
+  prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+  prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  prop.location.id = c->device;
+  size_t gran = 0;
+  cu_check(api.granularity(&gran, &prop, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED), "cuMemGetAllocationGranularity");
+  c->chunk_bytes = ((size_t(256) << 20) + gran - 1) / gran * gran;
+  c->reserve_bytes = size_t(128) << 30;  // 128 GiB of address space; physical memory on demand
+  cu_check(api.reserve(&c->base, c->reserve_bytes, 0, 0, 0), "cuMemAddressReserve");
+}
+
+void arena_release(mbx_ctx* c) {
+  if (c->dry || !c->base) return;
+  const VmmApi& api = vmm();
+  for (size_t k = 0; k < c->chunks.size(); ++k) {
+    api.unmap(c->base + k * c->chunk_bytes, c->chunk_bytes);
+    api.release(c->chunks[k]);
+  }
+  c->chunks.clear();
+  api.addr_free(c->base, c->reserve_bytes);
+  c->base = 0;
+}
+
+static void arena_map_to(mbx_ctx* c, size_t bytes) {
+  if (c->dry) return;
+  const VmmApi& api = vmm();
+  while (c->mapped_bytes < bytes) {
+    if (c->mapped_bytes + c->chunk_bytes > c->reserve_bytes) throw mbatch::Error("arena reservation exhausted");
+    CUmemAllocationProp prop{};
+    prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+    prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    prop.location.id = c->device;
+    CUmemGenericAllocationHandle h;
+    cu_check(api.create(&h, c->chunk_bytes, &prop, 0), "cuMemCreate");
+    cu_check(api.map(c->base + c->mapped_bytes, c->chunk_bytes, 0, h, 0), "cuMemMap");
+    CUmemAccessDesc acc{};
+    acc.location = prop.location;
+    acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+    cu_check(api.set_access(c->base + c->mapped_bytes, c->chunk_bytes, &acc, 1), "cuMemSetAccess");
+    c->chunks.push_back(h);
+    c->mapped_bytes += c->chunk_bytes;
+  }
+}
+
+int64_t arena_alloc(mbx_ctx* c, int64_t floats) {
+  MBATCH_CHECK(floats >= 0, "negative allocation");
+  int64_t off = c->used;
+  size_t need = size_t(off + floats) * sizeof(float);
+  if (need > c->mapped_bytes) arena_map_to(c, need);
+  c->used += floats;
+  return off;
+}
+
+void arena_check(const mbx_ctx* c, int64_t off, int64_t n) {
+  MBATCH_CHECK(off >= 0 && off + n <= c->used, "tensor handle out of arena bounds");
+}
+
+void meta_reserve(mbx_ctx* c, size_t bytes) {
+  bytes = (bytes + 7) & ~size_t(7);
+  if (c->meta.cursor + bytes <= c->meta.cap) return;
+  meta_commit(c);
+  if (!c->dry) cuda_check(cudaStreamSynchronize(c->stream), "meta recycle");
+  c->meta.cursor = c->meta.committed = 0;
+  if (bytes > c->meta.cap) {
+    size_t cap = std::max(bytes, c->meta.cap * 2);
+    if (c->dry) {
+      std::free(c->meta.host);
+      c->meta.host = static_cast<char*>(std::malloc(cap));
+    } else {
+      if (c->meta.host) cudaFreeHost(c->meta.host);
+      if (c->meta.dev) cudaFree(c->meta.dev);
+      cuda_check(cudaMallocHost(&c->meta.host, cap), "meta host");
+      cuda_check(cudaMalloc(&c->meta.dev, cap), "meta dev");
+    }
+    c->meta.cap = cap;
+  }
+}
+
+size_t meta_stage(mbx_ctx* c, const void* src, size_t bytes) {
+  size_t b8 = (bytes + 7) & ~size_t(7);
+  if (c->meta.cursor + b8 > c->meta.cap) meta_reserve(c, b8);
+  size_t off = c->meta.cursor;
+  if (bytes) std::memcpy(c->meta.host + off, src, bytes);
+  c->meta.cursor += b8;
+  return off;
+}
+
+void meta_commit(mbx_ctx* c) {
+  if (c->dry) {
+    c->meta.committed = c->meta.cursor;
+    return;
+  }
+  if (c->meta.cursor > c->meta.committed) {
+    cuda_check(cudaMemcpyAsync(c->meta.dev + c->meta.committed, c->meta.host + c->meta.committed,
+                               c->meta.cursor - c->meta.committed, cudaMemcpyHostToDevice, c->stream),
+               "meta H2D");
+    c->meta.committed = c->meta.cursor;
+  }
+}
+
+void ensure_input_stage(mbx_ctx* c, size_t floats) {
+  if (floats <= c->in_cap) return;
+  size_t cap = std::max(floats, c->in_cap * 2);
+  if (c->dry) {
+    std::free(c->in_host);
+    c->in_host = static_cast<float*>(std::malloc(cap * sizeof(float)));
+  } else {
+    cuda_check(cudaStreamSynchronize(c->stream), "input stage grow");
+    if (c->in_host) cudaFreeHost(c->in_host);
+    cuda_check(cudaMallocHost(&c->in_host, cap * sizeof(float)), "input stage");
+  }
+  c->in_cap = cap;
+}
+
+void ensure_d2h(mbx_ctx* c, size_t floats) {
+  if (c->dry || floats <= c->d2h_cap) return;
+  cuda_check(cudaStreamSynchronize(c->stream), "d2h grow");
+  size_t cap = std::max(floats, c->d2h_cap * 2);
+  if (c->d2h_host) cudaFreeHost(c->d2h_host);
+  if (c->d2h_dev) cudaFree(c->d2h_dev);
+  cuda_check(cudaMallocHost(&c->d2h_host, cap * sizeof(float)), "d2h host");
+  cuda_check(cudaMalloc(&c->d2h_dev, cap * sizeof(float)), "d2h dev");
+  c->d2h_cap = cap;
+}
+
+// ---------------------------------------------------------------------------------------------
+// Plan compiler: ExecutablePlan -> DPlan (shapes, temp layout, column-split analysis)
+
+namespace {
+
+using mbatch::backend::ExecutablePlan;
+using mbatch::backend::OpCode;
+using mbatch::backend::PlanRef;
+using mbatch::backend::PlanStep;
+using mbatch::backend::Shape;
+
+Shape ref_shape(const ExecutablePlan& p, const PlanRef& r, size_t cur_step) {
+  Shape s;
+  switch (r.kind) {
+    case PlanRef::Kind::kShared:
+      MBATCH_CHECK(r.index >= 0 && size_t(r.index) < p.shared_shapes.size(), "plan: shared ref out of range");
+      s = p.shared_shapes[r.index];
+      break;
+    case PlanRef::Kind::kBatched:
+      MBATCH_CHECK(r.index >= 0 && size_t(r.index) < p.batched_shapes.size(), "plan: batched ref out of range");
+      s = p.batched_shapes[r.index];
+      break;
+    case PlanRef::Kind::kTemp:
+      MBATCH_CHECK(r.index >= 0 && size_t(r.index) < cur_step, "plan: temp ref to a later step");
+      s = p.steps[r.index].out_shape;
+      break;
+  }
+  if (r.cols >= 0) {
+    MBATCH_CHECK(s.rows == 1, "column slices require row vectors");
+    MBATCH_CHECK(r.col_off >= 0 && r.col_off + r.cols <= s.cols, "plan: column slice out of range");
+    s = Shape{1, r.cols};
+  }
+  return s;
+}
+
+DRef to_dref(const ExecutablePlan& p, const PlanRef& r, size_t cur) {
+  Shape s = ref_shape(p, r, cur);
+  DRef d{};
+  d.kind = r.kind == PlanRef::Kind::kShared ? kRefShared : r.kind == PlanRef::Kind::kBatched ? kRefBatched : kRefTemp;
+  d.index = r.index;
+  d.col_off = r.col_off;
+  d.cols = r.cols;
+  d.rows_r = s.rows;
+  d.cols_r = s.cols;
+  return d;
+}
+
+void split_analysis(const ExecutablePlan& p, DPlan& d) {
+  const size_t n = p.steps.size();
+  d.unit = 0;
+  if (p.outputs.empty()) return;
+  Shape o0 = ref_shape(p, p.outputs[0], n);
+  if (o0.rows != 1) return;
+  const int U = o0.cols;
+  std::vector<bool> capable(n, false), full(n, false);
+  for (size_t s = 0; s < n; ++s) {
+    const PlanStep& st = p.steps[s];
+    if (st.out_shape.rows != 1) continue;
+    if (st.kind == PlanStep::Kind::kFusedDense) {
+      bool ok = true;
+      for (size_t w = 1; w < st.ins.size(); ++w) ok = ok && ref_shape(p, st.ins[w], s).cols == U;
+      capable[s] = ok;
+    } else if (st.kind == PlanStep::Kind::kChain) {
+      capable[s] = st.out_shape.cols == U;
+    } else if (st.op == OpCode::kDense) {
+      capable[s] = st.out_shape.cols == U;
+    } else if (mbatch::backend::is_elementwise(st.op)) {
+      capable[s] = st.out_shape.cols == U;
+    }
+  }
+  auto temp_ins = [&](size_t s) {
+    std::vector<std::pair<PlanRef, bool>> v;  // (ref, is_dense_A)
+    const PlanStep& st = p.steps[s];
+    for (size_t i = 0; i < st.ins.size(); ++i) {
+      bool dense_a = (st.kind == PlanStep::Kind::kFusedDense || (st.kind == PlanStep::Kind::kOp && st.op == OpCode::kDense)) && i == 0;
+      if (st.ins[i].kind == PlanRef::Kind::kTemp) v.push_back({st.ins[i], dense_a});
+    }
+    for (auto& l : st.chain)
+      if (l.rhs && l.rhs->kind == PlanRef::Kind::kTemp) v.push_back({*l.rhs, false});
+    return v;
+  };
+  // A split consumer may read a producer's columns only if the column maps line up.
+  auto aligned = [&](const PlanRef& r) {
+    const PlanStep& prod = p.steps[r.index];
+    if (r.cols < 0) return prod.out_shape.cols == U;
+    if (r.cols != U || r.col_off % U != 0) return false;
+    if (prod.kind == PlanStep::Kind::kFusedDense) {
+      int col = 0;
+      for (size_t w = 1; w < prod.ins.size(); ++w) {
+        if (col == r.col_off) return true;
+        col += ref_shape(p, prod.ins[w], r.index).cols;
+      }
+      return false;
+    }
+    return prod.out_shape.cols == U && r.col_off == 0;
+  };
+  bool changed = true;
+  while (changed) {
+    changed = false;
+    for (size_t s = 0; s < n; ++s) {
+      bool split = capable[s] && !full[s];
+      for (auto& [r, dense_a] : temp_ins(s)) {
+        bool need = dense_a || !split || !aligned(r);
+        if (need && !full[r.index]) { full[r.index] = true; changed = true; }
+      }
+    }
+    for (size_t k = 0; k < p.outputs.size(); ++k) {
+      const PlanRef& r = p.outputs[k];
+      if (r.kind != PlanRef::Kind::kTemp) continue;
+      if (!aligned(r) && !full[r.index]) { full[r.index] = true; changed = true; }
+    }
+  }
+  bool any_dense_split = false;
+  for (size_t s = 0; s < n; ++s) {
+    d.steps[s].split = capable[s] && !full[s];
+    const PlanStep& st = p.steps[s];
+    if (d.steps[s].split && (st.kind == PlanStep::Kind::kFusedDense || (st.kind == PlanStep::Kind::kOp && st.op == OpCode::kDense)))
+      any_dense_split = true;
+  }
+  for (size_t k = 0; k < p.outputs.size(); ++k) {
+    const PlanRef& r = p.outputs[k];
+    d.out_split[k] = r.kind == PlanRef::Kind::kTemp && d.steps[r.index].split && aligned(r);
+  }
+  if (any_dense_split) d.unit = U;
+  else
+    for (size_t s = 0; s < n; ++s) d.steps[s].split = 0;
+}
+
+}  // namespace
+
+DPlan compile_plan(const ExecutablePlan& p, int64_t& temp_per_inst, std::vector<Shape>& out_shapes) {
+  DPlan d{};
+  MBATCH_CHECK(p.steps.size() <= size_t(kMaxSteps), "plan: too many steps for the device plan VM");
+  MBATCH_CHECK(p.outputs.size() <= size_t(kMaxOut), "plan: too many outputs");
+  MBATCH_CHECK(p.shared_shapes.size() <= size_t(kMaxShared), "plan: too many shared inputs");
+  MBATCH_CHECK(p.batched_shapes.size() <= size_t(kMaxBatched), "plan: too many batched inputs");
+  d.ghost = p.ghost;
+  d.nsteps = int(p.steps.size());
+  d.nout = int(p.outputs.size());
+  d.nshared = int(p.shared_shapes.size());
+  d.nbatched = int(p.batched_shapes.size());
+  int64_t off = 0;
+  temp_per_inst = 0;
+  for (size_t s = 0; s < p.steps.size(); ++s) {
+    const PlanStep& st = p.steps[s];
+    DStep& ds = d.steps[s];
+    ds.kind = st.kind == PlanStep::Kind::kOp ? kStepOp : st.kind == PlanStep::Kind::kFusedDense ? kStepFused : kStepChain;
+    ds.op = int(st.op);
+    ds.rows = st.out_shape.rows;
+    ds.cols = st.out_shape.cols;
+    MBATCH_CHECK(st.ins.size() <= size_t(kMaxIn) && st.chain.size() <= size_t(kMaxChain), "plan: step too wide");
+    ds.nin = int(st.ins.size());
+    ds.nchain = int(st.chain.size());
+    std::vector<Shape> in_shapes;
+    for (size_t i = 0; i < st.ins.size(); ++i) {
+      ds.ins[i] = to_dref(p, st.ins[i], s);
+      in_shapes.push_back(Shape{ds.ins[i].rows_r, ds.ins[i].cols_r});
+    }
+    switch (st.kind) {
+      case PlanStep::Kind::kOp: {
+        MBATCH_CHECK(st.op != OpCode::kFill, "plan: fill is not a batched step");
+        Shape expect = mbatch::backend::infer_shape(st.op, in_shapes);
+        MBATCH_CHECK(expect == st.out_shape, std::string(mbatch::backend::op_name(st.op)) + ": output shape mismatch");
+        break;
+      }
+      case PlanStep::Kind::kFusedDense: {
+        MBATCH_CHECK(st.ins.size() >= 2 && in_shapes[0].rows == 1, "plan: fused dense needs (1,k) x weights");
+        int total = 0;
+        for (size_t w = 1; w < in_shapes.size(); ++w) {
+          MBATCH_CHECK(in_shapes[w].rows == in_shapes[0].cols, "dense: shape mismatch, expected (m,k)x(k,n), got " +
+                                                                    in_shapes[0].str() + " x " + in_shapes[w].str());
+          total += in_shapes[w].cols;
+        }
+        MBATCH_CHECK(st.out_shape == (Shape{1, total}), "dense: output shape mismatch");
+        break;
+      }
+      case PlanStep::Kind::kChain: {
+        MBATCH_CHECK(st.ins.size() == 1 && in_shapes[0] == st.out_shape, "plan: chain base shape mismatch");
+        for (size_t l = 0; l < st.chain.size(); ++l) {
+          MBATCH_CHECK(mbatch::backend::is_elementwise(st.chain[l].op), "op not fusable in an elementwise chain");
+          ds.chain[l].op = int(st.chain[l].op);
+          ds.chain[l].has_rhs = st.chain[l].rhs.has_value();
+          if (st.chain[l].rhs) {
+            ds.chain[l].rhs = to_dref(p, *st.chain[l].rhs, s);
+            MBATCH_CHECK(ds.chain[l].rhs.rows_r * ds.chain[l].rhs.cols_r == st.out_shape.size(),
+                         std::string(mbatch::backend::op_name(st.chain[l].op)) + ": shape mismatch in chain");
+          }
+        }
+        break;
+      }
+    }
+    ds.temp_off = int32_t(off);
+    off += st.out_shape.size();
+  }
+  d.temp_floats = int32_t(off);
+  temp_per_inst = off;
+  out_shapes.clear();
+  for (size_t k = 0; k < p.outputs.size(); ++k) {
+    MBATCH_CHECK(p.outputs[k].kind == PlanRef::Kind::kTemp, "plan outputs must be step results");
+    d.outputs[k] = to_dref(p, p.outputs[k], p.steps.size());
+    out_shapes.push_back(Shape{d.outputs[k].rows_r, d.outputs[k].cols_r});
+  }
+  split_analysis(p, d);
+  return d;
+}
+
+int register_plan(mbx_ctx* c, const ExecutablePlan& plan) {
+  std::vector<int32_t> enc = mbatch::backend::encode_plan(plan);
+  auto it = c->plan_by_enc.find(enc);
+  if (it != c->plan_by_enc.end()) return it->second;
+  PlanEntry pe;
+  pe.plan = plan;
+  pe.hplan = compile_plan(plan, pe.temp_floats_per_inst, pe.out_shapes);
+  if (!plan.ghost) {
+    if (!c->dry) {
+      cuda_check(cudaMalloc(&pe.dplan, sizeof(DPlan)), "plan alloc");
+      cuda_check(cudaMemcpy(pe.dplan, &pe.hplan, sizeof(DPlan), cudaMemcpyHostToDevice), "plan upload");
+    }
+    const int64_t tf = std::max<int64_t>(1, pe.hplan.temp_floats);
+    const int64_t budget = 192 * 1024 / 4;
+    MBATCH_CHECK(tf <= budget, "plan: per-instance temporaries exceed shared memory");
+    pe.tm = int(std::min<int64_t>(kMaxTM, std::max<int64_t>(1, budget / tf)));
+    pe.smem = int(pe.tm * tf * 4);
+    pe.threads = 256;
+    if (pe.hplan.unit > 0) {
+      pe.unit_chunk = pe.hplan.unit >= 64 ? 32 : pe.hplan.unit;
+      pe.max_split = (pe.hplan.unit + pe.unit_chunk - 1) / pe.unit_chunk;
+    } else {
+      pe.unit_chunk = 0;
+      pe.max_split = 1;
+    }
+    tc_prepare(c, pe);
+  }
+  int id = int(c->plans.size());
+  c->plans.push_back(std::move(pe));
+  c->plan_by_enc[enc] = id;
+  return id;
+}
+
+BatchLaunch prepare_batch(mbx_ctx* c, int plan_id, int b, const int64_t* shared_off,
+                          const int64_t* batched_off, int gather_mode, int64_t* out_off,
+                          int64_t* gather_bytes) {
+  MBATCH_CHECK(b > 0, "exec_batched: empty batch");
+  MBATCH_CHECK(plan_id >= 0 && size_t(plan_id) < c->plans.size(), "exec_batched: unknown plan");
+  const PlanEntry& pe = c->plans[plan_id];
+  const ExecutablePlan& p = pe.plan;
+  BatchLaunch L;
+  L.plan_id = plan_id;
+  L.b = b;
+  if (gather_bytes) *gather_bytes = 0;
+  if (p.ghost) return L;
+  const int ns = int(p.shared_shapes.size()), nb = int(p.batched_shapes.size()), no = int(p.outputs.size());
+  for (int s = 0; s < ns; ++s) arena_check(c, shared_off[s], p.shared_shapes[s].size());
+  for (int i = 0; i < b; ++i)
+    for (int j = 0; j < nb; ++j) arena_check(c, batched_off[int64_t(i) * nb + j], p.batched_shapes[j].size());
+
+  std::vector<int64_t> eff(batched_off, batched_off + int64_t(b) * nb);
+  if (gather_mode == MBX_GATHER_EXPLICIT) {
+    for (int j = 0; j < nb; ++j) {
+      const int64_t size = p.batched_shapes[j].size();
+      bool contiguous = true;
+      for (int i = 0; i + 1 < b; ++i)
+        contiguous = contiguous && batched_off[int64_t(i + 1) * nb + j] == batched_off[int64_t(i) * nb + j] + size;
+      if (contiguous) continue;
+      const int64_t region = arena_alloc(c, int64_t(b) * size);
+      std::vector<int64_t> src(b);
+      for (int i = 0; i < b; ++i) {
+        src[i] = batched_off[int64_t(i) * nb + j];
+        eff[int64_t(i) * nb + j] = region + int64_t(i) * size;
+      }
+      L.gathers.push_back({int(size), meta_stage(c, src.data(), src.size() * 8), region});
+      if (gather_bytes) *gather_bytes += int64_t(b) * size * int64_t(sizeof(float));
+    }
+  }
+  std::vector<int64_t> bases(no);
+  for (int k = 0; k < no; ++k) {
+    const int64_t size = pe.out_shapes[k].size();
+    bases[k] = arena_alloc(c, int64_t(b) * size);
+    for (int i = 0; i < b; ++i) out_off[int64_t(i) * no + k] = bases[k] + int64_t(i) * size;
+  }
+  // Per-instance step temporaries: the reference allocates them in the arena (exec_batched.cpp:
+  // 106); here they live on chip, but the offsets are reserved so every later handle offset
+  // equals the reference's.
+  arena_alloc(c, int64_t(b) * pe.temp_floats_per_inst);
+  L.shared_meta = meta_stage(c, shared_off, size_t(ns) * 8);
+  L.batched_meta = meta_stage(c, eff.data(), eff.size() * 8);
+  L.out_meta = meta_stage(c, bases.data(), bases.size() * 8);
+  return L;
+}
+
+void issue_batch(mbx_ctx* c, const BatchLaunch& L) {
+  const PlanEntry& pe = c->plans[L.plan_id];
+  if (pe.plan.ghost || c->dry) return;
+  float* arena = arena_ptr(c);
+  for (const auto& g : L.gathers) {
+    cuda_check(launch_gather_rows(arena, meta_dev<int64_t>(c, g.src_meta), g.dst, L.b, g.size, c->stream), "gather");
+    ++c->launches;
+    ++g_launches;
+  }
+  if (c->precision != MBX_PREC_FP32 && pe.tc_kind >= 0) {
+    cuda_check(tc_launch(c, pe, L), "tensor-core plan kernel");
+    ++c->launches;
+    ++g_launches;
+    return;
+  }
+  VmLaunch v{};
+  v.plan = pe.dplan;
+  v.arena = arena;
+  v.b = L.b;
+  v.tm = pe.tm;
+  const int ntiles = (L.b + pe.tm - 1) / pe.tm;
+  v.nsplit = pe.max_split > 1 ? std::clamp((296 + ntiles - 1) / ntiles, 1, pe.max_split) : 1;
+  v.unit_chunk = pe.unit_chunk;
+  v.threads = pe.threads;
+  v.smem_bytes = pe.smem;
+  v.shared_off = meta_dev<int64_t>(c, L.shared_meta);
+  v.batched_off = meta_dev<int64_t>(c, L.batched_meta);
+  v.out_base = meta_dev<int64_t>(c, L.out_meta);
+  cuda_check(launch_plan_vm(v, c->stream), "plan VM");
+  ++c->launches;
+  ++g_launches;
+}
+
+}  // namespace mbx
+
+// =============================================================================================
+// mbatch::backend C++ surface
+
+namespace mbatch {
+namespace backend {
+
+const char* op_name(OpCode op) {
+  switch (op) {
+    case OpCode::kDense: return "dense";
+    case OpCode::kAdd: return "add";
+    case OpCode::kMul: return "mul";
+    case OpCode::kSigmoid: return "sigmoid";
+    case OpCode::kTanh: return "tanh";
+    case OpCode::kRelu: return "relu";
+    case OpCode::kConcat: return "concat";
+    case OpCode::kArgmax: return "argmax";
+    case OpCode::kFill: return "fill";
+  }
+  return "?";
+}
+
+bool is_elementwise(OpCode op) {
+  switch (op) {
+    case OpCode::kAdd: case OpCode::kMul: case OpCode::kSigmoid: case OpCode::kTanh: case OpCode::kRelu:
+      return true;
+    default:
+      return false;
+  }
+}
+
+int op_arity(OpCode op) {
+  switch (op) {
+    case OpCode::kDense: case OpCode::kAdd: case OpCode::kMul: case OpCode::kConcat: return 2;
+    case OpCode::kSigmoid: case OpCode::kTanh: case OpCode::kRelu: case OpCode::kArgmax: return 1;
+    case OpCode::kFill: return 0;
+  }
+  return -1;
+}
+
+std::string Shape::str() const {
+  std::ostringstream os;
+  os << "(" << rows << ", " << cols << ")";
+  return os.str();
+}
+
+Shape infer_shape(OpCode op, const std::vector<Shape>& in) {
+  MBATCH_CHECK(static_cast<int>(in.size()) == op_arity(op), std::string(op_name(op)) + ": bad arity");
+  switch (op) {
+    case OpCode::kDense:
+      MBATCH_CHECK(in[0].cols == in[1].rows, std::string("dense: shape mismatch, expected (m,k)x(k,n), got ") +
+                                                  in[0].str() + " x " + in[1].str());
+      return Shape{in[0].rows, in[1].cols};
+    case OpCode::kAdd:
+    case OpCode::kMul:
+      MBATCH_CHECK(in[0] == in[1], std::string(op_name(op)) + ": shape mismatch, expected " + in[0].str() +
+                                       ", actual " + in[1].str());
+      return in[0];
+    case OpCode::kSigmoid: case OpCode::kTanh: case OpCode::kRelu:
+      return in[0];
+    case OpCode::kConcat:
+      MBATCH_CHECK(in[0].rows == in[1].rows, std::string("concat: row mismatch, ") + in[0].str() + " vs " + in[1].str());
+      return Shape{in[0].rows, in[0].cols + in[1].cols};
+    case OpCode::kArgmax:
+      MBATCH_CHECK(in[0].rows == 1, "argmax: expected a (1,n) tensor, got " + in[0].str());
+      return Shape{1, 1};
+    case OpCode::kFill:
+      return Shape{};
+  }
+  throw Error("unknown op");
+}
+
+static void put_ref(std::vector<int32_t>& e, const PlanRef& r) {
+  e.push_back(r.kind == PlanRef::Kind::kShared ? 0 : r.kind == PlanRef::Kind::kBatched ? 1 : 2);
+  e.push_back(r.index);
+  e.push_back(r.col_off);
+  e.push_back(r.cols);
+}
+
+std::vector<int32_t> encode_plan(const ExecutablePlan& p) {
+  std::vector<int32_t> e;
+  e.push_back(p.ghost ? 1 : 0);
+  e.push_back(int32_t(p.shared_shapes.size()));
+  for (auto& s : p.shared_shapes) { e.push_back(s.rows); e.push_back(s.cols); }
+  e.push_back(int32_t(p.batched_shapes.size()));
+  for (auto& s : p.batched_shapes) { e.push_back(s.rows); e.push_back(s.cols); }
+  e.push_back(int32_t(p.steps.size()));
+  for (auto& st : p.steps) {
+    e.push_back(st.kind == PlanStep::Kind::kOp ? 0 : st.kind == PlanStep::Kind::kFusedDense ? 1 : 2);
+    e.push_back(int32_t(st.op));
+    e.push_back(st.out_shape.rows);
+    e.push_back(st.out_shape.cols);
+    e.push_back(int32_t(st.ins.size()));
+    for (auto& r : st.ins) put_ref(e, r);
+    e.push_back(int32_t(st.chain.size()));
+    for (auto& l : st.chain) {
+      e.push_back(int32_t(l.op));
+      e.push_back(l.rhs ? 1 : 0);
+      put_ref(e, l.rhs ? *l.rhs : PlanRef{});
+    }
+  }
+  e.push_back(int32_t(p.outputs.size()));
+  for (auto& r : p.outputs) put_ref(e, r);
+  return e;
+}
+
+ExecutablePlan decode_plan(const int32_t* e, int64_t n) {
+  int64_t i = 0;
+  auto get = [&]() -> int32_t {
+    MBATCH_CHECK(i < n, "plan encoding truncated");
+    return e[i++];
+  };
+  auto ref = [&]() {
+    PlanRef r;
+    int k = get();
+    MBATCH_CHECK(k >= 0 && k <= 2, "plan encoding: bad ref kind");
+    r.kind = k == 0 ? PlanRef::Kind::kShared : k == 1 ? PlanRef::Kind::kBatched : PlanRef::Kind::kTemp;
+    r.index = get();
+    r.col_off = get();
+    r.cols = get();
+    return r;
+  };
+  auto op = [&]() {
+    int o = get();
+    MBATCH_CHECK(o >= 0 && o <= 8, "plan encoding: bad op");
+    return OpCode(o);
+  };
+  ExecutablePlan p;
+  p.ghost = get() != 0;
+  int ns = get();
+  for (int k = 0; k < ns; ++k) { int r = get(); int c = get(); p.shared_shapes.push_back({r, c}); }
+  int nb = get();
+  for (int k = 0; k < nb; ++k) { int r = get(); int c = get(); p.batched_shapes.push_back({r, c}); }
+  int nst = get();
+  for (int s = 0; s < nst; ++s) {
+    PlanStep st;
+    int k = get();
+    MBATCH_CHECK(k >= 0 && k <= 2, "plan encoding: bad step kind");
+    st.kind = k == 0 ? PlanStep::Kind::kOp : k == 1 ? PlanStep::Kind::kFusedDense : PlanStep::Kind::kChain;
+    st.op = op();
+    st.out_shape.rows = get();
+    st.out_shape.cols = get();
+    int nin = get();
+    for (int q = 0; q < nin; ++q) st.ins.push_back(ref());
+    int nc = get();
+    for (int q = 0; q < nc; ++q) {
+      ChainLink l;
+      l.op = op();
+      int has = get();
+      PlanRef r = ref();
+      if (has) l.rhs = r;
+      st.chain.push_back(l);
+    }
+    p.steps.push_back(std::move(st));
+  }
+  int no = get();
+  for (int k = 0; k < no; ++k) p.outputs.push_back(ref());
+  MBATCH_CHECK(i == n, "plan encoding has trailing data");
+  return p;
+}
+
+// ---- Arena ------------------------------------------------------------------------------------
+
+static void throw_if(int rc, mbx_ctx* c) {
+  if (rc != 0) throw Error(mbx_last_error(c));
+}
+
+Arena::Arena(int device, int precision) : owned_(true) {
+  mbx_ctx* c = nullptr;
+  if (mbx_ctx_create(device, precision, &c) != 0) throw Error("mbx_ctx_create failed");
+  ctx_ = c;
+}
+Arena::Arena(mbx_ctx* ctx) : ctx_(ctx), owned_(false) {}
+Arena::~Arena() {
+  if (owned_) mbx_ctx_destroy(ctx_);
+}
+TensorHandle Arena::alloc(Shape shape) {
+  int64_t off = 0;
+  throw_if(mbx_arena_alloc(ctx_, shape.rows, shape.cols, &off), ctx_);
+  return TensorHandle{off, shape};
+}
+int64_t Arena::used() const { return mbx_arena_used(ctx_); }
+void Arena::check(const TensorHandle& h) const {
+  MBATCH_CHECK(h.valid() && h.offset + h.size() <= used(), "tensor handle out of arena bounds");
+}
+void Arena::upload(const TensorHandle& h, const Float* src) {
+  check(h);
+  throw_if(mbx_arena_upload(ctx_, h.offset, src, h.size()), ctx_);
+}
+void Arena::download(const TensorHandle& h, Float* dst) const {
+  check(h);
+  throw_if(mbx_arena_download(ctx_, h.offset, dst, h.size()), ctx_);
+}
+std::vector<Float> Arena::read(const TensorHandle& h) const {
+  std::vector<Float> v(h.size());
+  download(h, v.data());
+  return v;
+}
+void Arena::sync() const { throw_if(mbx_sync(ctx_), ctx_); }
+
+void exec_primop(Arena& arena, OpCode op, const std::vector<TensorHandle>& inputs, const TensorHandle& out,
+                 Float fill_value) {
+  std::vector<int64_t> offs;
+  std::vector<int> rows, cols;
+  for (auto& h : inputs) {
+    offs.push_back(h.offset);
+    rows.push_back(h.shape.rows);
+    cols.push_back(h.shape.cols);
+  }
+  throw_if(mbx_exec_primop(arena.ctx(), int(op), int(inputs.size()), offs.data(), rows.data(), cols.data(),
+                           out.offset, out.shape.rows, out.shape.cols, fill_value),
+           arena.ctx());
+}
+
+BatchedResult exec_batched(Arena& arena, const ExecutablePlan& plan, const std::vector<BatchedCall>& instances,
+                           GatherMode mode) {
+  MBATCH_CHECK(!instances.empty(), "exec_batched: empty batch");
+  BatchedResult res;
+  if (plan.ghost) {
+    res.outputs.resize(instances.size());
+    return res;
+  }
+  const size_t b = instances.size();
+  const BatchedCall& first = instances[0];
+  MBATCH_CHECK(first.shared.size() == plan.shared_shapes.size() && first.batched.size() == plan.batched_shapes.size(),
+               "exec_batched: arity mismatch");
+  for (size_t i = 1; i < b; ++i)
+    for (size_t s = 0; s < first.shared.size(); ++s)
+      MBATCH_CHECK(instances[i].shared[s] == first.shared[s],
+                   "shared-param handle mismatch across instances (analysis bug)");
+  for (size_t s = 0; s < first.shared.size(); ++s)
+    MBATCH_CHECK(first.shared[s].shape == plan.shared_shapes[s], "exec_batched: shared input shape mismatch, expected " +
+                                                                     plan.shared_shapes[s].str() + ", actual " +
+                                                                     first.shared[s].shape.str());
+  std::vector<int64_t> shared, batched;
+  for (auto& h : first.shared) shared.push_back(h.offset);
+  for (auto& call : instances) {
+    MBATCH_CHECK(call.batched.size() == plan.batched_shapes.size(), "exec_batched: arity mismatch");
+    for (size_t j = 0; j < call.batched.size(); ++j) {
+      MBATCH_CHECK(call.batched[j].shape == plan.batched_shapes[j], "exec_batched: batched input shape mismatch, expected " +
+                                                                        plan.batched_shapes[j].str() + ", actual " +
+                                                                        call.batched[j].shape.str());
+      batched.push_back(call.batched[j].offset);
+    }
+  }
+  mbx_ctx* c = arena.ctx();
+  std::vector<int32_t> enc = encode_plan(plan);
+  int pid = -1;
+  throw_if(mbx_plan_register(c, enc.data(), int64_t(enc.size()), &pid), c);
+  std::vector<int64_t> outs(b * plan.outputs.size());
+  int64_t gb = 0;
+  throw_if(mbx_exec_batched(c, pid, int(b), shared.data(), batched.data(),
+                            mode == GatherMode::kFused ? MBX_GATHER_FUSED : MBX_GATHER_EXPLICIT, outs.data(), &gb),
+           c);
+  res.gather_bytes = gb;
+  const auto& shapes = c->plans[pid].out_shapes;
+  res.outputs.resize(b);
+  for (size_t i = 0; i < b; ++i)
+    for (size_t k = 0; k < plan.outputs.size(); ++k)
+      res.outputs[i].push_back(TensorHandle{outs[i * plan.outputs.size() + k], shapes[k]});
+  return res;
+}
+
+}  // namespace backend
+}  // namespace mbatch

@@ -1,0 +1,461 @@
+// capi.cpp — the C ABI (include/mbx.h).  Every entry point catches mbatch::Error (and any other
+// exception) and turns it into a nonzero status plus mbx_last_error(ctx), so the boundary never
+// throws; the C++ surface (include/mbatch/*.hpp) rethrows the same text.
+#include <atomic>
+#include <cstring>
+#include <memory>
+
+#include "ctx.h"
+#include "exec.h"
+#include "mbatch/zoo.hpp"
+#include "tc.h"
+
+namespace mbx {
+extern std::atomic<int64_t> g_launches;
+void arena_init(mbx_ctx* c);
+void arena_release(mbx_ctx* c);
+}  // namespace mbx
+
+using mbatch::Error;
+using mbatch::runtime::HostValue;
+
+namespace {
+
+thread_local std::string g_err;  // errors before a context exists
+
+template <class F>
+int guarded(mbx_ctx* c, F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const std::exception& e) {
+    if (c) c->err = e.what();
+    else g_err = e.what();
+    return 1;
+  } catch (...) {
+    if (c) c->err = "unknown error";
+    else g_err = "unknown error";
+    return 1;
+  }
+}
+
+void encode(const HostValue& v, std::vector<int32_t>& t, std::vector<float>& d) {
+  switch (v.kind) {
+    case HostValue::Kind::kTensor:
+      t.push_back(0); t.push_back(v.shape.rows); t.push_back(v.shape.cols);
+      d.insert(d.end(), v.data.begin(), v.data.end());
+      return;
+    case HostValue::Kind::kInt: t.push_back(1); t.push_back(int32_t(v.ival)); return;
+    case HostValue::Kind::kFloat: t.push_back(1); t.push_back(int32_t(v.fval)); return;
+    case HostValue::Kind::kList: t.push_back(2); break;
+    case HostValue::Kind::kTuple: t.push_back(3); break;
+    case HostValue::Kind::kAdt: t.push_back(4); t.push_back(v.ctor == "Node" ? 1 : 0); break;
+  }
+  t.push_back(int32_t(v.items.size()));
+  for (auto& it : v.items) encode(it, t, d);
+}
+
+HostValue decode(const int32_t* t, int64_t nt, int64_t& ti, const float* d, int64_t nd, int64_t& di) {
+  MBATCH_CHECK(ti < nt, "hostval encoding truncated");
+  int kind = t[ti++];
+  switch (kind) {
+    case 0: {
+      MBATCH_CHECK(ti + 2 <= nt, "hostval encoding truncated");
+      int r = t[ti++], c = t[ti++];
+      int64_t n = int64_t(r) * c;
+      MBATCH_CHECK(r >= 0 && c >= 0 && di + n <= nd, "hostval data truncated");
+      std::vector<float> v(d + di, d + di + n);
+      di += n;
+      return HostValue::tensor({r, c}, std::move(v));
+    }
+    case 1: MBATCH_CHECK(ti < nt, "hostval encoding truncated"); return HostValue::scalar(t[ti++]);
+    case 2: case 3: case 4: {
+      int ctor = 0;
+      if (kind == 4) { MBATCH_CHECK(ti < nt, "hostval encoding truncated"); ctor = t[ti++]; }
+      MBATCH_CHECK(ti < nt, "hostval encoding truncated");
+      int n = t[ti++];
+      std::vector<HostValue> items;
+      for (int k = 0; k < n; ++k) items.push_back(decode(t, nt, ti, d, nd, di));
+      if (kind == 2) return HostValue::list(std::move(items));
+      if (kind == 3) return HostValue::tuple(std::move(items));
+      return HostValue::adt(ctor ? "Node" : "Leaf", std::move(items));
+    }
+  }
+  throw Error("hostval encoding: bad kind " + std::to_string(kind));
+}
+
+}  // namespace
+
+struct mbx_model {
+  mbx_ctx* ctx = nullptr;
+  mbatch::runtime::CompiledModel cm;
+  std::unique_ptr<mbatch::runtime::Session> session;
+  std::vector<std::string> param_names;
+};
+
+struct mbx_result {
+  mbatch::runtime::EvalResult r;
+  std::vector<int32_t> out_tok;
+  std::vector<float> out_data;
+};
+
+extern "C" {
+
+const char* mbx_version(void) { return "mbx 0.1 (sm_100a)"; }
+int64_t mbx_kernel_launch_count(void) { return mbx::g_launches.load(); }
+
+int mbx_ctx_create(int device, int precision, mbx_ctx** out) {
+  *out = nullptr;
+  auto c = std::make_unique<mbx_ctx>();
+  c->device = device;
+  c->dry = device < 0;
+  c->precision = precision;
+  int rc = guarded(nullptr, [&] {
+    MBATCH_CHECK(precision >= MBX_PREC_FP32 && precision <= MBX_PREC_BF16, "unknown precision");
+    if (!c->dry) {
+      mbx::cuda_check(cudaSetDevice(device), "cudaSetDevice");
+      mbx::cuda_check(cudaFree(nullptr), "context init");
+      mbx::cuda_check(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream");
+      mbx::arena_init(c.get());
+    }
+    mbx::meta_reserve(c.get(), size_t(8) << 20);
+  });
+  if (rc) return rc;
+  *out = c.release();
+  return 0;
+}
+
+void mbx_ctx_destroy(mbx_ctx* c) {
+  if (!c) return;
+  if (!c->dry) {
+    cudaStreamSynchronize(c->stream);
+    for (auto& pe : c->plans) {
+      if (pe.dplan) cudaFree(pe.dplan);
+      mbx::tc_release(pe);
+    }
+    if (c->meta.host) cudaFreeHost(c->meta.host);
+    if (c->meta.dev) cudaFree(c->meta.dev);
+    if (c->d2h_host) cudaFreeHost(c->d2h_host);
+    if (c->d2h_dev) cudaFree(c->d2h_dev);
+    if (c->in_host) cudaFreeHost(c->in_host);
+    try { mbx::arena_release(c); } catch (...) {}
+    cudaStreamDestroy(c->stream);
+  } else {
+    std::free(c->meta.host);
+    std::free(c->in_host);
+  }
+  delete c;
+}
+
+const char* mbx_last_error(const mbx_ctx* c) { return c ? c->err.c_str() : g_err.c_str(); }
+
+int mbx_ctx_set_precision(mbx_ctx* c, int precision) {
+  return guarded(c, [&] {
+    MBATCH_CHECK(precision >= MBX_PREC_FP32 && precision <= MBX_PREC_BF16, "unknown precision");
+    c->precision = precision;
+  });
+}
+
+int mbx_sync(mbx_ctx* c) {
+  return guarded(c, [&] {
+    if (!c->dry) mbx::cuda_check(cudaStreamSynchronize(c->stream), "sync");
+  });
+}
+
+int mbx_arena_alloc(mbx_ctx* c, int rows, int cols, int64_t* offset) {
+  return guarded(c, [&] {
+    MBATCH_CHECK(rows >= 0 && cols >= 0, "negative shape");
+    *offset = mbx::arena_alloc(c, int64_t(rows) * cols);
+  });
+}
+
+int64_t mbx_arena_used(const mbx_ctx* c) { return c->used; }
+
+int mbx_arena_upload(mbx_ctx* c, int64_t off, const float* src, int64_t n) {
+  return guarded(c, [&] {
+    mbx::arena_check(c, off, n);
+    if (c->dry || n == 0) return;
+    mbx::cuda_check(cudaMemcpyAsync(mbx::arena_ptr(c) + off, src, size_t(n) * 4, cudaMemcpyHostToDevice, c->stream), "upload");
+    mbx::cuda_check(cudaStreamSynchronize(c->stream), "upload sync");
+  });
+}
+
+int mbx_arena_download(mbx_ctx* c, int64_t off, float* dst, int64_t n) {
+  return guarded(c, [&] {
+    mbx::arena_check(c, off, n);
+    if (c->dry) {
+      std::memset(dst, 0, size_t(n) * 4);
+      return;
+    }
+    mbx::meta_commit(c);
+    mbx::cuda_check(cudaMemcpyAsync(dst, mbx::arena_ptr(c) + off, size_t(n) * 4, cudaMemcpyDeviceToHost, c->stream), "download");
+    mbx::cuda_check(cudaStreamSynchronize(c->stream), "download sync");
+  });
+}
+
+int mbx_arena_rewind(mbx_ctx* c, int64_t used) {
+  return guarded(c, [&] {
+    MBATCH_CHECK(used >= 0 && used <= c->used, "rewind past the arena end");
+    c->used = used;
+  });
+}
+
+int mbx_plan_register(mbx_ctx* c, const int32_t* enc, int64_t n, int* plan_id) {
+  return guarded(c, [&] { *plan_id = mbx::register_plan(c, mbatch::backend::decode_plan(enc, n)); });
+}
+
+int mbx_exec_batched(mbx_ctx* c, int plan_id, int b, const int64_t* shared_off, const int64_t* batched_off,
+                     int gather_mode, int64_t* out_off, int64_t* gather_bytes) {
+  return guarded(c, [&] {
+    const auto& pe = c->plans.at(plan_id);
+    size_t bytes = 8 * (pe.plan.shared_shapes.size() + size_t(b) * pe.plan.batched_shapes.size() * 2 + pe.plan.outputs.size()) + 64;
+    mbx::meta_reserve(c, bytes);
+    mbx::BatchLaunch L = mbx::prepare_batch(c, plan_id, b, shared_off, batched_off, gather_mode, out_off, gather_bytes);
+    mbx::meta_commit(c);
+    mbx::issue_batch(c, L);
+  });
+}
+
+int mbx_exec_primop(mbx_ctx* c, int op, int nin, const int64_t* in_off, const int* in_rows, const int* in_cols,
+                    int64_t out_off, int out_rows, int out_cols, float fill) {
+  using namespace mbatch::backend;
+  return guarded(c, [&] {
+    MBATCH_CHECK(op >= 0 && op <= 8, "unknown op");
+    OpCode o = OpCode(op);
+    std::vector<Shape> shapes;
+    for (int i = 0; i < nin; ++i) shapes.push_back(Shape{in_rows[i], in_cols[i]});
+    const Shape out{out_rows, out_cols};
+    if (o != OpCode::kFill) {
+      Shape expect = infer_shape(o, shapes);
+      MBATCH_CHECK(expect == out, std::string(op_name(o)) + ": output shape mismatch");
+    }
+    for (int i = 0; i < nin; ++i) mbx::arena_check(c, in_off[i], shapes[i].size());
+    mbx::arena_check(c, out_off, out.size());
+    if (c->dry) return;
+    if (o == OpCode::kFill) {
+      mbx::cuda_check(mbx::launch_fill(mbx::arena_ptr(c), out_off, out.size(), fill, c->stream), "fill");
+      ++c->launches;
+      ++mbx::g_launches;
+      return;
+    }
+    ExecutablePlan p;
+    p.shared_shapes = shapes;
+    PlanStep st;
+    st.kind = PlanStep::Kind::kOp;
+    st.op = o;
+    for (int i = 0; i < nin; ++i) st.ins.push_back(PlanRef{PlanRef::Kind::kShared, i, 0, -1});
+    st.out_shape = out;
+    p.steps.push_back(st);
+    p.outputs.push_back(PlanRef{PlanRef::Kind::kTemp, 0, 0, -1});
+    int pid = mbx::register_plan(c, p);
+    const auto& pe = c->plans[pid];
+    mbx::meta_reserve(c, size_t(nin + 1) * 8 + 32);
+    size_t sm = mbx::meta_stage(c, in_off, size_t(nin) * 8);
+    size_t om = mbx::meta_stage(c, &out_off, 8);
+    mbx::meta_commit(c);
+    mbx::VmLaunch v{};
+    v.plan = pe.dplan;
+    v.arena = mbx::arena_ptr(c);
+    v.b = 1;
+    v.tm = 1;
+    v.nsplit = 1;
+    v.unit_chunk = 0;
+    v.threads = 256;
+    v.smem_bytes = int(std::max<int64_t>(1, pe.hplan.temp_floats) * 4);
+    v.shared_off = mbx::meta_dev<int64_t>(c, sm);
+    v.batched_off = nullptr;
+    v.out_base = mbx::meta_dev<int64_t>(c, om);
+    mbx::cuda_check(mbx::launch_plan_vm(v, c->stream), "primop");
+    ++c->launches;
+    ++mbx::g_launches;
+  });
+}
+
+// ---- models ------------------------------------------------------------------------------
+
+int mbx_model_create(mbx_ctx* c, const char* name, int hidden, mbx_model** out) {
+  *out = nullptr;
+  auto m = std::make_unique<mbx_model>();
+  int rc = guarded(c, [&] {
+    m->ctx = c;
+    m->cm = mbatch::zoo::get_model(name, hidden);
+    m->session = std::make_unique<mbatch::runtime::Session>(m->cm, c);
+    for (auto& d : m->cm.params)
+      if (!d.is_instance_input) m->param_names.push_back(d.name);
+  });
+  if (rc) return rc;
+  *out = m.release();
+  return 0;
+}
+
+void mbx_model_destroy(mbx_model* m) { delete m; }
+
+int mbx_model_make_params(mbx_model* m, unsigned seed) {
+  return guarded(m->ctx, [&] { m->session->set_params(mbatch::zoo::make_params(m->cm, seed)); });
+}
+
+int mbx_model_set_param(mbx_model* m, const char* name, const float* data, int64_t n) {
+  return guarded(m->ctx, [&] {
+    auto it = m->session->param_handles().find(name);
+    MBATCH_CHECK(it != m->session->param_handles().end(), std::string("unknown model parameter ") + name);
+    MBATCH_CHECK(n == it->second.size(), std::string("parameter ") + name + " has the wrong size");
+    if (mbx_arena_upload(m->ctx, it->second.offset, data, n) != 0) throw Error(m->ctx->err);
+  });
+}
+
+int mbx_model_num_params(const mbx_model* m) { return int(m->param_names.size()); }
+const char* mbx_model_param_name(const mbx_model* m, int i) { return m->param_names.at(size_t(i)).c_str(); }
+
+int mbx_model_make_inputs(mbx_model* m, unsigned seed, int batch, int32_t* toks, int64_t* ntok, float* data, int64_t* ndata) {
+  return guarded(m->ctx, [&] {
+    auto inputs = mbatch::zoo::make_inputs(m->cm, seed, batch);
+    std::vector<int32_t> t;
+    std::vector<float> d;
+    for (auto& inst : inputs)
+      for (auto& decl : m->cm.params)
+        if (decl.is_instance_input) encode(inst.at(decl.name), t, d);
+    if (toks) {
+      MBATCH_CHECK(*ntok >= int64_t(t.size()) && *ndata >= int64_t(d.size()), "buffers too small");
+      std::memcpy(toks, t.data(), t.size() * 4);
+      std::memcpy(data, d.data(), d.size() * 4);
+    }
+    *ntok = int64_t(t.size());
+    *ndata = int64_t(d.size());
+  });
+}
+
+int mbx_model_num_sigs(const mbx_model* m) { return int(m->cm.kernels.signatures.size()); }
+const char* mbx_model_sig_name(const mbx_model* m, int sig) { return m->cm.kernels.signatures.at(size_t(sig)).name.c_str(); }
+
+int mbx_model_plan_encoding(const mbx_model* m, int sig, int32_t* enc, int64_t* n) {
+  return guarded(m->ctx, [&] {
+    auto e = mbatch::backend::encode_plan(m->cm.kernels.plans.at(size_t(sig)));
+    if (enc) {
+      MBATCH_CHECK(*n >= int64_t(e.size()), "buffer too small");
+      std::memcpy(enc, e.data(), e.size() * 4);
+    }
+    *n = int64_t(e.size());
+  });
+}
+
+void mbx_options_default(mbx_options* o) {
+  o->scheduler = MBX_SCHED_DEPTH;
+  o->gather = MBX_GATHER_FUSED;
+  o->hoist = 1;
+  o->phases = 1;
+  o->record_nodes = 1;
+  o->time_kernels = 0;
+}
+
+int mbx_evaluate_batch(mbx_model* m, int batch, const int32_t* toks, int64_t ntok, const float* data, int64_t ndata,
+                       const mbx_options* opts, mbx_result** out) {
+  *out = nullptr;
+  auto res = std::make_unique<mbx_result>();
+  int rc = guarded(m->ctx, [&] {
+    MBATCH_CHECK(batch >= 1, "evaluate_batch: need at least one instance");
+    std::vector<mbatch::runtime::InstanceInput> inputs(batch);
+    int64_t ti = 0, di = 0;
+    for (int i = 0; i < batch; ++i)
+      for (auto& decl : m->cm.params)
+        if (decl.is_instance_input) inputs[i][decl.name] = decode(toks, ntok, ti, data, ndata, di);
+    MBATCH_CHECK(ti == ntok && di == ndata, "hostval encoding: trailing data");
+    mbatch::runtime::ExecOptions o;
+    mbx_options d;
+    mbx_options_default(&d);
+    const mbx_options& oo = opts ? *opts : d;
+    o.scheduler = oo.scheduler == MBX_SCHED_AGENDA ? mbatch::runtime::ExecOptions::Scheduler::kAgenda
+                                                   : mbatch::runtime::ExecOptions::Scheduler::kDepth;
+    o.gather = oo.gather == MBX_GATHER_EXPLICIT ? mbatch::backend::GatherMode::kExplicit : mbatch::backend::GatherMode::kFused;
+    o.hoist = oo.hoist != 0;
+    o.phases = oo.phases != 0;
+    o.record_nodes = oo.record_nodes != 0;
+    o.time_kernels = oo.time_kernels != 0;
+    res->r = m->session->evaluate(inputs, o);
+    for (auto& v : res->r.outputs) encode(v, res->out_tok, res->out_data);
+  });
+  if (rc) return rc;
+  *out = res.release();
+  return 0;
+}
+
+void mbx_result_destroy(mbx_result* r) { delete r; }
+
+int mbx_result_outputs(const mbx_result* r, int32_t* toks, int64_t* ntok, float* data, int64_t* ndata) {
+  if (toks) {
+    if (*ntok < int64_t(r->out_tok.size()) || *ndata < int64_t(r->out_data.size())) return 1;
+    std::memcpy(toks, r->out_tok.data(), r->out_tok.size() * 4);
+    std::memcpy(data, r->out_data.data(), r->out_data.size() * 4);
+  }
+  *ntok = int64_t(r->out_tok.size());
+  *ndata = int64_t(r->out_data.size());
+  return 0;
+}
+
+int mbx_result_counters(const mbx_result* r, int64_t* o) {
+  const auto& t = r->r.trace;
+  o[0] = t.kernel_launches;
+  o[1] = t.total_nodes;
+  o[2] = t.scheduler_ops;
+  o[3] = t.sync_points;
+  o[4] = t.gather_bytes;
+  o[5] = t.dfg_edges;
+  o[6] = int64_t(t.batches.size());
+  o[7] = int64_t(t.flush_boundaries.size());
+  o[8] = r->r.timing.device_launches;
+  return 0;
+}
+
+int mbx_result_batches(const mbx_result* r, int32_t* rows5, int32_t* ids) {
+  size_t k = 0;
+  for (size_t b = 0; b < r->r.trace.batches.size(); ++b) {
+    const auto& br = r->r.trace.batches[b];
+    rows5[5 * b] = br.phase;
+    rows5[5 * b + 1] = br.depth;
+    rows5[5 * b + 2] = br.sig;
+    rows5[5 * b + 3] = br.size;
+    rows5[5 * b + 4] = br.ghost ? 1 : 0;
+    for (int id : br.node_ids) ids[k++] = id;
+  }
+  return 0;
+}
+
+int mbx_result_flush_boundaries(const mbx_result* r, int32_t* out) {
+  for (size_t k = 0; k < r->r.trace.flush_boundaries.size(); ++k) out[k] = r->r.trace.flush_boundaries[k];
+  return 0;
+}
+
+int mbx_result_nodes(const mbx_result* r, int32_t* hdr, int64_t* refs, int64_t* nrefs) {
+  int64_t need = 0;
+  for (const auto& n : r->r.nodes)
+    need += 3 * int64_t(n.shared_ins.size() + n.batched_ins.size() + n.outputs.size()) + int64_t(n.producers.size());
+  if (!hdr) {
+    *nrefs = need;
+    return 0;
+  }
+  if (*nrefs < need) return 1;
+  int64_t k = 0;
+  for (size_t i = 0; i < r->r.nodes.size(); ++i) {
+    const auto& n = r->r.nodes[i];
+    int32_t* h = hdr + 11 * i;
+    h[0] = n.id; h[1] = n.sig_id; h[2] = n.block_id; h[3] = n.instance; h[4] = n.phase; h[5] = n.depth;
+    h[6] = n.ghost; h[7] = int32_t(n.shared_ins.size()); h[8] = int32_t(n.batched_ins.size());
+    h[9] = int32_t(n.producers.size()); h[10] = int32_t(n.outputs.size());
+    for (auto& t : n.shared_ins) { refs[k++] = t.node; refs[k++] = t.out; refs[k++] = t.handle.offset; }
+    for (auto& t : n.batched_ins) { refs[k++] = t.node; refs[k++] = t.out; refs[k++] = t.handle.offset; }
+    for (int p : n.producers) refs[k++] = p;
+    for (auto& o : n.outputs) { refs[k++] = o.offset; refs[k++] = o.shape.rows; refs[k++] = o.shape.cols; }
+  }
+  *nrefs = need;
+  return 0;
+}
+
+int mbx_result_timing(const mbx_result* r, double* o) {
+  o[0] = r->r.timing.host_total_us;
+  o[1] = r->r.timing.host_dfg_us;
+  o[2] = r->r.timing.device_span_us;
+  o[3] = double(r->r.timing.h2d_bytes);
+  o[4] = double(r->r.timing.d2h_bytes);
+  return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,108 @@
+// ctx.h — internal state of an mbx_ctx: device, stream, HBM arena, index staging, plan registry.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <map>
+#include <string>
+#include <vector>
+
+#include "devplan.h"
+#include "kernels.h"
+#include "mbatch/backend.hpp"
+
+namespace mbx {
+
+// A registered plan: the host plan, its compiled device form and its launch configuration.
+struct PlanEntry {
+  mbatch::backend::ExecutablePlan plan;
+  DPlan hplan{};
+  DPlan* dplan = nullptr;            // device copy
+  int64_t temp_floats_per_inst = 0;  // sum of step output sizes (reference arena parity)
+  std::vector<mbatch::backend::Shape> out_shapes;
+  int tm = 1, threads = 256, smem = 0, unit_chunk = 0, max_split = 1;
+  int tc_kind = -1;                  // tensor-core kernel for this plan (kernels_tc.cu), -1 none
+  void* tc_state = nullptr;          // packed weights etc., owned by kernels_tc
+};
+
+// Pinned host staging + device mirror for per-launch index arrays (offset tables).
+struct MetaRing {
+  char* host = nullptr;
+  char* dev = nullptr;
+  size_t cap = 0, cursor = 0, committed = 0;
+};
+
+}  // namespace mbx
+
+struct mbx_ctx {
+  int device = 0;
+  bool dry = false;  // device < 0: host bookkeeping only (offsets, traces), no CUDA calls
+  int precision = MBX_PREC_FP32;
+  cudaStream_t stream = nullptr;
+  // HBM arena: one virtual-address reservation, physical chunks mapped on demand, so offsets
+  // (the reference's TensorHandle::offset) are stable while the arena grows.
+  CUdeviceptr base = 0;
+  size_t reserve_bytes = 0, mapped_bytes = 0, chunk_bytes = 0;
+  std::vector<CUmemGenericAllocationHandle> chunks;
+  int64_t used = 0;  // floats
+  mbx::MetaRing meta;
+  // D2H staging for packed outputs / decisions.
+  float* d2h_host = nullptr;
+  float* d2h_dev = nullptr;
+  size_t d2h_cap = 0;  // floats
+  // Pinned staging for a mini-batch's instance inputs (one H2D copy per evaluation).
+  float* in_host = nullptr;
+  size_t in_cap = 0;  // floats
+  std::vector<mbx::PlanEntry> plans;
+  std::map<std::vector<int32_t>, int> plan_by_enc;
+  std::string err;
+  int64_t launches = 0;
+  cudaEvent_t ev_a = nullptr, ev_b = nullptr;
+};
+
+namespace mbx {
+
+// Throws mbatch::Error on CUDA failure.
+void cuda_check(cudaError_t e, const char* what);
+void cu_check(CUresult r, const char* what);
+
+float* arena_ptr(mbx_ctx* c);
+// Bump allocation in floats (maps more physical memory when needed).
+int64_t arena_alloc(mbx_ctx* c, int64_t floats);
+void arena_check(const mbx_ctx* c, int64_t off, int64_t n);
+
+// Index staging: reserve bytes (8-aligned) in the pinned ring; returns the byte offset.
+size_t meta_stage(mbx_ctx* c, const void* src, size_t bytes);
+// Guarantees `bytes` of contiguous free space (may synchronize and recycle the ring).
+void meta_reserve(mbx_ctx* c, size_t bytes);
+// Issues one H2D copy for everything staged since the last commit.
+void meta_commit(mbx_ctx* c);
+template <class T>
+const T* meta_dev(mbx_ctx* c, size_t off) { return reinterpret_cast<const T*>(c->meta.dev + off); }
+
+void ensure_d2h(mbx_ctx* c, size_t floats);
+void ensure_input_stage(mbx_ctx* c, size_t floats);
+
+// Plan registry (backend.cpp).
+int register_plan(mbx_ctx* c, const mbatch::backend::ExecutablePlan& plan);
+
+// One batched launch of a registered plan whose offsets are already staged.
+struct BatchLaunch {
+  int plan_id = -1;
+  int b = 0;
+  size_t shared_meta = 0, batched_meta = 0, out_meta = 0;
+  // EXPLICIT gathers to run first: (slot size, src offsets meta, dst offset)
+  struct Gather { int size; size_t src_meta; int64_t dst; };
+  std::vector<Gather> gathers;
+};
+
+// Host half of exec_batched: validation, gather accounting, reference-order allocation of
+// scratch / output regions / temporaries, staging of offset tables.  Fills `out_off`
+// (b * nout) and returns the launch record (not yet issued).
+BatchLaunch prepare_batch(mbx_ctx* c, int plan_id, int b, const int64_t* shared_off,
+                          const int64_t* batched_off, int gather_mode, int64_t* out_off,
+                          int64_t* gather_bytes);
+// Device half: enqueues the gather copies and the plan kernel (meta must be committed).
+void issue_batch(mbx_ctx* c, const BatchLaunch& L);
+
+}  // namespace mbx

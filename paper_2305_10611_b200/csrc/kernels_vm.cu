@@ -1,0 +1,277 @@
+// kernels_vm.cu — the FP32 plan VM: one generic sm_100a kernel that executes ANY
+// backend::ExecutablePlan over a batch of DFG nodes, bit-identical to the reference.
+//
+// Reference semantics being reproduced (proj/src/exec_batched.cpp:80-145, backend.cpp:105-181):
+//   for each instance: for each step: kOp -> exec_primop, kFusedDense -> one dense per stacked
+//   weight into its column range, kChain -> v = base[k]; v = op(v, rhs[k]) ...; then copy the
+//   plan outputs into batch-contiguous output regions.
+// Bit-exactness: dense accumulates c = 0; c += a[p] * w[p][j] for p ascending with separately
+// rounded fp32 multiply and add (__fmul_rn/__fadd_rn, no FMA contraction), exactly the
+// reference's i-k-j loop per output element; activations use the glibc-exact restatements in
+// libm_fp32.cuh.
+//
+// Mapping: grid = (ceil(b / tm) node tiles) x (nsplit column tiles).  A CTA keeps the temps of
+// its tm nodes in shared memory, computes "full" steps entirely and "split" steps (column-local
+// w.r.t. the plan's output unit, see devplan.h) only over its column tile, so a shared weight
+// tile is read once per node tile instead of once per node, and wide layers spread over many
+// SMs.  Operands are read straight from the arena through the per-node offset arrays (the
+// gather is fused into the operand loads; nothing is materialized).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "devplan.h"
+#include "kernels.h"
+#include "libm_fp32.cuh"
+
+namespace mbx {
+
+using namespace mbx_libm;
+
+namespace {
+
+__device__ __forceinline__ float apply_op(int op, float v, float rhs) {
+  switch (op) {
+    case kAdd: return fadd(v, rhs);
+    case kMul: return fmul(v, rhs);
+    case kSigmoid: return sigmoidf_exact(v);
+    case kTanh: return tanhf_exact(v);
+    case kRelu: return reluf_exact(v);
+    default: return v;
+  }
+}
+
+struct Ctx {
+  const DPlan* P;
+  float* arena;
+  const int64_t* shared_off;
+  const int64_t* batched_off;
+  float* temps;   // smem base
+  int node0, nn;  // first node of the tile, nodes in the tile
+};
+
+__device__ __forceinline__ const float* ref_ptr(const Ctx& c, const DRef& r, int t) {
+  int64_t slice = r.cols >= 0 ? r.col_off : 0;
+  switch (r.kind) {
+    case kRefShared: return c.arena + c.shared_off[r.index] + slice;
+    case kRefBatched:
+      return c.arena + c.batched_off[int64_t(c.node0 + t) * c.P->nbatched + r.index] + slice;
+    default: return c.temps + int64_t(t) * c.P->temp_floats + c.P->steps[r.index].temp_off + slice;
+  }
+}
+
+__device__ __forceinline__ float* temp_ptr(const Ctx& c, int step, int t) {
+  return c.temps + int64_t(t) * c.P->temp_floats + c.P->steps[step].temp_off;
+}
+
+// out[i, j] for j in [j0, j1) of a (m x n) = A (m x k) . W (k x n), written at column
+// out_col0 + j of an out row of width out_ld.  W is shared (same for all tile nodes) or
+// batched (per node).
+__device__ void dense_range(const Ctx& c, const DRef& a, const DRef& w, int s, int out_ld,
+                            int out_col0, int j0, int j1) {
+  const int m = a.rows_r, k = a.cols_r, n = w.cols_r;
+  const int ncr = j1 - j0;
+  if (ncr <= 0) return;
+  if (w.kind == kRefShared) {
+    const float* W = ref_ptr(c, w, 0);
+    const float* A[kMaxTM];
+#pragma unroll
+    for (int t = 0; t < kMaxTM; ++t) A[t] = t < c.nn ? ref_ptr(c, a, t) : nullptr;
+    const int total = m * ncr;
+    for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
+      const int i = idx / ncr, j = j0 + idx % ncr;
+      float acc[kMaxTM];
+#pragma unroll
+      for (int t = 0; t < kMaxTM; ++t) acc[t] = 0.0f;
+      const float* wc = W + j;
+      for (int p = 0; p < k; ++p) {
+        const float wv = __ldg(wc + int64_t(p) * n);
+#pragma unroll
+        for (int t = 0; t < kMaxTM; ++t)
+          if (t < c.nn) acc[t] = fadd(acc[t], fmul(A[t][i * k + p], wv));
+      }
+#pragma unroll
+      for (int t = 0; t < kMaxTM; ++t)
+        if (t < c.nn) temp_ptr(c, s, t)[i * out_ld + out_col0 + j] = acc[t];
+    }
+  } else {
+    const int total = c.nn * m * ncr;
+    for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
+      const int t = idx / (m * ncr);
+      const int r = idx % (m * ncr);
+      const int i = r / ncr, j = j0 + r % ncr;
+      const float* A = ref_ptr(c, a, t);
+      const float* W = ref_ptr(c, w, t);
+      float acc = 0.0f;
+      for (int p = 0; p < k; ++p) acc = fadd(acc, fmul(A[i * k + p], W[int64_t(p) * n + j]));
+      temp_ptr(c, s, t)[i * out_ld + out_col0 + j] = acc;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) plan_vm_kernel(VmLaunch L) {
+  extern __shared__ float smem[];
+  const DPlan* P = L.plan;
+  Ctx c;
+  c.P = P;
+  c.arena = L.arena;
+  c.shared_off = L.shared_off;
+  c.batched_off = L.batched_off;
+  c.temps = smem;
+  c.node0 = blockIdx.x * L.tm;
+  c.nn = min(L.tm, L.b - c.node0);
+  if (c.nn <= 0) return;
+  const int u0 = blockIdx.y * L.unit_chunk;
+  const int u1 = min(u0 + L.unit_chunk, P->unit > 0 ? P->unit : 0);
+  const bool tiled = L.nsplit > 1;
+
+  for (int s = 0; s < P->nsteps; ++s) {
+    const DStep& st = P->steps[s];
+    const bool sp = tiled && st.split;
+    switch (st.kind) {
+      case kStepFused: {
+        int col = 0;
+        for (int w = 1; w < st.nin; ++w) {
+          const DRef& wr = st.ins[w];
+          if (sp) dense_range(c, st.ins[0], wr, s, st.cols, col, u0, u1);
+          else dense_range(c, st.ins[0], wr, s, st.cols, col, 0, wr.cols_r);
+          col += wr.cols_r;
+        }
+        break;
+      }
+      case kStepOp: {
+        if (st.op == kDense) {
+          if (sp) dense_range(c, st.ins[0], st.ins[1], s, st.cols, 0, u0, u1);
+          else dense_range(c, st.ins[0], st.ins[1], s, st.cols, 0, 0, st.cols);
+        } else if (st.op == kConcat) {
+          const int rows = st.rows, ca = st.ins[0].cols_r, cb = st.ins[1].cols_r;
+          const int total = c.nn * rows * (ca + cb);
+          for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
+            const int t = idx / (rows * (ca + cb));
+            const int e = idx % (rows * (ca + cb));
+            const int r = e / (ca + cb), j = e % (ca + cb);
+            float v = j < ca ? ref_ptr(c, st.ins[0], t)[r * ca + j] : ref_ptr(c, st.ins[1], t)[r * cb + j - ca];
+            temp_ptr(c, s, t)[e] = v;
+          }
+        } else if (st.op == kArgmax) {
+          // first index of the max (backend.cpp:164-173); one thread per node.
+          for (int t = threadIdx.x; t < c.nn; t += blockDim.x) {
+            const float* a = ref_ptr(c, st.ins[0], t);
+            int best = 0;
+            for (int i = 1; i < st.ins[0].cols_r; ++i)
+              if (a[i] > a[best]) best = i;
+            temp_ptr(c, s, t)[0] = static_cast<float>(best);
+          }
+        } else {
+          // elementwise add / mul / sigmoid / tanh / relu
+          const int n = st.rows * st.cols;
+          const int e0 = sp ? u0 : 0, e1 = sp ? u1 : n;
+          const int ncr = e1 - e0;
+          const int total = c.nn * ncr;
+          for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
+            const int t = idx / ncr, e = e0 + idx % ncr;
+            const float a = ref_ptr(c, st.ins[0], t)[e];
+            const float b = st.nin > 1 ? ref_ptr(c, st.ins[1], t)[e] : 0.0f;
+            temp_ptr(c, s, t)[e] = apply_op(st.op, a, b);
+          }
+        }
+        break;
+      }
+      case kStepChain: {
+        const int n = st.rows * st.cols;
+        const int e0 = sp ? u0 : 0, e1 = sp ? u1 : n;
+        const int ncr = e1 - e0;
+        const int total = c.nn * ncr;
+        for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
+          const int t = idx / ncr, e = e0 + idx % ncr;
+          float v = ref_ptr(c, st.ins[0], t)[e];
+          for (int l = 0; l < st.nchain; ++l) {
+            const DLink& lk = st.chain[l];
+            const float rhs = lk.has_rhs ? ref_ptr(c, lk.rhs, t)[e] : 0.0f;
+            v = apply_op(lk.op, v, rhs);
+          }
+          temp_ptr(c, s, t)[e] = v;
+        }
+        break;
+      }
+    }
+    __syncthreads();
+  }
+
+  // Plan outputs -> batch-contiguous regions (exec_batched.cpp:146-154).
+  for (int k = 0; k < P->nout; ++k) {
+    const DRef& o = P->outputs[k];
+    const int size = o.rows_r * o.cols_r;
+    const bool osp = tiled && P->out_split[k];
+    if (!osp && blockIdx.y != 0) continue;
+    const int e0 = osp ? u0 : 0, e1 = osp ? u1 : size;
+    const int ncr = e1 - e0;
+    const int total = c.nn * ncr;
+    for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
+      const int t = idx / ncr, e = e0 + idx % ncr;
+      c.arena[L.out_base[k] + int64_t(c.node0 + t) * size + e] = ref_ptr(c, o, t)[e];
+    }
+  }
+}
+
+// EXPLICIT gather (exec_batched.cpp:46-65): copy each instance's batched slot into a
+// contiguous scratch region.
+__global__ void gather_rows_kernel(float* arena, const int64_t* src_off, int64_t dst_off, int b,
+                                   int size) {
+  const int64_t total = int64_t(b) * size;
+  for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < total;
+       idx += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = idx / size, e = idx % size;
+    arena[dst_off + idx] = arena[src_off[i] + e];
+  }
+}
+
+// Packs n arena ranges (offset, size) into a contiguous staging buffer (one D2H copy for all
+// outputs / scalar decisions of a flush).
+__global__ void pack_ranges_kernel(const float* arena, const int64_t* ranges, int n, float* dst) {
+  for (int r = blockIdx.x; r < n; r += gridDim.x) {
+    const int64_t off = ranges[3 * r], size = ranges[3 * r + 1], dst_off = ranges[3 * r + 2];
+    for (int64_t e = threadIdx.x; e < size; e += blockDim.x) dst[dst_off + e] = arena[off + e];
+  }
+}
+
+__global__ void fill_kernel(float* arena, int64_t off, int64_t n, float v) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    arena[off + i] = v;
+}
+
+}  // namespace
+
+cudaError_t launch_plan_vm(const VmLaunch& L, cudaStream_t stream) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(plan_vm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    attr_set = true;
+  }
+  dim3 grid((L.b + L.tm - 1) / L.tm, L.nsplit);
+  plan_vm_kernel<<<grid, L.threads, L.smem_bytes, stream>>>(L);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gather_rows(float* arena, const int64_t* src_off, int64_t dst_off, int b, int size,
+                               cudaStream_t stream) {
+  int64_t total = int64_t(b) * size;
+  int blocks = int(std::min<int64_t>((total + 255) / 256, 148 * 8));
+  gather_rows_kernel<<<blocks, 256, 0, stream>>>(arena, src_off, dst_off, b, size);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pack_ranges(const float* arena, const int64_t* ranges, int n, float* dst,
+                               cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  pack_ranges_kernel<<<std::min(n, 148 * 4), 128, 0, stream>>>(arena, ranges, n, dst);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fill(float* arena, int64_t off, int64_t n, float v, cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  int blocks = int(std::min<int64_t>((n + 255) / 256, 148 * 8));
+  fill_kernel<<<blocks, 256, 0, stream>>>(arena, off, n, v);
+  return cudaGetLastError();
+}
+
+}  // namespace mbx

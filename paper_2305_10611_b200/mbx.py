@@ -1,0 +1,455 @@
+"""ctypes binding of libmbx.so (include/mbx.h) — the host-side mirror of the reference's
+`mbatch` runtime API (proj/include/mbatch/runtime.hpp) for Python callers and tests.
+
+Names follow the reference: ``evaluate_batch`` returns an ``EvalResult`` with ``outputs`` (host
+values), ``trace`` (a ``ScheduleTrace``: batches, counters, flush boundaries) and ``nodes`` (the
+DFG node table).  Errors raise ``MbatchError`` carrying the reference's message text.
+
+There is no fallback: if the native library is missing or the CUDA device cannot be opened the
+calls raise — the product path is the sm_100a library or nothing.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass, field
+from typing import Any, List, Optional, Sequence, Tuple
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libmbx.so")
+
+PREC = {"fp32": 0, "bf16x3": 1, "bf16": 2}
+OPS = ["dense", "add", "mul", "sigmoid", "tanh", "relu", "concat", "argmax", "fill"]
+
+
+class MbatchError(RuntimeError):
+    """mbatch::Error raised across the C ABI (same message text as the reference)."""
+
+
+class _Opts(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int32) for n in
+                ("scheduler", "gather", "hoist", "phases", "record_nodes", "time_kernels")]
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise MbatchError(f"native library not built: {LIB_PATH} (run __graft_entry__.build())")
+    L = ctypes.CDLL(LIB_PATH)
+    P, I, I64, F = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_float
+    pI32, pI64, pF, pD = (ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int64),
+                          ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_double))
+    sig = {
+        "mbx_version": (ctypes.c_char_p, []),
+        "mbx_kernel_launch_count": (I64, []),
+        "mbx_ctx_create": (I, [I, I, ctypes.POINTER(P)]),
+        "mbx_ctx_destroy": (None, [P]),
+        "mbx_last_error": (ctypes.c_char_p, [P]),
+        "mbx_ctx_set_precision": (I, [P, I]),
+        "mbx_sync": (I, [P]),
+        "mbx_arena_alloc": (I, [P, I, I, pI64]),
+        "mbx_arena_used": (I64, [P]),
+        "mbx_arena_upload": (I, [P, I64, pF, I64]),
+        "mbx_arena_download": (I, [P, I64, pF, I64]),
+        "mbx_arena_rewind": (I, [P, I64]),
+        "mbx_plan_register": (I, [P, pI32, I64, ctypes.POINTER(I)]),
+        "mbx_exec_batched": (I, [P, I, I, pI64, pI64, I, pI64, pI64]),
+        "mbx_exec_primop": (I, [P, I, I, pI64, ctypes.POINTER(I), ctypes.POINTER(I), I64, I, I, F]),
+        "mbx_model_create": (I, [P, ctypes.c_char_p, I, ctypes.POINTER(P)]),
+        "mbx_model_destroy": (None, [P]),
+        "mbx_model_make_params": (I, [P, ctypes.c_uint]),
+        "mbx_model_set_param": (I, [P, ctypes.c_char_p, pF, I64]),
+        "mbx_model_num_params": (I, [P]),
+        "mbx_model_param_name": (ctypes.c_char_p, [P, I]),
+        "mbx_model_make_inputs": (I, [P, ctypes.c_uint, I, pI32, pI64, pF, pI64]),
+        "mbx_model_num_sigs": (I, [P]),
+        "mbx_model_sig_name": (ctypes.c_char_p, [P, I]),
+        "mbx_model_plan_encoding": (I, [P, I, pI32, pI64]),
+        "mbx_options_default": (None, [ctypes.POINTER(_Opts)]),
+        "mbx_evaluate_batch": (I, [P, I, pI32, I64, pF, I64, ctypes.POINTER(_Opts), ctypes.POINTER(P)]),
+        "mbx_result_destroy": (None, [P]),
+        "mbx_result_outputs": (I, [P, pI32, pI64, pF, pI64]),
+        "mbx_result_counters": (I, [P, pI64]),
+        "mbx_result_batches": (I, [P, pI32, pI32]),
+        "mbx_result_flush_boundaries": (I, [P, pI32]),
+        "mbx_result_nodes": (I, [P, pI32, pI64, pI64]),
+        "mbx_result_timing": (I, [P, pD]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(L, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = L
+    return L
+
+
+def exported_symbols() -> List[str]:
+    """mbx_* functions declared in include/mbx.h (for ABI checks)."""
+    return [s for s in ("mbx_version mbx_kernel_launch_count mbx_ctx_create mbx_ctx_destroy mbx_last_error "
+                        "mbx_ctx_set_precision mbx_sync mbx_arena_alloc mbx_arena_used mbx_arena_upload "
+                        "mbx_arena_download mbx_arena_rewind mbx_plan_register mbx_exec_batched mbx_exec_primop "
+                        "mbx_model_create mbx_model_destroy mbx_model_make_params mbx_model_set_param "
+                        "mbx_model_num_params mbx_model_param_name mbx_model_make_inputs mbx_model_num_sigs "
+                        "mbx_model_sig_name mbx_model_plan_encoding mbx_options_default mbx_evaluate_batch "
+                        "mbx_result_destroy mbx_result_outputs mbx_result_counters mbx_result_batches "
+                        "mbx_result_flush_boundaries mbx_result_nodes mbx_result_timing").split()]
+
+
+def _ptr(a: np.ndarray, ct):
+    return a.ctypes.data_as(ctypes.POINTER(ct))
+
+
+# ---- host values ---------------------------------------------------------------------------
+
+@dataclass
+class Adt:
+    ctor: str
+    fields: list
+
+
+def decode_hostvals(toks: np.ndarray, data: np.ndarray, count: int) -> list:
+    """Decodes `count` values of the hostval encoding (see include/mbx.h)."""
+    ti, di = 0, 0
+
+    def one():
+        nonlocal ti, di
+        k = int(toks[ti]); ti += 1
+        if k == 0:
+            r, c = int(toks[ti]), int(toks[ti + 1]); ti += 2
+            v = np.array(data[di:di + r * c], dtype=np.float32).reshape(r, c); di += r * c
+            return v
+        if k == 1:
+            v = int(toks[ti]); ti += 1
+            return v
+        ctor = None
+        if k == 4:
+            ctor = "Node" if int(toks[ti]) else "Leaf"; ti += 1
+        n = int(toks[ti]); ti += 1
+        items = [one() for _ in range(n)]
+        if k == 2:
+            return items
+        if k == 3:
+            return tuple(items)
+        return Adt(ctor, items)
+
+    out = [one() for _ in range(count)]
+    assert ti == len(toks) and di == len(data), "trailing hostval data"
+    return out
+
+
+def flatten_floats(v) -> np.ndarray:
+    """All tensor data of a host value, depth-first (the digest order of the oracle)."""
+    parts = []
+
+    def go(x):
+        if isinstance(x, np.ndarray):
+            parts.append(x.reshape(-1))
+        elif isinstance(x, (list, tuple)):
+            for y in x:
+                go(y)
+        elif isinstance(x, Adt):
+            for y in x.fields:
+                go(y)
+
+    go(v)
+    return np.concatenate(parts).astype(np.float32) if parts else np.zeros(0, np.float32)
+
+
+# ---- results -------------------------------------------------------------------------------
+
+@dataclass
+class BatchRecord:
+    phase: int
+    depth: int
+    sig: int
+    size: int
+    ghost: bool
+    node_ids: List[int]
+
+
+@dataclass
+class ScheduleTrace:
+    batches: List[BatchRecord]
+    kernel_launches: int
+    total_nodes: int
+    scheduler_ops: int
+    sync_points: int
+    gather_bytes: int
+    dfg_edges: int
+    flush_boundaries: List[int]
+    device_launches: int = 0
+
+
+@dataclass
+class DFGNode:
+    id: int
+    sig_id: int
+    block_id: int
+    instance: int
+    phase: int
+    depth: int
+    ghost: bool
+    shared_ins: List[Tuple[int, int, int]]
+    batched_ins: List[Tuple[int, int, int]]
+    producers: List[int]
+    outputs: List[Tuple[int, int, int]]
+
+
+@dataclass
+class Timing:
+    host_total_us: float
+    host_dfg_us: float
+    device_span_us: float
+    h2d_bytes: int
+    d2h_bytes: int
+
+
+@dataclass
+class EvalResult:
+    outputs: list
+    trace: ScheduleTrace
+    nodes: List[DFGNode] = field(default_factory=list)
+    timing: Optional[Timing] = None
+    out_toks: Optional[np.ndarray] = None
+    out_data: Optional[np.ndarray] = None
+
+
+# ---- context / model -----------------------------------------------------------------------
+
+class Context:
+    """One device + stream + HBM arena (device < 0: host-only dry run, no CUDA)."""
+
+    def __init__(self, device: int = 0, precision: str = "fp32"):
+        L = lib()
+        h = ctypes.c_void_p()
+        if L.mbx_ctx_create(device, PREC[precision], ctypes.byref(h)) != 0:
+            raise MbatchError(L.mbx_last_error(None).decode())
+        self.h = h
+        self.device = device
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().mbx_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def check(self, rc: int):
+        if rc != 0:
+            raise MbatchError(lib().mbx_last_error(self.h).decode())
+
+    def set_precision(self, precision: str):
+        self.check(lib().mbx_ctx_set_precision(self.h, PREC[precision]))
+
+    def sync(self):
+        self.check(lib().mbx_sync(self.h))
+
+    # arena
+    def alloc(self, rows: int, cols: int) -> int:
+        off = ctypes.c_int64()
+        self.check(lib().mbx_arena_alloc(self.h, rows, cols, ctypes.byref(off)))
+        return off.value
+
+    def used(self) -> int:
+        return lib().mbx_arena_used(self.h)
+
+    def upload(self, offset: int, arr: np.ndarray):
+        a = np.ascontiguousarray(arr, dtype=np.float32).reshape(-1)
+        self.check(lib().mbx_arena_upload(self.h, offset, _ptr(a, ctypes.c_float), a.size))
+
+    def download(self, offset: int, n: int) -> np.ndarray:
+        a = np.empty(n, np.float32)
+        self.check(lib().mbx_arena_download(self.h, offset, _ptr(a, ctypes.c_float), n))
+        return a
+
+    def tensor(self, arr: np.ndarray) -> Tuple[int, Tuple[int, int]]:
+        arr = np.asarray(arr, np.float32)
+        if arr.ndim == 1:
+            arr = arr.reshape(1, -1)
+        off = self.alloc(*arr.shape)
+        self.upload(off, arr)
+        return off, arr.shape
+
+    # plans / batched execution (backend::exec_batched)
+    def register_plan(self, enc: Sequence[int]) -> int:
+        e = np.asarray(enc, np.int32)
+        pid = ctypes.c_int()
+        self.check(lib().mbx_plan_register(self.h, _ptr(e, ctypes.c_int32), e.size, ctypes.byref(pid)))
+        return pid.value
+
+    def exec_batched(self, plan_id: int, shared: Sequence[int], batched: np.ndarray, nout: int,
+                     gather: str = "fused") -> Tuple[np.ndarray, int]:
+        b = batched.shape[0]
+        s = np.asarray(shared, np.int64)
+        bt = np.ascontiguousarray(batched, np.int64)
+        out = np.zeros(b * nout, np.int64)
+        gb = ctypes.c_int64()
+        self.check(lib().mbx_exec_batched(self.h, plan_id, b, _ptr(s, ctypes.c_int64), _ptr(bt, ctypes.c_int64),
+                                          1 if gather == "explicit" else 0, _ptr(out, ctypes.c_int64),
+                                          ctypes.byref(gb)))
+        return out.reshape(b, nout), gb.value
+
+    def exec_primop(self, op: str, ins: Sequence[Tuple[int, Tuple[int, int]]], out: Tuple[int, Tuple[int, int]],
+                    fill: float = 0.0):
+        offs = np.array([o for o, _ in ins], np.int64)
+        rows = (ctypes.c_int * max(1, len(ins)))(*[s[0] for _, s in ins])
+        cols = (ctypes.c_int * max(1, len(ins)))(*[s[1] for _, s in ins])
+        self.check(lib().mbx_exec_primop(self.h, OPS.index(op), len(ins), _ptr(offs, ctypes.c_int64), rows, cols,
+                                         out[0], out[1][0], out[1][1], fill))
+
+
+class Model:
+    """A zoo model compiled for the device (zoo::get_model) with resident parameters."""
+
+    def __init__(self, ctx: Context, name: str, hidden: int):
+        self.ctx = ctx
+        self.name = name
+        self.hidden = hidden
+        h = ctypes.c_void_p()
+        ctx.check(lib().mbx_model_create(ctx.h, name.encode(), hidden, ctypes.byref(h)))
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().mbx_model_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def make_params(self, seed: int):
+        self.ctx.check(lib().mbx_model_make_params(self.h, seed))
+
+    def set_param(self, name: str, arr: np.ndarray):
+        a = np.ascontiguousarray(arr, np.float32).reshape(-1)
+        self.ctx.check(lib().mbx_model_set_param(self.h, name.encode(), _ptr(a, ctypes.c_float), a.size))
+
+    def param_names(self) -> List[str]:
+        return [lib().mbx_model_param_name(self.h, i).decode() for i in range(lib().mbx_model_num_params(self.h))]
+
+    def make_inputs(self, seed: int, batch: int) -> Tuple[np.ndarray, np.ndarray]:
+        nt, nd = ctypes.c_int64(), ctypes.c_int64()
+        self.ctx.check(lib().mbx_model_make_inputs(self.h, seed, batch, None, ctypes.byref(nt), None, ctypes.byref(nd)))
+        t = np.zeros(nt.value, np.int32)
+        d = np.zeros(nd.value, np.float32)
+        self.ctx.check(lib().mbx_model_make_inputs(self.h, seed, batch, _ptr(t, ctypes.c_int32), ctypes.byref(nt),
+                                                   _ptr(d, ctypes.c_float), ctypes.byref(nd)))
+        return t, d
+
+    def signatures(self) -> List[str]:
+        return [lib().mbx_model_sig_name(self.h, i).decode() for i in range(lib().mbx_model_num_sigs(self.h))]
+
+    def plan_encoding(self, sig: int) -> np.ndarray:
+        n = ctypes.c_int64()
+        self.ctx.check(lib().mbx_model_plan_encoding(self.h, sig, None, ctypes.byref(n)))
+        e = np.zeros(n.value, np.int32)
+        self.ctx.check(lib().mbx_model_plan_encoding(self.h, sig, _ptr(e, ctypes.c_int32), ctypes.byref(n)))
+        return e
+
+    def evaluate_batch(self, toks: np.ndarray, data: np.ndarray, batch: int, scheduler: str = "depth",
+                       gather: str = "fused", hoist: bool = True, phases: bool = True, record_nodes: bool = True,
+                       time_kernels: bool = False, decode: bool = True) -> EvalResult:
+        L = lib()
+        o = _Opts()
+        L.mbx_options_default(ctypes.byref(o))
+        o.scheduler = 1 if scheduler == "agenda" else 0
+        o.gather = 1 if gather == "explicit" else 0
+        o.hoist, o.phases = int(hoist), int(phases)
+        o.record_nodes, o.time_kernels = int(record_nodes), int(time_kernels)
+        t = np.ascontiguousarray(toks, np.int32)
+        d = np.ascontiguousarray(data, np.float32)
+        r = ctypes.c_void_p()
+        self.ctx.check(L.mbx_evaluate_batch(self.h, batch, _ptr(t, ctypes.c_int32), t.size, _ptr(d, ctypes.c_float),
+                                            d.size, ctypes.byref(o), ctypes.byref(r)))
+        try:
+            return _read_result(r, batch, record_nodes, decode)
+        finally:
+            L.mbx_result_destroy(r)
+
+
+def _read_result(r, batch: int, record_nodes: bool, decode: bool) -> EvalResult:
+    L = lib()
+    nt, nd = ctypes.c_int64(), ctypes.c_int64()
+    L.mbx_result_outputs(r, None, ctypes.byref(nt), None, ctypes.byref(nd))
+    ot = np.zeros(nt.value, np.int32)
+    od = np.zeros(nd.value, np.float32)
+    L.mbx_result_outputs(r, _ptr(ot, ctypes.c_int32), ctypes.byref(nt), _ptr(od, ctypes.c_float), ctypes.byref(nd))
+    c = np.zeros(9, np.int64)
+    L.mbx_result_counters(r, _ptr(c, ctypes.c_int64))
+    nb = int(c[6])
+    rows = np.zeros(5 * max(1, nb), np.int32)
+    total_ids = 0
+    ids = np.zeros(max(1, int(c[1])), np.int32)
+    L.mbx_result_batches(r, _ptr(rows, ctypes.c_int32), _ptr(ids, ctypes.c_int32))
+    batches, k = [], 0
+    for b in range(nb):
+        ph, dp, sg, sz, gh = (int(x) for x in rows[5 * b:5 * b + 5])
+        batches.append(BatchRecord(ph, dp, sg, sz, bool(gh), [int(x) for x in ids[k:k + sz]]))
+        k += sz
+        total_ids += sz
+    fb = np.zeros(max(1, int(c[7])), np.int32)
+    L.mbx_result_flush_boundaries(r, _ptr(fb, ctypes.c_int32))
+    trace = ScheduleTrace(batches, int(c[0]), int(c[1]), int(c[2]), int(c[3]), int(c[4]), int(c[5]),
+                          [int(x) for x in fb[:int(c[7])]], int(c[8]))
+    nodes = []
+    if record_nodes and c[1] > 0:
+        nr = ctypes.c_int64()
+        L.mbx_result_nodes(r, None, None, ctypes.byref(nr))
+        hdr = np.zeros(11 * int(c[1]), np.int32)
+        refs = np.zeros(max(1, nr.value), np.int64)
+        L.mbx_result_nodes(r, _ptr(hdr, ctypes.c_int32), _ptr(refs, ctypes.c_int64), ctypes.byref(nr))
+        k = 0
+        for i in range(int(c[1])):
+            h = [int(x) for x in hdr[11 * i:11 * i + 11]]
+            ns, nbt, npr, no = h[7], h[8], h[9], h[10]
+            sh = [tuple(int(x) for x in refs[k + 3 * j:k + 3 * j + 3]) for j in range(ns)]; k += 3 * ns
+            bt = [tuple(int(x) for x in refs[k + 3 * j:k + 3 * j + 3]) for j in range(nbt)]; k += 3 * nbt
+            pr = [int(x) for x in refs[k:k + npr]]; k += npr
+            ou = [tuple(int(x) for x in refs[k + 3 * j:k + 3 * j + 3]) for j in range(no)]; k += 3 * no
+            nodes.append(DFGNode(h[0], h[1], h[2], h[3], h[4], h[5], bool(h[6]), sh, bt, pr, ou))
+    tm = np.zeros(5, np.float64)
+    L.mbx_result_timing(r, _ptr(tm, ctypes.c_double))
+    timing = Timing(float(tm[0]), float(tm[1]), float(tm[2]), int(tm[3]), int(tm[4]))
+    outputs = decode_hostvals(ot, od, batch) if decode else []
+    return EvalResult(outputs, trace, nodes, timing, ot, od)
+
+
+# ---- plan encodings ------------------------------------------------------------------------
+
+def plan_from_dump(p: dict) -> List[int]:
+    """mbx_plan_register encoding of a plan as dumped by oracle/ref_harness.cpp."""
+    kind = {"S": 0, "B": 1, "T": 2}
+    stepk = {"op": 0, "fused_dense": 1, "chain": 2}
+    e = [1 if p["ghost"] else 0, len(p["shared_shapes"])]
+    for r, c in p["shared_shapes"]:
+        e += [r, c]
+    e.append(len(p["batched_shapes"]))
+    for r, c in p["batched_shapes"]:
+        e += [r, c]
+    e.append(len(p["steps"]))
+    for st in p["steps"]:
+        e += [stepk[st["kind"]], OPS.index(st["op"]), st["out"][0], st["out"][1], len(st["ins"])]
+        for k, i, off, cols in st["ins"]:
+            e += [kind[k], i, off, cols]
+        e.append(len(st["chain"]))
+        for l in st["chain"]:
+            e += [OPS.index(l["op"]), 1 if l["rhs"] is not None else 0]
+            e += ([kind[l["rhs"][0]], *l["rhs"][1:]] if l["rhs"] is not None else [2, 0, 0, -1])
+    e.append(len(p["outputs"]))
+    for k, i, off, cols in p["outputs"]:
+        e += [kind[k], i, off, cols]
+    return e
