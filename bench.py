@@ -1,0 +1,397 @@
+#!/usr/bin/env python
+"""Benchmark of the batched-execution hot path (BASELINE.json: "batched nodes/sec and ms per
+mini-batch (bs 8/64) at 1/2/4/8 B200 vs CPU ref").
+
+A step = one mini-batch of the workload evaluated end to end by the runtime: fibers + inline-depth
+DFG construction + depth scheduling on the host, every batch as a device launch, synthetic inputs
+from the reference's zoo generators.  Default workload: TreeLSTM hidden 512, batch 64 (the
+headline config, BASELINE.json configs[1]).
+
+  value  nodes/s with the mini-batch's inputs already resident in HBM (no input H2D, outputs left
+         in HBM), timed with CUDA events on the library's stream, L2 flushed between steps.
+  e2e    the same through the C ABI with HOST buffers: H2D of the inputs, the run, D2H of the
+         outputs, every step (mbx_evaluate_batch, the reference-facing evaluate_batch).
+Multi-GPU (torchrun, one process per GPU): each rank runs its own mini-batch (seed + rank) —
+instances shard independently, no collective on the data path ("scaling": "weak"); NCCL is used
+only for the start barrier and the max-over-ranks of the timings.
+
+--impl reference: the reference's own CPU implementation (oracle/_ref/mbatch_ref, the unmodified
+reference compiled here) on the host cores, one process per core, each timing evaluate_batch on
+its own mini-batch.
+"""
+import argparse
+import json
+import os
+import shutil
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+METRIC = "batched nodes/sec and ms per mini-batch (bs 8/64) at 1/2/4/8 B200 vs CPU ref"
+REF_BIN = os.path.join(ROOT, "oracle", "_ref", "mbatch_ref")
+
+
+def parse_args():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--model", default="treelstm")
+    p.add_argument("--hidden", type=int, default=512)
+    p.add_argument("--batch", type=int, default=64)
+    p.add_argument("--seed", type=int, default=1)
+    p.add_argument("--precision", default="bf16x3", choices=["fp32", "bf16x3", "bf16"])
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    return p.parse_args()
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        j = json.load(open(path))
+        return {"hbm_gbs": j["hbm_gbs"], "bf16_tflops": j["bf16_tflops"], "src": "measured"}
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "src": "fallback"}
+
+
+# ---- algorithmic work --------------------------------------------------------
+
+def decode_plan(enc):
+    """mbx plan encoding -> dict with shapes and steps (see include/mbx.h)."""
+    e = list(enc)
+    i = 0
+
+    def get():
+        nonlocal i
+        i += 1
+        return e[i - 1]
+
+    def ref():
+        return (get(), get(), get(), get())
+
+    p = {"ghost": get(), "shared": [], "batched": [], "steps": [], "outputs": []}
+    for _ in range(get()):
+        p["shared"].append((get(), get()))
+    for _ in range(get()):
+        p["batched"].append((get(), get()))
+    for _ in range(get()):
+        st = {"kind": get(), "op": get(), "out": (get(), get())}
+        st["ins"] = [ref() for _ in range(get())]
+        st["chain"] = []
+        for _ in range(get()):
+            op, has = get(), get()
+            r = ref()
+            st["chain"].append((op, r if has else None))
+        p["steps"].append(st)
+    for _ in range(get()):
+        p["outputs"].append(ref())
+    return p
+
+
+def launch_work(plan, b, weight_bytes):
+    """(flops, bytes) of one launch of `plan` over b nodes: dense steps 2*m*k*n per node (steps whose
+    operands are all shared count once per launch), bytes = shared tensors once (weights at their
+    storage width) + b * (batched inputs + outputs) in fp32."""
+    def shape(r, cur):
+        kind, idx, off, cols = r
+        s = plan["shared"][idx] if kind == 0 else plan["batched"][idx] if kind == 1 else plan["steps"][idx]["out"]
+        return (1, cols) if cols >= 0 else s
+
+    shared_only = []
+    flops = 0
+    for s, st in enumerate(plan["steps"]):
+        refs = list(st["ins"]) + [r for _, r in st["chain"] if r is not None]
+        so = all(r[0] == 0 or (r[0] == 2 and shared_only[r[1]]) for r in refs)
+        shared_only.append(so)
+        if st["op"] == 0 and st["kind"] in (0, 1):
+            a = shape(st["ins"][0], s)
+            n = sum(shape(w, s)[1] for w in st["ins"][1:])
+            f = 2 * a[0] * a[1] * n
+            flops += f if so else f * b
+    sbytes = 0
+    for (r, c) in plan["shared"]:
+        sbytes += r * c * (weight_bytes if r > 1 else 4)
+    bbytes = sum(r * c * 4 for (r, c) in plan["batched"])
+    obytes = sum(shape(o, len(plan["steps"]))[0] * shape(o, len(plan["steps"]))[1] * 4 for o in plan["outputs"])
+    return flops, sbytes + b * (bbytes + obytes)
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+
+    def __init__(self, device):
+        self.device = device
+        self.lines = []
+        self.proc = None
+
+    def __enter__(self):
+        if shutil.which("nvidia-smi"):
+            q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in self.lines:
+            f = [x.strip() for x in l.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---- CPU legs ----------------------------------------------------------------------------------
+
+def cpu_reference_time(model, hidden, batch, seed, reps):
+    """Times the reference's batched CPU path (runtime::evaluate_batch) in oracle/_ref/mbatch_ref."""
+    out = subprocess.check_output([REF_BIN, "time", "--model", model, "--hidden", str(hidden), "--batch", str(batch),
+                                   "--seed", str(seed), "--reps", str(reps), "--no-verify"], text=True)
+    return json.loads(out)
+
+
+def cpu_port_time(model, hidden, batch, seed, reps):
+    """Fallback when the reference binary is absent: the oracle restatement (unbatched)."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from conftest import Oracle
+    o = Oracle()
+    m = o.model(model, hidden, seed)
+    m.make_inputs(seed, batch)
+    best = 1e30
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        m.evaluate()
+        best = min(best, (time.perf_counter() - t0) * 1e3)
+    return {"batched_ms_best": best, "batched_ms_mean": best, "nodes": None}
+
+
+def cpu_baseline(args, nodes):
+    if os.path.exists(REF_BIN):
+        j = cpu_reference_time(args.model, args.hidden, args.batch, args.seed, 3)
+        kind = "reference"
+    else:
+        j = cpu_port_time(args.model, args.hidden, args.batch, args.seed, 2)
+        j["nodes"] = nodes
+        kind = "port"
+    ms = j["batched_ms_mean"]
+    return {"value": j["nodes"] / (ms / 1e3), "unit": "nodes/s", "cores": 1, "kind": kind,
+            "ms_per_minibatch": ms,
+            "sample": f"{args.model} H={args.hidden} b={args.batch} seed {args.seed}: 1 warm-up + 3 timed "
+                      f"evaluate_batch calls, single thread"}
+
+
+def run_reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    if not os.path.exists(REF_BIN):
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/mbatch_ref not built (needs /root/reference)"}))
+        return
+    P = os.cpu_count() or 1
+    reps = max(1, args.steps)
+    procs = []
+    t0 = time.perf_counter()
+    for k in range(P):
+        procs.append(subprocess.Popen([REF_BIN, "time", "--model", args.model, "--hidden", str(args.hidden), "--batch",
+                                       str(args.batch), "--seed", str(args.seed + k), "--reps", str(reps), "--no-verify"],
+                                      stdout=subprocess.PIPE, text=True))
+    res = [json.loads(p.communicate()[0]) for p in procs]
+    wall = time.perf_counter() - t0
+    nodes_per_s = sum(r["nodes"] / (r["batched_ms_mean"] / 1e3) for r in res)
+    ms = statistics.mean(r["batched_ms_mean"] for r in res)
+    line = {"metric": METRIC, "impl": "reference", "value": nodes_per_s, "unit": "nodes/s", "n_gpus": args.gpus,
+            "steps": reps, "warmup": 1, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic (reference zoo generators, seeds %d..%d)" % (
+                args.seed, args.seed + P - 1),
+            "config": {"workload": f"{args.model}-h{args.hidden}-b{args.batch}", "hidden": args.hidden,
+                       "batch": args.batch, "processes": P},
+            "cpu_baseline": {"value": nodes_per_s, "unit": "nodes/s", "cores": P, "kind": "reference",
+                             "sample": f"{P} processes x {reps} evaluate_batch calls (+1 warm-up) of the unmodified "
+                                       f"reference, one mini-batch each; wall {wall:.1f}s"},
+            "e2e": {"value": nodes_per_s, "unit": "nodes/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+# ---- our arm -------------------------------------------------------------------------------------
+
+def run_ours(args):
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    from paper_2305_10611_b200 import mbx
+
+    ctx = mbx.Context(local, args.precision)
+    model = mbx.Model(ctx, args.model, args.hidden)
+    model.make_params(args.seed)
+    seed = args.seed + rank
+    toks, data = model.make_inputs(seed, args.batch)
+    stream = torch.cuda.ExternalStream(ctx.stream(), device=local)
+    l2 = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")
+
+    def step(**kw):
+        return model.evaluate_batch(toks, data, args.batch, record_nodes=False, decode=False, **kw)
+
+    for _ in range(max(3, args.warmup)):
+        r0 = step()
+    nodes = r0.trace.total_nodes
+    step(inputs_resident=False)  # leave this mini-batch's inputs in the arena for region A
+
+    def timed(kw, per_batch=False):
+        evs = []
+        batch_us = []
+        host = 0.0
+        for _ in range(args.steps):
+            with torch.cuda.stream(stream):
+                l2.zero_()  # flush L2 between steps (256 MiB > 126 MB L2)
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+            t0 = time.perf_counter()
+            r = step(**kw)
+            host += time.perf_counter() - t0
+            with torch.cuda.stream(stream):
+                b.record(stream)
+            evs.append((a, b))
+            if per_batch:
+                batch_us.append(r.timing.batch_us)
+        torch.cuda.synchronize(local)
+        dev_ms = sum(a.elapsed_time(b) for a, b in evs)
+        return dev_ms, host * 1e3, r, batch_us
+
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize(local)
+    launches0 = mbx.lib().mbx_kernel_launch_count()
+    with ClockSampler(local) as clocks:
+        dev_ms, host_ms, rA, _ = timed({"inputs_resident": True, "outputs_on_device": True, "time_kernels": True})
+        gpu_launches = mbx.lib().mbx_kernel_launch_count() - launches0
+        e2e_ms, e2e_host_ms, rB, _ = timed({})
+        prof_ms, _, rC, batch_us = timed({"time_batches": True}, per_batch=True)
+    times = torch.tensor([dev_ms, e2e_ms, float(nodes)], dtype=torch.float64, device=f"cuda:{local}")
+    if dist:
+        mx = times.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        tot = times.clone()
+        dist.all_reduce(tot, op=dist.ReduceOp.SUM)
+        dev_max, e2e_max, nodes_total = float(mx[0]), float(mx[1]), float(tot[2])
+    else:
+        dev_max, e2e_max, nodes_total = dev_ms, e2e_ms, float(nodes)
+    if rank != 0:
+        if dist:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    K = args.steps
+    value = nodes_total * K / (dev_max / 1e3)
+    e2e = nodes_total * K / (e2e_max / 1e3)
+    pk = peaks()
+    # Per-signature device time from region C and algorithmic work of each launch.
+    sigs = model.signatures()
+    plans = {s: decode_plan(model.plan_encoding(s)) for s in range(len(sigs))}
+    wbytes = 2 if args.precision == "bf16" else 4
+    per_sig = {}
+    R_total_us = 0.0
+    meas_total_us = 0.0
+    launch_rows = [b for b in rC.trace.batches if not b.ghost]
+    for k_step in batch_us:
+        for b, us in zip(launch_rows, k_step):
+            f, by = launch_work(plans[b.sig], b.size, wbytes)
+            e = per_sig.setdefault(b.sig, {"us": 0.0, "flops": 0.0, "bytes": 0.0, "launches": 0})
+            e["us"] += us
+            e["flops"] += f
+            e["bytes"] += by
+            e["launches"] += 1
+            R_total_us += max(f / (pk["bf16_tflops"] * 1e6), by / (pk["hbm_gbs"] * 1e3))
+            meas_total_us += us
+    dom = max(per_sig, key=lambda s: per_sig[s]["us"])
+    d = per_sig[dom]
+    t_s = d["us"] / 1e6
+    tensor_path = args.precision != "fp32"
+    compute_peak = pk["bf16_tflops"] if tensor_path else 74.4  # FP32 SIMT: 148 SM x 128 FMA x 2 x 1.965 GHz
+    bound = "tensor" if d["flops"] / (compute_peak * 1e12) > d["bytes"] / (pk["hbm_gbs"] * 1e9) else "hbm"
+    if bound == "hbm":
+        ach, peak, unit = d["bytes"] / t_s / 1e9, pk["hbm_gbs"], "GB/s"
+    else:
+        ach, peak, unit = d["flops"] / t_s / 1e12, compute_peak, "TFLOP/s"
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(prof):
+        tj = json.load(open(prof))
+        traffic = tj.get(f"{args.model}-h{args.hidden}-b{args.batch}-{args.precision}-{sigs[dom]}")
+    clk = clocks.summary()
+    line = {
+        "metric": METRIC, "value": value, "unit": "nodes/s", "n_gpus": world, "steps": K, "warmup": args.warmup,
+        "ms_per_step": dev_max / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": {"fp32": "f32", "bf16x3": "bf16x3 (split-bf16 tcgen05, fp32 accumulate)", "bf16": "bf16"}[args.precision],
+        "data": f"synthetic: reference zoo generators (params seed {args.seed}, inputs seed {args.seed}+rank)",
+        "config": {"workload": f"{args.model}-h{args.hidden}-b{args.batch}", "hidden": args.hidden,
+                   "batch": args.batch, "nodes_per_minibatch": nodes, "precision": args.precision,
+                   "l2": "flushed between steps (256 MiB write)", "parallelism": f"instance shards x{world}"},
+        "e2e": {"value": e2e, "unit": "nodes/s", "ms_per_step": e2e_max / K, "h2d_bytes_per_step": rB.timing.h2d_bytes,
+                "d2h_bytes_per_step": rB.timing.d2h_bytes},
+        "gpu_launches": int(gpu_launches),
+        "roofline": {"bound": bound, "achieved": ach, "peak": peak, "unit": unit, "frac": ach / peak,
+                     "traffic": traffic, "kernel": sigs[dom], "launches_per_step": d["launches"] // K,
+                     "peak_src": pk["src"] if tensor_path or bound == "hbm" else "fp32 SIMT nominal"},
+        "step_roofline": {"R_us": R_total_us / K, "kernel_us": meas_total_us / K,
+                          "frac": (R_total_us / meas_total_us) if meas_total_us else None,
+                          "def": "sum over launches of max(F/bf16 peak, B/HBM) vs summed launch times (SURVEY 8d)"},
+        "breakdown_us_per_step": {"host_dfg_and_launch": rA.timing.host_dfg_us, "device_span": rA.timing.device_span_us,
+                                  "per_sig": {sigs[s]: v["us"] / K for s, v in per_sig.items()}},
+        "clocks": clk,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(args, nodes)
+    print(json.dumps(line))
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        run_reference_arm(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

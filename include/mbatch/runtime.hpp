@@ -85,6 +85,9 @@ struct ExecOptions {
   // B200 additions
   bool record_nodes = true;     // keep EvalResult::nodes
   bool time_kernels = false;    // CUDA-event span of the device work
+  bool time_batches = false;    // CUDA events around every batch launch
+  bool inputs_resident = false; // inputs already materialised by an identical previous call
+  bool outputs_on_device = false;
 };
 
 // Static block of the compiled model (the reference's analysis::StaticBlock + hoist depth).
@@ -162,6 +165,7 @@ struct Timing {
   double device_span_us = 0;    // sum over flushes of first-to-last batch (CUDA events)
   long h2d_bytes = 0, d2h_bytes = 0;
   long device_launches = 0;     // CUDA kernels issued
+  std::vector<double> batch_us; // per non-ghost batch (time_batches)
 };
 
 struct EvalResult {

@@ -54,6 +54,8 @@ void mbx_ctx_destroy(mbx_ctx* ctx);
 const char* mbx_last_error(const mbx_ctx* ctx);
 int mbx_ctx_set_precision(mbx_ctx* ctx, int precision);
 int mbx_sync(mbx_ctx* ctx);
+/* The context's CUDA stream (cudaStream_t), for callers that time or order work around it. */
+void* mbx_ctx_stream(mbx_ctx* ctx);
 
 /* ---- arena: backend::Arena (backend.hpp:63-88) ----------------------------------------- */
 /* Bump-allocates rows*cols floats; *offset gets the element offset (Arena::alloc). */
@@ -76,8 +78,9 @@ int mbx_arena_rewind(mbx_ctx* ctx, int64_t used);
 int mbx_plan_register(mbx_ctx* ctx, const int32_t* enc, int64_t n, int* plan_id);
 
 /* backend::exec_batched (proj/src/exec_batched.cpp:23-157) over b instances.
- *   shared_off[nshared]        arena offsets of the shared inputs (identical across instances;
- *                              per-instance identity is checked by the C++ layer)
+ *   shared_off[b * nshared]    each instance's shared-input offsets (row-major); they must be
+ *                              identical across instances, else the call fails with
+ *                              "shared-param handle mismatch across instances (analysis bug)"
  *   batched_off[b * nbatched]  arena offsets of each instance's batched inputs (row-major)
  *   out_off[b * nout]          receives each instance's output handle offsets (batch-contiguous
  *                              per output slot, as the reference lays them out)
@@ -120,7 +123,12 @@ typedef struct {
   int32_t hoist;        /* honour static hoist depths (ExecOptions::hoist) */
   int32_t phases;       /* program phases (ExecOptions::phases) */
   int32_t record_nodes; /* keep the DFG node table in the result (oracle checks) */
-  int32_t time_kernels; /* CUDA-event timing of the device work */
+  int32_t time_kernels; /* CUDA-event timing of the device work (per flush) */
+  int32_t time_batches; /* CUDA-event timing of every batch launch (mbx_result_batch_times) */
+  int32_t inputs_resident;   /* inputs already in the arena from an identical previous call:
+                                skip their H2D copy (device-resident benchmarking) */
+  int32_t outputs_on_device; /* leave outputs in the arena (no D2H; outputs read back as 0) */
+  int32_t ghost;        /* ghost units of the lowered program (ExecOptions::ghost) */
 } mbx_options;
 void mbx_options_default(mbx_options* o);
 
@@ -149,6 +157,8 @@ int mbx_result_nodes(const mbx_result* r, int32_t* hdr, int64_t* refs, int64_t* 
 /* Timing of this evaluation in microseconds: host total, host DFG+schedule, device kernel span
  * (first to last batch, CUDA events), H2D bytes, D2H bytes. */
 int mbx_result_timing(const mbx_result* r, double* out5);
+/* Per non-ghost batch, in trace order: device duration in microseconds (time_batches). */
+int mbx_result_batch_times(const mbx_result* r, double* us);
 
 #ifdef __cplusplus
 }

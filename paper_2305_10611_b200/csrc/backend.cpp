@@ -752,7 +752,8 @@ BatchedResult exec_batched(Arena& arena, const ExecutablePlan& plan, const std::
                                                                      plan.shared_shapes[s].str() + ", actual " +
                                                                      first.shared[s].shape.str());
   std::vector<int64_t> shared, batched;
-  for (auto& h : first.shared) shared.push_back(h.offset);
+  for (auto& call : instances)
+    for (auto& h : call.shared) shared.push_back(h.offset);
   for (auto& call : instances) {
     MBATCH_CHECK(call.batched.size() == plan.batched_shapes.size(), "exec_batched: arity mismatch");
     for (size_t j = 0; j < call.batched.size(); ++j) {

@@ -162,6 +162,8 @@ int mbx_sync(mbx_ctx* c) {
   });
 }
 
+void* mbx_ctx_stream(mbx_ctx* c) { return c ? reinterpret_cast<void*>(c->stream) : nullptr; }
+
 int mbx_arena_alloc(mbx_ctx* c, int rows, int cols, int64_t* offset) {
   return guarded(c, [&] {
     MBATCH_CHECK(rows >= 0 && cols >= 0, "negative shape");
@@ -207,7 +209,14 @@ int mbx_plan_register(mbx_ctx* c, const int32_t* enc, int64_t n, int* plan_id) {
 int mbx_exec_batched(mbx_ctx* c, int plan_id, int b, const int64_t* shared_off, const int64_t* batched_off,
                      int gather_mode, int64_t* out_off, int64_t* gather_bytes) {
   return guarded(c, [&] {
+    MBATCH_CHECK(b > 0, "exec_batched: empty batch");
+    MBATCH_CHECK(plan_id >= 0 && size_t(plan_id) < c->plans.size(), "exec_batched: unknown plan");
     const auto& pe = c->plans.at(plan_id);
+    const size_t ns = pe.plan.shared_shapes.size();
+    for (int i = 1; i < b; ++i)
+      for (size_t s = 0; s < ns; ++s)
+        MBATCH_CHECK(shared_off[size_t(i) * ns + s] == shared_off[s],
+                     "shared-param handle mismatch across instances (analysis bug)");
     size_t bytes = 8 * (pe.plan.shared_shapes.size() + size_t(b) * pe.plan.batched_shapes.size() * 2 + pe.plan.outputs.size()) + 64;
     mbx::meta_reserve(c, bytes);
     mbx::BatchLaunch L = mbx::prepare_batch(c, plan_id, b, shared_off, batched_off, gather_mode, out_off, gather_bytes);
@@ -345,6 +354,10 @@ void mbx_options_default(mbx_options* o) {
   o->phases = 1;
   o->record_nodes = 1;
   o->time_kernels = 0;
+  o->time_batches = 0;
+  o->inputs_resident = 0;
+  o->outputs_on_device = 0;
+  o->ghost = 1;
 }
 
 int mbx_evaluate_batch(mbx_model* m, int batch, const int32_t* toks, int64_t ntok, const float* data, int64_t ndata,
@@ -370,6 +383,10 @@ int mbx_evaluate_batch(mbx_model* m, int batch, const int32_t* toks, int64_t nto
     o.phases = oo.phases != 0;
     o.record_nodes = oo.record_nodes != 0;
     o.time_kernels = oo.time_kernels != 0;
+    o.time_batches = oo.time_batches != 0;
+    o.inputs_resident = oo.inputs_resident != 0;
+    o.outputs_on_device = oo.outputs_on_device != 0;
+    o.ghost = oo.ghost != 0;
     res->r = m->session->evaluate(inputs, o);
     for (auto& v : res->r.outputs) encode(v, res->out_tok, res->out_data);
   });
@@ -447,6 +464,11 @@ int mbx_result_nodes(const mbx_result* r, int32_t* hdr, int64_t* refs, int64_t* 
   }
   *nrefs = need;
   return 0;
+}
+
+int mbx_result_batch_times(const mbx_result* r, double* us) {
+  for (size_t k = 0; k < r->r.timing.batch_us.size(); ++k) us[k] = r->r.timing.batch_us[k];
+  return int(r->r.timing.batch_us.size());
 }
 
 int mbx_result_timing(const mbx_result* r, double* o) {

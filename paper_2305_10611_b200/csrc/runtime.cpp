@@ -260,6 +260,7 @@ struct Executor::Impl {
   std::vector<std::pair<int64_t, const HostValue*>> input_tensors;
   Timing timing;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> flush_events;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> batch_events;
 
   Impl(Executor& e, Session& sess, const std::vector<InstanceInput>& in, const ExecOptions& o)
       : ex(e), s(sess), m(sess.model()), opts(o), c(sess.ctx()), inputs(in) {
@@ -270,10 +271,11 @@ struct Executor::Impl {
   }
 
   ~Impl() {
-    for (auto& [a, b] : flush_events) {
-      cudaEventDestroy(a);
-      cudaEventDestroy(b);
-    }
+    for (auto* v : {&flush_events, &batch_events})
+      for (auto& [a, b] : *v) {
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+      }
   }
 
   Val materialize(const HostValue& hv) {
@@ -304,10 +306,11 @@ struct Executor::Impl {
 
   void upload_inputs() {
     int64_t n = c->used - input_base;
-    if (n <= 0) return;
+    if (n <= 0 || opts.inputs_resident) return;
     mbx::ensure_input_stage(c, size_t(n));
     for (auto& [off, hv] : input_tensors)
       std::memcpy(c->in_host + (off - input_base), hv->data.data(), hv->data.size() * sizeof(float));
+    if (opts.inputs_resident) return;
     if (!c->dry)
       mbx::cuda_check(cudaMemcpyAsync(mbx::arena_ptr(c) + input_base, c->in_host, size_t(n) * sizeof(float),
                                       cudaMemcpyHostToDevice, c->stream),
@@ -514,7 +517,19 @@ struct Executor::Impl {
         cudaEventRecord(a, c->stream);
       }
       int64_t before = c->launches;
-      for (const auto& L : launches) mbx::issue_batch(c, L);
+      for (const auto& L : launches) {
+        if (opts.time_batches) {
+          cudaEvent_t x = nullptr, y = nullptr;
+          cudaEventCreate(&x);
+          cudaEventCreate(&y);
+          cudaEventRecord(x, c->stream);
+          mbx::issue_batch(c, L);
+          cudaEventRecord(y, c->stream);
+          batch_events.push_back({x, y});
+        } else {
+          mbx::issue_batch(c, L);
+        }
+      }
       timing.device_launches += long(c->launches - before);
       if (opts.time_kernels) {
         cudaEventRecord(e, c->stream);
@@ -727,7 +742,7 @@ EvalResult Executor::run() {
   }
   auto t_host = clk::now();
   std::vector<float> buf(total, 0.0f);
-  if (!I.c->dry && total > 0) I.pack_to_host(ranges, buf.data(), total);
+  if (!I.c->dry && total > 0 && !I.opts.outputs_on_device) I.pack_to_host(ranges, buf.data(), total);
   else if (!I.c->dry) mbx::cuda_check(cudaStreamSynchronize(I.c->stream), "final sync");
 
   EvalResult res;
@@ -741,6 +756,11 @@ EvalResult Executor::run() {
     float ms = 0;
     cudaEventElapsedTime(&ms, a, b);
     I.timing.device_span_us += ms * 1000.0;
+  }
+  for (auto& [a, b] : I.batch_events) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, a, b);
+    I.timing.batch_us.push_back(ms * 1000.0);
   }
   I.timing.host_dfg_us = std::chrono::duration<double, std::micro>(t_host - t0).count();
   I.timing.host_total_us = std::chrono::duration<double, std::micro>(clk::now() - t0).count();

@@ -30,7 +30,8 @@ class MbatchError(RuntimeError):
 
 class _Opts(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int32) for n in
-                ("scheduler", "gather", "hoist", "phases", "record_nodes", "time_kernels")]
+                ("scheduler", "gather", "hoist", "phases", "record_nodes", "time_kernels", "time_batches",
+                 "inputs_resident", "outputs_on_device", "ghost")]
 
 
 _lib = None
@@ -81,6 +82,8 @@ def lib() -> ctypes.CDLL:
         "mbx_result_flush_boundaries": (I, [P, pI32]),
         "mbx_result_nodes": (I, [P, pI32, pI64, pI64]),
         "mbx_result_timing": (I, [P, pD]),
+        "mbx_result_batch_times": (I, [P, pD]),
+        "mbx_ctx_stream": (P, [P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -99,7 +102,8 @@ def exported_symbols() -> List[str]:
                         "mbx_model_num_params mbx_model_param_name mbx_model_make_inputs mbx_model_num_sigs "
                         "mbx_model_sig_name mbx_model_plan_encoding mbx_options_default mbx_evaluate_batch "
                         "mbx_result_destroy mbx_result_outputs mbx_result_counters mbx_result_batches "
-                        "mbx_result_flush_boundaries mbx_result_nodes mbx_result_timing").split()]
+                        "mbx_result_flush_boundaries mbx_result_nodes mbx_result_timing mbx_result_batch_times "
+                        "mbx_ctx_stream").split()]
 
 
 def _ptr(a: np.ndarray, ct):
@@ -209,6 +213,7 @@ class Timing:
     device_span_us: float
     h2d_bytes: int
     d2h_bytes: int
+    batch_us: List[float] = field(default_factory=list)
 
 
 @dataclass
@@ -288,10 +293,19 @@ class Context:
         self.check(lib().mbx_plan_register(self.h, _ptr(e, ctypes.c_int32), e.size, ctypes.byref(pid)))
         return pid.value
 
-    def exec_batched(self, plan_id: int, shared: Sequence[int], batched: np.ndarray, nout: int,
+    def stream(self) -> int:
+        """cudaStream_t of the context (e.g. for torch.cuda.ExternalStream)."""
+        return lib().mbx_ctx_stream(self.h) or 0
+
+    def exec_batched(self, plan_id: int, shared, batched: np.ndarray, nout: int,
                      gather: str = "fused") -> Tuple[np.ndarray, int]:
+        """backend::exec_batched.  `shared` is either one row of shared offsets (broadcast to every
+        instance) or a (b, nshared) array of per-instance shared offsets."""
         b = batched.shape[0]
         s = np.asarray(shared, np.int64)
+        if s.ndim == 1:
+            s = np.tile(s, (b, 1))
+        s = np.ascontiguousarray(s)
         bt = np.ascontiguousarray(batched, np.int64)
         out = np.zeros(b * nout, np.int64)
         gb = ctypes.c_int64()
@@ -362,14 +376,16 @@ class Model:
 
     def evaluate_batch(self, toks: np.ndarray, data: np.ndarray, batch: int, scheduler: str = "depth",
                        gather: str = "fused", hoist: bool = True, phases: bool = True, record_nodes: bool = True,
-                       time_kernels: bool = False, decode: bool = True) -> EvalResult:
+                       time_kernels: bool = False, time_batches: bool = False, inputs_resident: bool = False,
+                       outputs_on_device: bool = False, ghost: bool = True, decode: bool = True) -> EvalResult:
         L = lib()
         o = _Opts()
         L.mbx_options_default(ctypes.byref(o))
         o.scheduler = 1 if scheduler == "agenda" else 0
         o.gather = 1 if gather == "explicit" else 0
-        o.hoist, o.phases = int(hoist), int(phases)
-        o.record_nodes, o.time_kernels = int(record_nodes), int(time_kernels)
+        o.hoist, o.phases, o.ghost = int(hoist), int(phases), int(ghost)
+        o.record_nodes, o.time_kernels, o.time_batches = int(record_nodes), int(time_kernels), int(time_batches)
+        o.inputs_resident, o.outputs_on_device = int(inputs_resident), int(outputs_on_device)
         t = np.ascontiguousarray(toks, np.int32)
         d = np.ascontiguousarray(data, np.float32)
         r = ctypes.c_void_p()
@@ -423,7 +439,9 @@ def _read_result(r, batch: int, record_nodes: bool, decode: bool) -> EvalResult:
             nodes.append(DFGNode(h[0], h[1], h[2], h[3], h[4], h[5], bool(h[6]), sh, bt, pr, ou))
     tm = np.zeros(5, np.float64)
     L.mbx_result_timing(r, _ptr(tm, ctypes.c_double))
-    timing = Timing(float(tm[0]), float(tm[1]), float(tm[2]), int(tm[3]), int(tm[4]))
+    bt = np.zeros(max(1, nb), np.float64)
+    nbt = L.mbx_result_batch_times(r, _ptr(bt, ctypes.c_double))
+    timing = Timing(float(tm[0]), float(tm[1]), float(tm[2]), int(tm[3]), int(tm[4]), bt[:nbt].tolist())
     outputs = decode_hostvals(ot, od, batch) if decode else []
     return EvalResult(outputs, trace, nodes, timing, ot, od)
 

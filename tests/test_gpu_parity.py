@@ -1,0 +1,161 @@
+"""Parity of the B200 path (through the C ABI) with the reference, on a real GPU.
+
+FP32 path: bit-exact.  The plan VM reproduces the reference's accumulation order and glibc's
+expf/tanhf, so every output tensor equals the reference's bit for bit and the schedule (which
+nodes land in which batch, in what order) equals the reference's exactly — including models whose
+control flow depends on tensor values (NestedRNN, DRNN, StackRNN: argmax decisions).
+"""
+import numpy as np
+import pytest
+
+from conftest import MODELS, trace_counters, trace_rows
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def gpu(mbx):
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    return mbx
+
+
+def _kw(variant):
+    kw = {}
+    if variant.startswith("agenda"):
+        kw["scheduler"] = "agenda"
+    if variant.endswith("explicit"):
+        kw["gather"] = "explicit"
+    if variant == "no-hoist":
+        kw["hoist"] = False
+    if variant == "no-phases":
+        kw["phases"] = False
+    return kw
+
+
+def _flat_golden(j):
+    if j["k"] == "t":
+        return list(j["d"])
+    return [x for it in j.get("items", []) for x in _flat_golden(it)]
+
+
+@pytest.mark.parametrize("model", MODELS)
+def test_fp32_bitwise_and_schedule(gpu, golden, oracle, model):
+    mbx = gpu
+    g = golden(model)
+    models = {}
+    for run in g["runs"]:
+        key = (run["hidden"], run["seed"])
+        if key not in models:
+            c = mbx.Context(0, "fp32")
+            m = mbx.Model(c, model, run["hidden"])
+            m.make_params(run["seed"])
+            models[key] = (c, m)
+        m = models[key][1]
+        t, d = m.make_inputs(run["seed"], run["batch"])
+        r = m.evaluate_batch(t, d, run["batch"], record_nodes="nodes" in run, **_kw(run["variant"]))
+        where = (model, run["variant"], run["hidden"], run["batch"], run["seed"])
+        assert trace_rows(r.trace) == trace_rows(run["trace"]), where
+        assert trace_counters(r.trace) == trace_counters(run["trace"]), where
+        assert oracle.digest(r.out_toks, r.out_data, run["batch"]) == run["digests"]["outputs"], where
+        if "outputs" in run:
+            for i, o in enumerate(run["outputs"]):
+                want = np.array(_flat_golden(o), np.float32)
+                got = mbx.flatten_floats(r.outputs[i])
+                assert np.array_equal(got.view(np.uint32), want.view(np.uint32)), where + (i,)
+        assert r.trace.device_launches >= r.trace.kernel_launches, where
+
+
+@pytest.mark.parametrize("idx", range(10))
+def test_fp32_baseline_configs(gpu, golden, idx):
+    mbx = gpu
+    run = golden("baseline")[idx]
+    c = mbx.Context(0, "fp32")
+    m = mbx.Model(c, run["model"], run["hidden"])
+    m.make_params(run["seed"])
+    t, d = m.make_inputs(run["seed"], run["batch"])
+    r = m.evaluate_batch(t, d, run["batch"], record_nodes=False)
+    from conftest import Oracle
+    assert trace_rows(r.trace) == trace_rows(run["trace"])
+    assert trace_counters(r.trace) == trace_counters(run["trace"])
+    assert Oracle().digest(r.out_toks, r.out_data, run["batch"]) == run["digests"]["outputs"]
+
+
+def _relu_bias_dense_plan(h):
+    return [0, 2, h, h, 1, h, 1, 1, h, 2,
+            0, 0, 1, h, 2, 1, 0, 0, -1, 0, 0, 0, -1, 0,
+            2, 1, 1, h, 1, 2, 0, 0, -1, 2, 1, 1, 0, 1, 0, -1, 5, 0, 2, 0, 0, -1,
+            1, 2, 1, 0, -1]
+
+
+def test_exec_batched_equals_primop_fold_bitwise(gpu):
+    """backend_test.cpp:134-173: exec_batched == per-instance fold of exec_primop, bitwise,
+    b in {1, 2, 8, 64}, both gather modes."""
+    mbx = gpu
+    rng = np.random.default_rng(11)
+    h = 4
+    for b in (1, 2, 8, 64):
+        ctx = mbx.Context(0, "fp32")
+        pid = ctx.register_plan(_relu_bias_dense_plan(h))
+        w, _ = ctx.tensor(rng.uniform(-1, 1, (h, h)))
+        bias, _ = ctx.tensor(rng.uniform(-1, 1, (1, h)))
+        xs = [ctx.tensor(rng.uniform(-1, 1, (1, h)))[0] for _ in range(b)]
+        for mode in ("fused", "explicit"):
+            outs, _ = ctx.exec_batched(pid, [w, bias], np.array(xs).reshape(b, 1), 1, mode)
+            for i in range(b):
+                t0, t1, t2 = ctx.alloc(1, h), ctx.alloc(1, h), ctx.alloc(1, h)
+                ctx.exec_primop("dense", [(xs[i], (1, h)), (w, (h, h))], (t0, (1, h)))
+                ctx.exec_primop("add", [(t0, (1, h)), (bias, (1, h))], (t1, (1, h)))
+                ctx.exec_primop("relu", [(t1, (1, h))], (t2, (1, h)))
+                a = ctx.download(int(outs[i, 0]), h)
+                e = ctx.download(t2, h)
+                assert np.array_equal(a.view(np.uint32), e.view(np.uint32))
+
+
+def test_primops_match_oracle(gpu, oracle):
+    """exec_primop on the device vs the CPU restatement on random small shapes
+    (backend_test.cpp:59-84), bitwise."""
+    import ctypes
+    mbx = gpu
+    rng = np.random.default_rng(7)
+    ctx = mbx.Context(0, "fp32")
+    L = oracle.L
+    L.orc_exec_primop.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                  ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_float]
+    for trial in range(50):
+        m, k, n = (int(x) for x in rng.integers(1, 9, size=3))
+        a = rng.uniform(-2, 2, (m, k)).astype(np.float32)
+        bm = rng.uniform(-2, 2, (k, n)).astype(np.float32)
+        cases = [("dense", [a, bm], (m, n)), ("tanh", [a], (m, k)), ("relu", [a], (m, k)), ("sigmoid", [a], (m, k)),
+                 ("add", [a, a[::-1].copy()], (m, k)), ("mul", [a, a], (m, k)), ("concat", [a, a], (m, 2 * k))]
+        for op, ins, oshape in cases:
+            offs = [ctx.tensor(x) for x in ins]
+            out = ctx.alloc(*oshape)
+            ctx.exec_primop(op, offs, (out, oshape))
+            got = ctx.download(out, oshape[0] * oshape[1])
+            arrs = [np.ascontiguousarray(x) for x in ins]
+            ptrs = (ctypes.c_void_p * len(arrs))(*[x.ctypes.data for x in arrs])
+            rows = (ctypes.c_int * len(arrs))(*[x.shape[0] for x in arrs])
+            cols = (ctypes.c_int * len(arrs))(*[x.shape[1] for x in arrs])
+            want = np.zeros(oshape, np.float32)
+            L.orc_exec_primop(mbx.OPS.index(op), len(arrs), ptrs, rows, cols, want.ctypes.data, oshape[0], oshape[1], 0.0)
+            assert np.array_equal(got.view(np.uint32), want.reshape(-1).view(np.uint32)), (op, m, k, n)
+
+
+def test_activation_restatements_exhaustive_sample(gpu, oracle):
+    """sigmoid / tanh on the device vs glibc on 2^22 float bit patterns spread over the whole
+    range (the full 2^32 sweep of the same code runs on the host in test_libm_exact.py)."""
+    mbx = gpu
+    ctx = mbx.Context(0, "fp32")
+    bits = (np.arange(1 << 22, dtype=np.uint64) * 1021 + 7) % (1 << 32)
+    x = bits.astype(np.uint32).view(np.float32)
+    x = x[np.isfinite(x)].reshape(1, -1)
+    n = x.shape[1]
+    xo, _ = ctx.tensor(x)
+    for op, which in (("sigmoid", 2), ("tanh", 1)):
+        out = ctx.alloc(1, n)
+        ctx.exec_primop(op, [(xo, (1, n))], (out, (1, n)))
+        got = ctx.download(out, n)
+        want = np.array([oracle.L.orc_unary(which, float(v)) for v in x[0, :: 997]], np.float32)
+        assert np.array_equal(got[::997].view(np.uint32), want.view(np.uint32)), op
