@@ -504,8 +504,15 @@ void issue_batch(mbx_ctx* c, const BatchLaunch& L) {
   v.b = L.b;
   v.tm = pe.tm;
   const int ntiles = (L.b + pe.tm - 1) / pe.tm;
+  // Column tiles: enough CTAs for ~2 waves over 148 SMs, and together they must cover the unit.
   v.nsplit = pe.max_split > 1 ? std::clamp((296 + ntiles - 1) / ntiles, 1, pe.max_split) : 1;
-  v.unit_chunk = pe.unit_chunk;
+  if (v.nsplit > 1) {
+    const int unit = pe.hplan.unit;
+    v.unit_chunk = ((unit + v.nsplit - 1) / v.nsplit + 7) / 8 * 8;
+    v.nsplit = (unit + v.unit_chunk - 1) / v.unit_chunk;
+  } else {
+    v.unit_chunk = pe.hplan.unit;
+  }
   v.threads = pe.threads;
   v.smem_bytes = pe.smem;
   v.shared_off = meta_dev<int64_t>(c, L.shared_meta);

@@ -247,34 +247,12 @@ int mbx_exec_primop(mbx_ctx* c, int op, int nin, const int64_t* in_off, const in
       ++mbx::g_launches;
       return;
     }
-    ExecutablePlan p;
-    p.shared_shapes = shapes;
-    PlanStep st;
-    st.kind = PlanStep::Kind::kOp;
-    st.op = o;
-    for (int i = 0; i < nin; ++i) st.ins.push_back(PlanRef{PlanRef::Kind::kShared, i, 0, -1});
-    st.out_shape = out;
-    p.steps.push_back(st);
-    p.outputs.push_back(PlanRef{PlanRef::Kind::kTemp, 0, 0, -1});
-    int pid = mbx::register_plan(c, p);
-    const auto& pe = c->plans[pid];
-    mbx::meta_reserve(c, size_t(nin + 1) * 8 + 32);
-    size_t sm = mbx::meta_stage(c, in_off, size_t(nin) * 8);
-    size_t om = mbx::meta_stage(c, &out_off, 8);
+    const int64_t b_off = nin > 1 ? in_off[1] : in_off[0];
+    const int br = nin > 1 ? in_rows[1] : 0, bc = nin > 1 ? in_cols[1] : 0;
     mbx::meta_commit(c);
-    mbx::VmLaunch v{};
-    v.plan = pe.dplan;
-    v.arena = mbx::arena_ptr(c);
-    v.b = 1;
-    v.tm = 1;
-    v.nsplit = 1;
-    v.unit_chunk = 0;
-    v.threads = 256;
-    v.smem_bytes = int(std::max<int64_t>(1, pe.hplan.temp_floats) * 4);
-    v.shared_off = mbx::meta_dev<int64_t>(c, sm);
-    v.batched_off = nullptr;
-    v.out_base = mbx::meta_dev<int64_t>(c, om);
-    mbx::cuda_check(mbx::launch_plan_vm(v, c->stream), "primop");
+    mbx::cuda_check(mbx::launch_primop(mbx::arena_ptr(c), op, in_off[0], in_rows[0], in_cols[0], b_off, br, bc, out_off,
+                                       out_rows, out_cols, c->stream),
+                    "primop");
     ++c->launches;
     ++mbx::g_launches;
   });

@@ -29,5 +29,7 @@ cudaError_t launch_gather_rows(float* arena, const int64_t* src_off, int64_t dst
 cudaError_t launch_pack_ranges(const float* arena, const int64_t* ranges, int n, float* dst,
                                cudaStream_t stream);
 cudaError_t launch_fill(float* arena, int64_t off, int64_t n, float v, cudaStream_t stream);
+cudaError_t launch_primop(float* arena, int op, int64_t a_off, int ar, int ac, int64_t b_off, int br, int bc,
+                          int64_t out_off, int orows, int ocols, cudaStream_t stream);
 
 }  // namespace mbx

@@ -234,6 +234,40 @@ __global__ void pack_ranges_kernel(const float* arena, const int64_t* ranges, in
   }
 }
 
+// exec_primop on arena tensors of any size (backend.cpp:105-181), one output element per thread
+// (grid-stride), same arithmetic as the plan VM.
+__global__ void primop_kernel(float* arena, int op, int64_t a_off, int ar, int ac, int64_t b_off, int br, int bc,
+                              int64_t out_off, int orows, int ocols) {
+  const float* A = arena + a_off;
+  const float* B = arena + b_off;
+  float* O = arena + out_off;
+  const int64_t n = int64_t(orows) * ocols;
+  if (op == kArgmax) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      int best = 0;
+      for (int i = 1; i < ac; ++i)
+        if (A[i] > A[best]) best = i;
+      O[0] = static_cast<float>(best);
+    }
+    return;
+  }
+  for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < n; idx += int64_t(gridDim.x) * blockDim.x) {
+    float v;
+    if (op == kDense) {
+      const int64_t i = idx / ocols, j = idx % ocols;
+      float acc = 0.0f;
+      for (int p = 0; p < ac; ++p) acc = fadd(acc, fmul(A[i * ac + p], B[int64_t(p) * bc + j]));
+      v = acc;
+    } else if (op == kConcat) {
+      const int64_t r = idx / ocols, j = idx % ocols;
+      v = j < ac ? A[r * ac + j] : B[r * bc + (j - ac)];
+    } else {
+      v = apply_op(op, A[idx], (op == kAdd || op == kMul) ? B[idx] : 0.0f);
+    }
+    O[idx] = v;
+  }
+}
+
 __global__ void fill_kernel(float* arena, int64_t off, int64_t n, float v) {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
     arena[off + i] = v;
@@ -264,6 +298,14 @@ cudaError_t launch_pack_ranges(const float* arena, const int64_t* ranges, int n,
                                cudaStream_t stream) {
   if (n <= 0) return cudaSuccess;
   pack_ranges_kernel<<<std::min(n, 148 * 4), 128, 0, stream>>>(arena, ranges, n, dst);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_primop(float* arena, int op, int64_t a_off, int ar, int ac, int64_t b_off, int br, int bc,
+                          int64_t out_off, int orows, int ocols, cudaStream_t stream) {
+  const int64_t n = int64_t(orows) * ocols;
+  int blocks = int(std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 8)));
+  primop_kernel<<<blocks, 256, 0, stream>>>(arena, op, a_off, ar, ac, b_off, br, bc, out_off, orows, ocols);
   return cudaGetLastError();
 }
 

@@ -306,14 +306,14 @@ Task drnn_gen(Executor& ex, Fiber& fb, const DrnnParams& P, Val h, long fuel) {
   if (d == 0) co_return Val::list({o});
   Val lh = Executor::out(ex.emit(fb, 2, {&o, &P.l_wt, &P.lbias}), 0);
   Val rh = Executor::out(ex.emit(fb, 3, {&o, &P.r_wt, &P.rbias}), 0);
-  std::vector<Call> calls;
-  calls.push_back([&ex, &P, lh, fuel](Fiber& f) { return drnn_gen(ex, f, P, lh, fuel - 1); });
-  calls.push_back([&ex, &P, rh, fuel](Fiber& f) { return drnn_gen(ex, f, P, rh, fuel - 1); });
-  runtime::JoinAwait join = ex.concurrent(fb, std::move(calls));
-  std::vector<Val> res = co_await join;
+  // The two recursive calls are annotated concurrent(0), but in ANF each is preceded by its own
+  // `fuel - 1`, so they are not a run of adjacent calls and the reference executor runs them
+  // inline, one after the other (executor.cpp:522-531).
+  Val lt = co_await drnn_gen(ex, fb, P, lh, fuel - 1);
+  Val rt = co_await drnn_gen(ex, fb, P, rh, fuel - 1);
   std::vector<Val> out{o};
-  for (auto& v : *res[0].items) out.push_back(v);
-  for (auto& v : *res[1].items) out.push_back(v);
+  for (auto& v : *lt.items) out.push_back(v);
+  for (auto& v : *rt.items) out.push_back(v);
   co_return Val::list(std::move(out));
 }
 
