@@ -316,9 +316,93 @@ void split_analysis(const ExecutablePlan& p, DPlan& d) {
     const PlanRef& r = p.outputs[k];
     d.out_split[k] = r.kind == PlanRef::Kind::kTemp && d.steps[r.index].split && aligned(r);
   }
-  if (any_dense_split) d.unit = U;
+  // Column tiling pays when a contraction is split (its weight slice is read once per tile) or
+  // when the plan is purely column-local (no redundant full steps); otherwise run unsplit.
+  bool all_split = true;
+  for (size_t s = 0; s < n; ++s) all_split = all_split && d.steps[s].split;
+  if (any_dense_split || all_split) d.unit = U;
   else
     for (size_t s = 0; s < n; ++s) d.steps[s].split = 0;
+}
+
+// Splits `p` into a prefix of steps whose operands are all shared (computed once per launch) and
+// the rest, which reads the prefix's boundary tensors as extra shared inputs.  Returns false when
+// nothing worth hoisting (no contraction in the shared part) exists.
+bool hoist_shared_prefix(const ExecutablePlan& p, ExecutablePlan& prefix, ExecutablePlan& rest,
+                         std::vector<int64_t>& boundary_sizes) {
+  const size_t n = p.steps.size();
+  std::vector<bool> so(n, false);
+  bool has_dense = false;
+  auto refs_of = [&](const PlanStep& st) {
+    std::vector<PlanRef> r = st.ins;
+    for (auto& l : st.chain)
+      if (l.rhs) r.push_back(*l.rhs);
+    return r;
+  };
+  for (size_t s = 0; s < n; ++s) {
+    bool all = true;
+    for (auto& r : refs_of(p.steps[s]))
+      all = all && (r.kind == PlanRef::Kind::kShared || (r.kind == PlanRef::Kind::kTemp && so[r.index]));
+    so[s] = all;
+    const PlanStep& st = p.steps[s];
+    if (all && (st.kind == PlanStep::Kind::kFusedDense || (st.kind == PlanStep::Kind::kOp && st.op == OpCode::kDense)))
+      has_dense = true;
+  }
+  if (!has_dense) return false;
+  for (auto& o : p.outputs)
+    if (o.kind == PlanRef::Kind::kTemp && so[o.index]) return false;
+  bool any_rest = false;
+  for (size_t s = 0; s < n; ++s) any_rest = any_rest || !so[s];
+  if (!any_rest) return false;
+  // Boundary: shared-only steps read by the rest.
+  std::vector<int> bidx(n, -1), pidx(n, -1), ridx(n, -1);
+  prefix = ExecutablePlan{};
+  prefix.shared_shapes = p.shared_shapes;
+  rest = ExecutablePlan{};
+  rest.shared_shapes = p.shared_shapes;
+  rest.batched_shapes = p.batched_shapes;
+  boundary_sizes.clear();
+  for (size_t s = 0; s < n; ++s) {
+    if (!so[s]) continue;
+    pidx[s] = int(prefix.steps.size());
+    PlanStep st = p.steps[s];
+    for (auto& r : st.ins)
+      if (r.kind == PlanRef::Kind::kTemp) r.index = pidx[r.index];
+    for (auto& l : st.chain)
+      if (l.rhs && l.rhs->kind == PlanRef::Kind::kTemp) l.rhs->index = pidx[l.rhs->index];
+    prefix.steps.push_back(st);
+  }
+  for (size_t s = 0; s < n; ++s) {
+    if (so[s]) continue;
+    for (auto& r : refs_of(p.steps[s]))
+      if (r.kind == PlanRef::Kind::kTemp && so[r.index] && bidx[r.index] < 0) {
+        bidx[r.index] = int(rest.shared_shapes.size());
+        rest.shared_shapes.push_back(p.steps[r.index].out_shape);
+        prefix.outputs.push_back(PlanRef{PlanRef::Kind::kTemp, pidx[r.index], 0, -1});
+        boundary_sizes.push_back(p.steps[r.index].out_shape.size());
+      }
+  }
+  auto remap = [&](PlanRef r) {
+    if (r.kind != PlanRef::Kind::kTemp) return r;
+    if (so[r.index]) {
+      r.kind = PlanRef::Kind::kShared;
+      r.index = bidx[r.index];
+    } else {
+      r.index = ridx[r.index];
+    }
+    return r;
+  };
+  for (size_t s = 0; s < n; ++s) {
+    if (so[s]) continue;
+    ridx[s] = int(rest.steps.size());
+    PlanStep st = p.steps[s];
+    for (auto& r : st.ins) r = remap(r);
+    for (auto& l : st.chain)
+      if (l.rhs) l.rhs = remap(*l.rhs);
+    rest.steps.push_back(st);
+  }
+  for (auto& o : p.outputs) rest.outputs.push_back(remap(o));
+  return true;
 }
 
 }  // namespace
@@ -406,6 +490,20 @@ int register_plan(mbx_ctx* c, const ExecutablePlan& plan) {
   PlanEntry pe;
   pe.plan = plan;
   pe.hplan = compile_plan(plan, pe.temp_floats_per_inst, pe.out_shapes);
+  pe.exec_plan = plan;
+  ExecutablePlan prefix, rest;
+  std::vector<int64_t> bsizes;
+  if (!plan.ghost && hoist_shared_prefix(plan, prefix, rest, bsizes)) {
+    pe.prefix_plan = register_plan(c, prefix);
+    pe.exec_plan = rest;
+    pe.prefix_sizes = bsizes;
+    int64_t tmp = 0;
+    std::vector<Shape> tmp_shapes;
+    pe.hplan = compile_plan(rest, tmp, tmp_shapes);
+    int64_t total = 0;
+    for (int64_t s : bsizes) total += s;
+    if (!c->dry) cuda_check(cudaMalloc(&pe.prefix_scratch, size_t(total) * sizeof(float)), "prefix scratch");
+  }
   if (!plan.ghost) {
     if (!c->dry) {
       cuda_check(cudaMalloc(&pe.dplan, sizeof(DPlan)), "plan alloc");
@@ -477,7 +575,21 @@ BatchLaunch prepare_batch(mbx_ctx* c, int plan_id, int b, const int64_t* shared_
   // 106); here they live on chip, but the offsets are reserved so every later handle offset
   // equals the reference's.
   arena_alloc(c, int64_t(b) * pe.temp_floats_per_inst);
-  L.shared_meta = meta_stage(c, shared_off, size_t(ns) * 8);
+  if (pe.prefix_plan >= 0) {
+    // The hoisted prefix writes its boundary tensors into the plan's scratch; the main kernel
+    // reads them as extra shared inputs (offsets relative to the arena base).
+    std::vector<int64_t> sh(shared_off, shared_off + ns), pouts;
+    int64_t off = c->dry ? 0 : (reinterpret_cast<float*>(pe.prefix_scratch) - arena_ptr(c));
+    for (int64_t s : pe.prefix_sizes) {
+      sh.push_back(off);
+      pouts.push_back(off);
+      off += s;
+    }
+    L.shared_meta = meta_stage(c, sh.data(), sh.size() * 8);
+    L.prefix_out_meta = meta_stage(c, pouts.data(), pouts.size() * 8);
+  } else {
+    L.shared_meta = meta_stage(c, shared_off, size_t(ns) * 8);
+  }
   L.batched_meta = meta_stage(c, eff.data(), eff.size() * 8);
   L.out_meta = meta_stage(c, bases.data(), bases.size() * 8);
   return L;
@@ -489,6 +601,29 @@ void issue_batch(mbx_ctx* c, const BatchLaunch& L) {
   float* arena = arena_ptr(c);
   for (const auto& g : L.gathers) {
     cuda_check(launch_gather_rows(arena, meta_dev<int64_t>(c, g.src_meta), g.dst, L.b, g.size, c->stream), "gather");
+    ++c->launches;
+    ++g_launches;
+  }
+  if (pe.prefix_plan >= 0) {
+    const PlanEntry& pp = c->plans[pe.prefix_plan];
+    VmLaunch v{};
+    v.plan = pp.dplan;
+    v.arena = arena;
+    v.b = 1;
+    v.tm = 1;
+    v.nsplit = pp.max_split;
+    v.unit_chunk = pp.max_split > 1 ? pp.unit_chunk : pp.hplan.unit;
+    if (pp.max_split > 1) {  // spread the one-row contraction over ~148 CTAs
+      const int unit = pp.hplan.unit;
+      v.unit_chunk = std::max(8, ((unit + 147) / 148 + 7) / 8 * 8);
+      v.nsplit = (unit + v.unit_chunk - 1) / v.unit_chunk;
+    }
+    v.threads = pp.threads;
+    v.smem_bytes = int(std::max<int64_t>(1, pp.hplan.temp_floats) * 4);
+    v.shared_off = meta_dev<int64_t>(c, L.shared_meta);
+    v.batched_off = nullptr;
+    v.out_base = meta_dev<int64_t>(c, L.prefix_out_meta);
+    cuda_check(launch_plan_vm(v, c->stream), "shared prefix");
     ++c->launches;
     ++g_launches;
   }

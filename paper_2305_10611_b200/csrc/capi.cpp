@@ -131,6 +131,7 @@ void mbx_ctx_destroy(mbx_ctx* c) {
     cudaStreamSynchronize(c->stream);
     for (auto& pe : c->plans) {
       if (pe.dplan) cudaFree(pe.dplan);
+      if (pe.prefix_scratch) cudaFree(pe.prefix_scratch);
       mbx::tc_release(pe);
     }
     if (c->meta.host) cudaFreeHost(c->meta.host);
@@ -176,6 +177,7 @@ int64_t mbx_arena_used(const mbx_ctx* c) { return c->used; }
 int mbx_arena_upload(mbx_ctx* c, int64_t off, const float* src, int64_t n) {
   return guarded(c, [&] {
     mbx::arena_check(c, off, n);
+    ++c->upload_epoch;
     if (c->dry || n == 0) return;
     mbx::cuda_check(cudaMemcpyAsync(mbx::arena_ptr(c) + off, src, size_t(n) * 4, cudaMemcpyHostToDevice, c->stream), "upload");
     mbx::cuda_check(cudaStreamSynchronize(c->stream), "upload sync");
@@ -217,7 +219,7 @@ int mbx_exec_batched(mbx_ctx* c, int plan_id, int b, const int64_t* shared_off, 
       for (size_t s = 0; s < ns; ++s)
         MBATCH_CHECK(shared_off[size_t(i) * ns + s] == shared_off[s],
                      "shared-param handle mismatch across instances (analysis bug)");
-    size_t bytes = 8 * (pe.plan.shared_shapes.size() + size_t(b) * pe.plan.batched_shapes.size() * 2 + pe.plan.outputs.size()) + 64;
+    size_t bytes = 8 * (pe.plan.shared_shapes.size() + size_t(b) * pe.plan.batched_shapes.size() * 2 + pe.plan.outputs.size()) + 512;
     mbx::meta_reserve(c, bytes);
     mbx::BatchLaunch L = mbx::prepare_batch(c, plan_id, b, shared_off, batched_off, gather_mode, out_off, gather_bytes);
     mbx::meta_commit(c);
@@ -240,6 +242,7 @@ int mbx_exec_primop(mbx_ctx* c, int op, int nin, const int64_t* in_off, const in
     }
     for (int i = 0; i < nin; ++i) mbx::arena_check(c, in_off[i], shapes[i].size());
     mbx::arena_check(c, out_off, out.size());
+    ++c->upload_epoch;
     if (c->dry) return;
     if (o == OpCode::kFill) {
       mbx::cuda_check(mbx::launch_fill(mbx::arena_ptr(c), out_off, out.size(), fill, c->stream), "fill");

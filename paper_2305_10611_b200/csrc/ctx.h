@@ -15,7 +15,14 @@ namespace mbx {
 
 // A registered plan: the host plan, its compiled device form and its launch configuration.
 struct PlanEntry {
-  mbatch::backend::ExecutablePlan plan;
+  mbatch::backend::ExecutablePlan plan;       // as registered (reference semantics, arena parity)
+  mbatch::backend::ExecutablePlan exec_plan;  // what the kernels run (shared prefix hoisted out)
+  // Shared-prefix hoisting: steps whose operands are all shared compute the same value for every
+  // instance (e.g. the TreeLSTM leaf cell's [hz|hz].W); they run once per launch as `prefix_plan`
+  // (b = 1) into `prefix_scratch`, and exec_plan reads them as extra shared inputs.
+  int prefix_plan = -1;
+  std::vector<int64_t> prefix_sizes;  // floats per hoisted boundary tensor
+  float* prefix_scratch = nullptr;
   DPlan hplan{};
   DPlan* dplan = nullptr;            // device copy
   int64_t temp_floats_per_inst = 0;  // sum of step output sizes (reference arena parity)
@@ -57,6 +64,9 @@ struct mbx_ctx {
   std::map<std::vector<int32_t>, int> plan_by_enc;
   std::string err;
   int64_t launches = 0;
+  // Bumped by every host write into existing tensors (uploads, primops); tensor-core weight
+  // packs made under an older epoch are re-packed.
+  uint64_t upload_epoch = 0;
   cudaEvent_t ev_a = nullptr, ev_b = nullptr;
 };
 
@@ -91,6 +101,7 @@ struct BatchLaunch {
   int plan_id = -1;
   int b = 0;
   size_t shared_meta = 0, batched_meta = 0, out_meta = 0;
+  size_t prefix_out_meta = 0;  // hoisted shared prefix: its output offsets (scratch)
   // EXPLICIT gathers to run first: (slot size, src offsets meta, dst offset)
   struct Gather { int size; size_t src_meta; int64_t dst; };
   std::vector<Gather> gathers;

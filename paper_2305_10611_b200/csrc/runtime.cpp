@@ -459,7 +459,7 @@ struct Executor::Impl {
       if (b.ghost) continue;
       const auto& plan = m.kernels.plan(b.sig);
       const size_t nb = plan.batched_shapes.size();
-      meta_bytes += 8 * (plan.shared_shapes.size() + size_t(b.size) * nb * 2 + plan.outputs.size()) + 64;
+      meta_bytes += 8 * (plan.shared_shapes.size() + size_t(b.size) * nb * 2 + plan.outputs.size()) + 512;
     }
     mbx::meta_reserve(c, meta_bytes);
 
