@@ -372,21 +372,29 @@ bool hoist_shared_prefix(const ExecutablePlan& p, ExecutablePlan& prefix, Execut
       if (l.rhs && l.rhs->kind == PlanRef::Kind::kTemp) l.rhs->index = pidx[l.rhs->index];
     prefix.steps.push_back(st);
   }
+  // One boundary tensor per distinct (step, column slice) the rest reads, so a hoisted fused
+  // dense exposes one (1, N_g) output per gate and the prefix launch can split its columns.
+  std::map<std::tuple<int, int, int>, int> boundary;  // (step, col_off, cols) -> shared index
+  (void)bidx;
   for (size_t s = 0; s < n; ++s) {
     if (so[s]) continue;
     for (auto& r : refs_of(p.steps[s]))
-      if (r.kind == PlanRef::Kind::kTemp && so[r.index] && bidx[r.index] < 0) {
-        bidx[r.index] = int(rest.shared_shapes.size());
-        rest.shared_shapes.push_back(p.steps[r.index].out_shape);
-        prefix.outputs.push_back(PlanRef{PlanRef::Kind::kTemp, pidx[r.index], 0, -1});
-        boundary_sizes.push_back(p.steps[r.index].out_shape.size());
+      if (r.kind == PlanRef::Kind::kTemp && so[r.index]) {
+        auto key = std::make_tuple(r.index, r.cols >= 0 ? r.col_off : 0, r.cols);
+        if (boundary.count(key)) continue;
+        boundary[key] = int(rest.shared_shapes.size());
+        Shape sh = p.steps[r.index].out_shape;
+        if (r.cols >= 0) sh = Shape{1, r.cols};
+        rest.shared_shapes.push_back(sh);
+        prefix.outputs.push_back(PlanRef{PlanRef::Kind::kTemp, pidx[r.index], r.col_off, r.cols});
+        boundary_sizes.push_back(sh.size());
       }
   }
   auto remap = [&](PlanRef r) {
     if (r.kind != PlanRef::Kind::kTemp) return r;
     if (so[r.index]) {
-      r.kind = PlanRef::Kind::kShared;
-      r.index = bidx[r.index];
+      const int idx = boundary.at(std::make_tuple(r.index, r.cols >= 0 ? r.col_off : 0, r.cols));
+      r = PlanRef{PlanRef::Kind::kShared, idx, 0, -1};
     } else {
       r.index = ridx[r.index];
     }
@@ -627,7 +635,9 @@ void issue_batch(mbx_ctx* c, const BatchLaunch& L) {
     ++c->launches;
     ++g_launches;
   }
-  if (c->precision != MBX_PREC_FP32 && pe.tc_kind >= 0) {
+  // tc_kind 2 (pointwise) is exact and runs in every precision; tc_kind 1 (tensor cores) only
+  // when the context allows split-bf16 / bf16 contractions.
+  if (pe.tc_kind == 2 || (c->precision != MBX_PREC_FP32 && pe.tc_kind == 1)) {
     cuda_check(tc_launch(c, pe, L), "tensor-core plan kernel");
     ++c->launches;
     ++g_launches;
@@ -637,8 +647,9 @@ void issue_batch(mbx_ctx* c, const BatchLaunch& L) {
   v.plan = pe.dplan;
   v.arena = arena;
   v.b = L.b;
-  v.tm = pe.tm;
-  const int ntiles = (L.b + pe.tm - 1) / pe.tm;
+  // Node tile: as many nodes per CTA as fill ~one wave (weight-tile reuse), no more.
+  v.tm = std::clamp((L.b + 147) / 148, 1, pe.tm);
+  const int ntiles = (L.b + v.tm - 1) / v.tm;
   // Column tiles: enough CTAs for ~2 waves over 148 SMs, and together they must cover the unit.
   v.nsplit = pe.max_split > 1 ? std::clamp((296 + ntiles - 1) / ntiles, 1, pe.max_split) : 1;
   if (v.nsplit > 1) {

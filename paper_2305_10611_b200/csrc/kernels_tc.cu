@@ -45,12 +45,15 @@ constexpr int kStages = 3;
 constexpr int kMaxEpi = 24;
 
 // Micro-op program of a plan's column-local tail (see compile_epilogue).
-enum : int8_t { kSrcNone = 0, kSrcSlot = 1, kSrcAcc = 2, kSrcBatched = 3, kSrcShared = 4 };
+// Micro-op operands: a slot (earlier tail step), a gate of the accumulator tile, or one of the
+// prefetched input rows (loads[idx], a batched or shared input + column slice).
+enum : int8_t { kSrcNone = 0, kSrcSlot = 1, kSrcAcc = 2, kSrcBatched = 3, kSrcShared = 4, kSrcLoad = 5 };
 constexpr int kOpCopy = 99;
+constexpr int kMaxLoads = 12;
 struct EpiSrc {
   int8_t type;
   int8_t pad;
-  int16_t idx;  // slot / accumulator gate g / batched or shared input index
+  int16_t idx;  // slot / accumulator gate g / batched or shared input index / load index
   int32_t off;  // column-slice offset into the input row
 };
 struct EpiOp {
@@ -58,9 +61,10 @@ struct EpiOp {
   EpiSrc a, b;
 };
 struct EpiProg {
-  int32_t nops, nslots, nout, pad;
+  int32_t nops, nslots, nout, nloads;
   int32_t out_slot[kMaxOut];
-  EpiOp ops[60];
+  EpiSrc loads[kMaxLoads];
+  EpiOp ops[56];
 };
 
 struct TcArgs {
@@ -81,15 +85,18 @@ struct TcArgs {
   int ring_bytes;     // stages * (W chunk + X chunk); epilogue program, slots and D tile reuse it
   int stages;
   int bulk_x;         // 1: node rows land by bulk copy (every row offset 16-byte aligned)
+  int ksplit;         // K-split ranks per tile (= cluster size along grid z)
+  int epi_nslots, epi_nloads;
   int debug;          // MBX_TC_DEBUG bits (profiling only): 1 skip MMAs, 2 skip W copies
   unsigned long long* ts;  // MBX_TC_DEBUG & 16: %globaltimer phase stamps of CTA (0,0)
 };
 
 __device__ __forceinline__ void stamp(const TcArgs& P, int i) {
-  if (P.ts && blockIdx.x == 0 && blockIdx.y == 0) {
+  if (P.ts && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     P.ts[i] = t;
+    if (i == 0 || i == 4) P.ts[62 + (i == 4)] = clock64();
   }
 }
 
@@ -189,6 +196,9 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
+// One CTA = (node tile of NT nodes) x (unit tile of UC units = M gate rows) x (K-split rank).
+// The S K-split ranks of a tile form a thread-block cluster; their partial accumulators are
+// reduced through distributed shared memory and each rank finishes NT/S of the nodes.
 __global__ void __launch_bounds__(kTcThreads, 1) tc_gate_kernel(TcArgs P) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -198,14 +208,17 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gate_kernel(TcArgs P) {
   const int KC = P.KC;
   const int npass = P.npass;
   const int S = P.stages;
+  const int ksplit = P.ksplit;
+  uint32_t rank = 0;
+  if (ksplit > 1) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+  const int cpr = P.nchunks / ksplit;  // chunks per rank
+  const int c_begin = int(rank) * cpr;
   if (tid == 0) stamp(P, 0);
 
-  // Ring of S stages, each {W chunk [pass][M x KC], X chunk [pass][NT x KC]} in the canonical
-  // K-major no-swizzle layout; after the mainloop the ring is reused by the epilogue.
   const int wstage = P.w_chunk_bytes * (npass > 1 ? 2 : 1);
-  const int xchunk = P.NT * KC * 2;               // one pass of one X chunk (bf16)
+  const int xchunk = P.NT * KC * 2;
   const int xstage = xchunk * (npass > 1 ? 2 : 1);
-  const int rawbytes = P.bulk_x ? P.NT * KC * 4 : 0;  // fp32 rows landed by the bulk engine
+  const int rawbytes = P.bulk_x ? P.NT * KC * 4 : 0;
   const int stage_bytes = wstage + rawbytes + xstage;
   uint8_t* ring = smem;
   uint64_t* full_w = reinterpret_cast<uint64_t*>(smem + P.ring_bytes);
@@ -214,7 +227,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gate_kernel(TcArgs P) {
   uint64_t* done = empty + S;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
   int64_t* rowbase = reinterpret_cast<int64_t*>(done + 2);  // [NT][2] arena offset of each piece row
-  float* dsm = reinterpret_cast<float*>(smem + P.ring_bytes - P.NT * P.M * 4);  // epilogue: end of the ring
+  float* dsm = reinterpret_cast<float*>(smem + P.ring_bytes - P.NT * P.M * 4);  // [NT][M] partial D
 
   for (int i = tid; i < P.NT * 2; i += kTcThreads) {
     const int n = i >> 1, pc = i & 1;
@@ -249,24 +262,18 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gate_kernel(TcArgs P) {
   if (tid == 0) stamp(P, 1);
 
   if (warp == 0) {
-    // ---- Producer warp: per chunk, one bulk copy of the pre-packed weight chunk and (bulk_x)
-    // one bulk copy per node row segment, all on the bulk-copy (TMA) engine, S stages ahead.
+    // ---- Producer warp: the weight chunk (one bulk copy) and, with bulk_x, one bulk copy per
+    // node row segment, all on the bulk-copy (TMA) engine, up to S stages ahead of the MMAs.
     const uint8_t* wtile = P.wpack + size_t(tile_u) * P.nchunks * wstage;
-    for (int c = 0; c < P.nchunks; ++c) {
-      const int s = c % S;
+    for (int i = 0; i < cpr; ++i) {
+      const int c = c_begin + i, s = i % S;
       if (lane == 0) {
-        if (c >= S) mbar_wait(&empty[s], ((c / S) - 1) & 1);
+        if (i >= S) mbar_wait(&empty[s], ((i / S) - 1) & 1);
         const int wb = (P.debug & 2) ? 0 : wstage;
         mbar_expect_tx(&full_w[s], wb + ((P.bulk_x && !(P.debug & 64)) ? nn * KC * 4 : 0));
+        if (wb) bulk_g2s(ring + s * stage_bytes, wtile + size_t(c) * wstage, wstage, &full_w[s]);
       }
       __syncwarp();
-      if (!(P.debug & 2)) {
-        // The weight chunk in 4 KB pieces, one per lane, so the bulk engine works on many requests
-        // at once instead of one long one.
-        const int pieces = wstage >> 12;
-        for (int q = lane; q < pieces; q += 32)
-          bulk_g2s(ring + s * stage_bytes + (q << 12), wtile + size_t(c) * wstage + (size_t(q) << 12), 4096, &full_w[s]);
-      }
       if (P.bulk_x && !(P.debug & 64)) {
         uint8_t* raw = ring + s * stage_bytes + wstage;
         const int k0 = c * KC, k1 = k0 + KC;
@@ -286,41 +293,39 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gate_kernel(TcArgs P) {
     if (lane == 0) {
       const uint32_t ra = smem_u32(ring);
       const uint32_t sbo = uint32_t(KC * 16);
-      for (int c = 0; c < P.nchunks; ++c) {
-        const int s = c % S;
-        mbar_wait(&full_w[s], (c / S) & 1);
-        if (c < 16) stamp(P, 24 + c);
-        mbar_wait(&full_x[s], (c / S) & 1);
-        if (c < 16) stamp(P, 40 + c);
+      for (int i = 0; i < cpr; ++i) {
+        const int s = i % S;
+        mbar_wait(&full_w[s], (i / S) & 1);
+        mbar_wait(&full_x[s], (i / S) & 1);
         tc_fence_after();
         const uint32_t wa = ra + s * stage_bytes;
         const uint32_t xa = wa + wstage + rawbytes;
-        for (int ks = 0; ks < ((P.debug & 1) ? 0 : KC / 16); ++ks) {
-          const uint64_t a_hi = make_desc(wa + ks * 256, sbo);
-          const uint64_t b_hi = make_desc(xa + ks * 256, sbo);
-          mma_bf16(tmem, a_hi, b_hi, P.idesc, (c | ks) ? 1u : 0u);
+        const uint64_t a_hi = make_desc(wa, sbo), b_hi = make_desc(xa, sbo);
+        const uint64_t a_lo = make_desc(wa + P.w_chunk_bytes, sbo), b_lo = make_desc(xa + xchunk, sbo);
+        const int nks = (P.debug & 1) ? 0 : KC / 16;
+        for (int ks = 0; ks < nks; ++ks) {
+          const uint64_t step = uint64_t(ks * 16);  // +256 B in the 16-byte-unit address field
+          mma_bf16(tmem, a_hi + step, b_hi + step, P.idesc, (i | ks) ? 1u : 0u);
           if (npass > 1) {
-            const uint64_t a_lo = make_desc(wa + P.w_chunk_bytes + ks * 256, sbo);
-            const uint64_t b_lo = make_desc(xa + xchunk + ks * 256, sbo);
-            mma_bf16(tmem, a_hi, b_lo, P.idesc, 1u);
-            mma_bf16(tmem, a_lo, b_hi, P.idesc, 1u);
+            mma_bf16(tmem, a_hi + step, b_lo + step, P.idesc, 1u);
+            mma_bf16(tmem, a_lo + step, b_hi + step, P.idesc, 1u);
           }
         }
         mma_commit(&empty[s]);  // frees the stage once these MMAs have read it
-        if (c < 16) stamp(P, 8 + c);
       }
       mma_commit(done);
     }
   } else {
-    // ---- X producers: gather the tile's node rows chunk by chunk from the arena through the
-    // per-node offset table, split into bf16 hi / lo.  One unit = 8 consecutive K of one node.
+    // ---- X producers: the tile's node rows chunk by chunk (from the bulk-landed fp32 rows, or
+    // gathered with loads through the per-node offset table), split into bf16 hi / lo in the
+    // canonical layout.  One unit = 8 consecutive K of one node.
     const int gt = tid - 64;
     const int kb = KC >> 3;
     const int units = P.NT * kb;
-    for (int c = 0; c < P.nchunks; ++c) {
-      const int s = c % S;
-      if (P.bulk_x) mbar_wait(&full_w[s], (c / S) & 1);  // raw fp32 rows have landed
-      else if (c >= S) mbar_wait(&empty[s], ((c / S) - 1) & 1);
+    for (int i = 0; i < cpr; ++i) {
+      const int c = c_begin + i, s = i % S;
+      if (P.bulk_x) mbar_wait(&full_w[s], (i / S) & 1);
+      else if (i >= S) mbar_wait(&empty[s], ((i / S) - 1) & 1);
       const float* raw = reinterpret_cast<const float*>(ring + s * stage_bytes + wstage);
       uint8_t* xs = ring + s * stage_bytes + wstage + rawbytes;
       for (int idx = gt; idx < units; idx += kGatherWarps * 32) {
@@ -342,16 +347,16 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gate_kernel(TcArgs P) {
             v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = bq.x; v[5] = bq.y; v[6] = bq.z; v[7] = bq.w;
           } else {
 #pragma unroll
-            for (int i = 0; i < 8; ++i) v[i] = __ldg(src + i);
+            for (int q = 0; q < 8; ++q) v[q] = __ldg(src + q);
           }
         } else {
 #pragma unroll
-          for (int i = 0; i < 8; ++i) v[i] = 0.0f;
+          for (int q = 0; q < 8; ++q) v[q] = 0.0f;
         }
         const uint32_t off = canon_off(n, kk, KC);
         float h[8];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) h[i] = __bfloat162float(__float2bfloat16_rn(v[i]));
+        for (int q = 0; q < 8; ++q) h[q] = __bfloat162float(__float2bfloat16_rn(v[q]));
         uint4 hi;
         hi.x = pack_bf16(h[0], h[1]); hi.y = pack_bf16(h[2], h[3]); hi.z = pack_bf16(h[4], h[5]); hi.w = pack_bf16(h[6], h[7]);
         *reinterpret_cast<uint4*>(xs + off) = hi;
@@ -382,36 +387,84 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gate_kernel(TcArgs P) {
       float v[8];
       tmem_ld8(tmem + (uint32_t(q * 32) << 16) + uint32_t(c0), v);
 #pragma unroll
-      for (int i = 0; i < 8; ++i) dsm[(c0 + i) * P.M + row] = v[i];
+      for (int k = 0; k < 8; ++k) dsm[(c0 + k) * P.M + row] = v[k];
     }
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 0)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(P.tmem_cols) : "memory");
-  (void)nn;
   if (tid == 0) stamp(P, 3);
 
-  // Elementwise tail: the plan's column-local steps compiled (host side, compile_epilogue) into
-  // a micro-op program, interpreted per (node, unit) element; slot values live in shared memory
-  // (the X region is free now), one column of slots per thread.
+  // Epilogue scratch (the ring is free now): program | slots | prefetched operands | D rows.
+  const int ntr = P.NT / ksplit;        // nodes this rank finishes
+  const int nloc0 = int(rank) * ntr;    // first of them, within the tile
+  const int nloc = max(0, min(ntr, nn - nloc0));
+  const int E = ntr * P.UC;
   EpiProg* prog = reinterpret_cast<EpiProg*>(smem);
   float* slots = reinterpret_cast<float*>(smem + sizeof(EpiProg));
+  float* srcbuf = slots + P.epi_nslots * kTcThreads;
+  float* red = srcbuf + P.epi_nloads * E;
   for (int i = tid; i < int(sizeof(EpiProg) / 4); i += kTcThreads)
     reinterpret_cast<int*>(prog)[i] = reinterpret_cast<const int*>(P.epi)[i];
+
+  // Split-K: every rank's partial D is complete in its smem; rank r sums node columns
+  // [r*ntr, (r+1)*ntr) over the cluster in rank order (deterministic) via DSMEM.
+  if (ksplit > 1) {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    if (tid == 0) stamp(P, 5);
+    const uint32_t dsm_local = smem_u32(dsm);
+    for (int i = tid; i < ntr * P.M; i += kTcThreads) {
+      const int n = nloc0 + i / P.M, row = i % P.M;
+      const uint32_t off = uint32_t((n * P.M + row) * 4);
+      float acc = 0.0f;
+      for (int q = 0; q < ksplit; ++q) {
+        uint32_t ra;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(dsm_local + off), "r"(q));
+        float v;
+        asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(ra) : "memory");
+        acc += v;
+      }
+      red[i] = acc;
+    }
+    // Peers may still be reading this CTA's partial: keep it alive until everyone is done.
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  } else {
+    __syncthreads();
+    red = dsm;
+  }
   __syncthreads();
-  const int total = nn * P.UC;
+  if (tid == 0) stamp(P, 6);
+
+  // Prefetch every batched / shared operand the tail reads, all elements at once (one round of
+  // independent loads instead of a dependent chain per element).
   const int nops = prog->nops;
-  for (int idx = tid; idx < total; idx += kTcThreads) {
-    const int n = idx / P.UC, u = idx - n * P.UC;
+  for (int i = tid; i < prog->nloads * E; i += kTcThreads) {
+    const int j = i / E, e = i - j * E;
+    const int n = e / P.UC, u = e - n * P.UC;
+    float v = 0.0f;
+    if (n < nloc) {
+      const EpiSrc& s = prog->loads[j];
+      const int ug = tile_u * P.UC + u;
+      const int64_t node = node0 + nloc0 + n;
+      v = s.type == kSrcBatched ? P.arena[P.batched_off[node * P.nb + s.idx] + s.off + ug]
+                                : P.arena[P.shared_off[s.idx] + s.off + ug];
+    }
+    srcbuf[i] = v;
+  }
+  __syncthreads();
+  if (tid == 0) stamp(P, 7);
+
+  // Elementwise tail as a micro-op program per (node, unit) element.
+  for (int e = tid; e < nloc * P.UC; e += kTcThreads) {
+    const int n = e / P.UC, u = e - n * P.UC;
     const int ug = tile_u * P.UC + u;
-    const int64_t node = node0 + n;
+    const int64_t node = node0 + nloc0 + n;
     auto fetch = [&](const EpiSrc& s) -> float {
       switch (s.type) {
         case kSrcSlot: return slots[s.idx * kTcThreads + tid];
-        case kSrcAcc: return dsm[n * P.M + s.idx * P.UC + u];
-        case kSrcBatched: return P.arena[P.batched_off[node * P.nb + s.idx] + s.off + ug];
-        case kSrcShared: return P.arena[P.shared_off[s.idx] + s.off + ug];
+        case kSrcAcc: return red[n * P.M + s.idx * P.UC + u];
+        case kSrcLoad: return srcbuf[s.idx * E + e];
         default: return 0.0f;
       }
     };
@@ -436,6 +489,45 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gate_kernel(TcArgs P) {
   if (P.ts) {
     __syncthreads();
     if (tid == 0) stamp(P, 4);
+  }
+}
+
+struct PwArgs {
+  const EpiProg* epi;
+  float* arena;
+  const int64_t* shared_off;
+  const int64_t* batched_off;
+  const int64_t* out_base;
+  int b, E, nb, nslots;
+};
+
+// One thread per (node, element) of a pointwise plan; slots in shared memory, one column per
+// thread; glibc-exact activations (bit-identical to the reference).
+__global__ void __launch_bounds__(256) pointwise_kernel(PwArgs P) {
+  extern __shared__ float pw_slots[];
+  __shared__ EpiProg prog;
+  for (int i = threadIdx.x; i < int(sizeof(EpiProg) / 4); i += blockDim.x)
+    reinterpret_cast<int*>(&prog)[i] = reinterpret_cast<const int*>(P.epi)[i];
+  __syncthreads();
+  const int tid = threadIdx.x;
+  const int64_t total = int64_t(P.b) * P.E;
+  for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + tid; idx < total; idx += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t node = idx / P.E;
+    const int e = int(idx - node * P.E);
+    auto fetch = [&](const EpiSrc& s) -> float {
+      if (s.type == kSrcSlot) return pw_slots[s.idx * 256 + tid];
+      if (s.type != kSrcLoad) return 0.0f;
+      const EpiSrc& l = prog.loads[s.idx];
+      const int64_t base = l.type == kSrcBatched ? P.batched_off[node * P.nb + l.idx] : P.shared_off[l.idx];
+      return P.arena[base + l.off + e];
+    };
+    for (int i = 0; i < prog.nops; ++i) {
+      const EpiOp& o = prog.ops[i];
+      const float a = fetch(o.a);
+      const float bv = fetch(o.b);
+      pw_slots[o.dst * 256 + tid] = o.op == kOpCopy ? a : apply_op(o.op, a, bv);
+    }
+    for (int k = 0; k < prog.nout; ++k) P.arena[P.out_base[k] + node * P.E + e] = pw_slots[prog.out_slot[k] * 256 + tid];
   }
 }
 
@@ -513,9 +605,22 @@ bool compile_epilogue(const mbatch::backend::ExecutablePlan& p, TcState& st) {
         s.idx = int16_t(r.index - dstep - 1);
       }
     } else {
-      s.type = r.kind == PlanRef::Kind::kBatched ? kSrcBatched : kSrcShared;
-      s.idx = int16_t(r.index);
-      s.off = slice;
+      // Input rows are prefetched once per element: dedupe them into the load table.
+      EpiSrc l{};
+      l.type = r.kind == PlanRef::Kind::kBatched ? kSrcBatched : kSrcShared;
+      l.idx = int16_t(r.index);
+      l.off = slice;
+      int j = 0;
+      while (j < pr.nloads && !(pr.loads[j].type == l.type && pr.loads[j].idx == l.idx && pr.loads[j].off == l.off)) ++j;
+      if (j == pr.nloads) {
+        if (pr.nloads >= kMaxLoads) {
+          s.type = kSrcNone;  // too many distinct inputs: rejected below
+          return s;
+        }
+        pr.loads[pr.nloads++] = l;
+      }
+      s.type = kSrcLoad;
+      s.idx = int16_t(j);
     }
     return s;
   };
@@ -555,7 +660,9 @@ bool compile_epilogue(const mbatch::backend::ExecutablePlan& p, TcState& st) {
       pr.out_slot[k] = o.index - dstep - 1;
     }
   }
-  return pr.nslots <= 32;
+  for (int i = 0; i < pr.nops; ++i)
+    if (pr.ops[i].a.type == kSrcNone && pr.ops[i].op != kOpCopy) return false;
+  return pr.nslots <= 32 && pr.nloads < kMaxLoads;
 }
 
 bool analyse(const mbatch::backend::ExecutablePlan& p, const DPlan& d, TcState& st) {
@@ -648,27 +755,103 @@ bool analyse(const mbatch::backend::ExecutablePlan& p, const DPlan& d, TcState& 
   return compile_epilogue(p, st);
 }
 
-// Nodes per CTA (the MMA N): every CTA streams its unit tile's whole weight slice, so more node
-// tiles multiply L2 weight traffic while fewer lengthen each CTA's MMA chain.  Start from the
-// smallest tile that keeps the grid within one wave of 148 SMs.  MBX_TC_NT overrides (tuning).
-int pick_nt(int b, int utiles) {
-  static const int forced = [] {
+// Tiling of one launch: NT nodes per CTA (the MMA N) and S K-split ranks per tile.  Each CTA
+// ingests W_tile/S of weights (+ its node rows) through a per-SM pipe measured at ~110 GB/s
+// (tools/bench_bulk.cu), node tiles multiply the L2 weight traffic, and S > 1 adds a DSMEM
+// reduction.  A small cost model picks the cheapest tiling that fits one wave of 148 SMs.
+// MBX_TC_NT / MBX_TC_KSPLIT force a choice (tuning).
+struct Tiling {
+  int NT = 16, S = 1;
+};
+
+Tiling pick_tiling(int b, int utiles, int nchunks, int K, int KC, int npass) {
+  static const int forced_nt = [] {
     const char* e = std::getenv("MBX_TC_NT");
     return e ? std::atoi(e) : 0;
   }();
-  if (forced == 16 || forced == 32 || forced == 64 || forced == 128) return forced;
-  int nt = 16;
-  while (nt < 128 && ((b + nt - 1) / nt) * utiles > 148) nt <<= 1;
-  while (nt > 16 && nt / 2 >= b) nt >>= 1;
-  return nt;
+  static const int forced_s = [] {
+    const char* e = std::getenv("MBX_TC_KSPLIT");
+    return e ? std::atoi(e) : 0;
+  }();
+  const double wpass = npass > 1 ? 2 : 1;
+  const double w_tile_bytes = 128.0 * K * 2 * wpass;  // one unit tile's weights
+  Tiling best;
+  double best_t = 1e30;
+  for (int nt : {16, 32, 64, 128}) {
+    if (forced_nt && nt != forced_nt) continue;
+    if (nt > 16 && nt / 2 >= b) continue;  // do not over-pad small batches
+    for (int s : {1, 2, 4, 8}) {
+      if (forced_s && s != forced_s) continue;
+      if (nchunks % s != 0 || nt % s != 0) continue;
+      const int tiles = (b + nt - 1) / nt;
+      const int ctas = tiles * utiles * s;
+      if (ctas > 148 && !(forced_nt || forced_s)) continue;
+      const double ingest_us = (w_tile_bytes / s + double(nt) * K / s * 4) / 110e3;
+      const double mma_us = double(nchunks / s) * (KC / 16) * npass * std::max(16, nt / 2) / 1.9e3;
+      const double l2_us = tiles * w_tile_bytes * utiles / 16e6;
+      const double red_us = s > 1 ? (s - 1) * double(nt / s) * 128 * 4 / 20.0 / 1.9e3 : 0.0;
+      const double epi_us = double(nt / s) * 32 / 256 * 0.05;
+      const double t = 2.0 + std::max(std::max(ingest_us, mma_us), l2_us) + red_us + epi_us;
+      if (t < best_t) {
+        best_t = t;
+        best.NT = nt;
+        best.S = s;
+      }
+    }
+  }
+  return best;
 }
 
 }  // namespace
 
+// Pointwise plans: every step elementwise over one common shape (the hoisted TreeLSTM leaf cell,
+// MV-RNN's matrix add, ...).  They run one thread per (node, element) through the micro-op
+// program with the glibc-exact activations, so they stay bit-identical to the reference.
+bool analyse_pointwise(const mbatch::backend::ExecutablePlan& p, TcState& st) {
+  using mbatch::backend::OpCode;
+  using mbatch::backend::PlanRef;
+  using mbatch::backend::PlanStep;
+  using mbatch::backend::Shape;
+  if (p.ghost || p.steps.empty() || p.outputs.empty()) return false;
+  const Shape sh = p.steps[0].out_shape;
+  for (const auto& ps : p.steps) {
+    if (ps.out_shape != sh) return false;
+    if (ps.kind == PlanStep::Kind::kFusedDense) return false;
+    if (ps.kind == PlanStep::Kind::kOp && !mbatch::backend::is_elementwise(ps.op)) return false;
+    std::vector<PlanRef> refs = ps.ins;
+    for (auto& l : ps.chain)
+      if (l.rhs) refs.push_back(*l.rhs);
+    for (auto& r : refs) {
+      if (r.kind == PlanRef::Kind::kTemp) {
+        if (r.cols >= 0) return false;
+        continue;
+      }
+      const Shape in = r.kind == PlanRef::Kind::kShared ? p.shared_shapes[r.index] : p.batched_shapes[r.index];
+      if (r.cols >= 0 ? !(sh.rows == 1 && r.cols == sh.cols) : !(in == sh)) return false;
+    }
+  }
+  for (auto& o : p.outputs)
+    if (o.kind != PlanRef::Kind::kTemp || o.cols >= 0) return false;
+  st.dstep = -1;
+  st.U = sh.size();
+  st.K = 0;
+  return compile_epilogue(p, st);
+}
+
 void tc_prepare(mbx_ctx* c, PlanEntry& pe) {
   pe.tc_kind = -1;
   auto st = std::make_unique<TcState>();
-  if (!analyse(pe.exec_plan, pe.hplan, *st)) return;
+  if (!analyse(pe.exec_plan, pe.hplan, *st)) {
+    *st = TcState{};
+    if (!analyse_pointwise(pe.exec_plan, *st)) return;
+    pe.tc_kind = 2;
+    if (!c->dry) {
+      cuda_check(cudaMalloc(&st->dprog, sizeof(EpiProg)), "pointwise program");
+      cuda_check(cudaMemcpy(st->dprog, &st->prog, sizeof(EpiProg), cudaMemcpyHostToDevice), "pointwise program");
+    }
+    pe.tc_state = st.release();
+    return;
+  }
   if (!c->dry) {
     cuda_check(cudaMalloc(&st->dprog, sizeof(EpiProg)), "epilogue program");
     cuda_check(cudaMemcpy(st->dprog, &st->prog, sizeof(EpiProg), cudaMemcpyHostToDevice), "epilogue program");
@@ -688,6 +871,28 @@ void tc_release(PlanEntry& pe) {
 
 cudaError_t tc_launch(mbx_ctx* c, const PlanEntry& pe, const BatchLaunch& L) {
   auto* st = static_cast<TcState*>(pe.tc_state);
+  if (pe.tc_kind == 2) {
+    PwArgs a{};
+    a.epi = st->dprog;
+    a.arena = arena_ptr(c);
+    a.shared_off = meta_dev<int64_t>(c, L.shared_meta);
+    a.batched_off = meta_dev<int64_t>(c, L.batched_meta);
+    a.out_base = meta_dev<int64_t>(c, L.out_meta);
+    a.b = L.b;
+    a.E = st->U;
+    a.nb = int(pe.exec_plan.batched_shapes.size());
+    a.nslots = st->prog.nslots;
+    const int64_t total = int64_t(L.b) * a.E;
+    const int blocks = int(std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, 148 * 8)));
+    const int smem = a.nslots * 256 * 4;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(pointwise_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      attr = true;
+    }
+    pointwise_kernel<<<blocks, 256, smem, c->stream>>>(a);
+    return cudaGetLastError();
+  }
   const int npass = c->precision == MBX_PREC_BF16 ? 1 : 3;
   const int wpass = npass > 1 ? 2 : 1;
   // Resolve the shared offsets of the weights (host copy of the staged shared table).
@@ -743,7 +948,11 @@ cudaError_t tc_launch(mbx_ctx* c, const PlanEntry& pe, const BatchLaunch& L) {
   a.G = st->G;
   a.UC = st->UC;
   a.M = st->M;
-  a.NT = pick_nt(L.b, ntiles);
+  const Tiling tl = pick_tiling(L.b, ntiles, st->nchunks, st->K, st->KC, npass);
+  a.NT = tl.NT;
+  a.ksplit = tl.S;
+  a.epi_nslots = st->prog.nslots;
+  a.epi_nloads = st->prog.nloads;
   a.npass = npass;
   a.dstep = st->dstep;
   a.nb = int(pe.plan.batched_shapes.size());
@@ -791,8 +1000,15 @@ cudaError_t tc_launch(mbx_ctx* c, const PlanEntry& pe, const BatchLaunch& L) {
       // Print the previous launch's phase stamps (this call is serialized behind it anyway).
       cudaStreamSynchronize(c->stream);
       cudaMemcpy(ts, dts, 64 * 8, cudaMemcpyDeviceToHost);
-      std::fprintf(stderr, "tc phases us: alloc %.2f mainloop %.2f tmem %.2f epilogue %.2f\n", (ts[1] - ts[0]) / 1e3,
-                   (ts[2] - ts[1]) / 1e3, (ts[3] - ts[2]) / 1e3, (ts[4] - ts[3]) / 1e3);
+      std::fprintf(stderr,
+                   "tc phases us: alloc %.2f mainloop %.2f tmem %.2f epilogue %.2f [cluster-wait %.2f reduce %.2f "
+                   "prefetch %.2f tail %.2f] sm %.0f MHz\n",
+                   (ts[1] - ts[0]) / 1e3, (ts[2] - ts[1]) / 1e3, (ts[3] - ts[2]) / 1e3, (ts[4] - ts[3]) / 1e3,
+                   ts[5] ? (double(ts[5]) - ts[3]) / 1e3 : 0.0, ts[5] ? (double(ts[6]) - ts[5]) / 1e3 : 0.0,
+                   (double(ts[7]) - ts[6]) / 1e3, (double(ts[4]) - ts[7]) / 1e3,
+                   ts[4] > ts[0] ? double(ts[63] - ts[62]) / double(ts[4] - ts[0]) * 1e3 : 0.0);
+      ts[5] = 0;
+      cudaMemcpy(dts, ts, 64 * 8, cudaMemcpyHostToDevice);
       std::fprintf(stderr, "  chunk: W+raw landed / X converted / MMAs issued (us from start)\n");
       for (int k = 0; k < 16; ++k)
         std::fprintf(stderr, "  %2d %8.2f %8.2f %8.2f\n", k, (double(ts[24 + k]) - ts[0]) / 1e3,
@@ -801,21 +1017,35 @@ cudaError_t tc_launch(mbx_ctx* c, const PlanEntry& pe, const BatchLaunch& L) {
   }
   const int xstage = a.NT * a.KC * 2 * wpass + (a.bulk_x ? a.NT * a.KC * 4 : 0);
   const int stage_bytes = wstage + xstage;
-  const int epi_bytes = int(sizeof(EpiProg)) + st->prog.nslots * kTcThreads * 4 + dsm_bytes;
-  const int budget = 220 * 1024;
+  const int ntr = a.NT / a.ksplit;
+  const int epi_bytes = int(sizeof(EpiProg)) + st->prog.nslots * kTcThreads * 4 +
+                        st->prog.nloads * ntr * st->UC * 4 + ntr * a.M * 4 + dsm_bytes;
+  const int budget = 218 * 1024;
+  const int cpr = st->nchunks / a.ksplit;
   a.stages = std::min(6, std::max(2, budget / stage_bytes));
-  a.stages = std::min(a.stages, std::max(2, st->nchunks));
+  a.stages = std::min(a.stages, std::max(2, cpr));
   a.ring_bytes = std::max(a.stages * stage_bytes, (epi_bytes + 127) / 128 * 128);
   const int smem = a.ring_bytes + (3 * a.stages + 2) * 8 + a.NT * 2 * 8 + 16;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(tc_gate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(tc_gate_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     attr = true;
   }
   if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
-  dim3 grid((L.b + a.NT - 1) / a.NT, ntiles);
-  tc_gate_kernel<<<grid, kTcThreads, smem, c->stream>>>(a);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((L.b + a.NT - 1) / a.NT, ntiles, a.ksplit);
+  cfg.blockDim = dim3(kTcThreads);
+  cfg.dynamicSmemBytes = size_t(smem);
+  cfg.stream = c->stream;
+  cudaLaunchAttribute attrs[1];
+  attrs[0].id = cudaLaunchAttributeClusterDimension;
+  attrs[0].val.clusterDim.x = 1;
+  attrs[0].val.clusterDim.y = 1;
+  attrs[0].val.clusterDim.z = unsigned(a.ksplit);
+  cfg.attrs = attrs;
+  cfg.numAttrs = a.ksplit > 1 ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, tc_gate_kernel, a);
 }
 
 }  // namespace mbx

@@ -66,24 +66,41 @@ __device__ __forceinline__ float* temp_ptr(const Ctx& c, int step, int t) {
 // out[i, j] for j in [j0, j1) of a (m x n) = A (m x k) . W (k x n), written at column
 // out_col0 + j of an out row of width out_ld.  W is shared (same for all tile nodes) or
 // batched (per node).
+// Threads [tbase, tbase + tcount) of the CTA take part (the weights of a FusedDense run side by
+// side on disjoint thread groups).
 __device__ void dense_range(const Ctx& c, const DRef& a, const DRef& w, int s, int out_ld,
-                            int out_col0, int j0, int j1) {
+                            int out_col0, int j0, int j1, int tbase = 0, int tcount = -1) {
   const int m = a.rows_r, k = a.cols_r, n = w.cols_r;
   const int ncr = j1 - j0;
-  if (ncr <= 0) return;
+  if (tcount < 0) tcount = blockDim.x;
+  const int tid = int(threadIdx.x) - tbase;
+  if (ncr <= 0 || tid < 0 || tid >= tcount) return;
   if (w.kind == kRefShared) {
     const float* W = ref_ptr(c, w, 0);
     const float* A[kMaxTM];
 #pragma unroll
     for (int t = 0; t < kMaxTM; ++t) A[t] = t < c.nn ? ref_ptr(c, a, t) : nullptr;
     const int total = m * ncr;
-    for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
+    for (int idx = tid; idx < total; idx += tcount) {
       const int i = idx / ncr, j = j0 + idx % ncr;
       float acc[kMaxTM];
 #pragma unroll
       for (int t = 0; t < kMaxTM; ++t) acc[t] = 0.0f;
       const float* wc = W + j;
-      for (int p = 0; p < k; ++p) {
+      // Weights for 8 consecutive p are loaded into registers before they are consumed, so the
+      // loads overlap; the accumulation itself stays strictly sequential in p (reference order).
+      int p = 0;
+      for (; p + 8 <= k; p += 8) {
+        float w8[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) w8[q] = __ldg(wc + int64_t(p + q) * n);
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+#pragma unroll
+          for (int t = 0; t < kMaxTM; ++t)
+            if (t < c.nn) acc[t] = fadd(acc[t], fmul(A[t][i * k + p + q], w8[q]));
+      }
+      for (; p < k; ++p) {
         const float wv = __ldg(wc + int64_t(p) * n);
 #pragma unroll
         for (int t = 0; t < kMaxTM; ++t)
@@ -95,13 +112,14 @@ __device__ void dense_range(const Ctx& c, const DRef& a, const DRef& w, int s, i
     }
   } else {
     const int total = c.nn * m * ncr;
-    for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
+    for (int idx = tid; idx < total; idx += tcount) {
       const int t = idx / (m * ncr);
       const int r = idx % (m * ncr);
       const int i = r / ncr, j = j0 + r % ncr;
       const float* A = ref_ptr(c, a, t);
       const float* W = ref_ptr(c, w, t);
       float acc = 0.0f;
+#pragma unroll 8
       for (int p = 0; p < k; ++p) acc = fadd(acc, fmul(A[i * k + p], W[int64_t(p) * n + j]));
       temp_ptr(c, s, t)[i * out_ld + out_col0 + j] = acc;
     }
@@ -130,10 +148,12 @@ __global__ void __launch_bounds__(256) plan_vm_kernel(VmLaunch L) {
     switch (st.kind) {
       case kStepFused: {
         int col = 0;
+        const int nw = st.nin - 1;
+        const int group = blockDim.x / nw;
         for (int w = 1; w < st.nin; ++w) {
           const DRef& wr = st.ins[w];
-          if (sp) dense_range(c, st.ins[0], wr, s, st.cols, col, u0, u1);
-          else dense_range(c, st.ins[0], wr, s, st.cols, col, 0, wr.cols_r);
+          if (sp) dense_range(c, st.ins[0], wr, s, st.cols, col, u0, u1, (w - 1) * group, group);
+          else dense_range(c, st.ins[0], wr, s, st.cols, col, 0, wr.cols_r, (w - 1) * group, group);
           col += wr.cols_r;
         }
         break;
