@@ -266,6 +266,7 @@ def run_ours(args):
     l2 = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")
 
     def step(**kw):
+        kw.setdefault("trace", False)
         return model.evaluate_batch(toks, data, args.batch, record_nodes=False, decode=False, **kw)
 
     for _ in range(max(3, args.warmup)):
@@ -302,7 +303,7 @@ def run_ours(args):
         dev_ms, host_ms, rA, _ = timed({"inputs_resident": True, "outputs_on_device": True, "time_kernels": True})
         gpu_launches = mbx.lib().mbx_kernel_launch_count() - launches0
         e2e_ms, e2e_host_ms, rB, _ = timed({})
-        prof_ms, _, rC, batch_us = timed({"time_batches": True}, per_batch=True)
+        prof_ms, _, rC, batch_us = timed({"time_batches": True, "trace": True}, per_batch=True)
     times = torch.tensor([dev_ms, e2e_ms, float(nodes)], dtype=torch.float64, device=f"cuda:{local}")
     if dist:
         mx = times.clone()
@@ -373,7 +374,8 @@ def run_ours(args):
         "step_roofline": {"R_us": R_total_us / K, "kernel_us": meas_total_us / K,
                           "frac": (R_total_us / meas_total_us) if meas_total_us else None,
                           "def": "sum over launches of max(F/bf16 peak, B/HBM) vs summed launch times (SURVEY 8d)"},
-        "breakdown_us_per_step": {"host_dfg_and_launch": rA.timing.host_dfg_us, "device_span": rA.timing.device_span_us,
+        "breakdown_us_per_step": {"host_dfg_and_launch": rA.timing.host_dfg_us, "host_split": rA.timing.host_breakdown,
+                                  "device_span": rA.timing.device_span_us,
                                   "per_sig": {sigs[s]: v["us"] / K for s, v in per_sig.items()}},
         "clocks": clk,
     }

@@ -165,6 +165,8 @@ struct Timing {
   double device_span_us = 0;    // sum over flushes of first-to-last batch (CUDA events)
   long h2d_bytes = 0, d2h_bytes = 0;
   long device_launches = 0;     // CUDA kernels issued
+  // host_dfg_us split: fiber execution + DFG build, scheduling, offset tables, kernel issue
+  double host_fibers_us = 0, host_sched_us = 0, host_prepare_us = 0, host_issue_us = 0;
   std::vector<double> batch_us; // per non-ghost batch (time_batches)
 };
 

@@ -157,6 +157,9 @@ int mbx_result_nodes(const mbx_result* r, int32_t* hdr, int64_t* refs, int64_t* 
 /* Timing of this evaluation in microseconds: host total, host DFG+schedule, device kernel span
  * (first to last batch, CUDA events), H2D bytes, D2H bytes. */
 int mbx_result_timing(const mbx_result* r, double* out5);
+/* Split of the host DFG time in microseconds: fiber execution + DFG construction, depth
+ * scheduling, offset-table preparation, kernel issue. */
+int mbx_result_host_breakdown(const mbx_result* r, double* out4);
 /* Per non-ghost batch, in trace order: device duration in microseconds (time_batches). */
 int mbx_result_batch_times(const mbx_result* r, double* us);
 

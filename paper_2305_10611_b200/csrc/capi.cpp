@@ -461,4 +461,12 @@ int mbx_result_timing(const mbx_result* r, double* o) {
   return 0;
 }
 
+int mbx_result_host_breakdown(const mbx_result* r, double* o) {
+  o[0] = r->r.timing.host_fibers_us;
+  o[1] = r->r.timing.host_sched_us;
+  o[2] = r->r.timing.host_prepare_us;
+  o[3] = r->r.timing.host_issue_us;
+  return 0;
+}
+
 }  // extern "C"

@@ -444,6 +444,7 @@ struct Executor::Impl {
       if (!n.executed && n.phase <= phase_limit) window.push_back(&n);
     if (window.empty()) return false;
     trace.flush_boundaries.push_back(static_cast<int>(trace.batches.size()));
+    auto ts0 = clk::now();
     std::vector<BatchRecord> batches;
     if (opts.scheduler == ExecOptions::Scheduler::kDepth) {
       batches = schedule_depth(window, trace.scheduler_ops);
@@ -453,6 +454,8 @@ struct Executor::Impl {
       for (auto& [p, group] : by_phase)
         for (auto& b : schedule_agenda(group, trace.scheduler_ops)) batches.push_back(std::move(b));
     }
+    auto ts1 = clk::now();
+    timing.host_sched_us += std::chrono::duration<double, std::micro>(ts1 - ts0).count();
     // Reserve index staging for the whole window so nothing recycles mid-flush.
     size_t meta_bytes = 0;
     for (const auto& b : batches) {
@@ -509,6 +512,13 @@ struct Executor::Impl {
     }
     timing.h2d_bytes += long(c->meta.cursor - c->meta.committed);
     mbx::meta_commit(c);
+    auto ts2 = clk::now();
+    timing.host_prepare_us += std::chrono::duration<double, std::micro>(ts2 - ts1).count();
+    struct IssueClock {
+      Timing& t;
+      clk::time_point a = clk::now();
+      ~IssueClock() { t.host_issue_us += std::chrono::duration<double, std::micro>(clk::now() - a).count(); }
+    } issue_clock{timing};
     if (!c->dry && !launches.empty()) {
       cudaEvent_t a = nullptr, e = nullptr;
       if (opts.time_kernels) {
@@ -712,7 +722,9 @@ EvalResult Executor::run() {
   I.upload_inputs();
 
   while (true) {
+    auto tf = clk::now();
     I.run_runnable();
+    I.timing.host_fibers_us += std::chrono::duration<double, std::micro>(clk::now() - tf).count();
     bool all_done = true;
     for (const auto& fb : fibers_) all_done = all_done && fb->status == FiberStatus::kDone;
     if (all_done) break;

@@ -83,6 +83,7 @@ def lib() -> ctypes.CDLL:
         "mbx_result_nodes": (I, [P, pI32, pI64, pI64]),
         "mbx_result_timing": (I, [P, pD]),
         "mbx_result_batch_times": (I, [P, pD]),
+        "mbx_result_host_breakdown": (I, [P, pD]),
         "mbx_ctx_stream": (P, [P]),
     }
     for name, (res, args) in sig.items():
@@ -103,7 +104,7 @@ def exported_symbols() -> List[str]:
                         "mbx_model_sig_name mbx_model_plan_encoding mbx_options_default mbx_evaluate_batch "
                         "mbx_result_destroy mbx_result_outputs mbx_result_counters mbx_result_batches "
                         "mbx_result_flush_boundaries mbx_result_nodes mbx_result_timing mbx_result_batch_times "
-                        "mbx_ctx_stream").split()]
+                        "mbx_result_host_breakdown mbx_ctx_stream").split()]
 
 
 def _ptr(a: np.ndarray, ct):
@@ -214,6 +215,7 @@ class Timing:
     h2d_bytes: int
     d2h_bytes: int
     batch_us: List[float] = field(default_factory=list)
+    host_breakdown: dict = field(default_factory=dict)  # fibers / sched / prepare / issue (us)
 
 
 @dataclass
@@ -377,7 +379,8 @@ class Model:
     def evaluate_batch(self, toks: np.ndarray, data: np.ndarray, batch: int, scheduler: str = "depth",
                        gather: str = "fused", hoist: bool = True, phases: bool = True, record_nodes: bool = True,
                        time_kernels: bool = False, time_batches: bool = False, inputs_resident: bool = False,
-                       outputs_on_device: bool = False, ghost: bool = True, decode: bool = True) -> EvalResult:
+                       outputs_on_device: bool = False, ghost: bool = True, decode: bool = True,
+                       trace: bool = True) -> EvalResult:
         L = lib()
         o = _Opts()
         L.mbx_options_default(ctypes.byref(o))
@@ -392,12 +395,12 @@ class Model:
         self.ctx.check(L.mbx_evaluate_batch(self.h, batch, _ptr(t, ctypes.c_int32), t.size, _ptr(d, ctypes.c_float),
                                             d.size, ctypes.byref(o), ctypes.byref(r)))
         try:
-            return _read_result(r, batch, record_nodes, decode)
+            return _read_result(r, batch, record_nodes, decode, trace)
         finally:
             L.mbx_result_destroy(r)
 
 
-def _read_result(r, batch: int, record_nodes: bool, decode: bool) -> EvalResult:
+def _read_result(r, batch: int, record_nodes: bool, decode: bool, want_trace: bool = True) -> EvalResult:
     L = lib()
     nt, nd = ctypes.c_int64(), ctypes.c_int64()
     L.mbx_result_outputs(r, None, ctypes.byref(nt), None, ctypes.byref(nd))
@@ -406,11 +409,12 @@ def _read_result(r, batch: int, record_nodes: bool, decode: bool) -> EvalResult:
     L.mbx_result_outputs(r, _ptr(ot, ctypes.c_int32), ctypes.byref(nt), _ptr(od, ctypes.c_float), ctypes.byref(nd))
     c = np.zeros(9, np.int64)
     L.mbx_result_counters(r, _ptr(c, ctypes.c_int64))
-    nb = int(c[6])
+    nb = int(c[6]) if want_trace else 0
     rows = np.zeros(5 * max(1, nb), np.int32)
     total_ids = 0
     ids = np.zeros(max(1, int(c[1])), np.int32)
-    L.mbx_result_batches(r, _ptr(rows, ctypes.c_int32), _ptr(ids, ctypes.c_int32))
+    if want_trace:
+        L.mbx_result_batches(r, _ptr(rows, ctypes.c_int32), _ptr(ids, ctypes.c_int32))
     batches, k = [], 0
     for b in range(nb):
         ph, dp, sg, sz, gh = (int(x) for x in rows[5 * b:5 * b + 5])
@@ -439,9 +443,12 @@ def _read_result(r, batch: int, record_nodes: bool, decode: bool) -> EvalResult:
             nodes.append(DFGNode(h[0], h[1], h[2], h[3], h[4], h[5], bool(h[6]), sh, bt, pr, ou))
     tm = np.zeros(5, np.float64)
     L.mbx_result_timing(r, _ptr(tm, ctypes.c_double))
-    bt = np.zeros(max(1, nb), np.float64)
+    bt = np.zeros(max(1, int(c[6])), np.float64)
     nbt = L.mbx_result_batch_times(r, _ptr(bt, ctypes.c_double))
-    timing = Timing(float(tm[0]), float(tm[1]), float(tm[2]), int(tm[3]), int(tm[4]), bt[:nbt].tolist())
+    hb = np.zeros(4, np.float64)
+    L.mbx_result_host_breakdown(r, _ptr(hb, ctypes.c_double))
+    timing = Timing(float(tm[0]), float(tm[1]), float(tm[2]), int(tm[3]), int(tm[4]), bt[:nbt].tolist(),
+                    dict(zip(("fibers", "sched", "prepare", "issue"), hb.tolist())))
     outputs = decode_hostvals(ot, od, batch) if decode else []
     return EvalResult(outputs, trace, nodes, timing, ot, od)
 
