@@ -139,6 +139,7 @@ void mbx_ctx_destroy(mbx_ctx* c) {
     if (c->d2h_host) cudaFreeHost(c->d2h_host);
     if (c->d2h_dev) cudaFree(c->d2h_dev);
     if (c->in_host) cudaFreeHost(c->in_host);
+    if (c->tc_part) cudaFree(c->tc_part);
     try { mbx::arena_release(c); } catch (...) {}
     cudaStreamDestroy(c->stream);
   } else {

@@ -68,6 +68,9 @@ struct mbx_ctx {
   // packs made under an older epoch are re-packed.
   uint64_t upload_epoch = 0;
   cudaEvent_t ev_a = nullptr, ev_b = nullptr;
+  // Split-K partial accumulators of the tensor-core kernels (L2-resident scratch).
+  float* tc_part = nullptr;
+  size_t tc_part_bytes = 0;
 };
 
 namespace mbx {

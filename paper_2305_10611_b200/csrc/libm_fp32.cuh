@@ -12,7 +12,9 @@
 // the header also compiles for the host so tests/ can check it against the system libm over all
 // 2^32 inputs (tests/test_libm_exact.py).
 #pragma once
+#ifndef MBX_NVRTC
 #include <stdint.h>
+#endif
 
 #if defined(__CUDACC__)
 #define MBX_HD __host__ __device__ __forceinline__
@@ -206,3 +208,18 @@ MBX_HD float sigmoidf_exact(float x) { return fdiv(1.0f, fadd(1.0f, expf_exact(-
 MBX_HD float reluf_exact(float x) { return x > 0.0f ? x : 0.0f; }
 
 }  // namespace mbx_libm
+
+#if defined(__CUDA_ARCH__)
+// Activations of the tensor-core tails (the GEMM is already approximate; these are accurate to a
+// few ulp): sigmoid via __expf, tanh via __expf with a series near 0 against cancellation.
+__device__ __forceinline__ float mbx_fsig(float x) { return __fdividef(1.0f, 1.0f + __expf(-x)); }
+__device__ __forceinline__ float mbx_ftanh(float x) {
+  const float a = fabsf(x);
+  if (a < 0.0625f) {
+    const float x2 = x * x;
+    return x * (1.0f + x2 * (-0.333333343f + x2 * (0.133333340f + x2 * -0.0539682540f)));
+  }
+  const float t = __expf(-2.0f * a);
+  return copysignf(__fdividef(1.0f - t, 1.0f + t), x);
+}
+#endif

@@ -1,0 +1,548 @@
+// tc_gate.cuh — device source of the per-plan tensor-core and pointwise kernels.
+//
+// This file is not compiled on its own.  At plan registration (kernels_tc.cu: tc_prepare) the
+// host generates a prelude with the plan's compile-time shape (MBX_KC, MBX_U, MBX_G, MBX_UC, ...)
+// and its column-local elementwise tail as straight-line code (mbx_tail / mbx_pw_tail), then
+// compiles prelude + libm_fp32.cuh + tc_abi.h + this file for sm_100a with NVRTC (jit.cpp).  The
+// reference equally generates one kernel per signature (kernelgen.cpp:212-292 lowers each block
+// into a plan; ACRoBat emits a specialised batched kernel per plan).
+//
+// mbx_tc_gate — plans  [concat(p0, p1)] -> dense / FusedDense(row, shared W_1..W_G) -> tail:
+//   swap-AB tcgen05: MMA M = 128 gate rows of one unit tile (G gates x UC units, zero padded),
+//   N = NT nodes of one node tile, K in chunks of MBX_KC; fp32 accumulator in TMEM.
+//   grid = (node tiles, unit tiles, K-split ranks); the ranks of a tile form a cluster.
+//   warp 0      : weight producer — one cp.async.bulk per stage (TMA bulk engine), mbarrier ring
+//   warp 1      : MMA issuer — one thread issues tcgen05.mma / tcgen05.commit
+//   warps 2..7  : node-row gatherers — cp.async (16 B, or 4 B when rows are unaligned) straight
+//                 from the arena through the per-node offset table into an fp32 staging ring,
+//                 converted to split bf16 (hi, lo) in the canonical no-swizzle K-major layout;
+//                 afterwards they prefetch the tail's input rows while the MMAs drain.
+//   epilogue    : tcgen05.ld -> each rank pushes its partial accumulator for the nodes rank r
+//                 finishes straight into rank r's shared memory (st.shared::cluster), one cluster
+//                 barrier, then every thread sums the S partials in rank order (deterministic),
+//                 runs the generated tail and writes the outputs batch-contiguously.
+//   PDL: the weight stream starts before griddepcontrol.wait, everything that reads activations
+//   after it, so a launch overlaps its predecessor's tail when launched programmatically.
+//
+// mbx_pointwise — purely elementwise plans: one thread per (node, element), generated tail with
+//   the glibc-exact activations (bit-identical to the reference).
+
+#define MBX_M 128
+
+#define MBX_THREADS 256
+
+namespace mbx_gen {
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Spin on test_wait (try_wait may park the warp for a scheduler quantum).
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phase) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+// Weight tiles are re-read by every level of a phase: keep them in L2 (evict_last).
+__device__ __forceinline__ void bulk_g2s_keep(void* dst, const void* src, unsigned bytes, unsigned long long* bar,
+                                              unsigned long long policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ unsigned long long policy_evict_last() {
+  unsigned long long p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(valid ? 16 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* dst, const void* src, bool valid) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(valid ? 4 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+__device__ __forceinline__ void named_sync(int id, int threads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+
+// Canonical K-major, no-swizzle UMMA shared-memory descriptor: 8-row x 16-byte core matrices,
+// K-adjacent core matrices 128 B apart (LBO), 8-row groups SBO bytes apart; version 1 (sm_100).
+__device__ __forceinline__ unsigned long long make_desc(unsigned saddr, unsigned sbo) {
+  unsigned long long d = 0;
+  d |= (unsigned long long)((saddr >> 4) & 0x3FFF);
+  d |= (unsigned long long)((128u >> 4) & 0x3FFF) << 16;
+  d |= (unsigned long long)((sbo >> 4) & 0x3FFF) << 32;
+  d |= 1ull << 46;
+  return d;
+}
+
+__device__ __forceinline__ void mma_bf16(unsigned tmem_d, unsigned long long a, unsigned long long b, unsigned idesc,
+                                         unsigned acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+
+__device__ __forceinline__ void mma_commit(unsigned long long* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld8(unsigned addr, float* v) {
+  unsigned r[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(addr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ unsigned pack_bf16x2(float lo_elem, float hi_elem) {
+  unsigned r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi_elem), "f"(lo_elem));
+  return r;
+}
+__device__ __forceinline__ float bf16_round(float x) {
+  unsigned short h;
+  asm("cvt.rn.bf16.f32 %0, %1;" : "=h"(h) : "f"(x));
+  return __uint_as_float(unsigned(h) << 16);
+}
+
+// Byte offset of element (row r, k) inside one K-chunk of the canonical layout.
+__device__ __forceinline__ unsigned canon_off(int r, int kk) {
+  return unsigned((r >> 3) * (MBX_KC * 16) + (kk >> 3) * 128 + (r & 7) * 16 + (kk & 7) * 2);
+}
+
+}  // namespace mbx_gen
+
+#ifdef MBX_STAMPS
+#define MBX_STAMP(who, i)                                                                        \
+  do {                                                                                           \
+    if (threadIdx.x == (who)) {                                                                  \
+      unsigned long long t_;                                                                     \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                     \
+      P.stamps[((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * 8 + (i)] = t_; \
+    }                                                                                            \
+  } while (0)
+#define MBX_CSTAMP(i)                                                                                   \
+  do {                                                                                                  \
+    if (threadIdx.x == 64 && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && (i) < 64) {     \
+      unsigned long long t_ = clock64();                                                                \
+      P.stamps[gridDim.x * gridDim.y * gridDim.z * 8 + (i)] = t_;                                       \
+    }                                                                                                   \
+  } while (0)
+#define MBX_MSTAMP(i)                                                                                   \
+  do {                                                                                                  \
+    if (threadIdx.x == 32 && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && (i) < 30) {      \
+      unsigned long long t_ = clock64();                                                                \
+      P.stamps[gridDim.x * gridDim.y * gridDim.z * 8 + 32 + (i)] = t_;                                  \
+    }                                                                                                   \
+  } while (0)
+#else
+#define MBX_MSTAMP(i) \
+  do {                \
+  } while (0)
+#define MBX_CSTAMP(i) \
+  do {                \
+  } while (0)
+#define MBX_STAMP(who, i) \
+  do {                    \
+  } while (0)
+#endif
+
+#ifdef MBX_GATE_KERNEL
+// Roles (256 threads): warp 0 lane 0 = weight producer, warp 1 = TMEM owner + MMA issuer, warps
+// 2-7 = node-row gather (cp.async straight into the MMA stage, completion counted on an mbarrier
+// by cp.async.mbarrier.arrive) and in-place fp32 -> split bf16 conversion.
+#define MBX_GATHER 192
+#define MBX_STAGES 4
+#ifndef MBX_LOOKAHEAD
+#define MBX_LOOKAHEAD 2
+#endif
+extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_gate(const __grid_constant__ TcGateArgs P) {
+  using namespace mbx_gen;
+  extern __shared__ __align__(1024) unsigned char smem[];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int NT = P.NT;
+  const int node0 = blockIdx.x * NT;
+  const int tile_u = blockIdx.y;
+  const int nn = min(NT, P.b - node0);
+  MBX_STAMP(0, 0);
+  MBX_CSTAMP(63);
+  const int npass = P.npass;
+  constexpr int S = MBX_STAGES;  // power of two: stage / phase arithmetic is shifts and masks
+  const int ksplit = P.ksplit;
+  unsigned rank = 0;
+  if (ksplit > 1) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+  const int cpr = MBX_NCHUNKS / ksplit;  // chunks per rank
+  const int c_begin = int(rank) * cpr;
+  // Unit tiles read the same node rows: start each at a different chunk so concurrent requests
+  // spread over different L2 lines.  Chunk of pipeline step i: c_begin + (i + rot) mod cpr.
+  const int rot = (tile_u * 3) % cpr;
+  auto chunk_of = [&](int i) {
+    const int j = i + rot;
+    return c_begin + (j >= cpr ? j - cpr : j);
+  };
+  const int ntr = NT / ksplit;           // nodes this rank finishes
+  const int nloc0 = int(rank) * ntr;     // first of them within the tile
+  const int nloc = max(0, min(ntr, nn - nloc0));
+  const int E = ntr * MBX_UC;
+
+  const int wpass = npass > 1 ? 2 : 1;
+  const int wchunk = MBX_M * MBX_KC * 2;  // one pass of one weight chunk (bytes)
+  const int xchunk = NT * MBX_KC * 2;     // one pass of one node chunk
+  const int wstage = wchunk * wpass;
+  const int stage_bytes = wstage + 2 * xchunk;  // X part doubles as the fp32 landing zone
+  unsigned char* ring = smem + P.ring_off;
+  float* recv = reinterpret_cast<float*>(smem + P.recv_off);  // [S-1][ntr][128] peers' partials
+  float* srcbuf = reinterpret_cast<float*>(smem + P.src_off);
+  unsigned long long* full_w = reinterpret_cast<unsigned long long*>(smem + P.bar_off);
+  unsigned long long* full_x = full_w + S;
+  unsigned long long* xraw = full_x + S;
+  unsigned long long* empty = xraw + S;
+  unsigned long long* done = empty + S;
+  unsigned long long* rbar = done + 1;
+  unsigned long long* tready = rbar + 1;
+  unsigned* tmem_slot = reinterpret_cast<unsigned*>(rbar + 2);
+  long long* rowbase = reinterpret_cast<long long*>(rbar + 3);  // [NT][2]
+
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full_w[s], 1);
+      mbar_init(&full_x[s], MBX_GATHER / 32);
+      mbar_init(&xraw[s], MBX_GATHER);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(done, 1);
+    mbar_init(rbar, 1);
+    mbar_init(tready, 32);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (ksplit > 1) mbar_expect_tx(rbar, unsigned((ksplit - 1) * ntr * MBX_M * 4));
+  }
+  __syncthreads();
+  // Peers may push partials into this CTA's receive buffer once its mbarrier is armed.
+  if (ksplit > 1) asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+  pdl_launch_dependents();
+  MBX_STAMP(0, 1);
+
+  if (warp == 0) {
+    // ---- weight producer (weights are static: no dependency on the previous launch) ----
+    if (lane == 0) {
+      const unsigned char* wtile = P.wpack + (size_t)tile_u * MBX_NCHUNKS * wstage;
+      const unsigned long long keep = policy_evict_last();
+      for (int i = 0; i < cpr; ++i) {
+        const int c = chunk_of(i), s = i % S;
+        if (i >= S) mbar_wait(&empty[s], ((i / S) - 1) & 1);
+        mbar_expect_tx(&full_w[s], wstage);
+        bulk_g2s_keep(ring + s * stage_bytes, wtile + (size_t)c * wstage, wstage, &full_w[s], keep);
+      }
+    }
+  } else if (warp == 1) {
+    // ---- MMA issuer (also owns the TMEM allocation; the epilogue learns the address through
+    // the tready mbarrier) ----
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(P.tmem_cols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    tc_fence_before();
+    mbar_arrive(tready);
+    mbar_wait(tready, 0);
+    tc_fence_after();
+    const unsigned tmem = *tmem_slot;
+    if (lane == 0) {
+      // kind::f16, A = B = BF16, D = F32, both K-major, N = NT, M = 128.
+      const unsigned idesc = (1u << 4) | (1u << 7) | (1u << 10) | (unsigned(NT >> 3) << 17) | (unsigned(MBX_M >> 4) << 24);
+      const unsigned ra = smem_u32(ring);
+      const unsigned sbo = unsigned(MBX_KC * 16);
+      for (int i = 0; i < cpr; ++i) {
+        const int s = i % S;
+        mbar_wait(&full_w[s], (i / S) & 1);
+        MBX_MSTAMP(3 * i);
+        mbar_wait(&full_x[s], (i / S) & 1);
+        MBX_MSTAMP(3 * i + 1);
+        tc_fence_after();
+        const unsigned wa = ra + s * stage_bytes;
+        const unsigned xa = wa + wstage;
+        const unsigned long long a_hi = make_desc(wa, sbo), b_hi = make_desc(xa, sbo);
+        const unsigned long long a_lo = make_desc(wa + wchunk, sbo), b_lo = make_desc(xa + xchunk, sbo);
+#pragma unroll
+        for (int ks = 0; ks < MBX_KC / 16; ++ks) {
+          const unsigned long long step = (unsigned long long)(ks * 16);  // +256 B in 16-byte units
+          mma_bf16(tmem, a_hi + step, b_hi + step, idesc, (i | ks) ? 1u : 0u);
+          if (npass > 1) {
+            mma_bf16(tmem, a_hi + step, b_lo + step, idesc, 1u);
+            mma_bf16(tmem, a_lo + step, b_hi + step, idesc, 1u);
+          }
+        }
+        mma_commit(&empty[s]);
+        MBX_MSTAMP(3 * i + 2);
+      }
+      mma_commit(done);
+      MBX_STAMP(32, 4);
+    }
+  } else {
+    // ---- node rows (warps 2-7): cp.async 16 B quads (4 B when rows are unaligned) straight into
+    // the stage's landing zone, LOOKAHEAD chunks ahead; arrival of everyone's quads is counted
+    // on xraw[s] by cp.async.mbarrier.arrive; then each thread converts its share of the landed
+    // chunk to split bf16 in place. ----
+    const int gt = tid - 64;
+    pdl_wait();  // activations and offset tables of this launch are ready
+    for (int i = gt; i < NT * 2; i += MBX_GATHER) {
+      const int n = i >> 1, pc = i & 1;
+      long long base = 0;
+      if (n < nn && pc < MBX_NPIECES)
+        base = (P.piece_kind[pc] == 0 ? P.shared_off[P.piece_idx[pc]]
+                                      : P.batched_off[(long long)(node0 + n) * P.nb + P.piece_idx[pc]]) +
+               P.piece_off[pc];
+      rowbase[i] = base;
+    }
+    named_sync(1, MBX_GATHER);
+    // Lane mapping: each group of 8 lanes handles one quad position of 8 consecutive nodes, so its
+    // shared-memory writes cover one contiguous 128-byte core matrix (no bank conflicts); quad qq
+    // of a node row lands where its 8-element group's hi (even qq) or lo (odd qq) operand will
+    // live, so the conversion rewrites it in place.
+    constexpr int kq = MBX_KC / 4;  // 16-byte quads per node row per chunk
+    const int l8 = gt & 7;
+    const int g0 = gt >> 3;          // 0..23
+    const int ngroups = (NT >> 3) * kq;
+    const float* arena = P.arena;
+    auto issue = [&](int i) {
+      const int s = i % S;
+      if (i >= S) mbar_wait(&empty[s], ((i / S) - 1) & 1);
+      const int k = chunk_of(i) * MBX_KC;
+      const int p1 = (MBX_NPIECES > 1 && k >= MBX_PK0) ? 1 : 0;  // chunks never straddle the pieces
+      const int kin = k - (p1 ? MBX_PK0 : 0);
+      unsigned char* xs = ring + s * stage_bytes + wstage;
+      for (int g = g0; g < ngroups; g += MBX_GATHER / 8) {
+        const int qq = g % kq, nb8 = g / kq;
+        const int n = nb8 * 8 + l8;
+        const bool valid = n < nn;
+        const float* src = arena + (valid ? rowbase[2 * n + p1] + kin + qq * 4 : 0);
+        float* dst = reinterpret_cast<float*>(xs + nb8 * (MBX_KC * 16) + l8 * 16 + ((qq >> 1) << 7) +
+                                              ((qq & 1) ? xchunk : 0));
+        if (P.vec16) {
+          cp_async16(dst, src, valid);
+        } else {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) cp_async4(dst + e, src + e, valid);
+        }
+      }
+      asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&xraw[s])) : "memory");
+    };
+    auto prefetch_tail_inputs = [&]() {
+      // The tail's input rows for the nodes this rank finishes: one row = UC consecutive floats.
+      for (int r = gt; r < P.nloads * ntr; r += MBX_GATHER) {
+        const int j = r / ntr, n = r - j * ntr;
+        float* dst = srcbuf + j * E + n * MBX_UC;
+        const bool valid = n < nloc;
+        long long base = 0;
+        if (valid) {
+          const TcLoad& l = P.loads[j];
+          const long long node = node0 + nloc0 + n;
+          base = (l.kind == 1 ? P.batched_off[node * P.nb + l.idx] : P.shared_off[l.idx]) + l.off + tile_u * MBX_UC;
+        }
+        const float* src = arena + base;
+#pragma unroll 8
+        for (int u = 0; u < MBX_UC; ++u) cp_async4(dst + u, src + u, valid);
+      }
+    };
+    const int look = min(MBX_LOOKAHEAD, S - 1);
+    for (int j = 0; j < min(look, cpr); ++j) issue(j);
+    if (look >= cpr) prefetch_tail_inputs();
+    constexpr int kb = MBX_KC / 8;
+    const int ngroups8 = (NT >> 3) * kb;
+    for (int i = 0; i < cpr; ++i) {
+      if (i + look < cpr) {
+        issue(i + look);
+        if (i + look == cpr - 1) prefetch_tail_inputs();
+      }
+      const int s = i % S;
+      mbar_wait(&xraw[s], (i / S) & 1);
+      MBX_CSTAMP(2 * i);
+      unsigned char* xs = ring + s * stage_bytes + wstage;
+      for (int g = g0; g < ngroups8; g += MBX_GATHER / 8) {
+        const int m = g % kb, nb8 = g / kb;  // 8 lanes = one core matrix (8 nodes x 8 k)
+        const unsigned off = unsigned(nb8 * (MBX_KC * 16) + m * 128 + l8 * 16);
+        const float4 a = *reinterpret_cast<const float4*>(xs + off);
+        const float4 bq = *reinterpret_cast<const float4*>(xs + xchunk + off);
+        const float v[8] = {a.x, a.y, a.z, a.w, bq.x, bq.y, bq.z, bq.w};
+        unsigned hp[4], lp[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          hp[q] = pack_bf16x2(v[2 * q], v[2 * q + 1]);  // low half = element 2q
+          const float h0 = __uint_as_float(hp[q] << 16), h1 = __uint_as_float(hp[q] & 0xffff0000u);
+          lp[q] = pack_bf16x2(v[2 * q] - h0, v[2 * q + 1] - h1);
+        }
+        const uint4 hi = make_uint4(hp[0], hp[1], hp[2], hp[3]);
+        const uint4 lo = make_uint4(lp[0], lp[1], lp[2], lp[3]);
+        // All of a group's quads were read above by this thread, so in-place is safe.
+        *reinterpret_cast<uint4*>(xs + off) = hi;
+        if (npass > 1) *reinterpret_cast<uint4*>(xs + xchunk + off) = lo;
+      }
+      fence_async_smem();  // generic-proxy stores -> visible to the tensor core (async proxy)
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&full_x[s]);
+      MBX_CSTAMP(2 * i + 1);
+    }
+    cp_async_wait<0>();
+  }
+
+  // ---- epilogue ----
+  pdl_wait();
+  mbar_wait(tready, 0);
+  mbar_wait(done, 0);
+  MBX_STAMP(0, 5);
+  tc_fence_after();
+  const unsigned tmem = *tmem_slot;
+  // TMEM lane = gate row; warp w reads lanes 32*(w%4).. for half of the node columns into the
+  // drained ring: stg[node][row].
+  float* stg = reinterpret_cast<float*>(ring);
+  {
+    const int q = warp & 3, half = warp >> 2;
+    const int row = q * 32 + lane;
+    const int cols = NT / 2;
+    for (int c0 = half * cols; c0 < (half + 1) * cols; c0 += 8) {
+      float v[8];
+      tmem_ld8(tmem + (unsigned(q * 32) << 16) + unsigned(c0), v);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) stg[(c0 + k) * MBX_M + row] = v[k];
+    }
+  }
+  tc_fence_before();
+  if (ksplit > 1) {
+    fence_async_smem();  // staged partials -> visible to the bulk-copy engine
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");  // peers' barriers armed
+  }
+  __syncthreads();
+  MBX_STAMP(0, 2);
+  if (warp == 1)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(P.tmem_cols) : "memory");
+  if (ksplit > 1) {
+    // Split-K: push the partial rows of the nodes rank r finishes to rank r (DSMEM bulk copies,
+    // completion counted on r's receive mbarrier), then wait for the S-1 incoming slices.
+    if (tid == 0) {
+      const unsigned bytes = unsigned(ntr * MBX_M * 4);
+      for (int r = 0; r < ksplit; ++r) {
+        if (r == int(rank)) continue;
+        const int slot = int(rank) < r ? int(rank) : int(rank) - 1;
+        unsigned dst, bar;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
+                     : "=r"(dst)
+                     : "r"(smem_u32(recv + (size_t)slot * ntr * MBX_M)), "r"(r));
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(bar) : "r"(smem_u32(rbar)), "r"(r));
+        asm volatile(
+            "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+            "r"(smem_u32(stg + (size_t)r * ntr * MBX_M)), "r"(bytes), "r"(bar)
+            : "memory");
+      }
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+    mbar_wait(rbar, 0);
+  }
+  MBX_STAMP(0, 6);
+
+  // Sum the partials in rank order (deterministic) and run the plan's tail per (node, unit).
+  for (int e = tid; e < nloc * MBX_UC; e += MBX_THREADS) {
+    const int n = e / MBX_UC, u = e - n * MBX_UC;
+    float g[MBX_G];
+#pragma unroll
+    for (int gi = 0; gi < MBX_G; ++gi) {
+      const int col = gi * MBX_UC + u;
+      float acc = 0.0f;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        if (q >= ksplit) break;
+        const float v = q == int(rank) ? stg[(nloc0 + n) * MBX_M + col]
+                                       : recv[((q < int(rank) ? q : q - 1) * ntr + n) * MBX_M + col];
+        acc = q == 0 ? v : acc + v;
+      }
+      g[gi] = acc;
+    }
+    float l[MBX_NLOADS > 0 ? MBX_NLOADS : 1];
+#pragma unroll
+    for (int j = 0; j < MBX_NLOADS; ++j) l[j] = srcbuf[j * E + e];
+    float o[MBX_NOUT];
+    mbx_tail(g, l, o);
+    const long long node = node0 + nloc0 + n;
+    const int ug = tile_u * MBX_UC + u;
+#pragma unroll
+    for (int k = 0; k < MBX_NOUT; ++k) P.arena[P.out_base[k] + node * MBX_U + ug] = o[k];
+  }
+  if (ksplit > 1 && tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+#ifdef MBX_STAMPS
+  __syncthreads();
+  MBX_STAMP(0, 7);
+#endif
+}
+#endif  // MBX_GATE_KERNEL
+
+#ifdef MBX_POINTWISE_KERNEL
+// One thread per (node, element).
+extern "C" __global__ void __launch_bounds__(256) mbx_pointwise(const __grid_constant__ PwArgs P) {
+  const long long total = (long long)P.b * MBX_PW_E;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const long long node = idx / MBX_PW_E;
+    const int e = int(idx - node * MBX_PW_E);
+    float l[MBX_NLOADS > 0 ? MBX_NLOADS : 1];
+#pragma unroll
+    for (int j = 0; j < MBX_NLOADS; ++j) {
+      const TcLoad& d = P.loads[j];
+      const long long base = d.kind == 1 ? P.batched_off[node * P.nb + d.idx] : P.shared_off[d.idx];
+      l[j] = P.arena[base + d.off + e];
+    }
+    float o[MBX_NOUT];
+    mbx_pw_tail(l, o);
+#pragma unroll
+    for (int k = 0; k < MBX_NOUT; ++k) P.arena[P.out_base[k] + node * MBX_PW_E + e] = o[k];
+  }
+}
+#endif  // MBX_POINTWISE_KERNEL
