@@ -603,6 +603,13 @@ BatchLaunch prepare_batch(mbx_ctx* c, int plan_id, int b, const int64_t* shared_
   return L;
 }
 
+// Shared-memory floats the plan VM may use to stage shared weights (after its temps): up to
+// 128 KiB, within the 227 KiB per-CTA limit.
+static int vm_weight_stage_floats(int temp_floats) {
+  const int budget = (227 * 1024) / 4 - 256 - ((temp_floats + 3) & ~3);
+  return std::max(0, std::min(budget, 32 * 1024));
+}
+
 void issue_batch(mbx_ctx* c, const BatchLaunch& L) {
   const PlanEntry& pe = c->plans[L.plan_id];
   if (pe.plan.ghost || c->dry) return;
@@ -612,7 +619,23 @@ void issue_batch(mbx_ctx* c, const BatchLaunch& L) {
     ++c->launches;
     ++g_launches;
   }
+  bool prefix_cached = false;
   if (pe.prefix_plan >= 0) {
+    // The prefix reads shared inputs only; if they are all session parameters its result is a
+    // function of the parameters alone and the scratch still holds it.
+    const PlanEntry& pp = c->plans[pe.prefix_plan];
+    const int64_t* sh = reinterpret_cast<const int64_t*>(c->meta.host + L.shared_meta);
+    std::vector<int64_t> key;
+    bool persistent = true;
+    for (size_t k = 0; k < pp.plan.shared_shapes.size(); ++k) {
+      key.push_back(sh[k]);
+      persistent = persistent && sh[k] + pp.plan.shared_shapes[k].size() <= c->persist_end;
+    }
+    key.push_back(int64_t(c->upload_epoch));
+    prefix_cached = persistent && key == pe.prefix_key;
+    pe.prefix_key = persistent ? key : std::vector<int64_t>{};
+  }
+  if (pe.prefix_plan >= 0 && !prefix_cached) {
     const PlanEntry& pp = c->plans[pe.prefix_plan];
     VmLaunch v{};
     v.plan = pp.dplan;
@@ -627,7 +650,9 @@ void issue_batch(mbx_ctx* c, const BatchLaunch& L) {
       v.nsplit = (unit + v.unit_chunk - 1) / v.unit_chunk;
     }
     v.threads = pp.threads;
-    v.smem_bytes = int(std::max<int64_t>(1, pp.hplan.temp_floats) * 4);
+    v.temp_floats_total = int(std::max<int64_t>(1, pp.hplan.temp_floats));
+    v.wst_floats = vm_weight_stage_floats(v.temp_floats_total);
+    v.smem_bytes = (((v.temp_floats_total + 3) & ~3) + v.wst_floats) * 4;
     v.shared_off = meta_dev<int64_t>(c, L.shared_meta);
     v.batched_off = nullptr;
     v.out_base = meta_dev<int64_t>(c, L.prefix_out_meta);
@@ -660,7 +685,9 @@ void issue_batch(mbx_ctx* c, const BatchLaunch& L) {
     v.unit_chunk = pe.hplan.unit;
   }
   v.threads = pe.threads;
-  v.smem_bytes = pe.smem;
+  v.temp_floats_total = pe.smem / 4;
+  v.wst_floats = vm_weight_stage_floats(v.temp_floats_total);
+  v.smem_bytes = (((v.temp_floats_total + 3) & ~3) + v.wst_floats) * 4;
   v.shared_off = meta_dev<int64_t>(c, L.shared_meta);
   v.batched_off = meta_dev<int64_t>(c, L.batched_meta);
   v.out_base = meta_dev<int64_t>(c, L.out_meta);

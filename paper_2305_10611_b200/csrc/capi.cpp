@@ -202,6 +202,7 @@ int mbx_arena_rewind(mbx_ctx* c, int64_t used) {
   return guarded(c, [&] {
     MBATCH_CHECK(used >= 0 && used <= c->used, "rewind past the arena end");
     c->used = used;
+    c->persist_end = std::min(c->persist_end, used);  // memory above may be reused now
   });
 }
 

@@ -23,6 +23,8 @@ struct PlanEntry {
   int prefix_plan = -1;
   std::vector<int64_t> prefix_sizes;  // floats per hoisted boundary tensor
   float* prefix_scratch = nullptr;
+  // Shared offsets + upload epoch the scratch currently holds the prefix for (see persist_end).
+  mutable std::vector<int64_t> prefix_key;
   DPlan hplan{};
   DPlan* dplan = nullptr;            // device copy
   int64_t temp_floats_per_inst = 0;  // sum of step output sizes (reference arena parity)
@@ -68,6 +70,10 @@ struct mbx_ctx {
   // packs made under an older epoch are re-packed.
   uint64_t upload_epoch = 0;
   cudaEvent_t ev_a = nullptr, ev_b = nullptr;
+  // Arena floats [0, persist_end) hold session parameters that only change through host writes
+  // (which bump upload_epoch); set by runtime::Session.  Lets a hoisted all-shared prefix whose
+  // inputs all lie below it be computed once per upload epoch.
+  int64_t persist_end = 0;
   // Split-K partial accumulators of the tensor-core kernels (L2-resident scratch).
   float* tc_part = nullptr;
   size_t tc_part_bytes = 0;

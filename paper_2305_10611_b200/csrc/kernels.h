@@ -17,7 +17,9 @@ struct VmLaunch {
   int nsplit;                  // column tiles
   int unit_chunk;              // columns per tile
   int threads;
-  int smem_bytes;
+  int smem_bytes;              // temps (tm * temp_floats) + weight staging
+  int temp_floats_total;       // tm * temp_floats
+  int wst_floats;              // weight staging floats (0: stream weights from L2)
   const int64_t* shared_off;   // [nshared]
   const int64_t* batched_off;  // [b * nbatched]
   const int64_t* out_base;     // [nout] region base offsets

@@ -47,7 +47,22 @@ struct Ctx {
   const int64_t* batched_off;
   float* temps;   // smem base
   int node0, nn;  // first node of the tile, nodes in the tile
+  float* wst;     // weight staging area (after the temps), wst_floats long
+  int wst_floats;
 };
+
+__device__ __forceinline__ void cp_async4(float* dst, const float* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(uint32_t(__cvta_generic_to_shared(dst))), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async16(float* dst, const float* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(uint32_t(__cvta_generic_to_shared(dst))), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void group_sync(int gi, int count) {
+  if (count == int(blockDim.x)) __syncthreads();
+  else asm volatile("bar.sync %0, %1;" ::"r"(1 + gi), "r"(count) : "memory");
+}
 
 __device__ __forceinline__ const float* ref_ptr(const Ctx& c, const DRef& r, int t) {
   int64_t slice = r.cols >= 0 ? r.col_off : 0;
@@ -69,12 +84,80 @@ __device__ __forceinline__ float* temp_ptr(const Ctx& c, int step, int t) {
 // Threads [tbase, tbase + tcount) of the CTA take part (the weights of a FusedDense run side by
 // side on disjoint thread groups).
 __device__ void dense_range(const Ctx& c, const DRef& a, const DRef& w, int s, int out_ld,
-                            int out_col0, int j0, int j1, int tbase = 0, int tcount = -1) {
+                            int out_col0, int j0, int j1, int tbase = 0, int tcount = -1, int gi = 0, int ngroups = 1) {
   const int m = a.rows_r, k = a.cols_r, n = w.cols_r;
   const int ncr = j1 - j0;
   if (tcount < 0) tcount = blockDim.x;
   const int tid = int(threadIdx.x) - tbase;
   if (ncr <= 0 || tid < 0 || tid >= tcount) return;
+  const int per_group = (c.wst_floats / ngroups) & ~3;
+  if (w.kind == kRefShared && m * ncr <= tcount && per_group >= (ncr + m * c.nn) * 16) {
+    // Shared weights, at most one output column per thread: stage W[:, j0:j1] through shared
+    // memory in passes of KB rows, every row of a pass in flight at once (cp.async), then run
+    // the strictly sequential accumulation from shared memory.  Same arithmetic and order as
+    // the direct path below.
+    const float* W = ref_ptr(c, w, 0) + j0;
+    float* ws = c.wst + gi * per_group;
+    // Pass of KB rows: W rows [KB][ncr] then the A rows of every tile node [nn][m][KB].
+    const int arow = m * c.nn;
+    const int KB = min(k, (per_group / (ncr + arow)) & ~3);
+    float* as = ws + KB * ncr;
+    const bool vec = (ncr % 4 == 0) && (n % 4 == 0) && ((reinterpret_cast<uintptr_t>(W) & 15) == 0);
+    const bool active = tid < m * ncr;
+    const int i = active ? tid / ncr : 0, jj = active ? tid % ncr : 0;
+    float acc[kMaxTM];
+#pragma unroll
+    for (int t = 0; t < kMaxTM; ++t) acc[t] = 0.0f;
+    for (int p0 = 0; p0 < k; p0 += KB) {
+      const int kb = min(KB, k - p0);
+      if (vec) {
+        const int q4 = ncr / 4;
+        for (int idx = tid; idx < kb * q4; idx += tcount) {
+          const int r = idx / q4, q = idx - r * q4;
+          cp_async16(ws + r * ncr + 4 * q, W + int64_t(p0 + r) * n + 4 * q);
+        }
+      } else {
+        for (int idx = tid; idx < kb * ncr; idx += tcount) {
+          const int r = idx / ncr, q = idx - r * ncr;
+          cp_async4(ws + idx, W + int64_t(p0 + r) * n + q);
+        }
+      }
+      for (int idx = tid; idx < arow * kb; idx += tcount) {
+        const int rr = idx / kb, p = idx - rr * kb;  // rr = t * m + row
+        const int t = rr / m, row = rr - t * m;
+        const float* src = ref_ptr(c, a, t) + row * k + p0 + p;
+        if (a.kind == kRefTemp) as[idx] = *src;  // already in shared memory
+        else cp_async4(as + idx, src);
+      }
+      asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+      group_sync(gi, tcount);
+      if (active) {
+        const float* wc = ws + jj;
+        if (c.nn == 1) {  // one node (the hoisted shared prefix): a single dependent chain
+          const float* a0 = as + i * kb;
+          float acc0 = acc[0];
+#pragma unroll 8
+          for (int p = 0; p < kb; ++p) acc0 = fadd(acc0, fmul(a0[p], wc[p * ncr]));
+          acc[0] = acc0;
+        } else {
+#pragma unroll 4
+          for (int p = 0; p < kb; ++p) {
+            const float wv = wc[p * ncr];
+#pragma unroll
+            for (int t = 0; t < kMaxTM; ++t)
+              if (t < c.nn) acc[t] = fadd(acc[t], fmul(as[(t * m + i) * kb + p], wv));
+          }
+        }
+      }
+      group_sync(gi, tcount);
+    }
+    if (active) {
+#pragma unroll
+      for (int t = 0; t < kMaxTM; ++t)
+        if (t < c.nn) temp_ptr(c, s, t)[i * out_ld + out_col0 + j0 + jj] = acc[t];
+    }
+    return;
+  }
   if (w.kind == kRefShared) {
     const float* W = ref_ptr(c, w, 0);
     const float* A[kMaxTM];
@@ -135,6 +218,8 @@ __global__ void __launch_bounds__(256) plan_vm_kernel(VmLaunch L) {
   c.shared_off = L.shared_off;
   c.batched_off = L.batched_off;
   c.temps = smem;
+  c.wst = smem + ((L.temp_floats_total + 3) & ~3);  // 16-byte aligned for cp.async
+  c.wst_floats = L.wst_floats;
   c.node0 = blockIdx.x * L.tm;
   c.nn = min(L.tm, L.b - c.node0);
   if (c.nn <= 0) return;
@@ -149,11 +234,12 @@ __global__ void __launch_bounds__(256) plan_vm_kernel(VmLaunch L) {
       case kStepFused: {
         int col = 0;
         const int nw = st.nin - 1;
-        const int group = blockDim.x / nw;
+        // Disjoint thread groups of whole warps (named barriers need multiples of 32).
+        const int group = nw == 1 ? int(blockDim.x) : (int(blockDim.x) / nw) & ~31;
         for (int w = 1; w < st.nin; ++w) {
           const DRef& wr = st.ins[w];
-          if (sp) dense_range(c, st.ins[0], wr, s, st.cols, col, u0, u1, (w - 1) * group, group);
-          else dense_range(c, st.ins[0], wr, s, st.cols, col, 0, wr.cols_r, (w - 1) * group, group);
+          if (sp) dense_range(c, st.ins[0], wr, s, st.cols, col, u0, u1, (w - 1) * group, group, w - 1, nw);
+          else dense_range(c, st.ins[0], wr, s, st.cols, col, 0, wr.cols_r, (w - 1) * group, group, w - 1, nw);
           col += wr.cols_r;
         }
         break;

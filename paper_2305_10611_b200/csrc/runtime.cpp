@@ -230,6 +230,7 @@ void Session::set_params(const ParamEnv& params) {
 EvalResult Session::evaluate(const std::vector<InstanceInput>& inputs, const ExecOptions& opts) {
   MBATCH_CHECK(!inputs.empty(), "evaluate_batch: need at least one instance");
   if (mbx_arena_rewind(ctx_, params_end_) != 0) throw Error(mbx_last_error(ctx_));
+  ctx_->persist_end = params_end_;  // nothing below the rewind point is written by this evaluation
   Executor ex(*this, inputs, opts);
   return ex.run();
 }
