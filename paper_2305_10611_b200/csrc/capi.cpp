@@ -140,6 +140,7 @@ void mbx_ctx_destroy(mbx_ctx* c) {
     if (c->d2h_dev) cudaFree(c->d2h_dev);
     if (c->in_host) cudaFreeHost(c->in_host);
     if (c->tc_part) cudaFree(c->tc_part);
+    if (c->gbar) cudaFree(c->gbar);
     try { mbx::arena_release(c); } catch (...) {}
     cudaStreamDestroy(c->stream);
   } else {

@@ -77,6 +77,10 @@ struct mbx_ctx {
   // Split-K partial accumulators of the tensor-core kernels (L2-resident scratch).
   float* tc_part = nullptr;
   size_t tc_part_bytes = 0;
+  // Grid-barrier counter of the persistent multi-level kernels: monotonic; the host tracks the
+  // value every launch starts from (stream order makes the launches sequential).
+  unsigned* gbar = nullptr;
+  unsigned gbar_count = 0;
 };
 
 namespace mbx {
@@ -124,5 +128,12 @@ BatchLaunch prepare_batch(mbx_ctx* c, int plan_id, int b, const int64_t* shared_
                           int64_t* gather_bytes);
 // Device half: enqueues the gather copies and the plan kernel (meta must be committed).
 void issue_batch(mbx_ctx* c, const BatchLaunch& L);
+
+// Persistent multi-level launches (kernels_tc.cu): if launches [i, i+n) (n >= 2) are consecutive
+// batches of one tensor-core gate plan over the same weights that one mbx_tc_levels launch can
+// run, stages its level table (before meta_commit) into *table and returns n; else 0.
+int plan_levels(mbx_ctx* c, const std::vector<BatchLaunch>& Ls, size_t i, size_t* table);
+// Enqueues that launch (meta committed).
+void issue_levels(mbx_ctx* c, const std::vector<BatchLaunch>& Ls, size_t i, int n, size_t table);
 
 }  // namespace mbx

@@ -13,6 +13,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -28,6 +29,8 @@
 #include "tc_abi.h"
 
 namespace mbx {
+
+extern std::atomic<int64_t> g_launches;
 
 namespace {
 
@@ -94,7 +97,16 @@ struct TcState {
   EpiProg prog;
   std::string src;            // generated kernel source
   void* fn = nullptr;         // cudaKernel_t
+  void* fn_fast = nullptr;    // pointwise plans: fast-activation variant (tensor-core precisions)
   bool attr_set = false;
+  // Persistent multi-level variant (mbx_tc_levels): K-split ranks, maximal node tile, smem layout.
+  int lS = 0, lNT = 0, l_w_off = 0, l_x_off = 0, l_recv_off = 0, l_bar_off = 0, l_smem = 0;
+  int lxch = 0;  // 0: K ranks form a cluster (DSMEM exchange), 1: L2 exchange, no cluster
+  void* lfn = nullptr;
+  bool l_attr_set = false;
+  float* l_part = nullptr;      // lxch 1: partials buffer
+  unsigned* l_flags = nullptr;  // lxch 1: arrival counters
+  unsigned l_tiles = 0;         // node tiles run so far (the counters' common base / (S-1))
   // packed-weight cache: (weight offsets, precision, upload epoch) -> device buffer
   struct Packed {
     std::vector<int64_t> offs;
@@ -187,10 +199,13 @@ bool compile_epilogue(const mbatch::backend::ExecutablePlan& p, TcState& st) {
 
 // The tail as a device function over registers: g = accumulator gates, l = loaded input rows.
 // Gate tails (tolerance path) use the fast activations; pointwise tails the glibc-exact ones.
-std::string gen_tail(const EpiProg& pr, bool pointwise) {
+// fast_pw: the pointwise tail with the fast activations (tensor-core precisions only).
+std::string gen_tail(const EpiProg& pr, bool pointwise, bool fast_pw = false) {
   std::ostringstream o;
-  o << (pointwise ? "__device__ __forceinline__ void mbx_pw_tail(const float* l, float* o) {\n"
+  o << (pointwise ? (fast_pw ? "__device__ __forceinline__ void mbx_pw_tail_fast(const float* l, float* o) {\n"
+                             : "__device__ __forceinline__ void mbx_pw_tail(const float* l, float* o) {\n")
                   : "__device__ __forceinline__ void mbx_tail(const float* g, const float* l, float* o) {\n");
+  const bool exact = pointwise && !fast_pw;
   for (int s = 0; s < pr.nslots; ++s) o << "  float s" << s << " = 0.0f;\n";
   auto ref = [](const EpiSrc& s) -> std::string {
     switch (s.type) {
@@ -206,8 +221,8 @@ std::string gen_tail(const EpiProg& pr, bool pointwise) {
     switch (op.op) {
       case kAdd: o << "mbx_libm::fadd(" << a << ", " << b << ")"; break;
       case kMul: o << "mbx_libm::fmul(" << a << ", " << b << ")"; break;
-      case kSigmoid: o << (pointwise ? "mbx_libm::sigmoidf_exact(" : "mbx_fsig(") << a << ")"; break;
-      case kTanh: o << (pointwise ? "mbx_libm::tanhf_exact(" : "mbx_ftanh(") << a << ")"; break;
+      case kSigmoid: o << (exact ? "mbx_libm::sigmoidf_exact(" : "mbx_fsig(") << a << ")"; break;
+      case kTanh: o << (exact ? "mbx_libm::tanhf_exact(" : "mbx_ftanh(") << a << ")"; break;
       case kRelu: o << "mbx_libm::reluf_exact(" << a << ")"; break;
       default: o << a; break;
     }
@@ -233,6 +248,9 @@ std::string gen_gate_source(const TcState& st) {
     << st.UC << "\n#define MBX_NCHUNKS " << st.nchunks << "\n#define MBX_NPIECES " << st.npieces
     << "\n#define MBX_PK0 " << st.piece_k[0] << "\n#define MBX_NLOADS " << st.prog.nloads << "\n#define MBX_NOUT "
     << st.prog.nout << "\n#define MBX_RAW " << kRawStages << "\n";
+  if (st.lS > 0)
+    o << "#define MBX_LEVELS_KERNEL 1\n#define MBX_LS " << st.lS << "\n#define MBX_LNT " << st.lNT
+      << "\n#define MBX_LXCH " << st.lxch << "\n";
   o << gen_tail(st.prog, false);
   o << jit::kernel_source();
   return o.str();
@@ -244,6 +262,7 @@ std::string gen_pointwise_source(const TcState& st) {
   o << "#define MBX_POINTWISE_KERNEL 1\n#define MBX_KC 16\n#define MBX_PW_E " << st.U << "\n#define MBX_NLOADS "
     << st.prog.nloads << "\n#define MBX_NOUT " << st.prog.nout << "\n";
   o << gen_tail(st.prog, true);
+  o << gen_tail(st.prog, true, true);
   o << jit::kernel_source();
   return o.str();
 }
@@ -403,6 +422,43 @@ Layout layout_for(const TcState& st, int NT, int S, int npass) {
   return L;
 }
 
+// Persistent multi-level layout (mbx_tc_levels): the CTA's resident weight slice
+// [K/S x 128 rows, hi|lo], the node-row region (doubles as the accumulator staging), the peers'
+// partials (DSMEM exchange only) and the barriers.  Picks the largest K split S <= 8 whose grid
+// (unit tiles x S) fits on the 148 SMs, then the largest node tile that fits in shared memory.
+// Clusters of 8 one-CTA-per-SM blocks: at least 14 are co-resident on a 148-SM B200 (GPCs of
+// 18-20 SMs); with more unit tiles than that the ranks exchange partials through L2 instead.
+// Returns false if the plan has no such layout (it then runs level by level).
+bool levels_layout(TcState& st) {
+  auto al = [](int x) { return (x + 1023) / 1024 * 1024; };
+  const int utiles = st.U / st.UC;
+  for (int S : {8, 4, 2, 1}) {
+    if (st.nchunks % S != 0 || utiles * S > 148) continue;
+    const int cpr = st.nchunks / S;
+    if (cpr > 16) continue;
+    const int xch = (S > 1 && utiles * S > 14 * 8) ? 1 : 0;
+    for (int NT : {128, 64, 32}) {
+      if (NT / S < 2 || (NT / S) * st.UC > 4 * kTcThreads) continue;
+      const int w = al(cpr * kM * st.KC * 4);
+      const int x = al(std::max(cpr * NT * st.KC * 4, NT * kM * 4));
+      const int recv = al(S > 1 && xch == 0 ? (S - 1) * (NT / S) * kM * 4 : 0);
+      const int bars = (2 * cpr + 6) * 8 + NT * 16;
+      if (w + x + recv + bars > kSmemBudget) continue;
+      st.lS = S;
+      st.lNT = NT;
+      st.lxch = xch;
+      st.l_w_off = 0;
+      st.l_x_off = w;
+      st.l_recv_off = w + x;
+      st.l_bar_off = w + x + recv;
+      st.l_smem = w + x + recv + bars;
+      return true;
+    }
+  }
+  st.lS = 0;
+  return false;
+}
+
 // Clusters of S CTAs (one CTA per SM at this shared-memory size) that can be resident at once.
 int max_active_clusters(void* fn, int S, int smem) {
   static std::map<std::pair<int, int>, int> cache;
@@ -499,14 +555,17 @@ void tc_prepare(mbx_ctx* c, PlanEntry& pe) {
   pe.tc_kind = -1;
   auto st = std::make_unique<TcState>();
   if (analyse(pe.exec_plan, pe.hplan, *st)) {
+    levels_layout(*st);
     st->src = gen_gate_source(*st);
     st->fn = load_kernel(c, st->src, "mbx_tc_gate");
+    if (st->lS > 0) st->lfn = load_kernel(c, st->src, "mbx_tc_levels");
     pe.tc_kind = 1;
   } else {
     *st = TcState{};
     if (!analyse_pointwise(pe.exec_plan, *st)) return;
     st->src = gen_pointwise_source(*st);
     st->fn = load_kernel(c, st->src, "mbx_pointwise");
+    st->fn_fast = load_kernel(c, st->src, "mbx_pointwise_fast");
     pe.tc_kind = 2;
   }
   pe.tc_state = st.release();
@@ -516,6 +575,8 @@ void tc_release(PlanEntry& pe) {
   auto* st = static_cast<TcState*>(pe.tc_state);
   if (!st) return;
   for (auto& p : st->packs) cudaFree(p.buf);
+  if (st->l_part) cudaFree(st->l_part);
+  if (st->l_flags) cudaFree(st->l_flags);
   delete st;
   pe.tc_state = nullptr;
 }
@@ -541,32 +602,26 @@ bool pdl_enabled() {
 
 }  // namespace
 
-cudaError_t tc_launch(mbx_ctx* c, const PlanEntry& pe, const BatchLaunch& L) {
-  auto* st = static_cast<TcState*>(pe.tc_state);
-  if (pe.tc_kind == 2) {
-    PwArgs a{};
-    a.arena = arena_ptr(c);
-    a.shared_off = meta_dev<long long>(c, L.shared_meta);
-    a.batched_off = meta_dev<long long>(c, L.batched_meta);
-    a.out_base = meta_dev<long long>(c, L.out_meta);
-    a.b = L.b;
-    a.E = st->U;
-    a.nb = int(pe.exec_plan.batched_shapes.size());
-    a.nloads = st->prog.nloads;
-    fill_loads(st->prog, a.loads);
-    const int64_t total = int64_t(L.b) * a.E;
-    const int blocks = int(std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, 148 * 8)));
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(blocks);
-    cfg.blockDim = dim3(256);
-    cfg.stream = c->stream;
-    void* args[] = {&a};
-    return cudaLaunchKernelExC(&cfg, st->fn, args);
-  }
-  const int npass = c->precision == MBX_PREC_BF16 ? 1 : 3;
-  const int wpass = npass > 1 ? 2 : 1;
-  // Resolve the shared offsets of the weights (host copy of the staged shared table).
+// The split-bf16 weight pack of a gate plan for the weights at `shared_host` (host copy of a
+// staged shared-offset table); packs on first use and after every parameter upload.
+// 16-byte cp.async of the gathered rows needs every row segment 16-byte aligned.
+static bool rows_vec16(mbx_ctx* c, const TcState* st, const PlanEntry& pe, const BatchLaunch& L) {
+  bool ok = true;
   const int64_t* shared_host = reinterpret_cast<const int64_t*>(c->meta.host + L.shared_meta);
+  const int64_t* bat = reinterpret_cast<const int64_t*>(c->meta.host + L.batched_meta);
+  const int nb = int(pe.exec_plan.batched_shapes.size());
+  for (int pc = 0; pc < st->npieces; ++pc) {
+    ok = ok && st->piece_off[pc] % 4 == 0 && st->piece_k[pc] % 4 == 0;
+    if (st->piece_kind[pc] == kRefShared) ok = ok && shared_host[st->piece_idx[pc]] % 4 == 0;
+    else
+      for (int i = 0; i < L.b && ok; ++i) ok = bat[int64_t(i) * nb + st->piece_idx[pc]] % 4 == 0;
+  }
+  return ok;
+}
+
+static cudaError_t ensure_pack(mbx_ctx* c, TcState* st, const int64_t* shared_host, int npass, TcState::Packed** out,
+                        bool* fresh) {
+  const int wpass = npass > 1 ? 2 : 1;
   std::vector<int64_t> offs;
   for (int w : st->w_shared) offs.push_back(shared_host[w]);
   TcState::Packed* pk = nullptr;
@@ -575,7 +630,7 @@ cudaError_t tc_launch(mbx_ctx* c, const PlanEntry& pe, const BatchLaunch& L) {
   const int ntiles = st->U / st->UC;
   const size_t chunk_bytes = size_t(kM) * st->KC * 2;
   const size_t pack_bytes = size_t(ntiles) * st->nchunks * wpass * chunk_bytes;
-  bool fresh_pack = false;
+  *fresh = false;
   if (!pk) {
     // (Re)pack: weights changed (new offsets or a host upload since the last pack).
     for (auto it = st->packs.begin(); it != st->packs.end(); ++it)
@@ -602,8 +657,42 @@ cudaError_t tc_launch(mbx_ctx* c, const PlanEntry& pe, const BatchLaunch& L) {
     ++c->launches;
     st->packs.push_back(p);
     pk = &st->packs.back();
-    fresh_pack = true;
+    *fresh = true;
   }
+  *out = pk;
+  return cudaSuccess;
+}
+
+cudaError_t tc_launch(mbx_ctx* c, const PlanEntry& pe, const BatchLaunch& L) {
+  auto* st = static_cast<TcState*>(pe.tc_state);
+  if (pe.tc_kind == 2) {
+    PwArgs a{};
+    a.arena = arena_ptr(c);
+    a.shared_off = meta_dev<long long>(c, L.shared_meta);
+    a.batched_off = meta_dev<long long>(c, L.batched_meta);
+    a.out_base = meta_dev<long long>(c, L.out_meta);
+    a.b = L.b;
+    a.E = st->U;
+    a.nb = int(pe.exec_plan.batched_shapes.size());
+    a.nloads = st->prog.nloads;
+    fill_loads(st->prog, a.loads);
+    const int64_t total = int64_t(L.b) * a.E;
+    const int blocks = int(std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, 148 * 8)));
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(blocks);
+    cfg.blockDim = dim3(256);
+    cfg.stream = c->stream;
+    void* args[] = {&a};
+    // FP32 contexts: glibc-exact activations (bit-identical to the reference); the tensor-core
+    // precisions use the fast ones, as their gate tails do.
+    return cudaLaunchKernelExC(&cfg, c->precision == MBX_PREC_FP32 ? st->fn : st->fn_fast, args);
+  }
+  const int npass = c->precision == MBX_PREC_BF16 ? 1 : 3;
+  const int64_t* shared_host = reinterpret_cast<const int64_t*>(c->meta.host + L.shared_meta);
+  const int ntiles = st->U / st->UC;
+  TcState::Packed* pk = nullptr;
+  bool fresh_pack = false;
+  if (cudaError_t e = ensure_pack(c, st, shared_host, npass, &pk, &fresh_pack); e != cudaSuccess) return e;
   const Tiling tl = pick_tiling(*st, L.b, npass);
   if (!tl.L.stages) return cudaErrorInvalidConfiguration;
   TcGateArgs a{};
@@ -633,18 +722,7 @@ cudaError_t tc_launch(mbx_ctx* c, const PlanEntry& pe, const BatchLaunch& L) {
   a.bar_off = tl.L.bar_off;
   a.tmem_cols = a.NT < 32 ? 32 : a.NT;
   // 16-byte cp.async for the gathered rows needs every row segment 16-byte aligned.
-  {
-    bool ok = true;
-    const int64_t* bat = reinterpret_cast<const int64_t*>(c->meta.host + L.batched_meta);
-    const int nb = a.nb;
-    for (int pc = 0; pc < st->npieces; ++pc) {
-      ok = ok && st->piece_off[pc] % 4 == 0 && st->piece_k[pc] % 4 == 0;
-      if (st->piece_kind[pc] == kRefShared) ok = ok && shared_host[st->piece_idx[pc]] % 4 == 0;
-      else
-        for (int i = 0; i < L.b && ok; ++i) ok = bat[int64_t(i) * nb + st->piece_idx[pc]] % 4 == 0;
-    }
-    a.vec16 = ok ? 1 : 0;
-  }
+  a.vec16 = rows_vec16(c, st, pe, L) ? 1 : 0;
   if (!st->attr_set) {
     cudaError_t e = cudaFuncSetAttribute(st->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget);
     if (e != cudaSuccess) return e;
@@ -724,6 +802,184 @@ cudaError_t tc_launch(mbx_ctx* c, const PlanEntry& pe, const BatchLaunch& L) {
     std::fprintf(stderr, "\n");
   }
   return e;
+}
+
+// ---- persistent multi-level launches (mbx_tc_levels) ------------------------------------------
+
+static bool levels_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("MBX_LEVELS");
+    return !e || std::atoi(e) != 0;
+  }();
+  return on;
+}
+
+int plan_levels(mbx_ctx* c, const std::vector<BatchLaunch>& Ls, size_t i, size_t* table) {
+  const BatchLaunch& L0 = Ls[i];
+  const PlanEntry& pe = c->plans[L0.plan_id];
+  static const bool dbg = std::getenv("MBX_LEVELS_DEBUG") != nullptr;
+  if (dbg)
+    std::fprintf(stderr, "plan_levels: plan %d b=%d tc_kind=%d prefix=%d lS=%d\n", L0.plan_id, L0.b, pe.tc_kind,
+                 pe.prefix_plan, pe.tc_state ? static_cast<TcState*>(pe.tc_state)->lS : -1);
+  if (!levels_enabled() || pe.tc_kind != 1 || c->precision == MBX_PREC_FP32 || pe.prefix_plan >= 0) return 0;
+  auto* st = static_cast<TcState*>(pe.tc_state);
+  if (!st || st->lS == 0 || (!st->lfn && !c->dry)) return 0;
+  const size_t ns = pe.exec_plan.shared_shapes.size();
+  const int64_t* sh0 = reinterpret_cast<const int64_t*>(c->meta.host + L0.shared_meta);
+  size_t j = i;
+  for (; j < Ls.size(); ++j) {
+    const BatchLaunch& L = Ls[j];
+    if (L.plan_id != L0.plan_id || !L.gathers.empty()) break;
+    // Same weights and shared inputs: one resident weight slice serves every level.
+    if (std::memcmp(c->meta.host + L.shared_meta, sh0, ns * 8) != 0) break;
+    if (!rows_vec16(c, st, pe, L)) break;
+  }
+  const int n = int(j - i);
+  if (dbg) std::fprintf(stderr, "plan_levels: run of %d\n", n);
+  if (n < 2) return 0;
+  const int utiles = st->U / st->UC;
+  if (!c->dry) {
+    // Every CTA must be resident at once (grid barrier between levels).
+    if (!st->l_attr_set) {
+      if (cudaFuncSetAttribute(st->lfn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget) != cudaSuccess ||
+          cudaFuncSetAttribute(st->lfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+      }
+      st->l_attr_set = true;
+    }
+    const int resident = st->lS > 1 && st->lxch == 0 ? max_active_clusters(st->lfn, st->lS, st->l_smem)
+                                                     : 148 / st->lS;
+    if (dbg) std::fprintf(stderr, "plan_levels: resident clusters %d, need %d\n", resident, utiles);
+    if (resident < utiles) return 0;
+  }
+  std::vector<TcLevel> tbl(static_cast<size_t>(n));
+  for (int k = 0; k < n; ++k) {
+    const BatchLaunch& L = Ls[i + size_t(k)];
+    int nt = 16;
+    while (nt < L.b && nt < st->lNT) nt *= 2;
+    nt = std::max(nt, std::min(st->lNT, 2 * st->lS));
+    tbl[k].shared_off = meta_dev<long long>(c, L.shared_meta);
+    tbl[k].batched_off = meta_dev<long long>(c, L.batched_meta);
+    tbl[k].out_base = meta_dev<long long>(c, L.out_meta);
+    tbl[k].b = L.b;
+    tbl[k].nt = nt;
+  }
+  *table = meta_stage(c, tbl.data(), tbl.size() * sizeof(TcLevel));
+  return n;
+}
+
+void issue_levels(mbx_ctx* c, const std::vector<BatchLaunch>& Ls, size_t i, int n, size_t table) {
+  if (c->dry) return;
+  const BatchLaunch& L0 = Ls[i];
+  const PlanEntry& pe = c->plans[L0.plan_id];
+  auto* st = static_cast<TcState*>(pe.tc_state);
+  const int npass = c->precision == MBX_PREC_BF16 ? 1 : 3;
+  const int64_t* shared_host = reinterpret_cast<const int64_t*>(c->meta.host + L0.shared_meta);
+  TcState::Packed* pk = nullptr;
+  bool fresh_pack = false;
+  cuda_check(ensure_pack(c, st, shared_host, npass, &pk, &fresh_pack), "weight pack");
+  if (!c->gbar) {
+    cuda_check(cudaMalloc(&c->gbar, 256), "grid barrier counter");
+    cuda_check(cudaMemset(c->gbar, 0, 256), "grid barrier counter");
+    c->gbar_count = 0;
+  }
+  const int utiles = st->U / st->UC;
+  TcLevelsArgs a{};
+  a.arena = arena_ptr(c);
+  a.wpack = pk->buf;
+  a.levels = meta_dev<TcLevel>(c, table);
+  a.nlevels = n;
+  a.nb = int(pe.exec_plan.batched_shapes.size());
+  a.npass = npass;
+  for (int k = 0; k < 2; ++k) {
+    a.piece_kind[k] = st->piece_kind[k];
+    a.piece_idx[k] = st->piece_idx[k];
+    a.piece_off[k] = st->piece_off[k];
+  }
+  a.w_off = st->l_w_off;
+  a.x_off = st->l_x_off;
+  a.recv_off = st->l_recv_off;
+  a.bar_off = st->l_bar_off;
+  a.tmem_cols = std::max(32, st->lNT);
+  a.gbar = c->gbar;
+  a.gbar_base = c->gbar_count;
+  unsigned tiles = 0;
+  if (st->lxch == 1) {
+    if (!st->l_part) {
+      const size_t lloc = size_t((st->lNT / 8 + st->lS - 1) / st->lS) * 8;  // MBX_LLOC
+      const size_t part_bytes = size_t(2) * utiles * st->lS * st->lS * lloc * kM * 4;
+      cuda_check(cudaMalloc(&st->l_part, part_bytes), "levels partials");
+      cuda_check(cudaMalloc(&st->l_flags, size_t(utiles) * st->lS * 4), "levels flags");
+      cuda_check(cudaMemset(st->l_flags, 0, size_t(utiles) * st->lS * 4), "levels flags");
+      st->l_tiles = 0;
+    }
+    const TcLevel* tbl = reinterpret_cast<const TcLevel*>(c->meta.host + table);
+    for (int k = 0; k < n; ++k) tiles += unsigned((tbl[k].b + tbl[k].nt - 1) / tbl[k].nt);
+    a.part = st->l_part;
+    a.xflags = st->l_flags;
+    a.xflag_base = unsigned(st->lS - 1) * st->l_tiles;
+  }
+  fill_loads(st->prog, a.loads);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(1, unsigned(utiles), unsigned(st->lS));
+  cfg.blockDim = dim3(kTcThreads);
+  cfg.dynamicSmemBytes = size_t(st->l_smem);
+  cfg.stream = c->stream;
+  cudaLaunchAttribute attrs[2];
+  int na = 0;
+  if (st->lS > 1 && st->lxch == 0) {
+    attrs[na].id = cudaLaunchAttributeClusterDimension;
+    attrs[na].val.clusterDim.x = 1;
+    attrs[na].val.clusterDim.y = 1;
+    attrs[na].val.clusterDim.z = unsigned(st->lS);
+    ++na;
+  }
+  if (!fresh_pack && pdl_enabled()) {
+    attrs[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attrs[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  cfg.attrs = attrs;
+  cfg.numAttrs = unsigned(na);
+  const int nctas = utiles * st->lS;
+  static unsigned long long* lstamps = nullptr;
+  if (stamps_enabled()) {
+    if (!lstamps) cudaMalloc(&lstamps, size_t(148) * 64 * 8 * 8);
+    cudaMemsetAsync(lstamps, 0, size_t(nctas) * 64 * 8 * 8, c->stream);
+    a.stamps = lstamps;
+  }
+  void* args[] = {&a};
+  cuda_check(cudaLaunchKernelExC(&cfg, st->lfn, args), "multi-level tensor-core kernel");
+  if (stamps_enabled()) {
+    // Profiling aid: per level, median / max over CTAs of each phase (us after the level start).
+    std::vector<unsigned long long> h(size_t(nctas) * 64 * 8);
+    cudaStreamSynchronize(c->stream);
+    cudaMemcpy(h.data(), lstamps, h.size() * 8, cudaMemcpyDeviceToHost);
+    std::fprintf(stderr, "levels: %d levels, %d CTAs (S=%d, NT<=%d, exchange %s)\n", n, nctas, st->lS, st->lNT,
+                 st->lxch ? "L2" : "DSMEM");
+    const char* names[] = {"start", "mma_wait", "mma_done", "pushed", "reduced", "tile_end", "barrier", "converted"};
+    unsigned long long t00 = ~0ull;
+    for (int i2 = 0; i2 < nctas; ++i2) t00 = std::min(t00, h[size_t(i2) * 64 * 8]);
+    for (int lv = 0; lv < std::min(n, 64); ++lv) {
+      std::fprintf(stderr, "  lv %2d b=%3d:", lv, Ls[i + size_t(lv)].b);
+      for (int k = 0; k < 8; ++k) {
+        std::vector<double> v;
+        for (int i2 = 0; i2 < nctas; ++i2) {
+          const unsigned long long x = h[(size_t(i2) * 64 + lv) * 8 + k];
+          if (x) v.push_back((double(x) - double(t00)) / 1e3);
+        }
+        if (v.empty()) continue;
+        std::sort(v.begin(), v.end());
+        std::fprintf(stderr, " %s %.2f/%.2f", names[k], v[v.size() / 2], v.back());
+      }
+      std::fprintf(stderr, "\n");
+    }
+  }
+  c->gbar_count += unsigned(utiles * st->lS) * unsigned(n - 1);
+  st->l_tiles += tiles;
+  ++c->launches;
+  ++g_launches;
 }
 
 }  // namespace mbx

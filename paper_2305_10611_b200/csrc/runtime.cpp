@@ -262,6 +262,7 @@ struct Executor::Impl {
   Timing timing;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> flush_events;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> batch_events;
+  std::vector<int> batch_share;  // batches one timed launch covers (multi-level launches > 1)
 
   Impl(Executor& e, Session& sess, const std::vector<InstanceInput>& in, const ExecOptions& o)
       : ex(e), s(sess), m(sess.model()), opts(o), c(sess.ctx()), inputs(in) {
@@ -463,7 +464,7 @@ struct Executor::Impl {
       if (b.ghost) continue;
       const auto& plan = m.kernels.plan(b.sig);
       const size_t nb = plan.batched_shapes.size();
-      meta_bytes += 8 * (plan.shared_shapes.size() + size_t(b.size) * nb * 2 + plan.outputs.size()) + 512;
+      meta_bytes += 8 * (plan.shared_shapes.size() + size_t(b.size) * nb * 2 + plan.outputs.size()) + 512 + 64;
     }
     mbx::meta_reserve(c, meta_bytes);
 
@@ -511,6 +512,19 @@ struct Executor::Impl {
       ++trace.kernel_launches;
       trace.batches.push_back(std::move(batch));
     }
+    // Runs of consecutive batches of one tensor-core gate plan (e.g. every TreeLSTM internal
+    // depth) become one persistent multi-level launch; their level tables are staged here.
+    std::vector<std::pair<int, size_t>> levels(launches.size(), {0, 0});
+    for (size_t i = 0; i < launches.size();) {
+        size_t tbl = 0;
+        const int n = mbx::plan_levels(c, launches, i, &tbl);
+        if (n >= 2) {
+          levels[i] = {n, tbl};
+          i += size_t(n);
+        } else {
+          ++i;
+        }
+      }
     timing.h2d_bytes += long(c->meta.cursor - c->meta.committed);
     mbx::meta_commit(c);
     auto ts2 = clk::now();
@@ -528,18 +542,22 @@ struct Executor::Impl {
         cudaEventRecord(a, c->stream);
       }
       int64_t before = c->launches;
-      for (const auto& L : launches) {
+      for (size_t i = 0; i < launches.size();) {
+        const int n = levels[i].first > 0 ? levels[i].first : 1;
+        cudaEvent_t x = nullptr, y = nullptr;
         if (opts.time_batches) {
-          cudaEvent_t x = nullptr, y = nullptr;
           cudaEventCreate(&x);
           cudaEventCreate(&y);
           cudaEventRecord(x, c->stream);
-          mbx::issue_batch(c, L);
+        }
+        if (levels[i].first > 0) mbx::issue_levels(c, launches, i, n, levels[i].second);
+        else mbx::issue_batch(c, launches[i]);
+        if (opts.time_batches) {
           cudaEventRecord(y, c->stream);
           batch_events.push_back({x, y});
-        } else {
-          mbx::issue_batch(c, L);
+          batch_share.push_back(n);
         }
+        i += size_t(n);
       }
       timing.device_launches += long(c->launches - before);
       if (opts.time_kernels) {
@@ -770,10 +788,11 @@ EvalResult Executor::run() {
     cudaEventElapsedTime(&ms, a, b);
     I.timing.device_span_us += ms * 1000.0;
   }
-  for (auto& [a, b] : I.batch_events) {
+  for (size_t k = 0; k < I.batch_events.size(); ++k) {
     float ms = 0;
-    cudaEventElapsedTime(&ms, a, b);
-    I.timing.batch_us.push_back(ms * 1000.0);
+    cudaEventElapsedTime(&ms, I.batch_events[k].first, I.batch_events[k].second);
+    const int n = I.batch_share[k];
+    for (int j = 0; j < n; ++j) I.timing.batch_us.push_back(ms * 1000.0 / n);
   }
   I.timing.host_dfg_us = std::chrono::duration<double, std::micro>(t_host - t0).count();
   I.timing.host_total_us = std::chrono::duration<double, std::micro>(clk::now() - t0).count();

@@ -36,6 +36,34 @@ struct TcGateArgs {
   TcLoad loads[MBX_MAX_LOADS];
 };
 
+// One level (batch) of a persistent multi-level launch: the batch's staged offset tables.
+struct TcLevel {
+  const long long* shared_off;
+  const long long* batched_off;
+  const long long* out_base;
+  int b;   // nodes in the batch
+  int nt;  // node tile (MMA N) used for this level: 16, 32, 64 or MBX_LNT
+};
+
+struct TcLevelsArgs {
+  float* arena;
+  const unsigned char* wpack;    // same packing as TcGateArgs::wpack
+  const TcLevel* levels;         // [nlevels]
+  int nlevels;
+  int nb;
+  int npass;
+  int piece_kind[2], piece_idx[2], piece_off[2];
+  int w_off, x_off, recv_off, bar_off;  // dynamic shared memory layout (bytes)
+  int tmem_cols;
+  unsigned* gbar;                // grid barrier counter (monotonic across launches)
+  unsigned gbar_base;            // its value when this launch starts
+  float* part;                   // MBX_LXCH 1: partials [2][unit tiles][S][S][MBX_LNT/S][128]
+  unsigned* xflags;              // MBX_LXCH 1: per (unit tile, rank) arrival counters (monotonic)
+  unsigned xflag_base;           // their value when this launch starts
+  unsigned long long* stamps;    // MBX_STAMPS builds only
+  TcLoad loads[MBX_MAX_LOADS];
+};
+
 struct PwArgs {
   float* arena;
   const long long* shared_off;

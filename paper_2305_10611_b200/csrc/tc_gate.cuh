@@ -524,9 +524,419 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_gate(const _
 }
 #endif  // MBX_GATE_KERNEL
 
+#ifdef MBX_LEVELS_KERNEL
+// mbx_tc_levels — one persistent launch for a run of consecutive batches ("levels") of the same
+// gate plan, e.g. every internal-node depth of a TreeLSTM flush.
+//   grid = (1, unit tiles, MBX_LS K-split ranks), all CTAs co-resident (one per SM).
+//   * The CTA's weight slice (128 gate rows x K/MBX_LS, split bf16) is bulk-copied into shared
+//     memory ONCE and reused by every level: per level only the node rows move.
+//   * Per node tile: cp.async gathers the rows of this rank's K slice straight from the arena
+//     through the level's offset table, in-place fp32 -> split-bf16 conversion, tcgen05.mma into
+//     TMEM, partial accumulators exchanged between the K ranks of the unit tile, summed in rank
+//     order (deterministic), the generated tail, outputs written batch-contiguously.
+//     MBX_LXCH 0: the ranks form a cluster; partials move by DSMEM bulk copies.
+//     MBX_LXCH 1: no cluster (any grid that fits on the SMs); partials move through an
+//                 L2-resident buffer, completion signalled by per-(tile, rank) release counters.
+//   * Between levels a grid barrier (monotonic counter, release / acquire): level l+1 gathers the
+//     rows level l wrote.  Every read of activations bypasses L1 (.cg): L1 is not coherent.
+//     The offset-table lookups of the next level's first tile happen before the barrier.
+#define MBX_LGATHER 192
+#define MBX_LCPR (MBX_NCHUNKS / MBX_LS)
+#if MBX_LXCH == 0
+#define MBX_LLOC (MBX_LNT / MBX_LS)  // nodes a rank finishes per tile: a contiguous slice
+#else
+#define MBX_LLOC (((MBX_LNT / 8 + MBX_LS - 1) / MBX_LS) * 8)  // 8-node chunks c with c % S == rank
+#endif
+#define MBX_LEPT ((MBX_LLOC * MBX_UC + MBX_THREADS - 1) / MBX_THREADS)
+#ifdef MBX_STAMPS
+#define MBX_LSTAMP_T(t, lv, i)                                                                      \
+  do {                                                                                              \
+    if (threadIdx.x == (t) && (lv) < 64) {                                                          \
+      P.stamps[(((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * 64 + (lv)) * 8 + \
+               (i)] = mbx_gen::global_ns();                                                         \
+    }                                                                                               \
+  } while (0)
+#else
+#define MBX_LSTAMP_T(t, lv, i) \
+  do {                         \
+  } while (0)
+#endif
+#define MBX_LSTAMP(lv, i) MBX_LSTAMP_T(0, lv, i)
+
+namespace mbx_gen {
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// Spins (one thread) until *ctr reaches target; a wait that cannot complete (it never should)
+// traps after ~2 s instead of hanging the GPU.
+__device__ __forceinline__ void spin_until(const unsigned* ctr, unsigned target) {
+  if (int(ld_acquire_u32(ctr) - target) >= 0) return;
+  const unsigned long long t0 = global_ns();
+  while (int(ld_acquire_u32(ctr) - target) < 0)
+    if (global_ns() - t0 > 2000000000ull) __trap();
+}
+// Grid-wide barrier over co-resident CTAs.  `target` = counter value once every CTA arrived.
+__device__ __forceinline__ void grid_barrier(unsigned* ctr, unsigned target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    red_release_add(ctr, 1u);
+    spin_until(ctr, target);
+  }
+  __syncthreads();
+}
+}  // namespace mbx_gen
+
+extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const __grid_constant__ TcLevelsArgs P) {
+  using namespace mbx_gen;
+  extern __shared__ __align__(1024) unsigned char smem[];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int tile_u = blockIdx.y;
+  constexpr int S = MBX_LS;
+  constexpr int CPR = MBX_LCPR;
+  unsigned rank = 0;
+#if MBX_LXCH == 0
+  if (S > 1) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+#else
+  rank = blockIdx.z;
+#endif
+  const int c_begin = int(rank) * CPR;
+  const int npass = P.npass;
+  const int wpass = npass > 1 ? 2 : 1;
+  const int wchunk = MBX_M * MBX_KC * 2;
+  const int wstage = wchunk * wpass;
+  constexpr int xchunk = MBX_LNT * MBX_KC * 2;  // one pass of one node chunk at the maximal tile
+  unsigned char* wsm = smem + P.w_off;          // [CPR][wstage], resident for the whole launch
+  unsigned char* xsm = smem + P.x_off;          // [CPR][2 * xchunk]; after the MMAs: stg
+  float* stg = reinterpret_cast<float*>(xsm);   // [nt][128] this rank's partials (LXCH 1: own slice)
+  float* recv = reinterpret_cast<float*>(smem + P.recv_off);  // [S-1][nt/S][128] peers' partials
+  unsigned long long* wfull = reinterpret_cast<unsigned long long*>(smem + P.bar_off);
+  unsigned long long* xraw = wfull + 1;
+  unsigned long long* xfull = xraw + CPR;
+  unsigned long long* done = xfull + CPR;
+  unsigned long long* rbar = done + 1;
+  unsigned long long* tready = rbar + 1;
+  unsigned* tmem_slot = reinterpret_cast<unsigned*>(tready + 1);
+  long long* rowbase = reinterpret_cast<long long*>(tready + 2);  // [MBX_LNT][2]
+  (void)recv;
+
+  if (tid == 0) {
+    mbar_init(wfull, 1);
+    for (int j = 0; j < CPR; ++j) {
+      mbar_init(&xraw[j], MBX_LGATHER);
+      mbar_init(&xfull[j], MBX_LGATHER / 32);
+    }
+    mbar_init(done, 1);
+    mbar_init(rbar, 1);
+    mbar_init(tready, 32);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    // The weight slice: static, so it streams in before the previous kernel finishes (PDL).
+    mbar_expect_tx(wfull, unsigned(CPR * wstage));
+    const unsigned char* wtile = P.wpack + (size_t)tile_u * MBX_NCHUNKS * wstage;
+    const unsigned long long keep = policy_evict_last();
+    for (int j = 0; j < CPR; ++j)
+      bulk_g2s_keep(wsm + j * wstage, wtile + (size_t)(c_begin + j) * wstage, wstage, wfull, keep);
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(P.tmem_cols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+#if MBX_LXCH == 0
+  if (S > 1) cluster_sync();  // peers' barriers initialised before any remote arrive
+  else __syncthreads();
+#else
+  __syncthreads();
+#endif
+  tc_fence_after();
+  const unsigned tmem = *tmem_slot;
+  const unsigned nctas = gridDim.x * gridDim.y * gridDim.z;
+  const int gt = tid - 64;  // gather thread index (warps 2-7)
+  // Offset-table lookups of one tile's node rows (static: known before the producers finish).
+  auto fill_rowbase = [&](const TcLevel& L, int node0, int nt) {
+    const int nn = min(nt, L.b - node0);
+    for (int i = gt; i < nt * 2; i += MBX_LGATHER) {
+      const int n = i >> 1, pc = i & 1;
+      long long base = 0;
+      if (n < nn && pc < MBX_NPIECES)
+        base = (P.piece_kind[pc] == 0 ? L.shared_off[P.piece_idx[pc]]
+                                      : L.batched_off[(long long)(node0 + n) * P.nb + P.piece_idx[pc]]) +
+               P.piece_off[pc];
+      rowbase[i] = base;
+    }
+  };
+  if (warp >= 2) fill_rowbase(P.levels[0], 0, P.levels[0].nt);
+  pdl_wait();  // the first level's inputs come from earlier launches
+
+  unsigned it = 0;  // node tiles processed: parity of every per-tile mbarrier
+  for (int lv = 0; lv < P.nlevels; ++lv) {
+    const TcLevel& L = P.levels[lv];
+    const int b = L.b, nt = L.nt;
+    const int ntr = nt / S;
+    MBX_LSTAMP(lv, 0);
+    if (lv + 1 == P.nlevels) pdl_launch_dependents();
+    for (int node0 = 0; node0 < b; node0 += nt, ++it) {
+      const unsigned par = it & 1u;
+      const int nn = min(nt, b - node0);
+#if MBX_LXCH == 0
+      const int nloc0 = int(rank) * ntr;
+      const int nloc = max(0, min(ntr, nn - nloc0));
+      auto loc_col = [&](int m) { return nloc0 + m; };  // tile column of the rank's m-th node
+#else
+      // Rank r finishes the 8-node chunks c of the tile with c % S == r (lane-aligned slices).
+      const int nloc = MBX_LLOC;
+      auto loc_col = [&](int m) { return (((m >> 3) * S + int(rank)) << 3) + (m & 7); };
+#endif
+#if MBX_LXCH == 0
+      if (S > 1 && tid == 0) mbar_expect_tx(rbar, unsigned((S - 1) * ntr * MBX_M * 4));
+#endif
+      if (warp >= 2) {
+        // ---- gather + convert (warps 2-7); rowbase was filled during the previous tile ----
+        named_sync(1, MBX_LGATHER);
+        constexpr int kq = MBX_KC / 4;
+        const int l8 = gt & 7, g0 = gt >> 3;
+        const int ngroups = ((nn + 7) >> 3) * kq;  // columns past the last valid group are never read
+        const float* arena = P.arena;
+#pragma unroll 1
+        for (int j = 0; j < CPR; ++j) {
+          const int k = (c_begin + j) * MBX_KC;
+          const int p1 = (MBX_NPIECES > 1 && k >= MBX_PK0) ? 1 : 0;
+          const int kin = k - (p1 ? MBX_PK0 : 0);
+          unsigned char* xs = xsm + j * 2 * xchunk;
+          for (int g = g0; g < ngroups; g += MBX_LGATHER / 8) {
+            const int qq = g % kq, nb8 = g / kq;
+            const int n = nb8 * 8 + l8;
+            const bool valid = n < nn;
+            const float* src = arena + (valid ? rowbase[2 * n + p1] + kin + qq * 4 : 0);
+            float* dst = reinterpret_cast<float*>(xs + nb8 * (MBX_KC * 16) + l8 * 16 + ((qq >> 1) << 7) +
+                                                  ((qq & 1) ? xchunk : 0));
+            cp_async16(dst, src, valid);
+          }
+          asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&xraw[j])) : "memory");
+        }
+        // Every row address of this tile is issued: look up the next tile's rows now (its
+        // offset tables are static), off the critical path of the next gather.
+        named_sync(1, MBX_LGATHER);
+        if (node0 + nt < b) fill_rowbase(L, node0 + nt, nt);
+        else if (lv + 1 < P.nlevels) fill_rowbase(P.levels[lv + 1], 0, P.levels[lv + 1].nt);
+        constexpr int kb = MBX_KC / 8;
+        const int ngroups8 = ((nn + 7) >> 3) * kb;
+#pragma unroll 1
+        for (int j = 0; j < CPR; ++j) {
+          mbar_wait(&xraw[j], par);
+          unsigned char* xs = xsm + j * 2 * xchunk;
+          for (int g = g0; g < ngroups8; g += MBX_LGATHER / 8) {
+            const int m = g % kb, nb8 = g / kb;
+            const unsigned off = unsigned(nb8 * (MBX_KC * 16) + m * 128 + l8 * 16);
+            const float4 a = *reinterpret_cast<const float4*>(xs + off);
+            const float4 bq = *reinterpret_cast<const float4*>(xs + xchunk + off);
+            const float v[8] = {a.x, a.y, a.z, a.w, bq.x, bq.y, bq.z, bq.w};
+            unsigned hp[4], lp[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              hp[q] = pack_bf16x2(v[2 * q], v[2 * q + 1]);
+              const float h0 = __uint_as_float(hp[q] << 16), h1 = __uint_as_float(hp[q] & 0xffff0000u);
+              lp[q] = pack_bf16x2(v[2 * q] - h0, v[2 * q + 1] - h1);
+            }
+            *reinterpret_cast<uint4*>(xs + off) = make_uint4(hp[0], hp[1], hp[2], hp[3]);
+            if (npass > 1) *reinterpret_cast<uint4*>(xs + xchunk + off) = make_uint4(lp[0], lp[1], lp[2], lp[3]);
+          }
+          fence_async_smem();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&xfull[j]);
+        }
+        MBX_LSTAMP_T(64, lv, 7);
+      } else if (warp == 1 && lane == 0) {
+        // ---- MMA issuer ----
+        if (it == 0) mbar_wait(wfull, 0);
+        const unsigned idesc =
+            (1u << 4) | (1u << 7) | (1u << 10) | (unsigned(nt >> 3) << 17) | (unsigned(MBX_M >> 4) << 24);
+        const unsigned sbo = unsigned(MBX_KC * 16);
+#pragma unroll 1
+        for (int j = 0; j < CPR; ++j) {
+          mbar_wait(&xfull[j], par);
+          tc_fence_after();
+          const unsigned wa = smem_u32(wsm + j * wstage);
+          const unsigned xa = smem_u32(xsm + j * 2 * xchunk);
+          const unsigned long long a_hi = make_desc(wa, sbo), b_hi = make_desc(xa, sbo);
+          const unsigned long long a_lo = make_desc(wa + wchunk, sbo), b_lo = make_desc(xa + xchunk, sbo);
+#pragma unroll
+          for (int ks = 0; ks < MBX_KC / 16; ++ks) {
+            const unsigned long long step = (unsigned long long)(ks * 16);
+            mma_bf16(tmem, a_hi + step, b_hi + step, idesc, (j | ks) ? 1u : 0u);
+            if (npass > 1) {
+              mma_bf16(tmem, a_hi + step, b_lo + step, idesc, 1u);
+              mma_bf16(tmem, a_lo + step, b_hi + step, idesc, 1u);
+            }
+          }
+        }
+        mma_commit(done);
+      }
+      // ---- tail operands of the nodes this rank finishes: into registers while the MMAs run ----
+      float lreg[MBX_LEPT][MBX_NLOADS > 0 ? MBX_NLOADS : 1];
+#pragma unroll
+      for (int t = 0; t < MBX_LEPT; ++t) {
+        const int e = tid + t * MBX_THREADS;
+        const int n = e / MBX_UC, u = e - n * MBX_UC;
+        const bool valid = n < nloc && loc_col(n) < nn;
+        const long long node = node0 + loc_col(n);
+#pragma unroll
+        for (int j = 0; j < MBX_NLOADS; ++j) {
+          const TcLoad& l = P.loads[j];
+          float v = 0.0f;
+          if (valid) {
+            const long long base = (l.kind == 1 ? L.batched_off[node * P.nb + l.idx] : L.shared_off[l.idx]) + l.off +
+                                   tile_u * MBX_UC + u;
+            v = __ldcg(P.arena + base);
+          }
+          lreg[t][j] = v;
+        }
+      }
+      MBX_LSTAMP(lv, 1);
+      mbar_wait(done, par);
+      MBX_LSTAMP(lv, 2);
+      __syncwarp();
+      tc_fence_after();
+#if MBX_LXCH == 0
+      // ---- accumulators -> shared memory (the X region is free once the MMAs completed) ----
+      {
+        const int q = warp & 3, half = warp >> 2;
+        const int row = q * 32 + lane;
+        const int cols = nt / 2;
+        for (int c0 = half * cols; c0 < (half + 1) * cols; c0 += 8) {
+          float v[8];
+          tmem_ld8(tmem + (unsigned(q * 32) << 16) + unsigned(c0), v);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) stg[(c0 + k) * MBX_M + row] = v[k];
+        }
+      }
+      tc_fence_before();
+      if (S > 1) {
+        fence_async_smem();  // staged partials -> visible to the bulk-copy engine
+        cluster_sync();      // every rank staged its partials, armed rbar, consumed the last tile
+        MBX_LSTAMP(lv, 3);
+        if (tid == 0) {
+          const unsigned bytes = unsigned(ntr * MBX_M * 4);
+          for (int r = 0; r < S; ++r) {
+            if (r == int(rank)) continue;
+            const int slot = int(rank) < r ? int(rank) : int(rank) - 1;
+            unsigned dst, bar;
+            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
+                         : "=r"(dst)
+                         : "r"(smem_u32(recv + (size_t)slot * ntr * MBX_M)), "r"(r));
+            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(bar) : "r"(smem_u32(rbar)), "r"(r));
+            asm volatile(
+                "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    dst),
+                "r"(smem_u32(stg + (size_t)r * ntr * MBX_M)), "r"(bytes), "r"(bar)
+                : "memory");
+          }
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+        mbar_wait(rbar, par);
+      } else {
+        __syncthreads();
+      }
+      auto partial = [&](int q, int n, int col) -> float {
+        return q == int(rank) ? stg[(nloc0 + n) * MBX_M + col] : recv[((q < int(rank) ? q : q - 1) * ntr + n) * MBX_M + col];
+      };
+#else
+      // ---- accumulators: own rank's nodes -> shared memory, the peers' -> their L2 slots ----
+      // part layout: [tile parity][unit tile][destination rank][source rank][nt/S][128]
+      float* pbase = P.part + (size_t)(par * gridDim.y + tile_u) * S * S * MBX_LLOC * MBX_M;
+      {
+        // Warp w reads TMEM lanes 32*(w%4).. (gate rows) for every other 8-column chunk.
+        const int q = warp & 3, half = warp >> 2;
+        const int row = q * 32 + lane;
+        for (int ch = half; ch < (nn + 7) >> 3; ch += 2) {
+          float v[8];
+          tmem_ld8(tmem + (unsigned(q * 32) << 16) + unsigned(ch * 8), v);
+          const int r = ch % S, m0 = (ch / S) * 8;
+          float* dst = r == int(rank) ? stg + m0 * MBX_M + row : pbase + ((size_t)(r * S + int(rank)) * MBX_LLOC + m0) * MBX_M + row;
+          if (r == int(rank)) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) dst[k * MBX_M] = v[k];
+          } else {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) __stcg(dst + k * MBX_M, v[k]);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncthreads();
+      if (S > 1) {
+        unsigned* flags = P.xflags + tile_u * S;
+        if (tid < S && tid != int(rank)) red_release_add(flags + tid, 1u);
+        MBX_LSTAMP(lv, 3);
+        if (tid == 0) spin_until(flags + rank, P.xflag_base + unsigned(S - 1) * (it + 1));
+        __syncthreads();
+      }
+      auto partial = [&](int q, int n, int col) -> float {
+        return q == int(rank) ? stg[n * MBX_M + col]
+                              : __ldcg(pbase + ((size_t)(int(rank) * S + q) * MBX_LLOC + n) * MBX_M + col);
+      };
+#endif
+      MBX_LSTAMP(lv, 4);
+      // ---- sum the partials in rank order, run the tail, write the outputs ----
+#pragma unroll
+      for (int t = 0; t < MBX_LEPT; ++t) {
+        const int e = tid + t * MBX_THREADS;
+        const int n = e / MBX_UC, u = e - n * MBX_UC;
+        if (n < nloc && loc_col(n) < nn) {
+          float g[MBX_G];
+#pragma unroll
+          for (int gi = 0; gi < MBX_G; ++gi) {
+            const int col = gi * MBX_UC + u;
+            float acc = 0.0f;
+#pragma unroll
+            for (int q = 0; q < S; ++q) {
+              const float v = partial(q, n, col);
+              acc = q == 0 ? v : acc + v;
+            }
+            g[gi] = acc;
+          }
+          float o[MBX_NOUT];
+          mbx_tail(g, lreg[t], o);
+          const long long node = node0 + loc_col(n);
+          const int ug = tile_u * MBX_UC + u;
+#pragma unroll
+          for (int k = 0; k < MBX_NOUT; ++k) P.arena[L.out_base[k] + node * MBX_U + ug] = o[k];
+        }
+      }
+#if MBX_LXCH == 0
+      if (S > 1 && tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+#endif
+      __syncthreads();  // stg / recv / TMEM free for the next tile
+      tc_fence_after();
+      MBX_LSTAMP(lv, 5);
+    }
+    if (lv + 1 < P.nlevels) grid_barrier(P.gbar, P.gbar_base + unsigned(lv + 1) * nctas);
+    MBX_LSTAMP(lv, 6);
+  }
+#if MBX_LXCH == 0
+  if (S > 1) cluster_sync();  // no peer still pushes into this CTA's shared memory
+#endif
+  if (warp == 1)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(P.tmem_cols) : "memory");
+}
+#endif  // MBX_LEVELS_KERNEL
+
 #ifdef MBX_POINTWISE_KERNEL
-// One thread per (node, element).
-extern "C" __global__ void __launch_bounds__(256) mbx_pointwise(const __grid_constant__ PwArgs P) {
+// One thread per (node, element); the offset-table lookups are shared by the E elements of a
+// node.  FAST selects the fast activations (tensor-core precisions).
+template <bool FAST>
+__device__ __forceinline__ void mbx_pointwise_body(const PwArgs& P) {
   const long long total = (long long)P.b * MBX_PW_E;
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
        idx += (long long)gridDim.x * blockDim.x) {
@@ -540,9 +950,16 @@ extern "C" __global__ void __launch_bounds__(256) mbx_pointwise(const __grid_con
       l[j] = P.arena[base + d.off + e];
     }
     float o[MBX_NOUT];
-    mbx_pw_tail(l, o);
+    if (FAST) mbx_pw_tail_fast(l, o);
+    else mbx_pw_tail(l, o);
 #pragma unroll
     for (int k = 0; k < MBX_NOUT; ++k) P.arena[P.out_base[k] + node * MBX_PW_E + e] = o[k];
   }
+}
+extern "C" __global__ void __launch_bounds__(256) mbx_pointwise(const __grid_constant__ PwArgs P) {
+  mbx_pointwise_body<false>(P);
+}
+extern "C" __global__ void __launch_bounds__(256) mbx_pointwise_fast(const __grid_constant__ PwArgs P) {
+  mbx_pointwise_body<true>(P);
 }
 #endif  // MBX_POINTWISE_KERNEL
