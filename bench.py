@@ -2,15 +2,20 @@
 """Benchmark of the batched-execution hot path (BASELINE.json: "batched nodes/sec and ms per
 mini-batch (bs 8/64) at 1/2/4/8 B200 vs CPU ref").
 
-A step = one mini-batch of the workload evaluated end to end by the runtime: fibers + inline-depth
-DFG construction + depth scheduling on the host, every batch as a device launch, synthetic inputs
+A mini-batch of the workload is evaluated end to end by the runtime: fibers + inline-depth DFG
+construction + depth scheduling on the host, every batch as a device launch, synthetic inputs
 from the reference's zoo generators.  Default workload: TreeLSTM hidden 512, batch 64 (the
 headline config, BASELINE.json configs[1]).
 
-  value  nodes/s with the mini-batch's inputs already resident in HBM (no input H2D, outputs left
-         in HBM), timed with CUDA events on the library's stream, L2 flushed between steps.
-  e2e    the same through the C ABI with HOST buffers: H2D of the inputs, the run, D2H of the
-         outputs, every step (mbx_evaluate_batch, the reference-facing evaluate_batch).
+A step = T x R independent mini-batches (R per worker) evaluated by the native throughput pool
+(mbx_pool_run: T host worker threads, one context each, one shared device stream) — the same use
+of the host cores as the reference arm, which runs one process per core.
+  value  nodes/s with every mini-batch's inputs already resident in HBM (no input H2D, outputs
+         left in HBM), CUDA events on the pool stream around each step, L2 flushed between steps.
+  e2e    the same with HOST buffers: H2D of the inputs, the run, D2H of the outputs, every
+         mini-batch (mbx_evaluate_batch semantics per mini-batch).
+  latency  one mini-batch at a time on one context (ms per mini-batch, host split, per-signature
+         device times) — the roofline figures come from this single-stream run.
 Multi-GPU (torchrun, one process per GPU): each rank runs its own mini-batch (seed + rank) —
 instances shard independently, no collective on the data path ("scaling": "weak"); NCCL is used
 only for the start barrier and the max-over-ranks of the timings.
@@ -47,6 +52,9 @@ def parse_args():
     p.add_argument("--seed", type=int, default=1)
     p.add_argument("--precision", default="bf16x3", choices=["fp32", "bf16x3", "bf16"])
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--threads", type=int, default=0,
+                   help="host worker threads of the throughput pool (0: min(12, cores per rank - 2))")
+    p.add_argument("--per-thread", type=int, default=4, help="mini-batches per worker thread per step")
     return p.parse_args()
 
 
@@ -300,6 +308,8 @@ def run_ours(args):
     torch.cuda.synchronize(local)
     launches0 = mbx.lib().mbx_kernel_launch_count()
     with ClockSampler(local) as clocks:
+        pool_res = run_pool(args, mbx, torch, local, rank, world, nodes, l2)
+        launches0 = mbx.lib().mbx_kernel_launch_count()
         dev_ms, host_ms, rA, _ = timed({"inputs_resident": True, "outputs_on_device": True, "time_kernels": True})
         gpu_launches = mbx.lib().mbx_kernel_launch_count() - launches0
         e2e_ms, e2e_host_ms, rB, _ = timed({})
@@ -320,8 +330,9 @@ def run_ours(args):
         return
 
     K = args.steps
-    value = nodes_total * K / (dev_max / 1e3)
-    e2e = nodes_total * K / (e2e_max / 1e3)
+    lat_value = nodes_total * K / (dev_max / 1e3)
+    lat_e2e = nodes_total * K / (e2e_max / 1e3)
+    value, e2e = pool_res["value"], pool_res["e2e"]
     pk = peaks()
     # Per-signature device time from region C and algorithmic work of each launch.
     sigs = model.signatures()
@@ -359,15 +370,21 @@ def run_ours(args):
     clk = clocks.summary()
     line = {
         "metric": METRIC, "value": value, "unit": "nodes/s", "n_gpus": world, "steps": K, "warmup": args.warmup,
-        "ms_per_step": dev_max / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "ms_per_step": pool_res["ms_per_step"], "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": {"fp32": "f32", "bf16x3": "bf16x3 (split-bf16 tcgen05, fp32 accumulate)", "bf16": "bf16"}[args.precision],
         "data": f"synthetic: reference zoo generators (params seed {args.seed}, inputs seed {args.seed}+rank)",
         "config": {"workload": f"{args.model}-h{args.hidden}-b{args.batch}", "hidden": args.hidden,
                    "batch": args.batch, "nodes_per_minibatch": nodes, "precision": args.precision,
-                   "l2": "flushed between steps (256 MiB write)", "parallelism": f"instance shards x{world}"},
-        "e2e": {"value": e2e, "unit": "nodes/s", "ms_per_step": e2e_max / K, "h2d_bytes_per_step": rB.timing.h2d_bytes,
-                "d2h_bytes_per_step": rB.timing.d2h_bytes},
-        "gpu_launches": int(gpu_launches),
+                   "l2": "flushed between steps (256 MiB write)", "parallelism": f"instance shards x{world}",
+                   "minibatches_per_step": pool_res["threads"] * pool_res["per_thread"],
+                   "host_threads": pool_res["threads"]},
+        "e2e": {"value": e2e, "unit": "nodes/s", "ms_per_step": pool_res["e2e_ms_per_step"],
+                "h2d_bytes_per_step": rB.timing.h2d_bytes * pool_res["threads"] * pool_res["per_thread"],
+                "d2h_bytes_per_step": rB.timing.d2h_bytes * pool_res["threads"] * pool_res["per_thread"]},
+        "latency": {"ms_per_minibatch": dev_max / K, "e2e_ms_per_minibatch": e2e_max / K,
+                    "nodes_per_s": lat_value, "e2e_nodes_per_s": lat_e2e,
+                    "def": "one mini-batch at a time on one context, device events around each call"},
+        "gpu_launches": int(gpu_launches) + pool_res["launches"],
         "roofline": {"bound": bound, "achieved": ach, "peak": peak, "unit": unit, "frac": ach / peak,
                      "traffic": traffic, "kernel": sigs[dom], "launches_per_step": d["launches"] // K,
                      "peak_src": pk["src"] if tensor_path or bound == "hbm" else "fp32 SIMT nominal"},
@@ -385,6 +402,51 @@ def run_ours(args):
     if dist:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def run_pool(args, mbx, torch, local, rank, world, nodes, l2):
+    """Throughput: T worker threads, each evaluating its own mini-batch per step (mbx_pool_run).
+    Returns value / e2e nodes/s and the per-step device times (CUDA events on the pool stream)."""
+    cores = max(1, (os.cpu_count() or 1) // max(1, world))
+    T = args.threads or max(1, min(12, cores - 2))
+    pool = mbx.Pool(local, args.precision, args.model, args.hidden, args.seed, T)
+    ctx = mbx.Context(-1, args.precision)  # host-only: the synthetic inputs
+    gen = mbx.Model(ctx, args.model, args.hidden)
+    ins = [gen.make_inputs(args.seed + rank * T + w, args.batch) for w in range(T)]
+    stream = torch.cuda.ExternalStream(pool.stream(), device=local)
+
+    def steps(K, kw):
+        ms, total = 0.0, 0
+        for _ in range(K):
+            with torch.cuda.stream(stream):
+                l2.zero_()  # flush L2 between steps (256 MiB > 126 MB L2)
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+            total += pool.run(ins * args.per_thread, args.batch, **kw)
+            with torch.cuda.stream(stream):
+                b.record(stream)
+            b.synchronize()
+            ms += a.elapsed_time(b)
+        return ms, total
+
+    steps(max(3, args.warmup), {})
+    steps(1, {"inputs_resident": False})  # every worker's inputs now resident in its arena
+    launches0 = mbx.lib().mbx_kernel_launch_count()
+    dev_ms, n1 = steps(args.steps, {"inputs_resident": True, "outputs_on_device": True})
+    launches = mbx.lib().mbx_kernel_launch_count() - launches0
+    e2e_ms, n2 = steps(args.steps, {})
+    t = torch.tensor([dev_ms, e2e_ms, float(n1), float(n2)], dtype=torch.float64, device=f"cuda:{local}")
+    if world > 1:
+        import torch.distributed as dist
+        mx = t.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        tot = t.clone()
+        dist.all_reduce(tot, op=dist.ReduceOp.SUM)
+        dev_ms, e2e_ms, n1, n2 = float(mx[0]), float(mx[1]), float(tot[2]), float(tot[3])
+    pool.close()
+    return {"value": n1 / (dev_ms / 1e3), "e2e": n2 / (e2e_ms / 1e3), "ms_per_step": dev_ms / args.steps,
+            "e2e_ms_per_step": e2e_ms / args.steps, "threads": T, "per_thread": args.per_thread,
+            "launches": int(launches)}
 
 
 def main():

@@ -163,6 +163,24 @@ int mbx_result_host_breakdown(const mbx_result* r, double* out4);
 /* Per non-ghost batch, in trace order: device duration in microseconds (time_batches). */
 int mbx_result_batch_times(const mbx_result* r, double* us);
 
+/* ---- throughput mode: many mini-batches on one GPU, host work on T threads ----------------
+ * T worker contexts (each: arena, plan registry, model `model` at `hidden` with parameters from
+ * zoo::make_params(param_seed)) issue into one shared device stream.  mbx_pool_run evaluates
+ * mini-batch i (hostval-encoded toks[i] / data[i]) on worker i % T with `opts`; returns the
+ * total DFG node count.  Same semantics per mini-batch as mbx_evaluate_batch. */
+typedef struct mbx_pool mbx_pool;
+int mbx_pool_create(int device, int precision, const char* model, int hidden, unsigned param_seed,
+                    int threads, mbx_pool** out);
+void mbx_pool_destroy(mbx_pool* p);
+const char* mbx_pool_last_error(const mbx_pool* p);
+void mbx_pool_set_error(const char* msg); /* error text of a failed mbx_pool_create: mbx_last_error(NULL) */
+int mbx_pool_threads(const mbx_pool* p);
+void* mbx_pool_stream(mbx_pool* p);
+mbx_model* mbx_pool_model(mbx_pool* p, int worker);
+int mbx_pool_run(mbx_pool* p, int n, int batch, const int32_t* const* toks, const int64_t* ntok,
+                 const float* const* data, const int64_t* ndata, const mbx_options* opts,
+                 int64_t* total_nodes);
+
 #ifdef __cplusplus
 }
 #endif

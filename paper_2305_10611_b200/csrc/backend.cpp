@@ -29,6 +29,16 @@ void cu_check(CUresult r, const char* what) {
   if (r != CUDA_SUCCESS) throw mbatch::Error(std::string("cuda driver error ") + std::to_string(int(r)) + " in " + what);
 }
 
+void stream_wait_own(mbx_ctx* c, const char* what) {
+  if (c->dry) return;
+  if (!c->ev_sync) {
+    cuda_check(cudaStreamSynchronize(c->stream), what);
+    return;
+  }
+  cuda_check(cudaEventRecord(c->ev_sync, c->stream), what);
+  cuda_check(cudaEventSynchronize(c->ev_sync), what);
+}
+
 float* arena_ptr(mbx_ctx* c) { return reinterpret_cast<float*>(c->base); }
 
 // Driver VMM entry points, resolved through the runtime (cudaGetDriverEntryPoint) so the library

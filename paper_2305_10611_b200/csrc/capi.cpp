@@ -116,6 +116,7 @@ int mbx_ctx_create(int device, int precision, mbx_ctx** out) {
       mbx::cuda_check(cudaSetDevice(device), "cudaSetDevice");
       mbx::cuda_check(cudaFree(nullptr), "context init");
       mbx::cuda_check(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream");
+      mbx::cuda_check(cudaEventCreateWithFlags(&c->ev_sync, cudaEventDisableTiming), "event");
       mbx::arena_init(c.get());
     }
     mbx::meta_reserve(c.get(), size_t(8) << 20);
@@ -142,7 +143,8 @@ void mbx_ctx_destroy(mbx_ctx* c) {
     if (c->tc_part) cudaFree(c->tc_part);
     if (c->gbar) cudaFree(c->gbar);
     try { mbx::arena_release(c); } catch (...) {}
-    cudaStreamDestroy(c->stream);
+    if (c->ev_sync) cudaEventDestroy(c->ev_sync);
+    if (c->owns_stream) cudaStreamDestroy(c->stream);
   } else {
     std::free(c->meta.host);
     std::free(c->in_host);
@@ -151,6 +153,7 @@ void mbx_ctx_destroy(mbx_ctx* c) {
 }
 
 const char* mbx_last_error(const mbx_ctx* c) { return c ? c->err.c_str() : g_err.c_str(); }
+void mbx_pool_set_error(const char* msg) { g_err = msg ? msg : ""; }
 
 int mbx_ctx_set_precision(mbx_ctx* c, int precision) {
   return guarded(c, [&] {

@@ -48,6 +48,8 @@ struct mbx_ctx {
   bool dry = false;  // device < 0: host bookkeeping only (offsets, traces), no CUDA calls
   int precision = MBX_PREC_FP32;
   cudaStream_t stream = nullptr;
+  bool owns_stream = true;       // false: a pool's shared stream (mbx_pool_create)
+  cudaEvent_t ev_sync = nullptr;  // waits for this context's own work only (shared streams)
   // HBM arena: one virtual-address reservation, physical chunks mapped on demand, so offsets
   // (the reference's TensorHandle::offset) are stable while the arena grows.
   CUdeviceptr base = 0;
@@ -87,6 +89,9 @@ namespace mbx {
 
 // Throws mbatch::Error on CUDA failure.
 void cuda_check(cudaError_t e, const char* what);
+// Waits for everything this context enqueued so far (an event: on a pool's shared stream it does
+// not wait for work other workers enqueue later).
+void stream_wait_own(mbx_ctx* c, const char* what);
 void cu_check(CUresult r, const char* what);
 
 float* arena_ptr(mbx_ctx* c);

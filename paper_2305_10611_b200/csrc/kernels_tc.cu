@@ -20,6 +20,7 @@
 #include <cstring>
 #include <map>
 #include <memory>
+#include <mutex>
 #include <sstream>
 #include <string>
 #include <vector>
@@ -462,6 +463,8 @@ bool levels_layout(TcState& st) {
 // Clusters of S CTAs (one CTA per SM at this shared-memory size) that can be resident at once.
 int max_active_clusters(void* fn, int S, int smem) {
   static std::map<std::pair<int, int>, int> cache;
+  static std::mutex mu;  // contexts of a pool register and launch plans concurrently
+  std::lock_guard<std::mutex> lock(mu);
   auto key = std::make_pair(S, smem);
   auto it = cache.find(key);
   if (it != cache.end()) return it->second;
@@ -945,28 +948,29 @@ void issue_levels(mbx_ctx* c, const std::vector<BatchLaunch>& Ls, size_t i, int 
   const int nctas = utiles * st->lS;
   static unsigned long long* lstamps = nullptr;
   if (stamps_enabled()) {
-    if (!lstamps) cudaMalloc(&lstamps, size_t(148) * 64 * 8 * 8);
-    cudaMemsetAsync(lstamps, 0, size_t(nctas) * 64 * 8 * 8, c->stream);
+    if (!lstamps) cudaMalloc(&lstamps, size_t(148) * 64 * 16 * 8);
+    cudaMemsetAsync(lstamps, 0, size_t(nctas) * 64 * 16 * 8, c->stream);
     a.stamps = lstamps;
   }
   void* args[] = {&a};
   cuda_check(cudaLaunchKernelExC(&cfg, st->lfn, args), "multi-level tensor-core kernel");
   if (stamps_enabled()) {
     // Profiling aid: per level, median / max over CTAs of each phase (us after the level start).
-    std::vector<unsigned long long> h(size_t(nctas) * 64 * 8);
+    std::vector<unsigned long long> h(size_t(nctas) * 64 * 16);
     cudaStreamSynchronize(c->stream);
     cudaMemcpy(h.data(), lstamps, h.size() * 8, cudaMemcpyDeviceToHost);
     std::fprintf(stderr, "levels: %d levels, %d CTAs (S=%d, NT<=%d, exchange %s)\n", n, nctas, st->lS, st->lNT,
                  st->lxch ? "L2" : "DSMEM");
-    const char* names[] = {"start", "mma_wait", "mma_done", "pushed", "reduced", "tile_end", "barrier", "converted"};
+    const char* names[] = {"start", "mma_wait", "mma_done", "pushed", "reduced", "tile_end", "barrier", "converted",
+                           "g_sync", "g_issued", "g_landed0", "mma_issued"};
     unsigned long long t00 = ~0ull;
-    for (int i2 = 0; i2 < nctas; ++i2) t00 = std::min(t00, h[size_t(i2) * 64 * 8]);
+    for (int i2 = 0; i2 < nctas; ++i2) t00 = std::min(t00, h[size_t(i2) * 64 * 16]);
     for (int lv = 0; lv < std::min(n, 64); ++lv) {
       std::fprintf(stderr, "  lv %2d b=%3d:", lv, Ls[i + size_t(lv)].b);
-      for (int k = 0; k < 8; ++k) {
+      for (int k = 0; k < 12; ++k) {
         std::vector<double> v;
         for (int i2 = 0; i2 < nctas; ++i2) {
-          const unsigned long long x = h[(size_t(i2) * 64 + lv) * 8 + k];
+          const unsigned long long x = h[(size_t(i2) * 64 + lv) * 16 + k];
           if (x) v.push_back((double(x) - double(t00)) / 1e3);
         }
         if (v.empty()) continue;

@@ -614,7 +614,7 @@ struct Executor::Impl {
     ++timing.device_launches;
     mbx::cuda_check(cudaMemcpyAsync(c->d2h_host, c->d2h_dev, total * sizeof(float), cudaMemcpyDeviceToHost, c->stream),
                     "D2H");
-    mbx::cuda_check(cudaStreamSynchronize(c->stream), "D2H sync");
+    mbx::stream_wait_own(c, "D2H sync");
     std::memcpy(dst, c->d2h_host, total * sizeof(float));
     timing.d2h_bytes += long(total * sizeof(float));
     timing.h2d_bytes += long(ranges.size() * 8);
@@ -774,7 +774,7 @@ EvalResult Executor::run() {
   auto t_host = clk::now();
   std::vector<float> buf(total, 0.0f);
   if (!I.c->dry && total > 0 && !I.opts.outputs_on_device) I.pack_to_host(ranges, buf.data(), total);
-  else if (!I.c->dry) mbx::cuda_check(cudaStreamSynchronize(I.c->stream), "final sync");
+  else if (!I.c->dry) mbx::stream_wait_own(I.c, "final sync");
 
   EvalResult res;
   size_t cursor = 0, ti = 0;

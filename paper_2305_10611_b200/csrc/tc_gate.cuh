@@ -552,8 +552,8 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_gate(const _
 #define MBX_LSTAMP_T(t, lv, i)                                                                      \
   do {                                                                                              \
     if (threadIdx.x == (t) && (lv) < 64) {                                                          \
-      P.stamps[(((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * 64 + (lv)) * 8 + \
-               (i)] = mbx_gen::global_ns();                                                         \
+      P.stamps[(((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * 64 + (lv)) * 16 + \
+               (i)] = mbx_gen::global_ns();                                                          \
     }                                                                                               \
   } while (0)
 #else
@@ -704,6 +704,7 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const
       if (warp >= 2) {
         // ---- gather + convert (warps 2-7); rowbase was filled during the previous tile ----
         named_sync(1, MBX_LGATHER);
+        MBX_LSTAMP_T(64, lv, 8);
         constexpr int kq = MBX_KC / 4;
         const int l8 = gt & 7, g0 = gt >> 3;
         const int ngroups = ((nn + 7) >> 3) * kq;  // columns past the last valid group are never read
@@ -727,6 +728,7 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const
         }
         // Every row address of this tile is issued: look up the next tile's rows now (its
         // offset tables are static), off the critical path of the next gather.
+        MBX_LSTAMP_T(64, lv, 9);
         named_sync(1, MBX_LGATHER);
         if (node0 + nt < b) fill_rowbase(L, node0 + nt, nt);
         else if (lv + 1 < P.nlevels) fill_rowbase(P.levels[lv + 1], 0, P.levels[lv + 1].nt);
@@ -735,6 +737,7 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const
 #pragma unroll 1
         for (int j = 0; j < CPR; ++j) {
           mbar_wait(&xraw[j], par);
+          if (j == 0) MBX_LSTAMP_T(64, lv, 10);
           unsigned char* xs = xsm + j * 2 * xchunk;
           for (int g = g0; g < ngroups8; g += MBX_LGATHER / 8) {
             const int m = g % kb, nb8 = g / kb;
@@ -782,6 +785,7 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const
           }
         }
         mma_commit(done);
+        MBX_LSTAMP_T(32, lv, 11);
       }
       // ---- tail operands of the nodes this rank finishes: into registers while the MMAs run ----
       float lreg[MBX_LEPT][MBX_NLOADS > 0 ? MBX_NLOADS : 1];

@@ -85,6 +85,15 @@ def lib() -> ctypes.CDLL:
         "mbx_result_batch_times": (I, [P, pD]),
         "mbx_result_host_breakdown": (I, [P, pD]),
         "mbx_ctx_stream": (P, [P]),
+        "mbx_pool_create": (I, [I, I, ctypes.c_char_p, I, ctypes.c_uint, I, ctypes.POINTER(P)]),
+        "mbx_pool_destroy": (None, [P]),
+        "mbx_pool_last_error": (ctypes.c_char_p, [P]),
+        "mbx_pool_set_error": (None, [ctypes.c_char_p]),
+        "mbx_pool_threads": (I, [P]),
+        "mbx_pool_stream": (P, [P]),
+        "mbx_pool_model": (P, [P, I]),
+        "mbx_pool_run": (I, [P, I, I, ctypes.POINTER(pI32), pI64, ctypes.POINTER(pF), pI64, ctypes.POINTER(_Opts),
+                             pI64]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -104,7 +113,9 @@ def exported_symbols() -> List[str]:
                         "mbx_model_sig_name mbx_model_plan_encoding mbx_options_default mbx_evaluate_batch "
                         "mbx_result_destroy mbx_result_outputs mbx_result_counters mbx_result_batches "
                         "mbx_result_flush_boundaries mbx_result_nodes mbx_result_timing mbx_result_batch_times "
-                        "mbx_result_host_breakdown mbx_ctx_stream").split()]
+                        "mbx_result_host_breakdown mbx_ctx_stream mbx_pool_create mbx_pool_destroy "
+                        "mbx_pool_last_error mbx_pool_set_error mbx_pool_threads mbx_pool_stream mbx_pool_model "
+                        "mbx_pool_run").split()]
 
 
 def _ptr(a: np.ndarray, ct):
@@ -382,13 +393,8 @@ class Model:
                        outputs_on_device: bool = False, ghost: bool = True, decode: bool = True,
                        trace: bool = True) -> EvalResult:
         L = lib()
-        o = _Opts()
-        L.mbx_options_default(ctypes.byref(o))
-        o.scheduler = 1 if scheduler == "agenda" else 0
-        o.gather = 1 if gather == "explicit" else 0
-        o.hoist, o.phases, o.ghost = int(hoist), int(phases), int(ghost)
-        o.record_nodes, o.time_kernels, o.time_batches = int(record_nodes), int(time_kernels), int(time_batches)
-        o.inputs_resident, o.outputs_on_device = int(inputs_resident), int(outputs_on_device)
+        o = make_options(scheduler, gather, hoist, phases, record_nodes, time_kernels, time_batches, inputs_resident,
+                         outputs_on_device, ghost)
         t = np.ascontiguousarray(toks, np.int32)
         d = np.ascontiguousarray(data, np.float32)
         r = ctypes.c_void_p()
@@ -398,6 +404,62 @@ class Model:
             return _read_result(r, batch, record_nodes, decode, trace)
         finally:
             L.mbx_result_destroy(r)
+
+
+def make_options(scheduler: str = "depth", gather: str = "fused", hoist: bool = True, phases: bool = True,
+                 record_nodes: bool = False, time_kernels: bool = False, time_batches: bool = False,
+                 inputs_resident: bool = False, outputs_on_device: bool = False, ghost: bool = True) -> _Opts:
+    o = _Opts()
+    lib().mbx_options_default(ctypes.byref(o))
+    o.scheduler = 1 if scheduler == "agenda" else 0
+    o.gather = 1 if gather == "explicit" else 0
+    o.hoist, o.phases, o.ghost = int(hoist), int(phases), int(ghost)
+    o.record_nodes, o.time_kernels, o.time_batches = int(record_nodes), int(time_kernels), int(time_batches)
+    o.inputs_resident, o.outputs_on_device = int(inputs_resident), int(outputs_on_device)
+    return o
+
+
+class Pool:
+    """Throughput mode (mbx_pool_*): `threads` worker contexts on one device sharing one stream;
+    ``run`` evaluates many independent mini-batches, mini-batch i on worker i % threads, host work
+    in parallel, device work serialised in submission order."""
+
+    def __init__(self, device: int, precision: str, model: str, hidden: int, param_seed: int, threads: int):
+        self.h = ctypes.c_void_p()
+        if lib().mbx_pool_create(device, PREC[precision], model.encode(), hidden, param_seed, threads,
+                                 ctypes.byref(self.h)):
+            raise MbatchError(lib().mbx_last_error(None).decode())
+        self.threads = threads
+
+    def close(self):
+        if self.h:
+            lib().mbx_pool_destroy(self.h)
+            self.h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def stream(self) -> int:
+        return lib().mbx_pool_stream(self.h) or 0
+
+    def run(self, inputs: Sequence[Tuple[np.ndarray, np.ndarray]], batch: int, **opts) -> int:
+        """Evaluates every (toks, data) mini-batch; returns the total DFG node count."""
+        L = lib()
+        n = len(inputs)
+        ts = [np.ascontiguousarray(t, np.int32) for t, _ in inputs]
+        ds = [np.ascontiguousarray(d, np.float32) for _, d in inputs]
+        tp = (ctypes.POINTER(ctypes.c_int32) * n)(*[_ptr(t, ctypes.c_int32) for t in ts])
+        dp = (ctypes.POINTER(ctypes.c_float) * n)(*[_ptr(d, ctypes.c_float) for d in ds])
+        nt = (ctypes.c_int64 * n)(*[t.size for t in ts])
+        nd = (ctypes.c_int64 * n)(*[d.size for d in ds])
+        o = make_options(**opts)
+        total = ctypes.c_int64(0)
+        if L.mbx_pool_run(self.h, n, batch, tp, nt, dp, nd, ctypes.byref(o), ctypes.byref(total)):
+            raise MbatchError(L.mbx_pool_last_error(self.h).decode())
+        return int(total.value)
 
 
 def _read_result(r, batch: int, record_nodes: bool, decode: bool, want_trace: bool = True) -> EvalResult:
