@@ -134,11 +134,13 @@ BatchLaunch prepare_batch(mbx_ctx* c, int plan_id, int b, const int64_t* shared_
 // Device half: enqueues the gather copies and the plan kernel (meta must be committed).
 void issue_batch(mbx_ctx* c, const BatchLaunch& L);
 
-// Persistent multi-level launches (kernels_tc.cu): if launches [i, i+n) (n >= 2) are consecutive
+// Persistent multi-level launches (kernels_tc.cu): if launches [i, i+n) (n >= 1) are consecutive
 // batches of one tensor-core gate plan over the same weights that one mbx_tc_levels launch can
-// run, stages its level table (before meta_commit) into *table and returns n; else 0.
-int plan_levels(mbx_ctx* c, const std::vector<BatchLaunch>& Ls, size_t i, size_t* table);
+// run, stages its level table (before meta_commit) into *table, sets its node-tile groups
+// (grid x) and returns n; else 0.
+int plan_levels(mbx_ctx* c, const std::vector<BatchLaunch>& Ls, size_t i, size_t* table, int* groups, int* cfg);
 // Enqueues that launch (meta committed).
-void issue_levels(mbx_ctx* c, const std::vector<BatchLaunch>& Ls, size_t i, int n, size_t table);
+void issue_levels(mbx_ctx* c, const std::vector<BatchLaunch>& Ls, size_t i, int n, size_t table, int groups,
+                  int cfg);
 
 }  // namespace mbx

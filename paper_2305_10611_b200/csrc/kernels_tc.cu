@@ -19,6 +19,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <tuple>
 #include <memory>
 #include <mutex>
 #include <sstream>
@@ -40,6 +41,7 @@ constexpr int kM = 128;
 constexpr int kRawStages = 3;  // MBX_RAW in tc_gate.cuh
 constexpr int kMaxTail = 24;
 constexpr int kSmemBudget = 227 * 1024;
+constexpr int kLevelsStaticSmem = 64 * 32 + 64;  // mbx_tc_levels: its copy of the level table
 
 // ---- tail IR: a plan's steps after the contraction as ops over per-element values --------------
 enum : int8_t { kSrcNone = 0, kSrcSlot = 1, kSrcAcc = 2, kSrcBatched = 3, kSrcShared = 4, kSrcLoad = 5 };
@@ -101,12 +103,18 @@ struct TcState {
   void* fn_fast = nullptr;    // pointwise plans: fast-activation variant (tensor-core precisions)
   bool attr_set = false;
   // Persistent multi-level variant (mbx_tc_levels): K-split ranks, maximal node tile, smem layout.
-  int lS = 0, lNT = 0, l_w_off = 0, l_x_off = 0, l_recv_off = 0, l_bar_off = 0, l_smem = 0;
-  int lxch = 0;  // 0: K ranks form a cluster (DSMEM exchange), 1: L2 exchange, no cluster
-  void* lfn = nullptr;
-  bool l_attr_set = false;
-  float* l_part = nullptr;      // lxch 1: partials buffer
-  unsigned* l_flags = nullptr;  // lxch 1: arrival counters
+  // mbx_tc_levels configurations: [0] deep — the largest K split, weight slice resident, for runs
+  // of levels; [1] wide — a small K split, many node-tile groups, for one large batch.
+  struct LevelsCfg {
+    int S = 0, NT = 0, xch = 0;  // xch 0: K ranks form a cluster (DSMEM), 1: L2 exchange
+    int CY = 1;                  // unit tiles per cluster sharing node rows by multicast
+    int w_off = 0, x_off = 0, recv_off = 0, bar_off = 0, stage_off = 0, smem = 0;
+    std::string src;
+    void* fn = nullptr;
+    bool attr_set = false;
+    float* part = nullptr;      // xch 1: partials buffer
+    unsigned* flags = nullptr;  // xch 1: arrival counters
+  } lv[2];
   unsigned l_tiles = 0;         // node tiles run so far (the counters' common base / (S-1))
   // packed-weight cache: (weight offsets, precision, upload epoch) -> device buffer
   struct Packed {
@@ -249,9 +257,23 @@ std::string gen_gate_source(const TcState& st) {
     << st.UC << "\n#define MBX_NCHUNKS " << st.nchunks << "\n#define MBX_NPIECES " << st.npieces
     << "\n#define MBX_PK0 " << st.piece_k[0] << "\n#define MBX_NLOADS " << st.prog.nloads << "\n#define MBX_NOUT "
     << st.prog.nout << "\n#define MBX_RAW " << kRawStages << "\n";
-  if (st.lS > 0)
-    o << "#define MBX_LEVELS_KERNEL 1\n#define MBX_LS " << st.lS << "\n#define MBX_LNT " << st.lNT
-      << "\n#define MBX_LXCH " << st.lxch << "\n";
+  o << gen_tail(st.prog, false);
+  o << jit::kernel_source();
+  return o.str();
+}
+
+// Source of one mbx_tc_levels configuration (same plan shape and tail as the gate kernel).
+std::string gen_levels_source(const TcState& st, int k) {
+  const TcState::LevelsCfg& L = st.lv[k];
+  std::ostringstream o;
+  if (stamps_enabled()) o << "#define MBX_STAMPS 1\n";
+  o << jit::prelude_source();
+  o << "#define MBX_LEVELS_KERNEL 1\n"
+    << "#define MBX_KC " << st.KC << "\n#define MBX_U " << st.U << "\n#define MBX_G " << st.G << "\n#define MBX_UC "
+    << st.UC << "\n#define MBX_NCHUNKS " << st.nchunks << "\n#define MBX_NPIECES " << st.npieces
+    << "\n#define MBX_PK0 " << st.piece_k[0] << "\n#define MBX_NLOADS " << st.prog.nloads << "\n#define MBX_NOUT "
+    << st.prog.nout << "\n#define MBX_LS " << L.S << "\n#define MBX_LNT " << L.NT << "\n#define MBX_LXCH " << L.xch
+    << "\n#define MBX_LCY " << L.CY << "\n";
   o << gen_tail(st.prog, false);
   o << jit::kernel_source();
   return o.str();
@@ -430,55 +452,79 @@ Layout layout_for(const TcState& st, int NT, int S, int npass) {
 // Clusters of 8 one-CTA-per-SM blocks: at least 14 are co-resident on a 148-SM B200 (GPCs of
 // 18-20 SMs); with more unit tiles than that the ranks exchange partials through L2 instead.
 // Returns false if the plan has no such layout (it then runs level by level).
-bool levels_layout(TcState& st) {
+bool levels_layout(TcState& st, int k) {
   auto al = [](int x) { return (x + 1023) / 1024 * 1024; };
   const int utiles = st.U / st.UC;
-  for (int S : {8, 4, 2, 1}) {
-    if (st.nchunks % S != 0 || utiles * S > 148) continue;
+  TcState::LevelsCfg& C = st.lv[k];
+  C = TcState::LevelsCfg{};
+  static const int cy_max = [] {
+    const char* e = std::getenv("MBX_LEVELS_CY");
+    return e ? std::max(1, std::atoi(e)) : 4;
+  }();
+  // Unit tiles sharing node rows by multicast: clusters of up to 4 along y (always co-resident:
+  // 148 SMs hold 37 of them).  Clusters of 8 ranks along z (DSMEM exchange) only when no
+  // multicast cluster is formed and at most 14 of them are needed.
+  int CY = 1;
+  while (CY * 2 <= cy_max && utiles % (CY * 2) == 0) CY *= 2;
+  // deep: largest S first (smallest resident weight slice), then the largest node tile; wide:
+  // the largest node tile first (fewest tile rounds), then the smallest S that fits with it.
+  auto try_cfg = [&](int S, int NT) {
+    if (st.nchunks % S != 0 || utiles * S > 148) return false;
     const int cpr = st.nchunks / S;
-    if (cpr > 16) continue;
-    const int xch = (S > 1 && utiles * S > 14 * 8) ? 1 : 0;
-    for (int NT : {128, 64, 32}) {
-      if (NT / S < 2 || (NT / S) * st.UC > 4 * kTcThreads) continue;
-      const int w = al(cpr * kM * st.KC * 4);
-      const int x = al(std::max(cpr * NT * st.KC * 4, NT * kM * 4));
-      const int recv = al(S > 1 && xch == 0 ? (S - 1) * (NT / S) * kM * 4 : 0);
-      const int bars = (2 * cpr + 6) * 8 + NT * 16;
-      if (w + x + recv + bars > kSmemBudget) continue;
-      st.lS = S;
-      st.lNT = NT;
-      st.lxch = xch;
-      st.l_w_off = 0;
-      st.l_x_off = w;
-      st.l_recv_off = w + x;
-      st.l_bar_off = w + x + recv;
-      st.l_smem = w + x + recv + bars;
-      return true;
-    }
+    if (cpr > 16) return false;
+    const int xch = CY > 1 ? 1 : ((S > 1 && utiles * S > 14 * 8) ? 1 : 0);
+    // tail elements per thread x operands held in registers (MBX_LEPT x MBX_NLOADS) <= 16
+    if (NT / S < 2 || (NT / S) * st.UC * std::max(1, st.prog.nloads) > 16 * kTcThreads) return false;
+    const int w = al(cpr * kM * st.KC * 4);
+    const int x = al(std::max(cpr * (NT * st.KC * 4 + 128), NT * kM * 4));  // xstride per chunk
+    const int stage = CY > 1 ? al(NT * (cpr * st.KC * 4 + 16)) : 0;      // MBX_LSROW per row
+    const int recv = al(S > 1 && xch == 0 ? (S - 1) * (NT / S) * kM * 4 : 0);
+    const int bars = (2 * cpr + 6) * 8 + NT * 16;
+    if (w + x + stage + recv + bars > kSmemBudget - kLevelsStaticSmem) return false;
+    C.S = S;
+    C.NT = NT;
+    C.xch = xch;
+    C.CY = CY;
+    C.w_off = 0;
+    C.x_off = w;
+    C.stage_off = w + x;
+    C.recv_off = w + x + stage;
+    C.bar_off = w + x + stage + recv;
+    C.smem = w + x + stage + recv + bars;
+    return true;
+  };
+  if (k == 0) {
+    for (int S : {8, 4, 2, 1})
+      for (int NT : {128, 64, 32})
+        if (try_cfg(S, NT)) return true;
+  } else {
+    for (int NT : {128, 64, 32})
+      for (int S : {1, 2, 4, 8})
+        if (try_cfg(S, NT)) return true;
   }
-  st.lS = 0;
   return false;
 }
 
-// Clusters of S CTAs (one CTA per SM at this shared-memory size) that can be resident at once.
-int max_active_clusters(void* fn, int S, int smem) {
-  static std::map<std::pair<int, int>, int> cache;
+// Clusters of (1, cy, cz) CTAs (one CTA per SM at this shared-memory size) that can be resident
+// at once.
+int max_active_clusters(void* fn, int cy, int cz, int smem) {
+  static std::map<std::tuple<void*, int, int, int>, int> cache;
   static std::mutex mu;  // contexts of a pool register and launch plans concurrently
   std::lock_guard<std::mutex> lock(mu);
-  auto key = std::make_pair(S, smem);
+  auto key = std::make_tuple(fn, cy, cz, smem);
   auto it = cache.find(key);
   if (it != cache.end()) return it->second;
-  int n = 148 / S;
+  int n = 148 / (cy * cz);
   if (fn) {
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(1, 1, unsigned(S));
+    cfg.gridDim = dim3(1, unsigned(cy), unsigned(cz));
     cfg.blockDim = dim3(kTcThreads);
     cfg.dynamicSmemBytes = size_t(smem);
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = 1;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = unsigned(S);
+    at[0].val.clusterDim.y = unsigned(cy);
+    at[0].val.clusterDim.z = unsigned(cz);
     cfg.attrs = at;
     cfg.numAttrs = 1;
     int m = 0;
@@ -488,6 +534,7 @@ int max_active_clusters(void* fn, int S, int smem) {
   cache[key] = n;
   return n;
 }
+int max_active_clusters(void* fn, int S, int smem) { return max_active_clusters(fn, 1, S, smem); }
 
 // Tiling of one launch: NT nodes per CTA (the MMA N) and S K-split ranks per tile (cluster).
 // Cost model: each CTA ingests W_tile/S + its node rows through a per-SM pipe of ~110 GB/s
@@ -558,10 +605,17 @@ void tc_prepare(mbx_ctx* c, PlanEntry& pe) {
   pe.tc_kind = -1;
   auto st = std::make_unique<TcState>();
   if (analyse(pe.exec_plan, pe.hplan, *st)) {
-    levels_layout(*st);
     st->src = gen_gate_source(*st);
     st->fn = load_kernel(c, st->src, "mbx_tc_gate");
-    if (st->lS > 0) st->lfn = load_kernel(c, st->src, "mbx_tc_levels");
+    for (int k = 0; k < 2; ++k)
+      if (levels_layout(*st, k)) {
+        if (k == 1 && st->lv[1].S == st->lv[0].S && st->lv[1].NT == st->lv[0].NT) {
+          st->lv[1].S = 0;  // same configuration as deep
+          continue;
+        }
+        st->lv[k].src = gen_levels_source(*st, k);
+        st->lv[k].fn = load_kernel(c, st->lv[k].src, "mbx_tc_levels");
+      }
     pe.tc_kind = 1;
   } else {
     *st = TcState{};
@@ -578,8 +632,10 @@ void tc_release(PlanEntry& pe) {
   auto* st = static_cast<TcState*>(pe.tc_state);
   if (!st) return;
   for (auto& p : st->packs) cudaFree(p.buf);
-  if (st->l_part) cudaFree(st->l_part);
-  if (st->l_flags) cudaFree(st->l_flags);
+  for (auto& L : st->lv) {
+    if (L.part) cudaFree(L.part);
+    if (L.flags) cudaFree(L.flags);
+  }
   delete st;
   pe.tc_state = nullptr;
 }
@@ -817,16 +873,29 @@ static bool levels_enabled() {
   return on;
 }
 
-int plan_levels(mbx_ctx* c, const std::vector<BatchLaunch>& Ls, size_t i, size_t* table) {
+// Node tiles of each level for configuration C, and the node-tile groups (grid x) a launch uses.
+static int level_tiles(const TcState::LevelsCfg& C, int utiles, const std::vector<BatchLaunch>& Ls, size_t i, int n,
+                       std::vector<int>& nts) {
+  int max_tiles = 1;
+  nts.assign(static_cast<size_t>(n), 16);
+  for (int k = 0; k < n; ++k) {
+    const int b = Ls[i + size_t(k)].b;
+    int nt = 16;
+    while (nt < b && nt < C.NT) nt *= 2;
+    nt = std::max(nt, std::min(C.NT, 2 * C.S));
+    nts[size_t(k)] = nt;
+    max_tiles = std::max(max_tiles, (b + nt - 1) / nt);
+  }
+  return std::clamp(max_tiles, 1, std::max(1, 148 / (utiles * C.S)));
+}
+
+int plan_levels(mbx_ctx* c, const std::vector<BatchLaunch>& Ls, size_t i, size_t* table, int* groups, int* cfg) {
   const BatchLaunch& L0 = Ls[i];
   const PlanEntry& pe = c->plans[L0.plan_id];
   static const bool dbg = std::getenv("MBX_LEVELS_DEBUG") != nullptr;
-  if (dbg)
-    std::fprintf(stderr, "plan_levels: plan %d b=%d tc_kind=%d prefix=%d lS=%d\n", L0.plan_id, L0.b, pe.tc_kind,
-                 pe.prefix_plan, pe.tc_state ? static_cast<TcState*>(pe.tc_state)->lS : -1);
   if (!levels_enabled() || pe.tc_kind != 1 || c->precision == MBX_PREC_FP32 || pe.prefix_plan >= 0) return 0;
   auto* st = static_cast<TcState*>(pe.tc_state);
-  if (!st || st->lS == 0 || (!st->lfn && !c->dry)) return 0;
+  if (!st || st->lv[0].S == 0 || (!st->lv[0].fn && !c->dry)) return 0;
   const size_t ns = pe.exec_plan.shared_shapes.size();
   const int64_t* sh0 = reinterpret_cast<const int64_t*>(c->meta.host + L0.shared_meta);
   size_t j = i;
@@ -838,45 +907,73 @@ int plan_levels(mbx_ctx* c, const std::vector<BatchLaunch>& Ls, size_t i, size_t
     if (!rows_vec16(c, st, pe, L)) break;
   }
   const int n = int(j - i);
-  if (dbg) std::fprintf(stderr, "plan_levels: run of %d\n", n);
-  if (n < 2) return 0;
+  if (n < 1) return 0;
   const int utiles = st->U / st->UC;
+  std::vector<int> nts;
+  int k = 0;
+  int ng = level_tiles(st->lv[0], utiles, Ls, i, n, nts);
+  if (n == 1 && st->lv[1].S > 0 && (st->lv[1].fn || c->dry)) {
+    // One batch with more node tiles than the deep configuration has groups for: go wide.
+    std::vector<int> nts1;
+    const int ng1 = level_tiles(st->lv[1], utiles, Ls, i, n, nts1);
+    const int tiles0 = (L0.b + nts[0] - 1) / nts[0];
+    if (tiles0 > ng) {
+      k = 1;
+      ng = ng1;
+      nts = nts1;
+    }
+  }
+  TcState::LevelsCfg& C = st->lv[k];
   if (!c->dry) {
-    // Every CTA must be resident at once (grid barrier between levels).
-    if (!st->l_attr_set) {
-      if (cudaFuncSetAttribute(st->lfn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget) != cudaSuccess ||
-          cudaFuncSetAttribute(st->lfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
+    // Every CTA must be resident at once (grid barrier between levels, peers' partials).
+    if (!C.attr_set) {
+      if (cudaFuncSetAttribute(C.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, C.smem) != cudaSuccess ||
+          cudaFuncSetAttribute(C.fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
         cudaGetLastError();
         return 0;
       }
-      st->l_attr_set = true;
+      C.attr_set = true;
     }
-    const int resident = st->lS > 1 && st->lxch == 0 ? max_active_clusters(st->lfn, st->lS, st->l_smem)
-                                                     : 148 / st->lS;
-    if (dbg) std::fprintf(stderr, "plan_levels: resident clusters %d, need %d\n", resident, utiles);
-    if (resident < utiles) return 0;
+    // Resident clusters vs the clusters one node-tile group needs.
+    int resident, per_group;
+    if (C.CY > 1) {
+      resident = max_active_clusters(C.fn, C.CY, 1, C.smem);
+      per_group = utiles / C.CY * C.S;
+    } else if (C.S > 1 && C.xch == 0) {
+      resident = max_active_clusters(C.fn, C.S, C.smem);
+      per_group = utiles;
+    } else {
+      resident = 148;
+      per_group = utiles * C.S;
+    }
+    if (dbg)
+      std::fprintf(stderr, "plan_levels: plan %d b=%d run %d cfg %d: resident %d, need %d x %d\n", L0.plan_id, L0.b, n,
+                   k, resident, per_group, ng);
+    if (resident < per_group) return 0;
+    ng = std::min(ng, resident / per_group);
   }
+  *groups = ng;
+  *cfg = k;
   std::vector<TcLevel> tbl(static_cast<size_t>(n));
-  for (int k = 0; k < n; ++k) {
-    const BatchLaunch& L = Ls[i + size_t(k)];
-    int nt = 16;
-    while (nt < L.b && nt < st->lNT) nt *= 2;
-    nt = std::max(nt, std::min(st->lNT, 2 * st->lS));
-    tbl[k].shared_off = meta_dev<long long>(c, L.shared_meta);
-    tbl[k].batched_off = meta_dev<long long>(c, L.batched_meta);
-    tbl[k].out_base = meta_dev<long long>(c, L.out_meta);
-    tbl[k].b = L.b;
-    tbl[k].nt = nt;
+  for (int q = 0; q < n; ++q) {
+    const BatchLaunch& L = Ls[i + size_t(q)];
+    tbl[q].shared_off = meta_dev<long long>(c, L.shared_meta);
+    tbl[q].batched_off = meta_dev<long long>(c, L.batched_meta);
+    tbl[q].out_base = meta_dev<long long>(c, L.out_meta);
+    tbl[q].b = L.b;
+    tbl[q].nt = nts[size_t(q)];
   }
   *table = meta_stage(c, tbl.data(), tbl.size() * sizeof(TcLevel));
   return n;
 }
 
-void issue_levels(mbx_ctx* c, const std::vector<BatchLaunch>& Ls, size_t i, int n, size_t table) {
+void issue_levels(mbx_ctx* c, const std::vector<BatchLaunch>& Ls, size_t i, int n, size_t table, int groups,
+                  int cfg) {
   if (c->dry) return;
   const BatchLaunch& L0 = Ls[i];
   const PlanEntry& pe = c->plans[L0.plan_id];
   auto* st = static_cast<TcState*>(pe.tc_state);
+  TcState::LevelsCfg& C = st->lv[cfg];
   const int npass = c->precision == MBX_PREC_BF16 ? 1 : 3;
   const int64_t* shared_host = reinterpret_cast<const int64_t*>(c->meta.host + L0.shared_meta);
   TcState::Packed* pk = nullptr;
@@ -900,42 +997,39 @@ void issue_levels(mbx_ctx* c, const std::vector<BatchLaunch>& Ls, size_t i, int 
     a.piece_idx[k] = st->piece_idx[k];
     a.piece_off[k] = st->piece_off[k];
   }
-  a.w_off = st->l_w_off;
-  a.x_off = st->l_x_off;
-  a.recv_off = st->l_recv_off;
-  a.bar_off = st->l_bar_off;
-  a.tmem_cols = std::max(32, st->lNT);
+  a.w_off = C.w_off;
+  a.x_off = C.x_off;
+  a.recv_off = C.recv_off;
+  a.bar_off = C.bar_off;
+  a.stage_off = C.stage_off;
+  a.tmem_cols = std::max(32, C.NT);
   a.gbar = c->gbar;
   a.gbar_base = c->gbar_count;
-  unsigned tiles = 0;
-  if (st->lxch == 1) {
-    if (!st->l_part) {
-      const size_t lloc = size_t((st->lNT / 8 + st->lS - 1) / st->lS) * 8;  // MBX_LLOC
-      const size_t part_bytes = size_t(2) * utiles * st->lS * st->lS * lloc * kM * 4;
-      cuda_check(cudaMalloc(&st->l_part, part_bytes), "levels partials");
-      cuda_check(cudaMalloc(&st->l_flags, size_t(utiles) * st->lS * 4), "levels flags");
-      cuda_check(cudaMemset(st->l_flags, 0, size_t(utiles) * st->lS * 4), "levels flags");
-      st->l_tiles = 0;
+  if (C.xch == 1) {
+    if (!C.part) {
+      const size_t ngmax = size_t(std::max(1, 148 / (utiles * C.S)));
+      const size_t lloc = size_t((C.NT / 8 + C.S - 1) / C.S) * 8;  // MBX_LLOC
+      const size_t part_bytes = size_t(2) * ngmax * utiles * C.S * C.S * lloc * kM * 4;
+      cuda_check(cudaMalloc(&C.part, part_bytes), "levels partials");
+      cuda_check(cudaMalloc(&C.flags, ngmax * utiles * C.S * 4), "levels flags");
+      cuda_check(cudaMemset(C.flags, 0, ngmax * utiles * C.S * 4), "levels flags");
     }
-    const TcLevel* tbl = reinterpret_cast<const TcLevel*>(c->meta.host + table);
-    for (int k = 0; k < n; ++k) tiles += unsigned((tbl[k].b + tbl[k].nt - 1) / tbl[k].nt);
-    a.part = st->l_part;
-    a.xflags = st->l_flags;
-    a.xflag_base = unsigned(st->lS - 1) * st->l_tiles;
+    a.part = C.part;
+    a.xflags = C.flags;
   }
   fill_loads(st->prog, a.loads);
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(1, unsigned(utiles), unsigned(st->lS));
-  cfg.blockDim = dim3(kTcThreads);
-  cfg.dynamicSmemBytes = size_t(st->l_smem);
-  cfg.stream = c->stream;
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = dim3(unsigned(groups), unsigned(utiles), unsigned(C.S));
+  lc.blockDim = dim3(kTcThreads);
+  lc.dynamicSmemBytes = size_t(C.smem);
+  lc.stream = c->stream;
   cudaLaunchAttribute attrs[2];
   int na = 0;
-  if (st->lS > 1 && st->lxch == 0) {
+  if (C.CY > 1 || (C.S > 1 && C.xch == 0)) {
     attrs[na].id = cudaLaunchAttributeClusterDimension;
     attrs[na].val.clusterDim.x = 1;
-    attrs[na].val.clusterDim.y = 1;
-    attrs[na].val.clusterDim.z = unsigned(st->lS);
+    attrs[na].val.clusterDim.y = unsigned(C.CY);
+    attrs[na].val.clusterDim.z = C.CY > 1 ? 1u : unsigned(C.S);
     ++na;
   }
   if (!fresh_pack && pdl_enabled()) {
@@ -943,9 +1037,9 @@ void issue_levels(mbx_ctx* c, const std::vector<BatchLaunch>& Ls, size_t i, int 
     attrs[na].val.programmaticStreamSerializationAllowed = 1;
     ++na;
   }
-  cfg.attrs = attrs;
-  cfg.numAttrs = unsigned(na);
-  const int nctas = utiles * st->lS;
+  lc.attrs = attrs;
+  lc.numAttrs = unsigned(na);
+  const int nctas = groups * utiles * C.S;
   static unsigned long long* lstamps = nullptr;
   if (stamps_enabled()) {
     if (!lstamps) cudaMalloc(&lstamps, size_t(148) * 64 * 16 * 8);
@@ -953,25 +1047,26 @@ void issue_levels(mbx_ctx* c, const std::vector<BatchLaunch>& Ls, size_t i, int 
     a.stamps = lstamps;
   }
   void* args[] = {&a};
-  cuda_check(cudaLaunchKernelExC(&cfg, st->lfn, args), "multi-level tensor-core kernel");
+  cuda_check(cudaLaunchKernelExC(&lc, C.fn, args), "multi-level tensor-core kernel");
   if (stamps_enabled()) {
     // Profiling aid: per level, median / max over CTAs of each phase (us after the level start).
     std::vector<unsigned long long> h(size_t(nctas) * 64 * 16);
     cudaStreamSynchronize(c->stream);
     cudaMemcpy(h.data(), lstamps, h.size() * 8, cudaMemcpyDeviceToHost);
-    std::fprintf(stderr, "levels: %d levels, %d CTAs (S=%d, NT<=%d, exchange %s)\n", n, nctas, st->lS, st->lNT,
-                 st->lxch ? "L2" : "DSMEM");
+    std::fprintf(stderr, "levels: %d levels, %d CTAs (cfg %d, %d groups, S=%d, NT<=%d, CY=%d, exchange %s)\n", n, nctas,
+                 cfg, groups, C.S, C.NT, C.CY, C.xch ? "L2" : "DSMEM");
+    // clock64 stamps: cycles since the CTA's level-0 start (each CTA its own SM clock), in us at
+    // the nominal 1.965 GHz.
     const char* names[] = {"start", "mma_wait", "mma_done", "pushed", "reduced", "tile_end", "barrier", "converted",
-                           "g_sync", "g_issued", "g_landed0", "mma_issued"};
-    unsigned long long t00 = ~0ull;
-    for (int i2 = 0; i2 < nctas; ++i2) t00 = std::min(t00, h[size_t(i2) * 64 * 16]);
+                           "g_sync", "g_issued", "g_landed0", "mma_issued", "tmem_stg", "stg_sync"};
     for (int lv = 0; lv < std::min(n, 64); ++lv) {
       std::fprintf(stderr, "  lv %2d b=%3d:", lv, Ls[i + size_t(lv)].b);
-      for (int k = 0; k < 12; ++k) {
+      for (int k = 0; k < 14; ++k) {
         std::vector<double> v;
         for (int i2 = 0; i2 < nctas; ++i2) {
           const unsigned long long x = h[(size_t(i2) * 64 + lv) * 16 + k];
-          if (x) v.push_back((double(x) - double(t00)) / 1e3);
+          const unsigned long long t0 = h[size_t(i2) * 64 * 16];
+          if (x && t0) v.push_back((double(x) - double(t0)) / 1965.0);
         }
         if (v.empty()) continue;
         std::sort(v.begin(), v.end());
@@ -980,8 +1075,7 @@ void issue_levels(mbx_ctx* c, const std::vector<BatchLaunch>& Ls, size_t i, int 
       std::fprintf(stderr, "\n");
     }
   }
-  c->gbar_count += unsigned(utiles * st->lS) * unsigned(n - 1);
-  st->l_tiles += tiles;
+  c->gbar_count += unsigned(nctas) * unsigned(n - 1);
   ++c->launches;
   ++g_launches;
 }

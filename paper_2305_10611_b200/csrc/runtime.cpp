@@ -514,12 +514,17 @@ struct Executor::Impl {
     }
     // Runs of consecutive batches of one tensor-core gate plan (e.g. every TreeLSTM internal
     // depth) become one persistent multi-level launch; their level tables are staged here.
-    std::vector<std::pair<int, size_t>> levels(launches.size(), {0, 0});
+    struct LevelsRun {
+      int n = 0, groups = 1, cfg = 0;
+      size_t table = 0;
+    };
+    std::vector<LevelsRun> levels(launches.size());
     for (size_t i = 0; i < launches.size();) {
         size_t tbl = 0;
-        const int n = mbx::plan_levels(c, launches, i, &tbl);
-        if (n >= 2) {
-          levels[i] = {n, tbl};
+        int groups = 1, cfg = 0;
+        const int n = mbx::plan_levels(c, launches, i, &tbl, &groups, &cfg);
+        if (n >= 1) {
+          levels[i] = {n, groups, cfg, tbl};
           i += size_t(n);
         } else {
           ++i;
@@ -543,14 +548,14 @@ struct Executor::Impl {
       }
       int64_t before = c->launches;
       for (size_t i = 0; i < launches.size();) {
-        const int n = levels[i].first > 0 ? levels[i].first : 1;
+        const int n = levels[i].n > 0 ? levels[i].n : 1;
         cudaEvent_t x = nullptr, y = nullptr;
         if (opts.time_batches) {
           cudaEventCreate(&x);
           cudaEventCreate(&y);
           cudaEventRecord(x, c->stream);
         }
-        if (levels[i].first > 0) mbx::issue_levels(c, launches, i, n, levels[i].second);
+        if (levels[i].n > 0) mbx::issue_levels(c, launches, i, n, levels[i].table, levels[i].groups, levels[i].cfg);
         else mbx::issue_batch(c, launches[i]);
         if (opts.time_batches) {
           cudaEventRecord(y, c->stream);

@@ -54,12 +54,12 @@ struct TcLevelsArgs {
   int npass;
   int piece_kind[2], piece_idx[2], piece_off[2];
   int w_off, x_off, recv_off, bar_off;  // dynamic shared memory layout (bytes)
+  int stage_off;                 // MBX_LCY > 1: row-major fp32 staging of the multicast node rows
   int tmem_cols;
   unsigned* gbar;                // grid barrier counter (monotonic across launches)
   unsigned gbar_base;            // its value when this launch starts
-  float* part;                   // MBX_LXCH 1: partials [2][unit tiles][S][S][MBX_LNT/S][128]
-  unsigned* xflags;              // MBX_LXCH 1: per (unit tile, rank) arrival counters (monotonic)
-  unsigned xflag_base;           // their value when this launch starts
+  float* part;                   // MBX_LXCH 1: partials [2][groups][unit tiles][S][S][MBX_LLOC][128]
+  unsigned* xflags;              // MBX_LXCH 1: per (group, unit tile, rank) arrival counters, 0 at launch
   unsigned long long* stamps;    // MBX_STAMPS builds only
   TcLoad loads[MBX_MAX_LOADS];
 };

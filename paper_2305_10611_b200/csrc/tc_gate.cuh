@@ -527,7 +527,8 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_gate(const _
 #ifdef MBX_LEVELS_KERNEL
 // mbx_tc_levels — one persistent launch for a run of consecutive batches ("levels") of the same
 // gate plan, e.g. every internal-node depth of a TreeLSTM flush.
-//   grid = (1, unit tiles, MBX_LS K-split ranks), all CTAs co-resident (one per SM).
+//   grid = (node-tile groups, unit tiles, MBX_LS K-split ranks), all CTAs co-resident (one per
+//   SM); group x takes node tiles x, x + gridDim.x, ... of every level.
 //   * The CTA's weight slice (128 gate rows x K/MBX_LS, split bf16) is bulk-copied into shared
 //     memory ONCE and reused by every level: per level only the node rows move.
 //   * Per node tile: cp.async gathers the rows of this rank's K slice straight from the arena
@@ -536,11 +537,21 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_gate(const _
 //     order (deterministic), the generated tail, outputs written batch-contiguously.
 //     MBX_LXCH 0: the ranks form a cluster; partials move by DSMEM bulk copies.
 //     MBX_LXCH 1: no cluster (any grid that fits on the SMs); partials move through an
-//                 L2-resident buffer, completion signalled by per-(tile, rank) release counters.
+//                 L2-resident buffer, completion signalled by per-(group, unit tile, rank) release
+//                 counters, which each owner resets when the launch is done with them.
+//   * MBX_LCY > 1: the MBX_LCY unit tiles of a cluster (along y) need the same node rows; each
+//     CTA bulk-copies every MBX_LCY-th row of the tile once with .multicast::cluster into all of
+//     them (L2 reads / MBX_LCY), into a row-major fp32 staging area that the next tile's copies
+//     may refill as soon as every CTA of the cluster converted it (a cluster barrier phase).
 //   * Between levels a grid barrier (monotonic counter, release / acquire): level l+1 gathers the
 //     rows level l wrote.  Every read of activations bypasses L1 (.cg): L1 is not coherent.
 //     The offset-table lookups of the next level's first tile happen before the barrier.
 #define MBX_LGATHER 192
+#ifndef MBX_LCY
+#define MBX_LCY 1  // unit tiles per cluster sharing the node rows by TMA multicast
+#endif
+#define MBX_LSLICE (MBX_LCPR * MBX_KC)        // floats of a node row in this rank's K slice
+#define MBX_LSROW (MBX_LSLICE * 4 + 16)       // staging row stride (bytes): +16 spreads the banks
 #define MBX_LCPR (MBX_NCHUNKS / MBX_LS)
 #if MBX_LXCH == 0
 #define MBX_LLOC (MBX_LNT / MBX_LS)  // nodes a rank finishes per tile: a contiguous slice
@@ -553,7 +564,7 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_gate(const _
   do {                                                                                              \
     if (threadIdx.x == (t) && (lv) < 64) {                                                          \
       P.stamps[(((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * 64 + (lv)) * 16 + \
-               (i)] = mbx_gen::global_ns();                                                          \
+               (i)] = clock64();                                                                      \
     }                                                                                               \
   } while (0)
 #else
@@ -599,9 +610,11 @@ __device__ __forceinline__ void grid_barrier(unsigned* ctr, unsigned target) {
 extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const __grid_constant__ TcLevelsArgs P) {
   using namespace mbx_gen;
   extern __shared__ __align__(1024) unsigned char smem[];
+  __shared__ TcLevel slv[64];  // the first 64 entries of the level table
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int tile_u = blockIdx.y;
   constexpr int S = MBX_LS;
+  for (int i = tid; i < min(P.nlevels, 64); i += MBX_THREADS) slv[i] = P.levels[i];
   constexpr int CPR = MBX_LCPR;
   unsigned rank = 0;
 #if MBX_LXCH == 0
@@ -615,8 +628,12 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const
   const int wchunk = MBX_M * MBX_KC * 2;
   const int wstage = wchunk * wpass;
   constexpr int xchunk = MBX_LNT * MBX_KC * 2;  // one pass of one node chunk at the maximal tile
+  // The lo pass sits 64 B past the hi pass modulo 128, so the gather's 16-byte writes of a row's
+  // even and odd quads fall in different banks; chunks are xstride apart.
+  constexpr int xlo = xchunk + 64;
+  constexpr int xstride = 2 * xchunk + 128;
   unsigned char* wsm = smem + P.w_off;          // [CPR][wstage], resident for the whole launch
-  unsigned char* xsm = smem + P.x_off;          // [CPR][2 * xchunk]; after the MMAs: stg
+  unsigned char* xsm = smem + P.x_off;          // [CPR][xstride]; after the MMAs: stg
   float* stg = reinterpret_cast<float*>(xsm);   // [nt][128] this rank's partials (LXCH 1: own slice)
   float* recv = reinterpret_cast<float*>(smem + P.recv_off);  // [S-1][nt/S][128] peers' partials
   unsigned long long* wfull = reinterpret_cast<unsigned long long*>(smem + P.bar_off);
@@ -632,7 +649,7 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const
   if (tid == 0) {
     mbar_init(wfull, 1);
     for (int j = 0; j < CPR; ++j) {
-      mbar_init(&xraw[j], MBX_LGATHER);
+      mbar_init(&xraw[j], MBX_LCY > 1 ? 1 : MBX_LGATHER);
       mbar_init(&xfull[j], MBX_LGATHER / 32);
     }
     mbar_init(done, 1);
@@ -656,37 +673,51 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const
 #if MBX_LXCH == 0
   if (S > 1) cluster_sync();  // peers' barriers initialised before any remote arrive
   else __syncthreads();
+#elif MBX_LCY > 1
+  cluster_sync();  // peers' barriers initialised before any multicast lands here
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");  // staging free for tile 0
 #else
   __syncthreads();
 #endif
   tc_fence_after();
   const unsigned tmem = *tmem_slot;
   const unsigned nctas = gridDim.x * gridDim.y * gridDim.z;
+  const int grp = blockIdx.x, ngrp = gridDim.x;
   const int gt = tid - 64;  // gather thread index (warps 2-7)
   // Offset-table lookups of one tile's node rows (static: known before the producers finish).
-  auto fill_rowbase = [&](const TcLevel& L, int node0, int nt) {
+  auto fill_rowbase = [&](const TcLevel L, int node0, int nt) {
     const int nn = min(nt, L.b - node0);
     for (int i = gt; i < nt * 2; i += MBX_LGATHER) {
       const int n = i >> 1, pc = i & 1;
       long long base = 0;
       if (n < nn && pc < MBX_NPIECES)
-        base = (P.piece_kind[pc] == 0 ? L.shared_off[P.piece_idx[pc]]
-                                      : L.batched_off[(long long)(node0 + n) * P.nb + P.piece_idx[pc]]) +
+        base = (P.piece_kind[pc] == 0 ? __ldg(L.shared_off + P.piece_idx[pc])
+                                      : __ldg(L.batched_off + (long long)(node0 + n) * P.nb + P.piece_idx[pc])) +
                P.piece_off[pc];
       rowbase[i] = base;
     }
   };
-  if (warp >= 2) fill_rowbase(P.levels[0], 0, P.levels[0].nt);
+  bool have_rb = false;  // gather threads: rowbase already holds the next tile's rows
+  auto lvl = [&](int i) -> TcLevel { return i < 64 ? slv[i] : P.levels[i]; };
+  if (warp >= 2 && grp * slv[0].nt < slv[0].b) {
+    fill_rowbase(slv[0], grp * slv[0].nt, slv[0].nt);
+    have_rb = true;
+  }
   pdl_wait();  // the first level's inputs come from earlier launches
 
-  unsigned it = 0;  // node tiles processed: parity of every per-tile mbarrier
+  unsigned it = 0;  // node tiles processed by this CTA: parity of every per-tile mbarrier
   for (int lv = 0; lv < P.nlevels; ++lv) {
-    const TcLevel& L = P.levels[lv];
+    // By value: the compiler cannot prove the arena stores leave the table alone, and a reference
+    // would re-read it from global memory inside every loop.
+    const TcLevel L = lvl(lv);
+    long long obase[MBX_NOUT];
+#pragma unroll
+    for (int k = 0; k < MBX_NOUT; ++k) obase[k] = __ldg(L.out_base + k);
     const int b = L.b, nt = L.nt;
     const int ntr = nt / S;
     MBX_LSTAMP(lv, 0);
     if (lv + 1 == P.nlevels) pdl_launch_dependents();
-    for (int node0 = 0; node0 < b; node0 += nt, ++it) {
+    for (int node0 = grp * nt; node0 < b; node0 += ngrp * nt, ++it) {
       const unsigned par = it & 1u;
       const int nn = min(nt, b - node0);
 #if MBX_LXCH == 0
@@ -701,49 +732,129 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const
 #if MBX_LXCH == 0
       if (S > 1 && tid == 0) mbar_expect_tx(rbar, unsigned((S - 1) * ntr * MBX_M * 4));
 #endif
+      // ---- tail operands of the nodes this rank finishes: into registers, in flight during the
+      // gather and the MMAs (warps 0-1 now, the gather warps once their copies are issued) ----
+      float lreg[MBX_LEPT][MBX_NLOADS > 0 ? MBX_NLOADS : 1];
+      auto load_tail_operands = [&]() {
+#pragma unroll
+        for (int t = 0; t < MBX_LEPT; ++t) {
+          const int e = tid + t * MBX_THREADS;
+          const int n = e / MBX_UC, u = e - n * MBX_UC;
+          const bool valid = n < nloc && loc_col(n) < nn;
+          const long long node = node0 + loc_col(n);
+#pragma unroll
+          for (int j = 0; j < MBX_NLOADS; ++j) {
+            const TcLoad& l = P.loads[j];
+            float v = 0.0f;
+            if (valid) {
+              const long long base = (l.kind == 1 ? __ldg(L.batched_off + node * P.nb + l.idx) : __ldg(L.shared_off + l.idx)) +
+                                     l.off + tile_u * MBX_UC + u;
+              v = __ldcg(P.arena + base);
+            }
+            lreg[t][j] = v;
+          }
+        }
+      };
+#if MBX_LCY > 1
+      // Staging of the previous tile converted by every CTA of the cluster (warps 0-1 hold no
+      // staging: they pass their arrival for this phase on at once).
+      asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+      if (warp < 2) asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+#endif
+      if (warp < 2) load_tail_operands();
       if (warp >= 2) {
-        // ---- gather + convert (warps 2-7); rowbase was filled during the previous tile ----
+        // ---- gather + convert (warps 2-7); rowbase is normally filled during the previous tile ----
+        if (!have_rb) fill_rowbase(L, node0, nt);
+        have_rb = false;
         named_sync(1, MBX_LGATHER);
         MBX_LSTAMP_T(64, lv, 8);
+#if MBX_LCY > 1
+        unsigned char* stage = smem + P.stage_off;
+        {
+          unsigned cy;
+          asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(cy));
+          if (gt == 0) mbar_expect_tx(&xraw[0], unsigned(nn * MBX_LSLICE * 4));
+          // This CTA's share of the rows, each multicast to the whole cluster in one or two runs
+          // (the slice may straddle the two concatenated pieces).
+          const int kb0 = c_begin * MBX_KC, kb1 = kb0 + MBX_LSLICE;
+          const unsigned short mask = (unsigned short)((1u << MBX_LCY) - 1u);
+          for (int n = int(cy) + MBX_LCY * gt; n < nn; n += MBX_LCY * MBX_LGATHER) {
+#pragma unroll
+            for (int pc = 0; pc < 2; ++pc) {
+              const int lo = pc == 0 ? 0 : (MBX_NPIECES > 1 ? MBX_PK0 : MBX_NCHUNKS * MBX_KC);
+              const int hi = pc == 0 ? (MBX_NPIECES > 1 ? MBX_PK0 : MBX_NCHUNKS * MBX_KC) : MBX_NCHUNKS * MBX_KC;
+              const int r0 = max(lo, kb0), r1 = min(hi, kb1);
+              if (r0 >= r1) continue;
+              const float* src = P.arena + rowbase[2 * n + pc] + (r0 - lo);
+              const unsigned dst = smem_u32(stage + n * MBX_LSROW + (r0 - kb0) * 4);
+              asm volatile(
+                  "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster "
+                  "[%0], [%1], %2, [%3], %4;" ::"r"(dst),
+                  "l"(src), "r"(unsigned((r1 - r0) * 4)), "r"(smem_u32(&xraw[0])), "h"(mask)
+                  : "memory");
+            }
+          }
+        }
+#else
+        // Lane mapping: consecutive lanes take consecutive 16-byte quads of one node row, so a
+        // warp reads whole 128-byte row segments (coalesced); quad qq of node n lands where its
+        // 8-element group's hi (even qq) or lo (odd qq) operand will live (converted in place).
         constexpr int kq = MBX_KC / 4;
-        const int l8 = gt & 7, g0 = gt >> 3;
-        const int ngroups = ((nn + 7) >> 3) * kq;  // columns past the last valid group are never read
+        const int nq = ((nn + 7) & ~7) * kq;  // columns past the last valid 8-group are never read
         const float* arena = P.arena;
 #pragma unroll 1
         for (int j = 0; j < CPR; ++j) {
           const int k = (c_begin + j) * MBX_KC;
           const int p1 = (MBX_NPIECES > 1 && k >= MBX_PK0) ? 1 : 0;
           const int kin = k - (p1 ? MBX_PK0 : 0);
-          unsigned char* xs = xsm + j * 2 * xchunk;
-          for (int g = g0; g < ngroups; g += MBX_LGATHER / 8) {
-            const int qq = g % kq, nb8 = g / kq;
-            const int n = nb8 * 8 + l8;
+          unsigned char* xs = xsm + j * xstride;
+          for (int g = gt; g < nq; g += MBX_LGATHER) {
+            const int n = g / kq, qq = g - n * kq;
             const bool valid = n < nn;
             const float* src = arena + (valid ? rowbase[2 * n + p1] + kin + qq * 4 : 0);
-            float* dst = reinterpret_cast<float*>(xs + nb8 * (MBX_KC * 16) + l8 * 16 + ((qq >> 1) << 7) +
-                                                  ((qq & 1) ? xchunk : 0));
+            float* dst = reinterpret_cast<float*>(xs + (n >> 3) * (MBX_KC * 16) + (n & 7) * 16 + ((qq >> 1) << 7) +
+                                                  ((qq & 1) ? xlo : 0));
             cp_async16(dst, src, valid);
           }
           asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&xraw[j])) : "memory");
         }
+#endif
+        load_tail_operands();
         // Every row address of this tile is issued: look up the next tile's rows now (its
         // offset tables are static), off the critical path of the next gather.
         MBX_LSTAMP_T(64, lv, 9);
         named_sync(1, MBX_LGATHER);
-        if (node0 + nt < b) fill_rowbase(L, node0 + nt, nt);
-        else if (lv + 1 < P.nlevels) fill_rowbase(P.levels[lv + 1], 0, P.levels[lv + 1].nt);
+        if (node0 + ngrp * nt < b) {
+          fill_rowbase(L, node0 + ngrp * nt, nt);
+          have_rb = true;
+        } else if (lv + 1 < P.nlevels && grp * lvl(lv + 1).nt < lvl(lv + 1).b) {
+          const TcLevel Ln = lvl(lv + 1);
+          fill_rowbase(Ln, grp * Ln.nt, Ln.nt);
+          have_rb = true;
+        }
         constexpr int kb = MBX_KC / 8;
         const int ngroups8 = ((nn + 7) >> 3) * kb;
+        const int l8 = gt & 7, g0 = gt >> 3;
 #pragma unroll 1
         for (int j = 0; j < CPR; ++j) {
+#if MBX_LCY > 1
+          if (j == 0) mbar_wait(&xraw[0], par);
+#else
           mbar_wait(&xraw[j], par);
+#endif
           if (j == 0) MBX_LSTAMP_T(64, lv, 10);
-          unsigned char* xs = xsm + j * 2 * xchunk;
+          unsigned char* xs = xsm + j * xstride;
           for (int g = g0; g < ngroups8; g += MBX_LGATHER / 8) {
             const int m = g % kb, nb8 = g / kb;
             const unsigned off = unsigned(nb8 * (MBX_KC * 16) + m * 128 + l8 * 16);
+#if MBX_LCY > 1
+            const unsigned char* srow = stage + (nb8 * 8 + l8) * MBX_LSROW + (j * MBX_KC + m * 8) * 4;
+            const float4 a = *reinterpret_cast<const float4*>(srow);
+            const float4 bq = *reinterpret_cast<const float4*>(srow + 16);
+#else
             const float4 a = *reinterpret_cast<const float4*>(xs + off);
-            const float4 bq = *reinterpret_cast<const float4*>(xs + xchunk + off);
+            const float4 bq = *reinterpret_cast<const float4*>(xs + xlo + off);
+#endif
             const float v[8] = {a.x, a.y, a.z, a.w, bq.x, bq.y, bq.z, bq.w};
             unsigned hp[4], lp[4];
 #pragma unroll
@@ -753,12 +864,21 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const
               lp[q] = pack_bf16x2(v[2 * q] - h0, v[2 * q + 1] - h1);
             }
             *reinterpret_cast<uint4*>(xs + off) = make_uint4(hp[0], hp[1], hp[2], hp[3]);
-            if (npass > 1) *reinterpret_cast<uint4*>(xs + xchunk + off) = make_uint4(lp[0], lp[1], lp[2], lp[3]);
+            if (npass > 1) *reinterpret_cast<uint4*>(xs + xlo + off) = make_uint4(lp[0], lp[1], lp[2], lp[3]);
           }
-          fence_async_smem();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&xfull[j]);
+          // One proxy fence for the whole tile once the last chunk is written (a fence per chunk
+          // costs more than the MMAs it would let start early).
+          if (j + 1 == CPR) {
+            fence_async_smem();
+            __syncwarp();
+            if (lane == 0)
+              for (int q = 0; q < CPR; ++q) mbar_arrive(&xfull[q]);
+          }
         }
+#if MBX_LCY > 1
+        // This CTA's staging is consumed: the cluster may multicast the next tile's rows into it.
+        asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+#endif
         MBX_LSTAMP_T(64, lv, 7);
       } else if (warp == 1 && lane == 0) {
         // ---- MMA issuer ----
@@ -771,9 +891,9 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const
           mbar_wait(&xfull[j], par);
           tc_fence_after();
           const unsigned wa = smem_u32(wsm + j * wstage);
-          const unsigned xa = smem_u32(xsm + j * 2 * xchunk);
+          const unsigned xa = smem_u32(xsm + j * xstride);
           const unsigned long long a_hi = make_desc(wa, sbo), b_hi = make_desc(xa, sbo);
-          const unsigned long long a_lo = make_desc(wa + wchunk, sbo), b_lo = make_desc(xa + xchunk, sbo);
+          const unsigned long long a_lo = make_desc(wa + wchunk, sbo), b_lo = make_desc(xa + xlo, sbo);
 #pragma unroll
           for (int ks = 0; ks < MBX_KC / 16; ++ks) {
             const unsigned long long step = (unsigned long long)(ks * 16);
@@ -786,26 +906,6 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const
         }
         mma_commit(done);
         MBX_LSTAMP_T(32, lv, 11);
-      }
-      // ---- tail operands of the nodes this rank finishes: into registers while the MMAs run ----
-      float lreg[MBX_LEPT][MBX_NLOADS > 0 ? MBX_NLOADS : 1];
-#pragma unroll
-      for (int t = 0; t < MBX_LEPT; ++t) {
-        const int e = tid + t * MBX_THREADS;
-        const int n = e / MBX_UC, u = e - n * MBX_UC;
-        const bool valid = n < nloc && loc_col(n) < nn;
-        const long long node = node0 + loc_col(n);
-#pragma unroll
-        for (int j = 0; j < MBX_NLOADS; ++j) {
-          const TcLoad& l = P.loads[j];
-          float v = 0.0f;
-          if (valid) {
-            const long long base = (l.kind == 1 ? L.batched_off[node * P.nb + l.idx] : L.shared_off[l.idx]) + l.off +
-                                   tile_u * MBX_UC + u;
-            v = __ldcg(P.arena + base);
-          }
-          lreg[t][j] = v;
-        }
       }
       MBX_LSTAMP(lv, 1);
       mbar_wait(done, par);
@@ -825,6 +925,7 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const
           for (int k = 0; k < 8; ++k) stg[(c0 + k) * MBX_M + row] = v[k];
         }
       }
+      MBX_LSTAMP(lv, 12);
       tc_fence_before();
       if (S > 1) {
         fence_async_smem();  // staged partials -> visible to the bulk-copy engine
@@ -858,7 +959,7 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const
 #else
       // ---- accumulators: own rank's nodes -> shared memory, the peers' -> their L2 slots ----
       // part layout: [tile parity][unit tile][destination rank][source rank][nt/S][128]
-      float* pbase = P.part + (size_t)(par * gridDim.y + tile_u) * S * S * MBX_LLOC * MBX_M;
+      float* pbase = P.part + ((size_t)(par * ngrp + grp) * gridDim.y + tile_u) * S * S * MBX_LLOC * MBX_M;
       {
         // Warp w reads TMEM lanes 32*(w%4).. (gate rows) for every other 8-column chunk.
         const int q = warp & 3, half = warp >> 2;
@@ -877,13 +978,15 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const
           }
         }
       }
+      MBX_LSTAMP(lv, 12);
       tc_fence_before();
       __syncthreads();
+      MBX_LSTAMP(lv, 13);
       if (S > 1) {
-        unsigned* flags = P.xflags + tile_u * S;
+        unsigned* flags = P.xflags + (grp * gridDim.y + tile_u) * S;
         if (tid < S && tid != int(rank)) red_release_add(flags + tid, 1u);
         MBX_LSTAMP(lv, 3);
-        if (tid == 0) spin_until(flags + rank, P.xflag_base + unsigned(S - 1) * (it + 1));
+        if (tid == 0) spin_until(flags + rank, unsigned(S - 1) * (it + 1));
         __syncthreads();
       }
       auto partial = [&](int q, int n, int col) -> float {
@@ -915,7 +1018,7 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const
           const long long node = node0 + loc_col(n);
           const int ug = tile_u * MBX_UC + u;
 #pragma unroll
-          for (int k = 0; k < MBX_NOUT; ++k) P.arena[L.out_base[k] + node * MBX_U + ug] = o[k];
+          for (int k = 0; k < MBX_NOUT; ++k) P.arena[obase[k] + node * MBX_U + ug] = o[k];
         }
       }
 #if MBX_LXCH == 0
@@ -928,8 +1031,17 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const
     if (lv + 1 < P.nlevels) grid_barrier(P.gbar, P.gbar_base + unsigned(lv + 1) * nctas);
     MBX_LSTAMP(lv, 6);
   }
+#if MBX_LCY > 1
+  // Balance the staging barrier and keep this CTA's shared memory alive until no peer can still
+  // multicast into it.
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+#endif
 #if MBX_LXCH == 0
   if (S > 1) cluster_sync();  // no peer still pushes into this CTA's shared memory
+#else
+  // Every increment of this CTA's counter happened before its last wait: reset it for the next
+  // launch (stream order makes launches sequential).
+  if (S > 1 && tid == 0 && it > 0) P.xflags[(grp * gridDim.y + tile_u) * S + rank] = 0u;
 #endif
   if (warp == 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(P.tmem_cols) : "memory");

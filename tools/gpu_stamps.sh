@@ -1,4 +1,6 @@
 set -x
 mkdir -p gpurun_out
-MBX_TC_STAMPS=1 timeout 300 python tools/probe_step.py --reps 2 > gpurun_out/stamps.log 2>&1
-grep -A8 "^levels" gpurun_out/stamps.log | tail -8
+MBX_TC_STAMPS=1 timeout 120 python tools/probe_step.py --reps 2 > gpurun_out/stamps.log 2>&1
+MBX_PDL=0 MBX_TC_STAMPS=1 timeout 120 python tools/probe_step.py --reps 2 > gpurun_out/stamps_nopdl.log 2>&1
+timeout 120 python tools/probe_step.py --reps 3 > gpurun_out/probe.log 2>&1
+MBX_PDL=0 timeout 120 python tools/probe_step.py --reps 3 > gpurun_out/probe_nopdl.log 2>&1
