@@ -160,6 +160,51 @@ def decode_hostvals(toks: np.ndarray, data: np.ndarray, count: int) -> list:
     return out
 
 
+def instance_spans(toks: np.ndarray, batch: int) -> List[Tuple[int, int, int, int]]:
+    """Per instance of a `batch`-instance hostval encoding: (tok_begin, tok_end, data_begin,
+    data_end).  Instances are encoded one after another (each: its @main instance inputs)."""
+    ends = []
+    ti, di = 0, 0
+
+    def skip():
+        nonlocal ti, di
+        k = int(toks[ti]); ti += 1
+        if k == 0:
+            di += int(toks[ti]) * int(toks[ti + 1]); ti += 2
+        elif k == 1:
+            ti += 1
+        else:
+            if k == 4:
+                ti += 1
+            n = int(toks[ti]); ti += 1
+            for _ in range(n):
+                skip()
+
+    while ti < len(toks):
+        skip()
+        ends.append((ti, di))
+    assert len(ends) % batch == 0, "encoding does not hold `batch` instances"
+    per = len(ends) // batch
+    spans, t0, d0 = [], 0, 0
+    for i in range(batch):
+        t1, d1 = ends[(i + 1) * per - 1]
+        spans.append((t0, t1, d0, d1))
+        t0, d0 = t1, d1
+    return spans
+
+
+def shard_instances(toks: np.ndarray, data: np.ndarray, batch: int, rank: int, world: int):
+    """Contiguous instance shard of a mini-batch for multi-GPU execution: rank r of
+    `world` gets instances [lo, hi) with lo = r*batch//world.  Returns (toks, data, lo, hi).
+    Instances never exchange tensors, so each shard runs on its own GPU with no collective."""
+    lo, hi = rank * batch // world, (rank + 1) * batch // world
+    sp = instance_spans(toks, batch)
+    if hi <= lo:
+        return np.zeros(0, np.int32), np.zeros(0, np.float32), lo, hi
+    return (np.ascontiguousarray(toks[sp[lo][0]:sp[hi - 1][1]]), np.ascontiguousarray(data[sp[lo][2]:sp[hi - 1][3]]),
+            lo, hi)
+
+
 def flatten_floats(v) -> np.ndarray:
     """All tensor data of a host value, depth-first (the digest order of the oracle)."""
     parts = []
