@@ -170,6 +170,10 @@ void meta_commit(mbx_ctx* c) {
     c->meta.committed = c->meta.cursor;
     return;
   }
+  if (c->copy_pending) {  // the mini-batch's inputs (copy stream) before any kernel reads them
+    cuda_check(cudaStreamWaitEvent(c->stream, c->ev_copy, 0), "input copy wait");
+    c->copy_pending = false;
+  }
   if (c->meta.cursor > c->meta.committed) {
     cuda_check(cudaMemcpyAsync(c->meta.dev + c->meta.committed, c->meta.host + c->meta.committed,
                                c->meta.cursor - c->meta.committed, cudaMemcpyHostToDevice, c->stream),

@@ -117,6 +117,8 @@ int mbx_ctx_create(int device, int precision, mbx_ctx** out) {
       mbx::cuda_check(cudaFree(nullptr), "context init");
       mbx::cuda_check(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream");
       mbx::cuda_check(cudaEventCreateWithFlags(&c->ev_sync, cudaEventDisableTiming), "event");
+      mbx::cuda_check(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking), "copy stream");
+      mbx::cuda_check(cudaEventCreateWithFlags(&c->ev_copy, cudaEventDisableTiming), "event");
       mbx::arena_init(c.get());
     }
     mbx::meta_reserve(c.get(), size_t(8) << 20);
@@ -144,6 +146,11 @@ void mbx_ctx_destroy(mbx_ctx* c) {
     if (c->gbar) cudaFree(c->gbar);
     try { mbx::arena_release(c); } catch (...) {}
     if (c->ev_sync) cudaEventDestroy(c->ev_sync);
+    if (c->copy_stream) {
+      cudaStreamSynchronize(c->copy_stream);
+      cudaStreamDestroy(c->copy_stream);
+    }
+    if (c->ev_copy) cudaEventDestroy(c->ev_copy);
     if (c->owns_stream) cudaStreamDestroy(c->stream);
   } else {
     std::free(c->meta.host);

@@ -50,6 +50,12 @@ struct mbx_ctx {
   cudaStream_t stream = nullptr;
   bool owns_stream = true;       // false: a pool's shared stream (mbx_pool_create)
   cudaEvent_t ev_sync = nullptr;  // waits for this context's own work only (shared streams)
+  // Mini-batch inputs go H2D on a copy stream while the host builds the DFG; the kernel stream
+  // waits for that copy (event) only right before the first kernel that needs it, so a shared
+  // stream is not held up by one worker's copy.
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t ev_copy = nullptr;
+  bool copy_pending = false;
   // HBM arena: one virtual-address reservation, physical chunks mapped on demand, so offsets
   // (the reference's TensorHandle::offset) are stable while the arena grows.
   CUdeviceptr base = 0;

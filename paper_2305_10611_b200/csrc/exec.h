@@ -45,8 +45,15 @@ struct Val {
   size_t size() const { return items ? items->size() : 0; }
 };
 
+// Coroutine frames of the zoo programs are allocated per call (one per block-calling function,
+// one per forked child fiber): a per-thread size-class free list makes them ~free.
+void* frame_alloc(size_t bytes);
+void frame_free(void* p, size_t bytes) noexcept;
+
 struct Task {
   struct promise_type {
+    static void* operator new(size_t n) { return frame_alloc(n); }
+    static void operator delete(void* p, size_t n) noexcept { frame_free(p, n); }
     Val value;
     std::exception_ptr exc;
     std::coroutine_handle<> continuation;

@@ -23,6 +23,46 @@
 namespace mbatch {
 namespace runtime {
 
+// ---- coroutine frame pool (exec.h) ---------------------------------------------------------
+namespace {
+struct FramePool {
+  static constexpr size_t kClass = 64, kClasses = 64;  // 64-byte classes up to 4 KiB
+  std::vector<void*> free_[kClasses];
+  ~FramePool() {
+    for (auto& v : free_)
+      for (void* p : v) ::operator delete(p);
+  }
+};
+thread_local FramePool g_frames;
+}  // namespace
+
+void* frame_alloc(size_t bytes) {
+  const size_t c = (bytes + FramePool::kClass - 1) / FramePool::kClass;
+  if (c < FramePool::kClasses) {
+    auto& v = g_frames.free_[c];
+    if (!v.empty()) {
+      void* p = v.back();
+      v.pop_back();
+      return p;
+    }
+    return ::operator new(c * FramePool::kClass);
+  }
+  return ::operator new(bytes);
+}
+
+void frame_free(void* p, size_t bytes) noexcept {
+  const size_t c = (bytes + FramePool::kClass - 1) / FramePool::kClass;
+  if (c < FramePool::kClasses) {
+    try {
+      g_frames.free_[c].push_back(p);
+      return;
+    } catch (...) {
+    }
+  }
+  ::operator delete(p);
+}
+
+
 // ---------------------------------------------------------------------------------------------
 // Host values (proj/src/pipeline.cpp:9-63)
 
@@ -256,6 +296,7 @@ struct Executor::Impl {
   ScheduleTrace trace;
   std::unordered_map<std::string, int> memo;
   std::vector<const StaticBlockInfo*> block_by_id;
+  std::vector<const kernelgen::BlockBinding*> binding_by_id;
   // input staging (pinned)
   int64_t input_base = 0;
   std::vector<std::pair<int64_t, const HostValue*>> input_tensors;
@@ -269,7 +310,12 @@ struct Executor::Impl {
     int maxid = -1;
     for (const auto& b : m.blocks) maxid = std::max(maxid, b.id);
     block_by_id.assign(maxid + 1, nullptr);
-    for (const auto& b : m.blocks) block_by_id[b.id] = &b;
+    binding_by_id.assign(maxid + 1, nullptr);
+    for (const auto& b : m.blocks) {
+      block_by_id[b.id] = &b;
+      auto it = m.kernels.binding_of_block.find(b.id);
+      if (it != m.kernels.binding_of_block.end()) binding_by_id[b.id] = &it->second;
+    }
   }
 
   ~Impl() {
@@ -313,10 +359,16 @@ struct Executor::Impl {
     for (auto& [off, hv] : input_tensors)
       std::memcpy(c->in_host + (off - input_base), hv->data.data(), hv->data.size() * sizeof(float));
     if (opts.inputs_resident) return;
-    if (!c->dry)
+    if (!c->dry) {
+      cudaStream_t cs = c->copy_stream ? c->copy_stream : c->stream;
       mbx::cuda_check(cudaMemcpyAsync(mbx::arena_ptr(c) + input_base, c->in_host, size_t(n) * sizeof(float),
-                                      cudaMemcpyHostToDevice, c->stream),
+                                      cudaMemcpyHostToDevice, cs),
                       "input H2D");
+      if (c->copy_stream) {
+        mbx::cuda_check(cudaEventRecord(c->ev_copy, cs), "input copy event");
+        c->copy_pending = true;  // the kernel stream waits at the first meta_commit
+      }
+    }
     timing.h2d_bytes += n * long(sizeof(float));
   }
 
@@ -330,10 +382,13 @@ struct Executor::Impl {
   // -- DFG construction (executor.cpp:368-443) --------------------------------------------
   int emit(Fiber& fb, int blk_id, std::initializer_list<const Val*> ins) {
     const StaticBlockInfo& blk = *block_by_id.at(blk_id);
-    const kernelgen::BlockBinding& bind = m.kernels.binding_of_block.at(blk_id);
-    std::vector<const Val*> in(ins);
-    MBATCH_CHECK(in.size() == blk.inputs.size(), "block " + std::to_string(blk_id) + ": input arity");
+    const kernelgen::BlockBinding& bind = *binding_by_id[blk_id];
+    const Val* const* in = ins.begin();
+    if (ins.size() != blk.inputs.size()) throw Error("block " + std::to_string(blk_id) + ": input arity");
     DFGNode node;
+    node.shared_ins.reserve(bind.shared_input_pos.size());
+    node.batched_ins.reserve(bind.batched_input_pos.size());
+    node.producers.reserve(bind.shared_input_pos.size() + bind.batched_input_pos.size() + 1);
     for (int pos : bind.shared_input_pos) node.shared_ins.push_back(in[pos]->t);
     for (int pos : bind.batched_input_pos) node.batched_ins.push_back(in[pos]->t);
     const bool all_shared = node.batched_ins.empty();
@@ -780,6 +835,10 @@ EvalResult Executor::run() {
   std::vector<float> buf(total, 0.0f);
   if (!I.c->dry && total > 0 && !I.opts.outputs_on_device) I.pack_to_host(ranges, buf.data(), total);
   else if (!I.c->dry) mbx::stream_wait_own(I.c, "final sync");
+  if (I.c->copy_pending) {  // inputs no kernel read: the pinned staging is reused next call
+    mbx::cuda_check(cudaEventSynchronize(I.c->ev_copy), "input copy");
+    I.c->copy_pending = false;
+  }
 
   EvalResult res;
   size_t cursor = 0, ti = 0;
