@@ -7,7 +7,7 @@ construction + depth scheduling on the host, every batch as a device launch, syn
 from the reference's zoo generators.  Default workload: TreeLSTM hidden 512, batch 64 (the
 headline config, BASELINE.json configs[1]).
 
-A step = T x R independent mini-batches (R per worker) evaluated by the native throughput pool
+A step = T x R independent mini-batches (R = 16 per worker) evaluated by the native throughput pool
 (mbx_pool_run: T host worker threads, one context each, one shared device stream) — the same use
 of the host cores as the reference arm, which runs one process per core.
   value  nodes/s with every mini-batch's inputs already resident in HBM (no input H2D, outputs
@@ -54,7 +54,7 @@ def parse_args():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--threads", type=int, default=0,
                    help="host worker threads of the throughput pool (0: min(12, cores per rank - 2))")
-    p.add_argument("--per-thread", type=int, default=4, help="mini-batches per worker thread per step")
+    p.add_argument("--per-thread", type=int, default=16, help="mini-batches per worker thread per step")
     return p.parse_args()
 
 

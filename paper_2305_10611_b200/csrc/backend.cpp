@@ -676,7 +676,8 @@ void issue_batch(mbx_ctx* c, const BatchLaunch& L) {
   }
   // tc_kind 2 (pointwise) is exact and runs in every precision; tc_kind 1 (tensor cores) only
   // when the context allows split-bf16 / bf16 contractions.
-  if (pe.tc_kind == 2 || (c->precision != MBX_PREC_FP32 && pe.tc_kind == 1)) {
+  // tc_small (bit-exact small-dense) also runs in every precision.
+  if (pe.tc_kind == 2 || pe.tc_small || (c->precision != MBX_PREC_FP32 && pe.tc_kind == 1)) {
     cuda_check(tc_launch(c, pe, L), "tensor-core plan kernel");
     ++c->launches;
     ++g_launches;

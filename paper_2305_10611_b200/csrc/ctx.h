@@ -31,6 +31,7 @@ struct PlanEntry {
   std::vector<mbatch::backend::Shape> out_shapes;
   int tm = 1, threads = 256, smem = 0, unit_chunk = 0, max_split = 1;
   int tc_kind = -1;                  // tensor-core kernel for this plan (kernels_tc.cu), -1 none
+  bool tc_small = false;             // gate plan served by the bit-exact small-dense kernel
   void* tc_state = nullptr;          // packed weights etc., owned by kernels_tc
 };
 

@@ -101,6 +101,11 @@ struct TcState {
   std::string src;            // generated kernel source
   void* fn = nullptr;         // cudaKernel_t
   void* fn_fast = nullptr;    // pointwise plans: fast-activation variant (tensor-core precisions)
+  // Few output columns (U x G <= 64): the bit-exact CUDA-core small-dense kernel instead of the
+  // tensor cores, in every precision (sfn != nullptr).
+  void* sfn = nullptr;
+  int s_npc = 0, s_smem = 0;
+  bool s_attr = false;
   bool attr_set = false;
   // Persistent multi-level variant (mbx_tc_levels): K-split ranks, maximal node tile, smem layout.
   // mbx_tc_levels configurations: [0] deep — the largest K split, weight slice resident, for runs
@@ -209,12 +214,15 @@ bool compile_epilogue(const mbatch::backend::ExecutablePlan& p, TcState& st) {
 // The tail as a device function over registers: g = accumulator gates, l = loaded input rows.
 // Gate tails (tolerance path) use the fast activations; pointwise tails the glibc-exact ones.
 // fast_pw: the pointwise tail with the fast activations (tensor-core precisions only).
-std::string gen_tail(const EpiProg& pr, bool pointwise, bool fast_pw = false) {
+// exact_gate: a gate tail with the glibc-exact activations (mbx_tail_exact, the bit-exact
+// small-dense kernel).
+std::string gen_tail(const EpiProg& pr, bool pointwise, bool fast_pw = false, bool exact_gate = false) {
   std::ostringstream o;
   o << (pointwise ? (fast_pw ? "__device__ __forceinline__ void mbx_pw_tail_fast(const float* l, float* o) {\n"
                              : "__device__ __forceinline__ void mbx_pw_tail(const float* l, float* o) {\n")
-                  : "__device__ __forceinline__ void mbx_tail(const float* g, const float* l, float* o) {\n");
-  const bool exact = pointwise && !fast_pw;
+                  : (exact_gate ? "__device__ __forceinline__ void mbx_tail_exact(const float* g, const float* l, float* o) {\n"
+                                : "__device__ __forceinline__ void mbx_tail(const float* g, const float* l, float* o) {\n"));
+  const bool exact = (pointwise && !fast_pw) || exact_gate;
   for (int s = 0; s < pr.nslots; ++s) o << "  float s" << s << " = 0.0f;\n";
   auto ref = [](const EpiSrc& s) -> std::string {
     switch (s.type) {
@@ -275,6 +283,19 @@ std::string gen_levels_source(const TcState& st, int k) {
     << st.prog.nout << "\n#define MBX_LS " << L.S << "\n#define MBX_LNT " << L.NT << "\n#define MBX_LXCH " << L.xch
     << "\n#define MBX_LCY " << L.CY << "\n";
   o << gen_tail(st.prog, false);
+  o << jit::kernel_source();
+  return o.str();
+}
+
+// Source of the bit-exact small-dense kernel (plans with few output columns, e.g. a classifier).
+std::string gen_small_source(const TcState& st, int npc) {
+  std::ostringstream o;
+  o << jit::prelude_source();
+  o << "#define MBX_SMALL_KERNEL 1\n"
+    << "#define MBX_KC 16\n#define MBX_K " << st.K << "\n#define MBX_U " << st.U << "\n#define MBX_G " << st.G
+    << "\n#define MBX_NPIECES " << st.npieces << "\n#define MBX_PK0 " << st.piece_k[0] << "\n#define MBX_NLOADS "
+    << st.prog.nloads << "\n#define MBX_NOUT " << st.prog.nout << "\n#define MBX_SNPC " << npc << "\n";
+  o << gen_tail(st.prog, false, false, true);
   o << jit::kernel_source();
   return o.str();
 }
@@ -605,6 +626,14 @@ void tc_prepare(mbx_ctx* c, PlanEntry& pe) {
   pe.tc_kind = -1;
   auto st = std::make_unique<TcState>();
   if (analyse(pe.exec_plan, pe.hplan, *st)) {
+    if (st->U * st->G <= 64 && st->K * st->U * st->G <= 16384 && st->K % 8 == 0) {
+      // Nodes per CTA: enough CTAs to spread a batch over the SMs (chains are latency-bound).
+      st->s_npc = std::max(1, std::min({kTcThreads / st->U, 8, (160 * 1024 - st->K * st->U * st->G * 4) / (st->K * 4)}));
+      st->s_smem = (st->K * st->U * st->G + st->s_npc * st->K) * 4;
+      const std::string ssrc = gen_small_source(*st, st->s_npc);
+      st->sfn = load_kernel(c, ssrc, "mbx_small_dense");
+      pe.tc_small = true;
+    }
     st->src = gen_gate_source(*st);
     st->fn = load_kernel(c, st->src, "mbx_tc_gate");
     for (int k = 0; k < 2; ++k)
@@ -724,6 +753,35 @@ static cudaError_t ensure_pack(mbx_ctx* c, TcState* st, const int64_t* shared_ho
 
 cudaError_t tc_launch(mbx_ctx* c, const PlanEntry& pe, const BatchLaunch& L) {
   auto* st = static_cast<TcState*>(pe.tc_state);
+  if (pe.tc_small && st->sfn) {
+    SmallArgs a{};
+    a.arena = arena_ptr(c);
+    a.shared_off = meta_dev<long long>(c, L.shared_meta);
+    a.batched_off = meta_dev<long long>(c, L.batched_meta);
+    a.out_base = meta_dev<long long>(c, L.out_meta);
+    a.b = L.b;
+    a.nb = int(pe.exec_plan.batched_shapes.size());
+    for (int i = 0; i < 2; ++i) {
+      a.piece_kind[i] = st->piece_kind[i];
+      a.piece_idx[i] = st->piece_idx[i];
+      a.piece_off[i] = st->piece_off[i];
+    }
+    for (int g = 0; g < st->G; ++g) a.w_idx[g] = st->w_shared[size_t(g)];
+    a.nloads = st->prog.nloads;
+    fill_loads(st->prog, a.loads);
+    if (!st->s_attr) {
+      cudaError_t e = cudaFuncSetAttribute(st->sfn, cudaFuncAttributeMaxDynamicSharedMemorySize, st->s_smem);
+      if (e != cudaSuccess) return e;
+      st->s_attr = true;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(unsigned((L.b + st->s_npc - 1) / st->s_npc));
+    cfg.blockDim = dim3(kTcThreads);
+    cfg.dynamicSmemBytes = size_t(st->s_smem);
+    cfg.stream = c->stream;
+    void* args[] = {&a};
+    return cudaLaunchKernelExC(&cfg, st->sfn, args);
+  }
   if (pe.tc_kind == 2) {
     PwArgs a{};
     a.arena = arena_ptr(c);
@@ -893,7 +951,8 @@ int plan_levels(mbx_ctx* c, const std::vector<BatchLaunch>& Ls, size_t i, size_t
   const BatchLaunch& L0 = Ls[i];
   const PlanEntry& pe = c->plans[L0.plan_id];
   static const bool dbg = std::getenv("MBX_LEVELS_DEBUG") != nullptr;
-  if (!levels_enabled() || pe.tc_kind != 1 || c->precision == MBX_PREC_FP32 || pe.prefix_plan >= 0) return 0;
+  if (!levels_enabled() || pe.tc_kind != 1 || pe.tc_small || c->precision == MBX_PREC_FP32 || pe.prefix_plan >= 0)
+    return 0;
   auto* st = static_cast<TcState*>(pe.tc_state);
   if (!st || st->lv[0].S == 0 || (!st->lv[0].fn && !c->dry)) return 0;
   const size_t ns = pe.exec_plan.shared_shapes.size();

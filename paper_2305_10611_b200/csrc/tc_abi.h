@@ -64,6 +64,18 @@ struct TcLevelsArgs {
   TcLoad loads[MBX_MAX_LOADS];
 };
 
+struct SmallArgs {
+  float* arena;
+  const long long* shared_off;
+  const long long* batched_off;
+  const long long* out_base;
+  int b, nb;
+  int piece_kind[2], piece_idx[2], piece_off[2];
+  int w_idx[4];  // shared-input index of each gate weight
+  int nloads;
+  TcLoad loads[MBX_MAX_LOADS];
+};
+
 struct PwArgs {
   float* arena;
   const long long* shared_off;

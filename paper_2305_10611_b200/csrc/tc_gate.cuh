@@ -967,15 +967,12 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const
         for (int ch = half; ch < (nn + 7) >> 3; ch += 2) {
           float v[8];
           tmem_ld8(tmem + (unsigned(q * 32) << 16) + unsigned(ch * 8), v);
+          // Every rank's slice, this rank's own included, goes to the L2 buffer: the reduction
+          // then reads all S partials the same way (uniform, branch-free, all loads in flight).
           const int r = ch % S, m0 = (ch / S) * 8;
-          float* dst = r == int(rank) ? stg + m0 * MBX_M + row : pbase + ((size_t)(r * S + int(rank)) * MBX_LLOC + m0) * MBX_M + row;
-          if (r == int(rank)) {
+          float* dst = pbase + ((size_t)(r * S + int(rank)) * MBX_LLOC + m0) * MBX_M + row;
 #pragma unroll
-            for (int k = 0; k < 8; ++k) dst[k * MBX_M] = v[k];
-          } else {
-#pragma unroll
-            for (int k = 0; k < 8; ++k) __stcg(dst + k * MBX_M, v[k]);
-          }
+          for (int k = 0; k < 8; ++k) __stcg(dst + k * MBX_M, v[k]);
         }
       }
       MBX_LSTAMP(lv, 12);
@@ -990,31 +987,39 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const
         __syncthreads();
       }
       auto partial = [&](int q, int n, int col) -> float {
-        return q == int(rank) ? stg[n * MBX_M + col]
-                              : __ldcg(pbase + ((size_t)(int(rank) * S + q) * MBX_LLOC + n) * MBX_M + col);
+        return __ldcg(pbase + ((size_t)(int(rank) * S + q) * MBX_LLOC + n) * MBX_M + col);
       };
 #endif
       MBX_LSTAMP(lv, 4);
       // ---- sum the partials in rank order, run the tail, write the outputs ----
+      // Every partial of every element is read before the first output store: through generic
+      // pointers a store would order all later loads behind it (one L2 round trip per element).
+      float gsum[MBX_LEPT][MBX_G];
+#pragma unroll
+      for (int t = 0; t < MBX_LEPT; ++t) {
+        const int e = tid + t * MBX_THREADS;
+        const int n = e / MBX_UC, u = e - n * MBX_UC;
+        const bool valid = n < nloc && loc_col(n) < nn;
+#pragma unroll
+        for (int gi = 0; gi < MBX_G; ++gi) {
+          const int col = gi * MBX_UC + u;
+          float acc = 0.0f;
+#pragma unroll
+          float pv[S];
+#pragma unroll
+          for (int q = 0; q < S; ++q) pv[q] = partial(q, valid ? n : 0, col);  // invalid: a harmless row
+#pragma unroll
+          for (int q = 0; q < S; ++q) acc = q == 0 ? pv[q] : acc + pv[q];
+          gsum[t][gi] = acc;
+        }
+      }
 #pragma unroll
       for (int t = 0; t < MBX_LEPT; ++t) {
         const int e = tid + t * MBX_THREADS;
         const int n = e / MBX_UC, u = e - n * MBX_UC;
         if (n < nloc && loc_col(n) < nn) {
-          float g[MBX_G];
-#pragma unroll
-          for (int gi = 0; gi < MBX_G; ++gi) {
-            const int col = gi * MBX_UC + u;
-            float acc = 0.0f;
-#pragma unroll
-            for (int q = 0; q < S; ++q) {
-              const float v = partial(q, n, col);
-              acc = q == 0 ? v : acc + v;
-            }
-            g[gi] = acc;
-          }
           float o[MBX_NOUT];
-          mbx_tail(g, lreg[t], o);
+          mbx_tail(gsum[t], lreg[t], o);
           const long long node = node0 + loc_col(n);
           const int ug = tile_u * MBX_UC + u;
 #pragma unroll
@@ -1047,6 +1052,88 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(P.tmem_cols) : "memory");
 }
 #endif  // MBX_LEVELS_KERNEL
+
+#ifdef MBX_SMALL_KERNEL
+// mbx_small_dense — gate plans with few output columns (U x G <= 64, e.g. the TreeLSTM
+// classifier relu(h . c_wt + cbias), 512 x 8): tensor-core tiles would be 90% padding.  CUDA
+// cores, bit-exact: every output is the reference's sequential chain acc = acc + x[p] * w[p][j]
+// over p ascending with separately rounded multiply and add (proj/src/backend.cpp:116-131), the
+// tail with the glibc-exact activations.  CTA = MBX_SNPC nodes; W (all gates) and the nodes'
+// rows staged in shared memory; thread = (node, unit), G independent chains.
+extern "C" __global__ void __launch_bounds__(MBX_THREADS) mbx_small_dense(const __grid_constant__ SmallArgs P) {
+  extern __shared__ __align__(16) float sms[];
+  constexpr int K = MBX_K, U = MBX_U, G = MBX_G, NPC = MBX_SNPC;
+  float* ws = sms;              // [G][K][U]
+  float* xs = sms + G * K * U;  // [NPC][K]
+  const int tid = threadIdx.x;
+  const int node0 = blockIdx.x * NPC;
+  const int nn = min(NPC, P.b - node0);
+  // Weight bases into registers first: through generic pointers the compiler cannot prove the
+  // shared-memory stores leave the offset table alone and would re-read it every iteration.
+  const float* wsrc[G];
+#pragma unroll
+  for (int g = 0; g < G; ++g) wsrc[g] = P.arena + __ldg(P.shared_off + P.w_idx[g]);
+  // cp.async: every copy in flight at once (a load -> store loop through registers would be
+  // serialised by the possible aliasing of the generic pointers).
+#pragma unroll
+  for (int g = 0; g < G; ++g)
+    for (int r = tid; r < K * U; r += MBX_THREADS) mbx_gen::cp_async4(ws + g * K * U + r, wsrc[g] + r, true);
+  __shared__ long long rowb[NPC][2];
+  for (int i = tid; i < nn * 2; i += MBX_THREADS) {
+    const int n = i >> 1, pc = i & 1;
+    long long base = 0;
+    if (pc < MBX_NPIECES)
+      base = (P.piece_kind[pc] == 0 ? P.shared_off[P.piece_idx[pc]]
+                                    : P.batched_off[(long long)(node0 + n) * P.nb + P.piece_idx[pc]]) +
+             P.piece_off[pc] - (pc ? MBX_PK0 : 0);
+    rowb[n][pc] = base;
+  }
+  __syncthreads();
+  for (int i = tid; i < nn * K; i += MBX_THREADS) {
+    const int n = i / K, k = i - n * K;
+    const int pc = (MBX_NPIECES > 1 && k >= MBX_PK0) ? 1 : 0;
+    mbx_gen::cp_async4(xs + i, P.arena + rowb[n][pc] + k, true);
+  }
+  mbx_gen::cp_async_commit();
+  mbx_gen::cp_async_wait<0>();
+  __syncthreads();
+  for (int t = tid; t < nn * U; t += MBX_THREADS) {
+    const int n = t / U, u = t - n * U;
+    const float* x = xs + n * K;
+    float g[G];
+#pragma unroll
+    for (int gi = 0; gi < G; ++gi) g[gi] = 0.0f;
+    // Blocks of 8 p: operands and products first (independent), then the 8 dependent adds of
+    // each chain in p order — the add chain is the only serial part.
+    static_assert(K % 8 == 0, "K multiple of 8");
+    for (int p0 = 0; p0 < K; p0 += 8) {
+      float xv[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) xv[q] = x[p0 + q];
+#pragma unroll
+      for (int gi = 0; gi < G; ++gi) {
+        float pr[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) pr[q] = mbx_libm::fmul(xv[q], ws[(gi * K + p0 + q) * U + u]);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) g[gi] = mbx_libm::fadd(g[gi], pr[q]);
+      }
+    }
+    const long long node = node0 + n;
+    float l[MBX_NLOADS > 0 ? MBX_NLOADS : 1];
+#pragma unroll
+    for (int j = 0; j < MBX_NLOADS; ++j) {
+      const TcLoad& d = P.loads[j];
+      const long long base = d.kind == 1 ? P.batched_off[node * P.nb + d.idx] : P.shared_off[d.idx];
+      l[j] = P.arena[base + d.off + u];
+    }
+    float o[MBX_NOUT];
+    mbx_tail_exact(g, l, o);
+#pragma unroll
+    for (int k = 0; k < MBX_NOUT; ++k) P.arena[P.out_base[k] + node * U + u] = o[k];
+  }
+}
+#endif  // MBX_SMALL_KERNEL
 
 #ifdef MBX_POINTWISE_KERNEL
 // One thread per (node, element); the offset-table lookups are shared by the E elements of a
