@@ -700,7 +700,9 @@ void issue_batch(mbx_ctx* c, const BatchLaunch& L) {
     v.unit_chunk = pe.hplan.unit;
   }
   v.threads = pe.threads;
-  v.temp_floats_total = pe.smem / 4;
+  // Temporaries of the tile this launch actually uses (pe.smem is sized for the largest tile):
+  // the rest of shared memory stages weights.
+  v.temp_floats_total = int(std::max<int64_t>(1, pe.hplan.temp_floats)) * v.tm;
   v.wst_floats = vm_weight_stage_floats(v.temp_floats_total);
   v.smem_bytes = (((v.temp_floats_total + 3) & ~3) + v.wst_floats) * 4;
   v.shared_off = meta_dev<int64_t>(c, L.shared_meta);

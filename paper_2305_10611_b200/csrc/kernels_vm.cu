@@ -83,6 +83,8 @@ __device__ __forceinline__ float* temp_ptr(const Ctx& c, int step, int t) {
 // batched (per node).
 // Threads [tbase, tbase + tcount) of the CTA take part (the weights of a FusedDense run side by
 // side on disjoint thread groups).
+constexpr int kMaxCPT = 8;  // output elements per thread in the staged shared-weight path
+
 __device__ void dense_range(const Ctx& c, const DRef& a, const DRef& w, int s, int out_ld,
                             int out_col0, int j0, int j1, int tbase = 0, int tcount = -1, int gi = 0, int ngroups = 1) {
   const int m = a.rows_r, k = a.cols_r, n = w.cols_r;
@@ -91,11 +93,14 @@ __device__ void dense_range(const Ctx& c, const DRef& a, const DRef& w, int s, i
   const int tid = int(threadIdx.x) - tbase;
   if (ncr <= 0 || tid < 0 || tid >= tcount) return;
   const int per_group = (c.wst_floats / ngroups) & ~3;
-  if (w.kind == kRefShared && m * ncr <= tcount && per_group >= (ncr + m * c.nn) * 16) {
-    // Shared weights, at most one output column per thread: stage W[:, j0:j1] through shared
-    // memory in passes of KB rows, every row of a pass in flight at once (cp.async), then run
-    // the strictly sequential accumulation from shared memory.  Same arithmetic and order as
-    // the direct path below.
+  // Output elements (row i, column jj) per thread: up to kMaxCPT, all accumulated side by side.
+  const int cpt = (m * ncr + tcount - 1) / tcount;
+  if (w.kind == kRefShared && cpt <= kMaxCPT && per_group >= (ncr + m * c.nn) * 16) {
+    // Shared weights: stage W[:, j0:j1] through shared memory in passes of KB rows, every row of
+    // a pass in flight at once (cp.async), then run each output's strictly sequential
+    // accumulation (p ascending, separate multiply and add) from shared memory.  A thread owns
+    // up to kMaxCPT output elements (elements e = tid + q * tcount) for every tile node, so the
+    // chains of one thread are independent (ILP) and wide FusedDense steps use every thread.
     const float* W = ref_ptr(c, w, 0) + j0;
     float* ws = c.wst + gi * per_group;
     // Pass of KB rows: W rows [KB][ncr] then the A rows of every tile node [nn][m][KB].
@@ -103,11 +108,20 @@ __device__ void dense_range(const Ctx& c, const DRef& a, const DRef& w, int s, i
     const int KB = min(k, (per_group / (ncr + arow)) & ~3);
     float* as = ws + KB * ncr;
     const bool vec = (ncr % 4 == 0) && (n % 4 == 0) && ((reinterpret_cast<uintptr_t>(W) & 15) == 0);
-    const bool active = tid < m * ncr;
-    const int i = active ? tid / ncr : 0, jj = active ? tid % ncr : 0;
-    float acc[kMaxTM];
+    int ei[kMaxCPT], ej[kMaxCPT];
+    bool act[kMaxCPT];
 #pragma unroll
-    for (int t = 0; t < kMaxTM; ++t) acc[t] = 0.0f;
+    for (int q = 0; q < kMaxCPT; ++q) {
+      const int e = tid + q * tcount;
+      act[q] = q < cpt && e < m * ncr;
+      ei[q] = act[q] ? e / ncr : 0;
+      ej[q] = act[q] ? e % ncr : 0;
+    }
+    float acc[kMaxCPT][kMaxTM];
+#pragma unroll
+    for (int q = 0; q < kMaxCPT; ++q)
+#pragma unroll
+      for (int t = 0; t < kMaxTM; ++t) acc[q][t] = 0.0f;
     for (int p0 = 0; p0 < k; p0 += KB) {
       const int kb = min(KB, k - p0);
       if (vec) {
@@ -131,30 +145,34 @@ __device__ void dense_range(const Ctx& c, const DRef& a, const DRef& w, int s, i
       }
       asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
       group_sync(gi, tcount);
-      if (active) {
-        const float* wc = ws + jj;
+#pragma unroll
+      for (int q = 0; q < kMaxCPT; ++q) {
+        if (!act[q]) continue;
+        const float* wc = ws + ej[q];
         if (c.nn == 1) {  // one node (the hoisted shared prefix): a single dependent chain
-          const float* a0 = as + i * kb;
-          float acc0 = acc[0];
+          const float* a0 = as + ei[q] * kb;
+          float acc0 = acc[q][0];
 #pragma unroll 8
           for (int p = 0; p < kb; ++p) acc0 = fadd(acc0, fmul(a0[p], wc[p * ncr]));
-          acc[0] = acc0;
+          acc[q][0] = acc0;
         } else {
 #pragma unroll 4
           for (int p = 0; p < kb; ++p) {
             const float wv = wc[p * ncr];
 #pragma unroll
             for (int t = 0; t < kMaxTM; ++t)
-              if (t < c.nn) acc[t] = fadd(acc[t], fmul(as[(t * m + i) * kb + p], wv));
+              if (t < c.nn) acc[q][t] = fadd(acc[q][t], fmul(as[(t * m + ei[q]) * kb + p], wv));
           }
         }
       }
       group_sync(gi, tcount);
     }
-    if (active) {
+#pragma unroll
+    for (int q = 0; q < kMaxCPT; ++q) {
+      if (!act[q]) continue;
 #pragma unroll
       for (int t = 0; t < kMaxTM; ++t)
-        if (t < c.nn) temp_ptr(c, s, t)[i * out_ld + out_col0 + j0 + jj] = acc[t];
+        if (t < c.nn) temp_ptr(c, s, t)[ei[q] * out_ld + out_col0 + j0 + ej[q]] = acc[q][t];
     }
     return;
   }
