@@ -779,6 +779,13 @@ cudaError_t tc_launch(mbx_ctx* c, const PlanEntry& pe, const BatchLaunch& L) {
     cfg.blockDim = dim3(kTcThreads);
     cfg.dynamicSmemBytes = size_t(st->s_smem);
     cfg.stream = c->stream;
+    cudaLaunchAttribute at[1];
+    if (pdl_enabled()) {
+      at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[0].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+    }
     void* args[] = {&a};
     return cudaLaunchKernelExC(&cfg, st->sfn, args);
   }
@@ -799,6 +806,13 @@ cudaError_t tc_launch(mbx_ctx* c, const PlanEntry& pe, const BatchLaunch& L) {
     cfg.gridDim = dim3(blocks);
     cfg.blockDim = dim3(256);
     cfg.stream = c->stream;
+    cudaLaunchAttribute at[1];
+    if (pdl_enabled()) {
+      at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[0].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+    }
     void* args[] = {&a};
     // FP32 contexts: glibc-exact activations (bit-identical to the reference); the tensor-core
     // precisions use the fast ones, as their gate tails do.

@@ -1068,6 +1068,9 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS) mbx_small_dense(const 
   const int tid = threadIdx.x;
   const int node0 = blockIdx.x * NPC;
   const int nn = min(NPC, P.b - node0);
+  // PDL: every input (weights included: they may be a hoisted prefix's output) after the wait.
+  mbx_gen::pdl_wait();
+  mbx_gen::pdl_launch_dependents();
   // Weight bases into registers first: through generic pointers the compiler cannot prove the
   // shared-memory stores leave the offset table alone and would re-read it every iteration.
   const float* wsrc[G];
@@ -1140,6 +1143,9 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS) mbx_small_dense(const 
 // node.  FAST selects the fast activations (tensor-core precisions).
 template <bool FAST>
 __device__ __forceinline__ void mbx_pointwise_body(const PwArgs& P) {
+  // PDL: launched while the predecessor drains; its outputs are read only after the wait.
+  mbx_gen::pdl_wait();
+  mbx_gen::pdl_launch_dependents();
   const long long total = (long long)P.b * MBX_PW_E;
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
        idx += (long long)gridDim.x * blockDim.x) {
