@@ -55,6 +55,8 @@ def parse_args():
     p.add_argument("--threads", type=int, default=0,
                    help="host worker threads of the throughput pool (0: min(12, cores per rank - 2))")
     p.add_argument("--per-thread", type=int, default=16, help="mini-batches per worker thread per step")
+    p.add_argument("--no-other-configs", action="store_true",
+                   help="skip the per-config latency table of the other BASELINE configs")
     return p.parse_args()
 
 
@@ -396,12 +398,53 @@ def run_ours(args):
                                   "per_sig": {sigs[s]: v["us"] / K for s, v in per_sig.items()}},
         "clocks": clk,
     }
+    if world == 1 and not args.no_other_configs:
+        line["other_configs"] = other_configs(mbx, torch, local)
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args, nodes)
     print(json.dumps(line))
     if dist:
         dist.barrier()
         dist.destroy_process_group()
+
+
+# The other BASELINE.json configs with the precision SURVEY §8a assigns them (rel 1e-5 -> the
+# bit-exact FP32 path, rel 1e-3 -> bf16x3 tensor cores).  Parity for all of them: tests/.
+OTHER_CONFIGS = [("treelstm", 256, 8, "fp32"), ("treelstm", 512, 8, "bf16x3"), ("mvrnn", 128, 64, "fp32"),
+                 ("birnn", 512, 64, "bf16x3"), ("nestedrnn", 512, 64, "bf16x3"), ("nestedrnn", 512, 8, "bf16x3")]
+
+
+def other_configs(mbx, torch, local, reps=5):
+    """ms per mini-batch (one at a time on one context, CUDA events around each call, inputs
+    resident) and nodes/s for the other BASELINE configs."""
+    out = {}
+    for model, hidden, batch, prec in OTHER_CONFIGS:
+        ctx = mbx.Context(local, prec)
+        m = mbx.Model(ctx, model, hidden)
+        m.make_params(1)
+        toks, data = m.make_inputs(1, batch)
+        stream = torch.cuda.ExternalStream(ctx.stream(), device=local)
+        r = None
+        for _ in range(2):
+            r = m.evaluate_batch(toks, data, batch, record_nodes=False, decode=False, trace=False)
+        ms = []
+        for _ in range(reps):
+            with torch.cuda.stream(stream):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+            r = m.evaluate_batch(toks, data, batch, record_nodes=False, decode=False, trace=False,
+                                 inputs_resident=True, outputs_on_device=True, time_kernels=True)
+            with torch.cuda.stream(stream):
+                b.record(stream)
+            b.synchronize()
+            ms.append(a.elapsed_time(b))
+        best = min(ms)
+        out[f"{model}-h{hidden}-b{batch}-{prec}"] = {
+            "ms_per_minibatch": best, "nodes": r.trace.total_nodes, "nodes_per_s": r.trace.total_nodes / (best / 1e3),
+            "device_us": r.timing.device_span_us, "host_us": r.timing.host_dfg_us, "batches": r.trace.kernel_launches}
+        m.close()
+        ctx.close()
+    return out
 
 
 def run_pool(args, mbx, torch, local, rank, world, nodes, l2):

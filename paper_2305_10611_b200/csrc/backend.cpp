@@ -427,6 +427,98 @@ bool hoist_shared_prefix(const ExecutablePlan& p, ExecutablePlan& prefix, Execut
   return true;
 }
 
+
+// Splits `p` at the first step that needs a whole row of an earlier step (the dense over the
+// mixed hidden state and the argmax of NestedRNN's decision cell, zoo.cpp:145-174): every step
+// before it is column-local, so the head can spread over CTAs by columns, which the plan as a
+// whole cannot.  Head outputs: the original outputs it computes, then the boundary temporaries
+// the tail reads (each once); tail inputs: the original batched inputs, then those temporaries.
+// Returns false when no split point leaves a head with a contraction.
+bool split_at_reduction(const ExecutablePlan& p, ExecutablePlan& head, ExecutablePlan& tail, std::vector<int>& head_orig_out,
+                        std::vector<int>& head_bnd_step, std::vector<int>& tail_in_src, std::vector<int>& tail_orig_out) {
+  const size_t n = p.steps.size();
+  if (p.ghost || n < 3) return false;
+  auto refs_of = [&](const PlanStep& st) {
+    std::vector<PlanRef> r = st.ins;
+    for (auto& l : st.chain)
+      if (l.rhs) r.push_back(*l.rhs);
+    return r;
+  };
+  auto is_dense = [](const PlanStep& st) {
+    return st.kind == PlanStep::Kind::kFusedDense || (st.kind == PlanStep::Kind::kOp && st.op == OpCode::kDense);
+  };
+  // Split point: the first dense whose row operand is a temporary and whose width differs from the
+  // plan's unit (the head's first dense's width), i.e. a reduction over a whole computed row.
+  int first_dense = -1;
+  for (size_t s = 0; s < n; ++s)
+    if (is_dense(p.steps[s])) { first_dense = int(s); break; }
+  if (first_dense < 0) return false;
+  int cut = -1;
+  for (size_t s = size_t(first_dense) + 1; s < n; ++s) {
+    const PlanStep& st = p.steps[s];
+    if (is_dense(st) && st.ins[0].kind == PlanRef::Kind::kTemp) { cut = int(s); break; }
+    if (st.kind == PlanStep::Kind::kOp && st.op == OpCode::kArgmax) { cut = int(s); break; }
+  }
+  if (cut <= first_dense) return false;
+  head = ExecutablePlan{};
+  head.shared_shapes = p.shared_shapes;
+  head.batched_shapes = p.batched_shapes;
+  for (int s = 0; s < cut; ++s) head.steps.push_back(p.steps[size_t(s)]);
+  head_orig_out.clear();
+  head_bnd_step.clear();
+  tail_in_src.clear();
+  tail_orig_out.clear();
+  for (size_t k = 0; k < p.outputs.size(); ++k) {
+    const PlanRef& o = p.outputs[k];
+    if (o.kind == PlanRef::Kind::kTemp && o.index < cut) {
+      head.outputs.push_back(o);
+      head_orig_out.push_back(int(k));
+    }
+  }
+  // Temporaries of the head the tail reads: one tail batched input per step (slices kept).
+  std::map<int, int> tin;  // head step -> tail batched index
+  tail = ExecutablePlan{};
+  tail.shared_shapes = p.shared_shapes;
+  tail.batched_shapes = p.batched_shapes;
+  for (size_t s = size_t(cut); s < n; ++s)
+    for (auto& r : refs_of(p.steps[s]))
+      if (r.kind == PlanRef::Kind::kTemp && r.index < cut && !tin.count(r.index)) {
+        tin[r.index] = int(tail.batched_shapes.size());
+        tail.batched_shapes.push_back(p.steps[size_t(r.index)].out_shape);
+        int src = -1;
+        for (size_t k = 0; k < p.outputs.size(); ++k) {
+          const PlanRef& o = p.outputs[k];
+          if (o.kind == PlanRef::Kind::kTemp && o.index == r.index && o.cols < 0) src = int(k);
+        }
+        if (src < 0) {  // not an original output: a boundary output of the head
+          src = -1 - int(head_bnd_step.size());
+          head_bnd_step.push_back(r.index);
+          head.outputs.push_back(PlanRef{PlanRef::Kind::kTemp, r.index, 0, -1});
+        }
+        tail_in_src.push_back(src);
+      }
+  if (tin.empty()) return false;
+  auto remap = [&](PlanRef r) {
+    if (r.kind != PlanRef::Kind::kTemp) return r;
+    if (r.index < cut) return PlanRef{PlanRef::Kind::kBatched, tin.at(r.index), r.col_off, r.cols};
+    r.index -= cut;
+    return r;
+  };
+  for (size_t s = size_t(cut); s < n; ++s) {
+    PlanStep st = p.steps[s];
+    for (auto& r : st.ins) r = remap(r);
+    for (auto& l : st.chain)
+      if (l.rhs) l.rhs = remap(*l.rhs);
+    tail.steps.push_back(st);
+  }
+  for (size_t k = 0; k < p.outputs.size(); ++k) {
+    const PlanRef& o = p.outputs[k];
+    if (o.kind == PlanRef::Kind::kTemp && o.index < cut) continue;
+    tail.outputs.push_back(remap(o));
+    tail_orig_out.push_back(int(k));
+  }
+  return !head.outputs.empty() && !tail.outputs.empty();
+}
 }  // namespace
 
 DPlan compile_plan(const ExecutablePlan& p, int64_t& temp_per_inst, std::vector<Shape>& out_shapes) {
@@ -505,6 +597,9 @@ DPlan compile_plan(const ExecutablePlan& p, int64_t& temp_per_inst, std::vector<
   return d;
 }
 
+// Set while the head / tail of a split plan are registered (they stay on the exact FP32 VM).
+static thread_local bool force_vm_next = false;
+
 int register_plan(mbx_ctx* c, const ExecutablePlan& plan) {
   std::vector<int32_t> enc = mbatch::backend::encode_plan(plan);
   auto it = c->plan_by_enc.find(enc);
@@ -526,6 +621,29 @@ int register_plan(mbx_ctx* c, const ExecutablePlan& plan) {
     for (int64_t s : bsizes) total += s;
     if (!c->dry) cuda_check(cudaMalloc(&pe.prefix_scratch, size_t(total) * sizeof(float)), "prefix scratch");
   }
+  if (!plan.ghost && pe.prefix_plan < 0 && pe.hplan.unit <= 0 && !force_vm_next) {
+    ExecutablePlan head, tail;
+    std::vector<int> hoo, hbs, tis, too;
+    if (split_at_reduction(plan, head, tail, hoo, hbs, tis, too)) {
+      force_vm_next = true;  // decision-feeding: exact FP32 plan VM for both halves
+      const int hid = register_plan(c, head);
+      const int tid = register_plan(c, tail);
+      force_vm_next = false;
+      const PlanEntry& hpe = c->plans[size_t(hid)];
+      const PlanEntry& tpe = c->plans[size_t(tid)];
+      if (hpe.hplan.unit > 0 && hpe.prefix_plan < 0 && tpe.prefix_plan < 0) {  // the head splits over columns
+        pe.head_plan = hid;
+        pe.tail_plan = tid;
+        pe.head_nout_orig = int(hoo.size());
+        pe.head_orig_out = hoo;
+        pe.bnd_size.clear();
+        for (int st : hbs) pe.bnd_size.push_back(plan.steps[size_t(st)].out_shape.size());
+        pe.tail_in_src = tis;
+        pe.tail_orig_out = too;
+      }
+    }
+  }
+  pe.force_vm = force_vm_next;
   if (!plan.ghost) {
     if (!c->dry) {
       cuda_check(cudaMalloc(&pe.dplan, sizeof(DPlan)), "plan alloc");
@@ -544,7 +662,7 @@ int register_plan(mbx_ctx* c, const ExecutablePlan& plan) {
       pe.unit_chunk = 0;
       pe.max_split = 1;
     }
-    tc_prepare(c, pe);
+    if (!pe.force_vm) tc_prepare(c, pe);
   }
   int id = int(c->plans.size());
   c->plans.push_back(std::move(pe));
@@ -596,7 +714,52 @@ BatchLaunch prepare_batch(mbx_ctx* c, int plan_id, int b, const int64_t* shared_
   // Per-instance step temporaries: the reference allocates them in the arena (exec_batched.cpp:
   // 106); here they live on chip, but the offsets are reserved so every later handle offset
   // equals the reference's.
-  arena_alloc(c, int64_t(b) * pe.temp_floats_per_inst);
+  const int64_t temps = arena_alloc(c, int64_t(b) * pe.temp_floats_per_inst);
+  if (pe.head_plan >= 0) {
+    // Split plan: head (columns across CTAs) then tail (per node).  The boundary tensors the tail
+    // reads go into the reserved temporary region (batch-contiguous per boundary), so no
+    // allocation the reference does not make.
+    const PlanEntry& hp = c->plans[size_t(pe.head_plan)];
+    const PlanEntry& tp = c->plans[size_t(pe.tail_plan)];
+    std::vector<int64_t> bnd_base;
+    int64_t cur = temps;
+    for (int64_t sz : pe.bnd_size) {
+      bnd_base.push_back(cur);
+      cur += int64_t(b) * sz;
+    }
+    MBATCH_CHECK(cur <= temps + int64_t(b) * pe.temp_floats_per_inst, "split plan: boundary exceeds temporaries");
+    BatchLaunch LH, LT;
+    LH.plan_id = pe.head_plan;
+    LH.b = b;
+    LT.plan_id = pe.tail_plan;
+    LT.b = b;
+    LH.shared_meta = meta_stage(c, shared_off, size_t(ns) * 8);
+    LH.batched_meta = meta_stage(c, eff.data(), eff.size() * 8);
+    std::vector<int64_t> hout;
+    for (int k : pe.head_orig_out) hout.push_back(bases[size_t(k)]);
+    for (int64_t bb : bnd_base) hout.push_back(bb);
+    LH.out_meta = meta_stage(c, hout.data(), hout.size() * 8);
+    const int ntb = int(tp.plan.batched_shapes.size());
+    std::vector<int64_t> tb(size_t(b) * ntb);
+    for (int i = 0; i < b; ++i) {
+      for (int j = 0; j < nb; ++j) tb[size_t(i) * ntb + j] = eff[size_t(i) * nb + j];
+      for (size_t j = 0; j < pe.tail_in_src.size(); ++j) {
+        const int src = pe.tail_in_src[j];
+        const int64_t size = tp.plan.batched_shapes[size_t(nb) + j].size();
+        const int64_t base = src >= 0 ? bases[size_t(src)] : bnd_base[size_t(-1 - src)];
+        tb[size_t(i) * ntb + nb + j] = base + int64_t(i) * size;
+      }
+    }
+    LT.shared_meta = meta_stage(c, shared_off, size_t(ns) * 8);
+    LT.batched_meta = meta_stage(c, tb.data(), tb.size() * 8);
+    std::vector<int64_t> tout;
+    for (int k : pe.tail_orig_out) tout.push_back(bases[size_t(k)]);
+    LT.out_meta = meta_stage(c, tout.data(), tout.size() * 8);
+    (void)hp;
+    L.sub.push_back(LH);
+    L.sub.push_back(LT);
+    return L;
+  }
   if (pe.prefix_plan >= 0) {
     // The hoisted prefix writes its boundary tensors into the plan's scratch; the main kernel
     // reads them as extra shared inputs (offsets relative to the arena base).
@@ -632,6 +795,10 @@ void issue_batch(mbx_ctx* c, const BatchLaunch& L) {
     cuda_check(launch_gather_rows(arena, meta_dev<int64_t>(c, g.src_meta), g.dst, L.b, g.size, c->stream), "gather");
     ++c->launches;
     ++g_launches;
+  }
+  if (!L.sub.empty()) {  // split plan: head, then tail
+    for (const auto& S : L.sub) issue_batch(c, S);
+    return;
   }
   bool prefix_cached = false;
   if (pe.prefix_plan >= 0) {
@@ -687,8 +854,10 @@ void issue_batch(mbx_ctx* c, const BatchLaunch& L) {
   v.plan = pe.dplan;
   v.arena = arena;
   v.b = L.b;
-  // Node tile: as many nodes per CTA as fill ~one wave (weight-tile reuse), no more.
-  v.tm = std::clamp((L.b + 147) / 148, 1, pe.tm);
+  // Node tile: as many nodes per CTA as fill ~one wave (weight-tile reuse), no more; a plan that
+  // splits over columns keeps every split and grows the node tile instead (each CTA streams its
+  // weight slice once per tile, so one node per CTA would re-read the weights per node).
+  v.tm = pe.max_split > 1 ? std::clamp((L.b * pe.max_split + 295) / 296, 1, pe.tm) : std::clamp((L.b + 147) / 148, 1, pe.tm);
   const int ntiles = (L.b + v.tm - 1) / v.tm;
   // Column tiles: enough CTAs for ~2 waves over 148 SMs, and together they must cover the unit.
   v.nsplit = pe.max_split > 1 ? std::clamp((296 + ntiles - 1) / ntiles, 1, pe.max_split) : 1;

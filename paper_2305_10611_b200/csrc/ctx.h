@@ -30,6 +30,17 @@ struct PlanEntry {
   int64_t temp_floats_per_inst = 0;  // sum of step output sizes (reference arena parity)
   std::vector<mbatch::backend::Shape> out_shapes;
   int tm = 1, threads = 256, smem = 0, unit_chunk = 0, max_split = 1;
+  // Column-split head / reduction tail (see split_at_reduction in backend.cpp): a plan whose
+  // trailing steps need whole rows (a small dense over a gate result, argmax) runs as two plans,
+  // the head split over columns across CTAs, the tail per node.  Head outputs the tail reads
+  // live in the plan's (reference-reserved) temporary region, or are original outputs.
+  int head_plan = -1, tail_plan = -1;
+  int head_nout_orig = 0;                    // head outputs [0, n) are original outputs
+  std::vector<int> head_orig_out;            // original output index of head output k < n
+  std::vector<int64_t> bnd_size;             // head outputs [n, ...): boundary sizes (floats)
+  std::vector<int> tail_in_src;              // tail extra batched input j: >= 0 original output, < 0 -1-boundary
+  std::vector<int> tail_orig_out;            // original output index of tail output k
+  bool force_vm = false;                     // exact FP32 plan VM only (decision-feeding heads)
   int tc_kind = -1;                  // tensor-core kernel for this plan (kernels_tc.cu), -1 none
   bool tc_small = false;             // gate plan served by the bit-exact small-dense kernel
   void* tc_state = nullptr;          // packed weights etc., owned by kernels_tc
@@ -130,6 +141,7 @@ struct BatchLaunch {
   // EXPLICIT gathers to run first: (slot size, src offsets meta, dst offset)
   struct Gather { int size; size_t src_meta; int64_t dst; };
   std::vector<Gather> gathers;
+  std::vector<BatchLaunch> sub;  // head / tail launches of a split plan
 };
 
 // Host half of exec_batched: validation, gather accounting, reference-order allocation of
