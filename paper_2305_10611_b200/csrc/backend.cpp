@@ -662,7 +662,7 @@ int register_plan(mbx_ctx* c, const ExecutablePlan& plan) {
       pe.unit_chunk = 0;
       pe.max_split = 1;
     }
-    if (!pe.force_vm) tc_prepare(c, pe);
+    tc_prepare(c, pe);  // force_vm plans get only the bit-exact gate kernel, if any
   }
   int id = int(c->plans.size());
   c->plans.push_back(std::move(pe));
@@ -843,8 +843,10 @@ void issue_batch(mbx_ctx* c, const BatchLaunch& L) {
   }
   // tc_kind 2 (pointwise) is exact and runs in every precision; tc_kind 1 (tensor cores) only
   // when the context allows split-bf16 / bf16 contractions.
-  // tc_small (bit-exact small-dense) also runs in every precision.
-  if (pe.tc_kind == 2 || pe.tc_small || (c->precision != MBX_PREC_FP32 && pe.tc_kind == 1)) {
+  // The bit-exact gate kernel runs for small / decision plans in every precision and for every
+  // gate plan in FP32 contexts; pointwise plans always; tensor cores in the other precisions.
+  if (pe.tc_kind == 2 || pe.tc_small || (pe.tc_exact && c->precision == MBX_PREC_FP32) ||
+      (c->precision != MBX_PREC_FP32 && pe.tc_kind == 1)) {
     cuda_check(tc_launch(c, pe, L), "tensor-core plan kernel");
     ++c->launches;
     ++g_launches;

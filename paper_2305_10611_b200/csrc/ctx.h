@@ -42,7 +42,8 @@ struct PlanEntry {
   std::vector<int> tail_orig_out;            // original output index of tail output k
   bool force_vm = false;                     // exact FP32 plan VM only (decision-feeding heads)
   int tc_kind = -1;                  // tensor-core kernel for this plan (kernels_tc.cu), -1 none
-  bool tc_small = false;             // gate plan served by the bit-exact small-dense kernel
+  bool tc_small = false;             // gate plan served by the bit-exact kernel in every precision
+  bool tc_exact = false;             // the bit-exact CUDA-core gate kernel exists (FP32 contexts use it)
   void* tc_state = nullptr;          // packed weights etc., owned by kernels_tc
 };
 

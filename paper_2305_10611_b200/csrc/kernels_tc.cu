@@ -104,7 +104,7 @@ struct TcState {
   // Few output columns (U x G <= 64): the bit-exact CUDA-core small-dense kernel instead of the
   // tensor cores, in every precision (sfn != nullptr).
   void* sfn = nullptr;
-  int s_npc = 0, s_smem = 0;
+  int s_npc = 0, s_uc = 0, s_kb = 0, s_smem = 0;
   bool s_attr = false;
   bool attr_set = false;
   // Persistent multi-level variant (mbx_tc_levels): K-split ranks, maximal node tile, smem layout.
@@ -288,13 +288,14 @@ std::string gen_levels_source(const TcState& st, int k) {
 }
 
 // Source of the bit-exact small-dense kernel (plans with few output columns, e.g. a classifier).
-std::string gen_small_source(const TcState& st, int npc) {
+std::string gen_small_source(const TcState& st) {
   std::ostringstream o;
   o << jit::prelude_source();
   o << "#define MBX_SMALL_KERNEL 1\n"
     << "#define MBX_KC 16\n#define MBX_K " << st.K << "\n#define MBX_U " << st.U << "\n#define MBX_G " << st.G
     << "\n#define MBX_NPIECES " << st.npieces << "\n#define MBX_PK0 " << st.piece_k[0] << "\n#define MBX_NLOADS "
-    << st.prog.nloads << "\n#define MBX_NOUT " << st.prog.nout << "\n#define MBX_SNPC " << npc << "\n";
+    << st.prog.nloads << "\n#define MBX_NOUT " << st.prog.nout << "\n#define MBX_SNPC " << st.s_npc
+    << "\n#define MBX_SUC " << st.s_uc << "\n#define MBX_SKB " << st.s_kb << "\n";
   o << gen_tail(st.prog, false, false, true);
   o << jit::kernel_source();
   return o.str();
@@ -375,10 +376,11 @@ bool analyse(const mbatch::backend::ExecutablePlan& p, const DPlan& d, TcState& 
   }
   st.G = int(st.w_shared.size());
   if (st.G < 1 || st.G > 4) return false;
-  st.UC = std::min(U, kM / st.G);
-  // The TMEM epilogue reads 8 node columns at a time and the tail one (node, unit) element per
-  // thread; UC must tile U exactly.
-  if (U % st.UC != 0 || st.UC % 8 != 0) return false;
+  // Units per tile: the largest multiple of 8 with G x UC <= 128 that tiles U exactly (the TMEM
+  // epilogue reads 8 node columns at a time; G = 3 gives 32 units, 96 of the 128 MMA rows).
+  st.UC = std::min(U, kM / st.G) / 8 * 8;
+  while (st.UC >= 8 && U % st.UC != 0) st.UC -= 8;
+  if (st.UC < 8) return false;
   // K chunks never straddle the two concatenated pieces.
   st.KC = (st.K % 32 == 0 && st.piece_k[0] % 32 == 0) ? 32 : 16;
   st.nchunks = st.K / st.KC;
@@ -626,13 +628,24 @@ void tc_prepare(mbx_ctx* c, PlanEntry& pe) {
   pe.tc_kind = -1;
   auto st = std::make_unique<TcState>();
   if (analyse(pe.exec_plan, pe.hplan, *st)) {
-    if (st->U * st->G <= 64 && st->K * st->U * st->G <= 16384 && st->K % 8 == 0) {
-      // Nodes per CTA: enough CTAs to spread a batch over the SMs (chains are latency-bound).
-      st->s_npc = std::max(1, std::min({kTcThreads / st->U, 8, (160 * 1024 - st->K * st->U * st->G * 4) / (st->K * 4)}));
-      st->s_smem = (st->K * st->U * st->G + st->s_npc * st->K) * 4;
-      const std::string ssrc = gen_small_source(*st, st->s_npc);
+    // The bit-exact CUDA-core gate kernel: unit slices of <= 32 units, 256 / slice nodes per
+    // CTA (at most 8: chains are latency-bound, CTAs spread the batch), K chunks of 64 (or K).
+    st->s_uc = std::min(st->U, 32);
+    st->s_npc = std::max(1, std::min(kTcThreads / st->s_uc, 8));
+    st->s_kb = st->K % 64 == 0 ? 64 : (st->K % 32 == 0 ? 32 : (st->K % 8 == 0 ? 8 : 0));
+    if (st->s_kb > 0 && st->U % st->s_uc == 0) {
+      st->s_smem = 2 * (st->G * st->s_kb * st->s_uc + st->s_npc * st->s_kb) * 4;
+      const std::string ssrc = gen_small_source(*st);
       st->sfn = load_kernel(c, ssrc, "mbx_small_dense");
-      pe.tc_small = true;
+      pe.tc_exact = true;
+      // Few output columns: tensor-core tiles would be mostly padding; exact in every precision.
+      pe.tc_small = st->U * st->G <= 64;
+    }
+    if (pe.force_vm) {  // decision-feeding: exact only
+      pe.tc_small = pe.tc_exact;
+      pe.tc_kind = pe.tc_exact ? 1 : -1;
+      pe.tc_state = st.release();
+      return;
     }
     st->src = gen_gate_source(*st);
     st->fn = load_kernel(c, st->src, "mbx_tc_gate");
@@ -753,7 +766,7 @@ static cudaError_t ensure_pack(mbx_ctx* c, TcState* st, const int64_t* shared_ho
 
 cudaError_t tc_launch(mbx_ctx* c, const PlanEntry& pe, const BatchLaunch& L) {
   auto* st = static_cast<TcState*>(pe.tc_state);
-  if (pe.tc_small && st->sfn) {
+  if ((pe.tc_small || (pe.tc_exact && c->precision == MBX_PREC_FP32)) && st->sfn) {
     SmallArgs a{};
     a.arena = arena_ptr(c);
     a.shared_off = meta_dev<long long>(c, L.shared_meta);
@@ -775,7 +788,7 @@ cudaError_t tc_launch(mbx_ctx* c, const PlanEntry& pe, const BatchLaunch& L) {
       st->s_attr = true;
     }
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(unsigned((L.b + st->s_npc - 1) / st->s_npc));
+    cfg.gridDim = dim3(unsigned((L.b + st->s_npc - 1) / st->s_npc), unsigned(st->U / st->s_uc));
     cfg.blockDim = dim3(kTcThreads);
     cfg.dynamicSmemBytes = size_t(st->s_smem);
     cfg.stream = c->stream;

@@ -1054,34 +1054,35 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const
 #endif  // MBX_LEVELS_KERNEL
 
 #ifdef MBX_SMALL_KERNEL
-// mbx_small_dense — gate plans with few output columns (U x G <= 64, e.g. the TreeLSTM
-// classifier relu(h . c_wt + cbias), 512 x 8): tensor-core tiles would be 90% padding.  CUDA
-// cores, bit-exact: every output is the reference's sequential chain acc = acc + x[p] * w[p][j]
-// over p ascending with separately rounded multiply and add (proj/src/backend.cpp:116-131), the
-// tail with the glibc-exact activations.  CTA = MBX_SNPC nodes; W (all gates) and the nodes'
-// rows staged in shared memory; thread = (node, unit), G independent chains.
+// mbx_exact_gate — bit-exact CUDA-core path of the gate plans: the FP32 context's cells, the
+// decision-feeding cells (NestedRNN's, always exact), and plans with few output columns (U x G
+// <= 64, e.g. the TreeLSTM classifier relu(h . c_wt + cbias), where tensor-core tiles would be
+// mostly padding) in every precision.  Every output is the reference's sequential chain
+// acc = acc + x[p] * w[p][j] over p ascending with separately rounded multiply and add
+// (proj/src/backend.cpp:116-131), the tail with the glibc-exact activations.
+//   grid = (node tiles of MBX_SNPC nodes, unit slices of MBX_SUC units); thread = (node, unit),
+//   MBX_G independent chains.  The weight slice and the nodes' rows stream through shared memory
+//   in K chunks of MBX_SKB (double-buffered cp.async), so no operand is read twice from L2 by one
+//   CTA and the chains run from shared memory.
+#define MBX_SNT (MBX_SNPC * MBX_SUC)
 extern "C" __global__ void __launch_bounds__(MBX_THREADS) mbx_small_dense(const __grid_constant__ SmallArgs P) {
   extern __shared__ __align__(16) float sms[];
-  constexpr int K = MBX_K, U = MBX_U, G = MBX_G, NPC = MBX_SNPC;
-  float* ws = sms;              // [G][K][U]
-  float* xs = sms + G * K * U;  // [NPC][K]
+  constexpr int K = MBX_K, U = MBX_U, G = MBX_G, NPC = MBX_SNPC, UC = MBX_SUC, KB = MBX_SKB;
+  constexpr int WCH = G * KB * UC, XCH = NPC * KB, BUF = WCH + XCH;
+  static_assert(K % KB == 0 && KB % 8 == 0, "K chunking");
   const int tid = threadIdx.x;
   const int node0 = blockIdx.x * NPC;
+  const int u0 = blockIdx.y * UC;
   const int nn = min(NPC, P.b - node0);
   // PDL: every input (weights included: they may be a hoisted prefix's output) after the wait.
   mbx_gen::pdl_wait();
   mbx_gen::pdl_launch_dependents();
+  __shared__ long long rowb[NPC][2];
   // Weight bases into registers first: through generic pointers the compiler cannot prove the
   // shared-memory stores leave the offset table alone and would re-read it every iteration.
   const float* wsrc[G];
 #pragma unroll
-  for (int g = 0; g < G; ++g) wsrc[g] = P.arena + __ldg(P.shared_off + P.w_idx[g]);
-  // cp.async: every copy in flight at once (a load -> store loop through registers would be
-  // serialised by the possible aliasing of the generic pointers).
-#pragma unroll
-  for (int g = 0; g < G; ++g)
-    for (int r = tid; r < K * U; r += MBX_THREADS) mbx_gen::cp_async4(ws + g * K * U + r, wsrc[g] + r, true);
-  __shared__ long long rowb[NPC][2];
+  for (int g = 0; g < G; ++g) wsrc[g] = P.arena + __ldg(P.shared_off + P.w_idx[g]) + u0;
   for (int i = tid; i < nn * 2; i += MBX_THREADS) {
     const int n = i >> 1, pc = i & 1;
     long long base = 0;
@@ -1092,49 +1093,75 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS) mbx_small_dense(const 
     rowb[n][pc] = base;
   }
   __syncthreads();
-  for (int i = tid; i < nn * K; i += MBX_THREADS) {
-    const int n = i / K, k = i - n * K;
-    const int pc = (MBX_NPIECES > 1 && k >= MBX_PK0) ? 1 : 0;
-    mbx_gen::cp_async4(xs + i, P.arena + rowb[n][pc] + k, true);
-  }
-  mbx_gen::cp_async_commit();
-  mbx_gen::cp_async_wait<0>();
-  __syncthreads();
-  for (int t = tid; t < nn * U; t += MBX_THREADS) {
-    const int n = t / U, u = t - n * U;
-    const float* x = xs + n * K;
-    float g[G];
+  auto stage = [&](int c, float* buf) {
+    const int k0 = c * KB;
+    // cp.async: every copy in flight at once (a load -> store loop through registers would be
+    // serialised by the possible aliasing of the generic pointers).
 #pragma unroll
-    for (int gi = 0; gi < G; ++gi) g[gi] = 0.0f;
-    // Blocks of 8 p: operands and products first (independent), then the 8 dependent adds of
-    // each chain in p order — the add chain is the only serial part.
-    static_assert(K % 8 == 0, "K multiple of 8");
-    for (int p0 = 0; p0 < K; p0 += 8) {
-      float xv[8];
+    for (int g = 0; g < G; ++g)
+      for (int i = tid; i < KB * UC; i += MBX_THREADS) {
+        const int r = i / UC, q = i - r * UC;
+        mbx_gen::cp_async4(buf + (g * KB + r) * UC + q, wsrc[g] + (long long)(k0 + r) * U + q, true);
+      }
+    for (int i = tid; i < nn * KB; i += MBX_THREADS) {
+      const int n = i / KB, k = k0 + (i - n * KB);
+      const int pc = (MBX_NPIECES > 1 && k >= MBX_PK0) ? 1 : 0;
+      mbx_gen::cp_async4(buf + WCH + i, P.arena + rowb[n][pc] + k, true);
+    }
+    mbx_gen::cp_async_commit();
+  };
+  const int n = tid / UC, u = tid - n * UC;
+  const bool active = tid < MBX_SNT && n < nn && u0 + u < U;
+  float g[G];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) xv[q] = x[p0 + q];
+  for (int gi = 0; gi < G; ++gi) g[gi] = 0.0f;
+  constexpr int NCH = K / KB;
+  stage(0, sms);
+  for (int c = 0; c < NCH; ++c) {
+    float* cur = sms + (c & 1) * BUF;
+    if (c + 1 < NCH) {
+      stage(c + 1, sms + ((c + 1) & 1) * BUF);
+      mbx_gen::cp_async_wait<1>();
+    } else {
+      mbx_gen::cp_async_wait<0>();
+    }
+    __syncthreads();
+    if (active) {
+      const float* x = cur + WCH + n * KB;
+      const float* w = cur + u;
+      // Blocks of 8 p: operands and products first (independent), then the 8 dependent adds of
+      // each chain in p order — the add chain is the only serial part.
+#pragma unroll 1
+      for (int p0 = 0; p0 < KB; p0 += 8) {
+        float xv[8];
 #pragma unroll
-      for (int gi = 0; gi < G; ++gi) {
-        float pr[8];
+        for (int q = 0; q < 8; ++q) xv[q] = x[p0 + q];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) pr[q] = mbx_libm::fmul(xv[q], ws[(gi * K + p0 + q) * U + u]);
+        for (int gi = 0; gi < G; ++gi) {
+          float pr[8];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) g[gi] = mbx_libm::fadd(g[gi], pr[q]);
+          for (int q = 0; q < 8; ++q) pr[q] = mbx_libm::fmul(xv[q], w[(gi * KB + p0 + q) * UC]);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) g[gi] = mbx_libm::fadd(g[gi], pr[q]);
+        }
       }
     }
-    const long long node = node0 + n;
-    float l[MBX_NLOADS > 0 ? MBX_NLOADS : 1];
-#pragma unroll
-    for (int j = 0; j < MBX_NLOADS; ++j) {
-      const TcLoad& d = P.loads[j];
-      const long long base = d.kind == 1 ? P.batched_off[node * P.nb + d.idx] : P.shared_off[d.idx];
-      l[j] = P.arena[base + d.off + u];
-    }
-    float o[MBX_NOUT];
-    mbx_tail_exact(g, l, o);
-#pragma unroll
-    for (int k = 0; k < MBX_NOUT; ++k) P.arena[P.out_base[k] + node * U + u] = o[k];
+    __syncthreads();  // the buffer is refilled two chunks on
   }
+  if (!active) return;
+  const long long node = node0 + n;
+  const int ug = u0 + u;
+  float l[MBX_NLOADS > 0 ? MBX_NLOADS : 1];
+#pragma unroll
+  for (int j = 0; j < MBX_NLOADS; ++j) {
+    const TcLoad& d = P.loads[j];
+    const long long base = d.kind == 1 ? P.batched_off[node * P.nb + d.idx] : P.shared_off[d.idx];
+    l[j] = P.arena[base + d.off + ug];
+  }
+  float o[MBX_NOUT];
+  mbx_tail_exact(g, l, o);
+#pragma unroll
+  for (int k = 0; k < MBX_NOUT; ++k) P.arena[P.out_base[k] + node * U + ug] = o[k];
 }
 #endif  // MBX_SMALL_KERNEL
 
