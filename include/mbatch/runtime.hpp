@@ -58,6 +58,10 @@ struct HostValue {
   Kind kind = Kind::kTensor;
   Shape shape;
   std::vector<float> data;
+  // Tensor data borrowed from the caller instead of `data` (the C ABI's instance inputs: valid
+  // for the duration of the evaluate call, so the floats are copied once, into the pinned
+  // staging buffer, not first into a vector).
+  const float* ext = nullptr;
   long ival = 0;
   double fval = 0.0;
   std::vector<HostValue> items;

@@ -64,9 +64,12 @@ HostValue decode(const int32_t* t, int64_t nt, int64_t& ti, const float* d, int6
       int r = t[ti++], c = t[ti++];
       int64_t n = int64_t(r) * c;
       MBATCH_CHECK(r >= 0 && c >= 0 && di + n <= nd, "hostval data truncated");
-      std::vector<float> v(d + di, d + di + n);
+      HostValue v;
+      v.kind = HostValue::Kind::kTensor;
+      v.shape = {r, c};
+      v.ext = d + di;  // borrowed for the call
       di += n;
-      return HostValue::tensor({r, c}, std::move(v));
+      return v;
     }
     case 1: MBATCH_CHECK(ti < nt, "hostval encoding truncated"); return HostValue::scalar(t[ti++]);
     case 2: case 3: case 4: {

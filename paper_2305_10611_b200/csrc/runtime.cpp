@@ -357,7 +357,8 @@ struct Executor::Impl {
     if (n <= 0 || opts.inputs_resident) return;
     mbx::ensure_input_stage(c, size_t(n));
     for (auto& [off, hv] : input_tensors)
-      std::memcpy(c->in_host + (off - input_base), hv->data.data(), hv->data.size() * sizeof(float));
+      std::memcpy(c->in_host + (off - input_base), hv->ext ? hv->ext : hv->data.data(),
+                  size_t(hv->shape.size()) * sizeof(float));
     if (opts.inputs_resident) return;
     if (!c->dry) {
       cudaStream_t cs = c->copy_stream ? c->copy_stream : c->stream;
