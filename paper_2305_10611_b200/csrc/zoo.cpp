@@ -220,10 +220,14 @@ Task tlstm(Executor& ex, Fiber& fb, const TreeLstmParams& P, Val t) {
     int n = ex.emit(fb, 1, {&P.hz, &P.hz, &P.i_wt, &xt, &P.fl_wt, &P.fr_wt, &P.u_wt, &P.cz, &P.cz});
     co_return Val::tuple({Executor::out(n, 1), Executor::out(n, 0)});  // (tanh(c), c)
   }
-  Val l = t.at(0), r = t.at(1);
+  // The children's calls capture one pointer each (fits std::function's inline storage): the
+  // subtrees live in this frame until the join, and tlstm copies its argument at the call.
+  struct Sub { Executor* ex; const TreeLstmParams* P; const Val* t; };
+  const Sub sl{&ex, &P, &t.at(0)}, sr{&ex, &P, &t.at(1)};
   std::vector<Call> calls;
-  calls.push_back([&ex, &P, l](Fiber& f) { return tlstm(ex, f, P, l); });
-  calls.push_back([&ex, &P, r](Fiber& f) { return tlstm(ex, f, P, r); });
+  calls.reserve(2);
+  calls.push_back([a = &sl](Fiber& f) { return tlstm(*a->ex, f, *a->P, *a->t); });
+  calls.push_back([a = &sr](Fiber& f) { return tlstm(*a->ex, f, *a->P, *a->t); });
   runtime::JoinAwait join = ex.concurrent(fb, std::move(calls));
   std::vector<Val> res = co_await join;
   const Val &lh = res[0].at(0), &lc = res[0].at(1), &rh = res[1].at(0), &rc = res[1].at(1);
@@ -249,10 +253,12 @@ struct MvParams {
 
 Task mv(Executor& ex, Fiber& fb, const MvParams& P, Val t) {
   if (t.ctor == 0) co_return Val::tuple({t.at(0), t.at(1)});
-  Val l = t.at(0), r = t.at(1);
+  struct Sub { Executor* ex; const MvParams* P; const Val* t; };
+  const Sub sl{&ex, &P, &t.at(0)}, sr{&ex, &P, &t.at(1)};
   std::vector<Call> calls;
-  calls.push_back([&ex, &P, l](Fiber& f) { return mv(ex, f, P, l); });
-  calls.push_back([&ex, &P, r](Fiber& f) { return mv(ex, f, P, r); });
+  calls.reserve(2);
+  calls.push_back([a = &sl](Fiber& f) { return mv(*a->ex, f, *a->P, *a->t); });
+  calls.push_back([a = &sr](Fiber& f) { return mv(*a->ex, f, *a->P, *a->t); });
   runtime::JoinAwait join = ex.concurrent(fb, std::move(calls));
   std::vector<Val> res = co_await join;
   const Val &lv = res[0].at(0), &lm = res[0].at(1), &rv = res[1].at(0), &rm = res[1].at(1);
