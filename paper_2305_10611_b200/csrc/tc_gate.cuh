@@ -819,7 +819,6 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const
           asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&xraw[j])) : "memory");
         }
 #endif
-        load_tail_operands();
         // Every row address of this tile is issued: look up the next tile's rows now (its
         // offset tables are static), off the critical path of the next gather.
         MBX_LSTAMP_T(64, lv, 9);
@@ -866,20 +865,19 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const
             *reinterpret_cast<uint4*>(xs + off) = make_uint4(hp[0], hp[1], hp[2], hp[3]);
             if (npass > 1) *reinterpret_cast<uint4*>(xs + xlo + off) = make_uint4(lp[0], lp[1], lp[2], lp[3]);
           }
-          // One proxy fence for the whole tile once the last chunk is written (a fence per chunk
-          // costs more than the MMAs it would let start early).
-          if (j + 1 == CPR) {
-            fence_async_smem();
-            __syncwarp();
-            if (lane == 0)
-              for (int q = 0; q < CPR; ++q) mbar_arrive(&xfull[q]);
-          }
+          // Chunk j is ready for the tensor core: its MMAs overlap the next chunk's conversion.
+          fence_async_smem();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&xfull[j]);
         }
 #if MBX_LCY > 1
         // This CTA's staging is consumed: the cluster may multicast the next tile's rows into it.
         asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
 #endif
         MBX_LSTAMP_T(64, lv, 7);
+        // The tail's operands: off the gather -> convert critical path, in flight during the MMAs
+        // and the exchange.
+        load_tail_operands();
       } else if (warp == 1 && lane == 0) {
         // ---- MMA issuer ----
         if (it == 0) mbar_wait(wfull, 0);
