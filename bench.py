@@ -8,10 +8,12 @@ from the reference's zoo generators.  Default workload: TreeLSTM hidden 512, bat
 headline config, BASELINE.json configs[1]).
 
 A step = T x R independent mini-batches (R = 16 per worker) evaluated by the native throughput pool
-(mbx_pool_run: T host worker threads, one context each, one shared device stream) — the same use
-of the host cores as the reference arm, which runs one process per core.
+(mbx_pool_run: T host worker threads, one context and stream each; the persistent kernels chained
+through a per-device lane) — the same use of the host cores as the reference arm, which runs one
+process per core.
   value  nodes/s with every mini-batch's inputs already resident in HBM (no input H2D, outputs
-         left in HBM), CUDA events on the pool stream around each step, L2 flushed between steps.
+         left in HBM), CUDA events on the worker streams around each step, L2 flushed between
+         steps.
   e2e    the same with HOST buffers: H2D of the inputs, the run, D2H of the outputs, every
          mini-batch (mbx_evaluate_batch semantics per mini-batch).
   latency  one mini-batch at a time on one context (ms per mini-batch, host split, per-signature
@@ -456,20 +458,15 @@ def run_pool(args, mbx, torch, local, rank, world, nodes, l2):
     ctx = mbx.Context(-1, args.precision)  # host-only: the synthetic inputs
     gen = mbx.Model(ctx, args.model, args.hidden)
     ins = [gen.make_inputs(args.seed + rank * T + w, args.batch) for w in range(T)]
-    stream = torch.cuda.ExternalStream(pool.stream(), device=local)
-
     def steps(K, kw):
         ms, total = 0.0, 0
         for _ in range(K):
-            with torch.cuda.stream(stream):
-                l2.zero_()  # flush L2 between steps (256 MiB > 126 MB L2)
-                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                a.record(stream)
-            total += pool.run(ins * args.per_thread, args.batch, **kw)
-            with torch.cuda.stream(stream):
-                b.record(stream)
-            b.synchronize()
-            ms += a.elapsed_time(b)
+            l2.zero_()  # flush L2 between steps (256 MiB > 126 MB L2)
+            torch.cuda.synchronize(local)
+            # device time of the step: CUDA events on every worker stream (first start -> last end)
+            n, dev_ms = pool.run_timed(ins * args.per_thread, args.batch, **kw)
+            total += n
+            ms += dev_ms
         return ms, total
 
     steps(max(3, args.warmup), {})

@@ -164,8 +164,9 @@ int mbx_result_host_breakdown(const mbx_result* r, double* out4);
 int mbx_result_batch_times(const mbx_result* r, double* us);
 
 /* ---- throughput mode: many mini-batches on one GPU, host work on T threads ----------------
- * T worker contexts (each: arena, plan registry, model `model` at `hidden` with parameters from
- * zoo::make_params(param_seed)) issue into one shared device stream.  mbx_pool_run evaluates
+ * T worker contexts (each: stream, arena, plan registry, model `model` at `hidden` with
+ * parameters from zoo::make_params(param_seed)); launches needing co-resident CTAs are chained
+ * through a per-device lane, everything else overlaps across workers.  mbx_pool_run evaluates
  * mini-batch i (hostval-encoded toks[i] / data[i]) on worker i % T with `opts`; returns the
  * total DFG node count.  Same semantics per mini-batch as mbx_evaluate_batch. */
 typedef struct mbx_pool mbx_pool;
@@ -180,6 +181,11 @@ mbx_model* mbx_pool_model(mbx_pool* p, int worker);
 int mbx_pool_run(mbx_pool* p, int n, int batch, const int32_t* const* toks, const int64_t* ntok,
                  const float* const* data, const int64_t* ndata, const mbx_options* opts,
                  int64_t* total_nodes);
+/* Same, and the device time of the run (first worker-stream start to last worker-stream end,
+ * CUDA events) in *device_ms. */
+int mbx_pool_run_timed(mbx_pool* p, int n, int batch, const int32_t* const* toks, const int64_t* ntok,
+                       const float* const* data, const int64_t* ndata, const mbx_options* opts,
+                       int64_t* total_nodes, double* device_ms);
 
 #ifdef __cplusplus
 }

@@ -13,6 +13,9 @@
 #include <atomic>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
 #include <sstream>
 
 #include "ctx.h"
@@ -27,6 +30,47 @@ void cuda_check(cudaError_t e, const char* what) {
 }
 void cu_check(CUresult r, const char* what) {
   if (r != CUDA_SUCCESS) throw mbatch::Error(std::string("cuda driver error ") + std::to_string(int(r)) + " in " + what);
+}
+
+namespace {
+struct PersistentLane {
+  std::mutex mu;  // held from begin to end: the wait and the record enclose one launch
+  cudaEvent_t last = nullptr;
+};
+PersistentLane& lane_of(int device) {
+  static std::mutex m;
+  static std::map<int, std::unique_ptr<PersistentLane>> lanes;
+  std::lock_guard<std::mutex> lock(m);
+  auto& p = lanes[device];
+  if (!p) p = std::make_unique<PersistentLane>();
+  return *p;
+}
+}  // namespace
+
+void persistent_lane_begin(mbx_ctx* c) {
+  if (!c->serialize_persistent || c->dry) return;
+  PersistentLane& L = lane_of(c->device);
+  L.mu.lock();
+  if (L.last) cuda_check(cudaStreamWaitEvent(c->stream, L.last, 0), "persistent lane wait");
+}
+
+void persistent_lane_forget(mbx_ctx* c) {
+  if (!c->serialize_persistent || c->dry || !c->ev_persist) return;
+  PersistentLane& L = lane_of(c->device);
+  std::lock_guard<std::mutex> lock(L.mu);
+  if (L.last == c->ev_persist) {
+    cudaEventSynchronize(c->ev_persist);
+    L.last = nullptr;
+  }
+}
+
+void persistent_lane_end(mbx_ctx* c) {
+  if (!c->serialize_persistent || c->dry) return;
+  PersistentLane& L = lane_of(c->device);
+  if (!c->ev_persist) cuda_check(cudaEventCreateWithFlags(&c->ev_persist, cudaEventDisableTiming), "event");
+  cuda_check(cudaEventRecord(c->ev_persist, c->stream), "persistent lane record");
+  L.last = c->ev_persist;
+  L.mu.unlock();
 }
 
 void stream_wait_own(mbx_ctx* c, const char* what) {

@@ -135,6 +135,8 @@ void mbx_ctx_destroy(mbx_ctx* c) {
   if (!c) return;
   if (!c->dry) {
     cudaStreamSynchronize(c->stream);
+    mbx::persistent_lane_forget(c);
+    if (c->ev_persist) cudaEventDestroy(c->ev_persist);
     for (auto& pe : c->plans) {
       if (pe.dplan) cudaFree(pe.dplan);
       if (pe.prefix_scratch) cudaFree(pe.prefix_scratch);

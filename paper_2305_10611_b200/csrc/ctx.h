@@ -69,6 +69,12 @@ struct mbx_ctx {
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t ev_copy = nullptr;
   bool copy_pending = false;
+  // Contexts on one device that run concurrently (a pool's workers, each on its own stream):
+  // launches that need all their CTAs resident at once (mbx_tc_levels: grid barrier, cross-CTA
+  // counters) are chained through a per-device lane — each waits for the previous one to
+  // complete — so two of them are never partially resident together; everything else overlaps.
+  bool serialize_persistent = false;
+  cudaEvent_t ev_persist = nullptr;
   // HBM arena: one virtual-address reservation, physical chunks mapped on demand, so offsets
   // (the reference's TensorHandle::offset) are stable while the arena grows.
   CUdeviceptr base = 0;
@@ -108,6 +114,11 @@ namespace mbx {
 
 // Throws mbatch::Error on CUDA failure.
 void cuda_check(cudaError_t e, const char* what);
+// The per-device persistent-launch lane (see mbx_ctx::serialize_persistent): makes c->stream
+// wait for the previous lane launch; after the launch, persistent_lane_end records it.
+void persistent_lane_begin(mbx_ctx* c);
+void persistent_lane_end(mbx_ctx* c);
+void persistent_lane_forget(mbx_ctx* c);  // before destroying c (its event may be the lane's last)
 // Waits for everything this context enqueued so far (an event: on a pool's shared stream it does
 // not wait for work other workers enqueue later).
 void stream_wait_own(mbx_ctx* c, const char* what);

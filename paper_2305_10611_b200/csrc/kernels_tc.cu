@@ -275,6 +275,7 @@ std::string gen_levels_source(const TcState& st, int k) {
   const TcState::LevelsCfg& L = st.lv[k];
   std::ostringstream o;
   if (stamps_enabled()) o << "#define MBX_STAMPS 1\n";
+  if (std::getenv("MBX_FENCE_ONCE")) o << "#define MBX_FENCE_ONCE 1\n";
   o << jit::prelude_source();
   o << "#define MBX_LEVELS_KERNEL 1\n"
     << "#define MBX_KC " << st.KC << "\n#define MBX_U " << st.U << "\n#define MBX_G " << st.G << "\n#define MBX_UC "
@@ -487,15 +488,19 @@ bool levels_layout(TcState& st, int k) {
   // Unit tiles sharing node rows by multicast: clusters of up to 4 along y (always co-resident:
   // 148 SMs hold 37 of them).  Clusters of 8 ranks along z (DSMEM exchange) only when no
   // multicast cluster is formed and at most 14 of them are needed.
+  // The wide configuration (one large batch per launch) exchanges partials inside clusters of
+  // its S ranks (DSMEM): no cross-cluster waits, so it needs no co-residency beyond its clusters
+  // and runs beside other work (no persistent lane).
   int CY = 1;
-  while (CY * 2 <= cy_max && utiles % (CY * 2) == 0) CY *= 2;
+  if (k == 0)
+    while (CY * 2 <= cy_max && utiles % (CY * 2) == 0) CY *= 2;
   // deep: largest S first (smallest resident weight slice), then the largest node tile; wide:
   // the largest node tile first (fewest tile rounds), then the smallest S that fits with it.
   auto try_cfg = [&](int S, int NT) {
     if (st.nchunks % S != 0 || utiles * S > 148) return false;
     const int cpr = st.nchunks / S;
     if (cpr > 16) return false;
-    const int xch = CY > 1 ? 1 : ((S > 1 && utiles * S > 14 * 8) ? 1 : 0);
+    const int xch = CY > 1 ? 1 : ((S > 1 && k == 0 && utiles * S > 14 * 8) ? 1 : 0);
     // tail elements per thread x operands held in registers (MBX_LEPT x MBX_NLOADS) <= 16
     if (NT / S < 2 || (NT / S) * st.UC * std::max(1, st.prog.nloads) > 16 * kTcThreads) return false;
     const int w = al(cpr * kM * st.KC * 4);
@@ -1133,7 +1138,13 @@ void issue_levels(mbx_ctx* c, const std::vector<BatchLaunch>& Ls, size_t i, int 
     a.stamps = lstamps;
   }
   void* args[] = {&a};
-  cuda_check(cudaLaunchKernelExC(&lc, C.fn, args), "multi-level tensor-core kernel");
+  // Grid barrier (several levels) or cross-cluster counters (L2 exchange): every CTA must be
+  // resident at once, so such launches take the device's persistent lane.
+  const bool lane = n > 1 || (C.xch == 1 && C.S > 1);
+  if (lane) persistent_lane_begin(c);
+  const cudaError_t le = cudaLaunchKernelExC(&lc, C.fn, args);
+  if (lane) persistent_lane_end(c);
+  cuda_check(le, "multi-level tensor-core kernel");
   if (stamps_enabled()) {
     // Profiling aid: per level, median / max over CTAs of each phase (us after the level start).
     std::vector<unsigned long long> h(size_t(nctas) * 64 * 16);

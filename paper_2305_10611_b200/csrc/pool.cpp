@@ -3,12 +3,13 @@
 // The reference evaluates one mini-batch per call on one host thread (runtime::evaluate_batch,
 // proj/src/executor.cpp:782-787); its host side (fibers, inline-depth DFG, scheduling) is the
 // part that does not shrink with a faster device.  A pool runs T worker threads, each with its
-// own context (arena, offset-table ring, plan registry, model + parameters) and the same model,
-// all issuing into ONE device stream: the device work of different mini-batches is serialised in
-// submission order (so the persistent multi-level kernels, which need every CTA resident, never
-// overlap), while their host work (input decode, fibers, scheduling, offset tables) overlaps.
-// Mini-batch i runs on worker i % T, so a worker's inputs can stay resident across calls
-// (inputs_resident).  Each worker waits only for its own work (event sync, not stream sync).
+// own context (stream, arena, offset-table ring, plan registry, model + parameters): host work
+// overlaps, and so does device work of different mini-batches — except the launches that need
+// all their CTAs resident at once (the persistent mbx_tc_levels kernels), which are chained
+// through the per-device persistent lane (mbx_ctx::serialize_persistent) so two of them are
+// never partially resident together.  Mini-batch i runs on worker i % T, so a worker's inputs
+// can stay resident across calls (inputs_resident).
+#include <algorithm>
 #include <atomic>
 #include <cstring>
 #include <memory>
@@ -49,12 +50,7 @@ int mbx_pool_create(int device, int precision, const char* model, int hidden, un
   for (int t = 0; t < threads; ++t) {
     mbx_ctx* c = nullptr;
     if (mbx_ctx_create(device, precision, &c)) return fail(mbx_last_error(nullptr));
-    if (device >= 0) {
-      cudaStreamSynchronize(c->stream);
-      cudaStreamDestroy(c->stream);
-      c->stream = p->stream;
-      c->owns_stream = false;
-    }
+    c->serialize_persistent = true;
     p->ctxs.push_back(c);
     mbx_model* m = nullptr;
     if (mbx_model_create(c, model, hidden, &m)) return fail(mbx_last_error(c));
@@ -83,7 +79,23 @@ mbx_model* mbx_pool_model(mbx_pool* p, int worker) {
 
 int mbx_pool_run(mbx_pool* p, int n, int batch, const int32_t* const* toks, const int64_t* ntok,
                  const float* const* data, const int64_t* ndata, const mbx_options* opts, int64_t* total_nodes) {
+  return mbx_pool_run_timed(p, n, batch, toks, ntok, data, ndata, opts, total_nodes, nullptr);
+}
+
+int mbx_pool_run_timed(mbx_pool* p, int n, int batch, const int32_t* const* toks, const int64_t* ntok,
+                       const float* const* data, const int64_t* ndata, const mbx_options* opts,
+                       int64_t* total_nodes, double* device_ms) {
   const int T = int(p->ctxs.size());
+  // Device time of the whole run: an event in every worker stream before any work (the streams
+  // are idle, so they fire at once) and after all of it; the span is first start -> last end.
+  std::vector<cudaEvent_t> ev0(size_t(T), nullptr), ev1(size_t(T), nullptr);
+  const bool timed = device_ms && p->device >= 0;
+  if (timed)
+    for (int w = 0; w < T; ++w) {
+      cudaEventCreate(&ev0[size_t(w)]);
+      cudaEventCreate(&ev1[size_t(w)]);
+      cudaEventRecord(ev0[size_t(w)], p->ctxs[size_t(w)]->stream);
+    }
   std::atomic<int64_t> nodes{0};
   std::vector<std::string> errs(static_cast<size_t>(T));
   auto work = [&](int w) {
@@ -103,6 +115,23 @@ int mbx_pool_run(mbx_pool* p, int n, int batch, const int32_t* const* toks, cons
   for (int w = 1; w < T && w < n; ++w) th.emplace_back(work, w);
   work(0);
   for (auto& t : th) t.join();
+  if (timed) {
+    double span = 0.0;
+    for (int w = 0; w < T; ++w) {
+      cudaEventRecord(ev1[size_t(w)], p->ctxs[size_t(w)]->stream);
+      cudaEventSynchronize(ev1[size_t(w)]);
+    }
+    for (int a = 0; a < T; ++a)
+      for (int b = 0; b < T; ++b) {
+        float ms = 0.0f;
+        if (cudaEventElapsedTime(&ms, ev0[size_t(a)], ev1[size_t(b)]) == cudaSuccess) span = std::max(span, double(ms));
+      }
+    *device_ms = span;
+    for (int w = 0; w < T; ++w) {
+      cudaEventDestroy(ev0[size_t(w)]);
+      cudaEventDestroy(ev1[size_t(w)]);
+    }
+  }
   for (auto& e : errs)
     if (!e.empty()) {
       p->err = e;

@@ -865,10 +865,19 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const
             *reinterpret_cast<uint4*>(xs + off) = make_uint4(hp[0], hp[1], hp[2], hp[3]);
             if (npass > 1) *reinterpret_cast<uint4*>(xs + xlo + off) = make_uint4(lp[0], lp[1], lp[2], lp[3]);
           }
+#ifndef MBX_FENCE_ONCE
           // Chunk j is ready for the tensor core: its MMAs overlap the next chunk's conversion.
           fence_async_smem();
           __syncwarp();
           if (lane == 0) mbar_arrive(&xfull[j]);
+#else
+          if (j + 1 == CPR) {
+            fence_async_smem();
+            __syncwarp();
+            if (lane == 0)
+              for (int q = 0; q < CPR; ++q) mbar_arrive(&xfull[q]);
+          }
+#endif
         }
 #if MBX_LCY > 1
         // This CTA's staging is consumed: the cluster may multicast the next tile's rows into it.

@@ -94,6 +94,8 @@ def lib() -> ctypes.CDLL:
         "mbx_pool_model": (P, [P, I]),
         "mbx_pool_run": (I, [P, I, I, ctypes.POINTER(pI32), pI64, ctypes.POINTER(pF), pI64, ctypes.POINTER(_Opts),
                              pI64]),
+        "mbx_pool_run_timed": (I, [P, I, I, ctypes.POINTER(pI32), pI64, ctypes.POINTER(pF), pI64,
+                                   ctypes.POINTER(_Opts), pI64, pD]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -115,7 +117,7 @@ def exported_symbols() -> List[str]:
                         "mbx_result_flush_boundaries mbx_result_nodes mbx_result_timing mbx_result_batch_times "
                         "mbx_result_host_breakdown mbx_ctx_stream mbx_pool_create mbx_pool_destroy "
                         "mbx_pool_last_error mbx_pool_set_error mbx_pool_threads mbx_pool_stream mbx_pool_model "
-                        "mbx_pool_run").split()]
+                        "mbx_pool_run mbx_pool_run_timed").split()]
 
 
 def _ptr(a: np.ndarray, ct):
@@ -465,9 +467,10 @@ def make_options(scheduler: str = "depth", gather: str = "fused", hoist: bool = 
 
 
 class Pool:
-    """Throughput mode (mbx_pool_*): `threads` worker contexts on one device sharing one stream;
-    ``run`` evaluates many independent mini-batches, mini-batch i on worker i % threads, host work
-    in parallel, device work serialised in submission order."""
+    """Throughput mode (mbx_pool_*): `threads` worker contexts on one device, each with its own
+    stream; ``run`` evaluates many independent mini-batches, mini-batch i on worker i % threads,
+    host and device work overlapping across workers (launches needing co-resident CTAs chained
+    through the per-device persistent lane)."""
 
     def __init__(self, device: int, precision: str, model: str, hidden: int, param_seed: int, threads: int):
         self.h = ctypes.c_void_p()
@@ -492,6 +495,11 @@ class Pool:
 
     def run(self, inputs: Sequence[Tuple[np.ndarray, np.ndarray]], batch: int, **opts) -> int:
         """Evaluates every (toks, data) mini-batch; returns the total DFG node count."""
+        return self.run_timed(inputs, batch, **opts)[0]
+
+    def run_timed(self, inputs: Sequence[Tuple[np.ndarray, np.ndarray]], batch: int, **opts) -> Tuple[int, float]:
+        """Like run; also returns the device time of the run in ms (CUDA events on the worker
+        streams: first start to last end)."""
         L = lib()
         n = len(inputs)
         ts = [np.ascontiguousarray(t, np.int32) for t, _ in inputs]
@@ -502,9 +510,10 @@ class Pool:
         nd = (ctypes.c_int64 * n)(*[d.size for d in ds])
         o = make_options(**opts)
         total = ctypes.c_int64(0)
-        if L.mbx_pool_run(self.h, n, batch, tp, nt, dp, nd, ctypes.byref(o), ctypes.byref(total)):
+        ms = ctypes.c_double(0.0)
+        if L.mbx_pool_run_timed(self.h, n, batch, tp, nt, dp, nd, ctypes.byref(o), ctypes.byref(total), ctypes.byref(ms)):
             raise MbatchError(L.mbx_pool_last_error(self.h).decode())
-        return int(total.value)
+        return int(total.value), float(ms.value)
 
 
 def _read_result(r, batch: int, record_nodes: bool, decode: bool, want_trace: bool = True) -> EvalResult:
