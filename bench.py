@@ -55,7 +55,7 @@ def parse_args():
     p.add_argument("--precision", default="bf16x3", choices=["fp32", "bf16x3", "bf16"])
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--threads", type=int, default=0,
-                   help="host worker threads of the throughput pool (0: min(12, cores per rank - 2))")
+                   help="host worker threads of the throughput pool (0: cores per rank - 2)")
     p.add_argument("--per-thread", type=int, default=16, help="mini-batches per worker thread per step")
     p.add_argument("--no-other-configs", action="store_true",
                    help="skip the per-config latency table of the other BASELINE configs")
@@ -453,7 +453,7 @@ def run_pool(args, mbx, torch, local, rank, world, nodes, l2):
     """Throughput: T worker threads, each evaluating its own mini-batch per step (mbx_pool_run).
     Returns value / e2e nodes/s and the per-step device times (CUDA events on the pool stream)."""
     cores = max(1, (os.cpu_count() or 1) // max(1, world))
-    T = args.threads or max(1, min(12, cores - 2))
+    T = args.threads or max(1, cores - 2)
     pool = mbx.Pool(local, args.precision, args.model, args.hidden, args.seed, T)
     ctx = mbx.Context(-1, args.precision)  # host-only: the synthetic inputs
     gen = mbx.Model(ctx, args.model, args.hidden)

@@ -22,6 +22,25 @@
 namespace mbatch {
 namespace runtime {
 
+// Per-thread size-class free lists (runtime.cpp) for the small objects the fibers churn through:
+// coroutine frames, fibers, the shared item lists of tuple / list values.
+void* frame_alloc(size_t bytes);
+void frame_free(void* p, size_t bytes) noexcept;
+
+template <class T>
+struct PoolAlloc {
+  using value_type = T;
+  PoolAlloc() = default;
+  template <class U>
+  PoolAlloc(const PoolAlloc<U>&) {}
+  T* allocate(size_t n) { return static_cast<T*>(frame_alloc(n * sizeof(T))); }
+  void deallocate(T* p, size_t n) noexcept { frame_free(p, n * sizeof(T)); }
+  template <class U>
+  bool operator==(const PoolAlloc<U>&) const { return true; }
+  template <class U>
+  bool operator!=(const PoolAlloc<U>&) const { return false; }
+};
+
 struct Val {
   enum Kind : uint8_t { kTensor, kInt, kList, kTuple, kAdt };
   Kind kind = kInt;
@@ -36,7 +55,7 @@ struct Val {
     Val v;
     v.kind = k;
     v.ctor = ctor;
-    v.items = std::make_shared<const std::vector<Val>>(std::move(it));
+    v.items = std::allocate_shared<const std::vector<Val>>(PoolAlloc<std::vector<Val>>(), std::move(it));
     return v;
   }
   static Val list(std::vector<Val> it) { return seq(kList, std::move(it)); }
@@ -46,10 +65,7 @@ struct Val {
 };
 
 // Coroutine frames of the zoo programs are allocated per call (one per block-calling function,
-// one per forked child fiber): a per-thread size-class free list makes them ~free.
-void* frame_alloc(size_t bytes);
-void frame_free(void* p, size_t bytes) noexcept;
-
+// one per forked child fiber): the per-thread free lists make them ~free.
 struct Task {
   struct promise_type {
     static void* operator new(size_t n) { return frame_alloc(n); }
@@ -99,6 +115,8 @@ struct Task {
 enum class FiberStatus { kRunnable, kBlockedValue, kBlockedJoin, kDone };
 
 struct Fiber {
+  static void* operator new(size_t n) { return frame_alloc(n); }
+  static void operator delete(void* p, size_t n) noexcept { frame_free(p, n); }
   int id = -1;
   int instance = -1;
   int parent = -1;
