@@ -521,6 +521,15 @@ bool levels_layout(TcState& st, int k) {
     C.smem = w + x + stage + recv + bars;
     return true;
   };
+  static const int force_s = [] {
+    const char* e = std::getenv("MBX_LEVELS_DEEP_S");  // experiment: deep K split, DSMEM exchange
+    return e ? std::atoi(e) : 0;
+  }();
+  if (k == 0 && force_s > 0) {
+    CY = 1;
+    for (int NT : {128, 64, 32})
+      if (try_cfg(force_s, NT)) return true;
+  }
   if (k == 0) {
     for (int S : {8, 4, 2, 1})
       for (int NT : {128, 64, 32})
