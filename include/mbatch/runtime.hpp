@@ -206,8 +206,12 @@ class Session {
   int64_t params_end() const { return params_end_; }
   const std::map<std::string, TensorHandle>& param_handles() const { return param_handles_; }
   const std::vector<int>& plan_ids() const { return plan_ids_; }
+  // DFG node objects of earlier evaluations, kept with their vectors' capacity so the next
+  // evaluation's node construction allocates nothing (implementation detail of the executor).
+  std::vector<DFGNode>& node_pool() { return node_pool_; }
 
  private:
+  std::vector<DFGNode> node_pool_;
   const CompiledModel& model_;
   mbx_ctx* ctx_ = nullptr;
   bool owned_ = true;

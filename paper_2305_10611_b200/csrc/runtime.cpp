@@ -380,13 +380,29 @@ struct Executor::Impl {
     return n.outputs.at(r.out);
   }
 
+  // A DFG node from the session's pool (vectors cleared, capacity kept) or a fresh one.
+  DFGNode recycled_node() {
+    auto& pool = s.node_pool();
+    if (pool.empty()) return DFGNode{};
+    DFGNode n = std::move(pool.back());
+    pool.pop_back();
+    n.id = n.sig_id = n.block_id = n.instance = -1;
+    n.phase = n.depth = 0;
+    n.ghost = n.executed = false;
+    n.shared_ins.clear();
+    n.batched_ins.clear();
+    n.producers.clear();
+    n.outputs.clear();
+    return n;
+  }
+
   // -- DFG construction (executor.cpp:368-443) --------------------------------------------
   int emit(Fiber& fb, int blk_id, std::initializer_list<const Val*> ins) {
     const StaticBlockInfo& blk = *block_by_id.at(blk_id);
     const kernelgen::BlockBinding& bind = *binding_by_id[blk_id];
     const Val* const* in = ins.begin();
     if (ins.size() != blk.inputs.size()) throw Error("block " + std::to_string(blk_id) + ": input arity");
-    DFGNode node;
+    DFGNode node = recycled_node();
     node.shared_ins.reserve(bind.shared_input_pos.size());
     node.batched_ins.reserve(bind.batched_input_pos.size());
     node.producers.reserve(bind.shared_input_pos.size() + bind.batched_input_pos.size() + 1);
@@ -438,7 +454,7 @@ struct Executor::Impl {
   void ghosts(Fiber& fb, int count) {
     auto& nodes = ex.nodes_;
     for (int k = 0; k < count; ++k) {
-      DFGNode node;
+      DFGNode node = recycled_node();
       node.id = static_cast<int>(nodes.size());
       node.sig_id = m.kernels.ghost_sig;
       node.instance = fb.instance;
@@ -847,7 +863,14 @@ EvalResult Executor::run() {
   I.trace.total_nodes = static_cast<long>(nodes_.size());
   for (const auto& n : nodes_) I.trace.dfg_edges += static_cast<long>(n.producers.size());
   res.trace = std::move(I.trace);
-  if (I.opts.record_nodes) res.nodes = std::move(nodes_);
+  if (I.opts.record_nodes) {
+    res.nodes = std::move(nodes_);
+  } else {  // back to the session's pool for the next evaluation
+    auto& pool = I.s.node_pool();
+    pool.reserve(pool.size() + nodes_.size());
+    for (auto& n : nodes_) pool.push_back(std::move(n));
+    nodes_.clear();
+  }
   for (auto& [a, b] : I.flush_events) {
     float ms = 0;
     cudaEventElapsedTime(&ms, a, b);
