@@ -73,7 +73,7 @@ struct mbx_ctx {
   // launches that need all their CTAs resident at once (mbx_tc_levels: grid barrier, cross-CTA
   // counters) are chained through a per-device lane — each waits for the previous one to
   // complete — so two of them are never partially resident together; everything else overlaps.
-  bool serialize_persistent = false;
+  bool serialize_persistent = true;  // every context: any two may run concurrently on a device
   cudaEvent_t ev_persist = nullptr;
   // HBM arena: one virtual-address reservation, physical chunks mapped on demand, so offsets
   // (the reference's TensorHandle::offset) are stable while the arena grows.

@@ -50,7 +50,6 @@ int mbx_pool_create(int device, int precision, const char* model, int hidden, un
   for (int t = 0; t < threads; ++t) {
     mbx_ctx* c = nullptr;
     if (mbx_ctx_create(device, precision, &c)) return fail(mbx_last_error(nullptr));
-    c->serialize_persistent = true;
     p->ctxs.push_back(c);
     mbx_model* m = nullptr;
     if (mbx_model_create(c, model, hidden, &m)) return fail(mbx_last_error(c));
