@@ -33,9 +33,14 @@ void cu_check(CUresult r, const char* what) {
 }
 
 namespace {
+// One per device: a stream of its own that every co-residency-requiring launch of every context
+// on the device goes through (in host submission order), so two such kernels never run
+// concurrently, back-to-back kernels in it start with little gap, and the contexts' own streams
+// stay free for everything else.
 struct PersistentLane {
-  std::mutex mu;  // held from begin to end: the wait and the record enclose one launch
-  cudaEvent_t last = nullptr;
+  std::mutex mu;  // held from begin to end: the dependency edges enclose one launch
+  cudaStream_t stream = nullptr;
+  cudaEvent_t done = nullptr;
 };
 PersistentLane& lane_of(int device) {
   static std::mutex m;
@@ -47,31 +52,31 @@ PersistentLane& lane_of(int device) {
 }
 }  // namespace
 
-void persistent_lane_begin(mbx_ctx* c) {
-  if (!c->serialize_persistent || c->dry) return;
+cudaStream_t persistent_lane_begin(mbx_ctx* c) {
+  if (!c->serialize_persistent || c->dry) return c->stream;
   PersistentLane& L = lane_of(c->device);
   L.mu.lock();
-  if (L.last) cuda_check(cudaStreamWaitEvent(c->stream, L.last, 0), "persistent lane wait");
-}
-
-void persistent_lane_forget(mbx_ctx* c) {
-  if (!c->serialize_persistent || c->dry || !c->ev_persist) return;
-  PersistentLane& L = lane_of(c->device);
-  std::lock_guard<std::mutex> lock(L.mu);
-  if (L.last == c->ev_persist) {
-    cudaEventSynchronize(c->ev_persist);
-    L.last = nullptr;
+  if (!L.stream) {
+    cuda_check(cudaStreamCreateWithFlags(&L.stream, cudaStreamNonBlocking), "persistent lane stream");
+    cuda_check(cudaEventCreateWithFlags(&L.done, cudaEventDisableTiming), "persistent lane event");
   }
+  if (!c->ev_persist) cuda_check(cudaEventCreateWithFlags(&c->ev_persist, cudaEventDisableTiming), "event");
+  // The launch follows this context's work so far ...
+  cuda_check(cudaEventRecord(c->ev_persist, c->stream), "persistent lane record");
+  cuda_check(cudaStreamWaitEvent(L.stream, c->ev_persist, 0), "persistent lane wait");
+  return L.stream;
 }
 
 void persistent_lane_end(mbx_ctx* c) {
   if (!c->serialize_persistent || c->dry) return;
   PersistentLane& L = lane_of(c->device);
-  if (!c->ev_persist) cuda_check(cudaEventCreateWithFlags(&c->ev_persist, cudaEventDisableTiming), "event");
-  cuda_check(cudaEventRecord(c->ev_persist, c->stream), "persistent lane record");
-  L.last = c->ev_persist;
+  // ... and this context's later work follows the launch.
+  cuda_check(cudaEventRecord(L.done, L.stream), "persistent lane record");
+  cuda_check(cudaStreamWaitEvent(c->stream, L.done, 0), "persistent lane wait");
   L.mu.unlock();
 }
+
+void persistent_lane_forget(mbx_ctx* c) { (void)c; }
 
 void stream_wait_own(mbx_ctx* c, const char* what) {
   if (c->dry) return;

@@ -114,9 +114,10 @@ namespace mbx {
 
 // Throws mbatch::Error on CUDA failure.
 void cuda_check(cudaError_t e, const char* what);
-// The per-device persistent-launch lane (see mbx_ctx::serialize_persistent): makes c->stream
-// wait for the previous lane launch; after the launch, persistent_lane_end records it.
-void persistent_lane_begin(mbx_ctx* c);
+// The per-device persistent-launch lane (see mbx_ctx::serialize_persistent): returns the stream
+// to launch on (the lane's, ordered after c->stream's work so far); persistent_lane_end orders
+// c->stream's later work after the launch.
+cudaStream_t persistent_lane_begin(mbx_ctx* c);
 void persistent_lane_end(mbx_ctx* c);
 void persistent_lane_forget(mbx_ctx* c);  // before destroying c (its event may be the lane's last)
 // Waits for everything this context enqueued so far (an event: on a pool's shared stream it does

@@ -1150,7 +1150,7 @@ void issue_levels(mbx_ctx* c, const std::vector<BatchLaunch>& Ls, size_t i, int 
   // Grid barrier (several levels) or cross-cluster counters (L2 exchange): every CTA must be
   // resident at once, so such launches take the device's persistent lane.
   const bool lane = n > 1 || (C.xch == 1 && C.S > 1);
-  if (lane) persistent_lane_begin(c);
+  if (lane) lc.stream = persistent_lane_begin(c);
   const cudaError_t le = cudaLaunchKernelExC(&lc, C.fn, args);
   if (lane) persistent_lane_end(c);
   cuda_check(le, "multi-level tensor-core kernel");
