@@ -92,6 +92,10 @@ struct ExecOptions {
   bool time_batches = false;    // CUDA events around every batch launch
   bool inputs_resident = false; // inputs already materialised by an identical previous call
   bool outputs_on_device = false;
+  // Return once the device work and the output read-back are enqueued (no final sync, outputs not
+  // decoded): the caller synchronises the context's stream before reusing the context.  Used by
+  // the throughput pool to keep two mini-batches in flight per worker.
+  bool defer_sync = false;
 };
 
 // Static block of the compiled model (the reference's analysis::StaticBlock + hoist depth).

@@ -129,6 +129,8 @@ typedef struct {
                                 skip their H2D copy (device-resident benchmarking) */
   int32_t outputs_on_device; /* leave outputs in the arena (no D2H; outputs read back as 0) */
   int32_t ghost;        /* ghost units of the lowered program (ExecOptions::ghost) */
+  int32_t defer_sync;   /* return with the work and the output read-back enqueued; outputs not
+                           decoded; synchronise (mbx_sync) before reusing the context */
 } mbx_options;
 void mbx_options_default(mbx_options* o);
 

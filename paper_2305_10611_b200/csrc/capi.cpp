@@ -356,6 +356,7 @@ void mbx_options_default(mbx_options* o) {
   o->time_batches = 0;
   o->inputs_resident = 0;
   o->outputs_on_device = 0;
+  o->defer_sync = 0;
   o->ghost = 1;
 }
 
@@ -385,6 +386,7 @@ int mbx_evaluate_batch(mbx_model* m, int batch, const int32_t* toks, int64_t nto
     o.time_batches = oo.time_batches != 0;
     o.inputs_resident = oo.inputs_resident != 0;
     o.outputs_on_device = oo.outputs_on_device != 0;
+    o.defer_sync = oo.defer_sync != 0;
     o.ghost = oo.ghost != 0;
     res->r = m->session->evaluate(inputs, o);
     for (auto& v : res->r.outputs) encode(v, res->out_tok, res->out_data);

@@ -20,8 +20,11 @@
 #include "ctx.h"
 #include "mbx.h"
 
+constexpr int kInFlight = 2;  // contexts (mini-batches in flight) per worker
+
 struct mbx_pool {
   int device = 0;
+  int threads = 1;
   cudaStream_t stream = nullptr;
   std::vector<mbx_ctx*> ctxs;
   std::vector<mbx_model*> models;
@@ -47,7 +50,9 @@ int mbx_pool_create(int device, int precision, const char* model, int hidden, un
     if (cudaSetDevice(device) != cudaSuccess) return fail("cudaSetDevice");
     if (cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking) != cudaSuccess) return fail("stream");
   }
-  for (int t = 0; t < threads; ++t) {
+  // Two contexts per worker: a worker builds its next mini-batch's DFG on one while the device
+  // still runs the previous one on the other (deferred sync), so each keeps two in flight.
+  for (int t = 0; t < threads * kInFlight; ++t) {
     mbx_ctx* c = nullptr;
     if (mbx_ctx_create(device, precision, &c)) return fail(mbx_last_error(nullptr));
     p->ctxs.push_back(c);
@@ -56,6 +61,7 @@ int mbx_pool_create(int device, int precision, const char* model, int hidden, un
     p->models.push_back(m);
     if (mbx_model_make_params(m, param_seed)) return fail(mbx_last_error(c));
   }
+  p->threads = threads;
   *out = p.release();
   return 0;
 }
@@ -70,10 +76,10 @@ void mbx_pool_destroy(mbx_pool* p) {
 }
 
 const char* mbx_pool_last_error(const mbx_pool* p) { return p ? p->err.c_str() : ""; }
-int mbx_pool_threads(const mbx_pool* p) { return p ? int(p->ctxs.size()) : 0; }
+int mbx_pool_threads(const mbx_pool* p) { return p ? p->threads : 0; }
 void* mbx_pool_stream(mbx_pool* p) { return p ? reinterpret_cast<void*>(p->stream) : nullptr; }
 mbx_model* mbx_pool_model(mbx_pool* p, int worker) {
-  return p && worker >= 0 && worker < int(p->models.size()) ? p->models[size_t(worker)] : nullptr;
+  return p && worker >= 0 && worker < p->threads ? p->models[size_t(worker) * kInFlight] : nullptr;
 }
 
 int mbx_pool_run(mbx_pool* p, int n, int batch, const int32_t* const* toks, const int64_t* ntok,
@@ -84,24 +90,37 @@ int mbx_pool_run(mbx_pool* p, int n, int batch, const int32_t* const* toks, cons
 int mbx_pool_run_timed(mbx_pool* p, int n, int batch, const int32_t* const* toks, const int64_t* ntok,
                        const float* const* data, const int64_t* ndata, const mbx_options* opts,
                        int64_t* total_nodes, double* device_ms) {
-  const int T = int(p->ctxs.size());
-  // Device time of the whole run: an event in every worker stream before any work (the streams
+  const int T = p->threads;
+  const int C = int(p->ctxs.size());
+  // Device time of the whole run: an event in every context stream before any work (the streams
   // are idle, so they fire at once) and after all of it; the span is first start -> last end.
-  std::vector<cudaEvent_t> ev0(size_t(T), nullptr), ev1(size_t(T), nullptr);
+  std::vector<cudaEvent_t> ev0(size_t(C), nullptr), ev1(size_t(C), nullptr);
   const bool timed = device_ms && p->device >= 0;
   if (timed)
-    for (int w = 0; w < T; ++w) {
+    for (int w = 0; w < C; ++w) {
       cudaEventCreate(&ev0[size_t(w)]);
       cudaEventCreate(&ev1[size_t(w)]);
       cudaEventRecord(ev0[size_t(w)], p->ctxs[size_t(w)]->stream);
     }
+  mbx_options o;
+  mbx_options_default(&o);
+  if (opts) o = *opts;
+  o.defer_sync = 1;
   std::atomic<int64_t> nodes{0};
   std::vector<std::string> errs(static_cast<size_t>(T));
   auto work = [&](int w) {
-    for (int i = w; i < n; i += T) {
+    int k = 0;
+    for (int i = w; i < n; i += T, ++k) {
+      const int ci = w * kInFlight + (k % kInFlight);
+      mbx_ctx* c = p->ctxs[size_t(ci)];
+      // The context's previous mini-batch must be done before its arena and staging are reused.
+      if (k >= kInFlight && mbx_sync(c)) {
+        errs[size_t(w)] = mbx_last_error(c);
+        return;
+      }
       mbx_result* r = nullptr;
-      if (mbx_evaluate_batch(p->models[size_t(w)], batch, toks[i], ntok[i], data[i], ndata[i], opts, &r)) {
-        errs[size_t(w)] = mbx_last_error(p->ctxs[size_t(w)]);
+      if (mbx_evaluate_batch(p->models[size_t(ci)], batch, toks[i], ntok[i], data[i], ndata[i], &o, &r)) {
+        errs[size_t(w)] = mbx_last_error(c);
         return;
       }
       int64_t cnt[9];
@@ -109,6 +128,7 @@ int mbx_pool_run_timed(mbx_pool* p, int n, int batch, const int32_t* const* toks
       nodes += cnt[1];
       mbx_result_destroy(r);
     }
+    for (int q = 0; q < kInFlight; ++q) mbx_sync(p->ctxs[size_t(w * kInFlight + q)]);
   };
   std::vector<std::thread> th;
   for (int w = 1; w < T && w < n; ++w) th.emplace_back(work, w);
@@ -116,17 +136,17 @@ int mbx_pool_run_timed(mbx_pool* p, int n, int batch, const int32_t* const* toks
   for (auto& t : th) t.join();
   if (timed) {
     double span = 0.0;
-    for (int w = 0; w < T; ++w) {
+    for (int w = 0; w < C; ++w) {
       cudaEventRecord(ev1[size_t(w)], p->ctxs[size_t(w)]->stream);
       cudaEventSynchronize(ev1[size_t(w)]);
     }
-    for (int a = 0; a < T; ++a)
-      for (int b = 0; b < T; ++b) {
+    for (int a = 0; a < C; ++a)
+      for (int b = 0; b < C; ++b) {
         float ms = 0.0f;
         if (cudaEventElapsedTime(&ms, ev0[size_t(a)], ev1[size_t(b)]) == cudaSuccess) span = std::max(span, double(ms));
       }
     *device_ms = span;
-    for (int w = 0; w < T; ++w) {
+    for (int w = 0; w < C; ++w) {
       cudaEventDestroy(ev0[size_t(w)]);
       cudaEventDestroy(ev1[size_t(w)]);
     }

@@ -679,7 +679,9 @@ struct Executor::Impl {
     return out;
   }
 
-  void pack_to_host(const std::vector<int64_t>& ranges, float* dst, size_t total) {
+  // sync = false (defer_sync): the read-back is enqueued, the copy out of the pinned buffer is
+  // the caller's business after it synchronises.
+  void pack_to_host(const std::vector<int64_t>& ranges, float* dst, size_t total, bool sync = true) {
     mbx::meta_reserve(c, ranges.size() * 8 + 64);
     size_t moff = mbx::meta_stage(c, ranges.data(), ranges.size() * 8);
     mbx::meta_commit(c);
@@ -691,8 +693,10 @@ struct Executor::Impl {
     ++timing.device_launches;
     mbx::cuda_check(cudaMemcpyAsync(c->d2h_host, c->d2h_dev, total * sizeof(float), cudaMemcpyDeviceToHost, c->stream),
                     "D2H");
-    mbx::stream_wait_own(c, "D2H sync");
-    std::memcpy(dst, c->d2h_host, total * sizeof(float));
+    if (sync) {
+      mbx::stream_wait_own(c, "D2H sync");
+      std::memcpy(dst, c->d2h_host, total * sizeof(float));
+    }
     timing.d2h_bytes += long(total * sizeof(float));
     timing.h2d_bytes += long(ranges.size() * 8);
   }
@@ -850,8 +854,9 @@ EvalResult Executor::run() {
   }
   auto t_host = clk::now();
   std::vector<float> buf(total, 0.0f);
-  if (!I.c->dry && total > 0 && !I.opts.outputs_on_device) I.pack_to_host(ranges, buf.data(), total);
-  else if (!I.c->dry) mbx::stream_wait_own(I.c, "final sync");
+  const bool defer = I.opts.defer_sync && !I.c->dry;
+  if (!I.c->dry && total > 0 && !I.opts.outputs_on_device) I.pack_to_host(ranges, buf.data(), total, !defer);
+  else if (!I.c->dry && !defer) mbx::stream_wait_own(I.c, "final sync");
   if (I.c->copy_pending) {  // inputs no kernel read: the pinned staging is reused next call
     mbx::cuda_check(cudaEventSynchronize(I.c->ev_copy), "input copy");
     I.c->copy_pending = false;
@@ -859,7 +864,8 @@ EvalResult Executor::run() {
 
   EvalResult res;
   size_t cursor = 0, ti = 0;
-  for (size_t i = 0; i < I.inputs.size(); ++i) res.outputs.push_back(I.to_host(fibers_[i]->result, buf, cursor, ti, hs));
+  if (!defer)  // deferred: the outputs are read back but not decoded
+    for (size_t i = 0; i < I.inputs.size(); ++i) res.outputs.push_back(I.to_host(fibers_[i]->result, buf, cursor, ti, hs));
   I.trace.total_nodes = static_cast<long>(nodes_.size());
   for (const auto& n : nodes_) I.trace.dfg_edges += static_cast<long>(n.producers.size());
   res.trace = std::move(I.trace);

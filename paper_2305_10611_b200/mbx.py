@@ -31,7 +31,7 @@ class MbatchError(RuntimeError):
 class _Opts(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int32) for n in
                 ("scheduler", "gather", "hoist", "phases", "record_nodes", "time_kernels", "time_batches",
-                 "inputs_resident", "outputs_on_device", "ghost")]
+                 "inputs_resident", "outputs_on_device", "ghost", "defer_sync")]
 
 
 _lib = None
