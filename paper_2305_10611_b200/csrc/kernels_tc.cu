@@ -41,7 +41,7 @@ constexpr int kM = 128;
 constexpr int kRawStages = 3;  // MBX_RAW in tc_gate.cuh
 constexpr int kMaxTail = 24;
 constexpr int kSmemBudget = 227 * 1024;
-constexpr int kLevelsStaticSmem = 64 * 32 + 64;  // mbx_tc_levels: its copy of the level table
+constexpr int kLevelsStaticSmem = 64 * int(sizeof(TcLevel)) + 64;  // mbx_tc_levels: its copy of the level table
 
 // ---- tail IR: a plan's steps after the contraction as ops over per-element values --------------
 enum : int8_t { kSrcNone = 0, kSrcSlot = 1, kSrcAcc = 2, kSrcBatched = 3, kSrcShared = 4, kSrcLoad = 5 };
@@ -1004,7 +1004,6 @@ int plan_levels(mbx_ctx* c, const std::vector<BatchLaunch>& Ls, size_t i, size_t
     if (L.plan_id != L0.plan_id || !L.gathers.empty()) break;
     // Same weights and shared inputs: one resident weight slice serves every level.
     if (std::memcmp(c->meta.host + L.shared_meta, sh0, ns * 8) != 0) break;
-    if (!rows_vec16(c, st, pe, L)) break;
   }
   const int n = int(j - i);
   if (n < 1) return 0;
@@ -1062,6 +1061,8 @@ int plan_levels(mbx_ctx* c, const std::vector<BatchLaunch>& Ls, size_t i, size_t
     tbl[q].out_base = meta_dev<long long>(c, L.out_meta);
     tbl[q].b = L.b;
     tbl[q].nt = nts[size_t(q)];
+    tbl[q].vec16 = rows_vec16(c, st, pe, L) ? 1 : 0;
+    tbl[q].pad = 0;
   }
   *table = meta_stage(c, tbl.data(), tbl.size() * sizeof(TcLevel));
   return n;

@@ -41,8 +41,10 @@ struct TcLevel {
   const long long* shared_off;
   const long long* batched_off;
   const long long* out_base;
-  int b;   // nodes in the batch
-  int nt;  // node tile (MMA N) used for this level: 16, 32, 64 or MBX_LNT
+  int b;      // nodes in the batch
+  int nt;     // node tile (MMA N) used for this level: 16, 32, 64 or MBX_LNT
+  int vec16;  // 1: every gathered row segment is 16-byte aligned (bulk / 16-byte copies)
+  int pad;
 };
 
 struct TcLevelsArgs {

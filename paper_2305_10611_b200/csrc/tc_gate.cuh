@@ -773,10 +773,24 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const
         {
           unsigned cy;
           asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(cy));
+          const int kb0 = c_begin * MBX_KC, kb1 = kb0 + MBX_LSLICE;
+          if (!L.vec16) {
+            // Rows not 16-byte aligned (bulk copies need it): every CTA copies all its rows itself,
+            // 4 bytes at a time, into the same staging layout; completion: wait, sync, one arrive.
+            for (int i = gt; i < nn * MBX_LSLICE; i += MBX_LGATHER) {
+              const int n = i / MBX_LSLICE, kk = kb0 + (i - n * MBX_LSLICE);
+              const int pc = (MBX_NPIECES > 1 && kk >= MBX_PK0) ? 1 : 0;
+              cp_async4(stage + n * MBX_LSROW + (kk - kb0) * 4, P.arena + rowbase[2 * n + pc] + kk - (pc ? MBX_PK0 : 0),
+                        true);
+            }
+            cp_async_commit();
+            cp_async_wait<0>();
+            named_sync(1, MBX_LGATHER);
+            if (gt == 0) mbar_arrive(&xraw[0]);
+          } else {
           if (gt == 0) mbar_expect_tx(&xraw[0], unsigned(nn * MBX_LSLICE * 4));
           // This CTA's share of the rows, each multicast to the whole cluster in one or two runs
           // (the slice may straddle the two concatenated pieces).
-          const int kb0 = c_begin * MBX_KC, kb1 = kb0 + MBX_LSLICE;
           const unsigned short mask = (unsigned short)((1u << MBX_LCY) - 1u);
           for (int n = int(cy) + MBX_LCY * gt; n < nn; n += MBX_LCY * MBX_LGATHER) {
 #pragma unroll
@@ -793,6 +807,7 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const
                   "l"(src), "r"(unsigned((r1 - r0) * 4)), "r"(smem_u32(&xraw[0])), "h"(mask)
                   : "memory");
             }
+          }
           }
         }
 #else
@@ -814,7 +829,12 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const
             const float* src = arena + (valid ? rowbase[2 * n + p1] + kin + qq * 4 : 0);
             float* dst = reinterpret_cast<float*>(xs + (n >> 3) * (MBX_KC * 16) + (n & 7) * 16 + ((qq >> 1) << 7) +
                                                   ((qq & 1) ? xlo : 0));
-            cp_async16(dst, src, valid);
+            if (L.vec16) {
+              cp_async16(dst, src, valid);
+            } else {
+#pragma unroll
+              for (int e = 0; e < 4; ++e) cp_async4(dst + e, src + e, valid);
+            }
           }
           asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&xraw[j])) : "memory");
         }
