@@ -647,8 +647,16 @@ void tc_prepare(mbx_ctx* c, PlanEntry& pe) {
     st->s_uc = std::min(st->U, 32);
     st->s_npc = std::max(1, std::min(kTcThreads / st->s_uc, 8));
     st->s_kb = st->K % 64 == 0 ? 64 : (st->K % 32 == 0 ? 32 : (st->K % 8 == 0 ? 8 : 0));
+    // Decision-feeding cells run a few nodes per launch, many times (NestedRNN's inner loops):
+    // narrow unit slices spread the weights over more CTAs, and the whole slice is staged in one
+    // go (one round trip) when it fits.
+    if (pe.force_vm && st->U % 8 == 0 && st->K % 8 == 0) {
+      st->s_uc = 8;
+      if ((st->G * st->K * 8 + st->s_npc * st->K) * 4 <= 160 * 1024) st->s_kb = st->K;
+    }
     if (st->s_kb > 0 && st->U % st->s_uc == 0) {
-      st->s_smem = 2 * (st->G * st->s_kb * st->s_uc + st->s_npc * st->s_kb) * 4;
+      const int nbuf = st->s_kb == st->K ? 1 : 2;
+      st->s_smem = nbuf * (st->G * st->s_kb * st->s_uc + st->s_npc * st->s_kb) * 4;
       const std::string ssrc = gen_small_source(*st);
       st->sfn = load_kernel(c, ssrc, "mbx_small_dense");
       pe.tc_exact = true;
