@@ -191,6 +191,21 @@ std::vector<BatchRecord> schedule_agenda(const std::vector<const DFGNode*>& node
 using ParamEnv = std::map<std::string, HostValue>;
 using InstanceInput = std::map<std::string, HostValue>;
 
+// Instance inputs / outputs in the C ABI's flat hostval encoding (include/mbx.h: int32 tokens +
+// float data, depth-first; per instance its @main instance inputs in module order).  Evaluating
+// from the encoding skips building HostValue trees on the way in and out (mbx_evaluate_batch).
+struct EncodedValues {
+  int count = 0;  // instances (inputs) / values (outputs)
+  const int32_t* toks = nullptr;
+  int64_t ntok = 0;
+  const float* data = nullptr;  // borrowed for the call
+  int64_t ndata = 0;
+};
+struct EncodedOutputs {
+  std::vector<int32_t> toks;
+  std::vector<float> data;
+};
+
 // A device session: context + the model's parameters resident in the arena (module order,
 // offsets identical to the reference's Executor, proj/src/executor.cpp:153-158) + the model's
 // registered plans.  device < 0 runs the host logic only (no kernels; tensor values are zero),
@@ -205,6 +220,8 @@ class Session {
   Session& operator=(const Session&) = delete;
   void set_params(const ParamEnv& params);
   EvalResult evaluate(const std::vector<InstanceInput>& inputs, const ExecOptions& opts);
+  // The same from / to the flat encoding (EvalResult::outputs stays empty; *out gets them).
+  EvalResult evaluate_encoded(const EncodedValues& inputs, const ExecOptions& opts, EncodedOutputs* out);
   const CompiledModel& model() const { return model_; }
   mbx_ctx* ctx() const { return ctx_; }
   int64_t params_end() const { return params_end_; }

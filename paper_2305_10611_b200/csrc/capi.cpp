@@ -366,12 +366,14 @@ int mbx_evaluate_batch(mbx_model* m, int batch, const int32_t* toks, int64_t nto
   auto res = std::make_unique<mbx_result>();
   int rc = guarded(m->ctx, [&] {
     MBATCH_CHECK(batch >= 1, "evaluate_batch: need at least one instance");
-    std::vector<mbatch::runtime::InstanceInput> inputs(batch);
-    int64_t ti = 0, di = 0;
-    for (int i = 0; i < batch; ++i)
-      for (auto& decl : m->cm.params)
-        if (decl.is_instance_input) inputs[i][decl.name] = decode(toks, ntok, ti, data, ndata, di);
-    MBATCH_CHECK(ti == ntok && di == ndata, "hostval encoding: trailing data");
+    // The inputs are materialised straight from the encoding (no HostValue trees; the tensor
+    // data is copied once, into pinned staging) and the outputs encoded straight from the run.
+    mbatch::runtime::EncodedValues enc;
+    enc.count = batch;
+    enc.toks = toks;
+    enc.ntok = ntok;
+    enc.data = data;
+    enc.ndata = ndata;
     mbatch::runtime::ExecOptions o;
     mbx_options d;
     mbx_options_default(&d);
@@ -388,8 +390,10 @@ int mbx_evaluate_batch(mbx_model* m, int batch, const int32_t* toks, int64_t nto
     o.outputs_on_device = oo.outputs_on_device != 0;
     o.defer_sync = oo.defer_sync != 0;
     o.ghost = oo.ghost != 0;
-    res->r = m->session->evaluate(inputs, o);
-    for (auto& v : res->r.outputs) encode(v, res->out_tok, res->out_data);
+    mbatch::runtime::EncodedOutputs out;
+    res->r = m->session->evaluate_encoded(enc, o, &out);
+    res->out_tok = std::move(out.toks);
+    res->out_data = std::move(out.data);
   });
   if (rc) return rc;
   *out = res.release();

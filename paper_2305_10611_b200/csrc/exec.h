@@ -183,6 +183,8 @@ class Executor {
 
   // -- runtime side -----------------------------------------------------------------------
   Executor(Session& s, const std::vector<InstanceInput>& inputs, const ExecOptions& opts);
+  // Inputs (and outputs, into *out) in the flat hostval encoding.
+  Executor(Session& s, const EncodedValues& inputs, const ExecOptions& opts, EncodedOutputs* out);
   ~Executor();
   EvalResult run();
 

@@ -275,6 +275,14 @@ EvalResult Session::evaluate(const std::vector<InstanceInput>& inputs, const Exe
   return ex.run();
 }
 
+EvalResult Session::evaluate_encoded(const EncodedValues& inputs, const ExecOptions& opts, EncodedOutputs* out) {
+  MBATCH_CHECK(inputs.count >= 1, "evaluate_batch: need at least one instance");
+  if (mbx_arena_rewind(ctx_, params_end_) != 0) throw Error(mbx_last_error(ctx_));
+  ctx_->persist_end = params_end_;
+  Executor ex(*this, inputs, opts, out);
+  return ex.run();
+}
+
 EvalResult evaluate_batch(const CompiledModel& model, const ParamEnv& params, const std::vector<InstanceInput>& inputs) {
   Session s(model, 0, MBX_PREC_FP32);
   s.set_params(params);
@@ -293,6 +301,10 @@ struct Executor::Impl {
   ExecOptions opts;
   mbx_ctx* c;
   const std::vector<InstanceInput>& inputs;
+  const EncodedValues* enc = nullptr;  // encoded inputs (inputs is empty then)
+  EncodedOutputs* enc_out = nullptr;
+  int batch = 0;                       // instances
+  std::vector<std::pair<int64_t, std::pair<const float*, int64_t>>> enc_tensors;  // (offset, (src, n))
   ScheduleTrace trace;
   std::unordered_map<std::string, int> memo;
   std::vector<const StaticBlockInfo*> block_by_id;
@@ -306,7 +318,7 @@ struct Executor::Impl {
   std::vector<int> batch_share;  // batches one timed launch covers (multi-level launches > 1)
 
   Impl(Executor& e, Session& sess, const std::vector<InstanceInput>& in, const ExecOptions& o)
-      : ex(e), s(sess), m(sess.model()), opts(o), c(sess.ctx()), inputs(in) {
+      : ex(e), s(sess), m(sess.model()), opts(o), c(sess.ctx()), inputs(in), batch(int(in.size())) {
     int maxid = -1;
     for (const auto& b : m.blocks) maxid = std::max(maxid, b.id);
     block_by_id.assign(maxid + 1, nullptr);
@@ -352,6 +364,109 @@ struct Executor::Impl {
     throw Error("unreachable");
   }
 
+  // The flat-encoding counterpart of materialize(decode(...)): same arena order (list elements
+  // back to front, like the reference's cons cells), same errors as the C ABI's decoder.
+  void skip_enc(int64_t& ti, int64_t& di) {
+    const int32_t* t = enc->toks;
+    MBATCH_CHECK(ti < enc->ntok, "hostval encoding truncated");
+    const int kind = t[ti++];
+    if (kind == 0) {
+      MBATCH_CHECK(ti + 2 <= enc->ntok, "hostval encoding truncated");
+      di += int64_t(t[ti]) * t[ti + 1];
+      ti += 2;
+    } else if (kind == 1) {
+      ++ti;
+    } else if (kind >= 2 && kind <= 4) {
+      if (kind == 4) ++ti;
+      MBATCH_CHECK(ti < enc->ntok, "hostval encoding truncated");
+      const int n = t[ti++];
+      for (int k = 0; k < n; ++k) skip_enc(ti, di);
+    } else {
+      throw Error("hostval encoding: bad kind " + std::to_string(kind));
+    }
+  }
+  Val materialize_enc(int64_t& ti, int64_t& di) {
+    const int32_t* t = enc->toks;
+    MBATCH_CHECK(ti < enc->ntok, "hostval encoding truncated");
+    const int kind = t[ti++];
+    switch (kind) {
+      case 0: {
+        MBATCH_CHECK(ti + 2 <= enc->ntok, "hostval encoding truncated");
+        const int r = t[ti++], cc = t[ti++];
+        const int64_t n = int64_t(r) * cc;
+        MBATCH_CHECK(r >= 0 && cc >= 0 && di + n <= enc->ndata, "hostval data truncated");
+        const int64_t off = mbx::arena_alloc(c, n);
+        enc_tensors.push_back({off, {enc->data + di, n}});
+        di += n;
+        return Val::tensor(TensorRef{-1, 0, TensorHandle{off, Shape{r, cc}}});
+      }
+      case 1: MBATCH_CHECK(ti < enc->ntok, "hostval encoding truncated"); return Val::integer(t[ti++]);
+      case 2: {
+        MBATCH_CHECK(ti < enc->ntok, "hostval encoding truncated");
+        const int n = t[ti++];
+        std::vector<std::pair<int64_t, int64_t>> at(static_cast<size_t>(n));
+        for (int k = 0; k < n; ++k) {
+          at[size_t(k)] = {ti, di};
+          skip_enc(ti, di);
+        }
+        const int64_t tend = ti, dend = di;
+        std::vector<Val> items(static_cast<size_t>(n));
+        for (int k = n; k-- > 0;) {
+          int64_t a = at[size_t(k)].first, b = at[size_t(k)].second;
+          items[size_t(k)] = materialize_enc(a, b);
+        }
+        ti = tend;
+        di = dend;
+        return Val::list(std::move(items));
+      }
+      case 3:
+      case 4: {
+        int ctor = 0;
+        if (kind == 4) {
+          MBATCH_CHECK(ti < enc->ntok, "hostval encoding truncated");
+          ctor = t[ti++];
+        }
+        MBATCH_CHECK(ti < enc->ntok, "hostval encoding truncated");
+        const int n = t[ti++];
+        std::vector<Val> items;
+        items.reserve(size_t(n));
+        for (int k = 0; k < n; ++k) items.push_back(materialize_enc(ti, di));
+        if (kind == 3) return Val::tuple(std::move(items));
+        return Val::seq(Val::kAdt, std::move(items), ctor ? 1 : 0);
+      }
+    }
+    throw Error("hostval encoding: bad kind " + std::to_string(kind));
+  }
+
+  // to_host + the C ABI's encode in one pass.
+  void to_tokens(const Val& v, const std::vector<float>& buf, size_t& cursor, size_t& ti,
+                 const std::vector<TensorHandle>& hs, EncodedOutputs& out) {
+    switch (v.kind) {
+      case Val::kTensor: {
+        const TensorHandle& h = hs[ti++];
+        out.toks.push_back(0);
+        out.toks.push_back(h.shape.rows);
+        out.toks.push_back(h.shape.cols);
+        out.data.insert(out.data.end(), buf.begin() + cursor, buf.begin() + cursor + h.size());
+        cursor += h.size();
+        return;
+      }
+      case Val::kInt:
+        out.toks.push_back(1);
+        out.toks.push_back(int32_t(v.i));
+        return;
+      default:
+        if (v.kind == Val::kList) out.toks.push_back(2);
+        else if (v.kind == Val::kTuple) out.toks.push_back(3);
+        else {
+          out.toks.push_back(4);
+          out.toks.push_back(v.ctor == 1 ? 1 : 0);
+        }
+        out.toks.push_back(int32_t(v.size()));
+        for (size_t k = 0; k < v.size(); ++k) to_tokens(v.at(k), buf, cursor, ti, hs, out);
+    }
+  }
+
   void upload_inputs() {
     int64_t n = c->used - input_base;
     if (n <= 0 || opts.inputs_resident) return;
@@ -359,6 +474,8 @@ struct Executor::Impl {
     for (auto& [off, hv] : input_tensors)
       std::memcpy(c->in_host + (off - input_base), hv->ext ? hv->ext : hv->data.data(),
                   size_t(hv->shape.size()) * sizeof(float));
+    for (auto& [off, src] : enc_tensors)
+      std::memcpy(c->in_host + (off - input_base), src.first, size_t(src.second) * sizeof(float));
     if (opts.inputs_resident) return;
     if (!c->dry) {
       cudaStream_t cs = c->copy_stream ? c->copy_stream : c->stream;
@@ -729,6 +846,17 @@ struct Executor::Impl {
 
 Executor::Executor(Session& s, const std::vector<InstanceInput>& inputs, const ExecOptions& opts)
     : impl_(std::make_unique<Impl>(*this, s, inputs, opts)) {}
+
+namespace {
+const std::vector<InstanceInput> kNoInputs;
+}
+
+Executor::Executor(Session& s, const EncodedValues& inputs, const ExecOptions& opts, EncodedOutputs* out)
+    : impl_(std::make_unique<Impl>(*this, s, kNoInputs, opts)) {
+  impl_->enc = &inputs;
+  impl_->enc_out = out;
+  impl_->batch = inputs.count;
+}
 Executor::~Executor() = default;
 
 int Executor::emit(Fiber& fb, int blk, std::initializer_list<const Val*> inputs) { return impl_->emit(fb, blk, inputs); }
@@ -801,13 +929,18 @@ EvalResult Executor::run() {
   const CompiledModel& m = I.m;
   I.input_base = I.c->used;
   std::vector<Val> param_vals;
-  for (size_t i = 0; i < I.inputs.size(); ++i) {
+  int64_t eti = 0, edi = 0;  // encoded inputs: cursor into the token / data streams
+  for (size_t i = 0; i < size_t(I.batch); ++i) {
     auto fb = std::make_unique<Fiber>();
     fb->id = static_cast<int>(fibers_.size());
     fb->instance = static_cast<int>(i);
     std::vector<Val> args;
     for (const auto& d : m.params) {
       if (d.is_instance_input) {
+        if (I.enc) {
+          args.push_back(I.materialize_enc(eti, edi));
+          continue;
+        }
         auto it = I.inputs[i].find(d.name);
         MBATCH_CHECK(it != I.inputs[i].end(), "missing instance input " + d.name);
         args.push_back(I.materialize(it->second));
@@ -819,6 +952,7 @@ EvalResult Executor::run() {
     fb->root = m.program->run(*this, *raw, std::move(args));
     fibers_.push_back(std::move(fb));
   }
+  if (I.enc) MBATCH_CHECK(eti == I.enc->ntok && edi == I.enc->ndata, "hostval encoding: trailing data");
   I.upload_inputs();
 
   while (true) {
@@ -843,7 +977,7 @@ EvalResult Executor::run() {
 
   // Outputs: one pack + one D2H for every tensor of every instance result.
   std::vector<TensorHandle> hs;
-  for (size_t i = 0; i < I.inputs.size(); ++i) I.collect_tensors(fibers_[i]->result, hs);
+  for (size_t i = 0; i < size_t(I.batch); ++i) I.collect_tensors(fibers_[i]->result, hs);
   std::vector<int64_t> ranges;
   size_t total = 0;
   for (const auto& h : hs) {
@@ -864,8 +998,14 @@ EvalResult Executor::run() {
 
   EvalResult res;
   size_t cursor = 0, ti = 0;
-  if (!defer)  // deferred: the outputs are read back but not decoded
-    for (size_t i = 0; i < I.inputs.size(); ++i) res.outputs.push_back(I.to_host(fibers_[i]->result, buf, cursor, ti, hs));
+  if (!defer) {  // deferred: the outputs are read back but not decoded
+    if (I.enc_out) {
+      for (size_t i = 0; i < size_t(I.batch); ++i) I.to_tokens(fibers_[i]->result, buf, cursor, ti, hs, *I.enc_out);
+      I.enc_out->toks.shrink_to_fit();
+    } else {
+      for (size_t i = 0; i < size_t(I.batch); ++i) res.outputs.push_back(I.to_host(fibers_[i]->result, buf, cursor, ti, hs));
+    }
+  }
   I.trace.total_nodes = static_cast<long>(nodes_.size());
   for (const auto& n : nodes_) I.trace.dfg_edges += static_cast<long>(n.producers.size());
   res.trace = std::move(I.trace);
