@@ -273,7 +273,7 @@ def run_ours(args):
     model = mbx.Model(ctx, args.model, args.hidden)
     model.make_params(args.seed)
     seed = args.seed + rank
-    toks, data = model.make_inputs(seed, args.batch)
+    toks, data = pinned_inputs(torch, *model.make_inputs(seed, args.batch))
     stream = torch.cuda.ExternalStream(ctx.stream(), device=local)
     l2 = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")
 
@@ -449,6 +449,13 @@ def other_configs(mbx, torch, local, reps=5):
     return out
 
 
+def pinned_inputs(torch, toks, data):
+    """The hostval-encoded inputs with the float data stream in page-locked host memory."""
+    pd = torch.empty(data.size, dtype=torch.float32, pin_memory=True).numpy()
+    pd[:] = data
+    return toks, pd
+
+
 def run_pool(args, mbx, torch, local, rank, world, nodes, l2):
     """Throughput: T worker threads, each evaluating its own mini-batch per step (mbx_pool_run).
     Returns value / e2e nodes/s and the per-step device times (CUDA events on the pool stream)."""
@@ -457,7 +464,9 @@ def run_pool(args, mbx, torch, local, rank, world, nodes, l2):
     pool = mbx.Pool(local, args.precision, args.model, args.hidden, args.seed, T)
     ctx = mbx.Context(-1, args.precision)  # host-only: the synthetic inputs
     gen = mbx.Model(ctx, args.model, args.hidden)
-    ins = [gen.make_inputs(args.seed + rank * T + w, args.batch) for w in range(T)]
+    # Host inputs in pinned memory (the e2e contract: H2D from pinned host buffers): the library
+    # then copies each mini-batch's data stream in one piece and scatters it on the device.
+    ins = [pinned_inputs(torch, *gen.make_inputs(args.seed + rank * T + w, args.batch)) for w in range(T)]
     def steps(K, kw):
         ms, total = 0.0, 0
         for _ in range(K):

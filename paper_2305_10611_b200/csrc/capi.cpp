@@ -156,6 +156,9 @@ void mbx_ctx_destroy(mbx_ctx* c) {
       cudaStreamDestroy(c->copy_stream);
     }
     if (c->ev_copy) cudaEventDestroy(c->ev_copy);
+    if (c->in_dev) cudaFree(c->in_dev);
+    if (c->scat_host) cudaFreeHost(c->scat_host);
+    if (c->scat_dev) cudaFree(c->scat_dev);
     if (c->owns_stream) cudaStreamDestroy(c->stream);
   } else {
     std::free(c->meta.host);

@@ -69,6 +69,13 @@ struct mbx_ctx {
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t ev_copy = nullptr;
   bool copy_pending = false;
+  // Inputs already in pinned host memory (the caller's): one H2D of the whole data stream into
+  // in_dev, then a scatter kernel to the arena offsets (both on copy_stream) — no host memcpy.
+  float* in_dev = nullptr;
+  size_t in_dev_cap = 0;  // floats
+  int64_t* scat_host = nullptr;  // pinned (src, size, dst) triples
+  int64_t* scat_dev = nullptr;
+  size_t scat_cap = 0;  // triples
   // Contexts on one device that run concurrently (a pool's workers, each on its own stream):
   // launches that need all their CTAs resident at once (mbx_tc_levels: grid barrier, cross-CTA
   // counters) are chained through a per-device lane — each waits for the previous one to

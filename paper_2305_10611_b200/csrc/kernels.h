@@ -28,6 +28,7 @@ struct VmLaunch {
 cudaError_t launch_plan_vm(const VmLaunch& L, cudaStream_t stream);
 cudaError_t launch_gather_rows(float* arena, const int64_t* src_off, int64_t dst_off, int b, int size,
                                cudaStream_t stream);
+cudaError_t launch_scatter_ranges(const float* src, const int64_t* ranges, int n, float* arena, cudaStream_t stream);
 cudaError_t launch_pack_ranges(const float* arena, const int64_t* ranges, int n, float* dst,
                                cudaStream_t stream);
 cudaError_t launch_fill(float* arena, int64_t off, int64_t n, float v, cudaStream_t stream);

@@ -358,6 +358,16 @@ __global__ void pack_ranges_kernel(const float* arena, const int64_t* ranges, in
   }
 }
 
+// The inverse of pack_ranges: contiguous src -> arena ranges (mini-batch inputs copied H2D in one
+// piece from the caller's pinned buffer, then scattered to their arena offsets on the device).
+// ranges: (src offset, size, arena offset) triples.
+__global__ void scatter_ranges_kernel(const float* src, const int64_t* ranges, int n, float* arena) {
+  for (int r = blockIdx.x; r < n; r += gridDim.x) {
+    const int64_t so = ranges[3 * r], size = ranges[3 * r + 1], dof = ranges[3 * r + 2];
+    for (int64_t e = threadIdx.x; e < size; e += blockDim.x) arena[dof + e] = src[so + e];
+  }
+}
+
 // exec_primop on arena tensors of any size (backend.cpp:105-181), one output element per thread
 // (grid-stride), same arithmetic as the plan VM.
 __global__ void primop_kernel(float* arena, int op, int64_t a_off, int ar, int ac, int64_t b_off, int br, int bc,
@@ -415,6 +425,12 @@ cudaError_t launch_gather_rows(float* arena, const int64_t* src_off, int64_t dst
   int64_t total = int64_t(b) * size;
   int blocks = int(std::min<int64_t>((total + 255) / 256, 148 * 8));
   gather_rows_kernel<<<blocks, 256, 0, stream>>>(arena, src_off, dst_off, b, size);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_scatter_ranges(const float* src, const int64_t* ranges, int n, float* arena, cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  scatter_ranges_kernel<<<std::min(n, 148 * 4), 128, 0, stream>>>(src, ranges, n, arena);
   return cudaGetLastError();
 }
 

@@ -467,9 +467,51 @@ struct Executor::Impl {
     }
   }
 
+  // Encoded inputs whose data stream lies in pinned host memory: one H2D of the stream plus a
+  // device scatter, both on the copy stream.  Returns false when the data is pageable.
+  bool upload_pinned() {
+    if (!enc || c->dry || !c->copy_stream || enc_tensors.empty() || !input_tensors.empty()) return false;
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, enc->data) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    if (at.type != cudaMemoryTypeHost) return false;
+    const size_t nd = size_t(enc->ndata), nt = enc_tensors.size();
+    if (nd > c->in_dev_cap) {
+      if (c->in_dev) cudaFree(c->in_dev);
+      c->in_dev_cap = std::max(nd, c->in_dev_cap * 2);
+      mbx::cuda_check(cudaMalloc(&c->in_dev, c->in_dev_cap * sizeof(float)), "pinned input staging");
+    }
+    if (nt > c->scat_cap) {
+      if (c->scat_host) cudaFreeHost(c->scat_host);
+      if (c->scat_dev) cudaFree(c->scat_dev);
+      c->scat_cap = std::max(nt, c->scat_cap * 2);
+      mbx::cuda_check(cudaMallocHost(&c->scat_host, c->scat_cap * 3 * sizeof(int64_t)), "scatter table");
+      mbx::cuda_check(cudaMalloc(&c->scat_dev, c->scat_cap * 3 * sizeof(int64_t)), "scatter table");
+    }
+    for (size_t k = 0; k < nt; ++k) {
+      c->scat_host[3 * k] = int64_t(enc_tensors[k].second.first - enc->data);
+      c->scat_host[3 * k + 1] = enc_tensors[k].second.second;
+      c->scat_host[3 * k + 2] = enc_tensors[k].first;
+    }
+    cudaStream_t cs = c->copy_stream;
+    mbx::cuda_check(cudaMemcpyAsync(c->in_dev, enc->data, nd * sizeof(float), cudaMemcpyHostToDevice, cs), "input H2D");
+    mbx::cuda_check(cudaMemcpyAsync(c->scat_dev, c->scat_host, nt * 3 * sizeof(int64_t), cudaMemcpyHostToDevice, cs),
+                    "scatter table H2D");
+    mbx::cuda_check(mbx::launch_scatter_ranges(c->in_dev, c->scat_dev, int(nt), mbx::arena_ptr(c), cs), "input scatter");
+    ++c->launches;
+    ++timing.device_launches;
+    mbx::cuda_check(cudaEventRecord(c->ev_copy, cs), "input copy event");
+    c->copy_pending = true;
+    timing.h2d_bytes += long(nd * sizeof(float) + nt * 3 * sizeof(int64_t));
+    return true;
+  }
+
   void upload_inputs() {
     int64_t n = c->used - input_base;
     if (n <= 0 || opts.inputs_resident) return;
+    if (upload_pinned()) return;
     mbx::ensure_input_stage(c, size_t(n));
     for (auto& [off, hv] : input_tensors)
       std::memcpy(c->in_host + (off - input_base), hv->ext ? hv->ext : hv->data.data(),
