@@ -57,7 +57,11 @@ cudaStream_t persistent_lane_begin(mbx_ctx* c) {
   PersistentLane& L = lane_of(c->device);
   L.mu.lock();
   if (!L.stream) {
-    cuda_check(cudaStreamCreateWithFlags(&L.stream, cudaStreamNonBlocking), "persistent lane stream");
+    // Highest priority: when SMs free up, the block scheduler places the lane kernel's CTAs first
+    // (its resident CTAs wait at the grid barrier for the rest).
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    cuda_check(cudaStreamCreateWithPriority(&L.stream, cudaStreamNonBlocking, hi), "persistent lane stream");
     cuda_check(cudaEventCreateWithFlags(&L.done, cudaEventDisableTiming), "persistent lane event");
   }
   if (!c->ev_persist) cuda_check(cudaEventCreateWithFlags(&c->ev_persist, cudaEventDisableTiming), "event");
