@@ -230,9 +230,16 @@ class Session {
   // DFG node objects of earlier evaluations, kept with their vectors' capacity so the next
   // evaluation's node construction allocates nothing (implementation detail of the executor).
   std::vector<DFGNode>& node_pool() { return node_pool_; }
+  int64_t node_hint() const { return node_hint_; }
+  int64_t fiber_hint() const { return fiber_hint_; }
+  void set_hints(int64_t nodes, int64_t fibers) {
+    node_hint_ = nodes;
+    fiber_hint_ = fibers;
+  }
 
  private:
   std::vector<DFGNode> node_pool_;
+  int64_t node_hint_ = 0, fiber_hint_ = 0;
   const CompiledModel& model_;
   mbx_ctx* ctx_ = nullptr;
   bool owned_ = true;

@@ -2,7 +2,9 @@
 // exception) and turns it into a nonzero status plus mbx_last_error(ctx), so the boundary never
 // throws; the C++ surface (include/mbatch/*.hpp) rethrows the same text.
 #include <atomic>
+#include <cstdlib>
 #include <cstring>
+#include <malloc.h>
 #include <memory>
 
 #include "ctx.h"
@@ -109,6 +111,16 @@ int64_t mbx_kernel_launch_count(void) { return mbx::g_launches.load(); }
 
 int mbx_ctx_create(int device, int precision, mbx_ctx** out) {
   *out = nullptr;
+  // The runtime builds and frees a few hundred KB of DFG state per mini-batch on every worker
+  // thread: keep those blocks in the malloc arenas (no mmap/munmap or trim syscalls, which
+  // serialise in the kernel across threads).  Process-wide, set once.
+  static const bool tuned = [] {
+    if (std::getenv("MBX_NO_MALLOPT")) return false;
+    mallopt(M_MMAP_THRESHOLD, 64 << 20);
+    mallopt(M_TRIM_THRESHOLD, 512 << 20);
+    return true;
+  }();
+  (void)tuned;
   auto c = std::make_unique<mbx_ctx>();
   c->device = device;
   c->dry = device < 0;

@@ -1158,7 +1158,8 @@ void issue_levels(mbx_ctx* c, const std::vector<BatchLaunch>& Ls, size_t i, int 
   void* args[] = {&a};
   // Grid barrier (several levels) or cross-cluster counters (L2 exchange): every CTA must be
   // resident at once, so such launches take the device's persistent lane.
-  const bool lane = n > 1 || (C.xch == 1 && C.S > 1);
+  static const bool lane_all = std::getenv("MBX_LANE_ALL") != nullptr;  // experiment knob
+  const bool lane = lane_all || n > 1 || (C.xch == 1 && C.S > 1);
   if (lane) lc.stream = persistent_lane_begin(c);
   const cudaError_t le = cudaLaunchKernelExC(&lc, C.fn, args);
   if (lane) persistent_lane_end(c);

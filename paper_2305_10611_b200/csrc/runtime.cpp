@@ -971,6 +971,8 @@ EvalResult Executor::run() {
   const CompiledModel& m = I.m;
   I.input_base = I.c->used;
   std::vector<Val> param_vals;
+  nodes_.reserve(I.s.node_hint());    // the previous evaluation's node count: no regrowth
+  fibers_.reserve(I.s.fiber_hint());
   int64_t eti = 0, edi = 0;  // encoded inputs: cursor into the token / data streams
   for (size_t i = 0; i < size_t(I.batch); ++i) {
     auto fb = std::make_unique<Fiber>();
@@ -1051,6 +1053,7 @@ EvalResult Executor::run() {
   I.trace.total_nodes = static_cast<long>(nodes_.size());
   for (const auto& n : nodes_) I.trace.dfg_edges += static_cast<long>(n.producers.size());
   res.trace = std::move(I.trace);
+  I.s.set_hints(int64_t(nodes_.size()), int64_t(fibers_.size()));
   if (I.opts.record_nodes) {
     res.nodes = std::move(nodes_);
   } else {  // back to the session's pool for the next evaluation
