@@ -438,10 +438,10 @@ class Model:
                        gather: str = "fused", hoist: bool = True, phases: bool = True, record_nodes: bool = True,
                        time_kernels: bool = False, time_batches: bool = False, inputs_resident: bool = False,
                        outputs_on_device: bool = False, ghost: bool = True, decode: bool = True,
-                       trace: bool = True) -> EvalResult:
+                       trace: bool = True, defer_sync: bool = False) -> EvalResult:
         L = lib()
         o = make_options(scheduler, gather, hoist, phases, record_nodes, time_kernels, time_batches, inputs_resident,
-                         outputs_on_device, ghost)
+                         outputs_on_device, ghost, defer_sync)
         t = np.ascontiguousarray(toks, np.int32)
         d = np.ascontiguousarray(data, np.float32)
         r = ctypes.c_void_p()
@@ -455,7 +455,8 @@ class Model:
 
 def make_options(scheduler: str = "depth", gather: str = "fused", hoist: bool = True, phases: bool = True,
                  record_nodes: bool = False, time_kernels: bool = False, time_batches: bool = False,
-                 inputs_resident: bool = False, outputs_on_device: bool = False, ghost: bool = True) -> _Opts:
+                 inputs_resident: bool = False, outputs_on_device: bool = False, ghost: bool = True,
+                 defer_sync: bool = False) -> _Opts:
     o = _Opts()
     lib().mbx_options_default(ctypes.byref(o))
     o.scheduler = 1 if scheduler == "agenda" else 0
@@ -463,6 +464,7 @@ def make_options(scheduler: str = "depth", gather: str = "fused", hoist: bool = 
     o.hoist, o.phases, o.ghost = int(hoist), int(phases), int(ghost)
     o.record_nodes, o.time_kernels, o.time_batches = int(record_nodes), int(time_kernels), int(time_batches)
     o.inputs_resident, o.outputs_on_device = int(inputs_resident), int(outputs_on_device)
+    o.defer_sync = int(defer_sync)
     return o
 
 
