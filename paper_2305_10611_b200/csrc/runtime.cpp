@@ -939,6 +939,7 @@ void JoinAwait::await_suspend(std::coroutine_handle<> h) {
 
 std::vector<Val> JoinAwait::await_resume() {
   std::vector<Val> out;
+  out.reserve(fb->children.size());
   auto& fibers = ex->fibers();
   for (int id : fb->children) {
     Fiber& child = *fibers[id];
