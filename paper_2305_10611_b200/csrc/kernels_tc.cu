@@ -276,6 +276,7 @@ std::string gen_levels_source(const TcState& st, int k) {
   std::ostringstream o;
   if (stamps_enabled()) o << "#define MBX_STAMPS 1\n";
   if (std::getenv("MBX_FENCE_ONCE")) o << "#define MBX_FENCE_ONCE 1\n";
+  if (const char* e = std::getenv("MBX_POLLERS")) o << "#define MBX_POLLERS " << std::max(1, std::atoi(e)) << "\n";
   o << jit::prelude_source();
   o << "#define MBX_LEVELS_KERNEL 1\n"
     << "#define MBX_KC " << st.KC << "\n#define MBX_U " << st.U << "\n#define MBX_G " << st.G << "\n#define MBX_UC "

@@ -596,14 +596,38 @@ __device__ __forceinline__ void spin_until(const unsigned* ctr, unsigned target)
   while (int(ld_acquire_u32(ctr) - target) < 0)
     if (global_ns() - t0 > 2000000000ull) __trap();
 }
-// Grid-wide barrier over co-resident CTAs.  `target` = counter value once every CTA arrived.
-__device__ __forceinline__ void grid_barrier(unsigned* ctr, unsigned target) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    red_release_add(ctr, 1u);
-    spin_until(ctr, target);
+#ifndef MBX_POLLERS
+#define MBX_POLLERS 1  // warps whose lane 0 polls a wait counter, phase-staggered
+#endif
+// Block-wide wait (every thread calls it) until *ctr reaches target.  One L2 round trip of an
+// acquire load is ~0.6 us, so a single poller notices a release up to that late; MBX_POLLERS > 1
+// pollers started a fraction of a round trip apart sample the counter more often.  The first to
+// see it publishes `epoch` in *seen (shared) so the others stop; the thread that did the acquire
+// load then orders the block's later reads through the __syncthreads.  Measured on the TreeLSTM-512
+// b64 levels launch (ncu, 4 repeats): 1 poller 71.2-72.1 us, 4: 72.4-73.9, 8: 74.6-78.0 — the
+// extra polls contend with the arrivals on the counter's L2 line, so the default is one.
+__device__ __forceinline__ void block_wait(const unsigned* ctr, unsigned target, volatile unsigned* seen,
+                                           unsigned epoch) {
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0 && w < MBX_POLLERS) {
+    if (w) __nanosleep(unsigned(w) * (600u / MBX_POLLERS));
+    const unsigned long long t0 = global_ns();
+    while (*seen != epoch) {
+      if (int(ld_acquire_u32(ctr) - target) >= 0) {
+        *seen = epoch;
+        break;
+      }
+      if (global_ns() - t0 > 2000000000ull) __trap();
+    }
   }
   __syncthreads();
+}
+// Grid-wide barrier over co-resident CTAs.  `target` = counter value once every CTA arrived.
+__device__ __forceinline__ void grid_barrier(unsigned* ctr, unsigned target, volatile unsigned* seen,
+                                             unsigned epoch) {
+  __syncthreads();
+  if (threadIdx.x == 0) red_release_add(ctr, 1u);
+  block_wait(ctr, target, seen, epoch);
 }
 }  // namespace mbx_gen
 
@@ -611,7 +635,10 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const
   using namespace mbx_gen;
   extern __shared__ __align__(1024) unsigned char smem[];
   __shared__ TcLevel slv[64];  // the first 64 entries of the level table
+  __shared__ unsigned s_seen;  // block_wait: epoch of the last completed wait
+  unsigned wepoch = 0;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) s_seen = 0;
   const int tile_u = blockIdx.y;
   constexpr int S = MBX_LS;
   for (int i = tid; i < min(P.nlevels, 64); i += MBX_THREADS) slv[i] = P.levels[i];
@@ -1010,8 +1037,7 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const
         unsigned* flags = P.xflags + (grp * gridDim.y + tile_u) * S;
         if (tid < S && tid != int(rank)) red_release_add(flags + tid, 1u);
         MBX_LSTAMP(lv, 3);
-        if (tid == 0) spin_until(flags + rank, unsigned(S - 1) * (it + 1));
-        __syncthreads();
+        block_wait(flags + rank, unsigned(S - 1) * (it + 1), &s_seen, ++wepoch);
       }
       auto partial = [&](int q, int n, int col) -> float {
         return __ldcg(pbase + ((size_t)(int(rank) * S + q) * MBX_LLOC + n) * MBX_M + col);
@@ -1060,7 +1086,7 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const
       tc_fence_after();
       MBX_LSTAMP(lv, 5);
     }
-    if (lv + 1 < P.nlevels) grid_barrier(P.gbar, P.gbar_base + unsigned(lv + 1) * nctas);
+    if (lv + 1 < P.nlevels) grid_barrier(P.gbar, P.gbar_base + unsigned(lv + 1) * nctas, &s_seen, ++wepoch);
     MBX_LSTAMP(lv, 6);
   }
 #if MBX_LCY > 1
