@@ -104,7 +104,7 @@ struct TcState {
   // Few output columns (U x G <= 64): the bit-exact CUDA-core small-dense kernel instead of the
   // tensor cores, in every precision (sfn != nullptr).
   void* sfn = nullptr;
-  int s_npc = 0, s_uc = 0, s_kb = 0, s_smem = 0;
+  int s_npc = 0, s_uc = 0, s_kb = 0, s_st = 1, s_smem = 0;
   bool s_attr = false;
   bool attr_set = false;
   // Persistent multi-level variant (mbx_tc_levels): K-split ranks, maximal node tile, smem layout.
@@ -276,6 +276,7 @@ std::string gen_levels_source(const TcState& st, int k) {
   std::ostringstream o;
   if (stamps_enabled()) o << "#define MBX_STAMPS 1\n";
   if (std::getenv("MBX_FENCE_ONCE")) o << "#define MBX_FENCE_ONCE 1\n";
+  if (std::getenv("MBX_ARRIVE_RELEASE")) o << "#define MBX_ARRIVE_RELEASE 1\n";
   if (const char* e = std::getenv("MBX_POLLERS")) o << "#define MBX_POLLERS " << std::max(1, std::atoi(e)) << "\n";
   o << jit::prelude_source();
   o << "#define MBX_LEVELS_KERNEL 1\n"
@@ -297,7 +298,8 @@ std::string gen_small_source(const TcState& st) {
     << "#define MBX_KC 16\n#define MBX_K " << st.K << "\n#define MBX_U " << st.U << "\n#define MBX_G " << st.G
     << "\n#define MBX_NPIECES " << st.npieces << "\n#define MBX_PK0 " << st.piece_k[0] << "\n#define MBX_NLOADS "
     << st.prog.nloads << "\n#define MBX_NOUT " << st.prog.nout << "\n#define MBX_SNPC " << st.s_npc
-    << "\n#define MBX_SUC " << st.s_uc << "\n#define MBX_SKB " << st.s_kb << "\n";
+    << "\n#define MBX_SUC " << st.s_uc << "\n#define MBX_SKB " << st.s_kb << "\n#define MBX_SST " << st.s_st
+    << "\n";
   o << gen_tail(st.prog, false, false, true);
   o << jit::kernel_source();
   return o.str();
@@ -496,7 +498,7 @@ bool levels_layout(TcState& st, int k) {
   if (k == 0)
     while (CY * 2 <= cy_max && utiles % (CY * 2) == 0) CY *= 2;
   // deep: largest S first (smallest resident weight slice), then the largest node tile; wide:
-  // the largest node tile first (fewest tile rounds), then the smallest S that fits with it.
+  // the smallest S that fits, then the largest node tile.
   auto try_cfg = [&](int S, int NT) {
     if (st.nchunks % S != 0 || utiles * S > 148) return false;
     const int cpr = st.nchunks / S;
@@ -531,13 +533,24 @@ bool levels_layout(TcState& st, int k) {
     for (int NT : {128, 64, 32})
       if (try_cfg(force_s, NT)) return true;
   }
+  static const std::pair<int, int> force_wide = [] {  // experiment: MBX_LEVELS_WIDE=S,NT
+    const char* e = std::getenv("MBX_LEVELS_WIDE");
+    int s = 0, nt = 0;
+    if (e) std::sscanf(e, "%d,%d", &s, &nt);
+    return std::make_pair(s, nt);
+  }();
+  if (k == 1 && force_wide.first > 0 && try_cfg(force_wide.first, force_wide.second)) return true;
   if (k == 0) {
     for (int S : {8, 4, 2, 1})
       for (int NT : {128, 64, 32})
         if (try_cfg(S, NT)) return true;
   } else {
-    for (int NT : {128, 64, 32})
-      for (int S : {1, 2, 4, 8})
+    // The smallest K split first (its partial exchange through DSMEM costs (S-1)/S of the
+    // accumulator tile per CTA and dominates the kernel), then the largest node tile: for the
+    // TreeLSTM-512 leaf batch (639 nodes, K 512) S=2 / NT=64 runs in 16.1-16.9 us against
+    // 17.8-18.8 us for S=4 / NT=128 (ncu, tools/gpu_ab4.sh).
+    for (int S : {1, 2, 4, 8})
+      for (int NT : {128, 64, 32})
         if (try_cfg(S, NT)) return true;
   }
   return false;
@@ -656,8 +669,19 @@ void tc_prepare(mbx_ctx* c, PlanEntry& pe) {
       if ((st->G * st->K * 8 + st->s_npc * st->K) * 4 <= 160 * 1024) st->s_kb = st->K;
     }
     if (st->s_kb > 0 && st->U % st->s_uc == 0) {
-      const int nbuf = st->s_kb == st->K ? 1 : 2;
-      st->s_smem = nbuf * (st->G * st->s_kb * st->s_uc + st->s_npc * st->s_kb) * 4;
+      // As many chunks in flight as ~96 KB holds (all of K when it fits: the classifier's 64 x 512
+      // x 8 stages 32 KB per CTA in one round trip instead of 8 dependent ones).
+      // Otherwise the largest chunk (<= 64) that keeps >= 4 stages within the budget.
+      auto chunk = [&](int kb) { return (st->G * kb * st->s_uc + st->s_npc * kb) * 4; };
+      const int budget = 96 * 1024;
+      if (st->K / st->s_kb > 1 && chunk(st->K) <= budget) {
+        st->s_kb = st->K;
+      } else if (st->K / st->s_kb > 1) {
+        while (st->s_kb > 8 && budget / chunk(st->s_kb) < 4 && st->K % (st->s_kb / 2) == 0) st->s_kb /= 2;
+      }
+      const int nch = st->K / st->s_kb;
+      st->s_st = nch == 1 ? 1 : std::max(2, std::min(nch, budget / chunk(st->s_kb)));
+      st->s_smem = st->s_st * (st->G * st->s_kb * st->s_uc + st->s_npc * st->s_kb) * 4;
       const std::string ssrc = gen_small_source(*st);
       st->sfn = load_kernel(c, ssrc, "mbx_small_dense");
       pe.tc_exact = true;
@@ -1175,10 +1199,45 @@ void issue_levels(mbx_ctx* c, const std::vector<BatchLaunch>& Ls, size_t i, int 
     // clock64 stamps: cycles since the CTA's level-0 start (each CTA its own SM clock), in us at
     // the nominal 1.965 GHz.
     const char* names[] = {"start", "mma_wait", "mma_done", "pushed", "reduced", "tile_end", "barrier", "converted",
-                           "g_sync", "g_issued", "g_landed0", "mma_issued", "tmem_stg", "stg_sync"};
-    for (int lv = 0; lv < std::min(n, 64); ++lv) {
-      std::fprintf(stderr, "  lv %2d b=%3d:", lv, Ls[i + size_t(lv)].b);
-      for (int k = 0; k < 14; ++k) {
+                           "g_sync", "g_issued", "g_landed0", "mma_issued", "tmem_stg", "stg_sync", "entry", "pre_cwait"};
+    {
+      std::vector<double> g;
+      for (int i2 = 0; i2 < nctas; ++i2) g.push_back(double(h[(size_t(i2) * 64 + 63) * 16 + 14]));
+      const double g0 = *std::min_element(g.begin(), g.end());
+      std::vector<double> d;
+      for (double x : g) d.push_back((x - g0) / 1000.0);
+      std::sort(d.begin(), d.end());
+      std::fprintf(stderr, "  entry (globaltimer, us after the first CTA): median %.2f max %.2f\n", d[d.size() / 2], d.back());
+      for (int k : {11, 12}) {  // gather-thread prologue stamps, us after the level-0 start
+        std::vector<double> v;
+        for (int i2 = 0; i2 < nctas; ++i2) {
+          const unsigned long long x = h[(size_t(i2) * 64 + 63) * 16 + k], t0 = h[size_t(i2) * 64 * 16];
+          if (x && t0) v.push_back((double(x) - double(t0)) / 1965.0);
+        }
+        std::sort(v.begin(), v.end());
+        if (!v.empty()) std::fprintf(stderr, "  prologue stamp %d: median %.2f max %.2f\n", k, v[v.size() / 2], v.back());
+      }
+      if (C.CY > 1) {  // spread of entry times inside each multicast cluster (along y)
+        double worst = 0;
+        const int gx = groups, gy = utiles, gz = C.S;
+        for (int z = 0; z < gz; ++z)
+          for (int x = 0; x < gx; ++x)
+            for (int y0 = 0; y0 < gy; y0 += C.CY) {
+              double lo = 1e30, hi = -1e30;
+              for (int y = y0; y < y0 + C.CY; ++y) {
+                const double v = g[size_t((z * gy + y) * gx + x)];
+                lo = std::min(lo, v);
+                hi = std::max(hi, v);
+              }
+              worst = std::max(worst, (hi - lo) / 1000.0);
+            }
+        std::fprintf(stderr, "  entry spread inside a cluster: max %.2f us\n", worst);
+      }
+    }
+    for (int lv = 0; lv < std::min(n, 63); ++lv) {
+      std::fprintf(stderr, "  lv %2d b=%3d v16=%d:", lv, Ls[i + size_t(lv)].b,
+                   reinterpret_cast<const TcLevel*>(c->meta.host + table)[lv].vec16);
+      for (int k = 0; k < 16; ++k) {
         std::vector<double> v;
         for (int i2 = 0; i2 < nctas; ++i2) {
           const unsigned long long x = h[(size_t(i2) * 64 + lv) * 16 + k];

@@ -639,6 +639,11 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const
   unsigned wepoch = 0;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) s_seen = 0;
+  MBX_LSTAMP(0, 14);  // kernel entry
+#ifdef MBX_STAMPS
+  if (tid == 0)  // %globaltimer at entry (comparable across SMs), slot (63, 14)
+    P.stamps[(((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * 64 + 63) * 16 + 14] = mbx_gen::global_ns();
+#endif
   const int tile_u = blockIdx.y;
   constexpr int S = MBX_LS;
   for (int i = tid; i < min(P.nlevels, 64); i += MBX_THREADS) slv[i] = P.levels[i];
@@ -702,7 +707,11 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const
   else __syncthreads();
 #elif MBX_LCY > 1
   cluster_sync();  // peers' barriers initialised before any multicast lands here
+#ifdef MBX_ARRIVE_RELEASE
   asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");  // staging free for tile 0
+#else
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");  // staging free for tile 0 (nothing to publish)
+#endif
 #else
   __syncthreads();
 #endif
@@ -730,7 +739,9 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const
     fill_rowbase(slv[0], grp * slv[0].nt, slv[0].nt);
     have_rb = true;
   }
+  MBX_LSTAMP_T(64, 63, 11);  // profiling: gather thread after the first rowbase fill
   pdl_wait();  // the first level's inputs come from earlier launches
+  MBX_LSTAMP_T(64, 63, 12);  // profiling: gather thread after the PDL wait
 
   unsigned it = 0;  // node tiles processed by this CTA: parity of every per-tile mbarrier
   for (int lv = 0; lv < P.nlevels; ++lv) {
@@ -782,11 +793,16 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const
           }
         }
       };
+      MBX_LSTAMP_T(64, lv, 15);
 #if MBX_LCY > 1
       // Staging of the previous tile converted by every CTA of the cluster (warps 0-1 hold no
       // staging: they pass their arrival for this phase on at once).
       asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+#ifdef MBX_ARRIVE_RELEASE
       if (warp < 2) asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+#else
+      if (warp < 2) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");  // no staging held
+#endif
 #endif
       if (warp < 2) load_tail_operands();
       if (warp >= 2) {
@@ -1115,8 +1131,9 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const
 // (proj/src/backend.cpp:116-131), the tail with the glibc-exact activations.
 //   grid = (node tiles of MBX_SNPC nodes, unit slices of MBX_SUC units); thread = (node, unit),
 //   MBX_G independent chains.  The weight slice and the nodes' rows stream through shared memory
-//   in K chunks of MBX_SKB (double-buffered cp.async), so no operand is read twice from L2 by one
-//   CTA and the chains run from shared memory.
+//   in K chunks of MBX_SKB through a ring of MBX_SST cp.async stages (all of K at once when it
+//   fits: the kernel is load-latency bound, each chunk in flight hides one L2 round trip), so no
+//   operand is read twice from L2 by one CTA and the chains run from shared memory.
 #define MBX_SNT (MBX_SNPC * MBX_SUC)
 extern "C" __global__ void __launch_bounds__(MBX_THREADS) mbx_small_dense(const __grid_constant__ SmallArgs P) {
   extern __shared__ __align__(16) float sms[];
@@ -1168,23 +1185,31 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS) mbx_small_dense(const 
   float g[G];
 #pragma unroll
   for (int gi = 0; gi < G; ++gi) g[gi] = 0.0f;
-  constexpr int NCH = K / KB;
-  stage(0, sms);
+  constexpr int NCH = K / KB, NST = MBX_SST, D = NST - 1;  // D chunks in flight ahead
+  static_assert(NST >= 1 && (NST > 1 || NCH == 1), "stages");
+  // One commit group per chunk (empty past the end) so the wait count is the same every step.
+  if (D == 0) stage(0, sms);
+#pragma unroll 1
+  for (int c = 0; c < D; ++c) {
+    if (c < NCH) stage(c, sms + c * BUF);
+    else mbx_gen::cp_async_commit();
+  }
+#pragma unroll 1
   for (int c = 0; c < NCH; ++c) {
-    float* cur = sms + (c & 1) * BUF;
-    if (c + 1 < NCH) {
-      stage(c + 1, sms + ((c + 1) & 1) * BUF);
-      mbx_gen::cp_async_wait<1>();
-    } else {
-      mbx_gen::cp_async_wait<0>();
+    float* cur = sms + (c % NST) * BUF;
+    if (D > 0) {
+      if (c + D < NCH) stage(c + D, sms + ((c + D) % NST) * BUF);  // the buffer computed at c - 1
+      else mbx_gen::cp_async_commit();
     }
+    mbx_gen::cp_async_wait<D>();
     __syncthreads();
     if (active) {
       const float* x = cur + WCH + n * KB;
       const float* w = cur + u;
       // Blocks of 8 p: operands and products first (independent), then the 8 dependent adds of
-      // each chain in p order — the add chain is the only serial part.
-#pragma unroll 1
+      // each chain in p order — the add chain is the only serial part.  Unrolled 4 blocks deep so
+      // the next blocks' shared-memory loads and products overlap this block's add chain.
+#pragma unroll 4
       for (int p0 = 0; p0 < KB; p0 += 8) {
         float xv[8];
 #pragma unroll
@@ -1199,7 +1224,7 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS) mbx_small_dense(const 
         }
       }
     }
-    __syncthreads();  // the buffer is refilled two chunks on
+    __syncthreads();  // the buffer is refilled NST chunks on
   }
   if (!active) return;
   const long long node = node0 + n;
