@@ -277,6 +277,7 @@ std::string gen_levels_source(const TcState& st, int k) {
   if (stamps_enabled()) o << "#define MBX_STAMPS 1\n";
   if (std::getenv("MBX_FENCE_ONCE")) o << "#define MBX_FENCE_ONCE 1\n";
   if (std::getenv("MBX_ARRIVE_RELEASE")) o << "#define MBX_ARRIVE_RELEASE 1\n";
+  if (std::getenv("MBX_SENTINEL")) o << "#define MBX_SENTINEL 1\n";
   if (const char* e = std::getenv("MBX_POLLERS")) o << "#define MBX_POLLERS " << std::max(1, std::atoi(e)) << "\n";
   o << jit::prelude_source();
   o << "#define MBX_LEVELS_KERNEL 1\n"
@@ -479,6 +480,10 @@ Layout layout_for(const TcState& st, int NT, int S, int npass) {
 // Clusters of 8 one-CTA-per-SM blocks: at least 14 are co-resident on a 148-SM B200 (GPCs of
 // 18-20 SMs); with more unit tiles than that the ranks exchange partials through L2 instead.
 // Returns false if the plan has no such layout (it then runs level by level).
+__global__ void fill_u32(unsigned* p, size_t n, unsigned v) {
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) p[i] = v;
+}
+
 bool levels_layout(TcState& st, int k) {
   auto al = [](int x) { return (x + 1023) / 1024 * 1024; };
   const int utiles = st.U / st.UC;
@@ -1145,6 +1150,9 @@ void issue_levels(mbx_ctx* c, const std::vector<BatchLaunch>& Ls, size_t i, int 
       const size_t lloc = size_t((C.NT / 8 + C.S - 1) / C.S) * 8;  // MBX_LLOC
       const size_t part_bytes = size_t(2) * ngmax * utiles * C.S * C.S * lloc * kM * 4;
       cuda_check(cudaMalloc(&C.part, part_bytes), "levels partials");
+      // Every partial slot starts "not written" (MBX_PART_EMPTY in tc_gate.cuh).
+      fill_u32<<<148, 256, 0, c->stream>>>(reinterpret_cast<unsigned*>(C.part), part_bytes / 4, 0xffbadbadu);
+      cuda_check(cudaGetLastError(), "levels partials fill");
       cuda_check(cudaMalloc(&C.flags, ngmax * utiles * C.S * 4), "levels flags");
       cuda_check(cudaMemset(C.flags, 0, ngmax * utiles * C.S * 4), "levels flags");
     }

@@ -574,7 +574,23 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_gate(const _
 #endif
 #define MBX_LSTAMP(lv, i) MBX_LSTAMP_T(0, lv, i)
 
+#ifndef MBX_SENTINEL
+// L2 exchange, experiment (MBX_SENTINEL=1 through the env knob MBX_SENTINEL): consumers poll the
+// partial slots themselves instead of per-rank arrival counters.  Correct, but measured slower on
+// the TreeLSTM-512 b64 levels launch (ncu: 75.5-78.3 us against 70.0-72.6 us with counters): the
+// polling loads contend with the producers' stores in L2 and the saved round trip is lost.
+#define MBX_SENTINEL 0
+#endif
+#define MBX_PART_EMPTY 0xffbadbadu  // a NaN payload no computation produces: "partial not written yet"
 namespace mbx_gen {
+__device__ __forceinline__ void st_part(float* p, float v) {
+  asm volatile("st.relaxed.gpu.global.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
+}
+__device__ __forceinline__ float ld_part(const float* p) {
+  float v;
+  asm volatile("ld.relaxed.gpu.global.f32 %0, [%1];" : "=f"(v) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
   unsigned v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -1042,11 +1058,19 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const
           const int r = ch % S, m0 = (ch / S) * 8;
           float* dst = pbase + ((size_t)(r * S + int(rank)) * MBX_LLOC + m0) * MBX_M + row;
 #pragma unroll
-          for (int k = 0; k < 8; ++k) __stcg(dst + k * MBX_M, v[k]);
+          for (int k = 0; k < 8; ++k) {
+#if MBX_SENTINEL
+            // Only the tile's real nodes: every slot written is read and reset by its consumer.
+            if (ch * 8 + k < nn) st_part(dst + k * MBX_M, v[k]);
+#else
+            __stcg(dst + k * MBX_M, v[k]);
+#endif
+          }
         }
       }
       MBX_LSTAMP(lv, 12);
       tc_fence_before();
+#if !MBX_SENTINEL
       __syncthreads();
       MBX_LSTAMP(lv, 13);
       if (S > 1) {
@@ -1055,15 +1079,93 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const
         MBX_LSTAMP(lv, 3);
         block_wait(flags + rank, unsigned(S - 1) * (it + 1), &s_seen, ++wepoch);
       }
-      auto partial = [&](int q, int n, int col) -> float {
-        return __ldcg(pbase + ((size_t)(int(rank) * S + q) * MBX_LLOC + n) * MBX_M + col);
+#endif
+      auto paddr = [&](int q, int n, int col) -> float* {
+        return pbase + ((size_t)(int(rank) * S + q) * MBX_LLOC + n) * MBX_M + col;
       };
+      auto partial = [&](int q, int n, int col) -> float { return __ldcg(paddr(q, n, col)); };
 #endif
       MBX_LSTAMP(lv, 4);
       // ---- sum the partials in rank order, run the tail, write the outputs ----
       // Every partial of every element is read before the first output store: through generic
       // pointers a store would order all later loads behind it (one L2 round trip per element).
       float gsum[MBX_LEPT][MBX_G];
+#if MBX_LXCH == 1 && MBX_SENTINEL
+      // Partials arrive without a flag: every slot holds MBX_PART_EMPTY until its producer's store
+      // lands, so the loads poll the data itself (one L2 round trip fewer than counter + data).
+      // All loads are issued first; only slots still empty are re-read.  The consumer then puts
+      // the slot back to empty: its producer rewrites it two tiles later, after a grid barrier (or
+      // a fence, below, when one level has more tiles).
+      {
+        float pv[MBX_LEPT][MBX_G][S];
+#pragma unroll
+        for (int t = 0; t < MBX_LEPT; ++t) {
+          const int e = tid + t * MBX_THREADS;
+          const int n = e / MBX_UC, u = e - n * MBX_UC;
+          const bool valid = n < nloc && loc_col(n) < nn;
+#pragma unroll
+          for (int gi = 0; gi < MBX_G; ++gi)
+#pragma unroll
+            for (int q = 0; q < S; ++q) pv[t][gi][q] = valid ? ld_part(paddr(q, n, gi * MBX_UC + u)) : 0.0f;
+        }
+        // Rounds: re-issue every slot still empty (all in flight), then check them all.
+        auto empty = [&](int t, int gi, int q) -> bool {
+          const int e = tid + t * MBX_THREADS;
+          const int n = e / MBX_UC;
+          return n < nloc && loc_col(n) < nn && __float_as_uint(pv[t][gi][q]) == MBX_PART_EMPTY;
+        };
+        bool pending = false;
+#pragma unroll
+        for (int t = 0; t < MBX_LEPT; ++t)
+#pragma unroll
+          for (int gi = 0; gi < MBX_G; ++gi)
+#pragma unroll
+            for (int q = 0; q < S; ++q) pending |= empty(t, gi, q);
+        if (pending) {
+          const unsigned long long t0 = global_ns();
+          while (pending) {
+#pragma unroll
+            for (int t = 0; t < MBX_LEPT; ++t)
+#pragma unroll
+              for (int gi = 0; gi < MBX_G; ++gi)
+#pragma unroll
+                for (int q = 0; q < S; ++q)
+                  if (empty(t, gi, q)) {
+                    const int e = tid + t * MBX_THREADS;
+                    const int n = e / MBX_UC, u = e - n * MBX_UC;
+                    pv[t][gi][q] = ld_part(paddr(q, n, gi * MBX_UC + u));
+                  }
+            pending = false;
+#pragma unroll
+            for (int t = 0; t < MBX_LEPT; ++t)
+#pragma unroll
+              for (int gi = 0; gi < MBX_G; ++gi)
+#pragma unroll
+                for (int q = 0; q < S; ++q) pending |= empty(t, gi, q);
+            if (pending && global_ns() - t0 > 2000000000ull) __trap();
+          }
+        }
+#pragma unroll
+        for (int t = 0; t < MBX_LEPT; ++t) {
+          const int e = tid + t * MBX_THREADS;
+          const int n = e / MBX_UC, u = e - n * MBX_UC;
+          const bool valid = n < nloc && loc_col(n) < nn;
+          if (valid) {
+#pragma unroll
+            for (int gi = 0; gi < MBX_G; ++gi)
+#pragma unroll
+              for (int q = 0; q < S; ++q) st_part(paddr(q, n, gi * MBX_UC + u), __uint_as_float(MBX_PART_EMPTY));
+          }
+#pragma unroll
+          for (int gi = 0; gi < MBX_G; ++gi) {
+            float acc = pv[t][gi][0];
+#pragma unroll
+            for (int q = 1; q < S; ++q) acc = acc + pv[t][gi][q];
+            gsum[t][gi] = acc;
+          }
+        }
+      }
+#else
 #pragma unroll
       for (int t = 0; t < MBX_LEPT; ++t) {
         const int e = tid + t * MBX_THREADS;
@@ -1082,6 +1184,7 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const
           gsum[t][gi] = acc;
         }
       }
+#endif
 #pragma unroll
       for (int t = 0; t < MBX_LEPT; ++t) {
         const int e = tid + t * MBX_THREADS;
@@ -1097,6 +1200,11 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const
       }
 #if MBX_LXCH == 0
       if (S > 1 && tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+#elif MBX_SENTINEL
+      // A third tile of this level reuses this tile's partial slots with no grid barrier between:
+      // the empty markers must be in L2 before this CTA's next partials (which the producers
+      // observe before they write that tile).
+      if (node0 + 2 * ngrp * nt < b) __threadfence();
 #endif
       __syncthreads();  // stg / recv / TMEM free for the next tile
       tc_fence_after();
@@ -1115,7 +1223,7 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const
 #else
   // Every increment of this CTA's counter happened before its last wait: reset it for the next
   // launch (stream order makes launches sequential).
-  if (S > 1 && tid == 0 && it > 0) P.xflags[(grp * gridDim.y + tile_u) * S + rank] = 0u;
+  if (!MBX_SENTINEL && S > 1 && tid == 0 && it > 0) P.xflags[(grp * gridDim.y + tile_u) * S + rank] = 0u;
 #endif
   if (warp == 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(P.tmem_cols) : "memory");
