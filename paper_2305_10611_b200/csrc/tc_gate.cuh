@@ -960,7 +960,13 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const
         }
 #if MBX_LCY > 1
         // This CTA's staging is consumed: the cluster may multicast the next tile's rows into it.
+        // Relaxed: the only hazard is write-after-read, and every staging read has returned (its
+        // value fed a store above); .release would add a GPU-scope membar (ncu: stall_membar).
+#ifdef MBX_ARRIVE_RELEASE
         asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+#else
+        asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+#endif
 #endif
         MBX_LSTAMP_T(64, lv, 7);
         // The tail's operands: off the gather -> convert critical path, in flight during the MMAs
