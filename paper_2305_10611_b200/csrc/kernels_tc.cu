@@ -101,6 +101,7 @@ struct TcState {
   std::string src;            // generated kernel source
   void* fn = nullptr;         // cudaKernel_t
   void* fn_fast = nullptr;    // pointwise plans: fast-activation variant (tensor-core precisions)
+  void* fn4 = nullptr, *fn_fast4 = nullptr;  // pointwise plans, E % 4 == 0: 16-byte variants
   // Few output columns (U x G <= 64): the bit-exact CUDA-core small-dense kernel instead of the
   // tensor cores, in every precision (sfn != nullptr).
   void* sfn = nullptr;
@@ -717,6 +718,10 @@ void tc_prepare(mbx_ctx* c, PlanEntry& pe) {
     st->src = gen_pointwise_source(*st);
     st->fn = load_kernel(c, st->src, "mbx_pointwise");
     st->fn_fast = load_kernel(c, st->src, "mbx_pointwise_fast");
+    if (st->U % 4 == 0) {
+      st->fn4 = load_kernel(c, st->src, "mbx_pointwise4");
+      st->fn_fast4 = load_kernel(c, st->src, "mbx_pointwise_fast4");
+    }
     pe.tc_kind = 2;
   }
   pe.tc_state = st.release();
@@ -865,7 +870,23 @@ cudaError_t tc_launch(mbx_ctx* c, const PlanEntry& pe, const BatchLaunch& L) {
     a.nb = int(pe.exec_plan.batched_shapes.size());
     a.nloads = st->prog.nloads;
     fill_loads(st->prog, a.loads);
-    const int64_t total = int64_t(L.b) * a.E;
+    // 16-byte variant when every row it touches is 16-byte aligned (checked on the host copies
+    // of this batch's offset tables).
+    bool v4 = st->fn4 != nullptr;
+    if (v4) {
+      const int64_t* sh = reinterpret_cast<const int64_t*>(c->meta.host + L.shared_meta);
+      const int64_t* bt = reinterpret_cast<const int64_t*>(c->meta.host + L.batched_meta);
+      const int64_t* ob = reinterpret_cast<const int64_t*>(c->meta.host + L.out_meta);
+      for (int k = 0; k < st->prog.nout && v4; ++k) v4 = ob[k] % 4 == 0;
+      for (int j = 0; j < a.nloads && v4; ++j) {
+        const TcLoad& d = a.loads[j];
+        v4 = d.off % 4 == 0;
+        if (d.kind == 0) v4 = v4 && sh[d.idx] % 4 == 0;
+        else
+          for (int i = 0; i < L.b && v4; ++i) v4 = bt[int64_t(i) * a.nb + d.idx] % 4 == 0;
+      }
+    }
+    const int64_t total = int64_t(L.b) * a.E / (v4 ? 4 : 1);
     const int blocks = int(std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, 148 * 8)));
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(blocks);
@@ -881,7 +902,8 @@ cudaError_t tc_launch(mbx_ctx* c, const PlanEntry& pe, const BatchLaunch& L) {
     void* args[] = {&a};
     // FP32 contexts: glibc-exact activations (bit-identical to the reference); the tensor-core
     // precisions use the fast ones, as their gate tails do.
-    return cudaLaunchKernelExC(&cfg, c->precision == MBX_PREC_FP32 ? st->fn : st->fn_fast, args);
+    void* fn = c->precision == MBX_PREC_FP32 ? (v4 ? st->fn4 : st->fn) : (v4 ? st->fn_fast4 : st->fn_fast);
+    return cudaLaunchKernelExC(&cfg, fn, args);
   }
   const int npass = c->precision == MBX_PREC_BF16 ? 1 : 3;
   const int64_t* shared_host = reinterpret_cast<const int64_t*>(c->meta.host + L.shared_meta);

@@ -351,10 +351,25 @@ __global__ void gather_rows_kernel(float* arena, const int64_t* src_off, int64_t
 
 // Packs n arena ranges (offset, size) into a contiguous staging buffer (one D2H copy for all
 // outputs / scalar decisions of a flush).
+// One warp per range (a range is typically one node row of H floats): 16-byte copies when the
+// range and both ends are 16-byte aligned, else 4-byte ones.  Used for the outputs' D2H pack
+// (arena -> contiguous) and, inverted, for the inputs' scatter (contiguous -> arena).
+__device__ __forceinline__ void copy_range_warp(const float* __restrict__ s, float* __restrict__ d, int64_t size,
+                                                int lane) {
+  if (((reinterpret_cast<uintptr_t>(s) | reinterpret_cast<uintptr_t>(d)) & 15) == 0 && (size & 3) == 0) {
+    const float4* s4 = reinterpret_cast<const float4*>(s);
+    float4* d4 = reinterpret_cast<float4*>(d);
+    for (int64_t e = lane; e < size / 4; e += 32) d4[e] = s4[e];
+  } else {
+    for (int64_t e = lane; e < size; e += 32) d[e] = s[e];
+  }
+}
+
 __global__ void pack_ranges_kernel(const float* arena, const int64_t* ranges, int n, float* dst) {
-  for (int r = blockIdx.x; r < n; r += gridDim.x) {
+  const int lane = threadIdx.x & 31;
+  for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n; r += (gridDim.x * blockDim.x) >> 5) {
     const int64_t off = ranges[3 * r], size = ranges[3 * r + 1], dst_off = ranges[3 * r + 2];
-    for (int64_t e = threadIdx.x; e < size; e += blockDim.x) dst[dst_off + e] = arena[off + e];
+    copy_range_warp(arena + off, dst + dst_off, size, lane);
   }
 }
 
@@ -362,9 +377,10 @@ __global__ void pack_ranges_kernel(const float* arena, const int64_t* ranges, in
 // piece from the caller's pinned buffer, then scattered to their arena offsets on the device).
 // ranges: (src offset, size, arena offset) triples.
 __global__ void scatter_ranges_kernel(const float* src, const int64_t* ranges, int n, float* arena) {
-  for (int r = blockIdx.x; r < n; r += gridDim.x) {
+  const int lane = threadIdx.x & 31;
+  for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n; r += (gridDim.x * blockDim.x) >> 5) {
     const int64_t so = ranges[3 * r], size = ranges[3 * r + 1], dof = ranges[3 * r + 2];
-    for (int64_t e = threadIdx.x; e < size; e += blockDim.x) arena[dof + e] = src[so + e];
+    copy_range_warp(src + so, arena + dof, size, lane);
   }
 }
 
@@ -430,14 +446,14 @@ cudaError_t launch_gather_rows(float* arena, const int64_t* src_off, int64_t dst
 
 cudaError_t launch_scatter_ranges(const float* src, const int64_t* ranges, int n, float* arena, cudaStream_t stream) {
   if (n <= 0) return cudaSuccess;
-  scatter_ranges_kernel<<<std::min(n, 148 * 4), 128, 0, stream>>>(src, ranges, n, arena);
+  scatter_ranges_kernel<<<std::min((n + 7) / 8, 148 * 8), 256, 0, stream>>>(src, ranges, n, arena);
   return cudaGetLastError();
 }
 
 cudaError_t launch_pack_ranges(const float* arena, const int64_t* ranges, int n, float* dst,
                                cudaStream_t stream) {
   if (n <= 0) return cudaSuccess;
-  pack_ranges_kernel<<<std::min(n, 148 * 4), 128, 0, stream>>>(arena, ranges, n, dst);
+  pack_ranges_kernel<<<std::min((n + 7) / 8, 148 * 8), 256, 0, stream>>>(arena, ranges, n, dst);
   return cudaGetLastError();
 }
 

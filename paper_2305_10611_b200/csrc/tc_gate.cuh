@@ -1360,34 +1360,60 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS) mbx_small_dense(const 
 #ifdef MBX_POINTWISE_KERNEL
 // One thread per (node, element); the offset-table lookups are shared by the E elements of a
 // node.  FAST selects the fast activations (tensor-core precisions).
-template <bool FAST>
+template <bool FAST, int V>
 __device__ __forceinline__ void mbx_pointwise_body(const PwArgs& P) {
   // PDL: launched while the predecessor drains; its outputs are read only after the wait.
   mbx_gen::pdl_wait();
   mbx_gen::pdl_launch_dependents();
-  const long long total = (long long)P.b * MBX_PW_E;
+  // V = 4: each thread takes 4 consecutive elements with 16-byte loads and stores (the host
+  // checked that every row involved is 16-byte aligned); one offset lookup per 4 elements.
+  constexpr int EV = MBX_PW_E / V;
+  const long long total = (long long)P.b * EV;
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
        idx += (long long)gridDim.x * blockDim.x) {
-    const long long node = idx / MBX_PW_E;
-    const int e = int(idx - node * MBX_PW_E);
-    float l[MBX_NLOADS > 0 ? MBX_NLOADS : 1];
+    const long long node = idx / EV;
+    const int e = int(idx - node * EV) * V;
+    float l[V][MBX_NLOADS > 0 ? MBX_NLOADS : 1];
 #pragma unroll
     for (int j = 0; j < MBX_NLOADS; ++j) {
       const TcLoad& d = P.loads[j];
       const long long base = d.kind == 1 ? P.batched_off[node * P.nb + d.idx] : P.shared_off[d.idx];
-      l[j] = P.arena[base + d.off + e];
+      if (V == 4) {
+        const float4 v = *reinterpret_cast<const float4*>(P.arena + base + d.off + e);
+        l[0][j] = v.x;
+        l[V > 1 ? 1 : 0][j] = v.y;
+        l[V > 2 ? 2 : 0][j] = v.z;
+        l[V > 3 ? 3 : 0][j] = v.w;
+      } else {
+        l[0][j] = P.arena[base + d.off + e];
+      }
     }
-    float o[MBX_NOUT];
-    if (FAST) mbx_pw_tail_fast(l, o);
-    else mbx_pw_tail(l, o);
+    float o[V][MBX_NOUT];
 #pragma unroll
-    for (int k = 0; k < MBX_NOUT; ++k) P.arena[P.out_base[k] + node * MBX_PW_E + e] = o[k];
+    for (int w = 0; w < V; ++w) {
+      if (FAST) mbx_pw_tail_fast(l[w], o[w]);
+      else mbx_pw_tail(l[w], o[w]);
+    }
+#pragma unroll
+    for (int k = 0; k < MBX_NOUT; ++k) {
+      float* dst = P.arena + P.out_base[k] + node * MBX_PW_E + e;
+      if (V == 4) *reinterpret_cast<float4*>(dst) = make_float4(o[0][k], o[V > 1 ? 1 : 0][k], o[V > 2 ? 2 : 0][k], o[V > 3 ? 3 : 0][k]);
+      else *dst = o[0][k];
+    }
   }
 }
 extern "C" __global__ void __launch_bounds__(256) mbx_pointwise(const __grid_constant__ PwArgs P) {
-  mbx_pointwise_body<false>(P);
+  mbx_pointwise_body<false, 1>(P);
 }
 extern "C" __global__ void __launch_bounds__(256) mbx_pointwise_fast(const __grid_constant__ PwArgs P) {
-  mbx_pointwise_body<true>(P);
+  mbx_pointwise_body<true, 1>(P);
 }
+#if MBX_PW_E % 4 == 0
+extern "C" __global__ void __launch_bounds__(256) mbx_pointwise4(const __grid_constant__ PwArgs P) {
+  mbx_pointwise_body<false, 4>(P);
+}
+extern "C" __global__ void __launch_bounds__(256) mbx_pointwise_fast4(const __grid_constant__ PwArgs P) {
+  mbx_pointwise_body<true, 4>(P);
+}
+#endif
 #endif  // MBX_POINTWISE_KERNEL
