@@ -872,7 +872,8 @@ cudaError_t tc_launch(mbx_ctx* c, const PlanEntry& pe, const BatchLaunch& L) {
     fill_loads(st->prog, a.loads);
     // 16-byte variant when every row it touches is 16-byte aligned (checked on the host copies
     // of this batch's offset tables).
-    bool v4 = st->fn4 != nullptr;
+    static const bool no_v4 = std::getenv("MBX_PW_NO_VEC4") != nullptr;  // experiment knob
+    bool v4 = st->fn4 != nullptr && !no_v4;
     if (v4) {
       const int64_t* sh = reinterpret_cast<const int64_t*>(c->meta.host + L.shared_meta);
       const int64_t* bt = reinterpret_cast<const int64_t*>(c->meta.host + L.batched_meta);
@@ -1187,7 +1188,7 @@ void issue_levels(mbx_ctx* c, const std::vector<BatchLaunch>& Ls, size_t i, int 
   lc.blockDim = dim3(kTcThreads);
   lc.dynamicSmemBytes = size_t(C.smem);
   lc.stream = c->stream;
-  cudaLaunchAttribute attrs[2];
+  cudaLaunchAttribute attrs[3];
   int na = 0;
   if (C.CY > 1 || (C.S > 1 && C.xch == 0)) {
     attrs[na].id = cudaLaunchAttributeClusterDimension;
@@ -1199,6 +1200,16 @@ void issue_levels(mbx_ctx* c, const std::vector<BatchLaunch>& Ls, size_t i, int 
   if (!fresh_pack && pdl_enabled()) {
     attrs[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attrs[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  // Grid barrier / cross-cluster counters need every CTA resident at once: a cooperative launch
+  // has the hardware place the whole grid together, so resident CTAs never spin waiting for SMs
+  // that other contexts' kernels keep taking (which could outlast the 2 s wait limit).
+  static const bool coop = std::getenv("MBX_NO_COOP") == nullptr;
+  const bool needs_all = n > 1 || (C.xch == 1 && C.S > 1);
+  if (coop && needs_all) {
+    attrs[na].id = cudaLaunchAttributeCooperative;
+    attrs[na].val.cooperative = 1;
     ++na;
   }
   lc.attrs = attrs;
