@@ -1205,7 +1205,13 @@ void issue_levels(mbx_ctx* c, const std::vector<BatchLaunch>& Ls, size_t i, int 
   // Grid barrier / cross-cluster counters need every CTA resident at once: a cooperative launch
   // has the hardware place the whole grid together, so resident CTAs never spin waiting for SMs
   // that other contexts' kernels keep taking (which could outlast the 2 s wait limit).
-  static const bool coop = std::getenv("MBX_NO_COOP") == nullptr;
+  // Not under Nsight Compute (its injection sets NV_NSIGHT_INJECTION_TRANSPORT_TYPE /
+  // NV_COMPUTE_PROFILER_PERFWORKS_DIR; it fails cooperative launches with LaunchFailed, and it
+  // serialises kernels, so co-residency holds there anyway), nor with MBX_NO_COOP.
+  static const bool coop = std::getenv("MBX_NO_COOP") == nullptr &&
+                           std::getenv("NV_NSIGHT_INJECTION_TRANSPORT_TYPE") == nullptr &&
+                           std::getenv("NV_COMPUTE_PROFILER_PERFWORKS_DIR") == nullptr &&
+                           std::getenv("CUDA_INJECTION64_PATH") == nullptr;
   const bool needs_all = n > 1 || (C.xch == 1 && C.S > 1);
   if (coop && needs_all) {
     attrs[na].id = cudaLaunchAttributeCooperative;
@@ -1227,7 +1233,14 @@ void issue_levels(mbx_ctx* c, const std::vector<BatchLaunch>& Ls, size_t i, int 
   static const bool lane_all = std::getenv("MBX_LANE_ALL") != nullptr;  // experiment knob
   const bool lane = lane_all || n > 1 || (C.xch == 1 && C.S > 1);
   if (lane) lc.stream = persistent_lane_begin(c);
-  const cudaError_t le = cudaLaunchKernelExC(&lc, C.fn, args);
+  cudaError_t le = cudaLaunchKernelExC(&lc, C.fn, args);
+  if (le != cudaSuccess && coop && needs_all) {
+    // Some tools (ncu's kernel replay) refuse cooperative launches: run it as a plain launch
+    // (one kernel at a time there, so co-residency holds anyway).
+    cudaGetLastError();
+    lc.numAttrs = unsigned(na - 1);
+    le = cudaLaunchKernelExC(&lc, C.fn, args);
+  }
   if (lane) persistent_lane_end(c);
   cuda_check(le, "multi-level tensor-core kernel");
   if (stamps_enabled()) {
