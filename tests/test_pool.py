@@ -49,3 +49,23 @@ def test_pool_gpu(mbx, prec):
     r1 = ref.evaluate_batch(*ins[0], batch)
     pool.close()
     assert np.array_equal(r0.out_data.view(np.uint32), r1.out_data.view(np.uint32))
+
+
+@pytest.mark.gpu
+def test_pool_gpu_headline_stress(mbx):
+    """The headline configuration (TreeLSTM-512 b64 bf16x3) from as many host workers as the
+    bench uses, several rounds: the persistent launches (grid barrier, cooperative placement)
+    must never be starved by the other workers' clustered kernels (a starved grid barrier traps
+    after 2 s and the round fails)."""
+    import os
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    model, hidden, batch = "treelstm", 512, 64
+    ins, counts = _inputs(mbx, model, hidden, batch, list(range(1, 5)))
+    threads = max(2, min(14, (os.cpu_count() or 4) - 2))
+    pool = mbx.Pool(0, "bf16x3", model, hidden, 1, threads)
+    for _ in range(25):  # ~22k mini-batches: the bench's order of magnitude
+        n, ms = pool.run_timed(ins * (16 * threads), batch)
+        assert n == 16 * threads * sum(counts) and ms > 0
+    pool.close()
