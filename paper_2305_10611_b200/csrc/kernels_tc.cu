@@ -1112,6 +1112,11 @@ int plan_levels(mbx_ctx* c, const std::vector<BatchLaunch>& Ls, size_t i, size_t
     if (resident < per_group) return 0;
     ng = std::min(ng, resident / per_group);
   }
+  static const int wide_groups = [] {  // experiment: cap the wide launch's node-tile groups
+    const char* e = std::getenv("MBX_WIDE_GROUPS");
+    return e ? std::max(1, std::atoi(e)) : 0;
+  }();
+  if (k == 1 && wide_groups > 0) ng = std::min(ng, wide_groups);
   *groups = ng;
   *cfg = k;
   std::vector<TcLevel> tbl(static_cast<size_t>(n));
