@@ -478,6 +478,35 @@ struct Executor::Impl {
     }
     if (at.type != cudaMemoryTypeHost) return false;
     const size_t nd = size_t(enc->ndata), nt = enc_tensors.size();
+    cudaStream_t cs = c->copy_stream;
+    {
+      // When the tensors sit in the arena in stream order (runs that continue each other in both),
+      // a few direct H2D copies replace the staging copy + scatter kernel.
+      struct Run { int64_t src, size, dst; };
+      std::vector<Run> runs;
+      for (size_t k = 0; k < nt && runs.size() <= 8; ++k) {
+        const int64_t src = int64_t(enc_tensors[k].second.first - enc->data), size = enc_tensors[k].second.second,
+                      dst = enc_tensors[k].first;
+        if (!runs.empty() && runs.back().src + runs.back().size == src && runs.back().dst + runs.back().size == dst)
+          runs.back().size += size;
+        else
+          runs.push_back({src, size, dst});
+      }
+      if (runs.size() <= 8 && !std::getenv("MBX_INPUT_SCATTER")) {  // (env: force the scatter path)
+        float* arena = mbx::arena_ptr(c);
+        int64_t bytes = 0;
+        for (const Run& r : runs) {
+          mbx::cuda_check(cudaMemcpyAsync(arena + r.dst, enc->data + r.src, size_t(r.size) * sizeof(float),
+                                          cudaMemcpyHostToDevice, cs),
+                          "input H2D");
+          bytes += r.size * int64_t(sizeof(float));
+        }
+        mbx::cuda_check(cudaEventRecord(c->ev_copy, cs), "input copy event");
+        c->copy_pending = true;
+        timing.h2d_bytes += long(bytes);
+        return true;
+      }
+    }
     if (nd > c->in_dev_cap) {
       if (c->in_dev) cudaFree(c->in_dev);
       c->in_dev_cap = std::max(nd, c->in_dev_cap * 2);
@@ -495,7 +524,6 @@ struct Executor::Impl {
       c->scat_host[3 * k + 1] = enc_tensors[k].second.second;
       c->scat_host[3 * k + 2] = enc_tensors[k].first;
     }
-    cudaStream_t cs = c->copy_stream;
     mbx::cuda_check(cudaMemcpyAsync(c->in_dev, enc->data, nd * sizeof(float), cudaMemcpyHostToDevice, cs), "input H2D");
     mbx::cuda_check(cudaMemcpyAsync(c->scat_dev, c->scat_host, nt * 3 * sizeof(int64_t), cudaMemcpyHostToDevice, cs),
                     "scatter table H2D");

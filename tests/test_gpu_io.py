@@ -1,7 +1,8 @@
 """Host <-> device input paths of mbx_evaluate_batch on a GPU: pageable inputs (one host memcpy
-into pinned staging, one H2D) and pinned inputs (one H2D of the caller's data stream, scattered
-to the arena offsets by a device kernel) give bit-identical results, and so do resident inputs
-and deferred completion (the throughput pool's mode)."""
+into pinned staging, one H2D) and pinned inputs (direct H2D copies into the arena when the
+tensors lie in stream order there, else one H2D of the caller's data stream scattered to the
+arena offsets by a device kernel — forced with MBX_INPUT_SCATTER) give bit-identical results, and
+so do resident inputs and deferred completion (the throughput pool's mode)."""
 import numpy as np
 import pytest
 
@@ -18,9 +19,12 @@ def gpu(mbx):
 
 @pytest.mark.parametrize("model,hidden,batch,prec", [("treelstm", 512, 16, "bf16x3"), ("treelstm", 64, 8, "fp32"),
                                                      ("mvrnn", 32, 8, "fp32"), ("birnn", 128, 8, "bf16x3")])
-def test_pinned_and_pageable_inputs_agree(gpu, model, hidden, batch, prec):
+@pytest.mark.parametrize("scatter", [False, True])
+def test_pinned_and_pageable_inputs_agree(gpu, model, hidden, batch, prec, scatter, monkeypatch):
     import torch
     mbx = gpu
+    if scatter:
+        monkeypatch.setenv("MBX_INPUT_SCATTER", "1")
     c = mbx.Context(0, prec)
     m = mbx.Model(c, model, hidden)
     m.make_params(3)
