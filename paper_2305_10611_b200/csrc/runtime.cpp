@@ -869,6 +869,60 @@ struct Executor::Impl {
   // sync = false (defer_sync): the read-back is enqueued, the copy out of the pinned buffer is
   // the caller's business after it synchronises.
   void pack_to_host(const std::vector<int64_t>& ranges, float* dst, size_t total, bool sync = true) {
+    // Ranges that continue each other in the arena and in the output (batch-contiguous output
+    // regions: TreeLSTM's logits are one run) go out as a few direct D2H copies: no pack kernel.
+    std::vector<int64_t> runs;
+    for (size_t k = 0; k + 2 < ranges.size() && runs.size() <= 24; k += 3) {
+      const size_t r = runs.size();
+      if (r && runs[r - 3] + runs[r - 2] == ranges[k] && runs[r - 1] + runs[r - 2] == ranges[k + 2])
+        runs[r - 2] += ranges[k + 1];
+      else
+        runs.insert(runs.end(), {ranges[k], ranges[k + 1], ranges[k + 2]});
+    }
+    if (runs.size() <= 24) {
+      mbx::ensure_d2h(c, total);
+      if (c->copy_pending) {  // (meta_commit's job on the other path: inputs before any read)
+        mbx::cuda_check(cudaStreamWaitEvent(c->stream, c->ev_copy, 0), "input copy wait");
+        c->copy_pending = false;
+      }
+      for (size_t k = 0; k < runs.size(); k += 3)
+        mbx::cuda_check(cudaMemcpyAsync(c->d2h_host + runs[k + 2], mbx::arena_ptr(c) + runs[k],
+                                        size_t(runs[k + 1]) * sizeof(float), cudaMemcpyDeviceToHost, c->stream),
+                        "D2H");
+      if (sync) {
+        mbx::stream_wait_own(c, "D2H sync");
+        std::memcpy(dst, c->d2h_host, total * sizeof(float));
+      }
+      timing.d2h_bytes += long(total * sizeof(float));
+      return;
+    }
+    {
+      // Permuted but compact (one batch's output region read in instance order): one D2H of the
+      // covering span, the permutation done on the host.
+      int64_t lo = INT64_MAX, hi = 0;
+      for (size_t k = 0; k + 2 < ranges.size(); k += 3) {
+        lo = std::min(lo, ranges[k]);
+        hi = std::max(hi, ranges[k] + ranges[k + 1]);
+      }
+      const int64_t span = hi - lo;
+      if (span > 0 && size_t(span) <= 4 * total + 1024) {
+        mbx::ensure_d2h(c, std::max(total, size_t(span)));
+        if (c->copy_pending) {
+          mbx::cuda_check(cudaStreamWaitEvent(c->stream, c->ev_copy, 0), "input copy wait");
+          c->copy_pending = false;
+        }
+        mbx::cuda_check(cudaMemcpyAsync(c->d2h_host, mbx::arena_ptr(c) + lo, size_t(span) * sizeof(float),
+                                        cudaMemcpyDeviceToHost, c->stream),
+                        "D2H");
+        if (sync) {
+          mbx::stream_wait_own(c, "D2H sync");
+          for (size_t k = 0; k + 2 < ranges.size(); k += 3)
+            std::memcpy(dst + ranges[k + 2], c->d2h_host + (ranges[k] - lo), size_t(ranges[k + 1]) * sizeof(float));
+        }
+        timing.d2h_bytes += long(span * int64_t(sizeof(float)));
+        return;
+      }
+    }
     mbx::meta_reserve(c, ranges.size() * 8 + 64);
     size_t moff = mbx::meta_stage(c, ranges.data(), ranges.size() * 8);
     mbx::meta_commit(c);
