@@ -692,7 +692,8 @@ void tc_prepare(mbx_ctx* c, PlanEntry& pe) {
       st->sfn = load_kernel(c, ssrc, "mbx_small_dense");
       pe.tc_exact = true;
       // Few output columns: tensor-core tiles would be mostly padding; exact in every precision.
-      pe.tc_small = st->U * st->G <= 64;
+      static const bool no_small = std::getenv("MBX_NO_TC_SMALL") != nullptr;  // experiment knob
+      pe.tc_small = st->U * st->G <= 64 && !no_small;
     }
     if (pe.force_vm) {  // decision-feeding: exact only
       pe.tc_small = pe.tc_exact;
