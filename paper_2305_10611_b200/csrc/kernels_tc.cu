@@ -279,6 +279,7 @@ std::string gen_levels_source(const TcState& st, int k) {
   if (std::getenv("MBX_FENCE_ONCE")) o << "#define MBX_FENCE_ONCE 1\n";
   if (std::getenv("MBX_ARRIVE_RELEASE")) o << "#define MBX_ARRIVE_RELEASE 1\n";
   if (std::getenv("MBX_SENTINEL")) o << "#define MBX_SENTINEL 1\n";
+  if (const char* e = std::getenv("MBX_FLAG_STRIDE")) o << "#define MBX_FLAG_STRIDE " << std::clamp(std::atoi(e), 1, 32) << "\n";
   if (const char* e = std::getenv("MBX_POLLERS")) o << "#define MBX_POLLERS " << std::max(1, std::atoi(e)) << "\n";
   o << jit::prelude_source();
   o << "#define MBX_LEVELS_KERNEL 1\n"
@@ -1182,8 +1183,8 @@ void issue_levels(mbx_ctx* c, const std::vector<BatchLaunch>& Ls, size_t i, int 
       // Every partial slot starts "not written" (MBX_PART_EMPTY in tc_gate.cuh).
       fill_u32<<<148, 256, 0, c->stream>>>(reinterpret_cast<unsigned*>(C.part), part_bytes / 4, 0xffbadbadu);
       cuda_check(cudaGetLastError(), "levels partials fill");
-      cuda_check(cudaMalloc(&C.flags, ngmax * utiles * C.S * 4), "levels flags");
-      cuda_check(cudaMemset(C.flags, 0, ngmax * utiles * C.S * 4), "levels flags");
+      cuda_check(cudaMalloc(&C.flags, ngmax * utiles * C.S * 128), "levels flags");  // up to one line each
+      cuda_check(cudaMemset(C.flags, 0, ngmax * utiles * C.S * 128), "levels flags");
     }
     a.part = C.part;
     a.xflags = C.flags;

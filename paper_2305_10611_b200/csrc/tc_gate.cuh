@@ -581,6 +581,9 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_gate(const _
 // polling loads contend with the producers' stores in L2 and the saved round trip is lost.
 #define MBX_SENTINEL 0
 #endif
+#ifndef MBX_FLAG_STRIDE
+#define MBX_FLAG_STRIDE 1  // arrival counters' spacing (unsigned): 32 = one 128-byte line each
+#endif
 #define MBX_PART_EMPTY 0xffbadbadu  // a NaN payload no computation produces: "partial not written yet"
 namespace mbx_gen {
 __device__ __forceinline__ void st_part(float* p, float v) {
@@ -1080,10 +1083,10 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const
       __syncthreads();
       MBX_LSTAMP(lv, 13);
       if (S > 1) {
-        unsigned* flags = P.xflags + (grp * gridDim.y + tile_u) * S;
-        if (tid < S && tid != int(rank)) red_release_add(flags + tid, 1u);
+        unsigned* flags = P.xflags + (grp * gridDim.y + tile_u) * S * MBX_FLAG_STRIDE;
+        if (tid < S && tid != int(rank)) red_release_add(flags + tid * MBX_FLAG_STRIDE, 1u);
         MBX_LSTAMP(lv, 3);
-        block_wait(flags + rank, unsigned(S - 1) * (it + 1), &s_seen, ++wepoch);
+        block_wait(flags + rank * MBX_FLAG_STRIDE, unsigned(S - 1) * (it + 1), &s_seen, ++wepoch);
       }
 #endif
       auto paddr = [&](int q, int n, int col) -> float* {
@@ -1229,7 +1232,8 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const
 #else
   // Every increment of this CTA's counter happened before its last wait: reset it for the next
   // launch (stream order makes launches sequential).
-  if (!MBX_SENTINEL && S > 1 && tid == 0 && it > 0) P.xflags[(grp * gridDim.y + tile_u) * S + rank] = 0u;
+  if (!MBX_SENTINEL && S > 1 && tid == 0 && it > 0)
+    P.xflags[((grp * gridDim.y + tile_u) * S + rank) * MBX_FLAG_STRIDE] = 0u;
 #endif
   if (warp == 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(P.tmem_cols) : "memory");
