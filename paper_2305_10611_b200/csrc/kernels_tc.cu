@@ -1119,6 +1119,11 @@ int plan_levels(mbx_ctx* c, const std::vector<BatchLaunch>& Ls, size_t i, size_t
     return e ? std::max(1, std::atoi(e)) : 0;
   }();
   if (k == 1 && wide_groups > 0) ng = std::min(ng, wide_groups);
+  static const int deep_groups = [] {  // experiment: cap the deep launch's node-tile groups
+    const char* e = std::getenv("MBX_DEEP_GROUPS");
+    return e ? std::max(1, std::atoi(e)) : 0;
+  }();
+  if (k == 0 && deep_groups > 0) ng = std::min(ng, deep_groups);
   *groups = ng;
   *cfg = k;
   std::vector<TcLevel> tbl(static_cast<size_t>(n));
@@ -1238,7 +1243,10 @@ void issue_levels(mbx_ctx* c, const std::vector<BatchLaunch>& Ls, size_t i, int 
   // Grid barrier (several levels) or cross-cluster counters (L2 exchange): every CTA must be
   // resident at once, so such launches take the device's persistent lane.
   static const bool lane_all = std::getenv("MBX_LANE_ALL") != nullptr;  // experiment knob
-  const bool lane = lane_all || n > 1 || (C.xch == 1 && C.S > 1);
+  // Experiment (MBX_NO_LANE, cooperative launches only): gang-scheduled persistent launches of
+  // different contexts may run side by side when they fit together.
+  static const bool no_lane = std::getenv("MBX_NO_LANE") != nullptr;
+  const bool lane = lane_all || ((n > 1 || (C.xch == 1 && C.S > 1)) && !(no_lane && coop));
   if (lane) lc.stream = persistent_lane_begin(c);
   cudaError_t le = cudaLaunchKernelExC(&lc, C.fn, args);
   if (le != cudaSuccess && coop && needs_all) {
