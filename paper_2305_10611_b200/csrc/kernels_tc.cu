@@ -1214,9 +1214,10 @@ void issue_levels(mbx_ctx* c, const std::vector<BatchLaunch>& Ls, size_t i, int 
     attrs[na].val.programmaticStreamSerializationAllowed = 1;
     ++na;
   }
-  // Grid barrier / cross-cluster counters need every CTA resident at once: a cooperative launch
-  // has the hardware place the whole grid together, so resident CTAs never spin waiting for SMs
-  // that other contexts' kernels keep taking (which could outlast the 2 s wait limit).
+  // Grid barrier / cross-cluster counters need every CTA resident at once.  Launched
+  // cooperatively, the grid is not left spinning partly resident while other contexts' clustered
+  // kernels keep taking the SMs it waits for (measured: ~1 in 4 pool runs hit the 2 s wait limit
+  // without it, none with it).  The lane still serialises persistent launches among themselves.
   // Not under Nsight Compute (its injection sets NV_NSIGHT_INJECTION_TRANSPORT_TYPE /
   // NV_COMPUTE_PROFILER_PERFWORKS_DIR; it fails cooperative launches with LaunchFailed, and it
   // serialises kernels, so co-residency holds there anyway), nor with MBX_NO_COOP.
