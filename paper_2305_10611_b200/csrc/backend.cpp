@@ -840,19 +840,11 @@ static int vm_weight_stage_floats(int temp_floats) {
   return std::max(0, std::min(budget, 32 * 1024));
 }
 
-void issue_batch(mbx_ctx* c, const BatchLaunch& L) {
-  const PlanEntry& pe = c->plans[L.plan_id];
-  if (pe.plan.ghost || c->dry) return;
+// The hoisted all-shared prefix of a plan (e.g. the TreeLSTM leaf cell's [hz|hz] . W), computed
+// once per parameter upload; issued before the batch (or the fused launch) that reads it.
+void issue_prefix(mbx_ctx* c, const BatchLaunch& L) {
+  PlanEntry& pe = c->plans[L.plan_id];
   float* arena = arena_ptr(c);
-  for (const auto& g : L.gathers) {
-    cuda_check(launch_gather_rows(arena, meta_dev<int64_t>(c, g.src_meta), g.dst, L.b, g.size, c->stream), "gather");
-    ++c->launches;
-    ++g_launches;
-  }
-  if (!L.sub.empty()) {  // split plan: head, then tail
-    for (const auto& S : L.sub) issue_batch(c, S);
-    return;
-  }
   bool prefix_cached = false;
   if (pe.prefix_plan >= 0) {
     // The prefix reads shared inputs only; if they are all session parameters its result is a
@@ -894,6 +886,22 @@ void issue_batch(mbx_ctx* c, const BatchLaunch& L) {
     ++c->launches;
     ++g_launches;
   }
+}
+
+void issue_batch(mbx_ctx* c, const BatchLaunch& L) {
+  const PlanEntry& pe = c->plans[L.plan_id];
+  if (pe.plan.ghost || c->dry) return;
+  float* arena = arena_ptr(c);
+  for (const auto& g : L.gathers) {
+    cuda_check(launch_gather_rows(arena, meta_dev<int64_t>(c, g.src_meta), g.dst, L.b, g.size, c->stream), "gather");
+    ++c->launches;
+    ++g_launches;
+  }
+  if (!L.sub.empty()) {  // split plan: head, then tail
+    for (const auto& S : L.sub) issue_batch(c, S);
+    return;
+  }
+  issue_prefix(c, L);
   // tc_kind 2 (pointwise) is exact and runs in every precision; tc_kind 1 (tensor cores) only
   // when the context allows split-bf16 / bf16 contractions.
   // The bit-exact gate kernel runs for small / decision plans in every precision and for every

@@ -172,6 +172,7 @@ BatchLaunch prepare_batch(mbx_ctx* c, int plan_id, int b, const int64_t* shared_
                           int64_t* gather_bytes);
 // Device half: enqueues the gather copies and the plan kernel (meta must be committed).
 void issue_batch(mbx_ctx* c, const BatchLaunch& L);
+void issue_prefix(mbx_ctx* c, const BatchLaunch& L);
 
 // Persistent multi-level launches (kernels_tc.cu): if launches [i, i+n) (n >= 1) are consecutive
 // batches of one tensor-core gate plan over the same weights that one mbx_tc_levels launch can

@@ -64,6 +64,13 @@ struct TcLevelsArgs {
   unsigned* xflags;              // MBX_LXCH 1: per (group, unit tile, rank) arrival counters, 0 at launch
   unsigned long long* stamps;    // MBX_STAMPS builds only
   TcLoad loads[MBX_MAX_LOADS];
+  // MBX_FUSE_PW: a pointwise batch that consumes this (single-level) launch's rows in node order
+  // runs in its tail; load pw_xt is the value just computed, the others are shared rows.
+  const long long* pw_shared_off;
+  const long long* pw_out_base;
+  int pw_xt;
+  int pw_pad;
+  TcLoad pw_loads[MBX_MAX_LOADS];
 };
 
 struct SmallArgs {

@@ -1095,6 +1095,23 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const
       auto partial = [&](int q, int n, int col) -> float { return __ldcg(paddr(q, n, col)); };
 #endif
       MBX_LSTAMP(lv, 4);
+#ifdef MBX_FUSE_PW
+      // Fused pointwise batch: its shared rows depend on the unit only, and a thread's elements
+      // (tid + t * MBX_THREADS) all share one unit.
+      static_assert(MBX_THREADS % MBX_UC == 0, "fused tail: one unit per thread");
+      float pw_sh[MBX_PW_NLOADS];
+      long long pw_ob[MBX_PW_NOUT];
+      {
+        const int ug0 = tile_u * MBX_UC + tid % MBX_UC;
+#pragma unroll
+        for (int j = 0; j < MBX_PW_NLOADS; ++j) {
+          const TcLoad& d = P.pw_loads[j];
+          pw_sh[j] = j == P.pw_xt ? 0.0f : __ldcg(P.arena + __ldg(P.pw_shared_off + d.idx) + d.off + ug0);
+        }
+#pragma unroll
+        for (int k = 0; k < MBX_PW_NOUT; ++k) pw_ob[k] = __ldg(P.pw_out_base + k);
+      }
+#endif
       // ---- sum the partials in rank order, run the tail, write the outputs ----
       // Every partial of every element is read before the first output store: through generic
       // pointers a store would order all later loads behind it (one L2 round trip per element).
@@ -1205,6 +1222,19 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const
           const int ug = tile_u * MBX_UC + u;
 #pragma unroll
           for (int k = 0; k < MBX_NOUT; ++k) P.arena[obase[k] + node * MBX_U + ug] = o[k];
+#ifdef MBX_FUSE_PW
+          {
+            // The next batch (elementwise over these rows, same node order) from registers: its
+            // own row is o[0], its shared rows were loaded before the first store (pw_sh).
+            float lp[MBX_PW_NLOADS];
+#pragma unroll
+            for (int j = 0; j < MBX_PW_NLOADS; ++j) lp[j] = j == P.pw_xt ? o[0] : pw_sh[j];
+            float op[MBX_PW_NOUT];
+            mbx_pw_tail_fast(lp, op);
+#pragma unroll
+            for (int k = 0; k < MBX_PW_NOUT; ++k) P.arena[pw_ob[k] + node * MBX_U + ug] = op[k];
+          }
+#endif
         }
       }
 #if MBX_LXCH == 0
