@@ -1211,29 +1211,36 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const
         }
       }
 #endif
+      // Every element's tail first (independent activation chains the scheduler can interleave),
+      // then the stores: a store between two elements would keep their chains apart.
+      float ov[MBX_LEPT][MBX_NOUT];
+#ifdef MBX_FUSE_PW
+      float pv[MBX_LEPT][MBX_PW_NOUT];
+#endif
+#pragma unroll
+      for (int t = 0; t < MBX_LEPT; ++t) {
+        mbx_tail(gsum[t], lreg[t], ov[t]);
+#ifdef MBX_FUSE_PW
+        // The next batch (elementwise over these rows, same node order) from registers: its own
+        // row is ov[t][0], its shared rows were loaded before the partial sums (pw_sh).
+        float lp[MBX_PW_NLOADS];
+#pragma unroll
+        for (int j = 0; j < MBX_PW_NLOADS; ++j) lp[j] = j == P.pw_xt ? ov[t][0] : pw_sh[j];
+        mbx_pw_tail_fast(lp, pv[t]);
+#endif
+      }
 #pragma unroll
       for (int t = 0; t < MBX_LEPT; ++t) {
         const int e = tid + t * MBX_THREADS;
         const int n = e / MBX_UC, u = e - n * MBX_UC;
         if (n < nloc && loc_col(n) < nn) {
-          float o[MBX_NOUT];
-          mbx_tail(gsum[t], lreg[t], o);
           const long long node = node0 + loc_col(n);
           const int ug = tile_u * MBX_UC + u;
 #pragma unroll
-          for (int k = 0; k < MBX_NOUT; ++k) P.arena[obase[k] + node * MBX_U + ug] = o[k];
+          for (int k = 0; k < MBX_NOUT; ++k) P.arena[obase[k] + node * MBX_U + ug] = ov[t][k];
 #ifdef MBX_FUSE_PW
-          {
-            // The next batch (elementwise over these rows, same node order) from registers: its
-            // own row is o[0], its shared rows were loaded before the first store (pw_sh).
-            float lp[MBX_PW_NLOADS];
 #pragma unroll
-            for (int j = 0; j < MBX_PW_NLOADS; ++j) lp[j] = j == P.pw_xt ? o[0] : pw_sh[j];
-            float op[MBX_PW_NOUT];
-            mbx_pw_tail_fast(lp, op);
-#pragma unroll
-            for (int k = 0; k < MBX_PW_NOUT; ++k) P.arena[pw_ob[k] + node * MBX_U + ug] = op[k];
-          }
+          for (int k = 0; k < MBX_PW_NOUT; ++k) P.arena[pw_ob[k] + node * MBX_U + ug] = pv[t][k];
 #endif
         }
       }
