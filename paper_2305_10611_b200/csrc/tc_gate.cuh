@@ -1229,6 +1229,9 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const
         mbx_pw_tail_fast(lp, pv[t]);
 #endif
       }
+#if MBX_LXCH == 0
+      MBX_LSTAMP(lv, 13);  // profiling (DSMEM configurations): tails computed, stores next
+#endif
 #pragma unroll
       for (int t = 0; t < MBX_LEPT; ++t) {
         const int e = tid + t * MBX_THREADS;
