@@ -653,6 +653,40 @@ DPlan compile_plan(const ExecutablePlan& p, int64_t& temp_per_inst, std::vector<
 // Set while the head / tail of a split plan are registered (they stay on the exact FP32 VM).
 static thread_local bool force_vm_next = false;
 
+// [dense(row . shared W), argmax(that row)] with the row 1 x K and W K x N (N <= 32): NestedRNN's
+// decision tail after the head / tail split.  Whole operands only (no column slices).
+static void detect_dense_argmax(PlanEntry& pe) {
+  using mbatch::backend::PlanRef;
+  using mbatch::backend::PlanStep;
+  static const bool off = std::getenv("MBX_NO_DENSE_ARGMAX") != nullptr;  // experiment knob
+  const ExecutablePlan& p = pe.exec_plan;
+  if (off || pe.tc_kind != -1 || pe.prefix_plan >= 0 || p.ghost || p.steps.size() != 2 || p.outputs.empty() || p.outputs.size() > 2) return;
+  const PlanStep& d = p.steps[0];
+  const PlanStep& m = p.steps[1];
+  if (d.kind != PlanStep::Kind::kOp || d.op != OpCode::kDense || d.ins.size() != 2) return;
+  if (m.kind != PlanStep::Kind::kOp || m.op != OpCode::kArgmax || m.ins.size() != 1) return;
+  const PlanRef &a = d.ins[0], &w = d.ins[1], &r = m.ins[0];
+  if (r.kind != PlanRef::Kind::kTemp || r.index != 0 || r.cols >= 0) return;
+  if (w.kind != PlanRef::Kind::kShared || w.cols >= 0 || a.cols >= 0 || a.kind == PlanRef::Kind::kTemp) return;
+  const auto& as = a.kind == PlanRef::Kind::kBatched ? p.batched_shapes[size_t(a.index)] : p.shared_shapes[size_t(a.index)];
+  const auto& ws = p.shared_shapes[size_t(w.index)];
+  if (as.rows != 1 || as.cols != ws.rows || ws.cols < 1 || ws.cols > 32) return;
+  int outs[2] = {0, 0};
+  for (size_t k = 0; k < p.outputs.size(); ++k) {
+    const PlanRef& o = p.outputs[k];
+    if (o.kind != PlanRef::Kind::kTemp || o.cols >= 0 || o.index < 0 || o.index > 1) return;
+    outs[k] = o.index;
+  }
+  pe.da = true;
+  pe.da_k = ws.rows;
+  pe.da_n = ws.cols;
+  pe.da_a_batched = a.kind == PlanRef::Kind::kBatched ? 1 : 0;
+  pe.da_a_idx = a.index;
+  pe.da_w_idx = w.index;
+  pe.da_out[0] = outs[0];
+  pe.da_out[1] = outs[1];
+}
+
 int register_plan(mbx_ctx* c, const ExecutablePlan& plan) {
   std::vector<int32_t> enc = mbatch::backend::encode_plan(plan);
   auto it = c->plan_by_enc.find(enc);
@@ -716,6 +750,7 @@ int register_plan(mbx_ctx* c, const ExecutablePlan& plan) {
       pe.max_split = 1;
     }
     tc_prepare(c, pe);  // force_vm plans get only the bit-exact gate kernel, if any
+    detect_dense_argmax(pe);
   }
   int id = int(c->plans.size());
   c->plans.push_back(std::move(pe));
@@ -909,6 +944,16 @@ void issue_batch(mbx_ctx* c, const BatchLaunch& L) {
   if (pe.tc_kind == 2 || pe.tc_small || (pe.tc_exact && c->precision == MBX_PREC_FP32) ||
       (c->precision != MBX_PREC_FP32 && pe.tc_kind == 1)) {
     cuda_check(tc_launch(c, pe, L), "tensor-core plan kernel");
+    ++c->launches;
+    ++g_launches;
+    return;
+  }
+  if (pe.da) {
+    cuda_check(launch_dense_argmax(arena, meta_dev<int64_t>(c, L.shared_meta), meta_dev<int64_t>(c, L.batched_meta),
+                                   L.b, int(pe.exec_plan.batched_shapes.size()), pe.da_a_batched, pe.da_a_idx,
+                                   pe.da_w_idx, pe.da_k, pe.da_n, meta_dev<int64_t>(c, L.out_meta),
+                                   int(pe.exec_plan.outputs.size()), pe.da_out[0], pe.da_out[1], c->stream),
+               "dense + argmax");
     ++c->launches;
     ++g_launches;
     return;

@@ -41,6 +41,10 @@ struct PlanEntry {
   std::vector<int> tail_in_src;              // tail extra batched input j: >= 0 original output, < 0 -1-boundary
   std::vector<int> tail_orig_out;            // original output index of tail output k
   bool force_vm = false;                     // exact FP32 plan VM only (decision-feeding heads)
+  // dense (1 x K . K x N, N <= 32) + argmax plans (NestedRNN's decision tail): a dedicated exact
+  // kernel (launch_dense_argmax) instead of the general plan VM.  da_out[k]: 0 row, 1 decision.
+  bool da = false;
+  int da_k = 0, da_n = 0, da_a_batched = 0, da_a_idx = 0, da_w_idx = 0, da_out[2] = {0, 0};
   int tc_kind = -1;                  // tensor-core kernel for this plan (kernels_tc.cu), -1 none
   bool tc_small = false;             // gate plan served by the bit-exact kernel in every precision
   bool tc_exact = false;             // the bit-exact CUDA-core gate kernel exists (FP32 contexts use it)

@@ -425,6 +425,56 @@ __global__ void fill_kernel(float* arena, int64_t off, int64_t n, float v) {
 
 }  // namespace
 
+// dense + argmax plans (backend.cpp:116-131, :164-173), one CTA per node: the weight (K x N) and
+// the node's row go to shared memory, N threads run the exact sequential chains (p ascending,
+// separately rounded multiply and add), thread 0 takes the first index of the maximum.
+__global__ void __launch_bounds__(256) dense_argmax_kernel(float* arena, const int64_t* shared_off,
+                                                           const int64_t* batched_off, int nb, int a_batched, int a_idx,
+                                                           int w_idx, int K, int N, const int64_t* out_base, int nout,
+                                                           int out0, int out1) {
+  extern __shared__ float sm[];
+  float* ws = sm;           // [K][N]
+  float* as = sm + K * N;   // [K]
+  float* row = as + K;      // [N]
+  const int node = blockIdx.x;
+  const float* a = arena + (a_batched ? batched_off[int64_t(node) * nb + a_idx] : shared_off[a_idx]);
+  const float* w = arena + shared_off[w_idx];
+  for (int i = threadIdx.x; i < K * N; i += blockDim.x) ws[i] = w[i];
+  for (int i = threadIdx.x; i < K; i += blockDim.x) as[i] = a[i];
+  __syncthreads();
+  if (int(threadIdx.x) < N) {
+    float acc = 0.0f;
+#pragma unroll 8
+    for (int p = 0; p < K; ++p) acc = fadd(acc, fmul(as[p], ws[p * N + threadIdx.x]));
+    row[threadIdx.x] = acc;
+  }
+  __syncthreads();
+  const int outs[2] = {out0, out1};
+  for (int k = 0; k < nout; ++k) {
+    if (outs[k] == 0) {
+      for (int j = threadIdx.x; j < N; j += blockDim.x) arena[out_base[k] + int64_t(node) * N + j] = row[j];
+    } else if (threadIdx.x == 0) {
+      int best = 0;
+      for (int i = 1; i < N; ++i)
+        if (row[i] > row[best]) best = i;
+      arena[out_base[k] + node] = static_cast<float>(best);
+    }
+  }
+}
+
+cudaError_t launch_dense_argmax(float* arena, const int64_t* shared_off, const int64_t* batched_off, int b, int nb,
+                                int a_batched, int a_idx, int w_idx, int K, int N, const int64_t* out_base, int nout,
+                                int out0, int out1, cudaStream_t stream) {
+  const size_t smem = size_t(K * N + K + N) * sizeof(float);
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(dense_argmax_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+  }
+  dense_argmax_kernel<<<b, 256, smem, stream>>>(arena, shared_off, batched_off, nb, a_batched, a_idx, w_idx, K, N,
+                                                out_base, nout, out0, out1);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_plan_vm(const VmLaunch& L, cudaStream_t stream) {
   static bool attr_set = false;
   if (!attr_set) {
