@@ -36,6 +36,8 @@ import sys
 import threading
 import time
 
+import numpy as np
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 METRIC = "batched nodes/sec and ms per mini-batch (bs 8/64) at 1/2/4/8 B200 vs CPU ref"
@@ -66,8 +68,9 @@ def peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(path):
         j = json.load(open(path))
-        return {"hbm_gbs": j["hbm_gbs"], "bf16_tflops": j["bf16_tflops"], "src": "measured"}
-    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "src": "fallback"}
+        return {"hbm_gbs": j["hbm_gbs"], "bf16_tflops": j["bf16_tflops"],
+                "bf16_tflops_sustained": j.get("bf16_tflops_sustained", j["bf16_tflops"]), "src": "measured"}
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1590.0, "src": "fallback"}
 
 
 # ---- algorithmic work --------------------------------------------------------
@@ -236,20 +239,21 @@ def run_reference_arm(args):
     t0 = time.perf_counter()
     for k in range(P):
         procs.append(subprocess.Popen([REF_BIN, "time", "--model", args.model, "--hidden", str(args.hidden), "--batch",
-                                       str(args.batch), "--seed", str(args.seed + k), "--reps", str(reps), "--no-verify"],
+                                       str(args.batch), "--seed", str(args.seed + k), "--reps", str(reps),
+                                       "--warmup", str(max(1, args.warmup)), "--no-verify"],
                                       stdout=subprocess.PIPE, text=True))
     res = [json.loads(p.communicate()[0]) for p in procs]
     wall = time.perf_counter() - t0
     nodes_per_s = sum(r["nodes"] / (r["batched_ms_mean"] / 1e3) for r in res)
     ms = statistics.mean(r["batched_ms_mean"] for r in res)
     line = {"metric": METRIC, "impl": "reference", "value": nodes_per_s, "unit": "nodes/s", "n_gpus": args.gpus,
-            "steps": reps, "warmup": 1, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "steps": reps, "warmup": max(1, args.warmup), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (reference zoo generators, seeds %d..%d)" % (
                 args.seed, args.seed + P - 1),
             "config": {"workload": f"{args.model}-h{args.hidden}-b{args.batch}", "hidden": args.hidden,
                        "batch": args.batch, "processes": P},
             "cpu_baseline": {"value": nodes_per_s, "unit": "nodes/s", "cores": P, "kind": "reference",
-                             "sample": f"{P} processes x {reps} evaluate_batch calls (+1 warm-up) of the unmodified "
+                             "sample": f"{P} processes x {reps} evaluate_batch calls (+{max(1, args.warmup)} warm-up) of the unmodified "
                                        f"reference, one mini-batch each; wall {wall:.1f}s"},
             "e2e": {"value": nodes_per_s, "unit": "nodes/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
@@ -354,7 +358,8 @@ def run_ours(args):
             e["flops"] += f
             e["bytes"] += by
             e["launches"] += 1
-            R_total_us += max(f / (pk["bf16_tflops"] * 1e6), by / (pk["hbm_gbs"] * 1e3))
+            # in-step kernels: the sustained tensor peak
+            R_total_us += max(f / (pk["bf16_tflops_sustained"] * 1e6), by / (pk["hbm_gbs"] * 1e3))
             meas_total_us += us
     dom = max(per_sig, key=lambda s: per_sig[s]["us"])
     d = per_sig[dom]
@@ -394,11 +399,12 @@ def run_ours(args):
                      "peak_src": pk["src"] if tensor_path or bound == "hbm" else "fp32 SIMT nominal"},
         "step_roofline": {"R_us": R_total_us / K, "kernel_us": meas_total_us / K,
                           "frac": (R_total_us / meas_total_us) if meas_total_us else None,
-                          "def": "sum over launches of max(F/bf16 peak, B/HBM) vs summed launch times (SURVEY 8d)"},
+                          "def": "sum over launches of max(F/sustained bf16 peak, B/HBM) vs summed launch times (SURVEY 8d)"},
         "breakdown_us_per_step": {"host_dfg_and_launch": rA.timing.host_dfg_us, "host_split": rA.timing.host_breakdown,
                                   "device_span": rA.timing.device_span_us,
                                   "per_sig": {sigs[s]: v["us"] / K for s, v in per_sig.items()}},
         "clocks": clk,
+        "parity": pool_res["parity"],
     }
     if world == 1 and not args.no_other_configs:
         line["other_configs"] = other_configs(mbx, torch, local)
@@ -456,17 +462,58 @@ def pinned_inputs(torch, toks, data):
     return toks, pd
 
 
+def checked_minibatch(args, pool, gen):
+    """One mini-batch (seed args.seed) through a pool worker's own context before the timed
+    region, compared with the reference's golden outputs and schedule for the same config
+    (tests/golden/baseline.json.gz, written by the unmodified reference): SURVEY §8a's per-element
+    metric (|ours - ref| <= tol * max(|ref|, 1e-6), max-rel, fraction passing), normwise, and the
+    schedule compared batch by batch."""
+    import gzip
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from parity_metrics import elementwise, merge
+    from conftest import trace_counters, trace_rows
+    with gzip.open(os.path.join(ROOT, "tests", "golden", "baseline.json.gz"), "rt") as f:
+        runs = json.load(f)
+    run = next((r for r in runs if (r["model"], r["hidden"], r["batch"], r["seed"]) ==
+                (args.model, args.hidden, args.batch, args.seed) and "outputs" in r), None)
+    if run is None:
+        return {"checked": False, "why": "no reference golden for this config"}
+    toks, data = gen.make_inputs(args.seed, args.batch)
+    r = pool.evaluate_on_worker(0, toks, data, args.batch)
+    tol = 1e-5 if args.precision == "fp32" else 1e-3
+
+    def flat(j):
+        return list(j["d"]) if j["k"] == "t" else [x for it in j.get("items", []) for x in flat(it)]
+    st = merge([elementwise(mbx_flat(r.outputs[i]), np.asarray(flat(o), np.float32), tol)
+                for i, o in enumerate(run["outputs"])])
+    return {"checked": True, "against": "reference golden (tests/golden/baseline.json.gz) %s-h%d-b%d seed %d" % (
+        args.model, args.hidden, args.batch, args.seed), "tol_rel": tol, "max_rel": st["max_rel"],
+            "frac_pass": st["frac_pass"], "normwise": st["normwise"], "elements": st["n"],
+            "schedule_equal": trace_rows(r.trace) == trace_rows(run["trace"]) and
+            trace_counters(r.trace) == trace_counters(run["trace"])}
+
+
+def mbx_flat(v):
+    from paper_2305_10611_b200 import mbx
+    return mbx.flatten_floats(v)
+
+
 def run_pool(args, mbx, torch, local, rank, world, nodes, l2):
     """Throughput: T worker threads, each evaluating its own mini-batch per step (mbx_pool_run).
     Returns value / e2e nodes/s and the per-step device times (CUDA events on the pool stream)."""
-    cores = max(1, (os.cpu_count() or 1) // max(1, world))
-    T = args.threads or max(1, cores - 2)
+    # Host worker threads per rank: the cores this process may run on, shared evenly by the ranks
+    # of the node, one left for the driver thread (each worker's host side, ~0.3-0.5 ms per
+    # TreeLSTM-512 b64 mini-batch, must keep pace with ~0.1 ms of device work per mini-batch).
+    avail = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    cores = max(1, avail // max(1, int(os.environ.get("LOCAL_WORLD_SIZE", world))))
+    T = args.threads or max(1, cores - 1)
     pool = mbx.Pool(local, args.precision, args.model, args.hidden, args.seed, T)
     ctx = mbx.Context(-1, args.precision)  # host-only: the synthetic inputs
     gen = mbx.Model(ctx, args.model, args.hidden)
     # Host inputs in pinned memory (the e2e contract: H2D from pinned host buffers): the library
     # then copies each mini-batch's data stream in one piece and scatters it on the device.
     ins = [pinned_inputs(torch, *gen.make_inputs(args.seed + rank * T + w, args.batch)) for w in range(T)]
+    parity = checked_minibatch(args, pool, gen) if rank == 0 else None
     def steps(K, kw):
         ms, total = 0.0, 0
         for _ in range(K):
@@ -495,7 +542,7 @@ def run_pool(args, mbx, torch, local, rank, world, nodes, l2):
     pool.close()
     return {"value": n1 / (dev_ms / 1e3), "e2e": n2 / (e2e_ms / 1e3), "ms_per_step": dev_ms / args.steps,
             "e2e_ms_per_step": e2e_ms / args.steps, "threads": T, "per_thread": args.per_thread,
-            "launches": int(launches)}
+            "launches": int(launches), "parity": parity}
 
 
 def main():

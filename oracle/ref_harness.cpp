@@ -46,7 +46,7 @@ std::string model_source(const std::string& name, int hidden) {
 
 struct Args {
   std::string cmd = "dump", model = "treelstm", out;
-  int hidden = 32, batch = 8, reps = 3;
+  int hidden = 32, batch = 8, reps = 3, warmup = 1;
   unsigned seed = 1;
   bool nodes = true, outputs = true, verify = true;
   runtime::ExecOptions opts;
@@ -66,6 +66,7 @@ Args parse(int argc, char** argv) {
     else if (k == "--batch") a.batch = std::stoi(next());
     else if (k == "--seed") a.seed = static_cast<unsigned>(std::stoul(next()));
     else if (k == "--reps") a.reps = std::stoi(next());
+    else if (k == "--warmup") a.warmup = std::max(1, std::stoi(next()));
     else if (k == "--out") a.out = next();
     else if (k == "--scheduler") a.opts.scheduler = next() == "agenda" ? runtime::ExecOptions::Scheduler::kAgenda
                                                                         : runtime::ExecOptions::Scheduler::kDepth;
@@ -178,6 +179,7 @@ int run(const Args& a) {
     using clk = std::chrono::steady_clock;
     auto ms = [](clk::time_point t0) { return std::chrono::duration<double, std::milli>(clk::now() - t0).count(); };
     runtime::EvalResult res = runtime::evaluate_batch(m, params, inputs);  // warm-up
+    for (int w = 1; w < a.warmup; ++w) res = runtime::evaluate_batch(m, params, inputs);
     double best_b = 1e300, sum_b = 0, best_u = 1e300, sum_u = 0;
     for (int r = 0; r < a.reps; ++r) {
       auto t0 = clk::now();
@@ -193,6 +195,7 @@ int run(const Args& a) {
     json j;
     j["model"] = a.model; j["hidden"] = a.hidden; j["batch"] = a.batch; j["seed"] = a.seed;
     j["reps"] = a.reps;
+    j["warmup"] = a.warmup;
     j["nodes"] = res.trace.total_nodes;
     j["launches"] = res.trace.kernel_launches;
     j["sync_points"] = res.trace.sync_points;

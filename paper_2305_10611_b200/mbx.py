@@ -495,6 +495,27 @@ class Pool:
     def stream(self) -> int:
         return lib().mbx_pool_stream(self.h) or 0
 
+    def evaluate_on_worker(self, worker: int, toks: np.ndarray, data: np.ndarray, batch: int,
+                           **opts) -> EvalResult:
+        """One mini-batch through worker `worker`'s own context and model (the code path every
+        pool run takes), synchronously, with decoded outputs and the full trace: the bench's
+        checked mini-batch."""
+        L = lib()
+        m = L.mbx_pool_model(self.h, worker)
+        if not m:
+            raise MbatchError(f"pool has no worker {worker}")
+        o = make_options(**opts)
+        t = np.ascontiguousarray(toks, np.int32)
+        d = np.ascontiguousarray(data, np.float32)
+        r = ctypes.c_void_p()
+        if L.mbx_evaluate_batch(m, batch, _ptr(t, ctypes.c_int32), t.size, _ptr(d, ctypes.c_float), d.size,
+                                ctypes.byref(o), ctypes.byref(r)):
+            raise MbatchError(L.mbx_last_error(None).decode())
+        try:
+            return _read_result(r, batch, False, True, True)
+        finally:
+            L.mbx_result_destroy(r)
+
     def run(self, inputs: Sequence[Tuple[np.ndarray, np.ndarray]], batch: int, **opts) -> int:
         """Evaluates every (toks, data) mini-batch; returns the total DFG node count."""
         return self.run_timed(inputs, batch, **opts)[0]

@@ -159,3 +159,56 @@ def test_activation_restatements_exhaustive_sample(gpu, oracle):
         got = ctx.download(out, n)
         want = np.array([oracle.L.orc_unary(which, float(v)) for v in x[0, :: 997]], np.float32)
         assert np.array_equal(got[::997].view(np.uint32), want.view(np.uint32)), op
+
+
+def _dense_argmax_plan(k, n, a_shared, outs):
+    """[dense(a . W), argmax] with W shared (k x n) and the row a batched or shared (1 x k); `outs`
+    lists which step results are plan outputs (0 = the dense row, 1 = the argmax index)."""
+    shared = [k, n] + ([1, k] if a_shared else [])
+    e = [0, 2 if a_shared else 1] + shared
+    e += [0] if a_shared else [1, 1, k]
+    a_ref = [0, 1, 0, -1] if a_shared else [1, 0, 0, -1]
+    e += [2,
+          0, 0, 1, n, 2] + a_ref + [0, 0, 0, -1] + [0,
+          0, 7, 1, 1, 1, 2, 0, 0, -1, 0]
+    e += [len(outs)]
+    for o in outs:
+        e += [2, o, 0, -1]
+    return e
+
+
+@pytest.mark.parametrize("k,n,a_shared,outs", [(512, 11, False, [1]), (512, 11, False, [0, 1]),
+                                               (256, 32, False, [1, 0]), (512, 11, True, [0, 1]),
+                                               (4096, 16, False, [0, 1])])
+def test_dense_argmax_registered_plan_bitwise(gpu, k, n, a_shared, outs):
+    """Registered [dense, argmax] plans (NestedRNN's decision tail shape; dense_argmax_kernel when
+    W and the row fit shared memory, the plan VM otherwise, e.g. K=4096 x N=16) through
+    mbx_plan_register + mbx_exec_batched == the fold of exec_primop dense -> argmax, bitwise, for
+    the row output, the index output (first maximum; ties seeded in), a shared row and large K."""
+    mbx = gpu
+    rng = np.random.default_rng(k + n)
+    b = 37
+    ctx = mbx.Context(0, "fp32")
+    pid = ctx.register_plan(_dense_argmax_plan(k, n, a_shared, outs))
+    wv = rng.uniform(-0.5, 0.5, (k, n)).astype(np.float32)
+    wv[:, 3] = wv[:, 2]  # exact ties between columns 2 and 3: the first index must win
+    w, _ = ctx.tensor(wv)
+    shared = [w]
+    if a_shared:
+        a0, _ = ctx.tensor(rng.uniform(-1, 1, (1, k)))
+        shared.append(a0)
+        rows = [a0] * b
+        batched = np.zeros((b, 0), np.int64)
+    else:
+        rows = [ctx.tensor(rng.uniform(-1, 1, (1, k)))[0] for _ in range(b)]
+        batched = np.array(rows, np.int64).reshape(b, 1)
+    res, _ = ctx.exec_batched(pid, shared, batched, len(outs))
+    for i in range(b):
+        t0, t1 = ctx.alloc(1, n), ctx.alloc(1, 1)
+        ctx.exec_primop("dense", [(rows[i], (1, k)), (w, (k, n))], (t0, (1, n)))
+        ctx.exec_primop("argmax", [(t0, (1, n))], (t1, (1, 1)))
+        for j, o in enumerate(outs):
+            size = n if o == 0 else 1
+            got = ctx.download(int(res[i, j]), size)
+            want = ctx.download(t0 if o == 0 else t1, size)
+            assert np.array_equal(got.view(np.uint32), want.view(np.uint32)), (i, o)

@@ -2,8 +2,16 @@
 
 SURVEY §8a tolerance table: the schedule is always compared exactly (same batches, same node ids,
 same order, same counters; for NestedRNN / DRNN / StackRNN that also proves every argmax decision
-matched), and every output tensor must match the reference within the stated tolerance:
-    bf16x3 (TreeLSTM-512, BiRNN-512, NestedRNN-512 configs): normwise rel 1e-3 per instance
+matched), and every output tensor must match the reference within the stated tolerance.  The
+metric is SURVEY §8a's, per element: |gpu - ref| <= 1e-3 * max(|ref|, 1e-6), reported as max-rel
+and fraction of elements passing (tests/parity_metrics.py; every run's figures are written to
+gpurun_out/parity_tc.jsonl and summarised in profiles/r2_parity.md):
+    bf16x3 (TreeLSTM-512, BiRNN-512, NestedRNN-512 configs): >= 98% of elements within rel 1e-3
+          per element, and normwise rel <= 1e-3 (||gpu - ref|| / ||ref||) as a secondary check.
+          Not 100%: TreeLSTM-512 b64's logits are relu(h . c_wt + b) after 10 levels whose cell
+          state c accumulates the split-bf16 rounding (~5e-6 per level); logits that the relu leaves
+          near zero carry abs errors ~1e-4..1e-3 and fail the relative test (3 of 512 at seed 1,
+          7 of 512 at seed 2; max-rel 2.3e-3 / 2.4e-2).  Every other config passes 100%.
     bf16 (weights and rows rounded to bf16, single pass; not a headline precision, it cannot meet
           1e-3: TreeLSTM-512 b64 measures ~0.11 normwise on its 8 logits): rel 2.5e-1, a smoke
           check that the single-pass kernels run and stay finite
@@ -12,14 +20,26 @@ oracle/make_golden.py) or, where a golden run stores digests only, the FP32 devi
 test_gpu_parity.py proves bit-identical to the reference.  These runs go through the persistent
 multi-level kernel (mbx_tc_levels) wherever a flush has consecutive batches of one gate plan.
 """
+import json
+import os
+
 import numpy as np
 import pytest
 
-from conftest import MODELS, trace_counters, trace_rows
+from conftest import MODELS, ROOT, trace_counters, trace_rows
+from parity_metrics import elementwise, merge
 
 pytestmark = pytest.mark.gpu
 
 TOL = {"bf16x3": 1e-3, "bf16": 2.5e-1}
+MIN_PASS = {"bf16x3": 0.98, "bf16": 0.0}  # fraction of elements within TOL per element (see above)
+REPORT = os.path.join(ROOT, "gpurun_out", "parity_tc.jsonl")
+
+
+def _report(row):
+    os.makedirs(os.path.dirname(REPORT), exist_ok=True)
+    with open(REPORT, "a") as f:
+        f.write(json.dumps(row) + "\n")
 
 
 @pytest.fixture(scope="module")
@@ -69,15 +89,19 @@ def _check(mbx, run, model, prec):
     assert trace_rows(r.trace) == trace_rows(run["trace"]), where
     assert trace_counters(r.trace) == trace_counters(run["trace"]), where
     want = _reference_outputs(mbx, run, model, t, d)
-    worst = 0.0
+    stats = []
     for i, w in enumerate(want):
         got = mbx.flatten_floats(r.outputs[i])
         assert got.shape == w.shape, where + (i,)
         assert np.all(np.isfinite(got)), where + (i,)
-        err = float(np.linalg.norm(got - w) / max(1e-30, np.linalg.norm(w)))
-        worst = max(worst, err)
-        assert err <= TOL[prec], where + (i, err)
-    return worst
+        st = elementwise(got, w, TOL[prec])
+        stats.append(st)
+        assert st["normwise"] <= TOL[prec], where + (i, st)
+    tot = merge(stats)
+    _report(dict(model=model, prec=prec, hidden=run["hidden"], batch=run["batch"], seed=run["seed"],
+                 variant=run.get("variant"), schedule_equal=True, **tot))
+    assert tot["frac_pass"] >= MIN_PASS[prec], where + (tot,)
+    return tot
 
 
 @pytest.mark.parametrize("idx", range(10))
@@ -93,11 +117,9 @@ def test_tc_baseline_configs(gpu, golden, idx, prec):
 
 @pytest.mark.parametrize("model", MODELS)
 def test_tc_zoo_models(gpu, golden, model):
-    """Every zoo model at the reference's own sizes (H 32/64, b 1..64, seeds, scheduler and gather
-    variants) on the split-bf16 path: exact schedule, outputs within 1e-3."""
+    """Every zoo model at the reference's own sizes (H 32/64, b 1..64, seeds, both schedulers and
+    both gather modes) on the split-bf16 path: exact schedule, outputs within 1e-3."""
     for run in golden(model)["runs"]:
-        if run["variant"] == "depth-explicit":
-            continue
         _check(gpu, run, model, "bf16x3")
 
 
@@ -117,8 +139,8 @@ def test_levels_kernel_covers_internal_depths(gpu, golden):
     assert len(r.timing.batch_us) == len(launches)
     want = [np.array(_flat_golden(o), np.float32) for o in run["outputs"]]
     got = np.concatenate([mbx.flatten_floats(o) for o in r.outputs])
-    ref = np.concatenate(want)
-    assert np.linalg.norm(got - ref) / np.linalg.norm(ref) <= 1e-3
+    st = elementwise(got, np.concatenate(want), 1e-3)
+    assert st["normwise"] <= 1e-3 and st["frac_pass"] >= MIN_PASS["bf16x3"], st
 
 
 def test_fused_leaf_cell_opt_in(gpu):
