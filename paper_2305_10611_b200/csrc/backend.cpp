@@ -55,7 +55,7 @@ PersistentLane& lane_of(int device) {
 cudaStream_t persistent_lane_begin(mbx_ctx* c) {
   if (!c->serialize_persistent || c->dry) return c->stream;
   PersistentLane& L = lane_of(c->device);
-  L.mu.lock();
+  std::unique_lock<std::mutex> lock(L.mu);  // released on every error path below
   if (!L.stream) {
     // Highest priority: when SMs free up, the block scheduler places the lane kernel's CTAs first
     // (its resident CTAs wait at the grid barrier for the rest).
@@ -68,16 +68,18 @@ cudaStream_t persistent_lane_begin(mbx_ctx* c) {
   // The launch follows this context's work so far ...
   cuda_check(cudaEventRecord(c->ev_persist, c->stream), "persistent lane record");
   cuda_check(cudaStreamWaitEvent(L.stream, c->ev_persist, 0), "persistent lane wait");
+  lock.release();  // held until persistent_lane_end
   return L.stream;
 }
 
 void persistent_lane_end(mbx_ctx* c) {
   if (!c->serialize_persistent || c->dry) return;
   PersistentLane& L = lane_of(c->device);
-  // ... and this context's later work follows the launch.
+  std::unique_lock<std::mutex> lock(L.mu, std::adopt_lock);  // taken by persistent_lane_begin
+  // ... and this context's later work follows the launch.  (The lock is released even if these
+  // throw after a sticky device error, so the other workers fail instead of blocking.)
   cuda_check(cudaEventRecord(L.done, L.stream), "persistent lane record");
   cuda_check(cudaStreamWaitEvent(c->stream, L.done, 0), "persistent lane wait");
-  L.mu.unlock();
 }
 
 void persistent_lane_forget(mbx_ctx* c) { (void)c; }
@@ -140,6 +142,8 @@ void arena_init(mbx_ctx* c) {
   c->chunk_bytes = ((size_t(256) << 20) + gran - 1) / gran * gran;
   c->reserve_bytes = size_t(128) << 30;  // 128 GiB of address space; physical memory on demand
   cu_check(api.reserve(&c->base, c->reserve_bytes, 0, 0, 0), "cuMemAddressReserve");
+  // The split-bf16 shadow (same byte size, same offsets; mapped in lockstep with the arena).
+  cu_check(api.reserve(&c->shadow_base, c->reserve_bytes, 0, 0, 0), "cuMemAddressReserve (shadow)");
 }
 
 void arena_release(mbx_ctx* c) {
@@ -150,8 +154,15 @@ void arena_release(mbx_ctx* c) {
     api.release(c->chunks[k]);
   }
   c->chunks.clear();
+  for (size_t k = 0; k < c->shadow_chunks.size(); ++k) {
+    api.unmap(c->shadow_base + k * c->chunk_bytes, c->chunk_bytes);
+    api.release(c->shadow_chunks[k]);
+  }
+  c->shadow_chunks.clear();
   api.addr_free(c->base, c->reserve_bytes);
+  if (c->shadow_base) api.addr_free(c->shadow_base, c->reserve_bytes);
   c->base = 0;
+  c->shadow_base = 0;
 }
 
 static void arena_map_to(mbx_ctx* c, size_t bytes) {
@@ -163,14 +174,17 @@ static void arena_map_to(mbx_ctx* c, size_t bytes) {
     prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
     prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
     prop.location.id = c->device;
-    CUmemGenericAllocationHandle h;
-    cu_check(api.create(&h, c->chunk_bytes, &prop, 0), "cuMemCreate");
-    cu_check(api.map(c->base + c->mapped_bytes, c->chunk_bytes, 0, h, 0), "cuMemMap");
     CUmemAccessDesc acc{};
     acc.location = prop.location;
     acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
-    cu_check(api.set_access(c->base + c->mapped_bytes, c->chunk_bytes, &acc, 1), "cuMemSetAccess");
-    c->chunks.push_back(h);
+    for (int shadow = 0; shadow < 2; ++shadow) {
+      const CUdeviceptr at = (shadow ? c->shadow_base : c->base) + c->mapped_bytes;
+      CUmemGenericAllocationHandle h;
+      cu_check(api.create(&h, c->chunk_bytes, &prop, 0), "cuMemCreate");
+      cu_check(api.map(at, c->chunk_bytes, 0, h, 0), "cuMemMap");
+      cu_check(api.set_access(at, c->chunk_bytes, &acc, 1), "cuMemSetAccess");
+      (shadow ? c->shadow_chunks : c->chunks).push_back(h);
+    }
     c->mapped_bytes += c->chunk_bytes;
   }
 }
@@ -671,6 +685,9 @@ static void detect_dense_argmax(PlanEntry& pe) {
   const auto& as = a.kind == PlanRef::Kind::kBatched ? p.batched_shapes[size_t(a.index)] : p.shared_shapes[size_t(a.index)];
   const auto& ws = p.shared_shapes[size_t(w.index)];
   if (as.rows != 1 || as.cols != ws.rows || ws.cols < 1 || ws.cols > 32) return;
+  // The kernel stages W and the row in shared memory: (K*N + K + N) floats must fit the opt-in
+  // limit; larger plans keep the plan VM (any K).
+  if ((int64_t(ws.rows) * ws.cols + ws.rows + ws.cols) * 4 > 227 * 1024) return;
   int outs[2] = {0, 0};
   for (size_t k = 0; k < p.outputs.size(); ++k) {
     const PlanRef& o = p.outputs[k];

@@ -160,7 +160,7 @@ void mbx_ctx_destroy(mbx_ctx* c) {
     if (c->d2h_dev) cudaFree(c->d2h_dev);
     if (c->in_host) cudaFreeHost(c->in_host);
     if (c->tc_part) cudaFree(c->tc_part);
-    if (c->gbar) cudaFree(c->gbar);
+    if (c->img_buf) cudaFree(c->img_buf);
     try { mbx::arena_release(c); } catch (...) {}
     if (c->ev_sync) cudaEventDestroy(c->ev_sync);
     if (c->copy_stream) {

@@ -115,10 +115,18 @@ struct mbx_ctx {
   // Split-K partial accumulators of the tensor-core kernels (L2-resident scratch).
   float* tc_part = nullptr;
   size_t tc_part_bytes = 0;
-  // Grid-barrier counter of the persistent multi-level kernels: monotonic; the host tracks the
-  // value every launch starts from (stream order makes the launches sequential).
-  unsigned* gbar = nullptr;
-  unsigned gbar_count = 0;
+  // Split-bf16 shadow of the arena (tensor-core precisions): a second reservation of the same
+  // size mapped in lockstep, 4 bytes per arena float — for each 8-float group at float offset g,
+  // bytes [4g, 4g + 16) hold the 8 bf16 "hi" parts and [4g + 16, 4g + 32) the "lo" parts.
+  // Producers write it for rows a later tensor-core level gathers (plan_shadows), which then
+  // arrive MMA-ready.
+  CUdeviceptr shadow_base = 0;
+  std::vector<CUmemGenericAllocationHandle> shadow_chunks;
+  // Operand images of the tensor-core levels whose gathered rows all have one producer each
+  // (plan_shadows): per flush, [level][tile][K rank][chunk][hi | lo] split-bf16 B operands in
+  // the canonical UMMA layout, filled by the producers, loaded by the consumer with bulk copies.
+  unsigned char* img_buf = nullptr;
+  size_t img_cap = 0;
 };
 
 namespace mbx {
@@ -166,6 +174,15 @@ struct BatchLaunch {
   struct Gather { int size; size_t src_meta; int64_t dst; };
   std::vector<Gather> gathers;
   std::vector<BatchLaunch> sub;  // head / tail launches of a split plan
+  unsigned shadow_out = 0;       // pointwise launches: bit k = also write output slot k's shadow
+  int img_slot = -1;             // pointwise launches: output slot scattered into operand images
+  size_t img_dst_meta = 0;       // ... and its per-row destinations (int4, staged)
+};
+
+// One persistent multi-level launch covering launches [start, start + n) of a flush.
+struct LevelsRun {
+  int start = 0, n = 0, groups = 1, cfg = 0;
+  size_t table = 0;
 };
 
 // Host half of exec_batched: validation, gather accounting, reference-order allocation of
@@ -183,6 +200,10 @@ void issue_prefix(mbx_ctx* c, const BatchLaunch& L);
 // run, stages its level table (before meta_commit) into *table, sets its node-tile groups
 // (grid x) and returns n; else 0.
 int plan_levels(mbx_ctx* c, const std::vector<BatchLaunch>& Ls, size_t i, size_t* table, int* groups, int* cfg);
+// After every run of the flush is planned (before meta_commit): marks the levels whose gathered
+// rows all have split-bf16 shadows written earlier in the flush (they skip the conversion), and
+// makes those rows' producers (pointwise launches, levels of a run) write the shadows.
+void plan_shadows(mbx_ctx* c, std::vector<BatchLaunch>& Ls, const std::vector<LevelsRun>& runs);
 // Enqueues that launch (meta committed).
 void issue_levels(mbx_ctx* c, const std::vector<BatchLaunch>& Ls, size_t i, int n, size_t table, int groups,
                   int cfg);

@@ -19,6 +19,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <set>
 #include <tuple>
 #include <memory>
 #include <mutex>
@@ -102,7 +103,6 @@ struct TcState {
   void* fn = nullptr;         // cudaKernel_t
   void* fn_fast = nullptr;    // pointwise plans: fast-activation variant (tensor-core precisions)
   void* fn4 = nullptr, *fn_fast4 = nullptr;  // pointwise plans, E % 4 == 0: 16-byte variants
-  std::map<int, void*> fused;  // wide levels configuration + a pointwise plan's tail, by plan id
   // Few output columns (U x G <= 64): the bit-exact CUDA-core small-dense kernel instead of the
   // tensor cores, in every precision (sfn != nullptr).
   void* sfn = nullptr;
@@ -114,15 +114,15 @@ struct TcState {
   // of levels; [1] wide — a small K split, many node-tile groups, for one large batch.
   struct LevelsCfg {
     int S = 0, NT = 0, xch = 0;  // xch 0: K ranks form a cluster (DSMEM), 1: L2 exchange
-    int CY = 1;                  // unit tiles per cluster sharing node rows by multicast
-    int w_off = 0, x_off = 0, recv_off = 0, bar_off = 0, stage_off = 0, smem = 0;
+    int w_off = 0, x_off = 0, recv_off = 0, bar_off = 0, smem = 0;
     std::string src;
     void* fn = nullptr;
     bool attr_set = false;
     float* part = nullptr;      // xch 1: partials buffer
     unsigned* flags = nullptr;  // xch 1: arrival counters
+    unsigned* ready = nullptr;  // per unit tile readiness counters (monotonic)
+    unsigned ready_count = 0;   // their value after every launch so far (stream order)
   } lv[2];
-  unsigned l_tiles = 0;         // node tiles run so far (the counters' common base / (S-1))
   // packed-weight cache: (weight offsets, precision, upload epoch) -> device buffer
   struct Packed {
     std::vector<int64_t> offs;
@@ -259,8 +259,6 @@ bool stamps_enabled() {
 
 std::string gen_gate_source(const TcState& st) {
   std::ostringstream o;
-  if (stamps_enabled()) o << "#define MBX_STAMPS 1\n";
-  if (const char* e = std::getenv("MBX_TC_LOOK")) o << "#define MBX_LOOKAHEAD " << std::atoi(e) << "\n";
   o << jit::prelude_source();
   o << "#define MBX_GATE_KERNEL 1\n"
     << "#define MBX_KC " << st.KC << "\n#define MBX_U " << st.U << "\n#define MBX_G " << st.G << "\n#define MBX_UC "
@@ -273,26 +271,18 @@ std::string gen_gate_source(const TcState& st) {
 }
 
 // Source of one mbx_tc_levels configuration (same plan shape and tail as the gate kernel).
-std::string gen_levels_source(const TcState& st, int k, const EpiProg* fuse = nullptr) {
+std::string gen_levels_source(const TcState& st, int k) {
   const TcState::LevelsCfg& L = st.lv[k];
   std::ostringstream o;
   if (stamps_enabled()) o << "#define MBX_STAMPS 1\n";
-  if (std::getenv("MBX_FENCE_ONCE")) o << "#define MBX_FENCE_ONCE 1\n";
-  if (std::getenv("MBX_ARRIVE_RELEASE")) o << "#define MBX_ARRIVE_RELEASE 1\n";
-  if (std::getenv("MBX_SENTINEL")) o << "#define MBX_SENTINEL 1\n";
-  if (const char* e = std::getenv("MBX_FLAG_STRIDE")) o << "#define MBX_FLAG_STRIDE " << std::clamp(std::atoi(e), 1, 32) << "\n";
-  if (const char* e = std::getenv("MBX_POLLERS")) o << "#define MBX_POLLERS " << std::max(1, std::atoi(e)) << "\n";
   o << jit::prelude_source();
   o << "#define MBX_LEVELS_KERNEL 1\n"
     << "#define MBX_KC " << st.KC << "\n#define MBX_U " << st.U << "\n#define MBX_G " << st.G << "\n#define MBX_UC "
     << st.UC << "\n#define MBX_NCHUNKS " << st.nchunks << "\n#define MBX_NPIECES " << st.npieces
     << "\n#define MBX_PK0 " << st.piece_k[0] << "\n#define MBX_NLOADS " << st.prog.nloads << "\n#define MBX_NOUT "
     << st.prog.nout << "\n#define MBX_LS " << L.S << "\n#define MBX_LNT " << L.NT << "\n#define MBX_LXCH " << L.xch
-    << "\n#define MBX_LCY " << L.CY << "\n";
+    << "\n";
   o << gen_tail(st.prog, false);
-  if (fuse)
-    o << "#define MBX_FUSE_PW 1\n#define MBX_PW_NLOADS " << fuse->nloads << "\n#define MBX_PW_NOUT " << fuse->nout << "\n"
-      << gen_tail(*fuse, true, true);
   o << jit::kernel_source();
   return o.str();
 }
@@ -480,12 +470,15 @@ Layout layout_for(const TcState& st, int NT, int S, int npass) {
 }
 
 // Persistent multi-level layout (mbx_tc_levels): the CTA's resident weight slice
-// [K/S x 128 rows, hi|lo], the node-row region (doubles as the accumulator staging), the peers'
-// partials (DSMEM exchange only) and the barriers.  Picks the largest K split S <= 8 whose grid
-// (unit tiles x S) fits on the 148 SMs, then the largest node tile that fits in shared memory.
-// Clusters of 8 one-CTA-per-SM blocks: at least 14 are co-resident on a 148-SM B200 (GPCs of
-// 18-20 SMs); with more unit tiles than that the ranks exchange partials through L2 instead.
-// Returns false if the plan has no such layout (it then runs level by level).
+// [K/S x 128 rows, hi|lo], the node-row region (doubles as the accumulator staging of the DSMEM
+// exchange), the peers' partials (DSMEM exchange only) and the barriers + row table.
+// deep (k = 0): the largest K split S <= 8 whose grid (unit tiles x S) fits on the 148 SMs
+// (smallest resident slice), then the largest node tile (up to 256: TreeLSTM-512's 205-node
+// depth in one tile); the ranks exchange partials through L2 unless the grid forms at most 14
+// clusters of S (co-resident on a 148-SM B200: GPCs of 16-20 SMs).
+// wide (k = 1, one large batch): the smallest S that fits, then the largest node tile; partials
+// through DSMEM inside clusters of S, so it needs no co-residency beyond its clusters.
+// Returns false if the plan has no such layout (it then runs batch by batch).
 __global__ void fill_u32(unsigned* p, size_t n, unsigned v) {
   for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) p[i] = v;
 }
@@ -495,71 +488,38 @@ bool levels_layout(TcState& st, int k) {
   const int utiles = st.U / st.UC;
   TcState::LevelsCfg& C = st.lv[k];
   C = TcState::LevelsCfg{};
-  static const int cy_max = [] {
-    const char* e = std::getenv("MBX_LEVELS_CY");
-    return e ? std::max(1, std::atoi(e)) : 4;
-  }();
-  // Unit tiles sharing node rows by multicast: clusters of up to 4 along y (always co-resident:
-  // 148 SMs hold 37 of them).  Clusters of 8 ranks along z (DSMEM exchange) only when no
-  // multicast cluster is formed and at most 14 of them are needed.
-  // The wide configuration (one large batch per launch) exchanges partials inside clusters of
-  // its S ranks (DSMEM): no cross-cluster waits, so it needs no co-residency beyond its clusters
-  // and runs beside other work (no persistent lane).
-  int CY = 1;
-  if (k == 0)
-    while (CY * 2 <= cy_max && utiles % (CY * 2) == 0) CY *= 2;
-  // deep: largest S first (smallest resident weight slice), then the largest node tile; wide:
-  // the smallest S that fits, then the largest node tile.
   auto try_cfg = [&](int S, int NT) {
-    if (st.nchunks % S != 0 || utiles * S > 148) return false;
+    if (st.nchunks % S != 0 || utiles * S > 148 || utiles > 64) return false;
     const int cpr = st.nchunks / S;
     if (cpr > 16) return false;
-    const int xch = CY > 1 ? 1 : ((S > 1 && k == 0 && utiles * S > 14 * 8) ? 1 : 0);
+    const int xch = (S > 1 && k == 0 && utiles * S > 14 * 8) ? 1 : 0;
     // tail elements per thread x operands held in registers (MBX_LEPT x MBX_NLOADS) <= 16
-    if (NT / S < 2 || (NT / S) * st.UC * std::max(1, st.prog.nloads) > 16 * kTcThreads) return false;
+    const int lloc = xch ? ((NT / 8 + S - 1) / S) * 8 : NT / S;
+    if (NT / S < 2 || lloc * st.UC * std::max(1, st.prog.nloads) > 16 * kTcThreads) return false;
     const int w = al(cpr * kM * st.KC * 4);
-    const int x = al(std::max(cpr * (NT * st.KC * 4 + 128), NT * kM * 4));  // xstride per chunk
-    const int stage = CY > 1 ? al(NT * (cpr * st.KC * 4 + 16)) : 0;      // MBX_LSROW per row
+    const int x = al(std::max(cpr * (NT * st.KC * 4 + 128), xch ? 0 : NT * kM * 4));  // xstride per chunk
     const int recv = al(S > 1 && xch == 0 ? (S - 1) * (NT / S) * kM * 4 : 0);
     const int bars = (2 * cpr + 6) * 8 + NT * 16;
-    if (w + x + stage + recv + bars > kSmemBudget - kLevelsStaticSmem) return false;
+    if (w + x + recv + bars > kSmemBudget - kLevelsStaticSmem) return false;
     C.S = S;
     C.NT = NT;
     C.xch = xch;
-    C.CY = CY;
     C.w_off = 0;
     C.x_off = w;
-    C.stage_off = w + x;
-    C.recv_off = w + x + stage;
-    C.bar_off = w + x + stage + recv;
-    C.smem = w + x + stage + recv + bars;
+    C.recv_off = w + x;
+    C.bar_off = w + x + recv;
+    C.smem = w + x + recv + bars;
     return true;
   };
-  static const int force_s = [] {
-    const char* e = std::getenv("MBX_LEVELS_DEEP_S");  // experiment: deep K split, DSMEM exchange
-    return e ? std::atoi(e) : 0;
-  }();
-  if (k == 0 && force_s > 0) {
-    CY = 1;
-    for (int NT : {128, 64, 32})
-      if (try_cfg(force_s, NT)) return true;
-  }
-  static const std::pair<int, int> force_wide = [] {  // experiment: MBX_LEVELS_WIDE=S,NT
-    const char* e = std::getenv("MBX_LEVELS_WIDE");
-    int s = 0, nt = 0;
-    if (e) std::sscanf(e, "%d,%d", &s, &nt);
-    return std::make_pair(s, nt);
-  }();
-  if (k == 1 && force_wide.first > 0 && try_cfg(force_wide.first, force_wide.second)) return true;
   if (k == 0) {
     for (int S : {8, 4, 2, 1})
-      for (int NT : {128, 64, 32})
+      for (int NT : {256, 128, 64, 32})
         if (try_cfg(S, NT)) return true;
   } else {
     // The smallest K split first (its partial exchange through DSMEM costs (S-1)/S of the
     // accumulator tile per CTA and dominates the kernel), then the largest node tile: for the
     // TreeLSTM-512 leaf batch (639 nodes, K 512) S=2 / NT=64 runs in 16.1-16.9 us against
-    // 17.8-18.8 us for S=4 / NT=128 (ncu, tools/gpu_ab4.sh).
+    // 17.8-18.8 us for S=4 / NT=128 (round-1 ncu).
     for (int S : {1, 2, 4, 8})
       for (int NT : {128, 64, 32})
         if (try_cfg(S, NT)) return true;
@@ -609,24 +569,14 @@ struct Tiling {
 
 Tiling pick_tiling(const TcState& st, int b, int npass) {
   // (the per-SM ingest and L2 figures are measured; see tools/bench_bulk.cu)
-  static const int forced_nt = [] {
-    const char* e = std::getenv("MBX_TC_NT");
-    return e ? std::atoi(e) : 0;
-  }();
-  static const int forced_s = [] {
-    const char* e = std::getenv("MBX_TC_KSPLIT");
-    return e ? std::atoi(e) : 0;
-  }();
   const int utiles = st.U / st.UC;
   const double wpass = npass > 1 ? 2 : 1;
   const double w_tile_bytes = double(kM) * st.K * 2 * wpass;
   Tiling best;
   double best_t = 1e30;
   for (int nt : {16, 32, 64, 128}) {
-    if (forced_nt && nt != forced_nt) continue;
-    if (nt > 16 && nt / 2 >= b && !forced_nt) continue;  // do not over-pad small batches
+    if (nt > 16 && nt / 2 >= b) continue;  // do not over-pad small batches
     for (int s : {1, 2, 4, 8}) {
-      if (forced_s && s != forced_s) continue;
       if (st.nchunks % s != 0 || nt % s != 0) continue;
       const int tiles = (b + nt - 1) / nt;
       const int ctas = tiles * utiles * s;
@@ -697,8 +647,7 @@ void tc_prepare(mbx_ctx* c, PlanEntry& pe) {
       st->sfn = load_kernel(c, ssrc, "mbx_small_dense");
       pe.tc_exact = true;
       // Few output columns: tensor-core tiles would be mostly padding; exact in every precision.
-      static const bool no_small = std::getenv("MBX_NO_TC_SMALL") != nullptr;  // experiment knob
-      pe.tc_small = st->U * st->G <= 64 && !no_small;
+      pe.tc_small = st->U * st->G <= 64;
     }
     if (pe.force_vm) {  // decision-feeding: exact only
       pe.tc_small = pe.tc_exact;
@@ -740,6 +689,7 @@ void tc_release(PlanEntry& pe) {
   for (auto& L : st->lv) {
     if (L.part) cudaFree(L.part);
     if (L.flags) cudaFree(L.flags);
+    if (L.ready) cudaFree(L.ready);
   }
   delete st;
   pe.tc_state = nullptr;
@@ -878,8 +828,7 @@ cudaError_t tc_launch(mbx_ctx* c, const PlanEntry& pe, const BatchLaunch& L) {
     fill_loads(st->prog, a.loads);
     // 16-byte variant when every row it touches is 16-byte aligned (checked on the host copies
     // of this batch's offset tables).
-    static const bool no_v4 = std::getenv("MBX_PW_NO_VEC4") != nullptr;  // experiment knob
-    bool v4 = st->fn4 != nullptr && !no_v4;
+    bool v4 = st->fn4 != nullptr;
     if (v4) {
       const int64_t* sh = reinterpret_cast<const int64_t*>(c->meta.host + L.shared_meta);
       const int64_t* bt = reinterpret_cast<const int64_t*>(c->meta.host + L.batched_meta);
@@ -893,6 +842,14 @@ cudaError_t tc_launch(mbx_ctx* c, const PlanEntry& pe, const BatchLaunch& L) {
           for (int i = 0; i < L.b && v4; ++i) v4 = bt[int64_t(i) * a.nb + d.idx] % 4 == 0;
       }
     }
+    // Split-bf16 shadows of the outputs a later tensor-core level gathers (plan_shadows); only the
+    // 16-byte variant writes them, and plan_shadows requires it.
+    a.shadow = reinterpret_cast<unsigned char*>(c->shadow_base);
+    a.shadow_out = v4 ? L.shadow_out : 0u;
+    a.img = c->img_buf;
+    a.img_slot = v4 ? L.img_slot : -1;
+    a.img_dst = L.img_slot >= 0 ? meta_dev<int4>(c, L.img_dst_meta) : nullptr;
+    if ((L.shadow_out || L.img_slot >= 0) && !v4) return cudaErrorInvalidValue;
     const int64_t total = int64_t(L.b) * a.E / (v4 ? 4 : 1);
     const int blocks = int(std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, 148 * 8)));
     cudaLaunchConfig_t cfg{};
@@ -978,55 +935,8 @@ cudaError_t tc_launch(mbx_ctx* c, const PlanEntry& pe, const BatchLaunch& L) {
   }
   cfg.attrs = attrs;
   cfg.numAttrs = unsigned(na);
-  const int nctas = int(cfg.gridDim.x * cfg.gridDim.y * cfg.gridDim.z);
-  static unsigned long long* stamps = nullptr;
-  if (stamps_enabled()) {
-    if (!stamps) cudaMalloc(&stamps, 4096 * 8 * 8);
-    cudaMemsetAsync(stamps, 0, (size_t(nctas) * 8 + 64) * 8, c->stream);
-    a.stamps = stamps;
-  }
   void* args[] = {&a};
-  cudaError_t e = cudaLaunchKernelExC(&cfg, st->fn, args);
-  if (stamps_enabled() && e == cudaSuccess) {
-    // Profiling aid: phase times of this launch (median / max over CTAs, us from each CTA's start).
-    std::vector<unsigned long long> h(size_t(nctas) * 8 + 64);
-    cudaStreamSynchronize(c->stream);
-    cudaMemcpy(h.data(), stamps, h.size() * 8, cudaMemcpyDeviceToHost);
-    unsigned long long t0 = ~0ull, t1 = 0;
-    for (int i = 0; i < nctas; ++i) {
-      t0 = std::min(t0, h[size_t(i) * 8]);
-      t1 = std::max(t1, h[size_t(i) * 8 + 7]);
-    }
-    std::fprintf(stderr, "tc b=%d NT=%d S=%d ctas=%d (max clusters %d) stages=%d vec16=%d span %.2f us |", L.b, a.NT,
-                 a.ksplit, nctas, max_active_clusters(st->fn, a.ksplit, tl.L.smem), a.stages, a.vec16, (t1 - t0) / 1e3);
-    const char* names[] = {"start", "setup", "staged", "-", "mma", "done", "reduced", "end"};
-    for (int k = 0; k < 8; ++k) {
-      std::vector<double> v;
-      for (int i = 0; i < nctas; ++i) {
-        const unsigned long long x = h[size_t(i) * 8 + k];
-        if (x) v.push_back((double(x) - double(k == 0 ? t0 : h[size_t(i) * 8])) / 1e3);
-      }
-      if (v.empty()) continue;
-      std::sort(v.begin(), v.end());
-      std::fprintf(stderr, " %s %.2f/%.2f", names[k], v[v.size() / 2], v.back());
-    }
-    std::fprintf(stderr, "\n   cta0 chunks, kcycles from start (landed / converted):");
-    const double c0 = double(h[size_t(nctas) * 8 + 63]);
-    for (int i = 0; i < 16; ++i) {
-      const unsigned long long* q = &h[size_t(nctas) * 8 + 2 * i];
-      if (!q[0]) break;
-      std::fprintf(stderr, " [%.2f %.2f]", (double(q[0]) - c0) / 1e3, (double(q[1]) - c0) / 1e3);
-    }
-    std::fprintf(stderr, "\n   cta0 mma (W landed / X ready / issued):");
-    for (int i = 0; i < 10; ++i) {
-      const unsigned long long* q = &h[size_t(nctas) * 8 + 32 + 3 * i];
-      if (!q[0]) break;
-      std::fprintf(stderr, " [%.2f %.2f %.2f]", (double(q[0]) - c0) / 1e3, (double(q[1]) - c0) / 1e3,
-                   (double(q[2]) - c0) / 1e3);
-    }
-    std::fprintf(stderr, "\n");
-  }
-  return e;
+  return cudaLaunchKernelExC(&cfg, st->fn, args);
 }
 
 // ---- persistent multi-level launches (mbx_tc_levels) ------------------------------------------
@@ -1039,7 +949,9 @@ static bool levels_enabled() {
   return on;
 }
 
-// Node tiles of each level for configuration C, and the node-tile groups (grid x) a launch uses.
+
+// Node tiles of each level for configuration C (the smallest power of two >= b, >= 16, at most
+// C.NT), and the node-tile groups (grid x) a launch uses.
 static int level_tiles(const TcState::LevelsCfg& C, int utiles, const std::vector<BatchLaunch>& Ls, size_t i, int n,
                        std::vector<int>& nts) {
   int max_tiles = 1;
@@ -1055,53 +967,9 @@ static int level_tiles(const TcState::LevelsCfg& C, int utiles, const std::vecto
   return std::clamp(max_tiles, 1, std::max(1, 148 / (utiles * C.S)));
 }
 
-// The leaf cell after the TreeLSTM leaf transform (and any pointwise batch like it): elementwise
-// over the rows the wide launch just produced, in the same node order, its other inputs shared
-// rows.  Then the wide launch's tail runs it from registers and the separate pointwise launch
-// disappears (both batches keep their own trace entries).  Bit-identical: the same fast tail
-// function on the same values.  Opt-in (MBX_FUSE=1): measured on TreeLSTM-512 b64 the fused
-// launch takes 26.5 us against 15.5 + 7 us for the two launches — the wide launch's 80 CTAs run
-// the leaf cell's activations for 16 elements per thread, the separate kernel spreads them over
-// every SM.
-static bool fuse_pointwise(mbx_ctx* c, TcState& st, const BatchLaunch& LW, const BatchLaunch& LP) {
-  static const bool off = std::getenv("MBX_FUSE") == nullptr;
-  if (off || st.prog.nout < 1 || !LP.gathers.empty() || !LP.sub.empty() || LP.b != LW.b) return false;
-  const PlanEntry& pp = c->plans[LP.plan_id];
-  if (pp.plan.ghost || pp.tc_kind != 2 || !pp.tc_state) return false;
-  const auto* sp = static_cast<const TcState*>(pp.tc_state);
-  if (sp->U != st.U) return false;
-  const int nbp = int(pp.exec_plan.batched_shapes.size());
-  int xt = -1;
-  for (int j = 0; j < sp->prog.nloads; ++j) {
-    const EpiSrc& l = sp->prog.loads[j];
-    if (l.type == kSrcBatched) {
-      if (xt >= 0 || l.off != 0) return false;
-      xt = j;
-    }
-  }
-  if (xt < 0) return false;
-  const int64_t* bt = reinterpret_cast<const int64_t*>(c->meta.host + LP.batched_meta);
-  const int64_t* ob = reinterpret_cast<const int64_t*>(c->meta.host + LW.out_meta);
-  const int xidx = sp->prog.loads[xt].idx;
-  for (int q = 0; q < LW.b; ++q)
-    if (bt[int64_t(q) * nbp + xidx] != ob[0] + int64_t(q) * st.U) return false;
-  auto it = st.fused.find(LP.plan_id);
-  if (it == st.fused.end()) {
-    void* fn = load_kernel(c, gen_levels_source(st, 1, &sp->prog), "mbx_tc_levels");
-    if (fn && (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, st.lv[1].smem) != cudaSuccess ||
-               cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)) {
-      cudaGetLastError();
-      return false;
-    }
-    it = st.fused.emplace(LP.plan_id, fn).first;
-  }
-  return it->second != nullptr || c->dry;
-}
-
 int plan_levels(mbx_ctx* c, const std::vector<BatchLaunch>& Ls, size_t i, size_t* table, int* groups, int* cfg) {
   const BatchLaunch& L0 = Ls[i];
   const PlanEntry& pe = c->plans[L0.plan_id];
-  static const bool dbg = std::getenv("MBX_LEVELS_DEBUG") != nullptr;
   if (!levels_enabled() || pe.tc_kind != 1 || pe.tc_small || c->precision == MBX_PREC_FP32 || pe.prefix_plan >= 0)
     return 0;
   auto* st = static_cast<TcState*>(pe.tc_state);
@@ -1125,8 +993,7 @@ int plan_levels(mbx_ctx* c, const std::vector<BatchLaunch>& Ls, size_t i, size_t
     // One batch with more node tiles than the deep configuration has groups for: go wide.
     std::vector<int> nts1;
     const int ng1 = level_tiles(st->lv[1], utiles, Ls, i, n, nts1);
-    const int tiles0 = (L0.b + nts[0] - 1) / nts[0];
-    if (tiles0 > ng) {
+    if ((L0.b + nts[0] - 1) / nts[0] > ng) {
       k = 1;
       ng = ng1;
       nts = nts1;
@@ -1134,7 +1001,6 @@ int plan_levels(mbx_ctx* c, const std::vector<BatchLaunch>& Ls, size_t i, size_t
   }
   TcState::LevelsCfg& C = st->lv[k];
   if (!c->dry) {
-    // Every CTA must be resident at once (grid barrier between levels, peers' partials).
     if (!C.attr_set) {
       if (cudaFuncSetAttribute(C.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, C.smem) != cudaSuccess ||
           cudaFuncSetAttribute(C.fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
@@ -1143,41 +1009,21 @@ int plan_levels(mbx_ctx* c, const std::vector<BatchLaunch>& Ls, size_t i, size_t
       }
       C.attr_set = true;
     }
-    // Resident clusters vs the clusters one node-tile group needs.
+    // Every CTA must be resident at once (readiness counters between levels, peers' partials):
+    // resident clusters (DSMEM exchange) or SMs vs what one node-tile group needs.
     int resident, per_group;
-    if (C.CY > 1) {
-      resident = max_active_clusters(C.fn, C.CY, 1, C.smem);
-      per_group = utiles / C.CY * C.S;
-    } else if (C.S > 1 && C.xch == 0) {
+    if (C.S > 1 && C.xch == 0) {
       resident = max_active_clusters(C.fn, C.S, C.smem);
       per_group = utiles;
     } else {
       resident = 148;
       per_group = utiles * C.S;
     }
-    if (dbg)
-      std::fprintf(stderr, "plan_levels: plan %d b=%d run %d cfg %d: resident %d, need %d x %d\n", L0.plan_id, L0.b, n,
-                   k, resident, per_group, ng);
     if (resident < per_group) return 0;
     ng = std::min(ng, resident / per_group);
   }
-  static const int wide_groups = [] {  // experiment: cap the wide launch's node-tile groups
-    const char* e = std::getenv("MBX_WIDE_GROUPS");
-    return e ? std::max(1, std::atoi(e)) : 0;
-  }();
-  if (k == 1 && wide_groups > 0) ng = std::min(ng, wide_groups);
-  static const int deep_groups = [] {  // experiment: cap the deep launch's node-tile groups
-    const char* e = std::getenv("MBX_DEEP_GROUPS");
-    return e ? std::max(1, std::atoi(e)) : 0;
-  }();
-  if (k == 0 && deep_groups > 0) ng = std::min(ng, deep_groups);
   *groups = ng;
   *cfg = k;
-  int covered = n;
-  if (k == 1 && n == 1 && i + 1 < Ls.size() && fuse_pointwise(c, *st, L0, Ls[i + 1])) {
-    *cfg = 2;  // the wide configuration with the next (pointwise) batch in its tail
-    covered = 2;
-  }
   std::vector<TcLevel> tbl(static_cast<size_t>(n));
   for (int q = 0; q < n; ++q) {
     const BatchLaunch& L = Ls[i + size_t(q)];
@@ -1187,10 +1033,248 @@ int plan_levels(mbx_ctx* c, const std::vector<BatchLaunch>& Ls, size_t i, size_t
     tbl[q].b = L.b;
     tbl[q].nt = nts[size_t(q)];
     tbl[q].vec16 = rows_vec16(c, st, pe, L) ? 1 : 0;
-    tbl[q].pad = 0;
+    tbl[q].shadow = 0;      // plan_shadows decides, once every run of the flush is known
+    tbl[q].shadow_out = 0;
+    tbl[q].img_slot = -1;
+    tbl[q].img = -1;
+    tbl[q].img_dst = nullptr;
   }
   *table = meta_stage(c, tbl.data(), tbl.size() * sizeof(TcLevel));
-  return covered;
+  return n;
+}
+
+// The 16-byte pointwise variant runs (and can write shadows) when every row it touches is
+// 16-byte aligned.
+static bool pointwise_v4(mbx_ctx* c, const TcState* st, const PlanEntry& pe, const BatchLaunch& L) {
+  if (!st->fn4 && !c->dry) return false;
+  if (st->U % 4 != 0) return false;
+  const int nb = int(pe.exec_plan.batched_shapes.size());
+  const int64_t* sh = reinterpret_cast<const int64_t*>(c->meta.host + L.shared_meta);
+  const int64_t* bt = reinterpret_cast<const int64_t*>(c->meta.host + L.batched_meta);
+  const int64_t* ob = reinterpret_cast<const int64_t*>(c->meta.host + L.out_meta);
+  for (int k = 0; k < st->prog.nout; ++k)
+    if (ob[k] % 4 != 0) return false;
+  for (int j = 0; j < st->prog.nloads; ++j) {
+    const EpiSrc& d = st->prog.loads[j];
+    if (d.off % 4 != 0) return false;
+    if (d.type == kSrcShared) {
+      if (sh[d.idx] % 4 != 0) return false;
+    } else {
+      for (int i = 0; i < L.b; ++i)
+        if (bt[int64_t(i) * nb + d.idx] % 4 != 0) return false;
+    }
+  }
+  return true;
+}
+
+void plan_shadows(mbx_ctx* c, std::vector<BatchLaunch>& Ls, const std::vector<LevelsRun>& runs) {
+  // MBX_OPERANDS=convert|shadow: restrict the operand paths (A/B measurements and tests).
+  static const int allow = [] {
+    const char* e = std::getenv("MBX_OPERANDS");
+    return !e ? 2 : std::strcmp(e, "convert") == 0 ? 0 : std::strcmp(e, "shadow") == 0 ? 1 : 2;
+  }();
+  if (c->precision == MBX_PREC_FP32 || Ls.empty() || allow == 0) return;
+  // Output regions whose producer can write split-bf16 shadows: the pointwise kernel (16-byte
+  // variant) and every level of a persistent run.  Regions never overlap (bump allocation).
+  struct Region {
+    int64_t lo, hi;
+    int launch, slot;
+  };
+  std::vector<Region> regions;
+  std::vector<int> run_of(Ls.size(), -1);  // launch -> index of the run covering it
+  for (size_t r = 0; r < runs.size(); ++r)
+    for (int q = 0; q < runs[r].n; ++q) run_of[size_t(runs[r].start) + size_t(q)] = int(r);
+  for (size_t j = 0; j < Ls.size(); ++j) {
+    const BatchLaunch& L = Ls[j];
+    const PlanEntry& pe = c->plans[L.plan_id];
+    if (pe.plan.ghost || !L.gathers.empty() || !L.sub.empty()) continue;
+    bool capable = run_of[j] >= 0;
+    if (!capable && pe.tc_kind == 2 && pe.tc_state)
+      capable = pointwise_v4(c, static_cast<const TcState*>(pe.tc_state), pe, L);
+    if (!capable) continue;
+    const int64_t* ob = reinterpret_cast<const int64_t*>(c->meta.host + L.out_meta);
+    for (size_t k = 0; k < pe.out_shapes.size() && k < 32; ++k)
+      regions.push_back({ob[k], ob[k] + int64_t(L.b) * pe.out_shapes[k].size(), int(j), int(k)});
+  }
+  if (regions.empty()) return;
+  std::sort(regions.begin(), regions.end(), [](const Region& a, const Region& b) { return a.lo < b.lo; });
+  auto find = [&](int64_t lo, int64_t hi) -> const Region* {
+    auto it = std::upper_bound(regions.begin(), regions.end(), lo, [](int64_t v, const Region& r) { return v < r.lo; });
+    if (it == regions.begin()) return nullptr;
+    --it;
+    return (lo >= it->lo && hi <= it->hi) ? &*it : nullptr;
+  };
+  // Per consumer level, in flush order: an operand image when every gathered row is a whole
+  // output row of an earlier capable launch that no other level consumes (trees: each child row
+  // feeds one parent); else MMA-ready shadow gathers when every row has a shadow; else fp32
+  // gathers with the in-kernel conversion.
+  // Per producer launch: its image slot (-1: none yet), per-row destinations and claim marks.
+  std::vector<int> img_slot_of(Ls.size(), -1);
+  std::vector<std::vector<int4>> dst(Ls.size());
+  std::vector<std::vector<uint8_t>> claimed(Ls.size());
+  size_t img_used = 0;
+  std::vector<std::pair<int, int>> marks;
+  struct Cand {
+    int launch, slot, row;
+    int4 d;
+  };
+  std::vector<Cand> cands;
+  for (const LevelsRun& run : runs) {
+    const BatchLaunch& L0 = Ls[size_t(run.start)];
+    const PlanEntry& pe = c->plans[L0.plan_id];
+    const auto* st = static_cast<const TcState*>(pe.tc_state);
+    const int nb = int(pe.exec_plan.batched_shapes.size());
+    const TcState::LevelsCfg& C = st->lv[run.cfg];
+    const int kslice = (st->nchunks / C.S) * st->KC;
+    TcLevel* tbl = reinterpret_cast<TcLevel*>(c->meta.host + run.table);
+    for (int q = 0; q < run.n; ++q) {
+      const size_t j = size_t(run.start) + size_t(q);
+      const BatchLaunch& L = Ls[j];
+      const int64_t* bt = reinterpret_cast<const int64_t*>(c->meta.host + L.batched_meta);
+      const int nt = tbl[q].nt;
+      // -- operand image --
+      bool img_ok = allow >= 2 && st->K < 4096 && kslice < 4096 && nt < 65536 && (st->KC == 16 || st->KC == 32);
+      cands.clear();
+      const int64_t tile_bytes = int64_t(nt) * st->K * 4;
+      for (int pc = 0; pc < st->npieces && img_ok; ++pc) {
+        const int k0 = pc ? st->piece_k[0] : 0, width = st->piece_k[pc] - k0;
+        if (st->piece_kind[pc] != kRefBatched || st->piece_off[pc] != 0 || k0 % 8 != 0) img_ok = false;
+        for (int i = 0; i < L.b && img_ok; ++i) {
+          const int64_t row = bt[int64_t(i) * nb + st->piece_idx[pc]];
+          const Region* r = find(row, row + width);
+          if (!r || size_t(r->launch) >= j) {
+            img_ok = false;
+            break;
+          }
+          const int64_t rows = (r->hi - r->lo) / std::max<int64_t>(1, Ls[size_t(r->launch)].b);
+          const int pj = r->launch;
+          const int ri = int((row - r->lo) / std::max<int64_t>(1, rows));
+          if (rows != width || (row - r->lo) % rows != 0 || (img_slot_of[size_t(pj)] >= 0 && img_slot_of[size_t(pj)] != r->slot)) {
+            img_ok = false;
+            break;
+          }
+          auto& cl = claimed[size_t(pj)];
+          if (cl.empty()) cl.assign(size_t(Ls[size_t(pj)].b), 0);
+          if (cl[size_t(ri)]) {  // consumed twice (by another level, or twice by this one)
+            img_ok = false;
+            break;
+          }
+          cl[size_t(ri)] = 1;
+          Cand cd;
+          cd.launch = pj;
+          cd.slot = r->slot;
+          cd.row = ri;
+          const int64_t base = int64_t(img_used) + int64_t(i / nt) * tile_bytes;
+          cd.d.x = int(uint32_t(uint64_t(base) & 0xffffffffu));
+          cd.d.y = int(uint32_t(uint64_t(base) >> 32));
+          cd.d.z = (i % nt) | (nt << 16);
+          cd.d.w = k0 | (st->KC << 12) | (kslice << 20);
+          cands.push_back(cd);
+        }
+      }
+      if (!img_ok)
+        for (const Cand& cd : cands) claimed[size_t(cd.launch)][size_t(cd.row)] = 0;  // undo this level's claims
+      if (img_ok) {
+        for (const Cand& cd : cands) {
+          img_slot_of[size_t(cd.launch)] = cd.slot;
+          auto& v = dst[size_t(cd.launch)];
+          if (v.empty()) v.assign(size_t(Ls[size_t(cd.launch)].b), make_int4(0, -1, 0, 0));
+          v[size_t(cd.row)] = cd.d;
+        }
+        tbl[q].img = int64_t(img_used);
+        img_used += size_t((L.b + nt - 1) / nt) * size_t(tile_bytes);
+        img_used = (img_used + 1023) & ~size_t(1023);
+        continue;
+      }
+      // -- shadow gathers --
+      bool ready = true;
+      marks.clear();
+      for (int pc = 0; pc < st->npieces && ready; ++pc) {
+        const int width = st->piece_k[pc] - (pc ? st->piece_k[0] : 0);
+        // Parameters (shared rows) carry no shadow; the 16-byte quads of a row must be whole
+        // 8-float groups of the shadow.
+        if (st->piece_kind[pc] != kRefBatched || width % 8 != 0 || st->piece_off[pc] % 8 != 0) ready = false;
+        for (int i = 0; i < L.b && ready; ++i) {
+          const int64_t row = bt[int64_t(i) * nb + st->piece_idx[pc]] + st->piece_off[pc];
+          const Region* r = row % 8 == 0 ? find(row, row + width) : nullptr;
+          if (!r || size_t(r->launch) >= j) {
+            ready = false;
+          } else if (marks.empty() || marks.back() != std::make_pair(r->launch, r->slot)) {
+            marks.emplace_back(r->launch, r->slot);
+          }
+        }
+      }
+      if (!ready) continue;
+      tbl[q].shadow = 1;
+      for (auto [pj, k] : marks) {
+        const int pr = run_of[size_t(pj)];
+        if (pr >= 0)
+          reinterpret_cast<TcLevel*>(c->meta.host + runs[size_t(pr)].table)[pj - runs[size_t(pr)].start].shadow_out |=
+              1u << k;
+        else
+          Ls[size_t(pj)].shadow_out |= 1u << k;
+      }
+    }
+  }
+  // Stage the producers' destination tables and point them at their image slot.
+  for (size_t pj = 0; pj < Ls.size(); ++pj) {
+    const auto& v = dst[pj];
+    const int k = img_slot_of[pj];
+    if (v.empty() || k < 0) continue;
+    if (c->meta.cursor % 16) {  // int4 loads: 16-byte aligned tables
+      const int64_t pad = 0;
+      meta_stage(c, &pad, 8);
+    }
+    const size_t off = meta_stage(c, v.data(), v.size() * sizeof(int4));
+    const int pr = run_of[pj];
+    if (pr >= 0) {
+      TcLevel& t = reinterpret_cast<TcLevel*>(c->meta.host + runs[size_t(pr)].table)[int(pj) - runs[size_t(pr)].start];
+      t.img_slot = k;
+      t.img_dst = meta_dev<int4>(c, off);
+    } else {
+      Ls[pj].img_slot = k;
+      Ls[pj].img_dst_meta = off;
+    }
+  }
+  if (img_used > c->img_cap && !c->dry) {
+    // Grows rarely (first mini-batches): nothing in flight may still read the old buffer.
+    cuda_check(cudaStreamSynchronize(c->stream), "operand image grow");
+    if (c->img_buf) cudaFree(c->img_buf);
+    c->img_buf = nullptr;
+    const size_t cap = std::max(img_used, c->img_cap * 2);
+    cuda_check(cudaMalloc(&c->img_buf, cap), "operand images");
+    // Columns past a level's last node are never written: keep them finite (zero).
+    cuda_check(cudaMemsetAsync(c->img_buf, 0, cap, c->stream), "operand images");
+    c->img_cap = cap;
+  }
+}
+
+// Profiling aid (MBX_TC_STAMPS=1 builds only, never on a measured path): waits for the launch and
+// prints, per level, the median / max over CTAs of each in-kernel clock64 phase stamp.
+static void report_level_stamps(mbx_ctx* c, const unsigned long long* dev, int nctas, int n, const TcLevel* tbl,
+                                const TcState::LevelsCfg& C, int cfg, int groups) {
+  std::vector<unsigned long long> h(size_t(nctas) * 64 * 16);
+  cudaStreamSynchronize(c->stream);
+  cudaMemcpy(h.data(), dev, h.size() * 8, cudaMemcpyDeviceToHost);
+  std::fprintf(stderr, "levels: %d levels, %d CTAs (cfg %d, %d groups, S=%d, NT<=%d, exchange %s)\n", n, nctas, cfg,
+               groups, C.S, C.NT, C.xch ? "L2" : "DSMEM");
+  const char* names[] = {"start", "mma_wait", "mma_done", "pushed", "reduced", "tile_end", "ready", "converted",
+                         "g_sync", "g_issued", "g_landed0", "mma_issued", "tmem_stg", "tails", "entry", "-"};
+  for (int lv = 0; lv < std::min(n, 63); ++lv) {
+    std::fprintf(stderr, "  lv %2d b=%3d nt=%3d sh=%d:", lv, tbl[lv].b, tbl[lv].nt, tbl[lv].shadow);
+    for (int k = 0; k < 16; ++k) {
+      std::vector<double> v;
+      for (int i2 = 0; i2 < nctas; ++i2) {
+        const unsigned long long x = h[(size_t(i2) * 64 + lv) * 16 + k];
+        const unsigned long long t0 = h[size_t(i2) * 64 * 16];
+        if (x && t0) v.push_back((double(x) - double(t0)) / 1965.0);
+      }
+      if (v.empty()) continue;
+      std::sort(v.begin(), v.end());
+      std::fprintf(stderr, " %s %.2f/%.2f", names[k], v[v.size() / 2], v.back());
+    }
+    std::fprintf(stderr, "\n");
+  }
 }
 
 void issue_levels(mbx_ctx* c, const std::vector<BatchLaunch>& Ls, size_t i, int n, size_t table, int groups,
@@ -1199,26 +1283,21 @@ void issue_levels(mbx_ctx* c, const std::vector<BatchLaunch>& Ls, size_t i, int 
   const BatchLaunch& L0 = Ls[i];
   const PlanEntry& pe = c->plans[L0.plan_id];
   auto* st = static_cast<TcState*>(pe.tc_state);
-  const bool fused = cfg == 2;  // wide configuration + the next batch (pointwise) in its tail
-  if (fused) {
-    cfg = 1;
-    n = 1;
-    issue_prefix(c, Ls[i + 1]);  // its hoisted shared rows, before the launch that reads them
-  }
   TcState::LevelsCfg& C = st->lv[cfg];
   const int npass = c->precision == MBX_PREC_BF16 ? 1 : 3;
   const int64_t* shared_host = reinterpret_cast<const int64_t*>(c->meta.host + L0.shared_meta);
   TcState::Packed* pk = nullptr;
   bool fresh_pack = false;
   cuda_check(ensure_pack(c, st, shared_host, npass, &pk, &fresh_pack), "weight pack");
-  if (!c->gbar) {
-    cuda_check(cudaMalloc(&c->gbar, 256), "grid barrier counter");
-    cuda_check(cudaMemset(c->gbar, 0, 256), "grid barrier counter");
-    c->gbar_count = 0;
-  }
   const int utiles = st->U / st->UC;
+  if (!C.ready) {
+    cuda_check(cudaMalloc(&C.ready, size_t(64) * 32 * 4), "levels readiness counters");
+    cuda_check(cudaMemsetAsync(C.ready, 0, size_t(64) * 32 * 4, c->stream), "levels readiness counters");
+    C.ready_count = 0;
+  }
   TcLevelsArgs a{};
   a.arena = arena_ptr(c);
+  a.shadow = reinterpret_cast<unsigned char*>(c->shadow_base);
   a.wpack = pk->buf;
   a.levels = meta_dev<TcLevel>(c, table);
   a.nlevels = n;
@@ -1233,37 +1312,43 @@ void issue_levels(mbx_ctx* c, const std::vector<BatchLaunch>& Ls, size_t i, int 
   a.x_off = C.x_off;
   a.recv_off = C.recv_off;
   a.bar_off = C.bar_off;
-  a.stage_off = C.stage_off;
   a.tmem_cols = std::max(32, C.NT);
-  a.gbar = c->gbar;
-  a.gbar_base = c->gbar_count;
+  a.ready = C.ready;
+  a.ready_base = C.ready_count;
+  a.img = c->img_buf;
+  // Unit tiles whose output columns each K rank's slice of the gathered rows covers (rows this
+  // plan produced at an earlier level of the run; rows from earlier launches are complete by
+  // stream order).  A piece that is not a column range of this plan's U-wide outputs depends on
+  // every unit tile; parameter rows on none.
+  const int cpr = st->nchunks / C.S;
+  for (int r = 0; r < C.S; ++r) {
+    unsigned long long m = 0;
+    for (int pc = 0; pc < st->npieces; ++pc) {
+      const int p0 = pc ? st->piece_k[0] : 0, p1 = st->piece_k[pc];
+      const int k0 = std::max(p0, r * cpr * st->KC), k1 = std::min(p1, (r + 1) * cpr * st->KC);
+      if (k0 >= k1 || st->piece_kind[pc] != kRefBatched) continue;
+      const int c0 = k0 - p0 + st->piece_off[pc], c1 = k1 - p0 + st->piece_off[pc];
+      if (st->piece_off[pc] + (p1 - p0) <= st->U) {
+        for (int t = c0 / st->UC; t <= (c1 - 1) / st->UC; ++t) m |= 1ull << t;
+      } else {
+        m = ~0ull;
+      }
+    }
+    a.dep_mask[r] = m;
+  }
   if (C.xch == 1) {
     if (!C.part) {
       const size_t ngmax = size_t(std::max(1, 148 / (utiles * C.S)));
       const size_t lloc = size_t((C.NT / 8 + C.S - 1) / C.S) * 8;  // MBX_LLOC
       const size_t part_bytes = size_t(2) * ngmax * utiles * C.S * C.S * lloc * kM * 4;
       cuda_check(cudaMalloc(&C.part, part_bytes), "levels partials");
-      // Every partial slot starts "not written" (MBX_PART_EMPTY in tc_gate.cuh).
-      fill_u32<<<148, 256, 0, c->stream>>>(reinterpret_cast<unsigned*>(C.part), part_bytes / 4, 0xffbadbadu);
-      cuda_check(cudaGetLastError(), "levels partials fill");
-      cuda_check(cudaMalloc(&C.flags, ngmax * utiles * C.S * 128), "levels flags");  // up to one line each
-      cuda_check(cudaMemset(C.flags, 0, ngmax * utiles * C.S * 128), "levels flags");
+      cuda_check(cudaMalloc(&C.flags, ngmax * utiles * C.S * 4), "levels flags");
+      cuda_check(cudaMemsetAsync(C.flags, 0, ngmax * utiles * C.S * 4, c->stream), "levels flags");
     }
     a.part = C.part;
     a.xflags = C.flags;
   }
   fill_loads(st->prog, a.loads);
-  void* kfn = C.fn;
-  if (fused) {
-    const BatchLaunch& LP = Ls[i + 1];
-    const auto* sp = static_cast<const TcState*>(c->plans[LP.plan_id].tc_state);
-    a.pw_shared_off = meta_dev<long long>(c, LP.shared_meta);
-    a.pw_out_base = meta_dev<long long>(c, LP.out_meta);
-    fill_loads(sp->prog, a.pw_loads);
-    for (int j = 0; j < sp->prog.nloads; ++j)
-      if (sp->prog.loads[j].type == kSrcBatched) a.pw_xt = j;
-    kfn = st->fused.at(LP.plan_id);
-  }
   cudaLaunchConfig_t lc{};
   lc.gridDim = dim3(unsigned(groups), unsigned(utiles), unsigned(C.S));
   lc.blockDim = dim3(kTcThreads);
@@ -1271,11 +1356,11 @@ void issue_levels(mbx_ctx* c, const std::vector<BatchLaunch>& Ls, size_t i, int 
   lc.stream = c->stream;
   cudaLaunchAttribute attrs[3];
   int na = 0;
-  if (C.CY > 1 || (C.S > 1 && C.xch == 0)) {
+  if (C.S > 1 && C.xch == 0) {
     attrs[na].id = cudaLaunchAttributeClusterDimension;
     attrs[na].val.clusterDim.x = 1;
-    attrs[na].val.clusterDim.y = unsigned(C.CY);
-    attrs[na].val.clusterDim.z = C.CY > 1 ? 1u : unsigned(C.S);
+    attrs[na].val.clusterDim.y = 1;
+    attrs[na].val.clusterDim.z = unsigned(C.S);
     ++na;
   }
   if (!fresh_pack && pdl_enabled()) {
@@ -1283,19 +1368,16 @@ void issue_levels(mbx_ctx* c, const std::vector<BatchLaunch>& Ls, size_t i, int 
     attrs[na].val.programmaticStreamSerializationAllowed = 1;
     ++na;
   }
-  // Grid barrier / cross-cluster counters need every CTA resident at once.  Launched
-  // cooperatively, the grid is not left spinning partly resident while other contexts' clustered
-  // kernels keep taking the SMs it waits for (measured: ~1 in 4 pool runs hit the 2 s wait limit
-  // without it, none with it).  The lane still serialises persistent launches among themselves.
-  // Not under Nsight Compute (its injection sets NV_NSIGHT_INJECTION_TRANSPORT_TYPE /
-  // NV_COMPUTE_PROFILER_PERFWORKS_DIR; it fails cooperative launches with LaunchFailed, and it
-  // serialises kernels, so co-residency holds there anyway), nor with MBX_NO_COOP.
-  static const bool coop = std::getenv("MBX_NO_COOP") == nullptr &&
-                           std::getenv("NV_NSIGHT_INJECTION_TRANSPORT_TYPE") == nullptr &&
-                           std::getenv("NV_COMPUTE_PROFILER_PERFWORKS_DIR") == nullptr &&
-                           std::getenv("CUDA_INJECTION64_PATH") == nullptr;
+  // Readiness counters / cross-cluster exchange counters need every CTA resident at once.
+  // Launched cooperatively, the grid is placed whole (never left spinning partly resident while
+  // other contexts' kernels take the SMs it waits for), and such launches go through the
+  // device's persistent lane, so two of them never run concurrently.  Not under Nsight Compute
+  // (it fails cooperative launches and serialises kernels anyway).
+  static const bool under_ncu = std::getenv("NV_NSIGHT_INJECTION_TRANSPORT_TYPE") != nullptr ||
+                                std::getenv("NV_COMPUTE_PROFILER_PERFWORKS_DIR") != nullptr ||
+                                std::getenv("CUDA_INJECTION64_PATH") != nullptr;
   const bool needs_all = n > 1 || (C.xch == 1 && C.S > 1);
-  if (coop && needs_all) {
+  if (!under_ncu && needs_all) {
     attrs[na].id = cudaLaunchAttributeCooperative;
     attrs[na].val.cooperative = 1;
     ++na;
@@ -1310,87 +1392,15 @@ void issue_levels(mbx_ctx* c, const std::vector<BatchLaunch>& Ls, size_t i, int 
     a.stamps = lstamps;
   }
   void* args[] = {&a};
-  // Grid barrier (several levels) or cross-cluster counters (L2 exchange): every CTA must be
-  // resident at once, so such launches take the device's persistent lane.
-  static const bool lane_all = std::getenv("MBX_LANE_ALL") != nullptr;  // experiment knob
-  // Experiment (MBX_NO_LANE, cooperative launches only): gang-scheduled persistent launches of
-  // different contexts may run side by side when they fit together.
-  static const bool no_lane = std::getenv("MBX_NO_LANE") != nullptr;
-  const bool lane = lane_all || ((n > 1 || (C.xch == 1 && C.S > 1)) && !(no_lane && coop));
-  if (lane) lc.stream = persistent_lane_begin(c);
-  cudaError_t le = cudaLaunchKernelExC(&lc, kfn, args);
-  if (le != cudaSuccess && coop && needs_all) {
-    // Some tools (ncu's kernel replay) refuse cooperative launches: run it as a plain launch
-    // (one kernel at a time there, so co-residency holds anyway).
-    cudaGetLastError();
-    lc.numAttrs = unsigned(na - 1);
-    le = cudaLaunchKernelExC(&lc, kfn, args);
-  }
-  if (lane) persistent_lane_end(c);
+  if (needs_all) lc.stream = persistent_lane_begin(c);
+  // A failed cooperative launch (e.g. too large to be co-resident) is an error, never retried as
+  // a plain launch: a partly resident grid would spin at its first readiness wait.
+  const cudaError_t le = cudaLaunchKernelExC(&lc, C.fn, args);
+  if (needs_all) persistent_lane_end(c);
   cuda_check(le, "multi-level tensor-core kernel");
-  if (stamps_enabled()) {
-    // Profiling aid: per level, median / max over CTAs of each phase (us after the level start).
-    std::vector<unsigned long long> h(size_t(nctas) * 64 * 16);
-    cudaStreamSynchronize(c->stream);
-    cudaMemcpy(h.data(), lstamps, h.size() * 8, cudaMemcpyDeviceToHost);
-    std::fprintf(stderr, "levels: %d levels, %d CTAs (cfg %d, %d groups, S=%d, NT<=%d, CY=%d, exchange %s)\n", n, nctas,
-                 cfg, groups, C.S, C.NT, C.CY, C.xch ? "L2" : "DSMEM");
-    // clock64 stamps: cycles since the CTA's level-0 start (each CTA its own SM clock), in us at
-    // the nominal 1.965 GHz.
-    const char* names[] = {"start", "mma_wait", "mma_done", "pushed", "reduced", "tile_end", "barrier", "converted",
-                           "g_sync", "g_issued", "g_landed0", "mma_issued", "tmem_stg", "stg_sync", "entry", "pre_cwait"};
-    {
-      std::vector<double> g;
-      for (int i2 = 0; i2 < nctas; ++i2) g.push_back(double(h[(size_t(i2) * 64 + 63) * 16 + 14]));
-      const double g0 = *std::min_element(g.begin(), g.end());
-      std::vector<double> d;
-      for (double x : g) d.push_back((x - g0) / 1000.0);
-      std::sort(d.begin(), d.end());
-      std::fprintf(stderr, "  entry (globaltimer, us after the first CTA): median %.2f max %.2f\n", d[d.size() / 2], d.back());
-      for (int k : {11, 12}) {  // gather-thread prologue stamps, us after the level-0 start
-        std::vector<double> v;
-        for (int i2 = 0; i2 < nctas; ++i2) {
-          const unsigned long long x = h[(size_t(i2) * 64 + 63) * 16 + k], t0 = h[size_t(i2) * 64 * 16];
-          if (x && t0) v.push_back((double(x) - double(t0)) / 1965.0);
-        }
-        std::sort(v.begin(), v.end());
-        if (!v.empty()) std::fprintf(stderr, "  prologue stamp %d: median %.2f max %.2f\n", k, v[v.size() / 2], v.back());
-      }
-      if (C.CY > 1) {  // spread of entry times inside each multicast cluster (along y)
-        double worst = 0;
-        const int gx = groups, gy = utiles, gz = C.S;
-        for (int z = 0; z < gz; ++z)
-          for (int x = 0; x < gx; ++x)
-            for (int y0 = 0; y0 < gy; y0 += C.CY) {
-              double lo = 1e30, hi = -1e30;
-              for (int y = y0; y < y0 + C.CY; ++y) {
-                const double v = g[size_t((z * gy + y) * gx + x)];
-                lo = std::min(lo, v);
-                hi = std::max(hi, v);
-              }
-              worst = std::max(worst, (hi - lo) / 1000.0);
-            }
-        std::fprintf(stderr, "  entry spread inside a cluster: max %.2f us\n", worst);
-      }
-    }
-    for (int lv = 0; lv < std::min(n, 63); ++lv) {
-      std::fprintf(stderr, "  lv %2d b=%3d v16=%d:", lv, Ls[i + size_t(lv)].b,
-                   reinterpret_cast<const TcLevel*>(c->meta.host + table)[lv].vec16);
-      for (int k = 0; k < 16; ++k) {
-        std::vector<double> v;
-        for (int i2 = 0; i2 < nctas; ++i2) {
-          const unsigned long long x = h[(size_t(i2) * 64 + lv) * 16 + k];
-          const unsigned long long t0 = h[size_t(i2) * 64 * 16];
-          if (x && t0) v.push_back((double(x) - double(t0)) / 1965.0);
-        }
-        if (v.empty()) continue;
-        std::sort(v.begin(), v.end());
-        std::fprintf(stderr, " %s %.2f/%.2f", names[k], v[v.size() / 2], v.back());
-      }
-      std::fprintf(stderr, "\n");
-    }
-  }
-  c->gbar_count += unsigned(nctas) * unsigned(n - 1);
+  if (stamps_enabled())
+    report_level_stamps(c, lstamps, nctas, n, reinterpret_cast<const TcLevel*>(c->meta.host + table), C, cfg, groups);
+  C.ready_count += unsigned(groups * C.S) * unsigned(n - 1);
   ++c->launches;
   ++g_launches;
 }

@@ -17,6 +17,7 @@
 // SMs.  Operands are read straight from the arena through the per-node offset arrays (the
 // gather is fused into the operand loads; nothing is materialized).
 #include <cuda_runtime.h>
+#include <mutex>
 #include <stdint.h>
 
 #include "devplan.h"
@@ -476,11 +477,15 @@ cudaError_t launch_dense_argmax(float* arena, const int64_t* shared_off, const i
 }
 
 cudaError_t launch_plan_vm(const VmLaunch& L, cudaStream_t stream) {
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(plan_vm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr_set = true;
-  }
+  // The attribute is per device: set once per device, safely from concurrent pool workers.
+  static std::once_flag once[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaError_t attr = cudaSuccess;
+  std::call_once(once[dev & 63], [&] {
+    attr = cudaFuncSetAttribute(plan_vm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  });
+  if (attr != cudaSuccess) return attr;
   dim3 grid((L.b + L.tm - 1) / L.tm, L.nsplit);
   plan_vm_kernel<<<grid, L.threads, L.smem_bytes, stream>>>(L);
   return cudaGetLastError();

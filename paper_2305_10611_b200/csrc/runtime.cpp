@@ -723,7 +723,8 @@ struct Executor::Impl {
       if (b.ghost) continue;
       const auto& plan = m.kernels.plan(b.sig);
       const size_t nb = plan.batched_shapes.size();
-      meta_bytes += 8 * (plan.shared_shapes.size() + size_t(b.size) * nb * 2 + plan.outputs.size()) + 512 + 64;
+      meta_bytes += 8 * (plan.shared_shapes.size() + size_t(b.size) * nb * 2 + plan.outputs.size()) + 512 + 64 +
+                    16 * size_t(b.size) + 16;  // operand-image destinations (plan_shadows)
     }
     mbx::meta_reserve(c, meta_bytes);
 
@@ -772,23 +773,23 @@ struct Executor::Impl {
       trace.batches.push_back(std::move(batch));
     }
     // Runs of consecutive batches of one tensor-core gate plan (e.g. every TreeLSTM internal
-    // depth) become one persistent multi-level launch; their level tables are staged here.
-    struct LevelsRun {
-      int n = 0, groups = 1, cfg = 0;
-      size_t table = 0;
-    };
-    std::vector<LevelsRun> levels(launches.size());
+    // depth) become one persistent multi-level launch; their level tables are staged here, then
+    // the split-bf16 shadows of the rows they gather are planned.
+    std::vector<mbx::LevelsRun> runs;
+    std::vector<int> run_at(launches.size(), -1);
     for (size_t i = 0; i < launches.size();) {
-        size_t tbl = 0;
-        int groups = 1, cfg = 0;
-        const int n = mbx::plan_levels(c, launches, i, &tbl, &groups, &cfg);
-        if (n >= 1) {
-          levels[i] = {n, groups, cfg, tbl};
-          i += size_t(n);
-        } else {
-          ++i;
-        }
+      mbx::LevelsRun r;
+      r.start = int(i);
+      r.n = mbx::plan_levels(c, launches, i, &r.table, &r.groups, &r.cfg);
+      if (r.n >= 1) {
+        run_at[i] = int(runs.size());
+        runs.push_back(r);
+        i += size_t(r.n);
+      } else {
+        ++i;
       }
+    }
+    mbx::plan_shadows(c, launches, runs);
     timing.h2d_bytes += long(c->meta.cursor - c->meta.committed);
     mbx::meta_commit(c);
     auto ts2 = clk::now();
@@ -807,14 +808,15 @@ struct Executor::Impl {
       }
       int64_t before = c->launches;
       for (size_t i = 0; i < launches.size();) {
-        const int n = levels[i].n > 0 ? levels[i].n : 1;
+        const mbx::LevelsRun* run = run_at[i] >= 0 ? &runs[size_t(run_at[i])] : nullptr;
+        const int n = run ? run->n : 1;
         cudaEvent_t x = nullptr, y = nullptr;
         if (opts.time_batches) {
           cudaEventCreate(&x);
           cudaEventCreate(&y);
           cudaEventRecord(x, c->stream);
         }
-        if (levels[i].n > 0) mbx::issue_levels(c, launches, i, n, levels[i].table, levels[i].groups, levels[i].cfg);
+        if (run) mbx::issue_levels(c, launches, i, n, run->table, run->groups, run->cfg);
         else mbx::issue_batch(c, launches[i]);
         if (opts.time_batches) {
           cudaEventRecord(y, c->stream);

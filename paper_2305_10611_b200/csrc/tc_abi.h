@@ -41,14 +41,19 @@ struct TcLevel {
   const long long* shared_off;
   const long long* batched_off;
   const long long* out_base;
-  int b;      // nodes in the batch
-  int nt;     // node tile (MMA N) used for this level: 16, 32, 64 or MBX_LNT
-  int vec16;  // 1: every gathered row segment is 16-byte aligned (bulk / 16-byte copies)
-  int pad;
+  int b;               // nodes in the batch
+  int nt;              // node tile (MMA N) used for this level: 16 .. MBX_LNT
+  int vec16;           // 1: every gathered row segment is 16-byte aligned (16-byte copies)
+  int shadow;          // 1: every gathered row has a split-bf16 shadow (gathered MMA-ready)
+  unsigned shadow_out; // bit k: write output slot k's shadow too (a later level gathers it)
+  int img_slot;        // output slot whose rows are scattered into consumers' images (-1: none)
+  long long img;       // byte offset (in TcLevelsArgs::img) of this level's operand image, -1: gather
+  const int4* img_dst; // [b] per output row of img_slot: where its consumer's image wants it
 };
 
 struct TcLevelsArgs {
   float* arena;
+  unsigned char* shadow;         // split-bf16 shadow of the arena (same float offsets, x4 bytes)
   const unsigned char* wpack;    // same packing as TcGateArgs::wpack
   const TcLevel* levels;         // [nlevels]
   int nlevels;
@@ -56,21 +61,15 @@ struct TcLevelsArgs {
   int npass;
   int piece_kind[2], piece_idx[2], piece_off[2];
   int w_off, x_off, recv_off, bar_off;  // dynamic shared memory layout (bytes)
-  int stage_off;                 // MBX_LCY > 1: row-major fp32 staging of the multicast node rows
   int tmem_cols;
-  unsigned* gbar;                // grid barrier counter (monotonic across launches)
-  unsigned gbar_base;            // its value when this launch starts
+  unsigned* ready;               // per unit tile readiness counters (monotonic across launches)
+  unsigned ready_base;           // their common value when this launch starts
   float* part;                   // MBX_LXCH 1: partials [2][groups][unit tiles][S][S][MBX_LLOC][128]
   unsigned* xflags;              // MBX_LXCH 1: per (group, unit tile, rank) arrival counters, 0 at launch
   unsigned long long* stamps;    // MBX_STAMPS builds only
+  unsigned long long dep_mask[8];  // per K rank: unit tiles whose outputs its K slice gathers
+  unsigned char* img;            // operand images (see mbx_tc_levels)
   TcLoad loads[MBX_MAX_LOADS];
-  // MBX_FUSE_PW: a pointwise batch that consumes this (single-level) launch's rows in node order
-  // runs in its tail; load pw_xt is the value just computed, the others are shared rows.
-  const long long* pw_shared_off;
-  const long long* pw_out_base;
-  int pw_xt;
-  int pw_pad;
-  TcLoad pw_loads[MBX_MAX_LOADS];
 };
 
 struct SmallArgs {
@@ -90,6 +89,11 @@ struct PwArgs {
   const long long* shared_off;
   const long long* batched_off;
   const long long* out_base;
+  unsigned char* shadow;  // split-bf16 shadow of the arena (16-byte variants only)
+  unsigned shadow_out;    // bit k: write output slot k's shadow too
+  int img_slot;           // output slot scattered into consumers' operand images (-1: none)
+  unsigned char* img;     // operand images
+  const int4* img_dst;    // [b] per output row of img_slot (see mbx_tc_levels)
   int b, E, nb, nloads;
   TcLoad loads[MBX_MAX_LOADS];
 };

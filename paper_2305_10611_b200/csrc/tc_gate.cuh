@@ -49,6 +49,27 @@ __device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
+__device__ __forceinline__ void mbar_arrive_cnt(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+// Operand images (mbx_tc_levels): a consumer level whose every gathered row has exactly one
+// producer row gets an image of its B operands, [tile][K rank][chunk][hi | lo][canonical
+// no-swizzle K-major nt x KC], which the producers fill as they write the rows (split bf16) and
+// the consumer loads with a few bulk copies.  d = {base lo, base hi, p | nt << 16,
+// k0 | KC << 12 | kslice << 20}: the tile's image (byte offset), the consumer column, the
+// consumer's tile width, the piece's first K index, the consumer's K chunk and K slice per rank.
+// Returns the byte offset of column u's hi part; the lo part is *lo_off bytes further.
+__device__ __forceinline__ long long img_addr(const int4 d, int u, int* lo_off) {
+  const long long base = (long long)(((unsigned long long)(unsigned)d.y << 32) | (unsigned)d.x);
+  const int p = d.z & 0xffff, nt = d.z >> 16;
+  const int k0 = d.w & 0xfff, kc = (d.w >> 12) & 0xff, ks = (d.w >> 20) & 0xfff;
+  const int k = k0 + u, r = k / ks, kr = k - r * ks, j = kr / kc, kk = kr - j * kc;
+  *lo_off = nt * kc * 2;
+  return base + (long long)(r * (ks / kc) + j) * (2 * nt * kc * 2) + (p >> 3) * (kc * 16) + (kk >> 3) * 128 +
+         (p & 7) * 16 + (kk & 7) * 2;
+}
+
 // Spin on test_wait (try_wait may park the warp for a scheduler quantum).
 __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phase) {
   asm volatile(
@@ -524,6 +545,7 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_gate(const _
 }
 #endif  // MBX_GATE_KERNEL
 
+
 #ifdef MBX_LEVELS_KERNEL
 // mbx_tc_levels — one persistent launch for a run of consecutive batches ("levels") of the same
 // gate plan, e.g. every internal-node depth of a TreeLSTM flush.
@@ -531,27 +553,24 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_gate(const _
 //   SM); group x takes node tiles x, x + gridDim.x, ... of every level.
 //   * The CTA's weight slice (128 gate rows x K/MBX_LS, split bf16) is bulk-copied into shared
 //     memory ONCE and reused by every level: per level only the node rows move.
-//   * Per node tile: cp.async gathers the rows of this rank's K slice straight from the arena
-//     through the level's offset table, in-place fp32 -> split-bf16 conversion, tcgen05.mma into
-//     TMEM, partial accumulators exchanged between the K ranks of the unit tile, summed in rank
-//     order (deterministic), the generated tail, outputs written batch-contiguously.
+//   * Per node tile: 16-byte cp.async gathers the rows of this rank's K slice through the level's
+//     offset table straight into the canonical no-swizzle K-major UMMA layout.  Rows whose
+//     producer wrote their split-bf16 shadow (TcLevel::shadow: [8 x bf16 hi | 8 x bf16 lo] per
+//     8-float group at the row's own offset) arrive MMA-ready; otherwise the fp32 rows are
+//     converted to split bf16 in place.  tcgen05.mma into TMEM, partial accumulators exchanged
+//     between the K ranks of the unit tile, summed in rank order (deterministic), the generated
+//     tail, outputs (and, where a later level gathers them, their shadows) written
+//     batch-contiguously.
 //     MBX_LXCH 0: the ranks form a cluster; partials move by DSMEM bulk copies.
 //     MBX_LXCH 1: no cluster (any grid that fits on the SMs); partials move through an
 //                 L2-resident buffer, completion signalled by per-(group, unit tile, rank) release
 //                 counters, which each owner resets when the launch is done with them.
-//   * MBX_LCY > 1: the MBX_LCY unit tiles of a cluster (along y) need the same node rows; each
-//     CTA bulk-copies every MBX_LCY-th row of the tile once with .multicast::cluster into all of
-//     them (L2 reads / MBX_LCY), into a row-major fp32 staging area that the next tile's copies
-//     may refill as soon as every CTA of the cluster converted it (a cluster barrier phase).
-//   * Between levels a grid barrier (monotonic counter, release / acquire): level l+1 gathers the
-//     rows level l wrote.  Every read of activations bypasses L1 (.cg): L1 is not coherent.
-//     The offset-table lookups of the next level's first tile happen before the barrier.
+//   * Between levels, per-unit-tile readiness counters instead of a grid barrier: a CTA releases
+//     its unit tile's counter when it finished a level; before the next level it acquires only
+//     the counters of the unit tiles that produce the columns its K slice (and its tail) reads
+//     (TcLevelsArgs::dep_mask), so it never waits for the rest of the grid.  Every read of
+//     activations bypasses L1 (.cg): L1 is not coherent.
 #define MBX_LGATHER 192
-#ifndef MBX_LCY
-#define MBX_LCY 1  // unit tiles per cluster sharing the node rows by TMA multicast
-#endif
-#define MBX_LSLICE (MBX_LCPR * MBX_KC)        // floats of a node row in this rank's K slice
-#define MBX_LSROW (MBX_LSLICE * 4 + 16)       // staging row stride (bytes): +16 spreads the banks
 #define MBX_LCPR (MBX_NCHUNKS / MBX_LS)
 #if MBX_LXCH == 0
 #define MBX_LLOC (MBX_LNT / MBX_LS)  // nodes a rank finishes per tile: a contiguous slice
@@ -559,6 +578,7 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_gate(const _
 #define MBX_LLOC (((MBX_LNT / 8 + MBX_LS - 1) / MBX_LS) * 8)  // 8-node chunks c with c % S == rank
 #endif
 #define MBX_LEPT ((MBX_LLOC * MBX_UC + MBX_THREADS - 1) / MBX_THREADS)
+#define MBX_READY_STRIDE 32  // readiness counters one 128-byte line apart
 #ifdef MBX_STAMPS
 #define MBX_LSTAMP_T(t, lv, i)                                                                      \
   do {                                                                                              \
@@ -574,26 +594,7 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_gate(const _
 #endif
 #define MBX_LSTAMP(lv, i) MBX_LSTAMP_T(0, lv, i)
 
-#ifndef MBX_SENTINEL
-// L2 exchange, experiment (MBX_SENTINEL=1 through the env knob MBX_SENTINEL): consumers poll the
-// partial slots themselves instead of per-rank arrival counters.  Correct, but measured slower on
-// the TreeLSTM-512 b64 levels launch (ncu: 75.5-78.3 us against 70.0-72.6 us with counters): the
-// polling loads contend with the producers' stores in L2 and the saved round trip is lost.
-#define MBX_SENTINEL 0
-#endif
-#ifndef MBX_FLAG_STRIDE
-#define MBX_FLAG_STRIDE 1  // arrival counters' spacing (unsigned): 32 = one 128-byte line each
-#endif
-#define MBX_PART_EMPTY 0xffbadbadu  // a NaN payload no computation produces: "partial not written yet"
 namespace mbx_gen {
-__device__ __forceinline__ void st_part(float* p, float v) {
-  asm volatile("st.relaxed.gpu.global.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
-}
-__device__ __forceinline__ float ld_part(const float* p) {
-  float v;
-  asm volatile("ld.relaxed.gpu.global.f32 %0, [%1];" : "=f"(v) : "l"(p) : "memory");
-  return v;
-}
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
   unsigned v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -607,46 +608,25 @@ __device__ __forceinline__ unsigned long long global_ns() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
-// Spins (one thread) until *ctr reaches target; a wait that cannot complete (it never should)
-// traps after ~2 s instead of hanging the GPU.
+// One thread spins until *ctr reaches target (modular); a wait that cannot complete (it never
+// should: every CTA is co-resident) traps after ~2 s instead of hanging the GPU.
 __device__ __forceinline__ void spin_until(const unsigned* ctr, unsigned target) {
   if (int(ld_acquire_u32(ctr) - target) >= 0) return;
   const unsigned long long t0 = global_ns();
   while (int(ld_acquire_u32(ctr) - target) < 0)
     if (global_ns() - t0 > 2000000000ull) __trap();
 }
-#ifndef MBX_POLLERS
-#define MBX_POLLERS 1  // warps whose lane 0 polls a wait counter, phase-staggered
-#endif
-// Block-wide wait (every thread calls it) until *ctr reaches target.  One L2 round trip of an
-// acquire load is ~0.6 us, so a single poller notices a release up to that late; MBX_POLLERS > 1
-// pollers started a fraction of a round trip apart sample the counter more often.  The first to
-// see it publishes `epoch` in *seen (shared) so the others stop; the thread that did the acquire
-// load then orders the block's later reads through the __syncthreads.  Measured on the TreeLSTM-512
-// b64 levels launch (ncu, 4 repeats): 1 poller 71.2-72.1 us, 4: 72.4-73.9, 8: 74.6-78.0 — the
-// extra polls contend with the arrivals on the counter's L2 line, so the default is one.
-__device__ __forceinline__ void block_wait(const unsigned* ctr, unsigned target, volatile unsigned* seen,
-                                           unsigned epoch) {
-  const int w = threadIdx.x >> 5;
-  if ((threadIdx.x & 31) == 0 && w < MBX_POLLERS) {
-    if (w) __nanosleep(unsigned(w) * (600u / MBX_POLLERS));
-    const unsigned long long t0 = global_ns();
-    while (*seen != epoch) {
-      if (int(ld_acquire_u32(ctr) - target) >= 0) {
-        *seen = epoch;
-        break;
-      }
-      if (global_ns() - t0 > 2000000000ull) __trap();
-    }
-  }
-  __syncthreads();
-}
-// Grid-wide barrier over co-resident CTAs.  `target` = counter value once every CTA arrived.
-__device__ __forceinline__ void grid_barrier(unsigned* ctr, unsigned target, volatile unsigned* seen,
-                                             unsigned epoch) {
-  __syncthreads();
-  if (threadIdx.x == 0) red_release_add(ctr, 1u);
-  block_wait(ctr, target, seen, epoch);
+// Split-bf16 shadow of one output element at arena float offset o: bytes [4g, 4g + 16) of the
+// shadow hold the 8 bf16 "hi" parts of the 8-float group g = o & ~7, bytes [4g + 16, 4g + 32)
+// the "lo" parts (hi = bf16(x), lo = bf16(x - hi), exactly the gather's in-place conversion).
+__device__ __forceinline__ void store_shadow(unsigned char* shadow, long long o, float x) {
+  unsigned short h, l;
+  asm("cvt.rn.bf16.f32 %0, %1;" : "=h"(h) : "f"(x));
+  const float rest = x - __uint_as_float(unsigned(h) << 16);
+  asm("cvt.rn.bf16.f32 %0, %1;" : "=h"(l) : "f"(rest));
+  unsigned char* p = shadow + 4 * o - 2 * (o & 7);
+  *reinterpret_cast<unsigned short*>(p) = h;
+  *reinterpret_cast<unsigned short*>(p + 16) = l;
 }
 }  // namespace mbx_gen
 
@@ -654,15 +634,8 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const
   using namespace mbx_gen;
   extern __shared__ __align__(1024) unsigned char smem[];
   __shared__ TcLevel slv[64];  // the first 64 entries of the level table
-  __shared__ unsigned s_seen;  // block_wait: epoch of the last completed wait
-  unsigned wepoch = 0;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  if (tid == 0) s_seen = 0;
   MBX_LSTAMP(0, 14);  // kernel entry
-#ifdef MBX_STAMPS
-  if (tid == 0)  // %globaltimer at entry (comparable across SMs), slot (63, 14)
-    P.stamps[(((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * 64 + 63) * 16 + 14] = mbx_gen::global_ns();
-#endif
   const int tile_u = blockIdx.y;
   constexpr int S = MBX_LS;
   for (int i = tid; i < min(P.nlevels, 64); i += MBX_THREADS) slv[i] = P.levels[i];
@@ -684,8 +657,8 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const
   constexpr int xlo = xchunk + 64;
   constexpr int xstride = 2 * xchunk + 128;
   unsigned char* wsm = smem + P.w_off;          // [CPR][wstage], resident for the whole launch
-  unsigned char* xsm = smem + P.x_off;          // [CPR][xstride]; after the MMAs: stg
-  float* stg = reinterpret_cast<float*>(xsm);   // [nt][128] this rank's partials (LXCH 1: own slice)
+  unsigned char* xsm = smem + P.x_off;          // [CPR][xstride]; after the MMAs: stg (LXCH 0)
+  float* stg = reinterpret_cast<float*>(xsm);   // [nt][128] this rank's partials (LXCH 0)
   float* recv = reinterpret_cast<float*>(smem + P.recv_off);  // [S-1][nt/S][128] peers' partials
   unsigned long long* wfull = reinterpret_cast<unsigned long long*>(smem + P.bar_off);
   unsigned long long* xraw = wfull + 1;
@@ -696,11 +669,12 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const
   unsigned* tmem_slot = reinterpret_cast<unsigned*>(tready + 1);
   long long* rowbase = reinterpret_cast<long long*>(tready + 2);  // [MBX_LNT][2]
   (void)recv;
+  (void)stg;
 
   if (tid == 0) {
     mbar_init(wfull, 1);
     for (int j = 0; j < CPR; ++j) {
-      mbar_init(&xraw[j], MBX_LCY > 1 ? 1 : MBX_LGATHER);
+      mbar_init(&xraw[j], MBX_LGATHER);
       mbar_init(&xfull[j], MBX_LGATHER / 32);
     }
     mbar_init(done, 1);
@@ -724,21 +698,31 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const
 #if MBX_LXCH == 0
   if (S > 1) cluster_sync();  // peers' barriers initialised before any remote arrive
   else __syncthreads();
-#elif MBX_LCY > 1
-  cluster_sync();  // peers' barriers initialised before any multicast lands here
-#ifdef MBX_ARRIVE_RELEASE
-  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");  // staging free for tile 0
-#else
-  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");  // staging free for tile 0 (nothing to publish)
-#endif
 #else
   __syncthreads();
 #endif
   tc_fence_after();
   const unsigned tmem = *tmem_slot;
-  const unsigned nctas = gridDim.x * gridDim.y * gridDim.z;
   const int grp = blockIdx.x, ngrp = gridDim.x;
   const int gt = tid - 64;  // gather thread index (warps 2-7)
+  // Readiness counters this CTA acquires before a level: the unit tiles its K slice reads (per
+  // rank, from the host) and those its tail's batched loads read.
+  unsigned long long deps = P.dep_mask[rank];
+  for (int j = 0; j < MBX_NLOADS; ++j)
+    if (P.loads[j].kind == 1) {
+      const int c0 = P.loads[j].off + tile_u * MBX_UC;
+      if (c0 + MBX_UC <= MBX_U) {
+        for (int t = c0 / MBX_UC; t <= (c0 + MBX_UC - 1) / MBX_UC; ++t) deps |= 1ull << t;
+      } else {
+        deps = ~0ull;
+      }
+    }
+  // Its own unit tile always: then a counter reaching per_level * lv proves every CTA of that tile
+  // finished level lv - 1 (each increments once per level, only after its own wait at that level,
+  // which includes its own counter), however unevenly the CTAs progress.
+  deps |= 1ull << tile_u;
+  deps &= gridDim.y >= 64 ? ~0ull : ((1ull << gridDim.y) - 1ull);
+  const unsigned per_level = unsigned(ngrp * S);  // increments of one counter per completed level
   // Offset-table lookups of one tile's node rows (static: known before the producers finish).
   auto fill_rowbase = [&](const TcLevel L, int node0, int nt) {
     const int nn = min(nt, L.b - node0);
@@ -758,9 +742,7 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const
     fill_rowbase(slv[0], grp * slv[0].nt, slv[0].nt);
     have_rb = true;
   }
-  MBX_LSTAMP_T(64, 63, 11);  // profiling: gather thread after the first rowbase fill
   pdl_wait();  // the first level's inputs come from earlier launches
-  MBX_LSTAMP_T(64, 63, 12);  // profiling: gather thread after the PDL wait
 
   unsigned it = 0;  // node tiles processed by this CTA: parity of every per-tile mbarrier
   for (int lv = 0; lv < P.nlevels; ++lv) {
@@ -774,6 +756,15 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const
     const int ntr = nt / S;
     MBX_LSTAMP(lv, 0);
     if (lv + 1 == P.nlevels) pdl_launch_dependents();
+    if (lv > 0) {
+      // Levels 0..lv-1 of every unit tile this CTA reads are complete once their counters reach
+      // per_level * lv (each of the tile's CTAs adds 1 per finished level).  CTAs with no tile at
+      // this level wait too: an early increment would stand in for a missing one.
+      if (tid < 64 && ((deps >> tid) & 1ull))
+        spin_until(P.ready + tid * MBX_READY_STRIDE, P.ready_base + per_level * unsigned(lv));
+      __syncthreads();
+    }
+    MBX_LSTAMP(lv, 6);
     for (int node0 = grp * nt; node0 < b; node0 += ngrp * nt, ++it) {
       const unsigned par = it & 1u;
       const int nn = min(nt, b - node0);
@@ -781,17 +772,16 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const
       const int nloc0 = int(rank) * ntr;
       const int nloc = max(0, min(ntr, nn - nloc0));
       auto loc_col = [&](int m) { return nloc0 + m; };  // tile column of the rank's m-th node
+      if (S > 1 && tid == 0) mbar_expect_tx(rbar, unsigned((S - 1) * ntr * MBX_M * 4));
 #else
       // Rank r finishes the 8-node chunks c of the tile with c % S == r (lane-aligned slices).
-      const int nloc = MBX_LLOC;
+      const int nloc = ((nt / 8 + S - 1) / S) * 8;  // this tile's node slots of the rank (<= MBX_LLOC)
       auto loc_col = [&](int m) { return (((m >> 3) * S + int(rank)) << 3) + (m & 7); };
-#endif
-#if MBX_LXCH == 0
-      if (S > 1 && tid == 0) mbar_expect_tx(rbar, unsigned((S - 1) * ntr * MBX_M * 4));
 #endif
       // ---- tail operands of the nodes this rank finishes: into registers, in flight during the
       // gather and the MMAs (warps 0-1 now, the gather warps once their copies are issued) ----
       float lreg[MBX_LEPT][MBX_NLOADS > 0 ? MBX_NLOADS : 1];
+      int4 dreg[MBX_LEPT];  // image destinations of the element's row (L.img_slot >= 0)
       auto load_tail_operands = [&]() {
 #pragma unroll
         for (int t = 0; t < MBX_LEPT; ++t) {
@@ -799,6 +789,7 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const
           const int n = e / MBX_UC, u = e - n * MBX_UC;
           const bool valid = n < nloc && loc_col(n) < nn;
           const long long node = node0 + loc_col(n);
+          if (t * MBX_THREADS >= nloc * MBX_UC) break;  // warp-uniform: no element of this tile
 #pragma unroll
           for (int j = 0; j < MBX_NLOADS; ++j) {
             const TcLoad& l = P.loads[j];
@@ -810,75 +801,45 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const
             }
             lreg[t][j] = v;
           }
+          dreg[t] = make_int4(0, -1, 0, 0);
+          if (L.img_slot >= 0 && valid) dreg[t] = __ldg(L.img_dst + node);
         }
       };
-      MBX_LSTAMP_T(64, lv, 15);
-#if MBX_LCY > 1
-      // Staging of the previous tile converted by every CTA of the cluster (warps 0-1 hold no
-      // staging: they pass their arrival for this phase on at once).
-      asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
-#ifdef MBX_ARRIVE_RELEASE
-      if (warp < 2) asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
-#else
-      if (warp < 2) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");  // no staging held
-#endif
-#endif
       if (warp < 2) load_tail_operands();
       if (warp >= 2) {
-        // ---- gather + convert (warps 2-7); rowbase is normally filled during the previous tile ----
+        // ---- gather (+ conversion of fp32 rows) on warps 2-7; rowbase is normally filled during
+        // the previous tile ----
         if (!have_rb) fill_rowbase(L, node0, nt);
         have_rb = false;
         named_sync(1, MBX_LGATHER);
         MBX_LSTAMP_T(64, lv, 8);
-#if MBX_LCY > 1
-        unsigned char* stage = smem + P.stage_off;
-        {
-          unsigned cy;
-          asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(cy));
-          const int kb0 = c_begin * MBX_KC, kb1 = kb0 + MBX_LSLICE;
-          if (!L.vec16) {
-            // Rows not 16-byte aligned (bulk copies need it): every CTA copies all its rows itself,
-            // 4 bytes at a time, into the same staging layout; completion: wait, sync, one arrive.
-            for (int i = gt; i < nn * MBX_LSLICE; i += MBX_LGATHER) {
-              const int n = i / MBX_LSLICE, kk = kb0 + (i - n * MBX_LSLICE);
-              const int pc = (MBX_NPIECES > 1 && kk >= MBX_PK0) ? 1 : 0;
-              cp_async4(stage + n * MBX_LSROW + (kk - kb0) * 4, P.arena + rowbase[2 * n + pc] + kk - (pc ? MBX_PK0 : 0),
-                        true);
-            }
-            cp_async_commit();
-            cp_async_wait<0>();
-            named_sync(1, MBX_LGATHER);
-            if (gt == 0) mbar_arrive(&xraw[0]);
-          } else {
-          if (gt == 0) mbar_expect_tx(&xraw[0], unsigned(nn * MBX_LSLICE * 4));
-          // This CTA's share of the rows, each multicast to the whole cluster in one or two runs
-          // (the slice may straddle the two concatenated pieces).
-          const unsigned short mask = (unsigned short)((1u << MBX_LCY) - 1u);
-          for (int n = int(cy) + MBX_LCY * gt; n < nn; n += MBX_LCY * MBX_LGATHER) {
-#pragma unroll
-            for (int pc = 0; pc < 2; ++pc) {
-              const int lo = pc == 0 ? 0 : (MBX_NPIECES > 1 ? MBX_PK0 : MBX_NCHUNKS * MBX_KC);
-              const int hi = pc == 0 ? (MBX_NPIECES > 1 ? MBX_PK0 : MBX_NCHUNKS * MBX_KC) : MBX_NCHUNKS * MBX_KC;
-              const int r0 = max(lo, kb0), r1 = min(hi, kb1);
-              if (r0 >= r1) continue;
-              const float* src = P.arena + rowbase[2 * n + pc] + (r0 - lo);
-              const unsigned dst = smem_u32(stage + n * MBX_LSROW + (r0 - kb0) * 4);
-              asm volatile(
-                  "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster "
-                  "[%0], [%1], %2, [%3], %4;" ::"r"(dst),
-                  "l"(src), "r"(unsigned((r1 - r0) * 4)), "r"(smem_u32(&xraw[0])), "h"(mask)
-                  : "memory");
+        if (L.img >= 0) {
+          // Operand image: this rank's K slice of the tile, already split bf16 in the canonical
+          // layout — 2 bulk copies per chunk (hi, lo); the MMA issuer waits on xraw[j] itself.
+          if (gt == 0) {
+            // The image was written by other SMs' generic-proxy stores, released to this CTA
+            // through the readiness counters; the bulk copies read it through the async proxy.
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+            const int cb = nt * MBX_KC * 2;
+            const unsigned char* src =
+                P.img + L.img + (long long)(node0 / nt) * nt * (MBX_NCHUNKS * MBX_KC) * 4 + (long long)rank * CPR * 2 * cb;
+#pragma unroll 1
+            for (int j = 0; j < CPR; ++j) {
+              mbar_expect_tx(&xraw[j], unsigned(2 * cb));
+              mbar_arrive_cnt(&xraw[j], MBX_LGATHER - 1);
+              unsigned char* xs = xsm + j * xstride;
+              bulk_g2s(xs, src + (long long)j * 2 * cb, unsigned(cb), &xraw[j]);
+              bulk_g2s(xs + xlo, src + (long long)j * 2 * cb + cb, unsigned(cb), &xraw[j]);
             }
           }
-          }
-        }
-#else
+        } else {
         // Lane mapping: consecutive lanes take consecutive 16-byte quads of one node row, so a
         // warp reads whole 128-byte row segments (coalesced); quad qq of node n lands where its
-        // 8-element group's hi (even qq) or lo (odd qq) operand will live (converted in place).
+        // 8-element group's hi (even qq) or lo (odd qq) operand lives — for shadow rows that is
+        // exactly where the shadow already keeps it, for fp32 rows it is converted in place.
         constexpr int kq = MBX_KC / 4;
         const int nq = ((nn + 7) & ~7) * kq;  // columns past the last valid 8-group are never read
-        const float* arena = P.arena;
+        const unsigned char* src_base = L.shadow ? P.shadow : reinterpret_cast<const unsigned char*>(P.arena);
 #pragma unroll 1
         for (int j = 0; j < CPR; ++j) {
           const int k = (c_begin + j) * MBX_KC;
@@ -888,19 +849,18 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const
           for (int g = gt; g < nq; g += MBX_LGATHER) {
             const int n = g / kq, qq = g - n * kq;
             const bool valid = n < nn;
-            const float* src = arena + (valid ? rowbase[2 * n + p1] + kin + qq * 4 : 0);
-            float* dst = reinterpret_cast<float*>(xs + (n >> 3) * (MBX_KC * 16) + (n & 7) * 16 + ((qq >> 1) << 7) +
-                                                  ((qq & 1) ? xlo : 0));
+            const unsigned char* src = src_base + (valid ? 4 * (rowbase[2 * n + p1] + kin + qq * 4) : 0);
+            unsigned char* dst = xs + (n >> 3) * (MBX_KC * 16) + (n & 7) * 16 + ((qq >> 1) << 7) + ((qq & 1) ? xlo : 0);
             if (L.vec16) {
               cp_async16(dst, src, valid);
             } else {
 #pragma unroll
-              for (int e = 0; e < 4; ++e) cp_async4(dst + e, src + e, valid);
+              for (int e = 0; e < 4; ++e) cp_async4(dst + 4 * e, src + 4 * e, valid);
             }
           }
           asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&xraw[j])) : "memory");
         }
-#endif
+        }
         // Every row address of this tile is issued: look up the next tile's rows now (its
         // offset tables are static), off the critical path of the next gather.
         MBX_LSTAMP_T(64, lv, 9);
@@ -918,62 +878,40 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const
         const int l8 = gt & 7, g0 = gt >> 3;
 #pragma unroll 1
         for (int j = 0; j < CPR; ++j) {
-#if MBX_LCY > 1
-          if (j == 0) mbar_wait(&xraw[0], par);
-#else
-          mbar_wait(&xraw[j], par);
-#endif
-          if (j == 0) MBX_LSTAMP_T(64, lv, 10);
-          unsigned char* xs = xsm + j * xstride;
-          for (int g = g0; g < ngroups8; g += MBX_LGATHER / 8) {
-            const int m = g % kb, nb8 = g / kb;
-            const unsigned off = unsigned(nb8 * (MBX_KC * 16) + m * 128 + l8 * 16);
-#if MBX_LCY > 1
-            const unsigned char* srow = stage + (nb8 * 8 + l8) * MBX_LSROW + (j * MBX_KC + m * 8) * 4;
-            const float4 a = *reinterpret_cast<const float4*>(srow);
-            const float4 bq = *reinterpret_cast<const float4*>(srow + 16);
-#else
-            const float4 a = *reinterpret_cast<const float4*>(xs + off);
-            const float4 bq = *reinterpret_cast<const float4*>(xs + xlo + off);
-#endif
-            const float v[8] = {a.x, a.y, a.z, a.w, bq.x, bq.y, bq.z, bq.w};
-            unsigned hp[4], lp[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              hp[q] = pack_bf16x2(v[2 * q], v[2 * q + 1]);
-              const float h0 = __uint_as_float(hp[q] << 16), h1 = __uint_as_float(hp[q] & 0xffff0000u);
-              lp[q] = pack_bf16x2(v[2 * q] - h0, v[2 * q + 1] - h1);
-            }
-            *reinterpret_cast<uint4*>(xs + off) = make_uint4(hp[0], hp[1], hp[2], hp[3]);
-            if (npass > 1) *reinterpret_cast<uint4*>(xs + xlo + off) = make_uint4(lp[0], lp[1], lp[2], lp[3]);
+          if (L.img >= 0) {  // every barrier completes once per tile: pass xfull on
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&xfull[j]);
+            continue;
           }
-#ifndef MBX_FENCE_ONCE
-          // Chunk j is ready for the tensor core: its MMAs overlap the next chunk's conversion.
+          mbar_wait(&xraw[j], par);
+          if (j == 0) MBX_LSTAMP_T(64, lv, 10);
+          if (!L.shadow) {
+            unsigned char* xs = xsm + j * xstride;
+            for (int g = g0; g < ngroups8; g += MBX_LGATHER / 8) {
+              const int m = g % kb, nb8 = g / kb;
+              const unsigned off = unsigned(nb8 * (MBX_KC * 16) + m * 128 + l8 * 16);
+              const float4 a = *reinterpret_cast<const float4*>(xs + off);
+              const float4 bq = *reinterpret_cast<const float4*>(xs + xlo + off);
+              const float v[8] = {a.x, a.y, a.z, a.w, bq.x, bq.y, bq.z, bq.w};
+              unsigned hp[4], lp[4];
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                hp[q] = pack_bf16x2(v[2 * q], v[2 * q + 1]);  // low half = element 2q
+                const float h0 = __uint_as_float(hp[q] << 16), h1 = __uint_as_float(hp[q] & 0xffff0000u);
+                lp[q] = pack_bf16x2(v[2 * q] - h0, v[2 * q + 1] - h1);
+              }
+              *reinterpret_cast<uint4*>(xs + off) = make_uint4(hp[0], hp[1], hp[2], hp[3]);
+              if (npass > 1) *reinterpret_cast<uint4*>(xs + xlo + off) = make_uint4(lp[0], lp[1], lp[2], lp[3]);
+            }
+          }
+          // Chunk j is ready for the tensor core (async proxy): its MMAs overlap the next chunk.
           fence_async_smem();
           __syncwarp();
           if (lane == 0) mbar_arrive(&xfull[j]);
-#else
-          if (j + 1 == CPR) {
-            fence_async_smem();
-            __syncwarp();
-            if (lane == 0)
-              for (int q = 0; q < CPR; ++q) mbar_arrive(&xfull[q]);
-          }
-#endif
         }
-#if MBX_LCY > 1
-        // This CTA's staging is consumed: the cluster may multicast the next tile's rows into it.
-        // Relaxed: the only hazard is write-after-read, and every staging read has returned (its
-        // value fed a store above); .release would add a GPU-scope membar (ncu: stall_membar).
-#ifdef MBX_ARRIVE_RELEASE
-        asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
-#else
-        asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
-#endif
-#endif
         MBX_LSTAMP_T(64, lv, 7);
-        // The tail's operands: off the gather -> convert critical path, in flight during the MMAs
-        // and the exchange.
+        // The tail's operands: off the gather -> MMA critical path, in flight during the MMAs and
+        // the exchange.
         load_tail_operands();
       } else if (warp == 1 && lane == 0) {
         // ---- MMA issuer ----
@@ -983,7 +921,7 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const
         const unsigned sbo = unsigned(MBX_KC * 16);
 #pragma unroll 1
         for (int j = 0; j < CPR; ++j) {
-          mbar_wait(&xfull[j], par);
+          mbar_wait(L.img >= 0 ? &xraw[j] : &xfull[j], par);  // image chunks land by TMA (async proxy)
           tc_fence_after();
           const unsigned wa = smem_u32(wsm + j * wstage);
           const unsigned xa = smem_u32(xsm + j * xstride);
@@ -1052,8 +990,9 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const
         return q == int(rank) ? stg[(nloc0 + n) * MBX_M + col] : recv[((q < int(rank) ? q : q - 1) * ntr + n) * MBX_M + col];
       };
 #else
-      // ---- accumulators: own rank's nodes -> shared memory, the peers' -> their L2 slots ----
-      // part layout: [tile parity][unit tile][destination rank][source rank][nt/S][128]
+      // ---- accumulators -> every rank's L2 slots (the own slice too: the reduction then reads
+      // all S partials the same way, uniform and branch-free, every load in flight) ----
+      // part layout: [tile parity][group][unit tile][destination rank][source rank][LLOC][128]
       float* pbase = P.part + ((size_t)(par * ngrp + grp) * gridDim.y + tile_u) * S * S * MBX_LLOC * MBX_M;
       {
         // Warp w reads TMEM lanes 32*(w%4).. (gate rows) for every other 8-column chunk.
@@ -1062,136 +1001,32 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const
         for (int ch = half; ch < (nn + 7) >> 3; ch += 2) {
           float v[8];
           tmem_ld8(tmem + (unsigned(q * 32) << 16) + unsigned(ch * 8), v);
-          // Every rank's slice, this rank's own included, goes to the L2 buffer: the reduction
-          // then reads all S partials the same way (uniform, branch-free, all loads in flight).
           const int r = ch % S, m0 = (ch / S) * 8;
           float* dst = pbase + ((size_t)(r * S + int(rank)) * MBX_LLOC + m0) * MBX_M + row;
 #pragma unroll
-          for (int k = 0; k < 8; ++k) {
-#if MBX_SENTINEL
-            // Only the tile's real nodes: every slot written is read and reset by its consumer.
-            if (ch * 8 + k < nn) st_part(dst + k * MBX_M, v[k]);
-#else
-            __stcg(dst + k * MBX_M, v[k]);
-#endif
-          }
+          for (int k = 0; k < 8; ++k) __stcg(dst + k * MBX_M, v[k]);
         }
       }
       MBX_LSTAMP(lv, 12);
       tc_fence_before();
-#if !MBX_SENTINEL
       __syncthreads();
       MBX_LSTAMP(lv, 13);
       if (S > 1) {
-        unsigned* flags = P.xflags + (grp * gridDim.y + tile_u) * S * MBX_FLAG_STRIDE;
-        if (tid < S && tid != int(rank)) red_release_add(flags + tid * MBX_FLAG_STRIDE, 1u);
+        unsigned* flags = P.xflags + (grp * gridDim.y + tile_u) * S;
+        if (tid < S && tid != int(rank)) red_release_add(flags + tid, 1u);
         MBX_LSTAMP(lv, 3);
-        block_wait(flags + rank * MBX_FLAG_STRIDE, unsigned(S - 1) * (it + 1), &s_seen, ++wepoch);
+        if (tid == 0) spin_until(flags + rank, unsigned(S - 1) * (it + 1));
+        __syncthreads();
       }
-#endif
-      auto paddr = [&](int q, int n, int col) -> float* {
-        return pbase + ((size_t)(int(rank) * S + q) * MBX_LLOC + n) * MBX_M + col;
+      auto partial = [&](int q, int n, int col) -> float {
+        return __ldcg(pbase + ((size_t)(int(rank) * S + q) * MBX_LLOC + n) * MBX_M + col);
       };
-      auto partial = [&](int q, int n, int col) -> float { return __ldcg(paddr(q, n, col)); };
 #endif
       MBX_LSTAMP(lv, 4);
-#ifdef MBX_FUSE_PW
-      // Fused pointwise batch: its shared rows depend on the unit only, and a thread's elements
-      // (tid + t * MBX_THREADS) all share one unit.
-      static_assert(MBX_THREADS % MBX_UC == 0, "fused tail: one unit per thread");
-      float pw_sh[MBX_PW_NLOADS];
-      long long pw_ob[MBX_PW_NOUT];
-      {
-        const int ug0 = tile_u * MBX_UC + tid % MBX_UC;
-#pragma unroll
-        for (int j = 0; j < MBX_PW_NLOADS; ++j) {
-          const TcLoad& d = P.pw_loads[j];
-          pw_sh[j] = j == P.pw_xt ? 0.0f : __ldcg(P.arena + __ldg(P.pw_shared_off + d.idx) + d.off + ug0);
-        }
-#pragma unroll
-        for (int k = 0; k < MBX_PW_NOUT; ++k) pw_ob[k] = __ldg(P.pw_out_base + k);
-      }
-#endif
       // ---- sum the partials in rank order, run the tail, write the outputs ----
       // Every partial of every element is read before the first output store: through generic
       // pointers a store would order all later loads behind it (one L2 round trip per element).
       float gsum[MBX_LEPT][MBX_G];
-#if MBX_LXCH == 1 && MBX_SENTINEL
-      // Partials arrive without a flag: every slot holds MBX_PART_EMPTY until its producer's store
-      // lands, so the loads poll the data itself (one L2 round trip fewer than counter + data).
-      // All loads are issued first; only slots still empty are re-read.  The consumer then puts
-      // the slot back to empty: its producer rewrites it two tiles later, after a grid barrier (or
-      // a fence, below, when one level has more tiles).
-      {
-        float pv[MBX_LEPT][MBX_G][S];
-#pragma unroll
-        for (int t = 0; t < MBX_LEPT; ++t) {
-          const int e = tid + t * MBX_THREADS;
-          const int n = e / MBX_UC, u = e - n * MBX_UC;
-          const bool valid = n < nloc && loc_col(n) < nn;
-#pragma unroll
-          for (int gi = 0; gi < MBX_G; ++gi)
-#pragma unroll
-            for (int q = 0; q < S; ++q) pv[t][gi][q] = valid ? ld_part(paddr(q, n, gi * MBX_UC + u)) : 0.0f;
-        }
-        // Rounds: re-issue every slot still empty (all in flight), then check them all.
-        auto empty = [&](int t, int gi, int q) -> bool {
-          const int e = tid + t * MBX_THREADS;
-          const int n = e / MBX_UC;
-          return n < nloc && loc_col(n) < nn && __float_as_uint(pv[t][gi][q]) == MBX_PART_EMPTY;
-        };
-        bool pending = false;
-#pragma unroll
-        for (int t = 0; t < MBX_LEPT; ++t)
-#pragma unroll
-          for (int gi = 0; gi < MBX_G; ++gi)
-#pragma unroll
-            for (int q = 0; q < S; ++q) pending |= empty(t, gi, q);
-        if (pending) {
-          const unsigned long long t0 = global_ns();
-          while (pending) {
-#pragma unroll
-            for (int t = 0; t < MBX_LEPT; ++t)
-#pragma unroll
-              for (int gi = 0; gi < MBX_G; ++gi)
-#pragma unroll
-                for (int q = 0; q < S; ++q)
-                  if (empty(t, gi, q)) {
-                    const int e = tid + t * MBX_THREADS;
-                    const int n = e / MBX_UC, u = e - n * MBX_UC;
-                    pv[t][gi][q] = ld_part(paddr(q, n, gi * MBX_UC + u));
-                  }
-            pending = false;
-#pragma unroll
-            for (int t = 0; t < MBX_LEPT; ++t)
-#pragma unroll
-              for (int gi = 0; gi < MBX_G; ++gi)
-#pragma unroll
-                for (int q = 0; q < S; ++q) pending |= empty(t, gi, q);
-            if (pending && global_ns() - t0 > 2000000000ull) __trap();
-          }
-        }
-#pragma unroll
-        for (int t = 0; t < MBX_LEPT; ++t) {
-          const int e = tid + t * MBX_THREADS;
-          const int n = e / MBX_UC, u = e - n * MBX_UC;
-          const bool valid = n < nloc && loc_col(n) < nn;
-          if (valid) {
-#pragma unroll
-            for (int gi = 0; gi < MBX_G; ++gi)
-#pragma unroll
-              for (int q = 0; q < S; ++q) st_part(paddr(q, n, gi * MBX_UC + u), __uint_as_float(MBX_PART_EMPTY));
-          }
-#pragma unroll
-          for (int gi = 0; gi < MBX_G; ++gi) {
-            float acc = pv[t][gi][0];
-#pragma unroll
-            for (int q = 1; q < S; ++q) acc = acc + pv[t][gi][q];
-            gsum[t][gi] = acc;
-          }
-        }
-      }
-#else
 #pragma unroll
       for (int t = 0; t < MBX_LEPT; ++t) {
         const int e = tid + t * MBX_THREADS;
@@ -1200,38 +1035,35 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const
 #pragma unroll
         for (int gi = 0; gi < MBX_G; ++gi) {
           const int col = gi * MBX_UC + u;
-          float acc = 0.0f;
-#pragma unroll
           float pv[S];
 #pragma unroll
-          for (int q = 0; q < S; ++q) pv[q] = partial(q, valid ? n : 0, col);  // invalid: a harmless row
+          for (int q = 0; q < S; ++q) pv[q] = valid ? partial(q, n, col) : 0.0f;
+          float acc = pv[0];
 #pragma unroll
-          for (int q = 0; q < S; ++q) acc = q == 0 ? pv[q] : acc + pv[q];
+          for (int q = 1; q < S; ++q) acc = acc + pv[q];
           gsum[t][gi] = acc;
         }
       }
-#endif
       // Every element's tail first (independent activation chains the scheduler can interleave),
       // then the stores: a store between two elements would keep their chains apart.
       float ov[MBX_LEPT][MBX_NOUT];
-#ifdef MBX_FUSE_PW
-      float pv[MBX_LEPT][MBX_PW_NOUT];
-#endif
 #pragma unroll
-      for (int t = 0; t < MBX_LEPT; ++t) {
-        mbx_tail(gsum[t], lreg[t], ov[t]);
-#ifdef MBX_FUSE_PW
-        // The next batch (elementwise over these rows, same node order) from registers: its own
-        // row is ov[t][0], its shared rows were loaded before the partial sums (pw_sh).
-        float lp[MBX_PW_NLOADS];
+      for (int t = 0; t < MBX_LEPT; ++t)
+        if (t * MBX_THREADS < nloc * MBX_UC) mbx_tail(gsum[t], lreg[t], ov[t]);
+      MBX_LSTAMP(lv, 13);
+      const unsigned smask = L.shadow_out;
+      if (smask == 0 && L.img_slot < 0) {  // plain outputs (warp-uniform)
 #pragma unroll
-        for (int j = 0; j < MBX_PW_NLOADS; ++j) lp[j] = j == P.pw_xt ? ov[t][0] : pw_sh[j];
-        mbx_pw_tail_fast(lp, pv[t]);
-#endif
-      }
-#if MBX_LXCH == 0
-      MBX_LSTAMP(lv, 13);  // profiling (DSMEM configurations): tails computed, stores next
-#endif
+        for (int t = 0; t < MBX_LEPT; ++t) {
+          const int e = tid + t * MBX_THREADS;
+          const int n = e / MBX_UC, u = e - n * MBX_UC;
+          if (n < nloc && loc_col(n) < nn) {
+            const long long node = node0 + loc_col(n);
+#pragma unroll
+            for (int k = 0; k < MBX_NOUT; ++k) P.arena[obase[k] + node * MBX_U + tile_u * MBX_UC + u] = ov[t][k];
+          }
+        }
+      } else {
 #pragma unroll
       for (int t = 0; t < MBX_LEPT; ++t) {
         const int e = tid + t * MBX_THREADS;
@@ -1240,45 +1072,52 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const
           const long long node = node0 + loc_col(n);
           const int ug = tile_u * MBX_UC + u;
 #pragma unroll
-          for (int k = 0; k < MBX_NOUT; ++k) P.arena[obase[k] + node * MBX_U + ug] = ov[t][k];
-#ifdef MBX_FUSE_PW
-#pragma unroll
-          for (int k = 0; k < MBX_PW_NOUT; ++k) P.arena[pw_ob[k] + node * MBX_U + ug] = pv[t][k];
-#endif
+          for (int k = 0; k < MBX_NOUT; ++k) {
+            const long long o = obase[k] + node * MBX_U + ug;
+            P.arena[o] = ov[t][k];
+            if ((smask >> k) & 1u) store_shadow(P.shadow, o, ov[t][k]);
+            if (k == L.img_slot) {  // scattered into the consumer level's operand image
+              const int4 d = dreg[t];
+              if (d.y >= 0) {
+                int lo;
+                const long long a = img_addr(d, ug, &lo);
+                unsigned short h, l;
+                asm("cvt.rn.bf16.f32 %0, %1;" : "=h"(h) : "f"(ov[t][k]));
+                asm("cvt.rn.bf16.f32 %0, %1;" : "=h"(l) : "f"(ov[t][k] - __uint_as_float(unsigned(h) << 16)));
+                *reinterpret_cast<unsigned short*>(P.img + a) = h;
+                *reinterpret_cast<unsigned short*>(P.img + a + lo) = l;
+              }
+            }
+          }
         }
+      }
       }
 #if MBX_LXCH == 0
       if (S > 1 && tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-#elif MBX_SENTINEL
-      // A third tile of this level reuses this tile's partial slots with no grid barrier between:
-      // the empty markers must be in L2 before this CTA's next partials (which the producers
-      // observe before they write that tile).
-      if (node0 + 2 * ngrp * nt < b) __threadfence();
 #endif
       __syncthreads();  // stg / recv / TMEM free for the next tile
       tc_fence_after();
       MBX_LSTAMP(lv, 5);
     }
-    if (lv + 1 < P.nlevels) grid_barrier(P.gbar, P.gbar_base + unsigned(lv + 1) * nctas, &s_seen, ++wepoch);
-    MBX_LSTAMP(lv, 6);
+    // This CTA's part of level lv is written: release it to the level's consumers (the
+    // __syncthreads orders every thread's stores before thread 0's release).
+    if (lv + 1 < P.nlevels) {
+      __syncthreads();
+      if (tid == 0) red_release_add(P.ready + tile_u * MBX_READY_STRIDE, 1u);
+    }
   }
-#if MBX_LCY > 1
-  // Balance the staging barrier and keep this CTA's shared memory alive until no peer can still
-  // multicast into it.
-  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
-#endif
 #if MBX_LXCH == 0
   if (S > 1) cluster_sync();  // no peer still pushes into this CTA's shared memory
 #else
-  // Every increment of this CTA's counter happened before its last wait: reset it for the next
-  // launch (stream order makes launches sequential).
-  if (!MBX_SENTINEL && S > 1 && tid == 0 && it > 0)
-    P.xflags[((grp * gridDim.y + tile_u) * S + rank) * MBX_FLAG_STRIDE] = 0u;
+  // Every increment of this CTA's exchange counter happened before its last wait: reset it for
+  // the next launch (stream order makes launches sequential).
+  if (S > 1 && tid == 0 && it > 0) P.xflags[(grp * gridDim.y + tile_u) * S + rank] = 0u;
 #endif
   if (warp == 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(P.tmem_cols) : "memory");
 }
 #endif  // MBX_LEVELS_KERNEL
+
 
 #ifdef MBX_SMALL_KERNEL
 // mbx_exact_gate — bit-exact CUDA-core path of the gate plans: the FP32 context's cells, the
@@ -1440,9 +1279,46 @@ __device__ __forceinline__ void mbx_pointwise_body(const PwArgs& P) {
     }
 #pragma unroll
     for (int k = 0; k < MBX_NOUT; ++k) {
-      float* dst = P.arena + P.out_base[k] + node * MBX_PW_E + e;
-      if (V == 4) *reinterpret_cast<float4*>(dst) = make_float4(o[0][k], o[V > 1 ? 1 : 0][k], o[V > 2 ? 2 : 0][k], o[V > 3 ? 3 : 0][k]);
-      else *dst = o[0][k];
+      const long long off = P.out_base[k] + node * MBX_PW_E + e;
+      float* dst = P.arena + off;
+      if (V == 4) {
+        const float4 v = make_float4(o[0][k], o[V > 1 ? 1 : 0][k], o[V > 2 ? 2 : 0][k], o[V > 3 ? 3 : 0][k]);
+        *reinterpret_cast<float4*>(dst) = v;
+        // Split-bf16 shadow of the 4 values (half an 8-float group; see mbx_tc_levels): the
+        // later tensor-core level that gathers this row reads it MMA-ready.
+        if ((P.shadow_out >> k) & 1u) {
+          const float x[4] = {v.x, v.y, v.z, v.w};
+          unsigned hp[2], lp[2];
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            hp[q] = mbx_gen::pack_bf16x2(x[2 * q], x[2 * q + 1]);
+            const float h0 = __uint_as_float(hp[q] << 16), h1 = __uint_as_float(hp[q] & 0xffff0000u);
+            lp[q] = mbx_gen::pack_bf16x2(x[2 * q] - h0, x[2 * q + 1] - h1);
+          }
+          unsigned char* sp = P.shadow + 4 * off - 2 * (off & 7);
+          *reinterpret_cast<uint2*>(sp) = make_uint2(hp[0], hp[1]);
+          *reinterpret_cast<uint2*>(sp + 16) = make_uint2(lp[0], lp[1]);
+        }
+        if (k == P.img_slot) {  // scattered into the consumer level's operand image
+          const int4 d = P.img_dst[node];
+          if (d.y >= 0) {
+            const float x[4] = {v.x, v.y, v.z, v.w};
+            unsigned hp[2], lp[2];
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+              hp[q] = mbx_gen::pack_bf16x2(x[2 * q], x[2 * q + 1]);
+              const float h0 = __uint_as_float(hp[q] << 16), h1 = __uint_as_float(hp[q] & 0xffff0000u);
+              lp[q] = mbx_gen::pack_bf16x2(x[2 * q] - h0, x[2 * q + 1] - h1);
+            }
+            int lo;
+            const long long a = mbx_gen::img_addr(d, e, &lo);
+            *reinterpret_cast<uint2*>(P.img + a) = make_uint2(hp[0], hp[1]);
+            *reinterpret_cast<uint2*>(P.img + a + lo) = make_uint2(lp[0], lp[1]);
+          }
+        }
+      } else {
+        *dst = o[0][k];
+      }
     }
   }
 }

@@ -141,31 +141,3 @@ def test_levels_kernel_covers_internal_depths(gpu, golden):
     got = np.concatenate([mbx.flatten_floats(o) for o in r.outputs])
     st = elementwise(got, np.concatenate(want), 1e-3)
     assert st["normwise"] <= 1e-3 and st["frac_pass"] >= MIN_PASS["bf16x3"], st
-
-
-def test_fused_leaf_cell_opt_in(gpu):
-    """MBX_FUSE=1: the TreeLSTM leaf cell runs in the wide launch's tail — one device launch
-    fewer, outputs bit-identical to the unfused run (same fast tail on the same values)."""
-    import os
-    import subprocess
-    import sys
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    code = (
-        "import sys, numpy as np; sys.path.insert(0, %r)\n"
-        "from paper_2305_10611_b200 import mbx\n"
-        "c = mbx.Context(0, 'bf16x3'); m = mbx.Model(c, 'treelstm', 512); m.make_params(1)\n"
-        "t, d = m.make_inputs(1, 64); r = m.evaluate_batch(t, d, 64)\n"
-        "np.save(sys.argv[1], r.out_data); print(r.trace.device_launches)\n" % root)
-    outs = {}
-    for fuse in ("0", "1"):
-        env = dict(os.environ)
-        env.pop("MBX_FUSE", None)
-        if fuse == "1":
-            env["MBX_FUSE"] = "1"
-        path = os.path.join(root, "gpurun_out", "fuse_%s.npy" % fuse)
-        os.makedirs(os.path.dirname(path), exist_ok=True)
-        p = subprocess.run([sys.executable, "-c", code, path], env=env, capture_output=True, text=True, timeout=600)
-        assert p.returncode == 0, p.stderr[-2000:]
-        outs[fuse] = (int(p.stdout.strip().splitlines()[-1]), np.load(path))
-    assert outs["1"][0] == outs["0"][0] - 1, (outs["0"][0], outs["1"][0])
-    assert np.array_equal(outs["0"][1].view(np.uint32), outs["1"][1].view(np.uint32))
