@@ -14,7 +14,9 @@
  *   - Host values (model inputs / outputs) cross the ABI in the "hostval" encoding: an int32
  *     token stream plus a float32 data stream, depth-first:
  *        tensor: 0, rows, cols (rows*cols floats from the data stream) | int: 1, value
- *        list: 2, n, items... | tuple: 3, n, items... | adt: 4, ctor(0 Leaf,1 Node), n, fields...
+ *        | int64: 6, lo, hi | float64: 5, lo, hi (bits of the double)
+ *        list: 2, n, items... | tuple: 3, n, items...
+ *        | adt: 4, ctor (0 Leaf, 1 Node, -1 named: length, one token per byte), n, fields...
  *   - One context = one device + one CUDA stream + one arena; a context is used by one host
  *     thread at a time (the reference executor is single-threaded).
  */
@@ -65,6 +67,8 @@ int64_t mbx_arena_used(const mbx_ctx* ctx);                                  /* 
  * ("tensor handle out of arena bounds").  download synchronizes the stream. */
 int mbx_arena_upload(mbx_ctx* ctx, int64_t offset, const float* src, int64_t n);
 int mbx_arena_download(mbx_ctx* ctx, int64_t offset, float* dst, int64_t n);
+/* Arena::ptr: the device address of arena[off, off + n) (bounds-checked; NULL in dry contexts). */
+int mbx_arena_device_ptr(mbx_ctx* ctx, int64_t offset, int64_t n, float** out);
 /* Drops every allocation at or above `used` (session reuse; params below stay resident). */
 int mbx_arena_rewind(mbx_ctx* ctx, int64_t used);
 
@@ -90,6 +94,22 @@ int mbx_plan_register(mbx_ctx* ctx, const int32_t* enc, int64_t n, int* plan_id)
 int mbx_exec_batched(mbx_ctx* ctx, int plan_id, int b, const int64_t* shared_off,
                      const int64_t* batched_off, int gather_mode, int64_t* out_off,
                      int64_t* gather_bytes);
+
+/* Flush scope (runtime::Executor::flush, proj/src/executor.cpp:711-758): between
+ * mbx_flush_begin and mbx_flush_end, mbx_exec_batched validates, allocates and returns each
+ * batch's output handles at once (same offsets as outside a flush) but queues the device work;
+ * mbx_flush_end plans the queued batches together — consecutive batches of one tensor-core gate
+ * plan become one persistent multi-level launch (e.g. every TreeLSTM depth), gathered operands
+ * are written MMA-ready by their producers — and issues them with one offset-table H2D.  Every
+ * other call on the context (downloads, uploads, primops, mbx_read_ints, mbx_sync, evaluation)
+ * issues the queued work first, so the results are the same as without the scope. */
+int mbx_flush_begin(mbx_ctx* ctx);
+int mbx_flush_end(mbx_ctx* ctx);
+
+/* Decision read-back (Executor::read_scalar_int, proj/src/executor.cpp:235-238): out[k] =
+ * (long)arena[offs[k]] for every k, with one pack kernel and one D2H for all n values
+ * (synchronises). */
+int mbx_read_ints(mbx_ctx* ctx, const int64_t* offs, int n, int64_t* out);
 
 /* backend::exec_primop (proj/src/backend.cpp:105-181) on arena tensors. */
 int mbx_exec_primop(mbx_ctx* ctx, int op, int nin, const int64_t* in_off, const int* in_rows,

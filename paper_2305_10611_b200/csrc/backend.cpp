@@ -940,6 +940,38 @@ void issue_prefix(mbx_ctx* c, const BatchLaunch& L) {
   }
 }
 
+void issue_pending(mbx_ctx* c) {
+  std::vector<BatchLaunch> Ls;
+  Ls.swap(c->pending);
+  if (Ls.empty()) return;
+  std::vector<LevelsRun> runs;
+  std::vector<int> run_at(Ls.size(), -1);
+  for (size_t i = 0; i < Ls.size();) {
+    LevelsRun r;
+    r.start = int(i);
+    r.n = plan_levels(c, Ls, i, &r.table, &r.groups, &r.cfg);
+    if (r.n >= 1) {
+      run_at[i] = int(runs.size());
+      runs.push_back(r);
+      i += size_t(r.n);
+    } else {
+      ++i;
+    }
+  }
+  plan_shadows(c, Ls, runs);
+  meta_commit(c);
+  for (size_t i = 0; i < Ls.size();) {
+    if (run_at[i] >= 0) {
+      const LevelsRun& r = runs[size_t(run_at[i])];
+      issue_levels(c, Ls, i, r.n, r.table, r.groups, r.cfg);
+      i += size_t(r.n);
+    } else {
+      issue_batch(c, Ls[i]);
+      ++i;
+    }
+  }
+}
+
 void issue_batch(mbx_ctx* c, const BatchLaunch& L) {
   const PlanEntry& pe = c->plans[L.plan_id];
   if (pe.plan.ghost || c->dry) return;
@@ -1175,12 +1207,46 @@ static void throw_if(int rc, mbx_ctx* c) {
   if (rc != 0) throw Error(mbx_last_error(c));
 }
 
-Arena::Arena(int device, int precision) : owned_(true) {
+static int env_precision() {
+  const char* e = std::getenv("MBX_PRECISION");
+  if (!e || std::strcmp(e, "fp32") == 0) return MBX_PREC_FP32;
+  if (std::strcmp(e, "bf16x3") == 0) return MBX_PREC_BF16X3;
+  if (std::strcmp(e, "bf16") == 0) return MBX_PREC_BF16;
+  throw Error(std::string("MBX_PRECISION: unknown precision ") + e);
+}
+Arena::Arena(int64_t initial_capacity) : owned_(true) {
+  (void)initial_capacity;  // HBM is mapped on demand; offsets never move
+  const char* dev = std::getenv("MBX_DEVICE");
   mbx_ctx* c = nullptr;
-  if (mbx_ctx_create(device, precision, &c) != 0) throw Error("mbx_ctx_create failed");
+  if (mbx_ctx_create(dev ? std::atoi(dev) : 0, env_precision(), &c) != 0) throw Error(mbx_last_error(nullptr));
   ctx_ = c;
 }
-Arena::Arena(mbx_ctx* ctx) : ctx_(ctx), owned_(false) {}
+Arena::Arena(Device d) : owned_(true) {
+  mbx_ctx* c = nullptr;
+  if (mbx_ctx_create(d.id, d.precision, &c) != 0) throw Error(mbx_last_error(nullptr));
+  ctx_ = c;
+}
+Float* Arena::ptr(const TensorHandle& h) {
+  check(h);
+  float* p = nullptr;
+  throw_if(mbx_arena_device_ptr(ctx_, h.offset, h.size(), &p), ctx_);
+  return p;
+}
+const Float* Arena::ptr(const TensorHandle& h) const { return const_cast<Arena*>(this)->ptr(h); }
+std::vector<long> Arena::read_ints(const std::vector<TensorHandle>& hs) const {
+  std::vector<int64_t> offs, vals(hs.size());
+  for (const auto& h : hs) {
+    check(h);
+    offs.push_back(h.offset);
+  }
+  throw_if(mbx_read_ints(ctx_, offs.data(), int(offs.size()), vals.data()), ctx_);
+  return std::vector<long>(vals.begin(), vals.end());
+}
+FlushScope::FlushScope(Arena& a) : a_(a) { throw_if(mbx_flush_begin(a.ctx()), a.ctx()); }
+FlushScope::~FlushScope() noexcept(false) {
+  const int rc = mbx_flush_end(a_.ctx());
+  if (rc != 0 && !std::uncaught_exceptions()) throw Error(mbx_last_error(a_.ctx()));
+}
 Arena::~Arena() {
   if (owned_) mbx_ctx_destroy(ctx_);
 }

@@ -1,3 +1,4 @@
+#include <climits>
 // capi.cpp — the C ABI (include/mbx.h).  Every entry point catches mbatch::Error (and any other
 // exception) and turns it into a nonzero status plus mbx_last_error(ctx), so the boundary never
 // throws; the C++ surface (include/mbatch/*.hpp) rethrows the same text.
@@ -41,17 +42,53 @@ int guarded(mbx_ctx* c, F&& f) {
   }
 }
 
+// Scalars: kind 1 = int32, kind 6 = int64 (lo, hi), kind 5 = float64 (lo, hi bits).  ADT
+// constructors: 0 Leaf, 1 Node, -1 = named (length, one token per byte).
+void push64(std::vector<int32_t>& t, uint64_t bits) {
+  t.push_back(int32_t(uint32_t(bits & 0xffffffffu)));
+  t.push_back(int32_t(uint32_t(bits >> 32)));
+}
+uint64_t read64(const int32_t* t, int64_t nt, int64_t& ti) {
+  MBATCH_CHECK(ti + 2 <= nt, "hostval encoding truncated");
+  const uint64_t v = uint64_t(uint32_t(t[ti])) | (uint64_t(uint32_t(t[ti + 1])) << 32);
+  ti += 2;
+  return v;
+}
+
 void encode(const HostValue& v, std::vector<int32_t>& t, std::vector<float>& d) {
   switch (v.kind) {
     case HostValue::Kind::kTensor:
       t.push_back(0); t.push_back(v.shape.rows); t.push_back(v.shape.cols);
       d.insert(d.end(), v.data.begin(), v.data.end());
       return;
-    case HostValue::Kind::kInt: t.push_back(1); t.push_back(int32_t(v.ival)); return;
-    case HostValue::Kind::kFloat: t.push_back(1); t.push_back(int32_t(v.fval)); return;
+    case HostValue::Kind::kInt:
+      if (v.ival >= INT32_MIN && v.ival <= INT32_MAX) {
+        t.push_back(1);
+        t.push_back(int32_t(v.ival));
+      } else {
+        t.push_back(6);
+        push64(t, uint64_t(int64_t(v.ival)));
+      }
+      return;
+    case HostValue::Kind::kFloat: {
+      uint64_t bits;
+      std::memcpy(&bits, &v.fval, sizeof bits);
+      t.push_back(5);
+      push64(t, bits);
+      return;
+    }
     case HostValue::Kind::kList: t.push_back(2); break;
     case HostValue::Kind::kTuple: t.push_back(3); break;
-    case HostValue::Kind::kAdt: t.push_back(4); t.push_back(v.ctor == "Node" ? 1 : 0); break;
+    case HostValue::Kind::kAdt:
+      t.push_back(4);
+      if (v.ctor == "Leaf" || v.ctor == "Node") {
+        t.push_back(v.ctor == "Node" ? 1 : 0);
+      } else {
+        t.push_back(-1);
+        t.push_back(int32_t(v.ctor.size()));
+        for (unsigned char ch : v.ctor) t.push_back(int32_t(ch));
+      }
+      break;
   }
   t.push_back(int32_t(v.items.size()));
   for (auto& it : v.items) encode(it, t, d);
@@ -74,16 +111,36 @@ HostValue decode(const int32_t* t, int64_t nt, int64_t& ti, const float* d, int6
       return v;
     }
     case 1: MBATCH_CHECK(ti < nt, "hostval encoding truncated"); return HostValue::scalar(t[ti++]);
+    case 6: return HostValue::scalar(long(int64_t(read64(t, nt, ti))));
+    case 5: {
+      const uint64_t bits = read64(t, nt, ti);
+      HostValue v;
+      v.kind = HostValue::Kind::kFloat;
+      std::memcpy(&v.fval, &bits, sizeof bits);
+      return v;
+    }
     case 2: case 3: case 4: {
-      int ctor = 0;
-      if (kind == 4) { MBATCH_CHECK(ti < nt, "hostval encoding truncated"); ctor = t[ti++]; }
+      std::string ctor = "Leaf";
+      if (kind == 4) {
+        MBATCH_CHECK(ti < nt, "hostval encoding truncated");
+        const int id = t[ti++];
+        if (id >= 0) {
+          ctor = id ? "Node" : "Leaf";
+        } else {
+          MBATCH_CHECK(ti < nt, "hostval encoding truncated");
+          const int len = t[ti++];
+          MBATCH_CHECK(len >= 0 && ti + len <= nt, "hostval encoding truncated");
+          ctor.clear();
+          for (int k = 0; k < len; ++k) ctor.push_back(char(t[ti++]));
+        }
+      }
       MBATCH_CHECK(ti < nt, "hostval encoding truncated");
       int n = t[ti++];
       std::vector<HostValue> items;
       for (int k = 0; k < n; ++k) items.push_back(decode(t, nt, ti, d, nd, di));
       if (kind == 2) return HostValue::list(std::move(items));
       if (kind == 3) return HostValue::tuple(std::move(items));
-      return HostValue::adt(ctor ? "Node" : "Leaf", std::move(items));
+      return HostValue::adt(ctor, std::move(items));
     }
   }
   throw Error("hostval encoding: bad kind " + std::to_string(kind));
@@ -184,6 +241,7 @@ void mbx_pool_set_error(const char* msg) { g_err = msg ? msg : ""; }
 
 int mbx_ctx_set_precision(mbx_ctx* c, int precision) {
   return guarded(c, [&] {
+    mbx::settle(c);
     MBATCH_CHECK(precision >= MBX_PREC_FP32 && precision <= MBX_PREC_BF16, "unknown precision");
     c->precision = precision;
   });
@@ -191,6 +249,7 @@ int mbx_ctx_set_precision(mbx_ctx* c, int precision) {
 
 int mbx_sync(mbx_ctx* c) {
   return guarded(c, [&] {
+    mbx::settle(c);
     if (!c->dry) mbx::cuda_check(cudaStreamSynchronize(c->stream), "sync");
   });
 }
@@ -208,6 +267,7 @@ int64_t mbx_arena_used(const mbx_ctx* c) { return c->used; }
 
 int mbx_arena_upload(mbx_ctx* c, int64_t off, const float* src, int64_t n) {
   return guarded(c, [&] {
+    mbx::settle(c);
     mbx::arena_check(c, off, n);
     ++c->upload_epoch;
     if (c->dry || n == 0) return;
@@ -218,6 +278,7 @@ int mbx_arena_upload(mbx_ctx* c, int64_t off, const float* src, int64_t n) {
 
 int mbx_arena_download(mbx_ctx* c, int64_t off, float* dst, int64_t n) {
   return guarded(c, [&] {
+    mbx::settle(c);
     mbx::arena_check(c, off, n);
     if (c->dry) {
       std::memset(dst, 0, size_t(n) * 4);
@@ -229,8 +290,16 @@ int mbx_arena_download(mbx_ctx* c, int64_t off, float* dst, int64_t n) {
   });
 }
 
+int mbx_arena_device_ptr(mbx_ctx* c, int64_t off, int64_t n, float** out) {
+  return guarded(c, [&] {
+    mbx::arena_check(c, off, n);
+    *out = c->dry ? nullptr : mbx::arena_ptr(c) + off;
+  });
+}
+
 int mbx_arena_rewind(mbx_ctx* c, int64_t used) {
   return guarded(c, [&] {
+    mbx::settle(c);
     MBATCH_CHECK(used >= 0 && used <= c->used, "rewind past the arena end");
     c->used = used;
     c->persist_end = std::min(c->persist_end, used);  // memory above may be reused now
@@ -253,6 +322,16 @@ int mbx_exec_batched(mbx_ctx* c, int plan_id, int b, const int64_t* shared_off, 
         MBATCH_CHECK(shared_off[size_t(i) * ns + s] == shared_off[s],
                      "shared-param handle mismatch across instances (analysis bug)");
     size_t bytes = 8 * (pe.plan.shared_shapes.size() + size_t(b) * pe.plan.batched_shapes.size() * 2 + pe.plan.outputs.size()) + 512;
+    if (c->flush_active) {
+      // Queued: its offset tables stay staged until mbx_flush_end plans the whole sequence (level
+      // tables and operand-image destinations are staged then, so keep room for them too).
+      bytes += 64 /* one level-table entry */ + 16 * size_t(b) + 64;
+      if (c->meta.cursor + bytes > c->meta.cap) mbx::issue_pending(c);  // the ring may recycle now
+      mbx::meta_reserve(c, bytes);
+      c->pending.push_back(
+          mbx::prepare_batch(c, plan_id, b, shared_off, batched_off, gather_mode, out_off, gather_bytes));
+      return;
+    }
     mbx::meta_reserve(c, bytes);
     mbx::BatchLaunch L = mbx::prepare_batch(c, plan_id, b, shared_off, batched_off, gather_mode, out_off, gather_bytes);
     mbx::meta_commit(c);
@@ -260,10 +339,58 @@ int mbx_exec_batched(mbx_ctx* c, int plan_id, int b, const int64_t* shared_off, 
   });
 }
 
+int mbx_flush_begin(mbx_ctx* c) {
+  return guarded(c, [&] {
+    mbx::settle(c);
+    c->flush_active = true;
+  });
+}
+
+int mbx_flush_end(mbx_ctx* c) {
+  return guarded(c, [&] {
+    c->flush_active = false;
+    mbx::settle(c);
+  });
+}
+
+int mbx_read_ints(mbx_ctx* c, const int64_t* offs, int n, int64_t* out) {
+  return guarded(c, [&] {
+    MBATCH_CHECK(n >= 0, "read_ints: negative count");
+    for (int k = 0; k < n; ++k) mbx::arena_check(c, offs[k], 1);
+    mbx::settle(c);
+    if (n == 0) return;
+    if (c->dry) {
+      for (int k = 0; k < n; ++k) out[k] = 0;
+      return;
+    }
+    // One pack kernel + one D2H for every value (executor.cpp:235-238 reads them one by one).
+    std::vector<int64_t> ranges;
+    ranges.reserve(size_t(n) * 3);
+    for (int k = 0; k < n; ++k) {
+      ranges.push_back(offs[k]);
+      ranges.push_back(1);
+      ranges.push_back(k);
+    }
+    mbx::meta_reserve(c, ranges.size() * 8);
+    const size_t meta = mbx::meta_stage(c, ranges.data(), ranges.size() * 8);
+    mbx::meta_commit(c);
+    mbx::ensure_d2h(c, size_t(n));
+    mbx::cuda_check(mbx::launch_pack_ranges(mbx::arena_ptr(c), mbx::meta_dev<int64_t>(c, meta), n, c->d2h_dev, c->stream),
+                    "read_ints pack");
+    ++c->launches;
+    ++mbx::g_launches;
+    mbx::cuda_check(cudaMemcpyAsync(c->d2h_host, c->d2h_dev, size_t(n) * 4, cudaMemcpyDeviceToHost, c->stream),
+                    "read_ints D2H");
+    mbx::cuda_check(cudaStreamSynchronize(c->stream), "read_ints sync");
+    for (int k = 0; k < n; ++k) out[k] = static_cast<long>(c->d2h_host[k]);  // read_scalar_int
+  });
+}
+
 int mbx_exec_primop(mbx_ctx* c, int op, int nin, const int64_t* in_off, const int* in_rows, const int* in_cols,
                     int64_t out_off, int out_rows, int out_cols, float fill) {
   using namespace mbatch::backend;
   return guarded(c, [&] {
+    mbx::settle(c);
     MBATCH_CHECK(op >= 0 && op <= 8, "unknown op");
     OpCode o = OpCode(op);
     std::vector<Shape> shapes;
@@ -380,6 +507,7 @@ int mbx_evaluate_batch(mbx_model* m, int batch, const int32_t* toks, int64_t nto
   *out = nullptr;
   auto res = std::make_unique<mbx_result>();
   int rc = guarded(m->ctx, [&] {
+    mbx::settle(m->ctx);
     MBATCH_CHECK(batch >= 1, "evaluate_batch: need at least one instance");
     // The inputs are materialised straight from the encoding (no HostValue trees; the tensor
     // data is copied once, into pinned staging) and the outputs encoded straight from the run.

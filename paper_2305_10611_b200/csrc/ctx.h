@@ -58,6 +58,27 @@ struct MetaRing {
   size_t cap = 0, cursor = 0, committed = 0;
 };
 
+// One batched launch of a registered plan whose offsets are already staged.
+struct BatchLaunch {
+  int plan_id = -1;
+  int b = 0;
+  size_t shared_meta = 0, batched_meta = 0, out_meta = 0;
+  size_t prefix_out_meta = 0;  // hoisted shared prefix: its output offsets (scratch)
+  // EXPLICIT gathers to run first: (slot size, src offsets meta, dst offset)
+  struct Gather { int size; size_t src_meta; int64_t dst; };
+  std::vector<Gather> gathers;
+  std::vector<BatchLaunch> sub;  // head / tail launches of a split plan
+  unsigned shadow_out = 0;       // pointwise launches: bit k = also write output slot k's shadow
+  int img_slot = -1;             // pointwise launches: output slot scattered into operand images
+  size_t img_dst_meta = 0;       // ... and its per-row destinations (int4, staged)
+};
+
+// One persistent multi-level launch covering launches [start, start + n) of a flush.
+struct LevelsRun {
+  int start = 0, n = 0, groups = 1, cfg = 0;
+  size_t table = 0;
+};
+
 }  // namespace mbx
 
 struct mbx_ctx {
@@ -127,6 +148,11 @@ struct mbx_ctx {
   // the canonical UMMA layout, filled by the producers, loaded by the consumer with bulk copies.
   unsigned char* img_buf = nullptr;
   size_t img_cap = 0;
+  // mbx_flush_begin .. mbx_flush_end: exec_batched calls are prepared (offsets, handles) and
+  // queued, then planned and issued together like a runtime flush (persistent multi-level
+  // launches, operand images).
+  bool flush_active = false;
+  std::vector<mbx::BatchLaunch> pending;
 };
 
 namespace mbx {
@@ -164,26 +190,7 @@ void ensure_input_stage(mbx_ctx* c, size_t floats);
 // Plan registry (backend.cpp).
 int register_plan(mbx_ctx* c, const mbatch::backend::ExecutablePlan& plan);
 
-// One batched launch of a registered plan whose offsets are already staged.
-struct BatchLaunch {
-  int plan_id = -1;
-  int b = 0;
-  size_t shared_meta = 0, batched_meta = 0, out_meta = 0;
-  size_t prefix_out_meta = 0;  // hoisted shared prefix: its output offsets (scratch)
-  // EXPLICIT gathers to run first: (slot size, src offsets meta, dst offset)
-  struct Gather { int size; size_t src_meta; int64_t dst; };
-  std::vector<Gather> gathers;
-  std::vector<BatchLaunch> sub;  // head / tail launches of a split plan
-  unsigned shadow_out = 0;       // pointwise launches: bit k = also write output slot k's shadow
-  int img_slot = -1;             // pointwise launches: output slot scattered into operand images
-  size_t img_dst_meta = 0;       // ... and its per-row destinations (int4, staged)
-};
 
-// One persistent multi-level launch covering launches [start, start + n) of a flush.
-struct LevelsRun {
-  int start = 0, n = 0, groups = 1, cfg = 0;
-  size_t table = 0;
-};
 
 // Host half of exec_batched: validation, gather accounting, reference-order allocation of
 // scratch / output regions / temporaries, staging of offset tables.  Fills `out_off`
@@ -204,6 +211,13 @@ int plan_levels(mbx_ctx* c, const std::vector<BatchLaunch>& Ls, size_t i, size_t
 // rows all have split-bf16 shadows written earlier in the flush (they skip the conversion), and
 // makes those rows' producers (pointwise launches, levels of a run) write the shadows.
 void plan_shadows(mbx_ctx* c, std::vector<BatchLaunch>& Ls, const std::vector<LevelsRun>& runs);
+// Plans and issues the launches queued by mbx_flush_begin .. (exec_batched in flush mode):
+// persistent multi-level runs, operand images / shadows, one offset-table H2D, then the kernels.
+void issue_pending(mbx_ctx* c);
+// Issues queued launches (if any) before an operation that reads or writes the arena.
+inline void settle(mbx_ctx* c) {
+  if (!c->pending.empty()) issue_pending(c);
+}
 // Enqueues that launch (meta committed).
 void issue_levels(mbx_ctx* c, const std::vector<BatchLaunch>& Ls, size_t i, int n, size_t table, int groups,
                   int cfg);

@@ -14,6 +14,7 @@
 #include <coroutine>
 #include <exception>
 #include <functional>
+#include <cstring>
 #include <memory>
 #include <vector>
 
@@ -42,7 +43,7 @@ struct PoolAlloc {
 };
 
 struct Val {
-  enum Kind : uint8_t { kTensor, kInt, kList, kTuple, kAdt };
+  enum Kind : uint8_t { kTensor, kInt, kList, kTuple, kAdt, kFloat };  // kFloat: double bits in i
   Kind kind = kInt;
   int ctor = 0;  // kAdt: 0 Leaf, 1 Node
   long i = 0;
@@ -51,6 +52,8 @@ struct Val {
 
   static Val tensor(TensorRef r) { Val v; v.kind = kTensor; v.t = r; return v; }
   static Val integer(long x) { Val v; v.kind = kInt; v.i = x; return v; }
+  static Val real(double x) { Val v; v.kind = kFloat; std::memcpy(&v.i, &x, sizeof x); return v; }
+  double real_value() const { double x; std::memcpy(&x, &i, sizeof x); return x; }
   static Val seq(Kind k, std::vector<Val> it, int ctor = 0) {
     Val v;
     v.kind = k;

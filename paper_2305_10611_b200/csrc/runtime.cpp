@@ -346,7 +346,7 @@ struct Executor::Impl {
         return Val::tensor(TensorRef{-1, 0, TensorHandle{off, hv.shape}});
       }
       case HostValue::Kind::kInt: return Val::integer(hv.ival);
-      case HostValue::Kind::kFloat: return Val::integer(static_cast<long>(hv.fval));
+      case HostValue::Kind::kFloat: return Val::real(hv.fval);
       case HostValue::Kind::kList: {
         // The reference builds cons cells back to front, so later elements get lower offsets.
         std::vector<Val> items(hv.items.size());
@@ -358,10 +358,29 @@ struct Executor::Impl {
         std::vector<Val> items;
         for (const auto& f : hv.items) items.push_back(materialize(f));
         if (hv.kind == HostValue::Kind::kTuple) return Val::tuple(std::move(items));
-        return Val::seq(Val::kAdt, std::move(items), hv.ctor == "Node" ? 1 : 0);
+        return Val::seq(Val::kAdt, std::move(items), ctor_id(hv.ctor));
       }
     }
     throw Error("unreachable");
+  }
+
+  // The zoo programs' ADTs are binary trees (zoo.cpp): constructors Leaf and Node.
+  static int ctor_id(const std::string& name) {
+    MBATCH_CHECK(name == "Leaf" || name == "Node", "unknown ADT constructor " + name);
+    return name == "Node" ? 1 : 0;
+  }
+  // ADT constructor of the flat encoding (0 Leaf, 1 Node, -1 named: length + bytes).
+  int read_ctor(int64_t& ti) {
+    const int32_t* t = enc->toks;
+    MBATCH_CHECK(ti < enc->ntok, "hostval encoding truncated");
+    const int id = t[ti++];
+    if (id >= 0) return id ? 1 : 0;
+    MBATCH_CHECK(ti < enc->ntok, "hostval encoding truncated");
+    const int len = t[ti++];
+    MBATCH_CHECK(len >= 0 && ti + len <= enc->ntok, "hostval encoding truncated");
+    std::string name;
+    for (int k = 0; k < len; ++k) name.push_back(char(t[ti++]));
+    return ctor_id(name);
   }
 
   // The flat-encoding counterpart of materialize(decode(...)): same arena order (list elements
@@ -376,8 +395,11 @@ struct Executor::Impl {
       ti += 2;
     } else if (kind == 1) {
       ++ti;
+    } else if (kind == 5 || kind == 6) {
+      MBATCH_CHECK(ti + 2 <= enc->ntok, "hostval encoding truncated");
+      ti += 2;
     } else if (kind >= 2 && kind <= 4) {
-      if (kind == 4) ++ti;
+      if (kind == 4) read_ctor(ti);
       MBATCH_CHECK(ti < enc->ntok, "hostval encoding truncated");
       const int n = t[ti++];
       for (int k = 0; k < n; ++k) skip_enc(ti, di);
@@ -401,6 +423,16 @@ struct Executor::Impl {
         return Val::tensor(TensorRef{-1, 0, TensorHandle{off, Shape{r, cc}}});
       }
       case 1: MBATCH_CHECK(ti < enc->ntok, "hostval encoding truncated"); return Val::integer(t[ti++]);
+      case 5:
+      case 6: {
+        MBATCH_CHECK(ti + 2 <= enc->ntok, "hostval encoding truncated");
+        const uint64_t bits = uint64_t(uint32_t(t[ti])) | (uint64_t(uint32_t(t[ti + 1])) << 32);
+        ti += 2;
+        if (kind == 6) return Val::integer(long(int64_t(bits)));
+        double x;
+        std::memcpy(&x, &bits, sizeof x);
+        return Val::real(x);
+      }
       case 2: {
         MBATCH_CHECK(ti < enc->ntok, "hostval encoding truncated");
         const int n = t[ti++];
@@ -422,10 +454,7 @@ struct Executor::Impl {
       case 3:
       case 4: {
         int ctor = 0;
-        if (kind == 4) {
-          MBATCH_CHECK(ti < enc->ntok, "hostval encoding truncated");
-          ctor = t[ti++];
-        }
+        if (kind == 4) ctor = read_ctor(ti);
         MBATCH_CHECK(ti < enc->ntok, "hostval encoding truncated");
         const int n = t[ti++];
         std::vector<Val> items;
@@ -452,8 +481,19 @@ struct Executor::Impl {
         return;
       }
       case Val::kInt:
-        out.toks.push_back(1);
-        out.toks.push_back(int32_t(v.i));
+        if (v.i >= INT32_MIN && v.i <= INT32_MAX) {
+          out.toks.push_back(1);
+          out.toks.push_back(int32_t(v.i));
+        } else {
+          out.toks.push_back(6);
+          out.toks.push_back(int32_t(uint32_t(uint64_t(v.i) & 0xffffffffu)));
+          out.toks.push_back(int32_t(uint32_t(uint64_t(v.i) >> 32)));
+        }
+        return;
+      case Val::kFloat:
+        out.toks.push_back(5);
+        out.toks.push_back(int32_t(uint32_t(uint64_t(v.i) & 0xffffffffu)));
+        out.toks.push_back(int32_t(uint32_t(uint64_t(v.i) >> 32)));
         return;
       default:
         if (v.kind == Val::kList) out.toks.push_back(2);
@@ -959,6 +999,12 @@ struct Executor::Impl {
         return HostValue::tensor(h.shape, std::move(d));
       }
       case Val::kInt: return HostValue::scalar(v.i);
+      case Val::kFloat: {
+        HostValue h;
+        h.kind = HostValue::Kind::kFloat;
+        h.fval = v.real_value();
+        return h;
+      }
       default: {
         std::vector<HostValue> items;
         for (size_t k = 0; k < v.size(); ++k) items.push_back(to_host(v.at(k), buf, cursor, ti, hs));

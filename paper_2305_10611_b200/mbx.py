@@ -60,6 +60,10 @@ def lib() -> ctypes.CDLL:
         "mbx_arena_upload": (I, [P, I64, pF, I64]),
         "mbx_arena_download": (I, [P, I64, pF, I64]),
         "mbx_arena_rewind": (I, [P, I64]),
+        "mbx_arena_device_ptr": (I, [P, I64, I64, ctypes.POINTER(pF)]),
+        "mbx_flush_begin": (I, [P]),
+        "mbx_flush_end": (I, [P]),
+        "mbx_read_ints": (I, [P, pI64, I, pI64]),
         "mbx_plan_register": (I, [P, pI32, I64, ctypes.POINTER(I)]),
         "mbx_exec_batched": (I, [P, I, I, pI64, pI64, I, pI64, pI64]),
         "mbx_exec_primop": (I, [P, I, I, pI64, ctypes.POINTER(I), ctypes.POINTER(I), I64, I, I, F]),
@@ -106,18 +110,11 @@ def lib() -> ctypes.CDLL:
 
 
 def exported_symbols() -> List[str]:
-    """mbx_* functions declared in include/mbx.h (for ABI checks)."""
-    return [s for s in ("mbx_version mbx_kernel_launch_count mbx_ctx_create mbx_ctx_destroy mbx_last_error "
-                        "mbx_ctx_set_precision mbx_sync mbx_arena_alloc mbx_arena_used mbx_arena_upload "
-                        "mbx_arena_download mbx_arena_rewind mbx_plan_register mbx_exec_batched mbx_exec_primop "
-                        "mbx_model_create mbx_model_destroy mbx_model_make_params mbx_model_set_param "
-                        "mbx_model_num_params mbx_model_param_name mbx_model_make_inputs mbx_model_num_sigs "
-                        "mbx_model_sig_name mbx_model_plan_encoding mbx_options_default mbx_evaluate_batch "
-                        "mbx_result_destroy mbx_result_outputs mbx_result_counters mbx_result_batches "
-                        "mbx_result_flush_boundaries mbx_result_nodes mbx_result_timing mbx_result_batch_times "
-                        "mbx_result_host_breakdown mbx_ctx_stream mbx_pool_create mbx_pool_destroy "
-                        "mbx_pool_last_error mbx_pool_set_error mbx_pool_threads mbx_pool_stream mbx_pool_model "
-                        "mbx_pool_run mbx_pool_run_timed").split()]
+    """mbx_* functions declared in include/mbx.h (for ABI checks), parsed from the header."""
+    import re
+    hdr = open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include", "mbx.h")).read()
+    hdr = re.sub(r"/\*.*?\*/", "", hdr, flags=re.S)
+    return sorted(set(re.findall(r"\b(mbx_[a-z0-9_]+)\s*\(", hdr)))
 
 
 def _ptr(a: np.ndarray, ct):
@@ -146,9 +143,19 @@ def decode_hostvals(toks: np.ndarray, data: np.ndarray, count: int) -> list:
         if k == 1:
             v = int(toks[ti]); ti += 1
             return v
+        if k in (5, 6):  # float64 / int64 scalar: two tokens, low word first
+            bits = np.array([toks[ti], toks[ti + 1]], np.int32).view(np.uint32)
+            ti += 2
+            raw = np.array([int(bits[0]) | (int(bits[1]) << 32)], np.uint64)
+            return float(raw.view(np.float64)[0]) if k == 5 else int(raw.view(np.int64)[0])
         ctor = None
         if k == 4:
-            ctor = "Node" if int(toks[ti]) else "Leaf"; ti += 1
+            cid = int(toks[ti]); ti += 1
+            if cid >= 0:
+                ctor = "Node" if cid else "Leaf"
+            else:  # named constructor: length, one token per byte
+                n = int(toks[ti]); ti += 1
+                ctor = bytes(int(x) for x in toks[ti:ti + n]).decode(); ti += n
         n = int(toks[ti]); ti += 1
         items = [one() for _ in range(n)]
         if k == 2:
@@ -175,9 +182,13 @@ def instance_spans(toks: np.ndarray, batch: int) -> List[Tuple[int, int, int, in
             di += int(toks[ti]) * int(toks[ti + 1]); ti += 2
         elif k == 1:
             ti += 1
+        elif k in (5, 6):
+            ti += 2
         else:
             if k == 4:
-                ti += 1
+                cid = int(toks[ti]); ti += 1
+                if cid < 0:
+                    ti += 1 + int(toks[ti])
             n = int(toks[ti]); ti += 1
             for _ in range(n):
                 skip()
@@ -352,6 +363,20 @@ class Context:
         pid = ctypes.c_int()
         self.check(lib().mbx_plan_register(self.h, _ptr(e, ctypes.c_int32), e.size, ctypes.byref(pid)))
         return pid.value
+
+    def flush_begin(self):
+        """Opens a flush scope (mbx_flush_begin): exec_batched calls queue until flush_end."""
+        self.check(lib().mbx_flush_begin(self.h))
+
+    def flush_end(self):
+        self.check(lib().mbx_flush_end(self.h))
+
+    def read_ints(self, offsets: Sequence[int]) -> List[int]:
+        """(long) arena[off] for every offset, one device round trip (mbx_read_ints)."""
+        o = np.ascontiguousarray(offsets, np.int64)
+        out = np.zeros(max(1, o.size), np.int64)
+        self.check(lib().mbx_read_ints(self.h, _ptr(o, ctypes.c_int64), o.size, _ptr(out, ctypes.c_int64)))
+        return [int(x) for x in out[:o.size]]
 
     def stream(self) -> int:
         """cudaStream_t of the context (e.g. for torch.cuda.ExternalStream)."""

@@ -121,3 +121,66 @@ def test_device_context_fails_loudly_without_gpu(mbx):
         pytest.skip("GPU present")
     with pytest.raises(mbx.MbatchError):
         mbx.Context(0)
+
+
+def _reencode(toks, wide_ints=False, named_ctors=False):
+    """Rewrites a hostval token stream with int64 scalars (kind 6) and / or named ADT
+    constructors (kind 4, ctor -1 + bytes) — the encodings the C ABI accepts besides kind 1 and
+    ctor ids 0 / 1 (include/mbx.h)."""
+    import numpy as np
+    out, ti = [], 0
+
+    def one():
+        nonlocal ti
+        k = int(toks[ti]); ti += 1
+        if k == 0:
+            out.extend([0, int(toks[ti]), int(toks[ti + 1])]); ti += 2
+        elif k == 1:
+            v = int(toks[ti]); ti += 1
+            if wide_ints:
+                u = v & 0xFFFFFFFFFFFFFFFF
+                out.extend([6, np.uint32(u & 0xFFFFFFFF).view(np.int32).item(), np.uint32(u >> 32).view(np.int32).item()])
+            else:
+                out.extend([1, v])
+        else:
+            out.append(k)
+            if k == 4:
+                cid = int(toks[ti]); ti += 1
+                if named_ctors:
+                    name = b"Node" if cid else b"Leaf"
+                    out.extend([-1, len(name)] + list(name))
+                else:
+                    out.append(cid)
+            n = int(toks[ti]); ti += 1
+            out.append(n)
+            for _ in range(n):
+                one()
+
+    while ti < len(toks):
+        one()
+    return np.array(out, np.int32)
+
+
+@pytest.mark.parametrize("model", ["treelstm", "drnn", "stackrnn"])
+def test_hostval_wide_ints_and_named_ctors(mbx, model):
+    """int64 scalars and named constructors in the input encoding evaluate exactly like the
+    compact forms (same schedule, same decoded outputs), dry run."""
+    c = mbx.Context(-1, "fp32")
+    m = mbx.Model(c, model, 32)
+    m.make_params(1)
+    t, d = m.make_inputs(2, 4)
+    base = m.evaluate_batch(t, d, 4)
+    for kw in ({"wide_ints": True}, {"named_ctors": True}):
+        r = m.evaluate_batch(_reencode(t, **kw), d, 4)
+        assert [(b.sig, b.size, b.node_ids) for b in r.trace.batches] == \
+            [(b.sig, b.size, b.node_ids) for b in base.trace.batches]
+
+
+def test_hostval_decode_float_and_int64(mbx):
+    import numpy as np
+    bits = np.array([2.5], np.float64).view(np.uint32)
+    big = np.array([-(1 << 40)], np.int64).view(np.uint32)
+    toks = np.array([3, 3, 5, bits[0].view(np.int32), bits[1].view(np.int32), 6, big[0].view(np.int32),
+                     big[1].view(np.int32), 4, -1, 3, ord("F"), ord("o"), ord("o"), 0], np.int32)
+    v = mbx.decode_hostvals(toks, np.zeros(0, np.float32), 1)[0]
+    assert v[0] == 2.5 and v[1] == -(1 << 40) and v[2].ctor == "Foo" and v[2].fields == []
