@@ -704,6 +704,93 @@ static void detect_dense_argmax(PlanEntry& pe) {
   pe.da_out[1] = outs[1];
 }
 
+// MV-RNN's combine cell (proj/src/zoo.cpp:124-136): [dense(B x0, B M0), dense(B x1, B M1),
+// concat of the two, dense(that, S W), optional chain of shared-row add/mul and unaries], whole
+// operands only.  Runs on mv_cell_kernel (exact FP32, every precision).
+static bool detect_mv_cell(PlanEntry& pe, const ExecutablePlan& p) {
+  using mbatch::backend::PlanRef;
+  using mbatch::backend::PlanStep;
+  using RK = PlanRef::Kind;
+  if (p.ghost || p.outputs.size() != 1 || p.steps.size() < 4 || p.steps.size() > 5) return false;
+  auto whole = [](const PlanRef& r) { return r.cols < 0; };
+  auto op_step = [](const PlanStep& s, OpCode op, size_t nin) { return s.kind == PlanStep::Kind::kOp && s.op == op && s.ins.size() == nin; };
+  int K = -1, N = -1;
+  for (int g = 0; g < 2; ++g) {
+    const PlanStep& s = p.steps[size_t(g)];
+    if (!op_step(s, OpCode::kDense, 2)) return false;
+    const PlanRef &x = s.ins[0], &m = s.ins[1];
+    if (x.kind != RK::kBatched || m.kind != RK::kBatched || !whole(x) || !whole(m)) return false;
+    const auto &xs = p.batched_shapes[size_t(x.index)], &ms = p.batched_shapes[size_t(m.index)];
+    if (xs.rows != 1 || xs.cols != ms.rows) return false;
+    if (g == 0) {
+      K = ms.rows;
+      N = ms.cols;
+    } else if (ms.rows != K || ms.cols != N) {
+      return false;
+    }
+    pe.mv_x[g] = x.index;
+    pe.mv_m[g] = m.index;
+  }
+  const PlanStep& cat = p.steps[2];
+  if (!op_step(cat, OpCode::kConcat, 2)) return false;
+  const PlanRef &c0 = cat.ins[0], &c1 = cat.ins[1];
+  if (c0.kind != RK::kTemp || c1.kind != RK::kTemp || !whole(c0) || !whole(c1) || c0.index + c1.index != 1) return false;
+  pe.mv_first = c0.index == 0 ? 0 : 1;
+  const PlanStep& d = p.steps[3];
+  if (!op_step(d, OpCode::kDense, 2)) return false;
+  const PlanRef &a = d.ins[0], &w = d.ins[1];
+  if (a.kind != RK::kTemp || a.index != 2 || !whole(a) || w.kind != RK::kShared || !whole(w)) return false;
+  const auto& ws = p.shared_shapes[size_t(w.index)];
+  if (ws.rows != 2 * N) return false;
+  const int U = ws.cols;
+  pe.mv_w = w.index;
+  pe.mv_nlinks = 0;
+  int last = 3;
+  if (p.steps.size() == 5) {
+    const PlanStep& ch = p.steps[4];
+    if (ch.kind != PlanStep::Kind::kChain || ch.ins.size() != 1 || ch.ins[0].kind != RK::kTemp || ch.ins[0].index != 3 ||
+        !whole(ch.ins[0]) || ch.chain.size() > 4)
+      return false;
+    for (const auto& l : ch.chain) {
+      int rhs = -1;
+      if (l.rhs) {
+        const PlanRef& r = *l.rhs;
+        if (r.kind != RK::kShared || !whole(r) || p.shared_shapes[size_t(r.index)].size() != U) return false;
+        if (l.op != OpCode::kAdd && l.op != OpCode::kMul) return false;
+        rhs = r.index;
+      } else if (l.op != OpCode::kSigmoid && l.op != OpCode::kTanh && l.op != OpCode::kRelu) {
+        return false;
+      }
+      pe.mv_link_op[pe.mv_nlinks] = int(l.op);
+      pe.mv_link_rhs[pe.mv_nlinks] = rhs;
+      ++pe.mv_nlinks;
+    }
+    last = 4;
+  }
+  const PlanRef& o = p.outputs[0];
+  if (o.kind != RK::kTemp || o.index != last || !whole(o)) return false;
+  if (!mv_cell_supported(K, N, U)) return false;
+  pe.mv_k = K;
+  pe.mv_n = N;
+  pe.mv_u = U;
+  return true;
+}
+
+// [add(B0, B1)] over two batched matrices: the MV-RNN matrix add (zoo.cpp:135) that
+// issue_pending folds into the preceding combine-cell launch of the same nodes.
+static bool detect_mv_add(const ExecutablePlan& p) {
+  using mbatch::backend::PlanRef;
+  using mbatch::backend::PlanStep;
+  if (p.ghost || p.steps.size() != 1 || p.outputs.size() != 1 || p.batched_shapes.size() != 2 || !p.shared_shapes.empty()) return false;
+  const PlanStep& s = p.steps[0];
+  if (s.kind != PlanStep::Kind::kOp || s.op != OpCode::kAdd || s.ins.size() != 2) return false;
+  for (const auto& r : s.ins)
+    if (r.kind != PlanRef::Kind::kBatched || r.cols >= 0) return false;
+  if (s.ins[0].index + s.ins[1].index != 1 || !(p.batched_shapes[0] == p.batched_shapes[1])) return false;
+  const PlanRef& o = p.outputs[0];
+  return o.kind == PlanRef::Kind::kTemp && o.index == 0 && o.cols < 0;
+}
+
 int register_plan(mbx_ctx* c, const ExecutablePlan& plan) {
   std::vector<int32_t> enc = mbatch::backend::encode_plan(plan);
   auto it = c->plan_by_enc.find(enc);
@@ -725,7 +812,9 @@ int register_plan(mbx_ctx* c, const ExecutablePlan& plan) {
     for (int64_t s : bsizes) total += s;
     if (!c->dry) cuda_check(cudaMalloc(&pe.prefix_scratch, size_t(total) * sizeof(float)), "prefix scratch");
   }
-  if (!plan.ghost && pe.prefix_plan < 0 && pe.hplan.unit <= 0 && !force_vm_next) {
+  pe.mv = !force_vm_next && pe.prefix_plan < 0 && detect_mv_cell(pe, plan);
+  pe.mv_add = detect_mv_add(plan);
+  if (!plan.ghost && !pe.mv && pe.prefix_plan < 0 && pe.hplan.unit <= 0 && !force_vm_next) {
     ExecutablePlan head, tail;
     std::vector<int> hoo, hbs, tis, too;
     if (split_at_reduction(plan, head, tail, hoo, hbs, tis, too)) {
@@ -940,6 +1029,80 @@ void issue_prefix(mbx_ctx* c, const BatchLaunch& L) {
   }
 }
 
+// The MV-RNN combine cell, and with `add` the next batch's matrix add over the same nodes.
+static void issue_mv(mbx_ctx* c, const BatchLaunch& L, const BatchLaunch* add) {
+  PlanEntry& pe = c->plans[L.plan_id];
+  MvCellLaunch m{};
+  m.arena = arena_ptr(c);
+  m.shared_off = meta_dev<int64_t>(c, L.shared_meta);
+  m.batched_off = meta_dev<int64_t>(c, L.batched_meta);
+  m.b = L.b;
+  m.nb = int(pe.exec_plan.batched_shapes.size());
+  for (int g = 0; g < 2; ++g) {
+    m.x[g] = pe.mv_x[g];
+    m.m[g] = pe.mv_m[g];
+  }
+  m.first = pe.mv_first;
+  m.w = pe.mv_w;
+  m.K = pe.mv_k;
+  m.N = pe.mv_n;
+  m.U = pe.mv_u;
+  m.nlinks = pe.mv_nlinks;
+  for (int l = 0; l < 4; ++l) {
+    m.link_op[l] = pe.mv_link_op[l];
+    m.link_rhs[l] = pe.mv_link_rhs[l];
+  }
+  m.cell_out = meta_dev<int64_t>(c, L.out_meta);
+  m.add_out = add ? meta_dev<int64_t>(c, add->out_meta) : nullptr;
+  // W^T: transposed once per parameter upload when W is a session parameter, else per launch.
+  const int64_t w_off = reinterpret_cast<const int64_t*>(c->meta.host + L.shared_meta)[pe.mv_w];
+  const bool persistent = w_off + int64_t(2) * pe.mv_n * pe.mv_u <= c->persist_end;
+  if (!pe.mv_wt) cuda_check(cudaMalloc(&pe.mv_wt, mv_wt_floats(pe.mv_n, pe.mv_u) * sizeof(float)), "mv W^T");
+  const std::vector<int64_t> key{w_off, int64_t(c->upload_epoch)};
+  const bool fresh = !persistent || pe.mv_wt_key != key;
+  if (fresh) {
+    cuda_check(launch_mv_transpose(arena_ptr(c) + w_off, pe.mv_wt, pe.mv_n, pe.mv_u, c->stream), "mv W^T");
+    ++c->launches;
+    ++g_launches;
+  }
+  pe.mv_wt_key = persistent ? key : std::vector<int64_t>{};
+  m.wt = pe.mv_wt;
+  // PDL (the W^T slice streams in while the previous kernel finishes) unless that kernel wrote
+  // W^T or arbitrary arena tensors.
+  m.pdl = pdl_enabled() && !fresh && c->write_launch != c->launches;
+  cuda_check(launch_mv_cell(m, c->stream), "mv cell");
+  ++c->launches;
+  ++g_launches;
+}
+
+// Whether batch `a` (an [add(B0, B1)] plan) adds exactly the two matrices combine-cell batch `L`
+// reads, node for node (the MV-RNN add one depth after the cell, zoo.cpp:134-135).
+static bool mv_pair(const mbx_ctx* c, const BatchLaunch& L, const BatchLaunch& a) {
+  const PlanEntry& pe = c->plans[L.plan_id];
+  const PlanEntry& pa = c->plans[a.plan_id];
+  if (!pe.mv || !pa.mv_add || a.b != L.b || !L.gathers.empty() || !a.gathers.empty()) return false;
+  if (a.shadow_out != 0 || a.img_slot >= 0) return false;  // a later tensor-core level gathers its rows
+  if (!(pa.plan.batched_shapes[0] == mbatch::backend::Shape{pe.mv_k, pe.mv_n})) return false;
+  const int nb = int(pe.exec_plan.batched_shapes.size());
+  const int64_t* cb = reinterpret_cast<const int64_t*>(c->meta.host + L.batched_meta);
+  const int64_t* ab = reinterpret_cast<const int64_t*>(c->meta.host + a.batched_meta);
+  for (int i = 0; i < L.b; ++i) {
+    const int64_t m0 = cb[int64_t(i) * nb + pe.mv_m[0]], m1 = cb[int64_t(i) * nb + pe.mv_m[1]];
+    const int64_t a0 = ab[2 * int64_t(i)], a1 = ab[2 * int64_t(i) + 1];
+    if (!((a0 == m0 && a1 == m1) || (a0 == m1 && a1 == m0))) return false;  // fp32 + is commutative
+  }
+  return true;
+}
+
+int issue_batches(mbx_ctx* c, const std::vector<BatchLaunch>& Ls, size_t i) {
+  if (!c->dry && i + 1 < Ls.size() && mv_pair(c, Ls[i], Ls[i + 1])) {
+    issue_mv(c, Ls[i], &Ls[i + 1]);
+    return 2;
+  }
+  issue_batch(c, Ls[i]);
+  return 1;
+}
+
 void issue_pending(mbx_ctx* c) {
   std::vector<BatchLaunch> Ls;
   Ls.swap(c->pending);
@@ -966,8 +1129,7 @@ void issue_pending(mbx_ctx* c) {
       issue_levels(c, Ls, i, r.n, r.table, r.groups, r.cfg);
       i += size_t(r.n);
     } else {
-      issue_batch(c, Ls[i]);
-      ++i;
+      i += size_t(issue_batches(c, Ls, i));
     }
   }
 }
@@ -986,6 +1148,10 @@ void issue_batch(mbx_ctx* c, const BatchLaunch& L) {
     return;
   }
   issue_prefix(c, L);
+  if (pe.mv) {
+    issue_mv(c, L, nullptr);
+    return;
+  }
   // tc_kind 2 (pointwise) is exact and runs in every precision; tc_kind 1 (tensor cores) only
   // when the context allows split-bf16 / bf16 contractions.
   // The bit-exact gate kernel runs for small / decision plans in every precision and for every

@@ -209,6 +209,7 @@ void mbx_ctx_destroy(mbx_ctx* c) {
     for (auto& pe : c->plans) {
       if (pe.dplan) cudaFree(pe.dplan);
       if (pe.prefix_scratch) cudaFree(pe.prefix_scratch);
+      if (pe.mv_wt) cudaFree(pe.mv_wt);
       mbx::tc_release(pe);
     }
     if (c->meta.host) cudaFreeHost(c->meta.host);
@@ -406,7 +407,7 @@ int mbx_exec_primop(mbx_ctx* c, int op, int nin, const int64_t* in_off, const in
     if (c->dry) return;
     if (o == OpCode::kFill) {
       mbx::cuda_check(mbx::launch_fill(mbx::arena_ptr(c), out_off, out.size(), fill, c->stream), "fill");
-      ++c->launches;
+      c->write_launch = ++c->launches;
       ++mbx::g_launches;
       return;
     }
@@ -416,7 +417,7 @@ int mbx_exec_primop(mbx_ctx* c, int op, int nin, const int64_t* in_off, const in
     mbx::cuda_check(mbx::launch_primop(mbx::arena_ptr(c), op, in_off[0], in_rows[0], in_cols[0], b_off, br, bc, out_off,
                                        out_rows, out_cols, c->stream),
                     "primop");
-    ++c->launches;
+    c->write_launch = ++c->launches;
     ++mbx::g_launches;
   });
 }

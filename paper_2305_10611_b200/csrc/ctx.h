@@ -45,6 +45,13 @@ struct PlanEntry {
   // kernel (launch_dense_argmax) instead of the general plan VM.  da_out[k]: 0 row, 1 decision.
   bool da = false;
   int da_k = 0, da_n = 0, da_a_batched = 0, da_a_idx = 0, da_w_idx = 0, da_out[2] = {0, 0};
+  // MV-RNN combine cell [x0.M0, x1.M1 per instance, concat, . W, chain] (kernels_mv.cu), and the
+  // per-instance matrix add [B0 + B1] it can absorb when the flush issues the two back to back.
+  bool mv = false, mv_add = false;
+  int mv_x[2] = {0, 0}, mv_m[2] = {0, 0}, mv_first = 0, mv_w = 0, mv_k = 0, mv_n = 0, mv_u = 0;
+  int mv_nlinks = 0, mv_link_op[4] = {0, 0, 0, 0}, mv_link_rhs[4] = {-1, -1, -1, -1};
+  float* mv_wt = nullptr;                   // W^T (launch_mv_transpose)
+  mutable std::vector<int64_t> mv_wt_key;   // {W offset, upload epoch} it holds (session parameters)
   int tc_kind = -1;                  // tensor-core kernel for this plan (kernels_tc.cu), -1 none
   bool tc_small = false;             // gate plan served by the bit-exact kernel in every precision
   bool tc_exact = false;             // the bit-exact CUDA-core gate kernel exists (FP32 contexts use it)
@@ -125,6 +132,9 @@ struct mbx_ctx {
   std::map<std::vector<int32_t>, int> plan_by_enc;
   std::string err;
   int64_t launches = 0;
+  // `launches` right after the last kernel that wrote arbitrary arena tensors (primop / fill): a
+  // kernel issued next must not read shared inputs early under PDL.
+  int64_t write_launch = -1;
   // Bumped by every host write into existing tensors (uploads, primops); tensor-core weight
   // packs made under an older epoch are re-packed.
   uint64_t upload_epoch = 0;
@@ -200,6 +210,9 @@ BatchLaunch prepare_batch(mbx_ctx* c, int plan_id, int b, const int64_t* shared_
                           int64_t* gather_bytes);
 // Device half: enqueues the gather copies and the plan kernel (meta must be committed).
 void issue_batch(mbx_ctx* c, const BatchLaunch& L);
+// Issues Ls[i] — together with Ls[i + 1] in one launch when the two fuse (an MV-RNN combine
+// cell and the matrix add of the same nodes) — and returns how many launches it consumed.
+int issue_batches(mbx_ctx* c, const std::vector<BatchLaunch>& Ls, size_t i);
 void issue_prefix(mbx_ctx* c, const BatchLaunch& L);
 
 // Persistent multi-level launches (kernels_tc.cu): if launches [i, i+n) (n >= 1) are consecutive

@@ -26,6 +26,30 @@ struct VmLaunch {
 };
 
 cudaError_t launch_plan_vm(const VmLaunch& L, cudaStream_t stream);
+
+// MV-RNN combine cell, optionally fused with the next batch's matrix add (kernels_mv.cu).
+struct MvCellLaunch {
+  float* arena;
+  const int64_t* shared_off;   // the cell plan's shared offsets
+  const int64_t* batched_off;  // [b * nb]
+  int b, nb;
+  int x[2], m[2];              // batched slots of the two GEMVs' rows and matrices
+  int first;                   // concat position of x[0] . m[0] (0 or 1)
+  int w;                       // shared slot of the 2N x U weight
+  int K, N, U;
+  int nlinks;
+  int link_op[4], link_rhs[4];  // chain on the dense result; rhs: shared slot of a 1 x U row, -1 none
+  const int64_t* cell_out;      // [1] output region base
+  const int64_t* add_out;       // [1] fused matrix-add output region base, or nullptr
+  int cs;                       // column slices per node (set by launch_mv_cell)
+  int pdl;                      // programmatic dependent launch: W may be read before the wait
+  const float* wt;              // W^T, rows of 2N + 4 floats (launch_mv_transpose)
+};
+size_t mv_wt_floats(int N, int U);
+cudaError_t launch_mv_transpose(const float* w, float* wt, int N, int U, cudaStream_t stream);
+bool pdl_enabled();
+bool mv_cell_supported(int K, int N, int U);
+cudaError_t launch_mv_cell(const MvCellLaunch& L, cudaStream_t stream);
 cudaError_t launch_dense_argmax(float* arena, const int64_t* shared_off, const int64_t* batched_off, int b, int nb,
                                 int a_batched, int a_idx, int w_idx, int K, int N, const int64_t* out_base, int nout,
                                 int out0, int out1, cudaStream_t stream);

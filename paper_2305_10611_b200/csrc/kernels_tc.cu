@@ -706,6 +706,8 @@ void fill_loads(const EpiProg& pr, TcLoad* out) {
   }
 }
 
+}  // namespace
+
 bool pdl_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("MBX_PDL");
@@ -713,8 +715,6 @@ bool pdl_enabled() {
   }();
   return on;
 }
-
-}  // namespace
 
 // The split-bf16 weight pack of a gate plan for the weights at `shared_host` (host copy of a
 // staged shared-offset table); packs on first use and after every parameter upload.

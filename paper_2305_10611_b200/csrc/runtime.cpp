@@ -849,7 +849,7 @@ struct Executor::Impl {
       int64_t before = c->launches;
       for (size_t i = 0; i < launches.size();) {
         const mbx::LevelsRun* run = run_at[i] >= 0 ? &runs[size_t(run_at[i])] : nullptr;
-        const int n = run ? run->n : 1;
+        int n = run ? run->n : 1;
         cudaEvent_t x = nullptr, y = nullptr;
         if (opts.time_batches) {
           cudaEventCreate(&x);
@@ -857,7 +857,7 @@ struct Executor::Impl {
           cudaEventRecord(x, c->stream);
         }
         if (run) mbx::issue_levels(c, launches, i, n, run->table, run->groups, run->cfg);
-        else mbx::issue_batch(c, launches[i]);
+        else n = mbx::issue_batches(c, launches, i);
         if (opts.time_batches) {
           cudaEventRecord(y, c->stream);
           batch_events.push_back({x, y});
