@@ -685,9 +685,9 @@ static void detect_dense_argmax(PlanEntry& pe) {
   const auto& as = a.kind == PlanRef::Kind::kBatched ? p.batched_shapes[size_t(a.index)] : p.shared_shapes[size_t(a.index)];
   const auto& ws = p.shared_shapes[size_t(w.index)];
   if (as.rows != 1 || as.cols != ws.rows || ws.cols < 1 || ws.cols > 32) return;
-  // The kernel stages W and the row in shared memory: (K*N + K + N) floats must fit the opt-in
-  // limit; larger plans keep the plan VM (any K).
-  if ((int64_t(ws.rows) * ws.cols + ws.rows + ws.cols) * 4 > 227 * 1024) return;
+  // The kernel stages W, the row and the transposed products in shared memory; larger plans keep
+  // the plan VM (any K).
+  if (dense_argmax_smem(ws.rows, ws.cols) > 227 * 1024) return;
   int outs[2] = {0, 0};
   for (size_t k = 0; k < p.outputs.size(); ++k) {
     const PlanRef& o = p.outputs[k];
@@ -1164,10 +1164,14 @@ void issue_batch(mbx_ctx* c, const BatchLaunch& L) {
     return;
   }
   if (pe.da) {
+    // PDL (W streams in while the previous kernel finishes) when W is a session parameter and the
+    // previous kernel did not write arena tensors.
+    const int64_t w_off = reinterpret_cast<const int64_t*>(c->meta.host + L.shared_meta)[pe.da_w_idx];
+    const int da_pdl = pdl_enabled() && w_off + int64_t(pe.da_k) * pe.da_n <= c->persist_end && c->write_launch != c->launches;
     cuda_check(launch_dense_argmax(arena, meta_dev<int64_t>(c, L.shared_meta), meta_dev<int64_t>(c, L.batched_meta),
                                    L.b, int(pe.exec_plan.batched_shapes.size()), pe.da_a_batched, pe.da_a_idx,
                                    pe.da_w_idx, pe.da_k, pe.da_n, meta_dev<int64_t>(c, L.out_meta),
-                                   int(pe.exec_plan.outputs.size()), pe.da_out[0], pe.da_out[1], c->stream),
+                                   int(pe.exec_plan.outputs.size()), pe.da_out[0], pe.da_out[1], da_pdl, c->stream),
                "dense + argmax");
     ++c->launches;
     ++g_launches;

@@ -429,32 +429,63 @@ __global__ void fill_kernel(float* arena, int64_t off, int64_t n, float v) {
 // dense + argmax plans (backend.cpp:116-131, :164-173), one CTA per node: the weight (K x N) and
 // the node's row go to shared memory, N threads run the exact sequential chains (p ascending,
 // separately rounded multiply and add), thread 0 takes the first index of the maximum.
+// [dense(a . W), argmax] per node (NestedRNN's decision tail), exact: one CTA per node.  W
+// (K x N, N <= 32) and the row stream into shared memory with cp.async (W before the PDL wait: it
+// is a session parameter whenever PDL is on); every product a[p] * W[p][j] is formed by all
+// threads into a transposed buffer; thread j < N then adds column j's products in p order (the
+// reference's chain, backend.cpp:116-131) with 16-byte loads, and warp 0 takes the argmax (first
+// maximum, backend.cpp:164-173).
 __global__ void __launch_bounds__(256) dense_argmax_kernel(float* arena, const int64_t* shared_off,
                                                            const int64_t* batched_off, int nb, int a_batched, int a_idx,
                                                            int w_idx, int K, int N, const int64_t* out_base, int nout,
-                                                           int out0, int out1) {
-  extern __shared__ float sm[];
-  float* ws = sm;           // [K][N]
-  float* as = sm + K * N;   // [K]
-  float* row = as + K;      // [N]
-  const int node = blockIdx.x;
-  const float* a = arena + (a_batched ? batched_off[int64_t(node) * nb + a_idx] : shared_off[a_idx]);
-  const float* w = arena + shared_off[w_idx];
-  for (int i = threadIdx.x; i < K * N; i += blockDim.x) ws[i] = w[i];
-  for (int i = threadIdx.x; i < K; i += blockDim.x) as[i] = a[i];
+                                                           int out0, int out1, int pdl) {
+  extern __shared__ __align__(16) float sm[];
+  const int KP = (K + 7) & ~3;           // transposed row stride: 16-byte aligned, K + 4 .. K + 7
+  float* ws = sm;                         // [K][N]
+  float* as = ws + ((K * N + 3) & ~3);    // [K]
+  float* pt = as + ((K + 3) & ~3);        // [N][KP]
+  float* row = pt + N * KP;               // [N]
+  const int tid = threadIdx.x;
+  const int64_t node = blockIdx.x;
+  {
+    const float* w = arena + shared_off[w_idx];
+    if ((reinterpret_cast<uintptr_t>(w) & 15) == 0 && (K * N) % 4 == 0) {
+      for (int i = tid; i < K * N / 4; i += 256) cp_async16(ws + 4 * i, w + 4 * i);
+    } else {
+      for (int i = tid; i < K * N; i += 256) cp_async4(ws + i, w + i);
+    }
+  }
+  if (pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
+  {
+    const float* a = arena + (a_batched ? batched_off[node * nb + a_idx] : shared_off[a_idx]);
+    for (int i = tid; i < K; i += 256) cp_async4(as + i, a + i);
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
   __syncthreads();
-  if (int(threadIdx.x) < N) {
-    float acc = 0.0f;
-#pragma unroll 8
-    for (int p = 0; p < K; ++p) acc = fadd(acc, fmul(as[p], ws[p * N + threadIdx.x]));
-    row[threadIdx.x] = acc;
+  for (int p = tid; p < K; p += 256) {
+    const float av = as[p];
+    for (int j = 0; j < N; ++j) pt[j * KP + p] = fmul(av, ws[p * N + j]);
+  }
+  __syncthreads();
+  if (tid < N) {
+    const float* q = pt + tid * KP;
+    float acc = 0.0f;  // the reference zero-fills the output, then accumulates in p order
+    int p = 0;
+#pragma unroll 4
+    for (; p + 4 <= K; p += 4) {
+      const float4 v = *reinterpret_cast<const float4*>(q + p);
+      acc = fadd(fadd(fadd(fadd(acc, v.x), v.y), v.z), v.w);
+    }
+    for (; p < K; ++p) acc = fadd(acc, q[p]);
+    row[tid] = acc;
   }
   __syncthreads();
   const int outs[2] = {out0, out1};
   for (int k = 0; k < nout; ++k) {
     if (outs[k] == 0) {
-      for (int j = threadIdx.x; j < N; j += blockDim.x) arena[out_base[k] + int64_t(node) * N + j] = row[j];
-    } else if (threadIdx.x == 0) {
+      for (int j = tid; j < N; j += 256) arena[out_base[k] + node * N + j] = row[j];
+    } else if (tid == 0) {
       int best = 0;
       for (int i = 1; i < N; ++i)
         if (row[i] > row[best]) best = i;
@@ -463,17 +494,30 @@ __global__ void __launch_bounds__(256) dense_argmax_kernel(float* arena, const i
   }
 }
 
+size_t dense_argmax_smem(int K, int N) {
+  return size_t(((K * N + 3) & ~3) + ((K + 3) & ~3) + N * ((K + 7) & ~3) + N) * sizeof(float);
+}
+
 cudaError_t launch_dense_argmax(float* arena, const int64_t* shared_off, const int64_t* batched_off, int b, int nb,
                                 int a_batched, int a_idx, int w_idx, int K, int N, const int64_t* out_base, int nout,
-                                int out0, int out1, cudaStream_t stream) {
-  const size_t smem = size_t(K * N + K + N) * sizeof(float);
+                                int out0, int out1, int pdl, cudaStream_t stream) {
+  const size_t smem = dense_argmax_smem(K, N);
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(dense_argmax_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
   }
-  dense_argmax_kernel<<<b, 256, smem, stream>>>(arena, shared_off, batched_off, nb, a_batched, a_idx, w_idx, K, N,
-                                                out_base, nout, out0, out1);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(unsigned(b));
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, dense_argmax_kernel, arena, shared_off, batched_off, nb, a_batched, a_idx, w_idx, K, N,
+                            out_base, nout, out0, out1, pdl);
 }
 
 cudaError_t launch_plan_vm(const VmLaunch& L, cudaStream_t stream) {
