@@ -1067,6 +1067,12 @@ static bool pointwise_v4(mbx_ctx* c, const TcState* st, const PlanEntry& pe, con
   return true;
 }
 
+static int ilog2(int x) {
+  int l = 0;
+  while ((1 << (l + 1)) <= x) ++l;
+  return l;
+}
+
 void plan_shadows(mbx_ctx* c, std::vector<BatchLaunch>& Ls, const std::vector<LevelsRun>& runs) {
   // MBX_OPERANDS=convert|shadow: restrict the operand paths (A/B measurements and tests).
   static const int allow = [] {
@@ -1133,7 +1139,8 @@ void plan_shadows(mbx_ctx* c, std::vector<BatchLaunch>& Ls, const std::vector<Le
       const int64_t* bt = reinterpret_cast<const int64_t*>(c->meta.host + L.batched_meta);
       const int nt = tbl[q].nt;
       // -- operand image --
-      bool img_ok = allow >= 2 && st->K < 4096 && kslice < 4096 && nt < 65536 && (st->KC == 16 || st->KC == 32);
+      bool img_ok = allow >= 2 && st->K < 4096 && kslice < 4096 && (kslice & (kslice - 1)) == 0 && nt < 65536 &&
+                    (st->KC == 16 || st->KC == 32);
       cands.clear();
       const int64_t tile_bytes = int64_t(nt) * st->K * 4;
       for (int pc = 0; pc < st->npieces && img_ok; ++pc) {
@@ -1168,7 +1175,7 @@ void plan_shadows(mbx_ctx* c, std::vector<BatchLaunch>& Ls, const std::vector<Le
           cd.d.x = int(uint32_t(uint64_t(base) & 0xffffffffu));
           cd.d.y = int(uint32_t(uint64_t(base) >> 32));
           cd.d.z = (i % nt) | (nt << 16);
-          cd.d.w = k0 | (st->KC << 12) | (kslice << 20);
+          cd.d.w = k0 | (ilog2(st->KC) << 12) | (ilog2(kslice) << 16);
           cands.push_back(cd);
         }
       }
@@ -1259,7 +1266,7 @@ static void report_level_stamps(mbx_ctx* c, const unsigned long long* dev, int n
   std::fprintf(stderr, "levels: %d levels, %d CTAs (cfg %d, %d groups, S=%d, NT<=%d, exchange %s)\n", n, nctas, cfg,
                groups, C.S, C.NT, C.xch ? "L2" : "DSMEM");
   const char* names[] = {"start", "mma_wait", "mma_done", "pushed", "reduced", "tile_end", "ready", "converted",
-                         "g_sync", "g_issued", "g_landed0", "mma_issued", "tmem_stg", "tails", "entry", "-"};
+                         "g_sync", "g_issued", "stored", "mma_issued", "tmem_stg", "tails", "entry", "summed"};
   for (int lv = 0; lv < std::min(n, 63); ++lv) {
     std::fprintf(stderr, "  lv %2d b=%3d nt=%3d sh=%d:", lv, tbl[lv].b, tbl[lv].nt, tbl[lv].shadow);
     for (int k = 0; k < 16; ++k) {

@@ -57,16 +57,17 @@ __device__ __forceinline__ void mbar_arrive_cnt(unsigned long long* bar, unsigne
 // producer row gets an image of its B operands, [tile][K rank][chunk][hi | lo][canonical
 // no-swizzle K-major nt x KC], which the producers fill as they write the rows (split bf16) and
 // the consumer loads with a few bulk copies.  d = {base lo, base hi, p | nt << 16,
-// k0 | KC << 12 | kslice << 20}: the tile's image (byte offset), the consumer column, the
-// consumer's tile width, the piece's first K index, the consumer's K chunk and K slice per rank.
+// k0 | log2 KC << 12 | log2 kslice << 16}: the tile's image (byte offset), the consumer column,
+// the consumer's tile width, the piece's first K index, the consumer's K chunk and K slice per rank
+// (both powers of two: shifts, no divisions in the producers' store loop).
 // Returns the byte offset of column u's hi part; the lo part is *lo_off bytes further.
 __device__ __forceinline__ long long img_addr(const int4 d, int u, int* lo_off) {
   const long long base = (long long)(((unsigned long long)(unsigned)d.y << 32) | (unsigned)d.x);
   const int p = d.z & 0xffff, nt = d.z >> 16;
-  const int k0 = d.w & 0xfff, kc = (d.w >> 12) & 0xff, ks = (d.w >> 20) & 0xfff;
-  const int k = k0 + u, r = k / ks, kr = k - r * ks, j = kr / kc, kk = kr - j * kc;
-  *lo_off = nt * kc * 2;
-  return base + (long long)(r * (ks / kc) + j) * (2 * nt * kc * 2) + (p >> 3) * (kc * 16) + (kk >> 3) * 128 +
+  const int k0 = d.w & 0xfff, lkc = (d.w >> 12) & 0xf, lks = (d.w >> 16) & 0xf;
+  const int k = k0 + u, r = k >> lks, kr = k & ((1 << lks) - 1), j = kr >> lkc, kk = kr & ((1 << lkc) - 1);
+  *lo_off = nt << (lkc + 1);
+  return base + (long long)((r << (lks - lkc)) + j) * (nt << (lkc + 2)) + (p >> 3) * (16 << lkc) + (kk >> 3) * 128 +
          (p & 7) * 16 + (kk & 7) * 2;
 }
 
@@ -884,7 +885,7 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const
             continue;
           }
           mbar_wait(&xraw[j], par);
-          if (j == 0) MBX_LSTAMP_T(64, lv, 10);
+
           if (!L.shadow) {
             unsigned char* xs = xsm + j * xstride;
             for (int g = g0; g < ngroups8; g += MBX_LGATHER / 8) {
@@ -986,9 +987,12 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const
       } else {
         __syncthreads();
       }
-      auto partial = [&](int q, int n, int col) -> float {
-        return q == int(rank) ? stg[(nloc0 + n) * MBX_M + col] : recv[((q < int(rank) ? q : q - 1) * ntr + n) * MBX_M + col];
-      };
+      // Per source rank, the base of its partials of this rank's nodes (own: staging; peers: recv).
+      const float* pq[S];
+#pragma unroll
+      for (int q = 0; q < S; ++q)
+        pq[q] = q == int(rank) ? stg + nloc0 * MBX_M : recv + (q < int(rank) ? q : q - 1) * ntr * MBX_M;
+      auto partial = [&](int q, int n, int col) -> float { return pq[q][n * MBX_M + col]; };
 #else
       // ---- accumulators -> every rank's L2 slots (the own slice too: the reduction then reads
       // all S partials the same way, uniform and branch-free, every load in flight) ----
@@ -1035,15 +1039,19 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const
 #pragma unroll
         for (int gi = 0; gi < MBX_G; ++gi) {
           const int col = gi * MBX_UC + u;
+          // Branch-free: invalid elements read node 0's (in-bounds) partials and are never stored,
+          // so every element's loads issue together.
+          const int nv = valid ? n : 0;
           float pv[S];
 #pragma unroll
-          for (int q = 0; q < S; ++q) pv[q] = valid ? partial(q, n, col) : 0.0f;
+          for (int q = 0; q < S; ++q) pv[q] = partial(q, nv, col);
           float acc = pv[0];
 #pragma unroll
           for (int q = 1; q < S; ++q) acc = acc + pv[q];
           gsum[t][gi] = acc;
         }
       }
+      MBX_LSTAMP(lv, 15);
       // Every element's tail first (independent activation chains the scheduler can interleave),
       // then the stores: a store between two elements would keep their chains apart.
       float ov[MBX_LEPT][MBX_NOUT];
@@ -1092,6 +1100,7 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const
         }
       }
       }
+      MBX_LSTAMP(lv, 10);
 #if MBX_LXCH == 0
       if (S > 1 && tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 #endif
