@@ -791,6 +791,28 @@ static bool detect_mv_add(const ExecutablePlan& p) {
   return o.kind == PlanRef::Kind::kTemp && o.index == 0 && o.cols < 0;
 }
 
+// [concat(whole 1 x c rows, shared or batched)] -> output: concat_rows_kernel.
+static bool detect_concat(PlanEntry& pe, const ExecutablePlan& p) {
+  using mbatch::backend::PlanRef;
+  using mbatch::backend::PlanStep;
+  if (p.ghost || p.steps.size() != 1 || p.outputs.size() != 1) return false;
+  const PlanStep& st = p.steps[0];
+  if (st.kind != PlanStep::Kind::kOp || st.op != OpCode::kConcat || st.ins.size() > 8 || st.out_shape.rows != 1) return false;
+  const PlanRef& o = p.outputs[0];
+  if (o.kind != PlanRef::Kind::kTemp || o.index != 0 || o.cols >= 0) return false;
+  pe.cat_n = 0;
+  for (const auto& r : st.ins) {
+    if (r.cols >= 0 || r.kind == PlanRef::Kind::kTemp) return false;
+    const auto& sh = r.kind == PlanRef::Kind::kBatched ? p.batched_shapes[size_t(r.index)] : p.shared_shapes[size_t(r.index)];
+    if (sh.rows != 1) return false;
+    pe.cat_kind[pe.cat_n] = r.kind == PlanRef::Kind::kBatched ? 1 : 0;
+    pe.cat_idx[pe.cat_n] = r.index;
+    pe.cat_cols[pe.cat_n] = sh.cols;
+    ++pe.cat_n;
+  }
+  return true;
+}
+
 int register_plan(mbx_ctx* c, const ExecutablePlan& plan) {
   std::vector<int32_t> enc = mbatch::backend::encode_plan(plan);
   auto it = c->plan_by_enc.find(enc);
@@ -814,6 +836,7 @@ int register_plan(mbx_ctx* c, const ExecutablePlan& plan) {
   }
   pe.mv = !force_vm_next && pe.prefix_plan < 0 && detect_mv_cell(pe, plan);
   pe.mv_add = detect_mv_add(plan);
+  pe.cat = pe.prefix_plan < 0 && detect_concat(pe, plan);
   if (!plan.ghost && !pe.mv && pe.prefix_plan < 0 && pe.hplan.unit <= 0 && !force_vm_next) {
     ExecutablePlan head, tail;
     std::vector<int> hoo, hbs, tis, too;
@@ -1150,6 +1173,25 @@ void issue_batch(mbx_ctx* c, const BatchLaunch& L) {
   issue_prefix(c, L);
   if (pe.mv) {
     issue_mv(c, L, nullptr);
+    return;
+  }
+  if (pe.cat) {
+    ConcatLaunch cl{};
+    cl.shared_off = meta_dev<int64_t>(c, L.shared_meta);
+    cl.batched_off = meta_dev<int64_t>(c, L.batched_meta);
+    cl.out_base = meta_dev<int64_t>(c, L.out_meta);
+    cl.b = L.b;
+    cl.nb = int(pe.exec_plan.batched_shapes.size());
+    cl.nin = pe.cat_n;
+    cl.width = int(pe.out_shapes[0].cols);
+    for (int k = 0; k < pe.cat_n; ++k) {
+      cl.kind[k] = pe.cat_kind[k];
+      cl.idx[k] = pe.cat_idx[k];
+      cl.cols[k] = pe.cat_cols[k];
+    }
+    cuda_check(launch_concat_rows(arena, cl, c->stream), "concat");
+    ++c->launches;
+    ++g_launches;
     return;
   }
   // tc_kind 2 (pointwise) is exact and runs in every precision; tc_kind 1 (tensor cores) only

@@ -52,6 +52,9 @@ struct PlanEntry {
   int mv_nlinks = 0, mv_link_op[4] = {0, 0, 0, 0}, mv_link_rhs[4] = {-1, -1, -1, -1};
   float* mv_wt = nullptr;                   // W^T (launch_mv_transpose)
   mutable std::vector<int64_t> mv_wt_key;   // {W offset, upload epoch} it holds (session parameters)
+  // [concat of whole rows] plans (BiRNN's output concat): concat_rows_kernel.
+  bool cat = false;
+  int cat_n = 0, cat_kind[8] = {}, cat_idx[8] = {}, cat_cols[8] = {};
   int tc_kind = -1;                  // tensor-core kernel for this plan (kernels_tc.cu), -1 none
   bool tc_small = false;             // gate plan served by the bit-exact kernel in every precision
   bool tc_exact = false;             // the bit-exact CUDA-core gate kernel exists (FP32 contexts use it)

@@ -54,6 +54,15 @@ cudaError_t launch_dense_argmax(float* arena, const int64_t* shared_off, const i
                                 int a_batched, int a_idx, int w_idx, int K, int N, const int64_t* out_base, int nout,
                                 int out0, int out1, int pdl, cudaStream_t stream);
 size_t dense_argmax_smem(int K, int N);
+// [concat(rows...)] plans: out row i = the whole rows r_k(i) side by side (kernels_vm.cu).
+struct ConcatLaunch {
+  const int64_t* shared_off;
+  const int64_t* batched_off;
+  const int64_t* out_base;  // [1]
+  int b, nb, nin, width;
+  int kind[8], idx[8], cols[8];  // kind 1 batched, 0 shared
+};
+cudaError_t launch_concat_rows(float* arena, const ConcatLaunch& L, cudaStream_t stream);
 cudaError_t launch_gather_rows(float* arena, const int64_t* src_off, int64_t dst_off, int b, int size,
                                cudaStream_t stream);
 cudaError_t launch_scatter_ranges(const float* src, const int64_t* ranges, int n, float* arena, cudaStream_t stream);

@@ -340,6 +340,27 @@ __global__ void __launch_bounds__(256) plan_vm_kernel(VmLaunch L) {
 
 // EXPLICIT gather (exec_batched.cpp:46-65): copy each instance's batched slot into a
 // contiguous scratch region.
+// [concat(rows...)] plans (BiRNN's output concat, zoo.cpp:47-76): out[i] = [r_0(i) | r_1(i) | ...]
+// for whole 1 x c_k rows (batched: per node; shared: the same row for every node).  A block per
+// node row; 16-byte copies when a piece and its destination are both 16-byte aligned.
+__global__ void __launch_bounds__(256) concat_rows_kernel(float* arena, ConcatLaunch L) {
+  const int64_t i = blockIdx.x;
+  float* out = arena + L.out_base[0] + i * L.width;
+  int col = 0;
+  for (int k = 0; k < L.nin; ++k) {
+    const int c = L.cols[k];
+    const float* src = arena + (L.kind[k] == 1 ? L.batched_off[i * L.nb + L.idx[k]] : L.shared_off[L.idx[k]]);
+    float* dst = out + col;
+    if (((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0 && (c & 3) == 0) {
+      for (int e = threadIdx.x; e < (c >> 2); e += blockDim.x)
+        reinterpret_cast<float4*>(dst)[e] = reinterpret_cast<const float4*>(src)[e];
+    } else {
+      for (int e = threadIdx.x; e < c; e += blockDim.x) dst[e] = src[e];
+    }
+    col += c;
+  }
+}
+
 __global__ void gather_rows_kernel(float* arena, const int64_t* src_off, int64_t dst_off, int b,
                                    int size) {
   const int64_t total = int64_t(b) * size;
@@ -532,6 +553,11 @@ cudaError_t launch_plan_vm(const VmLaunch& L, cudaStream_t stream) {
   if (attr != cudaSuccess) return attr;
   dim3 grid((L.b + L.tm - 1) / L.tm, L.nsplit);
   plan_vm_kernel<<<grid, L.threads, L.smem_bytes, stream>>>(L);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_concat_rows(float* arena, const ConcatLaunch& L, cudaStream_t stream) {
+  concat_rows_kernel<<<L.b, 128, 0, stream>>>(arena, L);
   return cudaGetLastError();
 }
 

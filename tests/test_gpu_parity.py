@@ -270,3 +270,29 @@ def test_mv_cell_registered_plan_bitwise(gpu, h, b, fused, misalign):
         assert np.array_equal(got.view(np.uint32), want.view(np.uint32)), ("cell", i)
         got, want = ctx.download(int(mout[i, 0]), h * h), ctx.download(t6, h * h)
         assert np.array_equal(got.view(np.uint32), want.view(np.uint32)), ("add", i)
+
+
+@pytest.mark.parametrize("misalign", [False, True])
+def test_concat_registered_plan_bitwise(gpu, misalign):
+    """BiRNN's output concat (zoo.cpp:47-76) registered and issued through mbx_exec_batched runs
+    on concat_rows_kernel: == exec_primop concat per node, bitwise, 16-byte aligned or not."""
+    mbx = gpu
+    rng = np.random.default_rng(5)
+    h, b = 96, 45
+    ctx = mbx.Context(0, "fp32")
+    model = mbx.Model(ctx, "birnn", h)
+    pid = ctx.register_plan(model.plan_encoding(model.signatures().index("concat")))
+    rows = []
+    for i in range(b):
+        if misalign:
+            ctx.alloc(1, 1 + i % 3)
+        rows.append((ctx.tensor(rng.uniform(-1, 1, (1, h)))[0], ctx.tensor(rng.uniform(-1, 1, (1, h)))[0]))
+    n0 = mbx.lib().mbx_kernel_launch_count()
+    out, _ = ctx.exec_batched(pid, [], np.array(rows, np.int64), 1)
+    ctx.sync()
+    assert mbx.lib().mbx_kernel_launch_count() - n0 == 1
+    for i, (f, bk) in enumerate(rows):
+        t = ctx.alloc(1, 2 * h)
+        ctx.exec_primop("concat", [(f, (1, h)), (bk, (1, h))], (t, (1, 2 * h)))
+        got, want = ctx.download(int(out[i, 0]), 2 * h), ctx.download(t, 2 * h)
+        assert np.array_equal(got.view(np.uint32), want.view(np.uint32)), i
