@@ -269,6 +269,12 @@ def run_ours(args):
     dist = None
     if world > 1:
         import torch.distributed as dist
+        # NCCL's init lines (ranks, transports) on stderr, so the rank count can be checked; the
+        # JSON line stays alone on stdout.  NCCL only carries the start barrier and the final
+        # max / sum of the timings: nothing on the data path.
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         torch.cuda.set_device(local)
         dist.init_process_group("nccl")
     from paper_2305_10611_b200 import mbx
@@ -406,6 +412,13 @@ def run_ours(args):
         "clocks": clk,
         "parity": pool_res["parity"],
     }
+    # Whether this rank's host workers can feed its GPU: each needs host_ms of CPU per mini-batch
+    # (DFG + scheduling + launch, the latency run's host split), the GPU ~ms_per_step / minibatches.
+    host_ms = rA.timing.host_dfg_us / 1e3
+    dev_mb_ms = pool_res["ms_per_step"] / max(1, pool_res["threads"] * pool_res["per_thread"])
+    line["host_capacity"] = {"cores_per_rank": pool_res["cores"], "workers": pool_res["threads"],
+                             "host_ms_per_minibatch": host_ms, "device_ms_per_minibatch": dev_mb_ms,
+                             "keeps_up": pool_res["threads"] / host_ms >= 1.0 / dev_mb_ms}
     if world == 1 and not args.no_other_configs:
         line["other_configs"] = other_configs(mbx, torch, local)
     if world == 1 and not args.no_cpu_baseline:
@@ -541,7 +554,7 @@ def run_pool(args, mbx, torch, local, rank, world, nodes, l2):
         dev_ms, e2e_ms, n1, n2 = float(mx[0]), float(mx[1]), float(tot[2]), float(tot[3])
     pool.close()
     return {"value": n1 / (dev_ms / 1e3), "e2e": n2 / (e2e_ms / 1e3), "ms_per_step": dev_ms / args.steps,
-            "e2e_ms_per_step": e2e_ms / args.steps, "threads": T, "per_thread": args.per_thread,
+            "e2e_ms_per_step": e2e_ms / args.steps, "threads": T, "cores": cores, "per_thread": args.per_thread,
             "launches": int(launches), "parity": parity}
 
 
