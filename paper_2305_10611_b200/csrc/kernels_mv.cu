@@ -120,11 +120,11 @@ __device__ __forceinline__ void copy_rows(float* dst, const float* src, int rows
 // The fused matrix add over this CTA's column slice: out = M1 + M0 (fp32 + is commutative, so
 // this equals the reference's lm + rm).
 __device__ __forceinline__ void mv_add_slice(const MvCellLaunch& A, const float* ms, int64_t node, int s, int K, int N,
-                                             int NC, int tid) {
+                                             int NC, int tid, int nthr) {
   float* out = A.arena + A.add_out[0] + node * int64_t(K) * N + s * NC;
   const int64_t ob = A.add_out[0] + node * int64_t(K) * N + s * NC;
-  if ((ob & 3) == 0 && (N & 3) == 0 && (NC & 3) == 0 && kMvThreads % (NC >> 2) == 0) {
-    const int q = NC >> 2, c4 = (tid % q) * 4, step = kMvThreads / q;
+  if ((ob & 3) == 0 && (N & 3) == 0 && (NC & 3) == 0 && nthr % (NC >> 2) == 0) {
+    const int q = NC >> 2, c4 = (tid % q) * 4, step = nthr / q;
 #pragma unroll 4
     for (int r = tid / q; r < K; r += step) {
       const float4 a = *reinterpret_cast<const float4*>(ms + r * NC + c4);
@@ -133,11 +133,51 @@ __device__ __forceinline__ void mv_add_slice(const MvCellLaunch& A, const float*
           make_float4(fadd(b.x, a.x), fadd(b.y, a.y), fadd(b.z, a.z), fadd(b.w, a.w));
     }
   } else {
-    for (int i = tid; i < K * NC; i += kMvThreads) {
+    for (int i = tid; i < K * NC; i += nthr) {
       const int r = i / NC, c = i - r * NC;
       out[int64_t(r) * N + c] = fadd(ms[(K + r) * NC + c], ms[r * NC + c]);
     }
   }
+}
+
+// acc = 0; acc = acc + x[r] * m[r * stride] for r = 0 .. n-1: the reference's sequential chain.
+// Products of a block of 16 steps are formed first (independent loads and multiplies), then added
+// in order, so the chain waits on the adds, not on every shared-memory load.
+__device__ __forceinline__ float chain_dot(const float* x, const float* m, int stride, int n) {
+  float acc = 0.0f;
+  int r = 0;
+  for (; r + 16 <= n; r += 16) {
+    float p[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) p[k] = fmul(x[r + k], m[(r + k) * stride]);
+#pragma unroll
+    for (int k = 0; k < 16; ++k) acc = fadd(acc, p[k]);
+  }
+  for (; r < n; ++r) acc = fadd(acc, fmul(x[r], m[r * stride]));
+  return acc;
+}
+
+// The same chain over a contiguous, 16-byte aligned m and x: 16-byte loads.
+__device__ __forceinline__ float chain_dot4(const float* x, const float* m, int n) {
+  float acc = 0.0f;
+  const float4* x4 = reinterpret_cast<const float4*>(x);
+  const float4* m4 = reinterpret_cast<const float4*>(m);
+  int r = 0;
+  for (; r + 16 <= n; r += 16) {
+    float p[16];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float4 a = x4[(r >> 2) + k], b = m4[(r >> 2) + k];
+      p[4 * k] = fmul(a.x, b.x);
+      p[4 * k + 1] = fmul(a.y, b.y);
+      p[4 * k + 2] = fmul(a.z, b.z);
+      p[4 * k + 3] = fmul(a.w, b.w);
+    }
+#pragma unroll
+    for (int k = 0; k < 16; ++k) acc = fadd(acc, p[k]);
+  }
+  for (; r < n; ++r) acc = fadd(acc, fmul(x[r], m[r]));
+  return acc;
 }
 
 // W (2N x U, row-major) -> W^T rows of 2N + 4 floats (column j contiguous, 16-byte aligned).
@@ -180,26 +220,15 @@ __global__ void __launch_bounds__(kMvThreads) mv_cell_kernel(const __grid_consta
   __syncthreads();
   MV_STAMP(2);
   if (CS > 1) asm volatile("barrier.cluster.wait.aligned;" ::: "memory");  // every peer runs: DSMEM is live
-  // ---- the fused matrix add, then T0 / T1: products in place, then the chains ----
-  if (A.add_out) mv_add_slice(A, ms, node, s, K, N, NC, tid);
-  __syncthreads();
-  MV_STAMP(4);
-  if (kMvThreads % NC == 0) {  // thread: one column, every (256 / NC)-th row (no division in the loop)
-    const int c = tid % NC, step = kMvThreads / NC;
-#pragma unroll 8
-    for (int gr = tid / NC; gr < 2 * K; gr += step) ms[gr * NC + c] = fmul(xs[gr], ms[gr * NC + c]);
-  } else {
-    for (int i = tid; i < 2 * K * NC; i += kMvThreads) ms[i] = fmul(xs[i / NC], ms[i]);
-  }
-  __syncthreads();
-  MV_STAMP(7);
+  // ---- T0 / T1 chains (warps holding threads [0, 2 NC)) and, beside them on the other warps,
+  // the fused matrix add ----
+  const int cthr = (2 * NC + 31) & ~31;  // threads of the chain warps
+  const bool add_beside = A.add_out && kMvThreads - cthr >= 32;
+  if (A.add_out && add_beside && tid >= cthr) mv_add_slice(A, ms, node, s, K, N, NC, tid - cthr, kMvThreads - cthr);
   if (tid < 2 * NC) {
     const int g = tid / NC, j = tid - g * NC;
-    // The reference zero-fills the dense output, then accumulates the products in row order.
-    const float* pp = ms + g * K * NC + j;
-    float acc = 0.0f;
-#pragma unroll 16
-    for (int r = 0; r < K; ++r) acc = fadd(acc, pp[r * NC]);
+    // The reference zero-fills the dense output, then accumulates in row order.
+    const float acc = chain_dot(xs + g * K, ms + g * K * NC + j, NC, K);
     const int pos = (g == 0 ? A.first : 1 - A.first) * N + s * NC + j;  // column of T2
     if (CS > 1) {
       const unsigned local = unsigned(__cvta_generic_to_shared(t2 + pos));
@@ -213,6 +242,10 @@ __global__ void __launch_bounds__(kMvThreads) mv_cell_kernel(const __grid_consta
     }
   }
   MV_STAMP(3);
+  if (A.add_out && !add_beside) {
+    __syncthreads();
+    mv_add_slice(A, ms, node, s, K, N, NC, tid, kMvThreads);
+  }
   if (CS > 1) {
     // Every slice of T2 is in every peer's shared memory (release / acquire at cluster scope).
     asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
@@ -220,28 +253,11 @@ __global__ void __launch_bounds__(kMvThreads) mv_cell_kernel(const __grid_consta
   } else {
     __syncthreads();
   }
-  // T3's products in place over this CTA's W^T slice, then column tid's chain.
-  for (int p = tid; p < 2 * N; p += kMvThreads) {
-    const float t = t2[p];
-#pragma unroll 8
-    for (int j = 0; j < UC; ++j) ws[j * (2 * N + 4) + p] = fmul(t, ws[j * (2 * N + 4) + p]);
-  }
-  __syncthreads();
   MV_STAMP(5);
-  // ---- T3 = T2 . W (this CTA's UC columns) and the chain ----
+  // ---- T3 = T2 . W (this CTA's UC columns, W^T rows contiguous) and the chain ----
   if (tid < UC) {
-    const float* pr = ws + tid * (2 * N + 4);
-    float v = 0.0f;
-    if ((N & 1) == 0) {
-      const float4* p4 = reinterpret_cast<const float4*>(pr);
-#pragma unroll 8
-      for (int q = 0; q < (N >> 1); ++q) {
-        const float4 b = p4[q];
-        v = fadd(fadd(fadd(fadd(v, b.x), b.y), b.z), b.w);
-      }
-    } else {
-      for (int p = 0; p < 2 * N; ++p) v = fadd(v, pr[p]);
-    }
+    const float* wr = ws + tid * (2 * N + 4);
+    float v = (N & 1) == 0 ? chain_dot4(t2, wr, 2 * N) : chain_dot(t2, wr, 1, 2 * N);
     const int col = s * UC + tid;
     for (int l = 0; l < A.nlinks; ++l) {
       const float rhs = A.link_rhs[l] >= 0 ? A.arena[A.shared_off[A.link_rhs[l]] + col] : 0.0f;
