@@ -579,6 +579,14 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_gate(const _
 #define MBX_LLOC (((MBX_LNT / 8 + MBX_LS - 1) / MBX_LS) * 8)  // 8-node chunks c with c % S == rank
 #endif
 #define MBX_LEPT ((MBX_LLOC * MBX_UC + MBX_THREADS - 1) / MBX_THREADS)
+// Elements are handed out in pairs of consecutive units of one node when the tile allows it, so
+// the partial sums load 8 bytes per (gate, rank) (half the load instructions) while every thread
+// still gets a share of the tail.
+#if MBX_UC % 2 == 0 && MBX_LEPT % 2 == 0
+#define MBX_LQ 2
+#else
+#define MBX_LQ 1
+#endif
 #define MBX_READY_STRIDE 32  // readiness counters one 128-byte line apart
 #ifdef MBX_STAMPS
 #define MBX_LSTAMP_T(t, lv, i)                                                                      \
@@ -616,6 +624,21 @@ __device__ __forceinline__ void spin_until(const unsigned* ctr, unsigned target)
   const unsigned long long t0 = global_ns();
   while (int(ld_acquire_u32(ctr) - target) < 0)
     if (global_ns() - t0 > 2000000000ull) __trap();
+}
+// Partials: shared memory (exchange through DSMEM) or L2 (.cg: written by other SMs this launch).
+__device__ __forceinline__ float ld_partial(const float* p) {
+#if MBX_LXCH == 0
+  return *p;
+#else
+  return __ldcg(p);
+#endif
+}
+__device__ __forceinline__ float2 ld_partial2(const float* p) {
+#if MBX_LXCH == 0
+  return *reinterpret_cast<const float2*>(p);
+#else
+  return __ldcg(reinterpret_cast<const float2*>(p));
+#endif
 }
 // Split-bf16 shadow of one output element at arena float offset o: bytes [4g, 4g + 16) of the
 // shadow hold the 8 bf16 "hi" parts of the 8-float group g = o & ~7, bytes [4g + 16, 4g + 32)
@@ -779,6 +802,16 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const
       const int nloc = ((nt / 8 + S - 1) / S) * 8;  // this tile's node slots of the rank (<= MBX_LLOC)
       auto loc_col = [&](int m) { return (((m >> 3) * S + int(rank)) << 3) + (m & 7); };
 #endif
+      // Element t of this thread: node n (of the rank's slots) and unit u; its linear index
+      // n * UC + u is quad * LQ + t % LQ with quad = tid + (t / LQ) * THREADS.
+      auto elem = [&](int t, int& n, int& u) {
+        constexpr int w = MBX_UC / MBX_LQ;
+        const int qd = tid + (t / MBX_LQ) * MBX_THREADS;
+        n = qd / w;
+        u = (qd - n * w) * MBX_LQ + t % MBX_LQ;
+      };
+      // Whether element block t / LQ holds any element of this tile (warp-uniform).
+      auto any_elem = [&](int t) { return (t / MBX_LQ) * MBX_THREADS * MBX_LQ < nloc * MBX_UC; };
       // ---- tail operands of the nodes this rank finishes: into registers, in flight during the
       // gather and the MMAs (warps 0-1 now, the gather warps once their copies are issued) ----
       float lreg[MBX_LEPT][MBX_NLOADS > 0 ? MBX_NLOADS : 1];
@@ -786,11 +819,11 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const
       auto load_tail_operands = [&]() {
 #pragma unroll
         for (int t = 0; t < MBX_LEPT; ++t) {
-          const int e = tid + t * MBX_THREADS;
-          const int n = e / MBX_UC, u = e - n * MBX_UC;
+          int n, u;
+          elem(t, n, u);
           const bool valid = n < nloc && loc_col(n) < nn;
           const long long node = node0 + loc_col(n);
-          if (t * MBX_THREADS >= nloc * MBX_UC) break;  // warp-uniform: no element of this tile
+          if (!any_elem(t)) break;  // warp-uniform: no element of this tile
 #pragma unroll
           for (int j = 0; j < MBX_NLOADS; ++j) {
             const TcLoad& l = P.loads[j];
@@ -992,7 +1025,7 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const
 #pragma unroll
       for (int q = 0; q < S; ++q)
         pq[q] = q == int(rank) ? stg + nloc0 * MBX_M : recv + (q < int(rank) ? q : q - 1) * ntr * MBX_M;
-      auto partial = [&](int q, int n, int col) -> float { return pq[q][n * MBX_M + col]; };
+      auto pptr = [&](int q, int n, int col) -> const float* { return pq[q] + n * MBX_M + col; };
 #else
       // ---- accumulators -> every rank's L2 slots (the own slice too: the reduction then reads
       // all S partials the same way, uniform and branch-free, every load in flight) ----
@@ -1022,33 +1055,46 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const
         if (tid == 0) spin_until(flags + rank, unsigned(S - 1) * (it + 1));
         __syncthreads();
       }
-      auto partial = [&](int q, int n, int col) -> float {
-        return __ldcg(pbase + ((size_t)(int(rank) * S + q) * MBX_LLOC + n) * MBX_M + col);
+      auto pptr = [&](int q, int n, int col) -> const float* {
+        return pbase + ((size_t)(int(rank) * S + q) * MBX_LLOC + n) * MBX_M + col;
       };
 #endif
       MBX_LSTAMP(lv, 4);
       // ---- sum the partials in rank order, run the tail, write the outputs ----
       // Every partial of every element is read before the first output store: through generic
       // pointers a store would order all later loads behind it (one L2 round trip per element).
+      // Branch-free: invalid elements read node 0's (in-bounds) partials and are never stored, so
+      // every element's loads issue together.
       float gsum[MBX_LEPT][MBX_G];
 #pragma unroll
-      for (int t = 0; t < MBX_LEPT; ++t) {
-        const int e = tid + t * MBX_THREADS;
-        const int n = e / MBX_UC, u = e - n * MBX_UC;
-        const bool valid = n < nloc && loc_col(n) < nn;
+      for (int t = 0; t < MBX_LEPT; t += MBX_LQ) {
+        int n, u;
+        elem(t, n, u);  // the quad's first element
+        const int nv = (n < nloc && loc_col(n) < nn) ? n : 0;
 #pragma unroll
         for (int gi = 0; gi < MBX_G; ++gi) {
           const int col = gi * MBX_UC + u;
-          // Branch-free: invalid elements read node 0's (in-bounds) partials and are never stored,
-          // so every element's loads issue together.
-          const int nv = valid ? n : 0;
+#if MBX_LQ == 2
+          float2 pv[S];
+#pragma unroll
+          for (int q = 0; q < S; ++q) pv[q] = ld_partial2(pptr(q, nv, col));
+          float2 acc = pv[0];
+#pragma unroll
+          for (int q = 1; q < S; ++q) {
+            acc.x = acc.x + pv[q].x;
+            acc.y = acc.y + pv[q].y;
+          }
+          gsum[t][gi] = acc.x;
+          gsum[t + 1][gi] = acc.y;
+#else
           float pv[S];
 #pragma unroll
-          for (int q = 0; q < S; ++q) pv[q] = partial(q, nv, col);
+          for (int q = 0; q < S; ++q) pv[q] = ld_partial(pptr(q, nv, col));
           float acc = pv[0];
 #pragma unroll
           for (int q = 1; q < S; ++q) acc = acc + pv[q];
           gsum[t][gi] = acc;
+#endif
         }
       }
       MBX_LSTAMP(lv, 15);
@@ -1057,14 +1103,14 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const
       float ov[MBX_LEPT][MBX_NOUT];
 #pragma unroll
       for (int t = 0; t < MBX_LEPT; ++t)
-        if (t * MBX_THREADS < nloc * MBX_UC) mbx_tail(gsum[t], lreg[t], ov[t]);
+        if (any_elem(t)) mbx_tail(gsum[t], lreg[t], ov[t]);
       MBX_LSTAMP(lv, 13);
       const unsigned smask = L.shadow_out;
       if (smask == 0 && L.img_slot < 0) {  // plain outputs (warp-uniform)
 #pragma unroll
         for (int t = 0; t < MBX_LEPT; ++t) {
-          const int e = tid + t * MBX_THREADS;
-          const int n = e / MBX_UC, u = e - n * MBX_UC;
+          int n, u;
+          elem(t, n, u);
           if (n < nloc && loc_col(n) < nn) {
             const long long node = node0 + loc_col(n);
 #pragma unroll
@@ -1074,8 +1120,8 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const
       } else {
 #pragma unroll
       for (int t = 0; t < MBX_LEPT; ++t) {
-        const int e = tid + t * MBX_THREADS;
-        const int n = e / MBX_UC, u = e - n * MBX_UC;
+        int n, u;
+        elem(t, n, u);
         if (n < nloc && loc_col(n) < nn) {
           const long long node = node0 + loc_col(n);
           const int ug = tile_u * MBX_UC + u;
