@@ -167,6 +167,22 @@ __device__ __forceinline__ void tmem_ld8(unsigned addr, float* v) {
   for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// 32 consecutive accumulator columns of this warp's 32 lanes, one wait.
+__device__ __forceinline__ void tmem_ld32(unsigned addr, float* v) {
+  unsigned r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,"
+      "%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(addr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
 __device__ __forceinline__ unsigned pack_bf16x2(float lo_elem, float hi_elem) {
   unsigned r;
   asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi_elem), "f"(lo_elem));
@@ -1032,16 +1048,24 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const
       // part layout: [tile parity][group][unit tile][destination rank][source rank][LLOC][128]
       float* pbase = P.part + ((size_t)(par * ngrp + grp) * gridDim.y + tile_u) * S * S * MBX_LLOC * MBX_M;
       {
-        // Warp w reads TMEM lanes 32*(w%4).. (gate rows) for every other 8-column chunk.
+        // Warp w reads TMEM lanes 32*(w%4).. (gate rows), every other 32-column block in one load
+        // (one wait per 4 chunks of 8 nodes).
         const int q = warp & 3, half = warp >> 2;
         const int row = q * 32 + lane;
-        for (int ch = half; ch < (nn + 7) >> 3; ch += 2) {
-          float v[8];
-          tmem_ld8(tmem + (unsigned(q * 32) << 16) + unsigned(ch * 8), v);
-          const int r = ch % S, m0 = (ch / S) * 8;
-          float* dst = pbase + ((size_t)(r * S + int(rank)) * MBX_LLOC + m0) * MBX_M + row;
+        const int nch = (nn + 7) >> 3;
+        for (int c0 = half * 32; c0 < nch * 8; c0 += 64) {
+          float v[32];
+          tmem_ld32(tmem + (unsigned(q * 32) << 16) + unsigned(c0), v);
 #pragma unroll
-          for (int k = 0; k < 8; ++k) __stcg(dst + k * MBX_M, v[k]);
+          for (int i = 0; i < 4; ++i) {
+            const int ch = (c0 >> 3) + i;
+            if (ch < nch) {
+              const int r = ch % S, m0 = (ch / S) * 8;
+              float* dst = pbase + ((size_t)(r * S + int(rank)) * MBX_LLOC + m0) * MBX_M + row;
+#pragma unroll
+              for (int k = 0; k < 8; ++k) __stcg(dst + k * MBX_M, v[8 * i + k]);
+            }
+          }
         }
       }
       MBX_LSTAMP(lv, 12);
