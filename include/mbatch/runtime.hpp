@@ -125,6 +125,10 @@ struct CompiledModel {
   std::vector<int> stage_phase;    // main stage -> phase
   std::shared_ptr<const Program> program;
   ExecOptions opts;
+  // analysis::static_nesting_estimate of the model's functions (analysis.cpp:1293-1324): the
+  // entry 0, a callee in another call-graph SCC its caller's level (+1 when it recurses); the
+  // zoo programs carry their modules' values.
+  std::map<std::string, int> nesting;
 };
 
 struct TensorRef {
@@ -253,6 +257,24 @@ class Session {
 // reference materialising them per Executor).
 EvalResult evaluate_batch(const CompiledModel& model, const ParamEnv& params,
                           const std::vector<InstanceInput>& inputs);
+
+// Unbatched evaluation (the reference's sequential oracle entry point, runtime.hpp:141-144):
+// every instance evaluated on its own, one instance per mini-batch, on the device; outputs equal
+// evaluate_batch's bit for bit in FP32 (the reference's batched == unbatched property).
+std::vector<HostValue> reference_evaluate(const CompiledModel& model, const ParamEnv& params,
+                                          const std::vector<InstanceInput>& inputs);
+
+// Exact invocation counts per kernel signature over a sample run, plus the static nesting-depth
+// estimate for comparison; ranked by count (pipeline.cpp:99-123).
+struct ProfileReport {
+  std::map<int, long> counts;          // sig id -> invocations (non-ghost DFG nodes)
+  std::map<int, int> static_estimate;  // sig id -> nesting level of its blocks' functions (max)
+  std::vector<int> ranking;            // sig ids, most-invoked first (ties: lower id)
+};
+ProfileReport profile_invocations(const CompiledModel& model, const ParamEnv& params,
+                                  const std::vector<InstanceInput>& inputs);
+// The same over the DFG node table of a finished evaluation (record_nodes).
+ProfileReport profile_from_nodes(const CompiledModel& model, const std::vector<DFGNode>& nodes);
 
 }  // namespace runtime
 }  // namespace mbatch

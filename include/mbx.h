@@ -159,6 +159,18 @@ void mbx_options_default(mbx_options* o);
 int mbx_evaluate_batch(mbx_model* m, int batch, const int32_t* toks, int64_t ntok,
                        const float* data, int64_t ndata, const mbx_options* opts,
                        mbx_result** out);
+/* runtime::reference_evaluate (runtime.hpp:141-144): every instance evaluated on its own (one
+ * instance per mini-batch, no cross-instance batching).  The result carries outputs only (read
+ * with mbx_result_outputs; its trace is empty); in FP32 they equal mbx_evaluate_batch's bitwise. */
+int mbx_reference_evaluate(mbx_model* m, int batch, const int32_t* toks, int64_t ntok,
+                           const float* data, int64_t ndata, mbx_result** out);
+/* runtime::profile_invocations (runtime.hpp:146-154): over one evaluation of the inputs, per
+ * signature k < mbx_model_num_sigs: counts[k] = non-ghost DFG nodes, levels[k] = static nesting
+ * estimate of its blocks' functions (-1: no block); ranking[0 .. *nranked) = invoked signatures,
+ * most-invoked first (ties: lower id). */
+int mbx_profile_invocations(mbx_model* m, int batch, const int32_t* toks, int64_t ntok,
+                            const float* data, int64_t ndata, int64_t* counts, int32_t* levels,
+                            int32_t* ranking, int* nranked);
 void mbx_result_destroy(mbx_result* r);
 /* Outputs, hostval-encoded (two-call size protocol). */
 int mbx_result_outputs(const mbx_result* r, int32_t* toks, int64_t* ntok, float* data,

@@ -4,6 +4,7 @@
 // throws; the C++ surface (include/mbatch/*.hpp) rethrows the same text.
 #include <atomic>
 #include <cstdlib>
+#include <array>
 #include <cstring>
 #include <malloc.h>
 #include <memory>
@@ -542,6 +543,80 @@ int mbx_evaluate_batch(mbx_model* m, int batch, const int32_t* toks, int64_t nto
   if (rc) return rc;
   *out = res.release();
   return 0;
+}
+
+// Splits hostval-encoded inputs into per-instance (token, data) spans: each instance is its
+// model's instance inputs in module order.
+static std::vector<std::array<int64_t, 4>> instance_spans(const mbx_model* m, int batch, const int32_t* toks,
+                                                           int64_t ntok, const float* data, int64_t ndata) {
+  int ninputs = 0;
+  for (const auto& d : m->cm.params) ninputs += d.is_instance_input ? 1 : 0;
+  std::vector<std::array<int64_t, 4>> spans;
+  int64_t ti = 0, di = 0;
+  for (int i = 0; i < batch; ++i) {
+    const int64_t t0 = ti, d0 = di;
+    for (int k = 0; k < ninputs; ++k) (void)decode(toks, ntok, ti, data, ndata, di);
+    spans.push_back({t0, ti - t0, d0, di - d0});
+  }
+  MBATCH_CHECK(ti == ntok && di == ndata, "hostval encoding: trailing values after the last instance");
+  return spans;
+}
+
+int mbx_reference_evaluate(mbx_model* m, int batch, const int32_t* toks, int64_t ntok, const float* data,
+                           int64_t ndata, mbx_result** out) {
+  *out = nullptr;
+  auto res = std::make_unique<mbx_result>();
+  int rc = guarded(m->ctx, [&] {
+    mbx::settle(m->ctx);
+    MBATCH_CHECK(batch >= 1, "evaluate_batch: need at least one instance");
+    mbatch::runtime::ExecOptions o;
+    o.ghost = true;
+    for (const auto& sp : instance_spans(m, batch, toks, ntok, data, ndata)) {
+      mbatch::runtime::EncodedValues enc;
+      enc.count = 1;
+      enc.toks = toks + sp[0];
+      enc.ntok = sp[1];
+      enc.data = data + sp[2];
+      enc.ndata = sp[3];
+      mbatch::runtime::EncodedOutputs eo;
+      mbatch::runtime::EvalResult r = m->session->evaluate_encoded(enc, o, &eo);
+      res->out_tok.insert(res->out_tok.end(), eo.toks.begin(), eo.toks.end());
+      res->out_data.insert(res->out_data.end(), eo.data.begin(), eo.data.end());
+      res->r.timing.device_launches += r.timing.device_launches;
+    }
+  });
+  if (rc) return rc;
+  *out = res.release();
+  return 0;
+}
+
+int mbx_profile_invocations(mbx_model* m, int batch, const int32_t* toks, int64_t ntok, const float* data,
+                            int64_t ndata, int64_t* counts, int32_t* levels, int32_t* ranking, int* nranked) {
+  return guarded(m->ctx, [&] {
+    mbx::settle(m->ctx);
+    MBATCH_CHECK(batch >= 1, "evaluate_batch: need at least one instance");
+    mbatch::runtime::EncodedValues enc;
+    enc.count = batch;
+    enc.toks = toks;
+    enc.ntok = ntok;
+    enc.data = data;
+    enc.ndata = ndata;
+    mbatch::runtime::ExecOptions o;
+    o.ghost = true;
+    o.record_nodes = true;
+    mbatch::runtime::EncodedOutputs eo;
+    mbatch::runtime::EvalResult r = m->session->evaluate_encoded(enc, o, &eo);
+    const auto rep = mbatch::runtime::profile_from_nodes(m->cm, r.nodes);
+    const int nsig = int(m->cm.kernels.signatures.size());
+    for (int k = 0; k < nsig; ++k) {
+      auto c = rep.counts.find(k);
+      auto l = rep.static_estimate.find(k);
+      counts[k] = c == rep.counts.end() ? 0 : c->second;
+      levels[k] = l == rep.static_estimate.end() ? -1 : l->second;
+    }
+    *nranked = int(rep.ranking.size());
+    for (size_t k = 0; k < rep.ranking.size(); ++k) ranking[k] = rep.ranking[k];
+  });
 }
 
 void mbx_result_destroy(mbx_result* r) { delete r; }

@@ -289,6 +289,50 @@ EvalResult evaluate_batch(const CompiledModel& model, const ParamEnv& params, co
   return s.evaluate(inputs, model.opts);
 }
 
+std::vector<HostValue> reference_evaluate(const CompiledModel& model, const ParamEnv& params,
+                                          const std::vector<InstanceInput>& inputs) {
+  Session s(model, 0, MBX_PREC_FP32);
+  s.set_params(params);
+  std::vector<HostValue> out;
+  out.reserve(inputs.size());
+  for (const auto& in : inputs) {
+    EvalResult r = s.evaluate({in}, model.opts);
+    out.push_back(std::move(r.outputs.at(0)));
+  }
+  return out;
+}
+
+ProfileReport profile_from_nodes(const CompiledModel& model, const std::vector<DFGNode>& nodes) {
+  ProfileReport rep;
+  for (const auto& n : nodes)
+    if (!n.ghost) ++rep.counts[n.sig_id];
+  for (const auto& blk : model.blocks) {
+    auto b = model.kernels.binding_of_block.find(blk.id);
+    if (b == model.kernels.binding_of_block.end()) continue;
+    const int sig = b->second.sig_id;
+    auto it = model.nesting.find(blk.func);
+    const int level = it == model.nesting.end() ? 0 : it->second;
+    auto cur = rep.static_estimate.find(sig);
+    if (cur == rep.static_estimate.end() || level > cur->second) rep.static_estimate[sig] = level;
+  }
+  for (const auto& [sig, count] : rep.counts) rep.ranking.push_back(sig);
+  std::sort(rep.ranking.begin(), rep.ranking.end(), [&](int a, int b) {
+    if (rep.counts.at(a) != rep.counts.at(b)) return rep.counts.at(a) > rep.counts.at(b);
+    return a < b;
+  });
+  return rep;
+}
+
+ProfileReport profile_invocations(const CompiledModel& model, const ParamEnv& params,
+                                  const std::vector<InstanceInput>& inputs) {
+  Session s(model, 0, MBX_PREC_FP32);
+  s.set_params(params);
+  ExecOptions o = model.opts;
+  o.record_nodes = true;
+  EvalResult res = s.evaluate(inputs, o);
+  return profile_from_nodes(model, res.nodes);
+}
+
 // ---------------------------------------------------------------------------------------------
 // Executor
 

@@ -413,6 +413,7 @@ CompiledModel get_model(const std::string& name, int H, const ExecOptions& opts)
     mb.block(2, "rnn", 2, {"state", "h_wt", "inp_linear"}, {1}, {0, 2}, -1, 1);
     m.stage_phase = {0, 1};
     m.program = std::make_shared<RnnProgram>();
+    m.nesting = {{"main", 0}, {"rnn", 1}};
   } else if (name == "birnn") {
     for (const char* d : {"f", "b"}) {
       std::string p = std::string(d) + "_rnn_";
@@ -432,6 +433,7 @@ CompiledModel get_model(const std::string& name, int H, const ExecOptions& opts)
     mb.block(4, "rnn__c1", 2, {"state", "h_wt", "inp_linear"}, {1}, {0, 2}, -1, 1);
     m.stage_phase = {0, 0, 1, 2};
     m.program = std::make_shared<BirnnProgram>();
+    m.nesting = {{"main", 0}, {"rnn__c0", 1}, {"rnn__c1", 1}};
   } else if (name == "treelstm") {
     mb.param("x_wt", H, H); mb.param("x_bias", 1, H); mb.param("xn", 1, H);
     mb.param("i_wt", H2, H); mb.param("fl_wt", H2, H); mb.param("fr_wt", H2, H); mb.param("u_wt", H2, H);
@@ -470,6 +472,7 @@ CompiledModel get_model(const std::string& name, int H, const ExecOptions& opts)
     mb.block(3, "tlstm", 3, {"x", "x_wt", "x_bias"}, {1, 2}, {0}, 0, 1);
     m.stage_phase = {0, 1};
     m.program = std::make_shared<TreeLstmProgram>();
+    m.nesting = {{"main", 0}, {"tlstm", 1}, {"tcell__c0", 1}, {"tcell__c1", 1}};
   } else if (name == "mvrnn") {
     mb.param("v_wt", H2, H); mb.param("vbias", 1, H); mb.param("c_wt", H, C); mb.param("cbias", 1, C); mb.input("t");
     mb.sig("relu_bias_dense", {P("c_wt", H, C), P("cbias", 1, C)}, {P("%t0", 1, H)}, {c1}, dense_tail(hc, c1, h1, {L(O::kAdd, S(1)), L(O::kRelu)}));
@@ -489,6 +492,7 @@ CompiledModel get_model(const std::string& name, int H, const ExecOptions& opts)
     mb.block(2, "mv", 2, {"%t13", "%t14"}, {}, {0, 1}, -1, 1);
     m.stage_phase = {0, 1};
     m.program = std::make_shared<MvRnnProgram>();
+    m.nesting = {{"main", 0}, {"mv", 1}};
   } else if (name == "nestedrnn") {
     mb.param("zb", 1, H); mb.param("z_wt", H2, H); mb.param("hb", 1, H); mb.param("h_wt", H2, H);
     mb.param("rb", 1, H); mb.param("r_wt", H2, H); mb.param("n_wt", H, 11); mb.param("ibias", 1, H);
@@ -515,6 +519,7 @@ CompiledModel get_model(const std::string& name, int H, const ExecOptions& opts)
     mb.block(1, "outer", 1, {"x", "h", "z_wt", "zb", "h_wt", "hb", "r_wt", "rb", "n_wt"}, {2, 3, 4, 5, 6, 7, 8}, {0, 1}, -1, 2);
     m.stage_phase = {0};
     m.program = std::make_shared<NestedRnnProgram>();
+    m.nesting = {{"main", 0}, {"outer", 1}, {"inner", 2}};
   } else if (name == "drnn") {
     mb.param("obias", 1, H); mb.param("o_wt", H, H); mb.param("d_wt", H, 2); mb.param("lbias", 1, H);
     mb.param("l_wt", H, H); mb.param("rbias", 1, H); mb.param("r_wt", H, H); mb.param("root_bias", 1, H);
@@ -530,6 +535,7 @@ CompiledModel get_model(const std::string& name, int H, const ExecOptions& opts)
     mb.block(4, "main", 0, {"x", "root_wt", "root_bias"}, {1, 2}, {0}, 0, 1);
     m.stage_phase = {0};
     m.program = std::make_shared<DrnnProgram>();
+    m.nesting = {{"main", 0}, {"gen", 1}};
   } else if (name == "stackrnn") {
     mb.param("hbias", 1, H); mb.param("s_wt", H2, H); mb.param("a_wt", H, 2); mb.param("ebias", 1, H);
     mb.param("e_wt", H, H); mb.param("pbias", 1, H); mb.param("p_wt", H, H); mb.param("rbias", 1, H);
@@ -562,6 +568,7 @@ CompiledModel get_model(const std::string& name, int H, const ExecOptions& opts)
     mb.block(5, "srnn", 4, {"%t20", "%t21", "o_wt", "obias"}, {2, 3}, {0, 1}, -1, 1);
     m.stage_phase = {0, 1};
     m.program = std::make_shared<StackRnnProgram>();
+    m.nesting = {{"main", 0}, {"srnn", 1}};
   } else if (name == "fig5") {
     mb.param("a_wt", H, H); mb.param("abias", 1, H); mb.param("b_wt", H, H); mb.param("bbias", 1, H);
     mb.input("x"); mb.input("sel");
@@ -572,6 +579,7 @@ CompiledModel get_model(const std::string& name, int H, const ExecOptions& opts)
     mb.block(1, "extra", 1, {"v", "a_wt", "abias"}, {1, 2}, {0}, 0, 1);
     m.stage_phase = {0, 1};
     m.program = std::make_shared<Fig5Program>();
+    m.nesting = {{"main", 0}, {"common", 0}, {"extra", 0}};
   } else {
     throw Error("unknown model '" + name + "'");
   }

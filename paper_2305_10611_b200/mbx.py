@@ -79,6 +79,8 @@ def lib() -> ctypes.CDLL:
         "mbx_model_plan_encoding": (I, [P, I, pI32, pI64]),
         "mbx_options_default": (None, [ctypes.POINTER(_Opts)]),
         "mbx_evaluate_batch": (I, [P, I, pI32, I64, pF, I64, ctypes.POINTER(_Opts), ctypes.POINTER(P)]),
+        "mbx_reference_evaluate": (I, [P, I, pI32, I64, pF, I64, ctypes.POINTER(P)]),
+        "mbx_profile_invocations": (I, [P, I, pI32, I64, pF, I64, pI64, pI32, pI32, ctypes.POINTER(I)]),
         "mbx_result_destroy": (None, [P]),
         "mbx_result_outputs": (I, [P, pI32, pI64, pF, pI64]),
         "mbx_result_counters": (I, [P, pI64]),
@@ -476,6 +478,41 @@ class Model:
             return _read_result(r, batch, record_nodes, decode, trace)
         finally:
             L.mbx_result_destroy(r)
+
+
+    def reference_evaluate(self, toks: np.ndarray, data: np.ndarray, batch: int) -> list:
+        """runtime::reference_evaluate: every instance on its own (no cross-instance batching);
+        decoded outputs, one per instance."""
+        L = lib()
+        t = np.ascontiguousarray(toks, np.int32)
+        d = np.ascontiguousarray(data, np.float32)
+        r = ctypes.c_void_p()
+        self.ctx.check(L.mbx_reference_evaluate(self.h, batch, _ptr(t, ctypes.c_int32), t.size,
+                                                _ptr(d, ctypes.c_float), d.size, ctypes.byref(r)))
+        try:
+            nt, nd = ctypes.c_int64(), ctypes.c_int64()
+            L.mbx_result_outputs(r, None, ctypes.byref(nt), None, ctypes.byref(nd))
+            ot, od = np.zeros(nt.value, np.int32), np.zeros(nd.value, np.float32)
+            L.mbx_result_outputs(r, _ptr(ot, ctypes.c_int32), ctypes.byref(nt), _ptr(od, ctypes.c_float), ctypes.byref(nd))
+            return decode_hostvals(ot, od, batch)
+        finally:
+            L.mbx_result_destroy(r)
+
+    def profile_invocations(self, toks: np.ndarray, data: np.ndarray, batch: int) -> dict:
+        """runtime::profile_invocations: {"counts": {sig: n}, "static_estimate": {sig: level},
+        "ranking": [sig, ...]} over one evaluation of the inputs."""
+        L = lib()
+        t = np.ascontiguousarray(toks, np.int32)
+        d = np.ascontiguousarray(data, np.float32)
+        ns = L.mbx_model_num_sigs(self.h)
+        counts, levels, ranking = np.zeros(ns, np.int64), np.zeros(ns, np.int32), np.zeros(ns, np.int32)
+        nr = ctypes.c_int()
+        self.ctx.check(L.mbx_profile_invocations(self.h, batch, _ptr(t, ctypes.c_int32), t.size, _ptr(d, ctypes.c_float),
+                                                 d.size, _ptr(counts, ctypes.c_int64), _ptr(levels, ctypes.c_int32),
+                                                 _ptr(ranking, ctypes.c_int32), ctypes.byref(nr)))
+        return {"counts": {k: int(counts[k]) for k in range(ns) if counts[k]},
+                "static_estimate": {k: int(levels[k]) for k in range(ns) if levels[k] >= 0},
+                "ranking": [int(x) for x in ranking[:nr.value]]}
 
 
 def make_options(scheduler: str = "depth", gather: str = "fused", hoist: bool = True, phases: bool = True,
