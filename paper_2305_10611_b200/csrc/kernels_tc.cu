@@ -108,6 +108,11 @@ struct TcState {
   void* sfn = nullptr;
   int s_npc = 0, s_uc = 0, s_kb = 0, s_st = 1, s_smem = 0;
   bool s_attr = false;
+  // Narrow variant (8-unit slices, compiled on first use) for batches too small to give the wide
+  // one's grid a wave: more CTAs, each streaming a quarter of the weight columns.
+  void* sfn_n = nullptr;
+  int n_kb = 0, n_st = 1, n_smem = 0;
+  bool n_attr = false;
   bool attr_set = false;
   // Persistent multi-level variant (mbx_tc_levels): K-split ranks, maximal node tile, smem layout.
   // mbx_tc_levels configurations: [0] deep — the largest K split, weight slice resident, for runs
@@ -288,14 +293,14 @@ std::string gen_levels_source(const TcState& st, int k) {
 }
 
 // Source of the bit-exact small-dense kernel (plans with few output columns, e.g. a classifier).
-std::string gen_small_source(const TcState& st) {
+std::string gen_small_source(const TcState& st, int npc, int uc, int kb, int stages) {
   std::ostringstream o;
   o << jit::prelude_source();
   o << "#define MBX_SMALL_KERNEL 1\n"
     << "#define MBX_KC 16\n#define MBX_K " << st.K << "\n#define MBX_U " << st.U << "\n#define MBX_G " << st.G
     << "\n#define MBX_NPIECES " << st.npieces << "\n#define MBX_PK0 " << st.piece_k[0] << "\n#define MBX_NLOADS "
-    << st.prog.nloads << "\n#define MBX_NOUT " << st.prog.nout << "\n#define MBX_SNPC " << st.s_npc
-    << "\n#define MBX_SUC " << st.s_uc << "\n#define MBX_SKB " << st.s_kb << "\n#define MBX_SST " << st.s_st
+    << st.prog.nloads << "\n#define MBX_NOUT " << st.prog.nout << "\n#define MBX_SNPC " << npc
+    << "\n#define MBX_SUC " << uc << "\n#define MBX_SKB " << kb << "\n#define MBX_SST " << stages
     << "\n";
   o << gen_tail(st.prog, false, false, true);
   o << jit::kernel_source();
@@ -627,24 +632,32 @@ void tc_prepare(mbx_ctx* c, PlanEntry& pe) {
     // go (one round trip) when it fits.
     if (pe.force_vm && st->U % 8 == 0 && st->K % 8 == 0) {
       st->s_uc = 8;
-      if ((st->G * st->K * 8 + st->s_npc * st->K) * 4 <= 160 * 1024) st->s_kb = st->K;
+      if ((st->G * (st->K + 4) * 8 + st->s_npc * st->K) * 4 <= 160 * 1024) st->s_kb = st->K;
     }
-    if (st->s_kb > 0 && st->U % st->s_uc == 0) {
-      // As many chunks in flight as ~96 KB holds (all of K when it fits: the classifier's 64 x 512
-      // x 8 stages 32 KB per CTA in one round trip instead of 8 dependent ones).
-      // Otherwise the largest chunk (<= 64) that keeps >= 4 stages within the budget.
-      auto chunk = [&](int kb) { return (st->G * kb * st->s_uc + st->s_npc * kb) * 4; };
+    // As many chunks in flight as ~96 KB holds (all of K when it fits: the classifier's 64 x 512
+    // x 8 stages 32 KB per CTA in one round trip instead of 8 dependent ones).
+    // Otherwise the largest chunk (<= 64) that keeps >= 4 stages within the budget.
+    auto staging = [&](int uc, int npc, int& kb, int& stages, int& smem) {
+      auto chunk = [&](int k) { return (st->G * (k + 4) * uc + npc * k) * 4; };
       const int budget = 96 * 1024;
-      if (st->K / st->s_kb > 1 && chunk(st->K) <= budget) {
-        st->s_kb = st->K;
-      } else if (st->K / st->s_kb > 1) {
-        while (st->s_kb > 8 && budget / chunk(st->s_kb) < 4 && st->K % (st->s_kb / 2) == 0) st->s_kb /= 2;
+      if (st->K / kb > 1 && chunk(st->K) <= budget) {
+        kb = st->K;
+      } else if (st->K / kb > 1) {
+        while (kb > 8 && budget / chunk(kb) < 4 && st->K % (kb / 2) == 0) kb /= 2;
       }
-      const int nch = st->K / st->s_kb;
-      st->s_st = nch == 1 ? 1 : std::max(2, std::min(nch, budget / chunk(st->s_kb)));
-      st->s_smem = st->s_st * (st->G * st->s_kb * st->s_uc + st->s_npc * st->s_kb) * 4;
-      const std::string ssrc = gen_small_source(*st);
+      const int nch = st->K / kb;
+      stages = nch == 1 ? 1 : std::max(2, std::min(nch, budget / chunk(kb)));
+      smem = stages * chunk(kb);
+    };
+    if (st->s_kb > 0 && st->U % st->s_uc == 0) {
+      const int kb0 = st->s_kb;
+      staging(st->s_uc, st->s_npc, st->s_kb, st->s_st, st->s_smem);
+      const std::string ssrc = gen_small_source(*st, st->s_npc, st->s_uc, st->s_kb, st->s_st);
       st->sfn = load_kernel(c, ssrc, "mbx_small_dense");
+      if (st->s_uc > 8 && st->U % 8 == 0) {
+        st->n_kb = kb0;
+        staging(8, 8, st->n_kb, st->n_st, st->n_smem);
+      }
       pe.tc_exact = true;
       // Few output columns: tensor-core tiles would be mostly padding; exact in every precision.
       pe.tc_small = st->U * st->G <= 64;
@@ -795,15 +808,22 @@ cudaError_t tc_launch(mbx_ctx* c, const PlanEntry& pe, const BatchLaunch& L) {
     for (int g = 0; g < st->G; ++g) a.w_idx[g] = st->w_shared[size_t(g)];
     a.nloads = st->prog.nloads;
     fill_loads(st->prog, a.loads);
-    if (!st->s_attr) {
-      cudaError_t e = cudaFuncSetAttribute(st->sfn, cudaFuncAttributeMaxDynamicSharedMemorySize, st->s_smem);
+    // The wide variant unless its grid would leave most SMs idle (a few nodes over few unit
+    // slices, e.g. TreeLSTM-256 b8's internal depths): then 8-unit slices, 4x the CTAs.
+    const bool narrow = st->n_kb > 0 && ((L.b + st->s_npc - 1) / st->s_npc) * (st->U / st->s_uc) < 74;
+    if (narrow && !st->sfn_n) st->sfn_n = load_kernel(c, gen_small_source(*st, 8, 8, st->n_kb, st->n_st), "mbx_small_dense");
+    void* fn = narrow ? st->sfn_n : st->sfn;
+    const int npc = narrow ? 8 : st->s_npc, uc = narrow ? 8 : st->s_uc, smem = narrow ? st->n_smem : st->s_smem;
+    bool& attr = narrow ? st->n_attr : st->s_attr;
+    if (!attr) {
+      cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       if (e != cudaSuccess) return e;
-      st->s_attr = true;
+      attr = true;
     }
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(unsigned((L.b + st->s_npc - 1) / st->s_npc), unsigned(st->U / st->s_uc));
+    cfg.gridDim = dim3(unsigned((L.b + npc - 1) / npc), unsigned(st->U / uc));
     cfg.blockDim = dim3(kTcThreads);
-    cfg.dynamicSmemBytes = size_t(st->s_smem);
+    cfg.dynamicSmemBytes = size_t(smem);
     cfg.stream = c->stream;
     cudaLaunchAttribute at[1];
     if (pdl_enabled()) {
@@ -813,7 +833,7 @@ cudaError_t tc_launch(mbx_ctx* c, const PlanEntry& pe, const BatchLaunch& L) {
       cfg.numAttrs = 1;
     }
     void* args[] = {&a};
-    return cudaLaunchKernelExC(&cfg, st->sfn, args);
+    return cudaLaunchKernelExC(&cfg, fn, args);
   }
   if (pe.tc_kind == 2) {
     PwArgs a{};

@@ -1214,7 +1214,11 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const
 extern "C" __global__ void __launch_bounds__(MBX_THREADS) mbx_small_dense(const __grid_constant__ SmallArgs P) {
   extern __shared__ __align__(16) float sms[];
   constexpr int K = MBX_K, U = MBX_U, G = MBX_G, NPC = MBX_SNPC, UC = MBX_SUC, KB = MBX_SKB;
-  constexpr int WCH = G * KB * UC, XCH = NPC * KB, BUF = WCH + XCH;
+  // Weight chunk transposed, [gate][unit][KB + 4]: a thread's column is contiguous along K, so
+  // its operands load 4 at a time (rows 4 floats apart: the transposing 4-byte copies of 8
+  // consecutive units land in different banks).
+  constexpr int KBP = KB + 4;
+  constexpr int WCH = G * UC * KBP, XCH = NPC * KB, BUF = WCH + XCH;
   static_assert(K % KB == 0 && KB % 8 == 0, "K chunking");
   const int tid = threadIdx.x;
   const int node0 = blockIdx.x * NPC;
@@ -1247,7 +1251,7 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS) mbx_small_dense(const 
     for (int g = 0; g < G; ++g)
       for (int i = tid; i < KB * UC; i += MBX_THREADS) {
         const int r = i / UC, q = i - r * UC;
-        mbx_gen::cp_async4(buf + (g * KB + r) * UC + q, wsrc[g] + (long long)(k0 + r) * U + q, true);
+        mbx_gen::cp_async4(buf + (g * UC + q) * KBP + r, wsrc[g] + (long long)(k0 + r) * U + q, true);
       }
     for (int i = tid; i < nn * KB; i += MBX_THREADS) {
       const int n = i / KB, k = k0 + (i - n * KB);
@@ -1280,21 +1284,23 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS) mbx_small_dense(const 
     mbx_gen::cp_async_wait<D>();
     __syncthreads();
     if (active) {
-      const float* x = cur + WCH + n * KB;
-      const float* w = cur + u;
-      // Blocks of 8 p: operands and products first (independent), then the 8 dependent adds of
-      // each chain in p order — the add chain is the only serial part.  Unrolled 4 blocks deep so
-      // the next blocks' shared-memory loads and products overlap this block's add chain.
+      const float4* x4 = reinterpret_cast<const float4*>(cur + WCH + n * KB);
+      const float* w = cur + u * KBP;
+      // Blocks of 8 p: operands (16-byte loads) and products first (independent), then the 8
+      // dependent adds of each chain in p order — the add chain is the only serial part.
+      // Unrolled 4 blocks deep so the next blocks' loads and products overlap this block's adds.
 #pragma unroll 4
       for (int p0 = 0; p0 < KB; p0 += 8) {
-        float xv[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) xv[q] = x[p0 + q];
+        const float4 xa = x4[p0 >> 2], xb = x4[(p0 >> 2) + 1];
+        const float xv[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
 #pragma unroll
         for (int gi = 0; gi < G; ++gi) {
+          const float4* w4 = reinterpret_cast<const float4*>(w + gi * UC * KBP + p0);
+          const float4 wa = w4[0], wb = w4[1];
+          const float wv[8] = {wa.x, wa.y, wa.z, wa.w, wb.x, wb.y, wb.z, wb.w};
           float pr[8];
 #pragma unroll
-          for (int q = 0; q < 8; ++q) pr[q] = mbx_libm::fmul(xv[q], w[(gi * KB + p0 + q) * UC]);
+          for (int q = 0; q < 8; ++q) pr[q] = mbx_libm::fmul(xv[q], wv[q]);
 #pragma unroll
           for (int q = 0; q < 8; ++q) g[gi] = mbx_libm::fadd(g[gi], pr[q]);
         }
