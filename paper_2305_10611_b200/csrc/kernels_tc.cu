@@ -1010,10 +1010,12 @@ int plan_levels(mbx_ctx* c, const std::vector<BatchLaunch>& Ls, size_t i, size_t
   int k = 0;
   int ng = level_tiles(st->lv[0], utiles, Ls, i, n, nts);
   if (n == 1 && st->lv[1].S > 0 && (st->lv[1].fn || c->dry)) {
-    // One batch with more node tiles than the deep configuration has groups for: go wide.
+    // One batch with more node tiles than the deep configuration has groups for, or a large one
+    // (>= 128 nodes: the same MMA work per CTA, but a K split of 2 exchanges an eighth of the
+    // partials of deep's 8; BiRNN's 510-node input transform 33 -> ~18 us): go wide.
     std::vector<int> nts1;
     const int ng1 = level_tiles(st->lv[1], utiles, Ls, i, n, nts1);
-    if ((L0.b + nts[0] - 1) / nts[0] > ng) {
+    if ((L0.b + nts[0] - 1) / nts[0] > ng || L0.b >= 128) {
       k = 1;
       ng = ng1;
       nts = nts1;
