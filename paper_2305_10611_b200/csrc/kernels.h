@@ -44,6 +44,7 @@ struct MvCellLaunch {
   int cs;                       // column slices per node (set by launch_mv_cell)
   int pdl;                      // programmatic dependent launch: W may be read before the wait
   const float* wt;              // W^T, rows of 2N + 4 floats (launch_mv_transpose)
+  int late_wt;                  // W^T's slice loaded once the matrices are consumed (set by launch_mv_cell)
 };
 size_t mv_wt_floats(int N, int U);
 cudaError_t launch_mv_transpose(const float* w, float* wt, int N, int U, cudaStream_t stream);

@@ -44,6 +44,7 @@ using namespace mbx_libm;
 namespace {
 
 constexpr int kMvThreads = 256;
+constexpr size_t kMaxCtasPerSm = 2048 / kMvThreads;
 
 #ifdef MBX_MV_STAMPS  // tools/mv_bench.cu: globaltimer stamps of CTA 0's phases
 __device__ unsigned long long g_mv_stamps[16];
@@ -196,17 +197,20 @@ __global__ void __launch_bounds__(kMvThreads) mv_cell_kernel(const __grid_consta
   const int tid = threadIdx.x;
   const int s = blockIdx.x;            // column slice (= rank in the cluster)
   const int64_t node = blockIdx.y;
-  float* ms = sm;                          // [2][K][NC]: this slice of M0, M1
-  float* ws = ms + mv_align4(2 * K * NC);  // [UC][2N + 4]: this slice of W, transposed
-  float* xs = ws + (2 * N + 4) * UC;       // [2][K]
-  float* t2 = xs + mv_align4(2 * K);       // [2N]
+  // late_wt (levels too large for one wave of CTAs): W^T's slice reuses the matrices' space once
+  // they are consumed (a third less shared memory, twice the CTAs per SM).
+  const int mreg = mv_align4(2 * K * NC), wreg = (2 * N + 4) * UC;
+  float* ms = sm;                                  // [2][K][NC]: this slice of M0, M1
+  float* ws = A.late_wt ? sm : ms + mreg;          // [UC][2N + 4]: this slice of W, transposed
+  float* xs = A.late_wt ? sm + max(mreg, wreg) : ws + wreg;  // [2][K]
+  float* t2 = xs + mv_align4(2 * K);               // [2N]
   MV_STAMP(0);
   if (CS > 1) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");  // peers started (DSMEM)
   const int64_t* bo = A.batched_off + node * A.nb;
   // This slice of W^T (the host's transposed copy of W): UC contiguous rows of 2N + 4 floats.  It
   // does not depend on the previous kernel (the host enables PDL only then), so it streams in
   // while that kernel, which produces this level's rows and matrices, finishes.
-  copy_flat(ws, A.wt + int64_t(s) * UC * (2 * N + 4), UC * (2 * N + 4), tid);
+  if (!A.late_wt) copy_flat(ws, A.wt + int64_t(s) * UC * (2 * N + 4), UC * (2 * N + 4), tid);
   asm volatile("cp.async.commit_group;" ::: "memory");
   if (A.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
   copy_rows(ms, A.arena + bo[A.m[0]] + s * NC, K, NC, N, tid);
@@ -246,11 +250,20 @@ __global__ void __launch_bounds__(kMvThreads) mv_cell_kernel(const __grid_consta
     __syncthreads();
     mv_add_slice(A, ms, node, s, K, N, NC, tid, kMvThreads);
   }
+  if (A.late_wt) {  // the matrices are consumed: W^T's slice into their space
+    __syncthreads();
+    copy_flat(ws, A.wt + int64_t(s) * UC * (2 * N + 4), UC * (2 * N + 4), tid);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
   if (CS > 1) {
     // Every slice of T2 is in every peer's shared memory (release / acquire at cluster scope).
     asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
     asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
   } else {
+    __syncthreads();
+  }
+  if (A.late_wt) {
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
     __syncthreads();
   }
   MV_STAMP(5);
@@ -277,9 +290,10 @@ int mv_cell_slices(int N, int U) {
   return 1;
 }
 
-size_t mv_cell_smem(int K, int N, int U) {
+size_t mv_cell_smem(int K, int N, int U, bool late_wt = false) {
   const int cs = mv_cell_slices(N, U);
-  return size_t(mv_align4(2 * K * (N / cs)) + (2 * N + 4) * (U / cs) + mv_align4(2 * K) + 2 * N) * sizeof(float);
+  const int mreg = mv_align4(2 * K * (N / cs)), wreg = (2 * N + 4) * (U / cs);
+  return size_t((late_wt ? std::max(mreg, wreg) : mreg + wreg) + mv_align4(2 * K) + 2 * N) * sizeof(float);
 }
 
 bool mv_cell_supported(int K, int N, int U) {
@@ -299,7 +313,14 @@ cudaError_t launch_mv_transpose(const float* w, float* wt, int N, int U, cudaStr
 cudaError_t launch_mv_cell(const MvCellLaunch& L0, cudaStream_t stream) {
   MvCellLaunch L = L0;
   L.cs = mv_cell_slices(L.N, L.U);
-  const size_t smem = mv_cell_smem(L.K, L.N, L.U);
+  // A level with more node clusters than one wave holds at the full layout (W^T staged up front)
+  // takes the late-W^T layout: two-thirds of the shared memory, more CTAs per SM.
+  auto nodes_per_wave = [&](size_t smem) {
+    const int per_sm = int(std::min<size_t>(kMaxCtasPerSm, (228 * 1024) / (smem + 1024)));
+    return 148 * per_sm / L.cs;
+  };
+  L.late_wt = L.b > nodes_per_wave(mv_cell_smem(L.K, L.N, L.U)) ? 1 : 0;
+  const size_t smem = mv_cell_smem(L.K, L.N, L.U, L.late_wt != 0);
   static std::once_flag once[64];
   int dev = 0;
   cudaGetDevice(&dev);
