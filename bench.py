@@ -54,7 +54,7 @@ def parse_args():
     p.add_argument("--hidden", type=int, default=512)
     p.add_argument("--batch", type=int, default=64)
     p.add_argument("--seed", type=int, default=1)
-    p.add_argument("--precision", default="bf16x3", choices=["fp32", "bf16x3", "bf16"])
+    p.add_argument("--precision", default="bf16x3", choices=["fp32", "bf16x3", "bf16x6", "bf16"])
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--threads", type=int, default=0,
                    help="host worker threads of the throughput pool (0: cores per rank - 2)")
@@ -386,7 +386,8 @@ def run_ours(args):
     line = {
         "metric": METRIC, "value": value, "unit": "nodes/s", "n_gpus": world, "steps": K, "warmup": args.warmup,
         "ms_per_step": pool_res["ms_per_step"], "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": {"fp32": "f32", "bf16x3": "bf16x3 (split-bf16 tcgen05, fp32 accumulate)", "bf16": "bf16"}[args.precision],
+        "dtype": {"fp32": "f32", "bf16x3": "bf16x3 (split-bf16 tcgen05, fp32 accumulate)",
+                  "bf16x6": "bf16x6 (three-part split-bf16 tcgen05, fp32 accumulate)", "bf16": "bf16"}[args.precision],
         "data": f"synthetic: reference zoo generators (params seed {args.seed}, inputs seed {args.seed}+rank)",
         "config": {"workload": f"{args.model}-h{args.hidden}-b{args.batch}", "hidden": args.hidden,
                    "batch": args.batch, "nodes_per_minibatch": nodes, "precision": args.precision,

@@ -42,7 +42,7 @@ enum { MBX_GATHER_FUSED = 0, MBX_GATHER_EXPLICIT = 1 };
  *   BF16X3: tcgen05 tensor cores on split bf16 operands (hi*hi + hi*lo + lo*hi, fp32 TMEM
  *         accumulation) where a tensor-core kernel exists for the plan, FP32 elsewhere.
  *   BF16: tcgen05 single bf16 pass (fastest, widest tolerance). */
-enum { MBX_PREC_FP32 = 0, MBX_PREC_BF16X3 = 1, MBX_PREC_BF16 = 2 };
+enum { MBX_PREC_FP32 = 0, MBX_PREC_BF16X3 = 1, MBX_PREC_BF16 = 2, MBX_PREC_BF16X6 = 3 };
 /* ExecOptions::Scheduler (proj/include/mbatch/runtime.hpp:45-55). */
 enum { MBX_SCHED_DEPTH = 0, MBX_SCHED_AGENDA = 1 };
 

@@ -1198,8 +1198,10 @@ void issue_batch(mbx_ctx* c, const BatchLaunch& L) {
   // when the context allows split-bf16 / bf16 contractions.
   // The bit-exact gate kernel runs for small / decision plans in every precision and for every
   // gate plan in FP32 contexts; pointwise plans always; tensor cores in the other precisions.
-  if (pe.tc_kind == 2 || pe.tc_small || (pe.tc_exact && c->precision == MBX_PREC_FP32) ||
-      (c->precision != MBX_PREC_FP32 && pe.tc_kind == 1)) {
+  // BF16X6 runs the tensor cores only in persistent levels runs (3-part operands); its single
+  // batches take the exact kernels like FP32.
+  const bool exact_batches = c->precision == MBX_PREC_FP32 || c->precision == MBX_PREC_BF16X6;
+  if (pe.tc_kind == 2 || pe.tc_small || (pe.tc_exact && exact_batches) || (!exact_batches && pe.tc_kind == 1)) {
     cuda_check(tc_launch(c, pe, L), "tensor-core plan kernel");
     ++c->launches;
     ++g_launches;
@@ -1424,6 +1426,7 @@ static int env_precision() {
   if (!e || std::strcmp(e, "fp32") == 0) return MBX_PREC_FP32;
   if (std::strcmp(e, "bf16x3") == 0) return MBX_PREC_BF16X3;
   if (std::strcmp(e, "bf16") == 0) return MBX_PREC_BF16;
+  if (std::strcmp(e, "bf16x6") == 0) return MBX_PREC_BF16X6;
   throw Error(std::string("MBX_PRECISION: unknown precision ") + e);
 }
 Arena::Arena(int64_t initial_capacity) : owned_(true) {

@@ -184,7 +184,7 @@ int mbx_ctx_create(int device, int precision, mbx_ctx** out) {
   c->dry = device < 0;
   c->precision = precision;
   int rc = guarded(nullptr, [&] {
-    MBATCH_CHECK(precision >= MBX_PREC_FP32 && precision <= MBX_PREC_BF16, "unknown precision");
+    MBATCH_CHECK(precision >= MBX_PREC_FP32 && precision <= MBX_PREC_BF16X6, "unknown precision");
     if (!c->dry) {
       mbx::cuda_check(cudaSetDevice(device), "cudaSetDevice");
       mbx::cuda_check(cudaFree(nullptr), "context init");
@@ -244,7 +244,7 @@ void mbx_pool_set_error(const char* msg) { g_err = msg ? msg : ""; }
 int mbx_ctx_set_precision(mbx_ctx* c, int precision) {
   return guarded(c, [&] {
     mbx::settle(c);
-    MBATCH_CHECK(precision >= MBX_PREC_FP32 && precision <= MBX_PREC_BF16, "unknown precision");
+    MBATCH_CHECK(precision >= MBX_PREC_FP32 && precision <= MBX_PREC_BF16X6, "unknown precision");
     c->precision = precision;
   });
 }

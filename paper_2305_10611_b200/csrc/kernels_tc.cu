@@ -63,6 +63,13 @@ struct EpiProg {
   std::vector<EpiOp> ops;
 };
 
+// Split-bf16 parts of a weight / operand for a pass count: bf16 (1 MMA), bf16x3 (hi, lo; 3 MMAs),
+// bf16x6 (hi, mid, lo; 6 MMAs: every product term down to 2^-24 relative).
+__host__ __device__ inline int npass_parts(int npass) { return npass == 1 ? 1 : (npass == 3 ? 2 : 3); }
+inline int npass_of(int precision) {
+  return precision == MBX_PREC_BF16 ? 1 : (precision == MBX_PREC_BF16X6 ? 6 : 3);
+}
+
 // Packs G weights (each K x U fp32, row-major, in the arena) into per-unit-tile, per-chunk
 // canonical K-major bf16 blocks: [tile][chunk][pass][M x KC].  Rows g*UC + j of tile t hold column
 // t*UC + j of weight g; rows >= G*UC are zero.
@@ -84,12 +91,14 @@ __global__ void tc_pack_kernel(const float* arena, const int64_t* w_off, int G, 
       const int g = r / UC, col = t * UC + r % UC, k = c * KC + kk;
       v = arena[w_off[g] + int64_t(k) * U + col];
     }
-    const __nv_bfloat16 h = __float2bfloat16_rn(v);
-    const float lo = v - __bfloat162float(h);
-    uint8_t* blk = out + ((int64_t(t) * nchunks + c) * (npass > 1 ? 2 : 1)) * chunk_bytes;
+    const int parts = npass_parts(npass);
+    uint8_t* blk = out + ((int64_t(t) * nchunks + c) * parts) * chunk_bytes;
     const uint32_t off = uint32_t((r >> 3) * (KC * 16) + (kk >> 3) * 128 + (r & 7) * 16 + (kk & 7) * 2);
-    *reinterpret_cast<__nv_bfloat16*>(blk + off) = h;
-    if (npass > 1) *reinterpret_cast<__nv_bfloat16*>(blk + chunk_bytes + off) = __float2bfloat16_rn(lo);
+    for (int q = 0; q < parts; ++q) {  // successive residuals: hi, [mid,] lo
+      const __nv_bfloat16 h = __float2bfloat16_rn(v);
+      *reinterpret_cast<__nv_bfloat16*>(blk + q * chunk_bytes + off) = h;
+      v = v - __bfloat162float(h);
+    }
   }
 }
 
@@ -119,6 +128,7 @@ struct TcState {
   // of levels; [1] wide — a small K split, many node-tile groups, for one large batch.
   struct LevelsCfg {
     int S = 0, NT = 0, xch = 0;  // xch 0: K ranks form a cluster (DSMEM), 1: L2 exchange
+    int parts = 2;               // split-bf16 parts the shared-memory layout holds (3: bf16x6)
     int w_off = 0, x_off = 0, recv_off = 0, bar_off = 0, smem = 0;
     std::string src;
     void* fn = nullptr;
@@ -286,8 +296,14 @@ std::string gen_levels_source(const TcState& st, int k) {
     << st.UC << "\n#define MBX_NCHUNKS " << st.nchunks << "\n#define MBX_NPIECES " << st.npieces
     << "\n#define MBX_PK0 " << st.piece_k[0] << "\n#define MBX_NLOADS " << st.prog.nloads << "\n#define MBX_NOUT "
     << st.prog.nout << "\n#define MBX_LS " << L.S << "\n#define MBX_LNT " << L.NT << "\n#define MBX_LXCH " << L.xch
-    << "\n";
-  o << gen_tail(st.prog, false);
+    << "\n#define MBX_LPARTS " << L.parts << "\n";
+  if (L.parts == 3) {
+    // bf16x6 (24-bit operands): the glibc-exact activations too, so the only difference from the
+    // FP32 path left is the tensor core's summation order.
+    o << gen_tail(st.prog, false, false, true) << "#define mbx_tail mbx_tail_exact\n";
+  } else {
+    o << gen_tail(st.prog, false);
+  }
   o << jit::kernel_source();
   return o.str();
 }
@@ -488,7 +504,7 @@ __global__ void fill_u32(unsigned* p, size_t n, unsigned v) {
   for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) p[i] = v;
 }
 
-bool levels_layout(TcState& st, int k) {
+bool levels_layout(TcState& st, int k, int parts) {
   auto al = [](int x) { return (x + 1023) / 1024 * 1024; };
   const int utiles = st.U / st.UC;
   TcState::LevelsCfg& C = st.lv[k];
@@ -501,14 +517,15 @@ bool levels_layout(TcState& st, int k) {
     // tail elements per thread x operands held in registers (MBX_LEPT x MBX_NLOADS) <= 16
     const int lloc = xch ? ((NT / 8 + S - 1) / S) * 8 : NT / S;
     if (NT / S < 2 || lloc * st.UC * std::max(1, st.prog.nloads) > 16 * kTcThreads) return false;
-    const int w = al(cpr * kM * st.KC * 4);
-    const int x = al(std::max(cpr * (NT * st.KC * 4 + 128), xch ? 0 : NT * kM * 4));  // xstride per chunk
+    const int w = al(cpr * kM * st.KC * 2 * parts);
+    const int x = al(std::max(cpr * parts * (NT * st.KC * 2 + 64), xch ? 0 : NT * kM * 4));  // xstride per chunk
     const int recv = al(S > 1 && xch == 0 ? (S - 1) * (NT / S) * kM * 4 : 0);
     const int bars = (2 * cpr + 6) * 8 + NT * 16;
     if (w + x + recv + bars > kSmemBudget - kLevelsStaticSmem) return false;
     C.S = S;
     C.NT = NT;
     C.xch = xch;
+    C.parts = parts;
     C.w_off = 0;
     C.x_off = w;
     C.recv_off = w + x;
@@ -671,7 +688,7 @@ void tc_prepare(mbx_ctx* c, PlanEntry& pe) {
     st->src = gen_gate_source(*st);
     st->fn = load_kernel(c, st->src, "mbx_tc_gate");
     for (int k = 0; k < 2; ++k)
-      if (levels_layout(*st, k)) {
+      if (levels_layout(*st, k, c->precision == MBX_PREC_BF16X6 ? 3 : 2)) {
         if (k == 1 && st->lv[1].S == st->lv[0].S && st->lv[1].NT == st->lv[0].NT) {
           st->lv[1].S = 0;  // same configuration as deep
           continue;
@@ -748,7 +765,7 @@ static bool rows_vec16(mbx_ctx* c, const TcState* st, const PlanEntry& pe, const
 
 static cudaError_t ensure_pack(mbx_ctx* c, TcState* st, const int64_t* shared_host, int npass, TcState::Packed** out,
                         bool* fresh) {
-  const int wpass = npass > 1 ? 2 : 1;
+  const int wpass = npass_parts(npass);
   std::vector<int64_t> offs;
   for (int w : st->w_shared) offs.push_back(shared_host[w]);
   TcState::Packed* pk = nullptr;
@@ -792,7 +809,7 @@ static cudaError_t ensure_pack(mbx_ctx* c, TcState* st, const int64_t* shared_ho
 
 cudaError_t tc_launch(mbx_ctx* c, const PlanEntry& pe, const BatchLaunch& L) {
   auto* st = static_cast<TcState*>(pe.tc_state);
-  if ((pe.tc_small || (pe.tc_exact && c->precision == MBX_PREC_FP32)) && st->sfn) {
+  if ((pe.tc_small || (pe.tc_exact && (c->precision == MBX_PREC_FP32 || c->precision == MBX_PREC_BF16X6))) && st->sfn) {
     SmallArgs a{};
     a.arena = arena_ptr(c);
     a.shared_off = meta_dev<long long>(c, L.shared_meta);
@@ -886,10 +903,11 @@ cudaError_t tc_launch(mbx_ctx* c, const PlanEntry& pe, const BatchLaunch& L) {
     void* args[] = {&a};
     // FP32 contexts: glibc-exact activations (bit-identical to the reference); the tensor-core
     // precisions use the fast ones, as their gate tails do.
-    void* fn = c->precision == MBX_PREC_FP32 ? (v4 ? st->fn4 : st->fn) : (v4 ? st->fn_fast4 : st->fn_fast);
+    const bool exact = c->precision == MBX_PREC_FP32 || c->precision == MBX_PREC_BF16X6;  // glibc-exact activations
+    void* fn = exact ? (v4 ? st->fn4 : st->fn) : (v4 ? st->fn_fast4 : st->fn_fast);
     return cudaLaunchKernelExC(&cfg, fn, args);
   }
-  const int npass = c->precision == MBX_PREC_BF16 ? 1 : 3;
+  const int npass = npass_of(c->precision);
   const int64_t* shared_host = reinterpret_cast<const int64_t*>(c->meta.host + L.shared_meta);
   const int ntiles = st->U / st->UC;
   TcState::Packed* pk = nullptr;
@@ -994,6 +1012,10 @@ int plan_levels(mbx_ctx* c, const std::vector<BatchLaunch>& Ls, size_t i, size_t
     return 0;
   auto* st = static_cast<TcState*>(pe.tc_state);
   if (!st || st->lv[0].S == 0 || (!st->lv[0].fn && !c->dry)) return 0;
+  // The kernel's split parts are 1 (bf16) or its layout's MBX_LPARTS: a plan registered under
+  // another multi-part precision runs batch by batch.
+  const int need_parts = npass_parts(npass_of(c->precision));
+  if (need_parts != 1 && need_parts != st->lv[0].parts) return 0;
   const size_t ns = pe.exec_plan.shared_shapes.size();
   const int64_t* sh0 = reinterpret_cast<const int64_t*>(c->meta.host + L0.shared_meta);
   size_t j = i;
@@ -1102,6 +1124,7 @@ void plan_shadows(mbx_ctx* c, std::vector<BatchLaunch>& Ls, const std::vector<Le
     return !e ? 2 : std::strcmp(e, "convert") == 0 ? 0 : std::strcmp(e, "shadow") == 0 ? 1 : 2;
   }();
   if (c->precision == MBX_PREC_FP32 || Ls.empty() || allow == 0) return;
+  const int parts = npass_parts(npass_of(c->precision));
   // Output regions whose producer can write split-bf16 shadows: the pointwise kernel (16-byte
   // variant) and every level of a persistent run.  Regions never overlap (bump allocation).
   struct Region {
@@ -1164,7 +1187,7 @@ void plan_shadows(mbx_ctx* c, std::vector<BatchLaunch>& Ls, const std::vector<Le
       bool img_ok = allow >= 2 && st->K < 4096 && kslice < 4096 && (kslice & (kslice - 1)) == 0 && nt < 65536 &&
                     (st->KC == 16 || st->KC == 32);
       cands.clear();
-      const int64_t tile_bytes = int64_t(nt) * st->K * 4;
+      const int64_t tile_bytes = int64_t(nt) * st->K * 2 * parts;
       for (int pc = 0; pc < st->npieces && img_ok; ++pc) {
         const int k0 = pc ? st->piece_k[0] : 0, width = st->piece_k[pc] - k0;
         if (st->piece_kind[pc] != kRefBatched || st->piece_off[pc] != 0 || k0 % 8 != 0) img_ok = false;
@@ -1197,7 +1220,7 @@ void plan_shadows(mbx_ctx* c, std::vector<BatchLaunch>& Ls, const std::vector<Le
           cd.d.x = int(uint32_t(uint64_t(base) & 0xffffffffu));
           cd.d.y = int(uint32_t(uint64_t(base) >> 32));
           cd.d.z = (i % nt) | (nt << 16);
-          cd.d.w = k0 | (ilog2(st->KC) << 12) | (ilog2(kslice) << 16);
+          cd.d.w = k0 | (ilog2(st->KC) << 12) | (ilog2(kslice) << 16) | (parts << 20);
           cands.push_back(cd);
         }
       }
@@ -1215,8 +1238,8 @@ void plan_shadows(mbx_ctx* c, std::vector<BatchLaunch>& Ls, const std::vector<Le
         img_used = (img_used + 1023) & ~size_t(1023);
         continue;
       }
-      // -- shadow gathers --
-      bool ready = true;
+      // -- shadow gathers (the shadow holds two parts: not for bf16x6) --
+      bool ready = parts == 2;
       marks.clear();
       for (int pc = 0; pc < st->npieces && ready; ++pc) {
         const int width = st->piece_k[pc] - (pc ? st->piece_k[0] : 0);
@@ -1313,7 +1336,7 @@ void issue_levels(mbx_ctx* c, const std::vector<BatchLaunch>& Ls, size_t i, int 
   const PlanEntry& pe = c->plans[L0.plan_id];
   auto* st = static_cast<TcState*>(pe.tc_state);
   TcState::LevelsCfg& C = st->lv[cfg];
-  const int npass = c->precision == MBX_PREC_BF16 ? 1 : 3;
+  const int npass = npass_of(c->precision);
   const int64_t* shared_host = reinterpret_cast<const int64_t*>(c->meta.host + L0.shared_meta);
   TcState::Packed* pk = nullptr;
   bool fresh_pack = false;

@@ -57,18 +57,34 @@ __device__ __forceinline__ void mbar_arrive_cnt(unsigned long long* bar, unsigne
 // producer row gets an image of its B operands, [tile][K rank][chunk][hi | lo][canonical
 // no-swizzle K-major nt x KC], which the producers fill as they write the rows (split bf16) and
 // the consumer loads with a few bulk copies.  d = {base lo, base hi, p | nt << 16,
-// k0 | log2 KC << 12 | log2 kslice << 16}: the tile's image (byte offset), the consumer column,
-// the consumer's tile width, the piece's first K index, the consumer's K chunk and K slice per rank
-// (both powers of two: shifts, no divisions in the producers' store loop).
-// Returns the byte offset of column u's hi part; the lo part is *lo_off bytes further.
-__device__ __forceinline__ long long img_addr(const int4 d, int u, int* lo_off) {
+// k0 | log2 KC << 12 | log2 kslice << 16 | parts << 20}: the tile's image (byte offset), the
+// consumer column, the consumer's tile width, the piece's first K index, the consumer's K chunk and
+// K slice per rank (both powers of two: shifts, no divisions in the producers' store loop), and the
+// split-bf16 parts (2: hi, lo; 3: hi, mid, lo).
+// Returns the byte offset of column u's hi part; part q is q * *part_off bytes further.
+__device__ __forceinline__ long long img_addr(const int4 d, int u, int* part_off) {
   const long long base = (long long)(((unsigned long long)(unsigned)d.y << 32) | (unsigned)d.x);
   const int p = d.z & 0xffff, nt = d.z >> 16;
-  const int k0 = d.w & 0xfff, lkc = (d.w >> 12) & 0xf, lks = (d.w >> 16) & 0xf;
+  const int k0 = d.w & 0xfff, lkc = (d.w >> 12) & 0xf, lks = (d.w >> 16) & 0xf, parts = (d.w >> 20) & 0xf;
   const int k = k0 + u, r = k >> lks, kr = k & ((1 << lks) - 1), j = kr >> lkc, kk = kr & ((1 << lkc) - 1);
-  *lo_off = nt << (lkc + 1);
-  return base + (long long)((r << (lks - lkc)) + j) * (nt << (lkc + 2)) + (p >> 3) * (16 << lkc) + (kk >> 3) * 128 +
-         (p & 7) * 16 + (kk & 7) * 2;
+  *part_off = nt << (lkc + 1);
+  return base + (long long)((r << (lks - lkc)) + j) * parts * (nt << (lkc + 1)) + (p >> 3) * (16 << lkc) +
+         (kk >> 3) * 128 + (p & 7) * 16 + (kk & 7) * 2;
+}
+__device__ __forceinline__ int img_parts(const int4 d) { return (d.w >> 20) & 0xf; }
+// x = sum of `parts` bf16 values (successive residuals, round to nearest): hi, [mid,] lo.
+__device__ __forceinline__ void split_bf16(float x, int parts, unsigned short* out) {
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+    if (q >= parts) {
+      out[q] = 0;
+      continue;
+    }
+    unsigned short h;
+    asm("cvt.rn.bf16.f32 %0, %1;" : "=h"(h) : "f"(x));
+    out[q] = h;
+    x = x - __uint_as_float(unsigned(h) << 16);
+  }
 }
 
 // Spin on test_wait (try_wait may park the warp for a scheduler quantum).
@@ -688,14 +704,20 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const
 #endif
   const int c_begin = int(rank) * CPR;
   const int npass = P.npass;
-  const int wpass = npass > 1 ? 2 : 1;
+  // Split-bf16 parts of each operand: 1 (bf16), 2 (bf16x3: hi, lo), 3 (bf16x6: hi, mid, lo);
+  // the shared-memory layout holds MBX_LPARTS.
+  // (A bf16x6 context registers its plans with MBX_LPARTS 3, the others with 2: compile-time
+  // bounds for the MMA and image loops.)
+  const int parts = npass == 1 ? 1 : MBX_LPARTS;
+  const int wpass = parts;
   const int wchunk = MBX_M * MBX_KC * 2;
   const int wstage = wchunk * wpass;
-  constexpr int xchunk = MBX_LNT * MBX_KC * 2;  // one pass of one node chunk at the maximal tile
-  // The lo pass sits 64 B past the hi pass modulo 128, so the gather's 16-byte writes of a row's
-  // even and odd quads fall in different banks; chunks are xstride apart.
+  constexpr int xchunk = MBX_LNT * MBX_KC * 2;  // one part of one node chunk at the maximal tile
+  // Part q sits q * (xchunk + 64) into the chunk: the lo part 64 B past the hi part modulo 128, so
+  // the gather's 16-byte writes of a row's even and odd quads fall in different banks; chunks are
+  // xstride apart.
   constexpr int xlo = xchunk + 64;
-  constexpr int xstride = 2 * xchunk + 128;
+  constexpr int xstride = MBX_LPARTS * (xchunk + 64);
   unsigned char* wsm = smem + P.w_off;          // [CPR][wstage], resident for the whole launch
   unsigned char* xsm = smem + P.x_off;          // [CPR][xstride]; after the MMAs: stg (LXCH 0)
   float* stg = reinterpret_cast<float*>(xsm);   // [nt][128] this rank's partials (LXCH 0)
@@ -871,15 +893,15 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const
             // through the readiness counters; the bulk copies read it through the async proxy.
             asm volatile("fence.proxy.async.global;" ::: "memory");
             const int cb = nt * MBX_KC * 2;
-            const unsigned char* src =
-                P.img + L.img + (long long)(node0 / nt) * nt * (MBX_NCHUNKS * MBX_KC) * 4 + (long long)rank * CPR * 2 * cb;
+            const unsigned char* src = P.img + L.img + (long long)(node0 / nt) * nt * (MBX_NCHUNKS * MBX_KC) * 2 * parts +
+                                       (long long)rank * CPR * parts * cb;
 #pragma unroll 1
             for (int j = 0; j < CPR; ++j) {
-              mbar_expect_tx(&xraw[j], unsigned(2 * cb));
+              mbar_expect_tx(&xraw[j], unsigned(parts * cb));
               mbar_arrive_cnt(&xraw[j], MBX_LGATHER - 1);
               unsigned char* xs = xsm + j * xstride;
-              bulk_g2s(xs, src + (long long)j * 2 * cb, unsigned(cb), &xraw[j]);
-              bulk_g2s(xs + xlo, src + (long long)j * 2 * cb + cb, unsigned(cb), &xraw[j]);
+              for (int q = 0; q < parts; ++q)
+                bulk_g2s(xs + q * xlo, src + (long long)(j * parts + q) * cb, unsigned(cb), &xraw[j]);
             }
           }
         } else {
@@ -943,15 +965,19 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const
               const float4 a = *reinterpret_cast<const float4*>(xs + off);
               const float4 bq = *reinterpret_cast<const float4*>(xs + xlo + off);
               const float v[8] = {a.x, a.y, a.z, a.w, bq.x, bq.y, bq.z, bq.w};
-              unsigned hp[4], lp[4];
+              unsigned short sp[8][3];
 #pragma unroll
-              for (int q = 0; q < 4; ++q) {
-                hp[q] = pack_bf16x2(v[2 * q], v[2 * q + 1]);  // low half = element 2q
-                const float h0 = __uint_as_float(hp[q] << 16), h1 = __uint_as_float(hp[q] & 0xffff0000u);
-                lp[q] = pack_bf16x2(v[2 * q] - h0, v[2 * q + 1] - h1);
+              for (int e = 0; e < 8; ++e) split_bf16(v[e], parts, sp[e]);
+#pragma unroll
+              for (int q = 0; q < 3; ++q) {
+                if (q >= parts) break;
+                uint4 w;  // low half of each word = the even element
+                w.x = unsigned(sp[0][q]) | (unsigned(sp[1][q]) << 16);
+                w.y = unsigned(sp[2][q]) | (unsigned(sp[3][q]) << 16);
+                w.z = unsigned(sp[4][q]) | (unsigned(sp[5][q]) << 16);
+                w.w = unsigned(sp[6][q]) | (unsigned(sp[7][q]) << 16);
+                *reinterpret_cast<uint4*>(xs + q * xlo + off) = w;
               }
-              *reinterpret_cast<uint4*>(xs + off) = make_uint4(hp[0], hp[1], hp[2], hp[3]);
-              if (npass > 1) *reinterpret_cast<uint4*>(xs + xlo + off) = make_uint4(lp[0], lp[1], lp[2], lp[3]);
             }
           }
           // Chunk j is ready for the tensor core (async proxy): its MMAs overlap the next chunk.
@@ -975,15 +1001,21 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const
           tc_fence_after();
           const unsigned wa = smem_u32(wsm + j * wstage);
           const unsigned xa = smem_u32(xsm + j * xstride);
-          const unsigned long long a_hi = make_desc(wa, sbo), b_hi = make_desc(xa, sbo);
-          const unsigned long long a_lo = make_desc(wa + wchunk, sbo), b_lo = make_desc(xa + xlo, sbo);
+          const unsigned long long a0 = make_desc(wa, sbo), b0 = make_desc(xa, sbo);
+          const unsigned long long a1 = make_desc(wa + wchunk, sbo), b1 = make_desc(xa + xlo, sbo);
+          const unsigned long long a2 = make_desc(wa + 2 * wchunk, sbo), b2 = make_desc(xa + 2 * xlo, sbo);
 #pragma unroll
           for (int ks = 0; ks < MBX_KC / 16; ++ks) {
             const unsigned long long step = (unsigned long long)(ks * 16);
-            mma_bf16(tmem, a_hi + step, b_hi + step, idesc, (j | ks) ? 1u : 0u);
-            if (npass > 1) {
-              mma_bf16(tmem, a_hi + step, b_lo + step, idesc, 1u);
-              mma_bf16(tmem, a_lo + step, b_hi + step, idesc, 1u);
+            mma_bf16(tmem, a0 + step, b0 + step, idesc, (j | ks) ? 1u : 0u);
+            if (parts > 1) {  // bf16x3: + hi.lo + lo.hi
+              mma_bf16(tmem, a0 + step, b1 + step, idesc, 1u);
+              mma_bf16(tmem, a1 + step, b0 + step, idesc, 1u);
+            }
+            if (parts > 2) {  // bf16x6: + hi.lo' + mid.mid + lo'.hi (the terms down to 2^-24)
+              mma_bf16(tmem, a0 + step, b2 + step, idesc, 1u);
+              mma_bf16(tmem, a1 + step, b1 + step, idesc, 1u);
+              mma_bf16(tmem, a2 + step, b0 + step, idesc, 1u);
             }
           }
         }
@@ -1157,13 +1189,14 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const
             if (k == L.img_slot) {  // scattered into the consumer level's operand image
               const int4 d = dreg[t];
               if (d.y >= 0) {
-                int lo;
-                const long long a = img_addr(d, ug, &lo);
-                unsigned short h, l;
-                asm("cvt.rn.bf16.f32 %0, %1;" : "=h"(h) : "f"(ov[t][k]));
-                asm("cvt.rn.bf16.f32 %0, %1;" : "=h"(l) : "f"(ov[t][k] - __uint_as_float(unsigned(h) << 16)));
-                *reinterpret_cast<unsigned short*>(P.img + a) = h;
-                *reinterpret_cast<unsigned short*>(P.img + a + lo) = l;
+                int po;
+                const long long a = img_addr(d, ug, &po);
+                const int np = parts;  // the consumer's image has this launch's parts
+                unsigned short sp[3];
+                split_bf16(ov[t][k], np, sp);
+#pragma unroll
+                for (int q = 0; q < 3; ++q)  // static indices: sp stays in registers
+                  if (q < np) *reinterpret_cast<unsigned short*>(P.img + a + q * po) = sp[q];
               }
             }
           }
@@ -1388,17 +1421,17 @@ __device__ __forceinline__ void mbx_pointwise_body(const PwArgs& P) {
           const int4 d = P.img_dst[node];
           if (d.y >= 0) {
             const float x[4] = {v.x, v.y, v.z, v.w};
-            unsigned hp[2], lp[2];
+            const int np = mbx_gen::img_parts(d);
+            unsigned short sp[4][3];
 #pragma unroll
-            for (int q = 0; q < 2; ++q) {
-              hp[q] = mbx_gen::pack_bf16x2(x[2 * q], x[2 * q + 1]);
-              const float h0 = __uint_as_float(hp[q] << 16), h1 = __uint_as_float(hp[q] & 0xffff0000u);
-              lp[q] = mbx_gen::pack_bf16x2(x[2 * q] - h0, x[2 * q + 1] - h1);
-            }
-            int lo;
-            const long long a = mbx_gen::img_addr(d, e, &lo);
-            *reinterpret_cast<uint2*>(P.img + a) = make_uint2(hp[0], hp[1]);
-            *reinterpret_cast<uint2*>(P.img + a + lo) = make_uint2(lp[0], lp[1]);
+            for (int q = 0; q < 4; ++q) mbx_gen::split_bf16(x[q], np, sp[q]);
+            int po;
+            const long long a = mbx_gen::img_addr(d, e, &po);
+#pragma unroll
+            for (int q = 0; q < 3; ++q)  // static indices: sp stays in registers
+              if (q < np)
+                *reinterpret_cast<uint2*>(P.img + a + q * po) = make_uint2(unsigned(sp[0][q]) | (unsigned(sp[1][q]) << 16),
+                                                                         unsigned(sp[2][q]) | (unsigned(sp[3][q]) << 16));
           }
         }
       } else {

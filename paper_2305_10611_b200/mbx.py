@@ -18,9 +18,9 @@ from typing import Any, List, Optional, Sequence, Tuple
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libmbx.so")
+LIB_PATH = os.environ.get("MBX_LIB") or os.path.join(_HERE, "lib", "libmbx.so")  # MBX_LIB: A/B builds (tools/)
 
-PREC = {"fp32": 0, "bf16x3": 1, "bf16": 2}
+PREC = {"fp32": 0, "bf16x3": 1, "bf16": 2, "bf16x6": 3}
 OPS = ["dense", "add", "mul", "sigmoid", "tanh", "relu", "concat", "argmax", "fill"]
 
 
