@@ -1126,6 +1126,70 @@ int issue_batches(mbx_ctx* c, const std::vector<BatchLaunch>& Ls, size_t i) {
   return 1;
 }
 
+static bool leaf_mergeable(const mbx_ctx* c, const BatchLaunch& L) {
+  const PlanEntry& pe = c->plans[size_t(L.plan_id)];
+  if (pe.plan.ghost || !L.gathers.empty() || !L.sub.empty() || pe.prefix_plan >= 0 || L.shadow_out != 0 ||
+      L.img_slot >= 0 || L.out_node)
+    return false;
+  if (pe.da) return pe.tc_kind < 0 && !pe.tc_small && !pe.tc_exact;  // issue_batch's dense + argmax branch
+  return tc_small_kernel(pe);
+}
+
+bool mergeable(const mbx_ctx* c, const BatchLaunch& L) {
+  if (!L.sub.empty()) {
+    if (!L.gathers.empty()) return false;
+    for (const auto& S : L.sub)
+      if (!leaf_mergeable(c, S)) return false;
+    return true;
+  }
+  return leaf_mergeable(c, L);
+}
+
+bool same_shared(const mbx_ctx* c, const BatchLaunch& a, const BatchLaunch& b) {
+  if (a.plan_id != b.plan_id || a.sub.size() != b.sub.size()) return false;
+  if (!a.sub.empty()) {
+    for (size_t s = 0; s < a.sub.size(); ++s)
+      if (!same_shared(c, a.sub[s], b.sub[s])) return false;
+    return true;
+  }
+  const size_t ns = c->plans[size_t(a.plan_id)].exec_plan.shared_shapes.size();
+  return std::memcmp(c->meta.host + a.shared_meta, c->meta.host + b.shared_meta, ns * 8) == 0;
+}
+
+BatchLaunch merge_launches(mbx_ctx* c, const std::vector<const BatchLaunch*>& g) {
+  MBATCH_CHECK(!g.empty(), "merge_launches: empty group");
+  const BatchLaunch& f = *g[0];
+  BatchLaunch M;
+  M.plan_id = f.plan_id;
+  for (const BatchLaunch* L : g) M.b += L->b;
+  if (!f.sub.empty()) {  // split plan: merge the heads and the tails
+    for (size_t s = 0; s < f.sub.size(); ++s) {
+      std::vector<const BatchLaunch*> part;
+      for (const BatchLaunch* L : g) part.push_back(&L->sub[s]);
+      M.sub.push_back(merge_launches(c, part));
+    }
+    return M;
+  }
+  const PlanEntry& pe = c->plans[size_t(f.plan_id)];
+  const size_t nb = pe.exec_plan.batched_shapes.size(), no = pe.out_shapes.size();
+  std::vector<int64_t> rows, outs;
+  rows.reserve(size_t(M.b) * nb);
+  outs.reserve(size_t(M.b) * no);
+  for (const BatchLaunch* L : g) {
+    const int64_t* b = reinterpret_cast<const int64_t*>(c->meta.host + L->batched_meta);
+    rows.insert(rows.end(), b, b + size_t(L->b) * nb);
+    const int64_t* o = reinterpret_cast<const int64_t*>(c->meta.host + L->out_meta);
+    for (int i = 0; i < L->b; ++i)
+      for (size_t k = 0; k < no; ++k) outs.push_back(o[k] + int64_t(i) * pe.out_shapes[k].size());
+  }
+  M.shared_meta = f.shared_meta;
+  M.out_meta = f.out_meta;
+  M.batched_meta = meta_stage(c, rows.data(), rows.size() * 8);
+  M.out_node_meta = meta_stage(c, outs.data(), outs.size() * 8);
+  M.out_node = true;
+  return M;
+}
+
 void issue_pending(mbx_ctx* c) {
   std::vector<BatchLaunch> Ls;
   Ls.swap(c->pending);
@@ -1215,6 +1279,7 @@ void issue_batch(mbx_ctx* c, const BatchLaunch& L) {
     cuda_check(launch_dense_argmax(arena, meta_dev<int64_t>(c, L.shared_meta), meta_dev<int64_t>(c, L.batched_meta),
                                    L.b, int(pe.exec_plan.batched_shapes.size()), pe.da_a_batched, pe.da_a_idx,
                                    pe.da_w_idx, pe.da_k, pe.da_n, meta_dev<int64_t>(c, L.out_meta),
+                                   L.out_node ? meta_dev<int64_t>(c, L.out_node_meta) : nullptr,
                                    int(pe.exec_plan.outputs.size()), pe.da_out[0], pe.da_out[1], da_pdl, c->stream),
                "dense + argmax");
     ++c->launches;

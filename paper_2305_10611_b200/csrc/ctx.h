@@ -81,6 +81,10 @@ struct BatchLaunch {
   unsigned shadow_out = 0;       // pointwise launches: bit k = also write output slot k's shadow
   int img_slot = -1;             // pointwise launches: output slot scattered into operand images
   size_t img_dst_meta = 0;       // ... and its per-row destinations (int4, staged)
+  // Merged launch (merge_launches: several independent batches of one plan as one launch): node
+  // i's output k is at out_node_meta[i * nout + k] instead of out_meta[k] + i * size_k.
+  bool out_node = false;
+  size_t out_node_meta = 0;
 };
 
 // One persistent multi-level launch covering launches [start, start + n) of a flush.
@@ -216,6 +220,16 @@ void issue_batch(mbx_ctx* c, const BatchLaunch& L);
 // Issues Ls[i] — together with Ls[i + 1] in one launch when the two fuse (an MV-RNN combine
 // cell and the matrix add of the same nodes) — and returns how many launches it consumed.
 int issue_batches(mbx_ctx* c, const std::vector<BatchLaunch>& Ls, size_t i);
+// Whether launch L can be merged with other independent launches of its plan (merge_launches):
+// the exact small gate kernel, the dense + argmax kernel, and split plans made of them.
+bool mergeable(const mbx_ctx* c, const BatchLaunch& L);
+// Whether two launches of one plan read the same shared operands.
+bool same_shared(const mbx_ctx* c, const BatchLaunch& a, const BatchLaunch& b);
+// One launch over the nodes of g (mergeable launches of one plan, same shared operands, no node
+// reading another's output): node tables concatenated, per-node output offsets.
+BatchLaunch merge_launches(mbx_ctx* c, const std::vector<const BatchLaunch*>& g);
+// The exact small gate kernel serves this plan's batches in every precision (tc_launch).
+bool tc_small_kernel(const PlanEntry& pe);
 void issue_prefix(mbx_ctx* c, const BatchLaunch& L);
 
 // Persistent multi-level launches (kernels_tc.cu): if launches [i, i+n) (n >= 1) are consecutive

@@ -52,8 +52,8 @@ bool pdl_enabled();
 bool mv_cell_supported(int K, int N, int U);
 cudaError_t launch_mv_cell(const MvCellLaunch& L, cudaStream_t stream);
 cudaError_t launch_dense_argmax(float* arena, const int64_t* shared_off, const int64_t* batched_off, int b, int nb,
-                                int a_batched, int a_idx, int w_idx, int K, int N, const int64_t* out_base, int nout,
-                                int out0, int out1, int pdl, cudaStream_t stream);
+                                int a_batched, int a_idx, int w_idx, int K, int N, const int64_t* out_base,
+                                const int64_t* out_node, int nout, int out0, int out1, int pdl, cudaStream_t stream);
 size_t dense_argmax_smem(int K, int N);
 // [concat(rows...)] plans: out row i = the whole rows r_k(i) side by side (kernels_vm.cu).
 struct ConcatLaunch {

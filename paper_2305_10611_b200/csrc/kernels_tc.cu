@@ -807,6 +807,11 @@ static cudaError_t ensure_pack(mbx_ctx* c, TcState* st, const int64_t* shared_ho
   return cudaSuccess;
 }
 
+bool tc_small_kernel(const PlanEntry& pe) {
+  const auto* st = static_cast<const TcState*>(pe.tc_state);
+  return pe.tc_small && st && st->sfn;
+}
+
 cudaError_t tc_launch(mbx_ctx* c, const PlanEntry& pe, const BatchLaunch& L) {
   auto* st = static_cast<TcState*>(pe.tc_state);
   if ((pe.tc_small || (pe.tc_exact && (c->precision == MBX_PREC_FP32 || c->precision == MBX_PREC_BF16X6))) && st->sfn) {
@@ -815,6 +820,7 @@ cudaError_t tc_launch(mbx_ctx* c, const PlanEntry& pe, const BatchLaunch& L) {
     a.shared_off = meta_dev<long long>(c, L.shared_meta);
     a.batched_off = meta_dev<long long>(c, L.batched_meta);
     a.out_base = meta_dev<long long>(c, L.out_meta);
+    a.out_node = L.out_node ? meta_dev<long long>(c, L.out_node_meta) : nullptr;
     a.b = L.b;
     a.nb = int(pe.exec_plan.batched_shapes.size());
     for (int i = 0; i < 2; ++i) {

@@ -458,8 +458,9 @@ __global__ void fill_kernel(float* arena, int64_t off, int64_t n, float v) {
 // maximum, backend.cpp:164-173).
 __global__ void __launch_bounds__(256) dense_argmax_kernel(float* arena, const int64_t* shared_off,
                                                            const int64_t* batched_off, int nb, int a_batched, int a_idx,
-                                                           int w_idx, int K, int N, const int64_t* out_base, int nout,
-                                                           int out0, int out1, int pdl) {
+                                                           int w_idx, int K, int N, const int64_t* out_base,
+                                                           const int64_t* out_node, int nout, int out0, int out1,
+                                                           int pdl) {
   extern __shared__ __align__(16) float sm[];
   const int KP = (K + 7) & ~3;           // transposed row stride: 16-byte aligned, K + 4 .. K + 7
   float* ws = sm;                         // [K][N]
@@ -504,13 +505,15 @@ __global__ void __launch_bounds__(256) dense_argmax_kernel(float* arena, const i
   __syncthreads();
   const int outs[2] = {out0, out1};
   for (int k = 0; k < nout; ++k) {
+    // merged launches (several batches' nodes): per-node output offsets
+    const int64_t base = out_node ? out_node[node * nout + k] : out_base[k] + node * (outs[k] == 0 ? N : 1);
     if (outs[k] == 0) {
-      for (int j = tid; j < N; j += 256) arena[out_base[k] + node * N + j] = row[j];
+      for (int j = tid; j < N; j += 256) arena[base + j] = row[j];
     } else if (tid == 0) {
       int best = 0;
       for (int i = 1; i < N; ++i)
         if (row[i] > row[best]) best = i;
-      arena[out_base[k] + node] = static_cast<float>(best);
+      arena[base] = static_cast<float>(best);
     }
   }
 }
@@ -520,8 +523,8 @@ size_t dense_argmax_smem(int K, int N) {
 }
 
 cudaError_t launch_dense_argmax(float* arena, const int64_t* shared_off, const int64_t* batched_off, int b, int nb,
-                                int a_batched, int a_idx, int w_idx, int K, int N, const int64_t* out_base, int nout,
-                                int out0, int out1, int pdl, cudaStream_t stream) {
+                                int a_batched, int a_idx, int w_idx, int K, int N, const int64_t* out_base,
+                                const int64_t* out_node, int nout, int out0, int out1, int pdl, cudaStream_t stream) {
   const size_t smem = dense_argmax_smem(K, N);
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(dense_argmax_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
@@ -538,7 +541,7 @@ cudaError_t launch_dense_argmax(float* arena, const int64_t* shared_off, const i
   cfg.attrs = at;
   cfg.numAttrs = pdl ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, dense_argmax_kernel, arena, shared_off, batched_off, nb, a_batched, a_idx, w_idx, K, N,
-                            out_base, nout, out0, out1, pdl);
+                            out_base, out_node, nout, out0, out1, pdl);
 }
 
 cudaError_t launch_plan_vm(const VmLaunch& L, cudaStream_t stream) {

@@ -809,10 +809,17 @@ struct Executor::Impl {
       const size_t nb = plan.batched_shapes.size();
       meta_bytes += 8 * (plan.shared_shapes.size() + size_t(b.size) * nb * 2 + plan.outputs.size()) + 512 + 64 +
                     16 * size_t(b.size) + 16;  // operand-image destinations (plan_shadows)
+      // merge_launches: concatenated node tables + per-node output offsets (split plans: both halves)
+      const mbx::PlanEntry& pe = c->plans[size_t(s.plan_ids()[b.sig])];
+      for (int q : {pe.head_plan, pe.tail_plan, pe.head_plan < 0 ? int(s.plan_ids()[b.sig]) : -1})
+        if (q >= 0)
+          meta_bytes += 8 * size_t(b.size) * (c->plans[size_t(q)].exec_plan.batched_shapes.size() +
+                                               c->plans[size_t(q)].out_shapes.size()) + 16;
     }
     mbx::meta_reserve(c, meta_bytes);
 
     std::vector<mbx::BatchLaunch> launches;
+    std::vector<size_t> lbatch;  // launch -> its batch in trace.batches
     std::vector<int64_t> shared, batched, outs;
     for (auto& batch : batches) {
       if (batch.ghost) {
@@ -854,8 +861,10 @@ struct Executor::Impl {
       }
       trace.gather_bytes += gb;
       ++trace.kernel_launches;
+      lbatch.push_back(trace.batches.size());
       trace.batches.push_back(std::move(batch));
     }
+    if (!c->dry && !opts.time_batches) hoist_sinks(launches, lbatch);
     // Runs of consecutive batches of one tensor-core gate plan (e.g. every TreeLSTM internal
     // depth) become one persistent multi-level launch; their level tables are staged here, then
     // the split-bf16 shadows of the rows they gather are planned.
@@ -916,6 +925,60 @@ struct Executor::Impl {
       }
     }
     return true;
+  }
+
+  // Issue order of a flush (the trace keeps the reference's order).  A batch no later batch of
+  // the flush reads (a sink: NestedRNN's decision cells, whose results only the host and the
+  // next flush consume) need not run at its depth; mergeable sinks (the exact decision kernels)
+  // move behind the other batches and the sinks of one plan run as ONE launch.  NestedRNN: the
+  // inner steps between decision cells become one persistent levels run and a flush's ~10
+  // decision batches one head + one tail launch (instead of ~10 of each interleaved with
+  // single-level runs).  Results are unchanged: every node reads the same inputs.
+  std::vector<int> node_launch_;
+  void hoist_sinks(std::vector<mbx::BatchLaunch>& launches, const std::vector<size_t>& lbatch) {
+    const size_t n = launches.size();
+    if (n < 2) return;
+    auto& nodes = ex.nodes_;
+    if (node_launch_.size() < nodes.size()) node_launch_.resize(nodes.size(), -1);
+    for (size_t li = 0; li < n; ++li)
+      for (int id : trace.batches[lbatch[li]].node_ids) node_launch_[size_t(id)] = int(li);
+    std::vector<char> consumed(n, 0);
+    for (size_t li = 0; li < n; ++li)
+      for (int id : trace.batches[lbatch[li]].node_ids)
+        for (int p : nodes[size_t(id)].producers) {
+          const int q = node_launch_[size_t(p)];
+          if (q >= 0 && q != int(li)) consumed[size_t(q)] = 1;
+        }
+    for (size_t li = 0; li < n; ++li)
+      for (int id : trace.batches[lbatch[li]].node_ids) node_launch_[size_t(id)] = -1;
+    std::vector<size_t> keep, moved;
+    for (size_t li = 0; li < n; ++li) (!consumed[li] && mbx::mergeable(c, launches[li]) ? moved : keep).push_back(li);
+    if (moved.empty() || (moved.size() == 1 && (keep.empty() || moved[0] > keep.back()))) return;
+    // Sinks grouped by plan and shared operands (first-appearance order), each group one launch.
+    std::vector<std::vector<size_t>> groups;
+    for (size_t li : moved) {
+      bool placed = false;
+      for (auto& gr : groups)
+        if (mbx::same_shared(c, launches[gr[0]], launches[li])) {
+          gr.push_back(li);
+          placed = true;
+          break;
+        }
+      if (!placed) groups.push_back({li});
+    }
+    std::vector<mbx::BatchLaunch> out;
+    out.reserve(keep.size() + groups.size());
+    for (size_t li : keep) out.push_back(std::move(launches[li]));
+    for (const auto& gr : groups) {
+      if (gr.size() == 1) {
+        out.push_back(std::move(launches[gr[0]]));
+        continue;
+      }
+      std::vector<const mbx::BatchLaunch*> g;
+      for (size_t li : gr) g.push_back(&launches[li]);
+      out.push_back(mbx::merge_launches(c, g));
+    }
+    launches.swap(out);
   }
 
   // Reads the scalar decision of every blocked fiber whose value is now materialised with one

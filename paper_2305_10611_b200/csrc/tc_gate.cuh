@@ -1354,7 +1354,8 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS) mbx_small_dense(const 
   float o[MBX_NOUT];
   mbx_tail_exact(g, l, o);
 #pragma unroll
-  for (int k = 0; k < MBX_NOUT; ++k) P.arena[P.out_base[k] + node * U + ug] = o[k];
+  for (int k = 0; k < MBX_NOUT; ++k)
+    P.arena[(P.out_node ? P.out_node[node * MBX_NOUT + k] : P.out_base[k] + node * U) + ug] = o[k];
 }
 #endif  // MBX_SMALL_KERNEL
 
