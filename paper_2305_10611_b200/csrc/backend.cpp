@@ -37,10 +37,16 @@ namespace {
 // on the device goes through (in host submission order), so two such kernels never run
 // concurrently, back-to-back kernels in it start with little gap, and the contexts' own streams
 // stay free for everything else.
+// Two lanes: launches of at most half the SMs alternate between them (two run at once, and
+// together they always fit: no grid can wait for SMs the other holds); a larger launch takes
+// lane 0 after lane 1's work and lane 1 follows it (it runs alone).
 struct PersistentLane {
   std::mutex mu;  // held from begin to end: the dependency edges enclose one launch
-  cudaStream_t stream = nullptr;
-  cudaEvent_t done = nullptr;
+  cudaStream_t stream[2] = {nullptr, nullptr};
+  cudaEvent_t done[2] = {nullptr, nullptr};
+  int next = 0;
+  int cur = 0;          // lane of the launch between begin and end
+  bool whole = false;   // ... and whether it is a whole-device launch
 };
 PersistentLane& lane_of(int device) {
   static std::mutex m;
@@ -52,24 +58,36 @@ PersistentLane& lane_of(int device) {
 }
 }  // namespace
 
-cudaStream_t persistent_lane_begin(mbx_ctx* c) {
+cudaStream_t persistent_lane_begin(mbx_ctx* c, int ctas) {
   if (!c->serialize_persistent || c->dry) return c->stream;
   PersistentLane& L = lane_of(c->device);
   std::unique_lock<std::mutex> lock(L.mu);  // released on every error path below
-  if (!L.stream) {
+  if (!L.stream[0]) {
     // Highest priority: when SMs free up, the block scheduler places the lane kernel's CTAs first
     // (its resident CTAs wait at the grid barrier for the rest).
     int lo = 0, hi = 0;
     cudaDeviceGetStreamPriorityRange(&lo, &hi);
-    cuda_check(cudaStreamCreateWithPriority(&L.stream, cudaStreamNonBlocking, hi), "persistent lane stream");
-    cuda_check(cudaEventCreateWithFlags(&L.done, cudaEventDisableTiming), "persistent lane event");
+    for (int k = 0; k < 2; ++k) {
+      cuda_check(cudaStreamCreateWithPriority(&L.stream[k], cudaStreamNonBlocking, hi), "persistent lane stream");
+      cuda_check(cudaEventCreateWithFlags(&L.done[k], cudaEventDisableTiming), "persistent lane event");
+    }
   }
   if (!c->ev_persist) cuda_check(cudaEventCreateWithFlags(&c->ev_persist, cudaEventDisableTiming), "event");
+  // Half-lane launches only from half-budget contexts (their plans checked that two grids fit,
+  // clusters included); anything else runs alone.
+  L.whole = c->sm_budget > 74 || 2 * ctas > 148;
+  if (L.whole) {
+    L.cur = 0;
+    cuda_check(cudaStreamWaitEvent(L.stream[0], L.done[1], 0), "persistent lane wait");  // runs alone
+  } else {
+    L.cur = L.next;
+    L.next ^= 1;
+  }
   // The launch follows this context's work so far ...
   cuda_check(cudaEventRecord(c->ev_persist, c->stream), "persistent lane record");
-  cuda_check(cudaStreamWaitEvent(L.stream, c->ev_persist, 0), "persistent lane wait");
+  cuda_check(cudaStreamWaitEvent(L.stream[L.cur], c->ev_persist, 0), "persistent lane wait");
   lock.release();  // held until persistent_lane_end
-  return L.stream;
+  return L.stream[L.cur];
 }
 
 void persistent_lane_end(mbx_ctx* c) {
@@ -78,8 +96,9 @@ void persistent_lane_end(mbx_ctx* c) {
   std::unique_lock<std::mutex> lock(L.mu, std::adopt_lock);  // taken by persistent_lane_begin
   // ... and this context's later work follows the launch.  (The lock is released even if these
   // throw after a sticky device error, so the other workers fail instead of blocking.)
-  cuda_check(cudaEventRecord(L.done, L.stream), "persistent lane record");
-  cuda_check(cudaStreamWaitEvent(c->stream, L.done, 0), "persistent lane wait");
+  cuda_check(cudaEventRecord(L.done[L.cur], L.stream[L.cur]), "persistent lane record");
+  if (L.whole) cuda_check(cudaStreamWaitEvent(L.stream[1], L.done[0], 0), "persistent lane wait");
+  cuda_check(cudaStreamWaitEvent(c->stream, L.done[L.cur], 0), "persistent lane wait");
 }
 
 void persistent_lane_forget(mbx_ctx* c) { (void)c; }

@@ -183,6 +183,9 @@ int mbx_ctx_create(int device, int precision, mbx_ctx** out) {
   c->device = device;
   c->dry = device < 0;
   c->precision = precision;
+  // MBX_SM_BUDGET=74: plan persistent launches for half the device, as pool contexts do
+  // (measurements of the pool's configurations on one context).
+  if (const char* e = std::getenv("MBX_SM_BUDGET")) c->sm_budget = std::max(16, std::min(148, std::atoi(e)));
   int rc = guarded(nullptr, [&] {
     MBATCH_CHECK(precision >= MBX_PREC_FP32 && precision <= MBX_PREC_BF16X6, "unknown precision");
     if (!c->dry) {

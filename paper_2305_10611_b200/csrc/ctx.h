@@ -120,6 +120,9 @@ struct mbx_ctx {
   // counters) are chained through a per-device lane — each waits for the previous one to
   // complete — so two of them are never partially resident together; everything else overlaps.
   bool serialize_persistent = true;  // every context: any two may run concurrently on a device
+  // SMs one persistent launch may occupy: 148, or 74 for pool contexts (mbx_pool_create), whose
+  // persistent launches then run two at a time on the device's two lanes (persistent_lane_begin).
+  int sm_budget = 148;
   cudaEvent_t ev_persist = nullptr;
   // HBM arena: one virtual-address reservation, physical chunks mapped on demand, so offsets
   // (the reference's TensorHandle::offset) are stable while the arena grows.
@@ -179,7 +182,7 @@ void cuda_check(cudaError_t e, const char* what);
 // The per-device persistent-launch lane (see mbx_ctx::serialize_persistent): returns the stream
 // to launch on (the lane's, ordered after c->stream's work so far); persistent_lane_end orders
 // c->stream's later work after the launch.
-cudaStream_t persistent_lane_begin(mbx_ctx* c);
+cudaStream_t persistent_lane_begin(mbx_ctx* c, int ctas = 148);
 void persistent_lane_end(mbx_ctx* c);
 void persistent_lane_forget(mbx_ctx* c);  // before destroying c (its event may be the lane's last)
 // Waits for everything this context enqueued so far (an event: on a pool's shared stream it does

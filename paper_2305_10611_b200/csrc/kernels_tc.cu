@@ -504,13 +504,13 @@ __global__ void fill_u32(unsigned* p, size_t n, unsigned v) {
   for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) p[i] = v;
 }
 
-bool levels_layout(TcState& st, int k, int parts) {
+bool levels_layout(TcState& st, int k, int parts, int max_ctas) {
   auto al = [](int x) { return (x + 1023) / 1024 * 1024; };
   const int utiles = st.U / st.UC;
   TcState::LevelsCfg& C = st.lv[k];
   C = TcState::LevelsCfg{};
   auto try_cfg = [&](int S, int NT) {
-    if (st.nchunks % S != 0 || utiles * S > 148 || utiles > 64) return false;
+    if (st.nchunks % S != 0 || utiles * S > max_ctas || utiles > 64) return false;
     const int cpr = st.nchunks / S;
     if (cpr > 16) return false;
     const int xch = (S > 1 && k == 0 && utiles * S > 14 * 8) ? 1 : 0;
@@ -688,7 +688,7 @@ void tc_prepare(mbx_ctx* c, PlanEntry& pe) {
     st->src = gen_gate_source(*st);
     st->fn = load_kernel(c, st->src, "mbx_tc_gate");
     for (int k = 0; k < 2; ++k)
-      if (levels_layout(*st, k, c->precision == MBX_PREC_BF16X6 ? 3 : 2)) {
+      if (levels_layout(*st, k, c->precision == MBX_PREC_BF16X6 ? 3 : 2, c->sm_budget)) {
         if (k == 1 && st->lv[1].S == st->lv[0].S && st->lv[1].NT == st->lv[0].NT) {
           st->lv[1].S = 0;  // same configuration as deep
           continue;
@@ -997,7 +997,7 @@ static bool levels_enabled() {
 // Node tiles of each level for configuration C (the smallest power of two >= b, >= 16, at most
 // C.NT), and the node-tile groups (grid x) a launch uses.
 static int level_tiles(const TcState::LevelsCfg& C, int utiles, const std::vector<BatchLaunch>& Ls, size_t i, int n,
-                       std::vector<int>& nts) {
+                       std::vector<int>& nts, int sm_budget) {
   int max_tiles = 1;
   nts.assign(static_cast<size_t>(n), 16);
   for (int k = 0; k < n; ++k) {
@@ -1008,7 +1008,7 @@ static int level_tiles(const TcState::LevelsCfg& C, int utiles, const std::vecto
     nts[size_t(k)] = nt;
     max_tiles = std::max(max_tiles, (b + nt - 1) / nt);
   }
-  return std::clamp(max_tiles, 1, std::max(1, 148 / (utiles * C.S)));
+  return std::clamp(max_tiles, 1, std::max(1, sm_budget / (utiles * C.S)));
 }
 
 int plan_levels(mbx_ctx* c, const std::vector<BatchLaunch>& Ls, size_t i, size_t* table, int* groups, int* cfg) {
@@ -1036,13 +1036,13 @@ int plan_levels(mbx_ctx* c, const std::vector<BatchLaunch>& Ls, size_t i, size_t
   const int utiles = st->U / st->UC;
   std::vector<int> nts;
   int k = 0;
-  int ng = level_tiles(st->lv[0], utiles, Ls, i, n, nts);
+  int ng = level_tiles(st->lv[0], utiles, Ls, i, n, nts, c->sm_budget);
   if (n == 1 && st->lv[1].S > 0 && (st->lv[1].fn || c->dry)) {
     // One batch with more node tiles than the deep configuration has groups for, or a large one
     // (>= 128 nodes: the same MMA work per CTA, but a K split of 2 exchanges an eighth of the
     // partials of deep's 8; BiRNN's 510-node input transform 33 -> ~18 us): go wide.
     std::vector<int> nts1;
-    const int ng1 = level_tiles(st->lv[1], utiles, Ls, i, n, nts1);
+    const int ng1 = level_tiles(st->lv[1], utiles, Ls, i, n, nts1, c->sm_budget);
     if ((L0.b + nts[0] - 1) / nts[0] > ng || L0.b >= 128) {
       k = 1;
       ng = ng1;
@@ -1062,11 +1062,12 @@ int plan_levels(mbx_ctx* c, const std::vector<BatchLaunch>& Ls, size_t i, size_t
     // Every CTA must be resident at once (readiness counters between levels, peers' partials):
     // resident clusters (DSMEM exchange) or SMs vs what one node-tile group needs.
     int resident, per_group;
+    // (Half-device contexts: two such launches must fit at once.)
     if (C.S > 1 && C.xch == 0) {
-      resident = max_active_clusters(C.fn, C.S, C.smem);
+      resident = max_active_clusters(C.fn, C.S, C.smem) * c->sm_budget / 148;
       per_group = utiles;
     } else {
-      resident = 148;
+      resident = c->sm_budget;
       per_group = utiles * C.S;
     }
     if (resident < per_group) return 0;
@@ -1450,7 +1451,7 @@ void issue_levels(mbx_ctx* c, const std::vector<BatchLaunch>& Ls, size_t i, int 
     a.stamps = lstamps;
   }
   void* args[] = {&a};
-  if (needs_all) lc.stream = persistent_lane_begin(c);
+  if (needs_all) lc.stream = persistent_lane_begin(c, nctas);
   // A failed cooperative launch (e.g. too large to be co-resident) is an error, never retried as
   // a plain launch: a partly resident grid would spin at its first readiness wait.
   const cudaError_t le = cudaLaunchKernelExC(&lc, C.fn, args);

@@ -11,6 +11,7 @@
 // can stay resident across calls (inputs_resident).
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -56,6 +57,12 @@ int mbx_pool_create(int device, int precision, const char* model, int hidden, un
     mbx_ctx* c = nullptr;
     if (mbx_ctx_create(device, precision, &c)) return fail(mbx_last_error(nullptr));
     p->ctxs.push_back(c);
+    // Persistent launches on half the SMs, two at a time (several workers keep both lanes busy).
+    static const bool half = [] {
+      const char* e = std::getenv("MBX_POOL_HALF");
+      return !e || std::atoi(e) != 0;
+    }();
+    if (half && threads > 1) c->sm_budget = 74;
     mbx_model* m = nullptr;
     if (mbx_model_create(c, model, hidden, &m)) return fail(mbx_last_error(c));
     p->models.push_back(m);
