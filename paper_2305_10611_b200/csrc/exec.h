@@ -165,6 +165,15 @@ class Program {
   virtual ~Program() = default;
   // Body of @main for one instance; `args` are main's parameters in module order.
   virtual Task run(Executor& ex, Fiber& fb, std::vector<Val> args) const = 0;
+  // Programs without tensor-dependent control flow (no scalar awaits) can build the whole DFG
+  // without coroutines: run_flat makes the same emits, in the same order, from the same fiber
+  // states (phase, depth counter, join maxima) the fiber scheduler (run_runnable) would produce,
+  // and leaves each root fiber done with its result.  tests/test_flat_builder.py checks node
+  // tables and traces against the coroutine path.
+  virtual bool has_flat() const { return false; }
+  virtual void run_flat(Executor& ex, std::vector<Fiber*>& roots, std::vector<std::vector<Val>>& args) const {
+    (void)ex, (void)roots, (void)args;
+  }
 };
 
 class Executor {

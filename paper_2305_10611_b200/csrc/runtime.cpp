@@ -782,11 +782,13 @@ struct Executor::Impl {
   }
 
   // -- flush (executor.cpp:711-758) -------------------------------------------------------
+  size_t exec_lo_ = 0;  // every node below this index is executed
   bool flush(int phase_limit) {
     auto& nodes = ex.nodes_;
     std::vector<const DFGNode*> window;
-    for (const auto& n : nodes)
-      if (!n.executed && n.phase <= phase_limit) window.push_back(&n);
+    while (exec_lo_ < nodes.size() && nodes[exec_lo_].executed) ++exec_lo_;  // (nodes before: all executed)
+    for (size_t k = exec_lo_; k < nodes.size(); ++k)
+      if (!nodes[k].executed && nodes[k].phase <= phase_limit) window.push_back(&nodes[k]);
     if (window.empty()) return false;
     trace.flush_boundaries.push_back(static_cast<int>(trace.batches.size()));
     auto ts0 = clk::now();
@@ -1212,6 +1214,11 @@ EvalResult Executor::run() {
   nodes_.reserve(I.s.node_hint());    // the previous evaluation's node count: no regrowth
   fibers_.reserve(I.s.fiber_hint());
   int64_t eti = 0, edi = 0;  // encoded inputs: cursor into the token / data streams
+  const char* flat_env = std::getenv("MBX_FLAT_DFG");  // 0: the coroutine path (tests compare both)
+  const bool flat_ok = !flat_env || std::atoi(flat_env) != 0;
+  const bool flat = flat_ok && m.program->has_flat();
+  std::vector<std::vector<Val>> flat_args;
+  std::vector<Fiber*> flat_roots;
   for (size_t i = 0; i < size_t(I.batch); ++i) {
     auto fb = std::make_unique<Fiber>();
     fb->id = static_cast<int>(fibers_.size());
@@ -1231,11 +1238,22 @@ EvalResult Executor::run() {
       }
     }
     Fiber* raw = fb.get();
-    fb->root = m.program->run(*this, *raw, std::move(args));
+    if (flat) {
+      flat_roots.push_back(raw);
+      flat_args.push_back(std::move(args));
+    } else {
+      fb->root = m.program->run(*this, *raw, std::move(args));
+    }
     fibers_.push_back(std::move(fb));
   }
   if (I.enc) MBATCH_CHECK(eti == I.enc->ntok && edi == I.enc->ndata, "hostval encoding: trailing data");
   I.upload_inputs();
+  if (flat) {
+    auto tf = clk::now();
+    m.program->run_flat(*this, flat_roots, flat_args);
+    for (Fiber* fb : flat_roots) MBATCH_CHECK(fb->status == FiberStatus::kDone, "flat DFG builder left a fiber running");
+    I.timing.host_fibers_us += std::chrono::duration<double, std::micro>(clk::now() - tf).count();
+  }
 
   while (true) {
     auto tf = clk::now();

@@ -13,6 +13,7 @@
 // (tests/golden/*.json) and every trace against the reference executor's.
 #include "mbatch/zoo.hpp"
 
+#include <deque>
 #include <random>
 
 #include "exec.h"
@@ -235,8 +236,113 @@ Task tlstm(Executor& ex, Fiber& fb, const TreeLstmParams& P, Val t) {
   co_return Val::tuple({Executor::out(n, 1), Executor::out(n, 0)});
 }
 
+// The fiber scheduler's order for tlstm without coroutines (Program::run_flat): light fibers in
+// creation order, resumed in passes over the growing list exactly as run_runnable does — a tree
+// node's fiber spawns its two children (appended) and blocks; leaves emit and finish in the same
+// pass; a parent resumes in the pass after its last child finished (its depth counter the max of
+// its children's), emits its cell, and finishes; a root then takes stage 1 and the classifier.
+struct FlatTree {
+  Fiber* fb;
+  const Val* t;
+  int parent;
+  int state;  // 0: not started, 1: resumed after its join
+  int kids[2];
+  int inst;   // instance (its params)
+  Val res;    // (h, c) of a finished subtree
+};
+
+template <class Leaf, class Node, class Root>
+void run_tree_flat(Executor& ex, std::vector<Fiber*>& roots, const std::vector<const Val*>& trees, Leaf leaf, Node node,
+                   Root root_done) {
+  std::deque<Fiber> extra;
+  std::vector<FlatTree> F;
+  F.reserve(roots.size() * 32);
+  for (size_t i = 0; i < roots.size(); ++i) F.push_back(FlatTree{roots[i], trees[i], -1, 0, {-1, -1}, int(i), Val{}});
+  // A pass of run_runnable visits, in index order, the fibers made runnable in the previous pass
+  // (parents whose last child finished: lower indices than anything created since), then every
+  // fiber created during this pass (appended, runnable).  No rescans of blocked fibers.
+  std::vector<int> cur(roots.size()), next;
+  for (size_t i = 0; i < roots.size(); ++i) cur[i] = int(i);
+  auto resume = [&](size_t i) {
+    Fiber& fb = *F[i].fb;
+    const bool is_root = F[i].parent < 0;
+    if (F[i].state == 0) {
+      if (is_root) ex.stage(fb, 0);
+      const Val& t = *F[i].t;
+      if (t.ctor != 0) {  // Node(l, r): concurrent children, then join
+        for (int k = 0; k < 2; ++k) {
+          Fiber& cf = extra.emplace_back();
+          cf.instance = fb.instance;
+          cf.phase = fb.phase;
+          cf.depth_counter = fb.depth_counter;
+          F[i].kids[k] = int(F.size());
+          F.push_back(FlatTree{&cf, &t.at(size_t(k)), int(i), 0, {-1, -1}, F[i].inst, Val{}});
+        }
+        fb.status = runtime::FiberStatus::kBlockedJoin;
+        fb.pending_children = 2;
+        F[i].state = 1;
+        return;
+      }
+      F[i].res = leaf(fb, F[i].inst, t);
+    } else {
+      const FlatTree &a = F[size_t(F[i].kids[0])], &b = F[size_t(F[i].kids[1])];
+      fb.depth_counter = std::max(fb.depth_counter, a.fb->depth_counter);
+      fb.depth_counter = std::max(fb.depth_counter, b.fb->depth_counter);
+      F[i].res = node(fb, F[i].inst, a.res, b.res);
+    }
+    if (is_root) root_done(fb, F[i].inst, F[i].res);
+    fb.status = runtime::FiberStatus::kDone;
+    fb.has_result = true;
+    const int p = F[i].parent;
+    if (p >= 0) {
+      Fiber& pf = *F[size_t(p)].fb;
+      if (--pf.pending_children == 0 && pf.status == runtime::FiberStatus::kBlockedJoin) {
+        pf.status = runtime::FiberStatus::kRunnable;
+        next.push_back(p);
+      }
+    }
+  };
+  while (!cur.empty()) {
+    const size_t created = F.size();
+    next.clear();
+    for (int i : cur) resume(size_t(i));
+    for (size_t i = created; i < F.size(); ++i) resume(i);
+    std::sort(next.begin(), next.end());
+    cur.swap(next);
+  }
+}
+
 class TreeLstmProgram : public runtime::Program {
  public:
+  bool has_flat() const override { return true; }
+  void run_flat(Executor& ex, std::vector<Fiber*>& roots, std::vector<std::vector<Val>>& args) const override {
+    std::vector<TreeLstmParams> P;
+    std::vector<const Val*> trees;
+    P.reserve(args.size());
+    for (auto& a : args) {
+      P.push_back(TreeLstmParams{a[0], a[1], a[2], a[3], a[4], a[5], a[6], a[7], a[8], a[9], a[10]});
+      trees.push_back(&a[11]);
+    }
+    run_tree_flat(
+        ex, roots, trees,
+        [&](Fiber& fb, int i, const Val& t) {  // tlstm's Leaf branch
+          const TreeLstmParams& p = P[size_t(i)];
+          Val xt = Executor::out(ex.emit(fb, 3, {&t.at(0), &p.x_wt, &p.x_bias}), 0);
+          int n = ex.emit(fb, 1, {&p.hz, &p.hz, &p.i_wt, &xt, &p.fl_wt, &p.fr_wt, &p.u_wt, &p.cz, &p.cz});
+          return Val::tuple({Executor::out(n, 1), Executor::out(n, 0)});
+        },
+        [&](Fiber& fb, int i, const Val& l, const Val& r) {  // tlstm's Node branch after the join
+          const TreeLstmParams& p = P[size_t(i)];
+          const Val &lh = l.at(0), &lc = l.at(1), &rh = r.at(0), &rc = r.at(1);
+          int n = ex.emit(fb, 2, {&lh, &rh, &p.i_wt, &p.xn, &p.fl_wt, &p.fr_wt, &p.u_wt, &lc, &rc});
+          return Val::tuple({Executor::out(n, 1), Executor::out(n, 0)});
+        },
+        [&](Fiber& fb, int i, const Val& res) {  // TreeLstmProgram::run after co_await tlstm
+          const TreeLstmParams& p = P[size_t(i)];
+          ex.stage(fb, 1);
+          fb.result = Executor::out(ex.emit(fb, 0, {&res.at(0), &p.c_wt, &p.cbias}), 0);
+        });
+  }
   Task run(Executor& ex, Fiber& fb, std::vector<Val> a) const override {
     TreeLstmParams P{a[0], a[1], a[2], a[3], a[4], a[5], a[6], a[7], a[8], a[9], a[10]};
     ex.stage(fb, 0);
@@ -270,6 +376,31 @@ Task mv(Executor& ex, Fiber& fb, const MvParams& P, Val t) {
 
 class MvRnnProgram : public runtime::Program {
  public:
+  bool has_flat() const override { return true; }
+  void run_flat(Executor& ex, std::vector<Fiber*>& roots, std::vector<std::vector<Val>>& args) const override {
+    std::vector<MvParams> P;
+    std::vector<const Val*> trees;
+    P.reserve(args.size());
+    for (auto& a : args) {
+      P.push_back(MvParams{a[0], a[1], a[2], a[3]});
+      trees.push_back(&a[4]);
+    }
+    run_tree_flat(
+        ex, roots, trees,
+        [&](Fiber&, int, const Val& t) { return Val::tuple({t.at(0), t.at(1)}); },  // mv's Leaf branch
+        [&](Fiber& fb, int i, const Val& l, const Val& r) {                        // mv's Node branch
+          const MvParams& p = P[size_t(i)];
+          const Val &lv = l.at(0), &lm = l.at(1), &rv = r.at(0), &rm = r.at(1);
+          int n1 = ex.emit(fb, 1, {&lv, &rm, &rv, &lm, &p.v_wt, &p.vbias});
+          int n2 = ex.emit(fb, 2, {&lm, &rm});
+          return Val::tuple({Executor::out(n1, 0), Executor::out(n2, 0)});
+        },
+        [&](Fiber& fb, int i, const Val& res) {  // MvRnnProgram::run after co_await mv
+          const MvParams& p = P[size_t(i)];
+          ex.stage(fb, 1);
+          fb.result = Executor::out(ex.emit(fb, 0, {&res.at(0), &p.c_wt, &p.cbias}), 0);
+        });
+  }
   Task run(Executor& ex, Fiber& fb, std::vector<Val> a) const override {
     MvParams P{a[0], a[1], a[2], a[3]};
     ex.stage(fb, 0);
