@@ -150,6 +150,23 @@ std::pair<std::string, Shape> P(const std::string& n, int r, int c) { return {n,
 // =============================================================================================
 // Model bodies.  Each Program receives @main's parameters in module order.
 
+// Programs without awaits (rnn, birnn, fig5): each root fiber runs start to finish when the first
+// scheduler pass resumes it, in instance order — run_flat calls the same body in that order.
+class StraightProgram : public runtime::Program {
+ public:
+  virtual Val body(Executor& ex, Fiber& fb, std::vector<Val>& a) const = 0;
+  Task run(Executor& ex, Fiber& fb, std::vector<Val> a) const override { co_return body(ex, fb, a); }
+  bool has_flat() const override { return true; }
+  void run_flat(Executor& ex, std::vector<Fiber*>& roots, std::vector<std::vector<Val>>& args) const override {
+    for (size_t i = 0; i < roots.size(); ++i) {
+      Fiber& fb = *roots[i];
+      fb.result = body(ex, fb, args[i]);
+      fb.has_result = true;
+      fb.status = runtime::FiberStatus::kDone;
+    }
+  }
+};
+
 // ---- rnn (zoo.cpp:26-45) / birnn (zoo.cpp:47-76) ----------------------------------------------
 // @rnn: per element, inp_linear = bias + dense(inp, i_wt) [hoisted block], then
 // new_state = sigmoid(inp_linear + dense(state, h_wt)) [recurrent block].
@@ -166,9 +183,9 @@ std::vector<Val> rnn_chain(Executor& ex, Fiber& fb, const Val& inps, Val state, 
   return out;
 }
 
-class RnnProgram : public runtime::Program {
+class RnnProgram : public StraightProgram {
  public:
-  Task run(Executor& ex, Fiber& fb, std::vector<Val> a) const override {
+  Val body(Executor& ex, Fiber& fb, std::vector<Val>& a) const override {
     // a: rnn_bias, rnn_i_wt, rnn_h_wt, rnn_init, c_wt, cbias, inps
     ex.stage(fb, 0);
     std::vector<Val> res = rnn_chain(ex, fb, a[6], a[3], a[0], a[1], a[2], 1, 2);
@@ -181,13 +198,13 @@ class RnnProgram : public runtime::Program {
       deepest = std::max(deepest, fb.depth_counter);
     }
     fb.depth_counter = deepest;
-    co_return Val::list(std::move(out));
+    return Val::list(std::move(out));
   }
 };
 
-class BirnnProgram : public runtime::Program {
+class BirnnProgram : public StraightProgram {
  public:
-  Task run(Executor& ex, Fiber& fb, std::vector<Val> a) const override {
+  Val body(Executor& ex, Fiber& fb, std::vector<Val>& a) const override {
     // a: f_bias, f_i_wt, f_h_wt, f_init, b_bias, b_i_wt, b_h_wt, b_init, inps_list
     ex.stage(fb, 0);
     std::vector<Val> rev(a[8].items->rbegin(), a[8].items->rend());
@@ -206,7 +223,7 @@ class BirnnProgram : public runtime::Program {
       deepest = std::max(deepest, fb.depth_counter);
     }
     fb.depth_counter = deepest;
-    co_return Val::list(std::move(out));
+    return Val::list(std::move(out));
   }
 };
 
@@ -497,9 +514,9 @@ class StackRnnProgram : public runtime::Program {
 };
 
 // ---- fig5 (zoo.cpp:243-259) ---------------------------------------------------------------
-class Fig5Program : public runtime::Program {
+class Fig5Program : public StraightProgram {
  public:
-  Task run(Executor& ex, Fiber& fb, std::vector<Val> a) const override {
+  Val body(Executor& ex, Fiber& fb, std::vector<Val>& a) const override {
     // a: a_wt, abias, b_wt, bbias, x, sel
     ex.stage(fb, 0);
     Val r;
@@ -513,7 +530,7 @@ class Fig5Program : public runtime::Program {
       r = Executor::out(ex.emit(fb, 0, {&e, &a[2], &a[3]}), 0);
     }
     ex.stage(fb, 1);
-    co_return Executor::out(ex.emit(fb, 0, {&r, &a[2], &a[3]}), 0);
+    return Executor::out(ex.emit(fb, 0, {&r, &a[2], &a[3]}), 0);
   }
 };
 

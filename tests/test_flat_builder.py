@@ -10,7 +10,7 @@ import pytest
 from conftest import trace_counters, trace_rows
 from test_zoo_parity import _node_rows
 
-FLAT_MODELS = ["treelstm", "mvrnn"]
+FLAT_MODELS = ["treelstm", "mvrnn", "rnn", "birnn", "fig5"]
 VARIANTS = [{}, {"scheduler": "agenda"}, {"gather": "explicit"}, {"hoist": False}, {"phases": False}]
 
 
