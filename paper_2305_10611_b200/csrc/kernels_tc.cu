@@ -117,11 +117,16 @@ struct TcState {
   void* sfn = nullptr;
   int s_npc = 0, s_uc = 0, s_kb = 0, s_st = 1, s_smem = 0;
   bool s_attr = false;
-  // Narrow variant (8-unit slices, compiled on first use) for batches too small to give the wide
-  // one's grid a wave: more CTAs, each streaming a quarter of the weight columns.
-  void* sfn_n = nullptr;
-  int n_kb = 0, n_st = 1, n_smem = 0;
-  bool n_attr = false;
+  // Narrow variant (8-unit slices of 8 nodes, compiled on first use) for batches too small to
+  // give the wide one's grid a wave.  (4- and 2-unit slices were measured: the same kernel times,
+  // but the flush slower in situ, 81-85 -> 96-106 us for TreeLSTM-256 b8.)
+  struct SmallVar {
+    void* fn = nullptr;
+    int kb = 0, st = 1, smem = 0, threads = 0;
+    bool attr = false;
+  };
+  SmallVar nv;
+  bool narrow_ok = false;
   bool attr_set = false;
   // Persistent multi-level variant (mbx_tc_levels): K-split ranks, maximal node tile, smem layout.
   // mbx_tc_levels configurations: [0] deep — the largest K split, weight slice resident, for runs
@@ -309,6 +314,13 @@ std::string gen_levels_source(const TcState& st, int k) {
 }
 
 // Source of the bit-exact small-dense kernel (plans with few output columns, e.g. a classifier).
+// Threads of a small-dense block: one per (gate, node, unit) when that fits 256 (the gates split
+// over threads), else one per (node, unit); whole warps, at least 64.
+int small_threads(const TcState& st, int npc, int uc) {
+  const int t = npc * uc * st.G <= kTcThreads ? npc * uc * st.G : npc * uc;
+  return std::clamp((t + 31) / 32 * 32, 64, kTcThreads);
+}
+
 std::string gen_small_source(const TcState& st, int npc, int uc, int kb, int stages) {
   std::ostringstream o;
   o << jit::prelude_source();
@@ -317,7 +329,8 @@ std::string gen_small_source(const TcState& st, int npc, int uc, int kb, int sta
     << "\n#define MBX_NPIECES " << st.npieces << "\n#define MBX_PK0 " << st.piece_k[0] << "\n#define MBX_NLOADS "
     << st.prog.nloads << "\n#define MBX_NOUT " << st.prog.nout << "\n#define MBX_SNPC " << npc
     << "\n#define MBX_SUC " << uc << "\n#define MBX_SKB " << kb << "\n#define MBX_SST " << stages
-    << "\n";
+    << "\n#define MBX_SGS " << (npc * uc * st.G <= kTcThreads ? st.G : 1) << "\n#define MBX_STHREADS "
+    << small_threads(st, npc, uc) << "\n";
   o << gen_tail(st.prog, false, false, true);
   o << jit::kernel_source();
   return o.str();
@@ -671,9 +684,11 @@ void tc_prepare(mbx_ctx* c, PlanEntry& pe) {
       staging(st->s_uc, st->s_npc, st->s_kb, st->s_st, st->s_smem);
       const std::string ssrc = gen_small_source(*st, st->s_npc, st->s_uc, st->s_kb, st->s_st);
       st->sfn = load_kernel(c, ssrc, "mbx_small_dense");
-      if (st->s_uc > 8 && st->U % 8 == 0) {
-        st->n_kb = kb0;
-        staging(8, 8, st->n_kb, st->n_st, st->n_smem);
+      if (st->U % 8 == 0 && st->s_uc > 8) {
+        st->narrow_ok = true;
+        st->nv.kb = kb0;
+        staging(8, 8, st->nv.kb, st->nv.st, st->nv.smem);
+        st->nv.threads = small_threads(*st, 8, 8);
       }
       pe.tc_exact = true;
       // Few output columns: tensor-core tiles would be mostly padding; exact in every precision.
@@ -833,11 +848,15 @@ cudaError_t tc_launch(mbx_ctx* c, const PlanEntry& pe, const BatchLaunch& L) {
     fill_loads(st->prog, a.loads);
     // The wide variant unless its grid would leave most SMs idle (a few nodes over few unit
     // slices, e.g. TreeLSTM-256 b8's internal depths): then 8-unit slices, 4x the CTAs.
-    const bool narrow = st->n_kb > 0 && ((L.b + st->s_npc - 1) / st->s_npc) * (st->U / st->s_uc) < 74;
-    if (narrow && !st->sfn_n) st->sfn_n = load_kernel(c, gen_small_source(*st, 8, 8, st->n_kb, st->n_st), "mbx_small_dense");
-    void* fn = narrow ? st->sfn_n : st->sfn;
-    const int npc = narrow ? 8 : st->s_npc, uc = narrow ? 8 : st->s_uc, smem = narrow ? st->n_smem : st->s_smem;
-    bool& attr = narrow ? st->n_attr : st->s_attr;
+    // The wide variant unless its grid would leave most SMs idle (a few nodes over few unit
+    // slices, e.g. TreeLSTM-256 b8's internal depths): then 8-unit slices, 4x the CTAs.
+    TcState::SmallVar* nv =
+        st->narrow_ok && ((L.b + st->s_npc - 1) / st->s_npc) * (st->U / st->s_uc) < 74 ? &st->nv : nullptr;
+    if (nv && !nv->fn) nv->fn = load_kernel(c, gen_small_source(*st, 8, 8, nv->kb, nv->st), "mbx_small_dense");
+    void* fn = nv ? nv->fn : st->sfn;
+    const int npc = nv ? 8 : st->s_npc, uc = nv ? 8 : st->s_uc, smem = nv ? nv->smem : st->s_smem;
+    const int threads = nv ? nv->threads : small_threads(*st, st->s_npc, st->s_uc);
+    bool& attr = nv ? nv->attr : st->s_attr;
     if (!attr) {
       cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       if (e != cudaSuccess) return e;
@@ -845,7 +864,7 @@ cudaError_t tc_launch(mbx_ctx* c, const PlanEntry& pe, const BatchLaunch& L) {
     }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(unsigned((L.b + npc - 1) / npc), unsigned(st->U / uc));
-    cfg.blockDim = dim3(kTcThreads);
+    cfg.blockDim = dim3(unsigned(threads));
     cfg.dynamicSmemBytes = size_t(smem);
     cfg.stream = c->stream;
     cudaLaunchAttribute at[1];
@@ -855,8 +874,36 @@ cudaError_t tc_launch(mbx_ctx* c, const PlanEntry& pe, const BatchLaunch& L) {
       cfg.attrs = at;
       cfg.numAttrs = 1;
     }
+    static const bool sstamps = std::getenv("MBX_SMALL_STAMPS") != nullptr;  // profiling aid
+    static unsigned long long* sbuf = nullptr;
+    const int nctas = int(cfg.gridDim.x * cfg.gridDim.y);
+    if (sstamps) {
+      if (!sbuf) cudaMalloc(&sbuf, size_t(4096) * 8 * 8);
+      cudaMemsetAsync(sbuf, 0, size_t(nctas) * 8 * 8, c->stream);
+      a.stamps = sbuf;
+    }
     void* args[] = {&a};
-    return cudaLaunchKernelExC(&cfg, fn, args);
+    cudaError_t le = cudaLaunchKernelExC(&cfg, fn, args);
+    if (sstamps && le == cudaSuccess) {
+      std::vector<unsigned long long> h(size_t(nctas) * 8);
+      cudaStreamSynchronize(c->stream);
+      cudaMemcpy(h.data(), sbuf, h.size() * 8, cudaMemcpyDeviceToHost);
+      unsigned long long t0 = ~0ull;
+      for (int i = 0; i < nctas; ++i) t0 = std::min(t0, h[size_t(i) * 8]);
+      std::fprintf(stderr, "small b=%d grid=%dx%d threads=%d uc=%d:", L.b, cfg.gridDim.x, cfg.gridDim.y, threads, uc);
+      for (int k = 0; k < 6; ++k) {
+        double mx = 0, sum = 0;
+        int cnt = 0;
+        for (int i = 0; i < nctas; ++i)
+          if (h[size_t(i) * 8 + k]) {
+            const double v = double(h[size_t(i) * 8 + k] - t0) / 1000.0;
+            mx = std::max(mx, v), sum += v, ++cnt;
+          }
+        std::fprintf(stderr, " s%d %.2f/%.2f", k, cnt ? sum / cnt : 0.0, mx);
+      }
+      std::fprintf(stderr, "\n");
+    }
+    return le;
   }
   if (pe.tc_kind == 2) {
     PwArgs a{};
@@ -871,7 +918,14 @@ cudaError_t tc_launch(mbx_ctx* c, const PlanEntry& pe, const BatchLaunch& L) {
     fill_loads(st->prog, a.loads);
     // 16-byte variant when every row it touches is 16-byte aligned (checked on the host copies
     // of this batch's offset tables).
-    bool v4 = st->fn4 != nullptr;
+    // FP32 contexts: glibc-exact activations (bit-identical to the reference); the tensor-core
+    // precisions use the fast ones, as their gate tails do.
+    const bool exact = c->precision == MBX_PREC_FP32 || c->precision == MBX_PREC_BF16X6;
+    // The exact activations are long dependent chains (double-precision expf, fdlibm expm1f,
+    // divisions): one element per thread and enough CTAs to cover the SMs beats 16-byte
+    // vectors on few SMs (TreeLSTM-256 b8 leaf cells, 73 x 256 elements: 19 CTAs of 4 elements
+    // per thread), unless a later tensor-core level needs this launch's shadows or images.
+    bool v4 = st->fn4 != nullptr && !(exact && !L.shadow_out && L.img_slot < 0);
     if (v4) {
       const int64_t* sh = reinterpret_cast<const int64_t*>(c->meta.host + L.shared_meta);
       const int64_t* bt = reinterpret_cast<const int64_t*>(c->meta.host + L.batched_meta);
@@ -894,10 +948,12 @@ cudaError_t tc_launch(mbx_ctx* c, const PlanEntry& pe, const BatchLaunch& L) {
     a.img_dst = L.img_slot >= 0 ? meta_dev<int4>(c, L.img_dst_meta) : nullptr;
     if ((L.shadow_out || L.img_slot >= 0) && !v4) return cudaErrorInvalidValue;
     const int64_t total = int64_t(L.b) * a.E / (v4 ? 4 : 1);
-    const int blocks = int(std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, 148 * 8)));
+    // Block size: 256, or smaller (>= 64) so that a small batch still spreads over all SMs.
+    const int threads = int(std::clamp<int64_t>(((total + 147) / 148 + 31) / 32 * 32, 64, 256));
+    const int blocks = int(std::max<int64_t>(1, std::min<int64_t>((total + threads - 1) / threads, 148 * 8)));
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(blocks);
-    cfg.blockDim = dim3(256);
+    cfg.blockDim = dim3(threads);
     cfg.stream = c->stream;
     cudaLaunchAttribute at[1];
     if (pdl_enabled()) {
@@ -907,9 +963,6 @@ cudaError_t tc_launch(mbx_ctx* c, const PlanEntry& pe, const BatchLaunch& L) {
       cfg.numAttrs = 1;
     }
     void* args[] = {&a};
-    // FP32 contexts: glibc-exact activations (bit-identical to the reference); the tensor-core
-    // precisions use the fast ones, as their gate tails do.
-    const bool exact = c->precision == MBX_PREC_FP32 || c->precision == MBX_PREC_BF16X6;  // glibc-exact activations
     void* fn = exact ? (v4 ? st->fn4 : st->fn) : (v4 ? st->fn_fast4 : st->fn_fast);
     return cudaLaunchKernelExC(&cfg, fn, args);
   }

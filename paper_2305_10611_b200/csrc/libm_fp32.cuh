@@ -58,8 +58,10 @@ MBX_HD double u2d(uint64_t u) { double d; memcpy(&d, &u, 8); return d; }
 #endif
 
 // 2^(i/32) as doubles, bit patterns minus (i << 52)/32, as in glibc's __exp2f_data.tab.
+// (Global memory read through the L1, not __constant__: the 32 lanes of a warp index it
+// divergently, which the constant cache serialises.)
 #if defined(__CUDACC__)
-__device__ __constant__
+__device__
 #endif
 static const uint64_t kExp2fTab[32] = {
     0x3ff0000000000000ull, 0x3fefd9b0d3158574ull, 0x3fefb5586cf9890full, 0x3fef9301d0125b51ull,
@@ -72,7 +74,11 @@ static const uint64_t kExp2fTab[32] = {
     0x3fef5818dcfba487ull, 0x3fef7c97337b9b5full, 0x3fefa4afa2a490daull, 0x3fefd0765b6e4540ull,
 };
 
+#if defined(__CUDA_ARCH__)
+MBX_HD uint64_t exp2f_tab(uint32_t i) { return (uint64_t)__ldg(reinterpret_cast<const unsigned long long*>(&kExp2fTab[i])); }
+#else
 MBX_HD uint64_t exp2f_tab(uint32_t i) { return kExp2fTab[i]; }
+#endif
 
 // expf: |x| >= 88 / NaN special cases, then x*32/ln2 = k + r, 2^(k/32) from the table times a
 // cubic in r.

@@ -78,6 +78,7 @@ struct SmallArgs {
   const long long* batched_off;
   const long long* out_base;
   const long long* out_node;  // merged launches: [b][nout] output offsets (else out_base[k] + node * U)
+  unsigned long long* stamps; // MBX_SMALL_STAMPS profiling runs only: [CTA][8] globaltimer phase stamps
   int b, nb;
   int piece_kind[2], piece_idx[2], piece_off[2];
   int w_idx[4];  // shared-input index of each gate weight

@@ -1244,7 +1244,10 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS, 1) mbx_tc_levels(const
 //   fits: the kernel is load-latency bound, each chunk in flight hides one L2 round trip), so no
 //   operand is read twice from L2 by one CTA and the chains run from shared memory.
 #define MBX_SNT (MBX_SNPC * MBX_SUC)
-extern "C" __global__ void __launch_bounds__(MBX_THREADS) mbx_small_dense(const __grid_constant__ SmallArgs P) {
+#ifndef MBX_STHREADS
+#define MBX_STHREADS MBX_THREADS  // block size (narrow variants: fewer threads, more CTAs)
+#endif
+extern "C" __global__ void __launch_bounds__(MBX_STHREADS) mbx_small_dense(const __grid_constant__ SmallArgs P) {
   extern __shared__ __align__(16) float sms[];
   constexpr int K = MBX_K, U = MBX_U, G = MBX_G, NPC = MBX_SNPC, UC = MBX_SUC, KB = MBX_SKB;
   // Weight chunk transposed, [gate][unit][KB + 4]: a thread's column is contiguous along K, so
@@ -1254,19 +1257,29 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS) mbx_small_dense(const 
   constexpr int WCH = G * UC * KBP, XCH = NPC * KB, BUF = WCH + XCH;
   static_assert(K % KB == 0 && KB % 8 == 0, "K chunking");
   const int tid = threadIdx.x;
+  // Phase stamps (profiling builds of the host only: P.stamps is null on every measured path).
+  auto stamp = [&](int i) {
+    if (P.stamps && tid == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      P.stamps[(blockIdx.y * gridDim.x + blockIdx.x) * 8 + i] = t;
+    }
+  };
+  stamp(0);
   const int node0 = blockIdx.x * NPC;
   const int u0 = blockIdx.y * UC;
   const int nn = min(NPC, P.b - node0);
   // PDL: every input (weights included: they may be a hoisted prefix's output) after the wait.
   mbx_gen::pdl_wait();
   mbx_gen::pdl_launch_dependents();
+  stamp(1);
   __shared__ long long rowb[NPC][2];
   // Weight bases into registers first: through generic pointers the compiler cannot prove the
   // shared-memory stores leave the offset table alone and would re-read it every iteration.
   const float* wsrc[G];
 #pragma unroll
   for (int g = 0; g < G; ++g) wsrc[g] = P.arena + __ldg(P.shared_off + P.w_idx[g]) + u0;
-  for (int i = tid; i < nn * 2; i += MBX_THREADS) {
+  for (int i = tid; i < nn * 2; i += MBX_STHREADS) {
     const int n = i >> 1, pc = i & 1;
     long long base = 0;
     if (pc < MBX_NPIECES)
@@ -1276,32 +1289,111 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS) mbx_small_dense(const 
     rowb[n][pc] = base;
   }
   __syncthreads();
+  // Single-chunk launches (all of K staged at once: the narrow variants, decision heads): the
+  // weight slice comes in as VW-float vector loads of a row's unit run, all in flight from
+  // registers, then scattered into the transposed rows; node rows with 16-byte copies where
+  // aligned.  (A warp's staging is otherwise a long serial stream of 4-byte copies: with one or
+  // two warps per SM that stream, not bandwidth, sets the time.)
+  constexpr int NST0 = MBX_SST;
+  constexpr int VW = UC % 4 == 0 ? 4 : (UC % 2 == 0 ? 2 : 1);
+  constexpr int NVG = (KB * UC / VW + MBX_STHREADS - 1) / MBX_STHREADS;  // vectors per thread per gate
+  constexpr bool REG_STAGE = NST0 == 1 && VW > 1 && G * NVG * VW <= 64;
+  auto stage_direct = [&](float* buf) {
+    float wr[G][NVG][VW];
+#pragma unroll
+    for (int g = 0; g < G; ++g)
+#pragma unroll
+      for (int j = 0; j < NVG; ++j) {
+        const int v = tid + j * MBX_STHREADS, r = v / (UC / VW), q = v - r * (UC / VW);
+        if (v < KB * UC / VW) {
+          const float* src = wsrc[g] + (long long)r * U + q * VW;
+          if (VW == 4) {
+            const float4 x = __ldg(reinterpret_cast<const float4*>(src));
+            wr[g][j][0] = x.x, wr[g][j][VW > 1 ? 1 : 0] = x.y, wr[g][j][VW > 2 ? 2 : 0] = x.z, wr[g][j][VW > 3 ? 3 : 0] = x.w;
+          } else {
+            const float2 x = __ldg(reinterpret_cast<const float2*>(src));
+            wr[g][j][0] = x.x, wr[g][j][VW > 1 ? 1 : 0] = x.y;
+          }
+        }
+      }
+    for (int n = 0; n < nn; ++n)
+      for (int pc = 0; pc < MBX_NPIECES; ++pc) {
+        const int k0 = pc ? MBX_PK0 : 0, k1 = pc ? K : (MBX_NPIECES > 1 ? MBX_PK0 : K);
+        const float* row = P.arena + rowb[n][pc];
+        float* dst = buf + WCH + n * KB;
+        if (((rowb[n][pc] + k0) & 3) == 0 && (k0 & 3) == 0 && (k1 & 3) == 0) {
+          for (int k = k0 + 4 * tid; k < k1; k += 4 * MBX_STHREADS) mbx_gen::cp_async16(dst + k, row + k, true);
+        } else {
+          for (int k = k0 + tid; k < k1; k += MBX_STHREADS) mbx_gen::cp_async4(dst + k, row + k, true);
+        }
+      }
+    mbx_gen::cp_async_commit();
+#pragma unroll
+    for (int g = 0; g < G; ++g)
+#pragma unroll
+      for (int j = 0; j < NVG; ++j) {
+        const int v = tid + j * MBX_STHREADS, r = v / (UC / VW), q = v - r * (UC / VW);
+        if (v < KB * UC / VW)
+#pragma unroll
+          for (int e = 0; e < VW; ++e) buf[(g * UC + q * VW + e) * KBP + r] = wr[g][j][e];
+      }
+  };
   auto stage = [&](int c, float* buf) {
     const int k0 = c * KB;
     // cp.async: every copy in flight at once (a load -> store loop through registers would be
     // serialised by the possible aliasing of the generic pointers).
 #pragma unroll
     for (int g = 0; g < G; ++g)
-      for (int i = tid; i < KB * UC; i += MBX_THREADS) {
+      for (int i = tid; i < KB * UC; i += MBX_STHREADS) {
         const int r = i / UC, q = i - r * UC;
         mbx_gen::cp_async4(buf + (g * UC + q) * KBP + r, wsrc[g] + (long long)(k0 + r) * U + q, true);
       }
-    for (int i = tid; i < nn * KB; i += MBX_THREADS) {
+    for (int i = tid; i < nn * KB; i += MBX_STHREADS) {
       const int n = i / KB, k = k0 + (i - n * KB);
       const int pc = (MBX_NPIECES > 1 && k >= MBX_PK0) ? 1 : 0;
       mbx_gen::cp_async4(buf + WCH + i, P.arena + rowb[n][pc] + k, true);
     }
     mbx_gen::cp_async_commit();
   };
-  const int n = tid / UC, u = tid - n * UC;
-  const bool active = tid < MBX_SNT && n < nn && u0 + u < U;
+  // MBX_SGS = G: each gate's chain on its own thread (thread = (gate, node, unit), G x more warps
+  // issuing: a thread's chain is a single instruction stream, so few threads with G chains each
+  // are issue-latency bound); the tail then reads the G sums back from shared memory.
+  // MBX_SGS = 1: one thread per (node, unit) with all G chains.
+#ifndef MBX_SGS
+#define MBX_SGS 1
+#endif
+  constexpr int GS = MBX_SGS, GT = G / GS;  // gates split over threads, gates per thread
+  static_assert(G % GS == 0 && MBX_SNT * GS <= MBX_STHREADS, "gate split");
+  const int gq = tid / MBX_SNT, tr = tid - gq * MBX_SNT;  // gate group, (node, unit) index
+  const int n = tr / UC, u = tr - n * UC;
+  const bool active = gq < GS && n < nn && u0 + u < U;
   float g[G];
 #pragma unroll
   for (int gi = 0; gi < G; ++gi) g[gi] = 0.0f;
+  // The tail's other operands (e.g. the children's cell states) are loaded now, by the threads
+  // that will run the tail: their latency hides under the staging and the chains.
+  const long long node = node0 + n;
+  const int ug = u0 + u;
+  float l[MBX_NLOADS > 0 ? MBX_NLOADS : 1];
+  if (active && gq == 0) {
+#pragma unroll
+    for (int j = 0; j < MBX_NLOADS; ++j) {
+      const TcLoad& d = P.loads[j];
+      const long long base = d.kind == 1 ? P.batched_off[node * P.nb + d.idx] : P.shared_off[d.idx];
+      l[j] = P.arena[base + d.off + ug];
+    }
+  }
   constexpr int NCH = K / KB, NST = MBX_SST, D = NST - 1;  // D chunks in flight ahead
   static_assert(NST >= 1 && (NST > 1 || NCH == 1), "stages");
   // One commit group per chunk (empty past the end) so the wait count is the same every step.
-  if (D == 0) stage(0, sms);
+  // (The vector path needs 16- / 8-byte aligned weight runs: every gate's base and U.)
+  bool direct = REG_STAGE && (U % VW) == 0;
+#pragma unroll
+  for (int g = 0; g < G; ++g) direct = direct && (reinterpret_cast<unsigned long long>(wsrc[g]) % (VW * 4)) == 0;
+  if (D == 0) {
+    if (direct) stage_direct(sms);
+    else stage(0, sms);
+  }
 #pragma unroll 1
   for (int c = 0; c < D; ++c) {
     if (c < NCH) stage(c, sms + c * BUF);
@@ -1316,6 +1408,7 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS) mbx_small_dense(const 
     }
     mbx_gen::cp_async_wait<D>();
     __syncthreads();
+    if (c == 0) stamp(2);
     if (active) {
       const float4* x4 = reinterpret_cast<const float4*>(cur + WCH + n * KB);
       const float* w = cur + u * KBP;
@@ -1327,7 +1420,8 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS) mbx_small_dense(const 
         const float4 xa = x4[p0 >> 2], xb = x4[(p0 >> 2) + 1];
         const float xv[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
 #pragma unroll
-        for (int gi = 0; gi < G; ++gi) {
+        for (int gj = 0; gj < GT; ++gj) {
+          const int gi = gq * GT + gj;
           const float4* w4 = reinterpret_cast<const float4*>(w + gi * UC * KBP + p0);
           const float4 wa = w4[0], wb = w4[1];
           const float wv[8] = {wa.x, wa.y, wa.z, wa.w, wb.x, wb.y, wb.z, wb.w};
@@ -1335,27 +1429,31 @@ extern "C" __global__ void __launch_bounds__(MBX_THREADS) mbx_small_dense(const 
 #pragma unroll
           for (int q = 0; q < 8; ++q) pr[q] = mbx_libm::fmul(xv[q], wv[q]);
 #pragma unroll
-          for (int q = 0; q < 8; ++q) g[gi] = mbx_libm::fadd(g[gi], pr[q]);
+          for (int q = 0; q < 8; ++q) g[gj] = mbx_libm::fadd(g[gj], pr[q]);
         }
       }
     }
     __syncthreads();  // the buffer is refilled NST chunks on
   }
-  if (!active) return;
-  const long long node = node0 + n;
-  const int ug = u0 + u;
-  float l[MBX_NLOADS > 0 ? MBX_NLOADS : 1];
+  stamp(3);
+  if (GS > 1) {  // gather the G sums of (node, unit) on its gate-group-0 thread
+    float* gsm = sms;  // [G][MBX_SNT] (the staging buffers are free after the last chunk)
+    if (active)
 #pragma unroll
-  for (int j = 0; j < MBX_NLOADS; ++j) {
-    const TcLoad& d = P.loads[j];
-    const long long base = d.kind == 1 ? P.batched_off[node * P.nb + d.idx] : P.shared_off[d.idx];
-    l[j] = P.arena[base + d.off + ug];
+      for (int gj = 0; gj < GT; ++gj) gsm[(gq * GT + gj) * MBX_SNT + tr] = g[gj];
+    __syncthreads();
+    if (gq != 0 || !active) return;
+#pragma unroll
+    for (int gi = 0; gi < G; ++gi) g[gi] = gsm[gi * MBX_SNT + tr];
   }
+  if (!active) return;
   float o[MBX_NOUT];
+  stamp(4);
   mbx_tail_exact(g, l, o);
 #pragma unroll
   for (int k = 0; k < MBX_NOUT; ++k)
     P.arena[(P.out_node ? P.out_node[node * MBX_NOUT + k] : P.out_base[k] + node * U) + ug] = o[k];
+  stamp(5);
 }
 #endif  // MBX_SMALL_KERNEL
 
