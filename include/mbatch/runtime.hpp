@@ -91,7 +91,7 @@ struct ExecOptions {
   bool time_kernels = false;    // CUDA-event span of the device work
   bool time_batches = false;    // CUDA events around every batch launch
   bool inputs_resident = false; // inputs already materialised by an identical previous call
-  bool outputs_on_device = false;
+  bool outputs_on_device = false; // outputs stay in the arena: no read-back, EvalResult::outputs empty
   // Return once the device work and the output read-back are enqueued (no final sync, outputs not
   // decoded): the caller synchronises the context's stream before reusing the context.  Used by
   // the throughput pool to keep two mini-batches in flight per worker.

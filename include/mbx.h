@@ -147,7 +147,7 @@ typedef struct {
   int32_t time_batches; /* CUDA-event timing of every batch launch (mbx_result_batch_times) */
   int32_t inputs_resident;   /* inputs already in the arena from an identical previous call:
                                 skip their H2D copy (device-resident benchmarking) */
-  int32_t outputs_on_device; /* leave outputs in the arena (no D2H; outputs read back as 0) */
+  int32_t outputs_on_device; /* leave outputs in the arena (no D2H; the result carries no output values) */
   int32_t ghost;        /* ghost units of the lowered program (ExecOptions::ghost) */
   int32_t defer_sync;   /* return with the work and the output read-back enqueued; outputs not
                            decoded; synchronise (mbx_sync) before reusing the context */

@@ -1287,7 +1287,9 @@ EvalResult Executor::run() {
     total += size_t(h.size());
   }
   auto t_host = clk::now();
-  std::vector<float> buf(total, 0.0f);
+  // Outputs left on the device: no read-back and no host values (the result carries none).
+  const bool keep = I.opts.outputs_on_device && !I.c->dry;
+  std::vector<float> buf(keep ? 0 : total, 0.0f);
   const bool defer = I.opts.defer_sync && !I.c->dry;
   if (!I.c->dry && total > 0 && !I.opts.outputs_on_device) I.pack_to_host(ranges, buf.data(), total, !defer);
   else if (!I.c->dry && !defer) mbx::stream_wait_own(I.c, "final sync");
@@ -1298,7 +1300,7 @@ EvalResult Executor::run() {
 
   EvalResult res;
   size_t cursor = 0, ti = 0;
-  if (!defer) {  // deferred: the outputs are read back but not decoded
+  if (!defer && !keep) {  // deferred: the outputs are read back but not decoded
     if (I.enc_out) {
       for (size_t i = 0; i < size_t(I.batch); ++i) I.to_tokens(fibers_[i]->result, buf, cursor, ti, hs, *I.enc_out);
       I.enc_out->toks.shrink_to_fit();
