@@ -134,7 +134,69 @@ struct DepthKey {
 
 }  // namespace
 
+// Buckets by (phase, depth) index first (both small non-negative integers), then (signature,
+// shared key) within — the same buckets in the same (key-ascending) order as the tree below, with
+// no tree of buckets per node.  Falls back to the tree for negative or sparse depth ranges.
+static bool schedule_depth_dense(const std::vector<const DFGNode*>& nodes, long& scheduler_ops,
+                                 std::vector<BatchRecord>& out) {
+  int maxp = 0, maxd = 0;
+  for (const DFGNode* n : nodes) {
+    if (n->phase < 0 || n->depth < 0) return false;
+    maxp = std::max(maxp, n->phase);
+    maxd = std::max(maxd, n->depth);
+  }
+  const size_t npd = size_t(maxp + 1) * size_t(maxd + 1);
+  if (npd > 4 * nodes.size() + 64) return false;
+  struct Sub {
+    int sig;
+    uint64_t shared;
+    bool ghost;
+    std::vector<int> ids;
+  };
+  std::vector<std::vector<Sub>> pd(npd);
+  for (const DFGNode* n : nodes) {
+    auto& v = pd[size_t(n->phase) * size_t(maxd + 1) + size_t(n->depth)];
+    const uint64_t sk = shared_key(*n);
+    Sub* b = nullptr;
+    for (auto& x : v)
+      if (x.sig == n->sig_id && x.shared == sk) {
+        b = &x;
+        break;
+      }
+    if (!b) b = &v.emplace_back(Sub{n->sig_id, sk, n->ghost, {}});
+    b->ids.push_back(n->id);  // the window is in id order: ids stay ascending
+    ++scheduler_ops;
+  }
+  for (size_t k = 0; k < npd; ++k) {
+    auto& v = pd[k];
+    if (v.empty()) continue;
+    std::sort(v.begin(), v.end(), [](const Sub& a, const Sub& b) {
+      return a.sig != b.sig ? a.sig < b.sig : a.shared < b.shared;
+    });
+    for (auto& x : v) {
+      BatchRecord b;
+      b.phase = int(k / size_t(maxd + 1));
+      b.depth = int(k % size_t(maxd + 1));
+      b.sig = x.sig;
+      b.ghost = x.ghost;
+      b.size = static_cast<int>(x.ids.size());
+      b.node_ids = std::move(x.ids);
+      scheduler_ops += b.size;
+      out.push_back(std::move(b));
+    }
+  }
+  return true;
+}
+
 std::vector<BatchRecord> schedule_depth(const std::vector<const DFGNode*>& nodes, long& scheduler_ops) {
+  {
+    std::vector<BatchRecord> out;
+    long ops = scheduler_ops;
+    if (schedule_depth_dense(nodes, ops, out)) {
+      scheduler_ops = ops;
+      return out;
+    }
+  }
   std::map<DepthKey, std::pair<bool, std::vector<int>>> buckets;
   for (const DFGNode* n : nodes) {
     auto& b = buckets[DepthKey{n->phase, n->depth, n->sig_id, shared_key(*n)}];
