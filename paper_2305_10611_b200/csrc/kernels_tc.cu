@@ -506,8 +506,10 @@ Layout layout_for(const TcState& st, int NT, int S, int npass) {
 // Persistent multi-level layout (mbx_tc_levels): the CTA's resident weight slice
 // [K/S x 128 rows, hi|lo], the node-row region (doubles as the accumulator staging of the DSMEM
 // exchange), the peers' partials (DSMEM exchange only) and the barriers + row table.
-// deep (k = 0): the largest K split S <= 8 whose grid (unit tiles x S) fits on the 148 SMs
-// (smallest resident slice), then the largest node tile (up to 256: TreeLSTM-512's 205-node
+// deep (k = 0): the largest K split S <= 16 whose grid (unit tiles x S) fits on the 148 SMs
+// (smallest resident slice; more ranks per level is faster while the grid fits: NestedRNN's inner
+// cell, K = U = 512, device 6.46 / 5.03 / 4.24 / 4.06 ms at S = 2 / 4 / 8 / 16; the 16-rank
+// cluster is non-portable), then the largest node tile (up to 256: TreeLSTM-512's 205-node
 // depth in one tile); the ranks exchange partials through L2 unless the grid forms at most 14
 // clusters of S (co-resident on a 148-SM B200: GPCs of 16-20 SMs).
 // wide (k = 1, one large batch): the smallest S that fits, then the largest node tile; partials
@@ -547,7 +549,7 @@ bool levels_layout(TcState& st, int k, int parts, int max_ctas) {
     return true;
   };
   if (k == 0) {
-    for (int S : {8, 4, 2, 1})
+    for (int S : {16, 8, 4, 2, 1})
       for (int NT : {256, 128, 64, 32})
         if (try_cfg(S, NT)) return true;
   } else {

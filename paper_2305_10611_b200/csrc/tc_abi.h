@@ -67,7 +67,7 @@ struct TcLevelsArgs {
   float* part;                   // MBX_LXCH 1: partials [2][groups][unit tiles][S][S][MBX_LLOC][128]
   unsigned* xflags;              // MBX_LXCH 1: per (group, unit tile, rank) arrival counters, 0 at launch
   unsigned long long* stamps;    // MBX_STAMPS builds only
-  unsigned long long dep_mask[8];  // per K rank: unit tiles whose outputs its K slice gathers
+  unsigned long long dep_mask[16]; // per K rank: unit tiles whose outputs its K slice gathers
   unsigned char* img;            // operand images (see mbx_tc_levels)
   TcLoad loads[MBX_MAX_LOADS];
 };
