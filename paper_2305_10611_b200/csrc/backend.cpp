@@ -923,7 +923,9 @@ BatchLaunch prepare_batch(mbx_ctx* c, int plan_id, int b, const int64_t* shared_
   for (int i = 0; i < b; ++i)
     for (int j = 0; j < nb; ++j) arena_check(c, batched_off[int64_t(i) * nb + j], p.batched_shapes[j].size());
 
-  std::vector<int64_t> eff(batched_off, batched_off + int64_t(b) * nb);
+  // Effective node rows: the caller's, or (EXPLICIT gathers) the packed copies.
+  thread_local std::vector<int64_t> eff;
+  eff.assign(batched_off, batched_off + int64_t(b) * nb);
   if (gather_mode == MBX_GATHER_EXPLICIT) {
     for (int j = 0; j < nb; ++j) {
       const int64_t size = p.batched_shapes[j].size();
@@ -941,7 +943,8 @@ BatchLaunch prepare_batch(mbx_ctx* c, int plan_id, int b, const int64_t* shared_
       if (gather_bytes) *gather_bytes += int64_t(b) * size * int64_t(sizeof(float));
     }
   }
-  std::vector<int64_t> bases(no);
+  thread_local std::vector<int64_t> bases;
+  bases.resize(size_t(no));
   for (int k = 0; k < no; ++k) {
     const int64_t size = pe.out_shapes[k].size();
     bases[k] = arena_alloc(c, int64_t(b) * size);

@@ -1211,11 +1211,16 @@ void plan_shadows(mbx_ctx* c, std::vector<BatchLaunch>& Ls, const std::vector<Le
   }
   if (regions.empty()) return;
   std::sort(regions.begin(), regions.end(), [](const Region& a, const Region& b) { return a.lo < b.lo; });
+  // (Consecutive rows of a level mostly come from one producer region: the last hit is tried
+  // first, then the binary search.)
+  const Region* last = nullptr;
   auto find = [&](int64_t lo, int64_t hi) -> const Region* {
+    if (last && lo >= last->lo && hi <= last->hi) return last;
     auto it = std::upper_bound(regions.begin(), regions.end(), lo, [](int64_t v, const Region& r) { return v < r.lo; });
     if (it == regions.begin()) return nullptr;
     --it;
-    return (lo >= it->lo && hi <= it->hi) ? &*it : nullptr;
+    if (lo >= it->lo && hi <= it->hi) return last = &*it;
+    return nullptr;
   };
   // Per consumer level, in flush order: an operand image when every gathered row is a whole
   // output row of an earlier capable launch that no other level consumes (trees: each child row

@@ -13,6 +13,7 @@
 // on the device and read back with one D2H copy each.
 #include <algorithm>
 #include <chrono>
+#include <cstdio>
 #include <climits>
 #include <cstring>
 #include <unordered_map>
@@ -883,7 +884,10 @@ struct Executor::Impl {
     mbx::meta_reserve(c, meta_bytes);
 
     std::vector<mbx::BatchLaunch> launches;
+    launches.reserve(batches.size());
     std::vector<size_t> lbatch;  // launch -> its batch in trace.batches
+    lbatch.reserve(batches.size());
+    std::vector<TensorHandle> first_shared;
     std::vector<int64_t> shared, batched, outs;
     for (auto& batch : batches) {
       if (batch.ghost) {
@@ -899,7 +903,7 @@ struct Executor::Impl {
       outs.assign(size_t(b) * no, 0);
       const DFGNode& first = nodes[batch.node_ids[0]];
       MBATCH_CHECK(first.shared_ins.size() == ns && first.batched_ins.size() == nb, "exec_batched: arity mismatch");
-      std::vector<TensorHandle> first_shared(ns);
+      first_shared.resize(ns);
       for (size_t k = 0; k < ns; ++k) {
         first_shared[k] = resolve(first.shared_ins[k]);
         shared[k] = first_shared[k].offset;
