@@ -265,7 +265,7 @@ struct FlatTree {
   int state;  // 0: not started, 1: resumed after its join
   int kids[2];
   int inst;   // instance (its params)
-  Val res;    // (h, c) of a finished subtree
+  Val res[2]; // the finished subtree's pair (e.g. (h, c)): no tuple allocated per tree node
 };
 
 template <class Leaf, class Node, class Root>
@@ -274,7 +274,7 @@ void run_tree_flat(Executor& ex, std::vector<Fiber*>& roots, const std::vector<c
   std::deque<Fiber> extra;
   std::vector<FlatTree> F;
   F.reserve(roots.size() * 32);
-  for (size_t i = 0; i < roots.size(); ++i) F.push_back(FlatTree{roots[i], trees[i], -1, 0, {-1, -1}, int(i), Val{}});
+  for (size_t i = 0; i < roots.size(); ++i) F.push_back(FlatTree{roots[i], trees[i], -1, 0, {-1, -1}, int(i), {}});
   // A pass of run_runnable visits, in index order, the fibers made runnable in the previous pass
   // (parents whose last child finished: lower indices than anything created since), then every
   // fiber created during this pass (appended, runnable).  No rescans of blocked fibers.
@@ -293,19 +293,19 @@ void run_tree_flat(Executor& ex, std::vector<Fiber*>& roots, const std::vector<c
           cf.phase = fb.phase;
           cf.depth_counter = fb.depth_counter;
           F[i].kids[k] = int(F.size());
-          F.push_back(FlatTree{&cf, &t.at(size_t(k)), int(i), 0, {-1, -1}, F[i].inst, Val{}});
+          F.push_back(FlatTree{&cf, &t.at(size_t(k)), int(i), 0, {-1, -1}, F[i].inst, {}});
         }
         fb.status = runtime::FiberStatus::kBlockedJoin;
         fb.pending_children = 2;
         F[i].state = 1;
         return;
       }
-      F[i].res = leaf(fb, F[i].inst, t);
+      leaf(fb, F[i].inst, t, F[i].res);
     } else {
       const FlatTree &a = F[size_t(F[i].kids[0])], &b = F[size_t(F[i].kids[1])];
       fb.depth_counter = std::max(fb.depth_counter, a.fb->depth_counter);
       fb.depth_counter = std::max(fb.depth_counter, b.fb->depth_counter);
-      F[i].res = node(fb, F[i].inst, a.res, b.res);
+      node(fb, F[i].inst, a.res, b.res, F[i].res);
     }
     if (is_root) root_done(fb, F[i].inst, F[i].res);
     fb.status = runtime::FiberStatus::kDone;
@@ -342,22 +342,23 @@ class TreeLstmProgram : public runtime::Program {
     }
     run_tree_flat(
         ex, roots, trees,
-        [&](Fiber& fb, int i, const Val& t) {  // tlstm's Leaf branch
+        [&](Fiber& fb, int i, const Val& t, Val* res) {  // tlstm's Leaf branch: res = (tanh(c), c)
           const TreeLstmParams& p = P[size_t(i)];
           Val xt = Executor::out(ex.emit(fb, 3, {&t.at(0), &p.x_wt, &p.x_bias}), 0);
           int n = ex.emit(fb, 1, {&p.hz, &p.hz, &p.i_wt, &xt, &p.fl_wt, &p.fr_wt, &p.u_wt, &p.cz, &p.cz});
-          return Val::tuple({Executor::out(n, 1), Executor::out(n, 0)});
+          res[0] = Executor::out(n, 1);
+          res[1] = Executor::out(n, 0);
         },
-        [&](Fiber& fb, int i, const Val& l, const Val& r) {  // tlstm's Node branch after the join
+        [&](Fiber& fb, int i, const Val* l, const Val* r, Val* res) {  // tlstm's Node branch after the join
           const TreeLstmParams& p = P[size_t(i)];
-          const Val &lh = l.at(0), &lc = l.at(1), &rh = r.at(0), &rc = r.at(1);
-          int n = ex.emit(fb, 2, {&lh, &rh, &p.i_wt, &p.xn, &p.fl_wt, &p.fr_wt, &p.u_wt, &lc, &rc});
-          return Val::tuple({Executor::out(n, 1), Executor::out(n, 0)});
+          int n = ex.emit(fb, 2, {&l[0], &r[0], &p.i_wt, &p.xn, &p.fl_wt, &p.fr_wt, &p.u_wt, &l[1], &r[1]});
+          res[0] = Executor::out(n, 1);
+          res[1] = Executor::out(n, 0);
         },
-        [&](Fiber& fb, int i, const Val& res) {  // TreeLstmProgram::run after co_await tlstm
+        [&](Fiber& fb, int i, const Val* res) {  // TreeLstmProgram::run after co_await tlstm
           const TreeLstmParams& p = P[size_t(i)];
           ex.stage(fb, 1);
-          fb.result = Executor::out(ex.emit(fb, 0, {&res.at(0), &p.c_wt, &p.cbias}), 0);
+          fb.result = Executor::out(ex.emit(fb, 0, {&res[0], &p.c_wt, &p.cbias}), 0);
         });
   }
   Task run(Executor& ex, Fiber& fb, std::vector<Val> a) const override {
@@ -404,18 +405,21 @@ class MvRnnProgram : public runtime::Program {
     }
     run_tree_flat(
         ex, roots, trees,
-        [&](Fiber&, int, const Val& t) { return Val::tuple({t.at(0), t.at(1)}); },  // mv's Leaf branch
-        [&](Fiber& fb, int i, const Val& l, const Val& r) {                        // mv's Node branch
-          const MvParams& p = P[size_t(i)];
-          const Val &lv = l.at(0), &lm = l.at(1), &rv = r.at(0), &rm = r.at(1);
-          int n1 = ex.emit(fb, 1, {&lv, &rm, &rv, &lm, &p.v_wt, &p.vbias});
-          int n2 = ex.emit(fb, 2, {&lm, &rm});
-          return Val::tuple({Executor::out(n1, 0), Executor::out(n2, 0)});
+        [&](Fiber&, int, const Val& t, Val* res) {  // mv's Leaf branch: (vector, matrix)
+          res[0] = t.at(0);
+          res[1] = t.at(1);
         },
-        [&](Fiber& fb, int i, const Val& res) {  // MvRnnProgram::run after co_await mv
+        [&](Fiber& fb, int i, const Val* l, const Val* r, Val* res) {  // mv's Node branch
+          const MvParams& p = P[size_t(i)];
+          int n1 = ex.emit(fb, 1, {&l[0], &r[1], &r[0], &l[1], &p.v_wt, &p.vbias});
+          int n2 = ex.emit(fb, 2, {&l[1], &r[1]});
+          res[0] = Executor::out(n1, 0);
+          res[1] = Executor::out(n2, 0);
+        },
+        [&](Fiber& fb, int i, const Val* res) {  // MvRnnProgram::run after co_await mv
           const MvParams& p = P[size_t(i)];
           ex.stage(fb, 1);
-          fb.result = Executor::out(ex.emit(fb, 0, {&res.at(0), &p.c_wt, &p.cbias}), 0);
+          fb.result = Executor::out(ex.emit(fb, 0, {&res[0], &p.c_wt, &p.cbias}), 0);
         });
   }
   Task run(Executor& ex, Fiber& fb, std::vector<Val> a) const override {
