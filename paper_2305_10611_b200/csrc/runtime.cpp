@@ -736,23 +736,26 @@ struct Executor::Impl {
     const kernelgen::BlockBinding& bind = *binding_by_id[blk_id];
     const Val* const* in = ins.begin();
     if (ins.size() != blk.inputs.size()) throw Error("block " + std::to_string(blk_id) + ": input arity");
-    DFGNode node = recycled_node();
+    auto& nodes = ex.nodes_;
+    const bool all_shared = bind.batched_input_pos.empty();
+    std::string memo_key;
+    if (all_shared) {
+      memo_key = std::to_string(blk.id) + "|";
+      for (int pos : bind.shared_input_pos) {
+        const TensorRef& r = in[pos]->t;
+        memo_key += std::to_string(r.node) + ":" + std::to_string(r.out) + ":" + std::to_string(r.handle.offset) + ";";
+      }
+      auto it = memo.find(memo_key);
+      if (it != memo.end()) return it->second;
+    }
+    // Built in place at the end of the node table (storage recycled from the session's pool).
+    DFGNode& node = nodes.emplace_back(recycled_node());
     node.shared_ins.reserve(bind.shared_input_pos.size());
     node.batched_ins.reserve(bind.batched_input_pos.size());
     node.producers.reserve(bind.shared_input_pos.size() + bind.batched_input_pos.size() + 1);
     for (int pos : bind.shared_input_pos) node.shared_ins.push_back(in[pos]->t);
     for (int pos : bind.batched_input_pos) node.batched_ins.push_back(in[pos]->t);
-    const bool all_shared = node.batched_ins.empty();
-    std::string memo_key;
-    if (all_shared) {
-      memo_key = std::to_string(blk.id) + "|";
-      for (const auto& r : node.shared_ins)
-        memo_key += std::to_string(r.node) + ":" + std::to_string(r.out) + ":" + std::to_string(r.handle.offset) + ";";
-      auto it = memo.find(memo_key);
-      if (it != memo.end()) return it->second;
-    }
-    auto& nodes = ex.nodes_;
-    node.id = static_cast<int>(nodes.size());
+    node.id = static_cast<int>(nodes.size()) - 1;
     node.sig_id = bind.sig_id;
     node.block_id = blk.id;
     node.instance = fb.instance;
@@ -780,9 +783,8 @@ struct Executor::Impl {
       fb.depth_counter = node.depth;
     }
     fb.last_node = node.id;
-    nodes.push_back(std::move(node));
-    if (all_shared) memo[memo_key] = static_cast<int>(nodes.size()) - 1;
-    return static_cast<int>(nodes.size()) - 1;
+    if (all_shared) memo[memo_key] = node.id;
+    return node.id;
   }
 
   void ghosts(Fiber& fb, int count) {
