@@ -268,12 +268,26 @@ struct FlatTree {
   Val res[2]; // the finished subtree's pair (e.g. (h, c)): no tuple allocated per tree node
 };
 
+// Tree nodes below the roots (one child fiber each).
+inline size_t count_subtrees(const Val& t) {
+  if (t.ctor == 0) return 0;
+  return 2 + count_subtrees(t.at(0)) + count_subtrees(t.at(1));
+}
+
 template <class Leaf, class Node, class Root>
 void run_tree_flat(Executor& ex, std::vector<Fiber*>& roots, const std::vector<const Val*>& trees, Leaf leaf, Node node,
                    Root root_done) {
-  std::deque<Fiber> extra;
-  std::vector<FlatTree> F;
-  F.reserve(roots.size() * 32);
+  // The child fibers: one block per call, reused across calls on this thread (sized up front so
+  // the pointers into it stay valid; fibers are plain records here, no coroutine frames).
+  size_t nsub = 0;
+  for (const Val* t : trees) nsub += count_subtrees(*t);
+  thread_local std::vector<Fiber> extra;
+  extra.clear();
+  extra.resize(nsub);
+  size_t next_extra = 0;
+  thread_local std::vector<FlatTree> F;
+  F.clear();
+  F.reserve(roots.size() + nsub);
   for (size_t i = 0; i < roots.size(); ++i) F.push_back(FlatTree{roots[i], trees[i], -1, 0, {-1, -1}, int(i), {}});
   // A pass of run_runnable visits, in index order, the fibers made runnable in the previous pass
   // (parents whose last child finished: lower indices than anything created since), then every
@@ -288,7 +302,7 @@ void run_tree_flat(Executor& ex, std::vector<Fiber*>& roots, const std::vector<c
       const Val& t = *F[i].t;
       if (t.ctor != 0) {  // Node(l, r): concurrent children, then join
         for (int k = 0; k < 2; ++k) {
-          Fiber& cf = extra.emplace_back();
+          Fiber& cf = extra[next_extra++];
           cf.instance = fb.instance;
           cf.phase = fb.phase;
           cf.depth_counter = fb.depth_counter;
