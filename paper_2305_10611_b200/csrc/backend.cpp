@@ -58,7 +58,7 @@ PersistentLane& lane_of(int device) {
 }
 }  // namespace
 
-cudaStream_t persistent_lane_begin(mbx_ctx* c, int ctas) {
+cudaStream_t persistent_lane_begin(mbx_ctx* c, bool half) {
   if (!c->serialize_persistent || c->dry) return c->stream;
   PersistentLane& L = lane_of(c->device);
   std::unique_lock<std::mutex> lock(L.mu);  // released on every error path below
@@ -73,9 +73,9 @@ cudaStream_t persistent_lane_begin(mbx_ctx* c, int ctas) {
     }
   }
   if (!c->ev_persist) cuda_check(cudaEventCreateWithFlags(&c->ev_persist, cudaEventDisableTiming), "event");
-  // Half-lane launches only from half-budget contexts (their plans checked that two grids fit,
-  // clusters included); anything else runs alone.
-  L.whole = c->sm_budget > 74 || 2 * ctas > 148;
+  // Half-lane launches: two such grids always fit together (the caller checked SMs and clusters,
+  // or the context planned for half the device); anything else runs alone.
+  L.whole = !half;
   if (L.whole) {
     L.cur = 0;
     cuda_check(cudaStreamWaitEvent(L.stream[0], L.done[1], 0), "persistent lane wait");  // runs alone

@@ -208,6 +208,7 @@ void mbx_ctx_destroy(mbx_ctx* c) {
   if (!c) return;
   if (!c->dry) {
     cudaStreamSynchronize(c->stream);
+    if (c->stream2) cudaStreamSynchronize(c->stream2);
     mbx::persistent_lane_forget(c);
     if (c->ev_persist) cudaEventDestroy(c->ev_persist);
     for (auto& pe : c->plans) {
@@ -233,6 +234,11 @@ void mbx_ctx_destroy(mbx_ctx* c) {
     if (c->in_dev) cudaFree(c->in_dev);
     if (c->scat_host) cudaFreeHost(c->scat_host);
     if (c->scat_dev) cudaFree(c->scat_dev);
+    if (c->stream2) {
+      cudaStreamSynchronize(c->stream2);
+      cudaStreamDestroy(c->stream2);
+    }
+    for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
     if (c->owns_stream) cudaStreamDestroy(c->stream);
   } else {
     std::free(c->meta.host);

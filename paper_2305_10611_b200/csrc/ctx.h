@@ -123,6 +123,13 @@ struct mbx_ctx {
   // SMs one persistent launch may occupy: 148, or 74 for pool contexts (mbx_pool_create), whose
   // persistent launches then run two at a time on the device's two lanes (persistent_lane_begin).
   int sm_budget = 148;
+  // Second kernel stream: a flush issues independent chains of launches (BiRNN's two directions)
+  // on stream and stream2 (runtime.cpp assign_streams); issue_slot selects the per-slot scratch
+  // (readiness counters, exchange buffers) of the persistent launches issued on each.
+  cudaStream_t stream2 = nullptr;
+  int issue_slot = 0;
+  bool prefer_pair = false;  // this flush has two independent runs: plan them to fit together
+  std::vector<cudaEvent_t> ev_pool;  // cross-stream dependency events, reused flush to flush
   cudaEvent_t ev_persist = nullptr;
   // HBM arena: one virtual-address reservation, physical chunks mapped on demand, so offsets
   // (the reference's TensorHandle::offset) are stable while the arena grows.
@@ -182,7 +189,7 @@ void cuda_check(cudaError_t e, const char* what);
 // The per-device persistent-launch lane (see mbx_ctx::serialize_persistent): returns the stream
 // to launch on (the lane's, ordered after c->stream's work so far); persistent_lane_end orders
 // c->stream's later work after the launch.
-cudaStream_t persistent_lane_begin(mbx_ctx* c, int ctas = 148);
+cudaStream_t persistent_lane_begin(mbx_ctx* c, bool half);
 void persistent_lane_end(mbx_ctx* c);
 void persistent_lane_forget(mbx_ctx* c);  // before destroying c (its event may be the lane's last)
 // Waits for everything this context enqueued so far (an event: on a pool's shared stream it does

@@ -138,11 +138,16 @@ struct TcState {
     std::string src;
     void* fn = nullptr;
     bool attr_set = false;
-    float* part = nullptr;      // xch 1: partials buffer
-    unsigned* flags = nullptr;  // xch 1: arrival counters
-    unsigned* ready = nullptr;  // per unit tile readiness counters (monotonic)
-    unsigned ready_count = 0;   // their value after every launch so far (stream order)
-  } lv[2];
+    // Per issue slot (mbx_ctx::issue_slot: the context's two streams, so two runs of one plan
+    // can run at once):
+    float* part[2] = {nullptr, nullptr};      // xch 1: partials buffer
+    unsigned* flags[2] = {nullptr, nullptr};  // xch 1: arrival counters
+    unsigned* ready[2] = {nullptr, nullptr};  // per unit tile readiness counters (monotonic)
+    unsigned ready_count[2] = {0, 0};         // their value after every launch so far (stream order)
+  } lv[3];
+  // lv[2]: a deep configuration whose grid leaves room for a second one (two independent runs of
+  // a flush at once, mbx_ctx::prefer_pair), built on first use; pair_tried: attempted.
+  bool pair_tried = false;
   // packed-weight cache: (weight offsets, precision, upload epoch) -> device buffer
   struct Packed {
     std::vector<int64_t> offs;
@@ -548,10 +553,11 @@ bool levels_layout(TcState& st, int k, int parts, int max_ctas) {
     C.smem = w + x + recv + bars;
     return true;
   };
-  if (k == 0) {
+  if (k == 0 || k == 2) {
+    // (k = 2: the largest K split below deep's whose grid fits twice on the SMs.)
     for (int S : {16, 8, 4, 2, 1})
       for (int NT : {256, 128, 64, 32})
-        if (try_cfg(S, NT)) return true;
+        if ((k == 0 || (S < st.lv[0].S && 2 * utiles * S <= 148)) && try_cfg(S, NT)) return true;
   } else {
     // The smallest K split first (its partial exchange through DSMEM costs (S-1)/S of the
     // accumulator tile per CTA and dominates the kernel), then the largest node tile: for the
@@ -733,11 +739,12 @@ void tc_release(PlanEntry& pe) {
   auto* st = static_cast<TcState*>(pe.tc_state);
   if (!st) return;
   for (auto& p : st->packs) cudaFree(p.buf);
-  for (auto& L : st->lv) {
-    if (L.part) cudaFree(L.part);
-    if (L.flags) cudaFree(L.flags);
-    if (L.ready) cudaFree(L.ready);
-  }
+  for (auto& L : st->lv)
+    for (int k = 0; k < 2; ++k) {
+      if (L.part[k]) cudaFree(L.part[k]);
+      if (L.flags[k]) cudaFree(L.flags[k]);
+      if (L.ready[k]) cudaFree(L.ready[k]);
+    }
   delete st;
   pe.tc_state = nullptr;
 }
@@ -1092,6 +1099,21 @@ int plan_levels(mbx_ctx* c, const std::vector<BatchLaunch>& Ls, size_t i, size_t
   std::vector<int> nts;
   int k = 0;
   int ng = level_tiles(st->lv[0], utiles, Ls, i, n, nts, c->sm_budget);
+  // A flush with two independent runs (runtime.cpp: BiRNN's directions, issued on two streams):
+  // runs take the paired configuration so that both grids are resident at once.
+  if (n > 1 && c->prefer_pair && c->sm_budget > 74) {
+    if (!st->pair_tried) {
+      st->pair_tried = true;
+      if (levels_layout(*st, 2, st->lv[0].parts, 148) && !c->dry) {
+        st->lv[2].src = gen_levels_source(*st, 2);
+        st->lv[2].fn = load_kernel(c, st->lv[2].src, "mbx_tc_levels");
+      }
+    }
+    if (st->lv[2].S > 0 && (st->lv[2].fn || c->dry)) {
+      k = 2;
+      ng = level_tiles(st->lv[2], utiles, Ls, i, n, nts, 74);
+    }
+  }
   if (n == 1 && st->lv[1].S > 0 && (st->lv[1].fn || c->dry)) {
     // One batch with more node tiles than the deep configuration has groups for, or a large one
     // (>= 128 nodes: the same MMA work per CTA, but a K split of 2 exchanges an eighth of the
@@ -1118,11 +1140,12 @@ int plan_levels(mbx_ctx* c, const std::vector<BatchLaunch>& Ls, size_t i, size_t
     // resident clusters (DSMEM exchange) or SMs vs what one node-tile group needs.
     int resident, per_group;
     // (Half-device contexts: two such launches must fit at once.)
+    const int budget = k == 2 ? 74 : c->sm_budget;
     if (C.S > 1 && C.xch == 0) {
-      resident = max_active_clusters(C.fn, C.S, C.smem) * c->sm_budget / 148;
+      resident = max_active_clusters(C.fn, C.S, C.smem) * budget / 148;
       per_group = utiles;
     } else {
-      resident = c->sm_budget;
+      resident = budget;
       per_group = utiles * C.S;
     }
     if (resident < per_group) return 0;
@@ -1409,10 +1432,11 @@ void issue_levels(mbx_ctx* c, const std::vector<BatchLaunch>& Ls, size_t i, int 
   bool fresh_pack = false;
   cuda_check(ensure_pack(c, st, shared_host, npass, &pk, &fresh_pack), "weight pack");
   const int utiles = st->U / st->UC;
-  if (!C.ready) {
-    cuda_check(cudaMalloc(&C.ready, size_t(64) * 32 * 4), "levels readiness counters");
-    cuda_check(cudaMemsetAsync(C.ready, 0, size_t(64) * 32 * 4, c->stream), "levels readiness counters");
-    C.ready_count = 0;
+  const int slot = c->issue_slot;
+  if (!C.ready[slot]) {
+    cuda_check(cudaMalloc(&C.ready[slot], size_t(64) * 32 * 4), "levels readiness counters");
+    cuda_check(cudaMemsetAsync(C.ready[slot], 0, size_t(64) * 32 * 4, c->stream), "levels readiness counters");
+    C.ready_count[slot] = 0;
   }
   TcLevelsArgs a{};
   a.arena = arena_ptr(c);
@@ -1432,8 +1456,8 @@ void issue_levels(mbx_ctx* c, const std::vector<BatchLaunch>& Ls, size_t i, int 
   a.recv_off = C.recv_off;
   a.bar_off = C.bar_off;
   a.tmem_cols = std::max(32, C.NT);
-  a.ready = C.ready;
-  a.ready_base = C.ready_count;
+  a.ready = C.ready[slot];
+  a.ready_base = C.ready_count[slot];
   a.img = c->img_buf;
   // Unit tiles whose output columns each K rank's slice of the gathered rows covers (rows this
   // plan produced at an earlier level of the run; rows from earlier launches are complete by
@@ -1456,16 +1480,16 @@ void issue_levels(mbx_ctx* c, const std::vector<BatchLaunch>& Ls, size_t i, int 
     a.dep_mask[r] = m;
   }
   if (C.xch == 1) {
-    if (!C.part) {
+    if (!C.part[slot]) {
       const size_t ngmax = size_t(std::max(1, 148 / (utiles * C.S)));
       const size_t lloc = size_t((C.NT / 8 + C.S - 1) / C.S) * 8;  // MBX_LLOC
       const size_t part_bytes = size_t(2) * ngmax * utiles * C.S * C.S * lloc * kM * 4;
-      cuda_check(cudaMalloc(&C.part, part_bytes), "levels partials");
-      cuda_check(cudaMalloc(&C.flags, ngmax * utiles * C.S * 4), "levels flags");
-      cuda_check(cudaMemsetAsync(C.flags, 0, ngmax * utiles * C.S * 4, c->stream), "levels flags");
+      cuda_check(cudaMalloc(&C.part[slot], part_bytes), "levels partials");
+      cuda_check(cudaMalloc(&C.flags[slot], ngmax * utiles * C.S * 4), "levels flags");
+      cuda_check(cudaMemsetAsync(C.flags[slot], 0, ngmax * utiles * C.S * 4, c->stream), "levels flags");
     }
-    a.part = C.part;
-    a.xflags = C.flags;
+    a.part = C.part[slot];
+    a.xflags = C.flags[slot];
   }
   fill_loads(st->prog, a.loads);
   cudaLaunchConfig_t lc{};
@@ -1511,7 +1535,12 @@ void issue_levels(mbx_ctx* c, const std::vector<BatchLaunch>& Ls, size_t i, int 
     a.stamps = lstamps;
   }
   void* args[] = {&a};
-  if (needs_all) lc.stream = persistent_lane_begin(c, nctas);
+  // Half-lane eligible when two such grids always fit together: at most half the SMs, and (DSMEM
+  // clusters) twice its clusters co-resident.  Pool contexts planned for half the device already.
+  bool half = 2 * nctas <= 148;
+  if (half && c->sm_budget > 74 && C.S > 1 && C.xch == 0)
+    half = 2 * groups * utiles <= max_active_clusters(C.fn, C.S, C.smem);
+  if (needs_all) lc.stream = persistent_lane_begin(c, half);
   // A failed cooperative launch (e.g. too large to be co-resident) is an error, never retried as
   // a plain launch: a partly resident grid would spin at its first readiness wait.
   const cudaError_t le = cudaLaunchKernelExC(&lc, C.fn, args);
@@ -1519,7 +1548,7 @@ void issue_levels(mbx_ctx* c, const std::vector<BatchLaunch>& Ls, size_t i, int 
   cuda_check(le, "multi-level tensor-core kernel");
   if (stamps_enabled())
     report_level_stamps(c, lstamps, nctas, n, reinterpret_cast<const TcLevel*>(c->meta.host + table), C, cfg, groups);
-  C.ready_count += unsigned(groups * C.S) * unsigned(n - 1);
+  C.ready_count[slot] += unsigned(groups * C.S) * unsigned(n - 1);
   ++c->launches;
   ++g_launches;
 }

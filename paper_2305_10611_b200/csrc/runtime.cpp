@@ -846,6 +846,147 @@ struct Executor::Impl {
     }
   }
 
+  // -- two-stream issue ---------------------------------------------------------------------
+  // Two or more runs of consecutive tensor-core batches (length >= 2) over different weights:
+  // the flush may run them at once (assign_streams), so they are planned to fit together.
+  bool pair_candidates(const std::vector<mbx::BatchLaunch>& L) const {
+    std::vector<std::pair<int, size_t>> seen;  // (plan, shared_meta of the run's first batch)
+    for (size_t i = 0; i < L.size();) {
+      const mbx::PlanEntry& pe = c->plans[size_t(L[i].plan_id)];
+      size_t j = i + 1;
+      if (pe.tc_kind == 1 && !pe.tc_small) {
+        const size_t ns = pe.exec_plan.shared_shapes.size();
+        while (j < L.size() && L[j].plan_id == L[i].plan_id &&
+               std::memcmp(c->meta.host + L[j].shared_meta, c->meta.host + L[i].shared_meta, ns * 8) == 0)
+          ++j;
+        if (j - i >= 2) {
+          bool fresh = true;
+          for (const auto& [p, off] : seen)
+            if (p == L[i].plan_id && std::memcmp(c->meta.host + off, c->meta.host + L[i].shared_meta, ns * 8) == 0)
+              fresh = false;
+          if (fresh) seen.push_back({L[i].plan_id, L[i].shared_meta});
+        }
+      }
+      i = j;
+    }
+    return seen.size() >= 2;
+  }
+
+  size_t ev_next_ = 0;
+  cudaEvent_t take_event() {
+    if (ev_next_ == c->ev_pool.size()) {
+      cudaEvent_t e;
+      mbx::cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+      c->ev_pool.push_back(e);
+    }
+    return c->ev_pool[ev_next_++];
+  }
+
+  // Independent chains of a flush on two streams: an issue unit (a persistent run, or one
+  // launch) depends on an earlier unit when one of its input rows lies in that unit's output
+  // regions.  A unit with no dependency goes to the stream the previous unit did not use; one
+  // whose dependencies all sit on one stream follows them; otherwise the primary stream, waiting
+  // for the other's units it reads.  Only when the flush has two persistent runs (BiRNN's two
+  // directions: each run and its input transform on its own stream) and no MV-RNN fusion pairs.
+  bool assign_streams(const std::vector<mbx::BatchLaunch>& L, const std::vector<mbx::LevelsRun>& runs,
+                      const std::vector<int>& run_at, std::vector<int>& ustream, std::vector<std::vector<int>>& uwait,
+                      std::vector<char>& usignal) {
+    int persistent = 0;
+    for (const auto& r : runs) persistent += r.n > 1;
+    if (persistent < 2) return false;
+    // Kept on one stream: MV-RNN cell + add pairs (fused at issue), merged sinks, hoisted
+    // prefixes (their cached scratch), and single tensor-core batches outside persistent runs
+    // (the context's split-K scratch).
+    for (size_t i = 0; i < L.size(); ++i) {
+      const mbx::PlanEntry& pe = c->plans[size_t(L[i].plan_id)];
+      if (pe.mv || pe.mv_add || L[i].out_node || pe.prefix_plan >= 0) return false;
+      if (run_at[i] < 0 && pe.tc_kind == 1 && !pe.tc_small) {
+        bool in_run = false;
+        for (const auto& r : runs) in_run = in_run || (int(i) >= r.start && int(i) < r.start + r.n);
+        if (!in_run) return false;
+      }
+    }
+    struct Region {
+      int64_t lo, hi;
+      int unit;
+    };
+    std::vector<Region> regions;
+    std::vector<std::pair<size_t, size_t>> units;  // [begin, end) launches
+    for (size_t i = 0; i < L.size();) {
+      const size_t n = run_at[i] >= 0 ? size_t(runs[size_t(run_at[i])].n) : 1;
+      units.push_back({i, i + n});
+      i += n;
+    }
+    auto for_leaves = [&](const mbx::BatchLaunch& l, auto&& f) {
+      if (l.sub.empty()) f(l);
+      else
+        for (const auto& sl : l.sub) f(sl);
+    };
+    for (size_t u = 0; u < units.size(); ++u)
+      for (size_t j = units[u].first; j < units[u].second; ++j)
+        for_leaves(L[j], [&](const mbx::BatchLaunch& l) {
+          const mbx::PlanEntry& pe = c->plans[size_t(l.plan_id)];
+          if (pe.plan.ghost) return;
+          const int64_t* ob = reinterpret_cast<const int64_t*>(c->meta.host + l.out_meta);
+          for (size_t k = 0; k < pe.out_shapes.size(); ++k)
+            regions.push_back({ob[k], ob[k] + int64_t(l.b) * pe.out_shapes[k].size(), int(u)});
+          for (const auto& g : l.gathers) regions.push_back({g.dst, g.dst + int64_t(l.b) * g.size, int(u)});
+        });
+    std::sort(regions.begin(), regions.end(), [](const Region& a, const Region& b) { return a.lo < b.lo; });
+    auto owner = [&](int64_t off) -> int {
+      auto it = std::upper_bound(regions.begin(), regions.end(), off, [](int64_t v, const Region& r) { return v < r.lo; });
+      if (it == regions.begin()) return -1;
+      --it;
+      return off < it->hi ? it->unit : -1;
+    };
+    ustream.assign(units.size(), 0);
+    uwait.assign(units.size(), {});
+    usignal.assign(units.size(), 0);
+    bool any2 = false;
+    for (size_t u = 0; u < units.size(); ++u) {
+      std::vector<int> deps;
+      auto add = [&](int64_t off) {
+        const int v = owner(off);
+        if (v >= 0 && v != int(u) && std::find(deps.begin(), deps.end(), v) == deps.end()) deps.push_back(v);
+      };
+      for (size_t j = units[u].first; j < units[u].second; ++j)
+        for_leaves(L[j], [&](const mbx::BatchLaunch& l) {
+          const mbx::PlanEntry& pe = c->plans[size_t(l.plan_id)];
+          if (pe.plan.ghost) return;
+          const size_t ns = pe.exec_plan.shared_shapes.size(), nb = pe.exec_plan.batched_shapes.size();
+          const int64_t* sh = reinterpret_cast<const int64_t*>(c->meta.host + l.shared_meta);
+          const int64_t* bt = reinterpret_cast<const int64_t*>(c->meta.host + l.batched_meta);
+          for (size_t k = 0; k < ns; ++k) add(sh[k]);
+          for (size_t k = 0; k < size_t(l.b) * nb; ++k) add(bt[k]);
+        });
+      // Runs over the same weights follow each other (one weight pack, made by the first).
+      const int r0 = run_at[units[u].first];
+      if (r0 >= 0)
+        for (size_t v = 0; v < u; ++v) {
+          const int rv = run_at[units[v].first];
+          if (rv < 0 || L[units[v].first].plan_id != L[units[u].first].plan_id) continue;
+          const size_t ns = c->plans[size_t(L[units[u].first].plan_id)].exec_plan.shared_shapes.size();
+          if (std::memcmp(c->meta.host + L[units[v].first].shared_meta, c->meta.host + L[units[u].first].shared_meta,
+                          ns * 8) == 0 &&
+              std::find(deps.begin(), deps.end(), int(v)) == deps.end())
+            deps.push_back(int(v));
+        }
+      int s = 0;
+      bool on0 = false, on1 = false;
+      for (int v : deps) (ustream[size_t(v)] ? on1 : on0) = true;
+      if (deps.empty()) s = u == 0 ? 0 : 1 - ustream[u - 1];
+      else if (on1 && !on0) s = 1;
+      ustream[u] = s;
+      for (int v : deps)
+        if (ustream[size_t(v)] != s) {
+          uwait[u].push_back(v);
+          usignal[size_t(v)] = 1;
+        }
+      any2 = any2 || s == 1;
+    }
+    return any2;
+  }
+
   // -- flush (executor.cpp:711-758) -------------------------------------------------------
   size_t exec_lo_ = 0;  // every node below this index is executed
   bool flush(int phase_limit) {
@@ -940,6 +1081,7 @@ struct Executor::Impl {
     // the split-bf16 shadows of the rows they gather are planned.
     std::vector<mbx::LevelsRun> runs;
     std::vector<int> run_at(launches.size(), -1);
+    c->prefer_pair = !opts.time_batches && pair_candidates(launches);
     for (size_t i = 0; i < launches.size();) {
       mbx::LevelsRun r;
       r.start = int(i);
@@ -970,9 +1112,42 @@ struct Executor::Impl {
         cudaEventRecord(a, c->stream);
       }
       int64_t before = c->launches;
-      for (size_t i = 0; i < launches.size();) {
+      std::vector<int> unit_stream;  // per issue unit (a run or a launch): 0 / 1
+      std::vector<std::vector<int>> unit_waits;  // units on the other stream it waits for
+      std::vector<char> unit_signal;             // a unit on the other stream waits for it
+      const bool dual = !opts.time_batches && assign_streams(launches, runs, run_at, unit_stream, unit_waits, unit_signal);
+      std::vector<cudaEvent_t> unit_ev(dual ? unit_stream.size() : 0, nullptr);
+      if (dual) {
+        if (!c->stream2) mbx::cuda_check(cudaStreamCreateWithFlags(&c->stream2, cudaStreamNonBlocking), "second stream");
+        cudaEvent_t ev_start = take_event();
+        mbx::cuda_check(cudaEventRecord(ev_start, c->stream), "flush start");  // offsets + inputs committed
+        mbx::cuda_check(cudaStreamWaitEvent(c->stream2, ev_start, 0), "flush start");
+      }
+      bool used2 = false;
+      size_t unit = 0;
+      for (size_t i = 0; i < launches.size(); ++unit) {
         const mbx::LevelsRun* run = run_at[i] >= 0 ? &runs[size_t(run_at[i])] : nullptr;
         int n = run ? run->n : 1;
+        const bool on2 = dual && unit_stream[unit] == 1;
+        if (dual) {
+          cudaStream_t own = on2 ? c->stream2 : c->stream;
+          for (int w : unit_waits[unit]) mbx::cuda_check(cudaStreamWaitEvent(own, unit_ev[size_t(w)], 0), "cross-stream wait");
+        }
+        if (on2) {
+          std::swap(c->stream, c->stream2);
+          c->issue_slot = 1;
+          used2 = true;
+        }
+        struct Restore {  // back to the primary stream even if the issue throws
+          mbx_ctx* c;
+          bool on;
+          ~Restore() {
+            if (on) {
+              std::swap(c->stream, c->stream2);
+              c->issue_slot = 0;
+            }
+          }
+        } restore{c, on2};
         cudaEvent_t x = nullptr, y = nullptr;
         if (opts.time_batches) {
           cudaEventCreate(&x);
@@ -981,6 +1156,10 @@ struct Executor::Impl {
         }
         if (run) mbx::issue_levels(c, launches, i, n, run->table, run->groups, run->cfg);
         else n = mbx::issue_batches(c, launches, i);
+        if (dual && unit_signal[unit]) {
+          unit_ev[unit] = take_event();
+          mbx::cuda_check(cudaEventRecord(unit_ev[unit], c->stream), "unit done");
+        }
         if (opts.time_batches) {
           cudaEventRecord(y, c->stream);
           batch_events.push_back({x, y});
@@ -988,6 +1167,12 @@ struct Executor::Impl {
         }
         i += size_t(n);
       }
+      if (used2) {  // the rest of this context's work (read-backs, the next flush) follows both
+        cudaEvent_t e = take_event();
+        mbx::cuda_check(cudaEventRecord(e, c->stream2), "second stream done");
+        mbx::cuda_check(cudaStreamWaitEvent(c->stream, e, 0), "second stream done");
+      }
+      ev_next_ = 0;  // reusable: every recorded event is ordered before later work of this context
       timing.device_launches += long(c->launches - before);
       if (opts.time_kernels) {
         cudaEventRecord(e, c->stream);
