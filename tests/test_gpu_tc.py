@@ -159,3 +159,29 @@ def test_levels_kernel_covers_internal_depths(gpu, golden):
     got = np.concatenate([mbx.flatten_floats(o) for o in r.outputs])
     st = elementwise(got, np.concatenate(want), 1e-3)
     assert st["normwise"] <= 1e-3 and st["frac_pass"] >= MIN_PASS["bf16x3"], st
+
+
+@pytest.mark.parametrize("prec", ["bf16x3", "bf16x6"])
+def test_two_stream_flush_matches_fp32(gpu, prec):
+    """BiRNN's two directions are independent persistent runs: the flush issues them on two
+    streams with the paired (co-resident) configuration (runtime.cpp assign_streams).  Its outputs
+    equal the single-stream issue order's (per-batch timing mode) within the precision's bar, and
+    both the FP32 path's, per element; the trace is the reference's either way."""
+    mbx = gpu
+    model, hidden, batch, seed = "birnn", 512, 16, 3
+    ref_ctx = mbx.Context(0, "fp32")
+    ref = mbx.Model(ref_ctx, model, hidden)
+    ref.make_params(seed)
+    t, d = ref.make_inputs(seed, batch)
+    want = ref.evaluate_batch(t, d, batch)
+    c = mbx.Context(0, prec)
+    m = mbx.Model(c, model, hidden)
+    m.make_params(seed)
+    dual = m.evaluate_batch(t, d, batch)
+    single = m.evaluate_batch(t, d, batch, time_batches=True)
+    assert trace_rows(dual.trace) == trace_rows(want.trace) == trace_rows(single.trace)
+    for i in range(batch):
+        w = mbx.flatten_floats(want.outputs[i])
+        for r in (dual, single):
+            st = elementwise(mbx.flatten_floats(r.outputs[i]), w, TOL[prec])
+            assert st["normwise"] <= NORM_TOL[prec] and st["frac_pass"] >= MIN_PASS[prec], (prec, i, st)
