@@ -1273,6 +1273,18 @@ void plan_shadows(mbx_ctx* c, std::vector<BatchLaunch>& Ls, const std::vector<Le
       const BatchLaunch& L = Ls[j];
       const int64_t* bt = reinterpret_cast<const int64_t*>(c->meta.host + L.batched_meta);
       const int nt = tbl[q].nt;
+      // Rows that no capable launch of this flush produced (earlier flushes, inputs, other
+      // kernels): neither an image nor shadow gathers can serve the level — one scan decides.
+      bool produced = true;
+      for (int pc = 0; pc < st->npieces && produced; ++pc) {
+        if (st->piece_kind[pc] != kRefBatched) continue;
+        const int width = st->piece_k[pc] - (pc ? st->piece_k[0] : 0);
+        for (int i = 0; i < L.b && produced; ++i) {
+          const int64_t row = bt[int64_t(i) * nb + st->piece_idx[pc]] + st->piece_off[pc];
+          produced = find(row, row + width) != nullptr;
+        }
+      }
+      if (!produced) continue;
       // -- operand image --
       bool img_ok = allow >= 2 && st->K < 4096 && kslice < 4096 && (kslice & (kslice - 1)) == 0 && nt < 65536 &&
                     (st->KC == 16 || st->KC == 32);

@@ -1094,6 +1094,7 @@ struct Executor::Impl {
         ++i;
       }
     }
+    c->prefer_pair = false;  // (planning only; the C-ABI flush scope plans single-stream)
     mbx::plan_shadows(c, launches, runs);
     timing.h2d_bytes += long(c->meta.cursor - c->meta.committed);
     mbx::meta_commit(c);
