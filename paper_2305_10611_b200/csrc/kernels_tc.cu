@@ -1118,8 +1118,10 @@ int plan_levels(mbx_ctx* c, const std::vector<BatchLaunch>& Ls, size_t i, size_t
     // One batch with more node tiles than the deep configuration has groups for, or a large one
     // (>= 128 nodes: the same MMA work per CTA, but a K split of 2 exchanges an eighth of the
     // partials of deep's 8; BiRNN's 510-node input transform 33 -> ~18 us): go wide.
+    // (A single-level launch with in-cluster exchange needs no co-residency and no lane: it may
+    // use the whole device even in a half-device context.)
     std::vector<int> nts1;
-    const int ng1 = level_tiles(st->lv[1], utiles, Ls, i, n, nts1, c->sm_budget);
+    const int ng1 = level_tiles(st->lv[1], utiles, Ls, i, n, nts1, st->lv[1].xch == 0 ? 148 : c->sm_budget);
     if ((L0.b + nts[0] - 1) / nts[0] > ng || L0.b >= 128) {
       k = 1;
       ng = ng1;
@@ -1140,7 +1142,7 @@ int plan_levels(mbx_ctx* c, const std::vector<BatchLaunch>& Ls, size_t i, size_t
     // resident clusters (DSMEM exchange) or SMs vs what one node-tile group needs.
     int resident, per_group;
     // (Half-device contexts: two such launches must fit at once.)
-    const int budget = k == 2 ? 74 : c->sm_budget;
+    const int budget = k == 2 ? 74 : (k == 1 && n == 1 && C.xch == 0) ? 148 : c->sm_budget;
     if (C.S > 1 && C.xch == 0) {
       resident = max_active_clusters(C.fn, C.S, C.smem) * budget / 148;
       per_group = utiles;
