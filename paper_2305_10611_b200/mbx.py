@@ -34,6 +34,13 @@ class _Opts(ctypes.Structure):
                  "inputs_resident", "outputs_on_device", "ghost", "defer_sync")]
 
 
+class BerxitConfig(ctypes.Structure):
+    """mbx_berxit_config (include/mbx_berxit.h)."""
+    _fields_ = [("hidden", ctypes.c_int32), ("heads", ctypes.c_int32), ("ffn", ctypes.c_int32),
+                ("layers", ctypes.c_int32), ("seq", ctypes.c_int32), ("classes", ctypes.c_int32),
+                ("exit_threshold", ctypes.c_float), ("ln_eps", ctypes.c_float)]
+
+
 _lib = None
 
 
@@ -102,6 +109,19 @@ def lib() -> ctypes.CDLL:
                              pI64]),
         "mbx_pool_run_timed": (I, [P, I, I, ctypes.POINTER(pI32), pI64, ctypes.POINTER(pF), pI64,
                                    ctypes.POINTER(_Opts), pI64, pD]),
+        "mbx_berxit_config_default": (None, [ctypes.POINTER(BerxitConfig)]),
+        "mbx_berxit_param_count": (I64, [ctypes.POINTER(BerxitConfig)]),
+        "mbx_berxit_make_params": (I, [ctypes.POINTER(BerxitConfig), ctypes.c_uint, pF]),
+        "mbx_berxit_make_input": (I, [ctypes.POINTER(BerxitConfig), ctypes.c_uint, I, pF]),
+        "mbx_berxit_create": (I, [I, I, ctypes.POINTER(BerxitConfig), I, ctypes.POINTER(P)]),
+        "mbx_berxit_destroy": (None, [P]),
+        "mbx_berxit_last_error": (ctypes.c_char_p, [P]),
+        "mbx_berxit_set_params": (I, [P, pF, I64]),
+        "mbx_berxit_run": (I, [P, I, pF, pF, pI32, pI32]),
+        "mbx_berxit_run_device": (I, [P, I, P]),
+        "mbx_berxit_read": (I, [P, I, pF, pI32, pI32]),
+        "mbx_berxit_stream": (P, [P]),
+        "mbx_berxit_launches_per_batch": (I, [P, I]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -114,7 +134,8 @@ def lib() -> ctypes.CDLL:
 def exported_symbols() -> List[str]:
     """mbx_* functions declared in include/mbx.h (for ABI checks), parsed from the header."""
     import re
-    hdr = open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include", "mbx.h")).read()
+    inc = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include")
+    hdr = "".join(open(os.path.join(inc, h)).read() for h in ("mbx.h", "mbx_berxit.h"))
     hdr = re.sub(r"/\*.*?\*/", "", hdr, flags=re.S)
     return sorted(set(re.findall(r"\b(mbx_[a-z0-9_]+)\s*\(", hdr)))
 
@@ -679,3 +700,106 @@ def plan_from_dump(p: dict) -> List[int]:
     for k, i, off, cols in p["outputs"]:
         e += [kind[k], i, off, cols]
     return e
+
+
+def berxit_config(**kw) -> BerxitConfig:
+    """mbx_berxit_config_default (BERT-base: H 768, 12 heads, FFN 3072, 12 shared layers, seq 128,
+    8 classes, exit threshold 0.6) with the given fields replaced."""
+    c = BerxitConfig()
+    lib().mbx_berxit_config_default(ctypes.byref(c))
+    for k, v in kw.items():
+        setattr(c, k, v)
+    return c
+
+
+def berxit_make_params(cfg: BerxitConfig, seed: int) -> np.ndarray:
+    n = lib().mbx_berxit_param_count(ctypes.byref(cfg))
+    out = np.empty(n, np.float32)
+    if lib().mbx_berxit_make_params(ctypes.byref(cfg), seed, _ptr(out, ctypes.c_float)):
+        raise MbatchError(lib().mbx_berxit_last_error(None).decode())
+    return out
+
+
+def berxit_make_inputs(cfg: BerxitConfig, seed: int, batch: int, first: int = 0) -> np.ndarray:
+    """Instances first .. first + batch - 1 of the synthetic input set, [batch][seq][hidden]."""
+    out = np.empty((batch, cfg.seq, cfg.hidden), np.float32)
+    for i in range(batch):
+        if lib().mbx_berxit_make_input(ctypes.byref(cfg), seed, first + i, _ptr(out[i], ctypes.c_float)):
+            raise MbatchError(lib().mbx_berxit_last_error(None).decode())
+    return out
+
+
+@dataclass
+class BerxitResult:
+    logits: np.ndarray       # [batch][classes]
+    exit_layer: np.ndarray   # [batch]
+    schedule: np.ndarray     # [layers][batch]: instance ids of layer l's batch, -1 padded
+
+    def batches(self) -> List[List[int]]:
+        return [[int(i) for i in row if i >= 0] for row in self.schedule]
+
+
+class Berxit:
+    """Berxit early-exit encoder on one B200 (include/mbx_berxit.h): parameters resident, one
+    mini-batch per ``run`` (per-layer batches over the running instances, exits decided on the
+    device)."""
+
+    def __init__(self, device: int = 0, precision: str = "bf16x3", cfg: Optional[BerxitConfig] = None,
+                 max_batch: int = 64):
+        self.cfg = cfg if cfg is not None else berxit_config()
+        self.max_batch = max_batch
+        h = ctypes.c_void_p()
+        if lib().mbx_berxit_create(device, PREC[precision], ctypes.byref(self.cfg), max_batch, ctypes.byref(h)):
+            raise MbatchError(lib().mbx_berxit_last_error(None).decode())
+        self.h = h
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h and _lib is not None:
+            try:
+                _lib.mbx_berxit_destroy(h)
+            except Exception:  # interpreter shutdown
+                pass
+            self.h = None
+
+    def _check(self, rc):
+        if rc:
+            raise MbatchError(lib().mbx_berxit_last_error(self.h).decode())
+
+    def set_params(self, params: np.ndarray):
+        p = np.ascontiguousarray(params, np.float32)
+        self._check(lib().mbx_berxit_set_params(self.h, _ptr(p, ctypes.c_float), p.size))
+
+    def make_params(self, seed: int) -> np.ndarray:
+        p = berxit_make_params(self.cfg, seed)
+        self.set_params(p)
+        return p
+
+    def _out(self, batch):
+        return (np.empty((batch, self.cfg.classes), np.float32), np.empty(batch, np.int32),
+                np.empty((self.cfg.layers, batch), np.int32))
+
+    def run(self, x: np.ndarray) -> BerxitResult:
+        """One mini-batch from host inputs [batch][seq][hidden] (synchronous)."""
+        x = np.ascontiguousarray(x, np.float32)
+        b = x.shape[0]
+        lg, ex, sc = self._out(b)
+        self._check(lib().mbx_berxit_run(self.h, b, _ptr(x, ctypes.c_float), _ptr(lg, ctypes.c_float),
+                                         _ptr(ex, ctypes.c_int32), _ptr(sc, ctypes.c_int32)))
+        return BerxitResult(lg, ex, sc)
+
+    def run_device(self, batch: int, x_dev_ptr: int):
+        """Enqueues one mini-batch whose inputs are at device address x_dev_ptr (asynchronous)."""
+        self._check(lib().mbx_berxit_run_device(self.h, batch, ctypes.c_void_p(x_dev_ptr)))
+
+    def read(self, batch: int) -> BerxitResult:
+        lg, ex, sc = self._out(batch)
+        self._check(lib().mbx_berxit_read(self.h, batch, _ptr(lg, ctypes.c_float), _ptr(ex, ctypes.c_int32),
+                                          _ptr(sc, ctypes.c_int32)))
+        return BerxitResult(lg, ex, sc)
+
+    def stream(self) -> int:
+        return lib().mbx_berxit_stream(self.h) or 0
+
+    def launches_per_batch(self, batch: int) -> int:
+        return lib().mbx_berxit_launches_per_batch(self.h, batch)
