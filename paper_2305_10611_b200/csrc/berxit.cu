@@ -6,19 +6,19 @@
 // never leaves the device: `alive` (instance ids in instance order) and `count` live in HBM, the
 // exit kernel of layer l writes layer l+1's list, and every kernel of a layer reads its tiles from
 // that list (a gather by index array: an exited instance's rows stay where they are, nothing is
-// compacted or copied).  One mini-batch = 2 + 8 L launches captured once per batch size as a CUDA
+// compacted or copied).  One mini-batch = 2 + 7 L launches captured once per batch size as a CUDA
 // graph; the host sees the results only.
 //
 // Per layer (all on one stream; instance rows [S = 128][.] stay at x[inst], the operand images at
 // x_img[inst] etc.):
 //   bx_gemm<PLAIN>   qkv  = x Wqkv^T + b                      (tcgen05, A = x_img)
-//   bx_attention     ctx_img = softmax(q k^T / 8) v per head  (fp32, writes the next A image)
+//   bx_attention     ctx_img = softmax(q k^T / 8) v per head  (tcgen05, writes the next A image)
 //   bx_gemm<RESID>   y    = x + ctx Wo^T + b
 //   bx_layernorm     x, x_img = LN1(y)
 //   bx_gemm<GELU>    f_img = GELU(x W1^T + b)                 (the epilogue writes the A image)
 //   bx_gemm<RESID>   y    = x + f W2^T + b
-//   bx_layernorm     x, x_img = LN2(y)
-//   bx_exit          LTE certainty, logits of the exiting instances, next layer's alive list
+//   bx_layernorm     x, x_img = LN2(y); CLS rows: LTE certainty, logits of the exiting instances;
+//                    the last CTA writes the next layer's running list (exit head fused)
 //
 // Operand images: every GEMM operand is stored by its producer as split bf16 (hi = rn(v),
 // lo = rn(v - hi); one part in BF16 precision) in the canonical no-swizzle K-major UMMA layout,
@@ -60,7 +60,6 @@ constexpr int kABlock = kSeq * kKC;  // bf16 elements of one A chunk part (16 KB
 constexpr int kWBlock = kNT * kKC;   // bf16 elements of one W chunk part (32 KB)
 constexpr int kGemmThreads = 192;
 constexpr int kStageSmem = 192 * 1024;
-constexpr int kAttSmem = 2 * kSeq * 64 * 4;  // K and V of one head, fp32
 
 enum Epi { EPI_PLAIN = 0, EPI_RESID = 1, EPI_GELU = 2 };
 
@@ -183,13 +182,15 @@ struct GemmArgs {
   const int* alive;
   const int* count;
   int kch, ntiles, N, P;
+  int nt;  // tile width (MMA N): 256, 128 or 64 — a row range of the weight image's 256-row tiles
 };
 
 template <int EPI>
 __global__ void __launch_bounds__(kGemmThreads, 1) bx_gemm(GemmArgs g) {
   extern __shared__ __align__(1024) unsigned char smem[];
   const int P = g.P;
-  const unsigned a_bytes = unsigned(P) * kABlock * 2, w_bytes = unsigned(P) * kWBlock * 2;
+  const int NT = g.nt;
+  const unsigned a_bytes = unsigned(P) * kABlock * 2, w_part = unsigned(NT) * 128, w_bytes = unsigned(P) * w_part;
   const unsigned stage_bytes = a_bytes + w_bytes;
   const int S = kStageSmem / int(stage_bytes);
   unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem + kStageSmem);
@@ -228,23 +229,25 @@ __global__ void __launch_bounds__(kGemmThreads, 1) bx_gemm(GemmArgs g) {
     if (lane == 0) {
       int it = 0;
       for (int t = blockIdx.x; t < ntile_total; t += gridDim.x) {
-        const int inst = g.alive[t / g.ntiles], nt = t % g.ntiles;
+        const int inst = g.alive[t / g.ntiles], n0 = (t % g.ntiles) * NT;
         const bf16_t* a = g.a_img + (size_t)inst * g.kch * P * kABlock;
-        const bf16_t* w = g.w_img + (size_t)nt * g.kch * P * kWBlock;
+        // rows n0 .. n0 + NT of the 256-row image tile: a contiguous range of each part block
+        const bf16_t* w = g.w_img + (size_t)(n0 / kNT) * g.kch * P * kWBlock + (n0 % kNT) * kKC;
         for (int c = 0; c < g.kch; ++c, ++it) {
           const int s = it % S;
           if (it >= S) mbar_wait(&empty[s], ((it / S) - 1) & 1);
           unsigned char* st = smem + s * stage_bytes;
           mbar_expect_tx(&full[s], stage_bytes);
           bulk_g2s(st, a + (size_t)c * P * kABlock, a_bytes, &full[s]);
-          bulk_g2s(st + a_bytes, w + (size_t)c * P * kWBlock, w_bytes, &full[s]);
+          for (int p = 0; p < P; ++p)
+            bulk_g2s(st + a_bytes + p * w_part, w + ((size_t)c * P + p) * kWBlock, w_part, &full[s]);
         }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
       // kind::f16: A = B = BF16, D = F32, both K-major, N = 256, M = 128.
-      const unsigned idesc = (1u << 4) | (1u << 7) | (1u << 10) | (unsigned(kNT >> 3) << 17) | (unsigned(kSeq >> 4) << 24);
+      const unsigned idesc = (1u << 4) | (1u << 7) | (1u << 10) | (unsigned(NT >> 3) << 17) | (unsigned(kSeq >> 4) << 24);
       int it = 0, tc = 0;
       for (int t = blockIdx.x; t < ntile_total; t += gridDim.x, ++tc) {
         const int acc = tc & 1;
@@ -262,7 +265,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) bx_gemm(GemmArgs g) {
             mma_bf16(d, ah, bh, idesc, (c | ks) ? 1u : 0u);
             if (P > 1) {
               const unsigned long long al = make_desc(sa + kABlock * 2 + ks * 256);
-              const unsigned long long bl = make_desc(sb + kWBlock * 2 + ks * 256);
+              const unsigned long long bl = make_desc(sb + w_part + ks * 256);
               mma_bf16(d, ah, bl, idesc, 1u);
               mma_bf16(d, al, bh, idesc, 1u);
             }
@@ -278,14 +281,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1) bx_gemm(GemmArgs g) {
     int tc = 0;
     for (int t = blockIdx.x; t < ntile_total; t += gridDim.x, ++tc) {
       const int acc = tc & 1;
-      const int inst = g.alive[t / g.ntiles], nt = t % g.ntiles;
+      const int inst = g.alive[t / g.ntiles], n0 = (t % g.ntiles) * NT;
       mbar_wait(&acc_full[acc], (tc >> 1) & 1);
       tc_fence_after();
 #pragma unroll 1
-      for (int cc = 0; cc < kNT / 32; ++cc) {
+      for (int cc = 0; cc < NT / 32; ++cc) {
         float v[32];
         tmem_ld32(tmem + (unsigned(32 * q) << 16) + unsigned(acc * kNT + cc * 32), v);
-        const int col0 = nt * kNT + cc * 32;
+        const int col0 = n0 + cc * 32;
         const float4* b4 = reinterpret_cast<const float4*>(g.bias + col0);
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
@@ -329,135 +332,286 @@ __global__ void __launch_bounds__(kGemmThreads, 1) bx_gemm(GemmArgs g) {
   }
 }
 
-// ---- attention: one CTA per (head, running instance), one query row per thread -----------------
-// q, k, v = columns [h*64, +64) of qkv's three H-wide blocks.  Online softmax over key blocks of
-// 16 (scores scaled by 1/8, exact in binary), output written as the Wo GEMM's A image (chunk h).
-__global__ void __launch_bounds__(128) bx_attention(const float* qkv, bf16_t* ctx_img, const int* alive,
-                                                    const int* count, int H, int P) {
-  extern __shared__ __align__(16) float att_smem[];
-  float (*Ks)[64] = reinterpret_cast<float (*)[64]>(att_smem);
-  float (*Vs)[64] = reinterpret_cast<float (*)[64]>(att_smem + kSeq * 64);
+// ---- attention: one CTA per (head, running instance) on tcgen05 ---------------------------------
+// S = Q K^T (M = 128 queries, N = 128 keys, K = 64) and O = P V (M = 128, N = 64, K = 128 keys),
+// split bf16 (3 products per K step in BF16X3) with fp32 TMEM accumulation; the softmax is fp32
+// per query row (thread = row = TMEM lane).  Q (scaled by 1/8, exact), K and V^T are converted
+// from qkv's fp32 rows straight into the canonical K-major layouts; P is written back as the A
+// operand of the second product, over Q and K (dead once S is in TMEM).  Shared memory (bytes):
+// Q [part] 16 K | K [part] 16 K (later P [key chunk][part] 16 K) | V^T [key chunk][part] 8 K
+// = 96 K: two CTAs per SM.
+constexpr int kAttSmem = 96 * 1024 + 64;
+
+__device__ __forceinline__ void st_split4(unsigned char* base_hi, int lo_off, int e_off, float a, float b, float c,
+                                          float d, int P) {
+  unsigned short h[4], l[4];
+  split2(a, h[0], l[0]);
+  split2(b, h[1], l[1]);
+  split2(c, h[2], l[2]);
+  split2(d, h[3], l[3]);
+  *reinterpret_cast<uint2*>(base_hi + 2 * e_off) =
+      make_uint2(unsigned(h[0]) | (unsigned(h[1]) << 16), unsigned(h[2]) | (unsigned(h[3]) << 16));
+  if (P > 1)
+    *reinterpret_cast<uint2*>(base_hi + lo_off + 2 * e_off) =
+        make_uint2(unsigned(l[0]) | (unsigned(l[1]) << 16), unsigned(l[2]) | (unsigned(l[3]) << 16));
+}
+
+__global__ void __launch_bounds__(128, 2) bx_attention(const float* qkv, bf16_t* ctx_img, const int* alive,
+                                                       const int* count, int H, int P) {
+  extern __shared__ __align__(1024) unsigned char asmem[];
+  unsigned char* sQ = asmem;
+  unsigned char* sK = asmem + 32768;
+  unsigned char* sVT = asmem + 65536;
+  unsigned char* sP = asmem;  // over Q and K
+  unsigned long long* bar = reinterpret_cast<unsigned long long*>(asmem + 98304);
+  unsigned* tmem_slot = reinterpret_cast<unsigned*>(asmem + 98304 + 16);
   const int m = blockIdx.y, h = blockIdx.x;
   if (m >= *count) return;
   const int inst = alive[m];
-  const int i = threadIdx.x;
+  const int t = threadIdx.x, warp = t >> 5;
+  if (t == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(256)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  // Thread t converts row t of Q, K (token t) and column t of V^T (key t): lanes = consecutive
+  // rows, so the 8-byte / 2-byte canonical stores of a warp fall on few bank wavefronts (lanes =
+  // consecutive columns put every lane of a row on the same bank: measured 1.5x slower).
   const size_t ld = 3 * (size_t)H;
-  const float* base = qkv + (size_t)inst * kSeq * ld;
-  for (int e = threadIdx.x; e < kSeq * 16; e += blockDim.x) {
-    const int j = e >> 4, c4 = e & 15;
-    reinterpret_cast<float4*>(&Ks[j][0])[c4] = reinterpret_cast<const float4*>(base + j * ld + H + h * 64)[c4];
-    reinterpret_cast<float4*>(&Vs[j][0])[c4] = reinterpret_cast<const float4*>(base + j * ld + 2 * H + h * 64)[c4];
-  }
-  float q[64], o[64];
-  const float4* q4 = reinterpret_cast<const float4*>(base + i * ld + h * 64);
+  const float* row = qkv + ((size_t)inst * kSeq + t) * ld + h * 64;
+#pragma unroll 4
+  for (int d4 = 0; d4 < 16; ++d4) {
+    const float4 q = reinterpret_cast<const float4*>(row)[d4];
+    const float4 k = reinterpret_cast<const float4*>(row + H)[d4];
+    const float4 v = reinterpret_cast<const float4*>(row + 2 * H)[d4];
+    const int e = canon(t, 4 * d4);
+    st_split4(sQ, 16384, e, q.x * 0.125f, q.y * 0.125f, q.z * 0.125f, q.w * 0.125f, P);
+    st_split4(sK, 16384, e, k.x, k.y, k.z, k.w, P);
+    const float vv[4] = {v.x, v.y, v.z, v.w};
+    unsigned char* vb = sVT + (t >> 6) * 16384;
 #pragma unroll
-  for (int d = 0; d < 16; ++d) {
-    const float4 x = q4[d];
-    q[4 * d] = x.x * 0.125f;
-    q[4 * d + 1] = x.y * 0.125f;
-    q[4 * d + 2] = x.z * 0.125f;
-    q[4 * d + 3] = x.w * 0.125f;
+    for (int j = 0; j < 4; ++j) {
+      unsigned short hi, lo;
+      split2(vv[j], hi, lo);
+      const int ev = canon(4 * d4 + j, t & 63);
+      reinterpret_cast<unsigned short*>(vb)[ev] = hi;
+      if (P > 1) reinterpret_cast<unsigned short*>(vb + 8192)[ev] = lo;
+    }
   }
-#pragma unroll
-  for (int d = 0; d < 64; ++d) o[d] = 0.f;
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  tc_fence_before();
   __syncthreads();
-  float mx = -INFINITY, l = 0.f;
-#pragma unroll 1
-  for (int jb = 0; jb < kSeq; jb += 16) {
-    float s[16];
+  tc_fence_after();
+  const unsigned tmem = *tmem_slot;
+  const unsigned idesc_s = (1u << 4) | (1u << 7) | (1u << 10) | (unsigned(128 >> 3) << 17) | (unsigned(kSeq >> 4) << 24);
+  const unsigned idesc_o = (1u << 4) | (1u << 7) | (1u << 10) | (unsigned(64 >> 3) << 17) | (unsigned(kSeq >> 4) << 24);
+  if (t == 0) {
+    const unsigned q0 = smem_u32(sQ), k0 = smem_u32(sK);
 #pragma unroll
-    for (int jj = 0; jj < 16; ++jj) s[jj] = 0.f;
-#pragma unroll
-    for (int d4 = 0; d4 < 16; ++d4) {
-#pragma unroll
-      for (int jj = 0; jj < 16; ++jj) {
-        const float4 k = reinterpret_cast<const float4*>(&Ks[jb + jj][0])[d4];
-        s[jj] = fmaf(q[4 * d4], k.x, s[jj]);
-        s[jj] = fmaf(q[4 * d4 + 1], k.y, s[jj]);
-        s[jj] = fmaf(q[4 * d4 + 2], k.z, s[jj]);
-        s[jj] = fmaf(q[4 * d4 + 3], k.w, s[jj]);
+    for (int ks = 0; ks < 4; ++ks) {
+      const unsigned long long qh = make_desc(q0 + ks * 256), kh = make_desc(k0 + ks * 256);
+      mma_bf16(tmem, qh, kh, idesc_s, ks ? 1u : 0u);
+      if (P > 1) {
+        mma_bf16(tmem, qh, make_desc(k0 + 16384 + ks * 256), idesc_s, 1u);
+        mma_bf16(tmem, make_desc(q0 + 16384 + ks * 256), kh, idesc_s, 1u);
       }
     }
-    float bm = s[0];
-#pragma unroll
-    for (int jj = 1; jj < 16; ++jj) bm = fmaxf(bm, s[jj]);
-    const float mn = fmaxf(mx, bm);
-    const float corr = expf(mx - mn);
-    l *= corr;
-#pragma unroll
-    for (int d = 0; d < 64; ++d) o[d] *= corr;
-#pragma unroll
-    for (int jj = 0; jj < 16; ++jj) {
-      const float p = expf(s[jj] - mn);
-      l += p;
-      const float4* v4 = reinterpret_cast<const float4*>(&Vs[jb + jj][0]);
-#pragma unroll
-      for (int d4 = 0; d4 < 16; ++d4) {
-        const float4 v = v4[d4];
-        o[4 * d4] = fmaf(p, v.x, o[4 * d4]);
-        o[4 * d4 + 1] = fmaf(p, v.y, o[4 * d4 + 1]);
-        o[4 * d4 + 2] = fmaf(p, v.z, o[4 * d4 + 2]);
-        o[4 * d4 + 3] = fmaf(p, v.w, o[4 * d4 + 3]);
-      }
-    }
-    mx = mn;
+    mma_commit(&bar[0]);
   }
+  mbar_wait(&bar[0], 0);
+  tc_fence_after();
+  // softmax of row t: lanes 32 warp .. of TMEM = rows
+  const unsigned lane_base = tmem + (unsigned(32 * warp) << 16);
+  float mx = -INFINITY;
+#pragma unroll 1
+  for (int c = 0; c < 4; ++c) {
+    float v[32];
+    tmem_ld32(lane_base + unsigned(c * 32), v);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) mx = fmaxf(mx, v[j]);
+  }
+  float l = 0.f;
+#pragma unroll 1
+  for (int c = 0; c < 4; ++c) {
+    float v[32];
+    tmem_ld32(lane_base + unsigned(c * 32), v);
+    unsigned char* pb = sP + (c >> 1) * 32768;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      v[j] = expf(v[j] - mx);
+      l += v[j];
+    }
+#pragma unroll
+    for (int j = 0; j < 32; j += 4)
+      st_split4(pb, 16384, canon(t, (c & 1) * 32 + j), v[j], v[j + 1], v[j + 2], v[j + 3], P);
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (t == 0) {
+    const unsigned p0 = smem_u32(sP), v0 = smem_u32(sVT);
+#pragma unroll
+    for (int c = 0; c < 2; ++c)
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks) {
+        const unsigned pa = p0 + c * 32768 + ks * 256, vb = v0 + c * 16384 + ks * 256;
+        const unsigned long long ph = make_desc(pa), vh = make_desc(vb);
+        mma_bf16(tmem + 128, ph, vh, idesc_o, (c | ks) ? 1u : 0u);
+        if (P > 1) {
+          mma_bf16(tmem + 128, ph, make_desc(vb + 8192), idesc_o, 1u);
+          mma_bf16(tmem + 128, make_desc(pa + 16384), vh, idesc_o, 1u);
+        }
+      }
+    mma_commit(&bar[1]);
+  }
+  mbar_wait(&bar[1], 0);
+  tc_fence_after();
   const float inv = 1.0f / l;
+  float o[64];
+  tmem_ld32(lane_base + 128, o);
+  tmem_ld32(lane_base + 160, o + 32);
 #pragma unroll
   for (int d = 0; d < 64; ++d) o[d] *= inv;
-  store_img_row<8>(ctx_img, H / kKC, P, inst, i, h * 64, o);
+  store_img_row<8>(ctx_img, H / kKC, P, inst, t, h * 64, o);
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256) : "memory");
+  }
 }
 
 // ---- layer norm: one warp per row; y -> x (fp32) and x_img ----------------------------------------
+// With `ex.on` (LN2) the warp of each running instance's first row (CLS) also runs the exit head
+// on the normalised row it holds in registers: certainty u = sigmoid(w_lte . h + b_lte); an exiting
+// instance writes its logits and exit layer.  The last CTA to finish (counter) compacts the running
+// list in instance order for the next layer and records this layer's batch in the schedule.
+struct ExitArgs {
+  int on;
+  const float *w_lte, *b_lte, *wc, *bc;
+  float* logits;
+  int *exit_layer, *sched, *keep;
+  unsigned* done;
+  int* alive_w;  // == alive (written by the last CTA only)
+  int* count_w;
+  int C, layer, L, bmax;
+  float tau;
+};
+
 __global__ void __launch_bounds__(256) bx_layernorm(const float* y, float* x, bf16_t* x_img, const float* gam,
                                                     const float* bet, const int* alive, const int* count, int H,
-                                                    int P, float eps) {
+                                                    int P, float eps, ExitArgs ex) {
   const int row = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   const int m = row / kSeq, r = row % kSeq;
-  if (m >= *count) return;
-  const int inst = alive[m];
-  const size_t off = ((size_t)inst * kSeq + r) * H;
-  const int nv = H / 128;  // float4 per lane
-  float4 v[8];
-  float sum = 0.f;
+  const int n = *count;
+  if (m < n) {
+    const int inst = alive[m];
+    const size_t off = ((size_t)inst * kSeq + r) * H;
+    const int nv = H / 128;  // float4 per lane
+    float4 v[8];
+    float sum = 0.f;
 #pragma unroll
-  for (int j = 0; j < 8; ++j)
-    if (j < nv) {
-      v[j] = reinterpret_cast<const float4*>(y + off)[lane + 32 * j];
-      sum += (v[j].x + v[j].y) + (v[j].z + v[j].w);
+    for (int j = 0; j < 8; ++j)
+      if (j < nv) {
+        v[j] = reinterpret_cast<const float4*>(y + off)[lane + 32 * j];
+        sum += (v[j].x + v[j].y) + (v[j].z + v[j].w);
+      }
+#pragma unroll
+    for (int s = 16; s; s >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, s);
+    const float mean = sum / float(H);
+    float var = 0.f;
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (j < nv) {
+        const float a = v[j].x - mean, b = v[j].y - mean, c = v[j].z - mean, d = v[j].w - mean;
+        var += (a * a + b * b) + (c * c + d * d);
+      }
+#pragma unroll
+    for (int s = 16; s; s >>= 1) var += __shfl_xor_sync(0xffffffffu, var, s);
+    const float inv = 1.0f / sqrtf(var / float(H) + eps);
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (j < nv) {
+        const int k = 4 * (lane + 32 * j);
+        const float4 g = __ldg(reinterpret_cast<const float4*>(gam + k));
+        const float4 b = __ldg(reinterpret_cast<const float4*>(bet + k));
+        float o[4] = {(v[j].x - mean) * inv * g.x + b.x, (v[j].y - mean) * inv * g.y + b.y,
+                      (v[j].z - mean) * inv * g.z + b.z, (v[j].w - mean) * inv * g.w + b.w};
+        v[j] = make_float4(o[0], o[1], o[2], o[3]);
+        reinterpret_cast<float4*>(x + off)[lane + 32 * j] = v[j];
+        unsigned short hh[4], ll[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) split2(o[e], hh[e], ll[e]);
+        const size_t base = ((size_t)inst * (H / kKC) + (k >> 6)) * P * kABlock + canon(r, k & 63);
+        *reinterpret_cast<uint2*>(x_img + base) =
+            make_uint2(unsigned(hh[0]) | (unsigned(hh[1]) << 16), unsigned(hh[2]) | (unsigned(hh[3]) << 16));
+        if (P > 1)
+          *reinterpret_cast<uint2*>(x_img + base + kABlock) =
+              make_uint2(unsigned(ll[0]) | (unsigned(ll[1]) << 16), unsigned(ll[2]) | (unsigned(ll[3]) << 16));
+      }
+    if (ex.on && r == 0) {
+      auto wdot = [&](const float* w) {
+        float a = 0.f;
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (j < nv) {
+            const float4 c = __ldg(reinterpret_cast<const float4*>(w) + lane + 32 * j);
+            a = fmaf(c.x, v[j].x, a);
+            a = fmaf(c.y, v[j].y, a);
+            a = fmaf(c.z, v[j].z, a);
+            a = fmaf(c.w, v[j].w, a);
+          }
+#pragma unroll
+        for (int s = 16; s; s >>= 1) a += __shfl_xor_sync(0xffffffffu, a, s);
+        return a;
+      };
+      const float z = wdot(ex.w_lte) + ex.b_lte[0];
+      const float u = 1.0f / (1.0f + expf(-z));
+      const bool out = (u >= ex.tau) || ex.layer == ex.L - 1;
+      if (out) {
+        for (int c = 0; c < ex.C; ++c) {
+          const float a = wdot(ex.wc + (size_t)c * H);
+          if (lane == 0) ex.logits[(size_t)inst * ex.C + c] = a + ex.bc[c];
+        }
+        if (lane == 0) ex.exit_layer[inst] = ex.layer;
+      }
+      if (lane == 0) ex.keep[m] = out ? 0 : 1;
     }
-#pragma unroll
-  for (int s = 16; s; s >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, s);
-  const float mean = sum / float(H);
-  float var = 0.f;
-#pragma unroll
-  for (int j = 0; j < 8; ++j)
-    if (j < nv) {
-      const float a = v[j].x - mean, b = v[j].y - mean, c = v[j].z - mean, d = v[j].w - mean;
-      var += (a * a + b * b) + (c * c + d * d);
+  }
+  if (!ex.on) return;
+  __shared__ int last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(ex.done, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (threadIdx.x < 32) {
+    const volatile int* keep = ex.keep;
+    int k = 0;
+    for (int b0 = 0; b0 < n; b0 += 32) {
+      const int mm = b0 + lane;
+      const int id = mm < n ? alive[mm] : -1;
+      const bool kp = mm < n && keep[mm];
+      if (mm < n) ex.sched[(size_t)ex.layer * ex.bmax + mm] = id;
+      const unsigned bal = __ballot_sync(0xffffffffu, kp);
+      if (kp) ex.alive_w[k + __popc(bal & ((1u << lane) - 1))] = id;
+      k += __popc(bal);
     }
-#pragma unroll
-  for (int s = 16; s; s >>= 1) var += __shfl_xor_sync(0xffffffffu, var, s);
-  const float inv = 1.0f / sqrtf(var / float(H) + eps);
-#pragma unroll
-  for (int j = 0; j < 8; ++j)
-    if (j < nv) {
-      const int k = 4 * (lane + 32 * j);
-      const float4 g = __ldg(reinterpret_cast<const float4*>(gam + k));
-      const float4 b = __ldg(reinterpret_cast<const float4*>(bet + k));
-      float o[4] = {(v[j].x - mean) * inv * g.x + b.x, (v[j].y - mean) * inv * g.y + b.y,
-                    (v[j].z - mean) * inv * g.z + b.z, (v[j].w - mean) * inv * g.w + b.w};
-      reinterpret_cast<float4*>(x + off)[lane + 32 * j] = make_float4(o[0], o[1], o[2], o[3]);
-      unsigned short hh[4], ll[4];
-#pragma unroll
-      for (int e = 0; e < 4; ++e) split2(o[e], hh[e], ll[e]);
-      const size_t base = ((size_t)inst * (H / kKC) + (k >> 6)) * P * kABlock + canon(r, k & 63);
-      *reinterpret_cast<uint2*>(x_img + base) =
-          make_uint2(unsigned(hh[0]) | (unsigned(hh[1]) << 16), unsigned(hh[2]) | (unsigned(hh[3]) << 16));
-      if (P > 1)
-        *reinterpret_cast<uint2*>(x_img + base + kABlock) =
-            make_uint2(unsigned(ll[0]) | (unsigned(ll[1]) << 16), unsigned(ll[2]) | (unsigned(ll[3]) << 16));
+    if (lane == 0) {
+      *ex.count_w = k;
+      *ex.done = 0;
     }
+  }
 }
 
 // ---- mini-batch start: alive = 0..b-1, count = b, schedule / exits reset; x -> x_img ---------
@@ -482,52 +636,6 @@ __global__ void __launch_bounds__(256) bx_to_image(const float* x, bf16_t* x_img
   const float4 a = reinterpret_cast<const float4*>(src)[0], c = reinterpret_cast<const float4*>(src)[1];
   v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = c.x; v[5] = c.y; v[6] = c.z; v[7] = c.w;
   store_img_row<1>(x_img, H / kKC, P, inst, r, k0, v);
-}
-
-// ---- exit head: one CTA; warp per running instance -------------------------------------------------
-__global__ void __launch_bounds__(256) bx_exit(const float* x, const float* w_lte, const float* b_lte,
-                                               const float* wc, const float* bc, int* alive, int* count,
-                                               float* logits, int* exit_layer, int* sched, int H, int C, int layer,
-                                               int L, int bmax, float tau) {
-  extern __shared__ int sh[];
-  int* ids = sh;              // [bmax]
-  int* keep = sh + bmax;      // [bmax]
-  const int n = *count;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  for (int m = threadIdx.x; m < n; m += blockDim.x) {
-    ids[m] = alive[m];
-    sched[(size_t)layer * bmax + m] = alive[m];
-  }
-  __syncthreads();
-  for (int m = warp; m < n; m += nw) {
-    const int inst = ids[m];
-    const float* h = x + (size_t)inst * kSeq * H;  // token 0 (CLS)
-    float z = 0.f;
-    for (int k = lane; k < H; k += 32) z = fmaf(w_lte[k], h[k], z);
-#pragma unroll
-    for (int s = 16; s; s >>= 1) z += __shfl_xor_sync(0xffffffffu, z, s);
-    z += b_lte[0];
-    const float u = 1.0f / (1.0f + expf(-z));
-    const bool ex = (u >= tau) || layer == L - 1;
-    if (ex) {
-      for (int c = 0; c < C; ++c) {
-        float a = 0.f;
-        for (int k = lane; k < H; k += 32) a = fmaf(wc[(size_t)c * H + k], h[k], a);
-#pragma unroll
-        for (int s = 16; s; s >>= 1) a += __shfl_xor_sync(0xffffffffu, a, s);
-        if (lane == 0) logits[(size_t)inst * C + c] = a + bc[c];
-      }
-      if (lane == 0) exit_layer[inst] = layer;
-    }
-    if (lane == 0) keep[m] = ex ? 0 : 1;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int k = 0;
-    for (int m = 0; m < n; ++m)
-      if (keep[m]) alive[k++] = ids[m];
-    *count = k;
-  }
 }
 
 // Weight W [N][K] fp32 -> image [N/256][K/64][P][256 x 64] split bf16.
@@ -558,7 +666,9 @@ struct mbx_berxit {
   bx::bf16_t *wqkv = nullptr, *wo = nullptr, *w1 = nullptr, *w2 = nullptr;
   float *x = nullptr, *y = nullptr, *qkv = nullptr, *logits = nullptr;
   bx::bf16_t *x_img = nullptr, *ctx_img = nullptr, *f_img = nullptr;
-  int *alive = nullptr, *count = nullptr, *exit_layer = nullptr, *sched = nullptr;
+  int *alive = nullptr, *count = nullptr, *exit_layer = nullptr, *sched = nullptr, *keep = nullptr;
+  float* wc_al = nullptr;    // 16-byte aligned copy of Wc
+  unsigned* done = nullptr;  // CTA counter of the exit-fused layer norm (self-resetting)
   bool params_set = false;
   std::map<int, cudaGraphExec_t> graphs;
   std::string err;
@@ -607,10 +717,18 @@ T* dalloc(size_t n) {
   return static_cast<T*>(p);
 }
 
-void launch_gemm(mbx_berxit* m, int epi, const bx::bf16_t* a_img, const bx::bf16_t* w_img, int K, int N,
+void launch_gemm(mbx_berxit* m, int b, int epi, const bx::bf16_t* a_img, const bx::bf16_t* w_img, int K, int N,
                  const float* bias, const float* resid, float* out, bx::bf16_t* out_img) {
-  bx::GemmArgs g{a_img, w_img, bias, resid, out, out_img, m->alive, m->count, K / bx::kKC, N / bx::kNT, N, m->P};
-  const int grid = std::min(m->sms, m->bmax * g.ntiles);
+  // Tile width: the smallest makespan ceil(tiles / SMs) x (width + fixed per-tile cost) for a
+  // batch of b running instances (BERT-base b64: 256 for QKV / W1, 128 for Wo / W2).
+  int nt = 256;
+  long best = -1;
+  for (int w : {256, 128, 64}) {
+    const long tiles = (long)b * (N / w), rounds = (tiles + m->sms - 1) / m->sms, cost = rounds * (w + 48);
+    if (best < 0 || cost < best) best = cost, nt = w;
+  }
+  bx::GemmArgs g{a_img, w_img, bias, resid, out, out_img, m->alive, m->count, K / bx::kKC, N / nt, N, m->P, nt};
+  const int grid = (int)std::min<long>(m->sms, (long)b * g.ntiles);
   const size_t smem = bx::kStageSmem + 256;
   switch (epi) {
     case bx::EPI_PLAIN: bx::bx_gemm<bx::EPI_PLAIN><<<grid, bx::kGemmThreads, smem, m->stream>>>(g); break;
@@ -630,18 +748,18 @@ void enqueue(mbx_berxit* m, int b) {
   bx::bx_to_image<<<unsigned((groups + 255) / 256), 256, 0, m->stream>>>(m->x, m->x_img, H, P, b);
   (void)wp;
   for (int l = 0; l < L; ++l) {
-    launch_gemm(m, bx::EPI_PLAIN, m->x_img, m->wqkv, H, 3 * H, m->bqkv, nullptr, m->qkv, nullptr);
+    launch_gemm(m, b, bx::EPI_PLAIN, m->x_img, m->wqkv, H, 3 * H, m->bqkv, nullptr, m->qkv, nullptr);
     bx::bx_attention<<<dim3(c.heads, m->bmax), 128, bx::kAttSmem, m->stream>>>(m->qkv, m->ctx_img, m->alive, m->count, H, P);
-    launch_gemm(m, bx::EPI_RESID, m->ctx_img, m->wo, H, H, m->bo, m->x, m->y, nullptr);
+    launch_gemm(m, b, bx::EPI_RESID, m->ctx_img, m->wo, H, H, m->bo, m->x, m->y, nullptr);
+    bx::ExitArgs off{};
     bx::bx_layernorm<<<m->bmax * bx::kSeq / 8, 256, 0, m->stream>>>(m->y, m->x, m->x_img, m->g1, m->be1, m->alive,
-                                                                    m->count, H, P, c.ln_eps);
-    launch_gemm(m, bx::EPI_GELU, m->x_img, m->w1, H, F, m->b1, nullptr, nullptr, m->f_img);
-    launch_gemm(m, bx::EPI_RESID, m->f_img, m->w2, F, H, m->b2, m->x, m->y, nullptr);
+                                                                    m->count, H, P, c.ln_eps, off);
+    launch_gemm(m, b, bx::EPI_GELU, m->x_img, m->w1, H, F, m->b1, nullptr, nullptr, m->f_img);
+    launch_gemm(m, b, bx::EPI_RESID, m->f_img, m->w2, F, H, m->b2, m->x, m->y, nullptr);
+    bx::ExitArgs ex{1, m->wl, m->bl, m->wc, m->bc, m->logits, m->exit_layer, m->sched, m->keep, m->done,
+                    m->alive, m->count, c.classes, l, L, m->bmax, c.exit_threshold};
     bx::bx_layernorm<<<m->bmax * bx::kSeq / 8, 256, 0, m->stream>>>(m->y, m->x, m->x_img, m->g2, m->be2, m->alive,
-                                                                    m->count, H, P, c.ln_eps);
-    bx::bx_exit<<<1, 256, 2 * m->bmax * sizeof(int), m->stream>>>(m->x, m->wl, m->bl, m->wc, m->bc, m->alive,
-                                                                  m->count, m->logits, m->exit_layer, m->sched, H,
-                                                                  c.classes, l, L, m->bmax, c.exit_threshold);
+                                                                    m->count, H, P, c.ln_eps, ex);
     bx::check(cudaGetLastError(), "berxit layer launch");
   }
 }
@@ -664,7 +782,7 @@ void run_graph(mbx_berxit* m, int b) {
     it = m->graphs.emplace(b, exec).first;
   }
   bx::check(cudaGraphLaunch(it->second, m->stream), "graph launch");
-  mbx::g_launches += 2 + 8 * m->c.layers;
+  mbx::g_launches += 2 + 7 * m->c.layers;
 }
 
 }  // namespace
@@ -748,6 +866,10 @@ int mbx_berxit_create(int device, int precision, const mbx_berxit_config* c, int
     m->count = dalloc<int>(1);
     m->exit_layer = dalloc<int>(B);
     m->sched = dalloc<int>(B * c->layers);
+    m->keep = dalloc<int>(B);
+    m->wc_al = dalloc<float>((size_t)c->classes * H);
+    m->done = dalloc<unsigned>(1);
+    bx::check(cudaMemset(m->done, 0, sizeof(unsigned)), "memset");
     const size_t smem = bx::kStageSmem + 256;
     bx::check(cudaFuncSetAttribute(bx::bx_gemm<bx::EPI_PLAIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)), "attr");
     bx::check(cudaFuncSetAttribute(bx::bx_gemm<bx::EPI_RESID>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)), "attr");
@@ -767,7 +889,7 @@ void mbx_berxit_destroy(mbx_berxit* m) {
   if (!m) return;
   for (auto& kv : m->graphs) cudaGraphExecDestroy(kv.second);
   void* bufs[] = {m->params, m->wqkv, m->wo, m->w1, m->w2, m->x, m->y, m->qkv, m->x_img, m->ctx_img,
-                  m->f_img, m->logits, m->alive, m->count, m->exit_layer, m->sched};
+                  m->f_img, m->logits, m->alive, m->count, m->exit_layer, m->sched, m->keep, m->done, m->wc_al};
   for (void* p : bufs)
     if (p) cudaFree(p);
   if (m->stream) cudaStreamDestroy(m->stream);
@@ -797,7 +919,10 @@ int mbx_berxit_set_params(mbx_berxit* m, const float* params, int64_t n) {
     m->be2 = p; p += H;
     m->wl = p; p += H;
     m->bl = p; p += 1;
-    m->wc = p; p += m->c.classes * H;
+    // Wc follows the single b_lte float: an aligned copy for the exit head's float4 loads.
+    bx::check(cudaMemcpyAsync(m->wc_al, p, sizeof(float) * m->c.classes * H, cudaMemcpyDeviceToDevice, m->stream),
+              "Wc copy");
+    m->wc = m->wc_al; p += m->c.classes * H;
     m->bc = p;
     auto img = [&](const float* W, bx::bf16_t* out, int64_t N, int64_t K) {
       const int64_t e = N * K;
@@ -857,6 +982,6 @@ int mbx_berxit_run(mbx_berxit* m, int batch, const float* x, float* logits, int3
 
 void* mbx_berxit_stream(mbx_berxit* m) { return m ? m->stream : nullptr; }
 
-int mbx_berxit_launches_per_batch(const mbx_berxit* m, int) { return 2 + 8 * m->c.layers; }
+int mbx_berxit_launches_per_batch(const mbx_berxit* m, int) { return 2 + 7 * m->c.layers; }
 
 }  // extern "C"
