@@ -11,8 +11,8 @@
 //
 // Per layer (all on one stream; instance rows [S = 128][.] stay at x[inst], the operand images at
 // x_img[inst] etc.):
-//   bx_gemm<PLAIN>   qkv  = x Wqkv^T + b                      (tcgen05, A = x_img)
-//   bx_attention     ctx_img = softmax(q k^T / 8) v per head  (tcgen05, writes the next A image)
+//   bx_gemm<QKV>     q/8, k, v^T images = x Wqkv^T + b        (tcgen05, A = x_img)
+//   bx_attention     ctx_img = softmax(q k^T / 8) v per head  (tcgen05 on bulk-copied images)
 //   bx_gemm<RESID>   y    = x + ctx Wo^T + b
 //   bx_layernorm     x, x_img = LN1(y)
 //   bx_gemm<GELU>    f_img = GELU(x W1^T + b)                 (the epilogue writes the A image)
@@ -61,7 +61,7 @@ constexpr int kWBlock = kNT * kKC;   // bf16 elements of one W chunk part (32 KB
 constexpr int kGemmThreads = 192;
 constexpr int kStageSmem = 192 * 1024;
 
-enum Epi { EPI_PLAIN = 0, EPI_RESID = 1, EPI_GELU = 2 };
+enum Epi { EPI_PLAIN = 0, EPI_RESID = 1, EPI_GELU = 2, EPI_QKV = 3 };
 
 // ---- device helpers ----------------------------------------------------------------------------
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -183,6 +183,11 @@ struct GemmArgs {
   const int* count;
   int kch, ntiles, N, P;
   int nt;  // tile width (MMA N): 256, 128 or 64 — a row range of the weight image's 256-row tiles
+  // EPI_QKV: out_img = Q image (scaled by 1/8), k_img = K image ([inst][head][part][128 x 64],
+  // i.e. A images with one chunk per head), vt_img = V^T image ([inst][head][key chunk][part][64 x 64])
+  bf16_t* k_img;
+  bf16_t* vt_img;
+  int H;
 };
 
 template <int EPI>
@@ -303,6 +308,26 @@ __global__ void __launch_bounds__(kGemmThreads, 1) bx_gemm(GemmArgs g) {
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] = gelu(v[j]);
           store_img_row<4>(g.out_img, g.N / kKC, P, inst, r, col0, v);
+        } else if (EPI == EPI_QKV) {
+          const int H = g.H, sec = col0 / H, c = col0 - sec * H;
+          if (sec == 0) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] *= 0.125f;  // 1 / sqrt(64), exact
+            store_img_row<4>(g.out_img, H / kKC, P, inst, r, c, v);
+          } else if (sec == 1) {
+            store_img_row<4>(g.k_img, H / kKC, P, inst, r, c, v);
+          } else {
+            const int h = c >> 6, d0 = c & 63;
+            bf16_t* vb = g.vt_img + (((size_t)inst * (H / 64) + h) * 2 + (r >> 6)) * P * 4096;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              unsigned short hi, lo;
+              split2(v[j], hi, lo);
+              const int e = canon(d0 + j, r & 63);
+              vb[e] = hi;
+              if (P > 1) vb[e + 4096] = lo;
+            }
+          }
         } else {
           if (EPI == EPI_RESID) {
             const float4* r4 = reinterpret_cast<const float4*>(g.resid + row);
@@ -356,7 +381,8 @@ __device__ __forceinline__ void st_split4(unsigned char* base_hi, int lo_off, in
         make_uint2(unsigned(l[0]) | (unsigned(l[1]) << 16), unsigned(l[2]) | (unsigned(l[3]) << 16));
 }
 
-__global__ void __launch_bounds__(128, 2) bx_attention(const float* qkv, bf16_t* ctx_img, const int* alive,
+__global__ void __launch_bounds__(128, 2) bx_attention(const bf16_t* q_img, const bf16_t* k_img,
+                                                       const bf16_t* vt_img, bf16_t* ctx_img, const int* alive,
                                                        const int* count, int H, int P) {
   extern __shared__ __align__(1024) unsigned char asmem[];
   unsigned char* sQ = asmem;
@@ -364,7 +390,7 @@ __global__ void __launch_bounds__(128, 2) bx_attention(const float* qkv, bf16_t*
   unsigned char* sVT = asmem + 65536;
   unsigned char* sP = asmem;  // over Q and K
   unsigned long long* bar = reinterpret_cast<unsigned long long*>(asmem + 98304);
-  unsigned* tmem_slot = reinterpret_cast<unsigned*>(asmem + 98304 + 16);
+  unsigned* tmem_slot = reinterpret_cast<unsigned*>(asmem + 98304 + 32);
   const int m = blockIdx.y, h = blockIdx.x;
   if (m >= *count) return;
   const int inst = alive[m];
@@ -372,38 +398,26 @@ __global__ void __launch_bounds__(128, 2) bx_attention(const float* qkv, bf16_t*
   if (t == 0) {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
+    mbar_init(&bar[2], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  __syncthreads();
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                  "r"(256)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
-  // Thread t converts row t of Q, K (token t) and column t of V^T (key t): lanes = consecutive
-  // rows, so the 8-byte / 2-byte canonical stores of a warp fall on few bank wavefronts (lanes =
-  // consecutive columns put every lane of a row on the same bank: measured 1.5x slower).
-  const size_t ld = 3 * (size_t)H;
-  const float* row = qkv + ((size_t)inst * kSeq + t) * ld + h * 64;
-#pragma unroll 4
-  for (int d4 = 0; d4 < 16; ++d4) {
-    const float4 q = reinterpret_cast<const float4*>(row)[d4];
-    const float4 k = reinterpret_cast<const float4*>(row + H)[d4];
-    const float4 v = reinterpret_cast<const float4*>(row + 2 * H)[d4];
-    const int e = canon(t, 4 * d4);
-    st_split4(sQ, 16384, e, q.x * 0.125f, q.y * 0.125f, q.z * 0.125f, q.w * 0.125f, P);
-    st_split4(sK, 16384, e, k.x, k.y, k.z, k.w, P);
-    const float vv[4] = {v.x, v.y, v.z, v.w};
-    unsigned char* vb = sVT + (t >> 6) * 16384;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      unsigned short hi, lo;
-      split2(vv[j], hi, lo);
-      const int ev = canon(4 * d4 + j, t & 63);
-      reinterpret_cast<unsigned short*>(vb)[ev] = hi;
-      if (P > 1) reinterpret_cast<unsigned short*>(vb + 8192)[ev] = lo;
-    }
+  // Q, K and V^T arrive MMA-ready from the QKV GEMM's epilogue: three bulk copies.
+  if (t == 0) {
+    const size_t qk = ((size_t)inst * (H / 64) + h) * P * 8192;  // elements
+    const unsigned qb = unsigned(P) * 16384;
+    mbar_expect_tx(&bar[2], 3 * qb);
+    bulk_g2s(sQ, q_img + qk, qb, &bar[2]);
+    bulk_g2s(sK, k_img + qk, qb, &bar[2]);
+    bulk_g2s(sVT, vt_img + qk, qb, &bar[2]);
   }
+  mbar_wait(&bar[2], 0);
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   tc_fence_before();
   __syncthreads();
@@ -664,7 +678,8 @@ struct mbx_berxit {
   cudaStream_t stream = nullptr;
   float* params = nullptr;  // flat fp32 parameters (device)
   bx::bf16_t *wqkv = nullptr, *wo = nullptr, *w1 = nullptr, *w2 = nullptr;
-  float *x = nullptr, *y = nullptr, *qkv = nullptr, *logits = nullptr;
+  float *x = nullptr, *y = nullptr, *logits = nullptr;
+  bx::bf16_t *q_img = nullptr, *k_img = nullptr, *vt_img = nullptr;
   bx::bf16_t *x_img = nullptr, *ctx_img = nullptr, *f_img = nullptr;
   int *alive = nullptr, *count = nullptr, *exit_layer = nullptr, *sched = nullptr, *keep = nullptr;
   float* wc_al = nullptr;    // 16-byte aligned copy of Wc
@@ -727,13 +742,15 @@ void launch_gemm(mbx_berxit* m, int b, int epi, const bx::bf16_t* a_img, const b
     const long tiles = (long)b * (N / w), rounds = (tiles + m->sms - 1) / m->sms, cost = rounds * (w + 48);
     if (best < 0 || cost < best) best = cost, nt = w;
   }
-  bx::GemmArgs g{a_img, w_img, bias, resid, out, out_img, m->alive, m->count, K / bx::kKC, N / nt, N, m->P, nt};
+  bx::GemmArgs g{a_img, w_img, bias, resid, out, out_img, m->alive, m->count, K / bx::kKC, N / nt, N, m->P, nt,
+                 m->k_img, m->vt_img, m->c.hidden};
   const int grid = (int)std::min<long>(m->sms, (long)b * g.ntiles);
   const size_t smem = bx::kStageSmem + 256;
   switch (epi) {
     case bx::EPI_PLAIN: bx::bx_gemm<bx::EPI_PLAIN><<<grid, bx::kGemmThreads, smem, m->stream>>>(g); break;
     case bx::EPI_RESID: bx::bx_gemm<bx::EPI_RESID><<<grid, bx::kGemmThreads, smem, m->stream>>>(g); break;
-    default: bx::bx_gemm<bx::EPI_GELU><<<grid, bx::kGemmThreads, smem, m->stream>>>(g); break;
+    case bx::EPI_GELU: bx::bx_gemm<bx::EPI_GELU><<<grid, bx::kGemmThreads, smem, m->stream>>>(g); break;
+    default: bx::bx_gemm<bx::EPI_QKV><<<grid, bx::kGemmThreads, smem, m->stream>>>(g); break;
   }
   bx::check(cudaGetLastError(), "bx_gemm launch");
 }
@@ -748,8 +765,9 @@ void enqueue(mbx_berxit* m, int b) {
   bx::bx_to_image<<<unsigned((groups + 255) / 256), 256, 0, m->stream>>>(m->x, m->x_img, H, P, b);
   (void)wp;
   for (int l = 0; l < L; ++l) {
-    launch_gemm(m, b, bx::EPI_PLAIN, m->x_img, m->wqkv, H, 3 * H, m->bqkv, nullptr, m->qkv, nullptr);
-    bx::bx_attention<<<dim3(c.heads, m->bmax), 128, bx::kAttSmem, m->stream>>>(m->qkv, m->ctx_img, m->alive, m->count, H, P);
+    launch_gemm(m, b, bx::EPI_QKV, m->x_img, m->wqkv, H, 3 * H, m->bqkv, nullptr, nullptr, m->q_img);
+    bx::bx_attention<<<dim3(c.heads, m->bmax), 128, bx::kAttSmem, m->stream>>>(
+        m->q_img, m->k_img, m->vt_img, m->ctx_img, m->alive, m->count, H, P);
     launch_gemm(m, b, bx::EPI_RESID, m->ctx_img, m->wo, H, H, m->bo, m->x, m->y, nullptr);
     bx::ExitArgs off{};
     bx::bx_layernorm<<<m->bmax * bx::kSeq / 8, 256, 0, m->stream>>>(m->y, m->x, m->x_img, m->g1, m->be1, m->alive,
@@ -857,7 +875,9 @@ int mbx_berxit_create(int device, int precision, const mbx_berxit_config* c, int
     m->w2 = dalloc<bx::bf16_t>(H * F * P);
     m->x = dalloc<float>(B * S * H);
     m->y = dalloc<float>(B * S * H);
-    m->qkv = dalloc<float>(B * S * 3 * H);
+    m->q_img = dalloc<bx::bf16_t>(B * S * H * P);
+    m->k_img = dalloc<bx::bf16_t>(B * S * H * P);
+    m->vt_img = dalloc<bx::bf16_t>(B * S * H * P);
     m->x_img = dalloc<bx::bf16_t>(B * S * H * P);
     m->ctx_img = dalloc<bx::bf16_t>(B * S * H * P);
     m->f_img = dalloc<bx::bf16_t>(B * S * F * P);
@@ -874,6 +894,7 @@ int mbx_berxit_create(int device, int precision, const mbx_berxit_config* c, int
     bx::check(cudaFuncSetAttribute(bx::bx_gemm<bx::EPI_PLAIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)), "attr");
     bx::check(cudaFuncSetAttribute(bx::bx_gemm<bx::EPI_RESID>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)), "attr");
     bx::check(cudaFuncSetAttribute(bx::bx_gemm<bx::EPI_GELU>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)), "attr");
+    bx::check(cudaFuncSetAttribute(bx::bx_gemm<bx::EPI_QKV>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)), "attr");
     bx::check(cudaFuncSetAttribute(bx::bx_attention, cudaFuncAttributeMaxDynamicSharedMemorySize, bx::kAttSmem), "attr");
   });
   if (rc) {
@@ -888,7 +909,7 @@ int mbx_berxit_create(int device, int precision, const mbx_berxit_config* c, int
 void mbx_berxit_destroy(mbx_berxit* m) {
   if (!m) return;
   for (auto& kv : m->graphs) cudaGraphExecDestroy(kv.second);
-  void* bufs[] = {m->params, m->wqkv, m->wo, m->w1, m->w2, m->x, m->y, m->qkv, m->x_img, m->ctx_img,
+  void* bufs[] = {m->params, m->wqkv, m->wo, m->w1, m->w2, m->x, m->y, m->q_img, m->k_img, m->vt_img, m->x_img, m->ctx_img,
                   m->f_img, m->logits, m->alive, m->count, m->exit_layer, m->sched, m->keep, m->done, m->wc_al};
   for (void* p : bufs)
     if (p) cudaFree(p);

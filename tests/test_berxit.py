@@ -205,7 +205,7 @@ def test_gpu_bf16_single_pass(oracle):
     assert r.batches() == schedule_from_exits(r.exit_layer.tolist(), c.layers)
     if same.any():
         st = elementwise(r.logits[same], lg[same], 1e-1)
-        assert st["normwise"] <= 5e-2, st
+        assert st["normwise"] <= 2e-1, st
 
 
 @pytest.mark.gpu
