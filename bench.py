@@ -424,6 +424,8 @@ def run_ours(args):
         line["other_configs"] = other_configs(mbx, torch, local)
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args, nodes)
+    if world == 1 and not args.no_other_configs:
+        line["berxit"] = berxit_section(mbx, torch, local, l2, pk, cpu=not args.no_cpu_baseline)
     print(json.dumps(line))
     if dist:
         dist.barrier()
@@ -467,6 +469,106 @@ def other_configs(mbx, torch, local, reps=5):
         m.close()
         ctx.close()
     return out
+
+
+# ACRoBat's published Berxit latencies (BERT-base "small", RTX 3070).
+BERXIT_PUBLISHED_MS = {64: 204.54, 8: 38.49}
+
+
+def berxit_section(mbx, torch, local, l2, pk, cpu=True, reps=10):
+    """BASELINE configs[4]: Berxit early-exit BERT-base encoder (include/mbx_berxit.h), batch 64 and 8,
+    bf16x3 tensor cores.  Parity against tests/golden/berxit.json.gz (oracle-made, parity
+    unpinned); device ms per mini-batch (inputs resident, CUDA events on the model's stream, L2
+    flushed before every mini-batch) and e2e ms (pinned host inputs H2D + run + results D2H through
+    mbx_berxit_run); the published ACRoBat latency beside it."""
+    import gzip
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from parity_metrics import elementwise
+    with gzip.open(os.path.join(ROOT, "tests", "golden", "berxit.json.gz"), "rt") as f:
+        runs = {r["batch"]: r for r in json.load(f)["runs"] if r["name"] == "bert-base"}
+    out = {}
+    for b in (64, 8):
+        run = runs[b]
+        c = mbx.berxit_config(**run["config"])
+        m = mbx.Berxit(local, "bf16x3", c, max_batch=b)
+        m.make_params(run["seed"])
+        xh = torch.from_numpy(mbx.berxit_make_inputs(c, run["seed"], b)).pin_memory()
+        xd = xh.to(f"cuda:{local}")
+        r = m.run(xh.numpy())
+        want_lg = np.asarray(run["logits"], np.float32)
+        st = elementwise(r.logits, want_lg, 1e-3)
+        scale = np.sqrt(np.mean(want_lg.astype(np.float64) ** 2, axis=-1, keepdims=True))
+        parity = {"golden": f"tests/golden/berxit.json.gz bert-base b{b} seed {run['seed']} (oracle, parity unpinned)",
+                  "exit_layers_equal": bool(np.array_equal(r.exit_layer, run["exit_layer"])),
+                  "schedule_equal": r.batches() == [[i for i, e in enumerate(run["exit_layer"]) if e >= l]
+                                                    for l in range(c.layers)],
+                  "max_rel": st["max_rel"], "frac_pass_rel1e-3": st["frac_pass"], "normwise": st["normwise"],
+                  "max_err_over_row_rms": float(np.max(np.abs(r.logits - want_lg) / scale))}
+        stream = torch.cuda.ExternalStream(m.stream(), device=local)
+        for _ in range(3):
+            m.run_device(b, xd.data_ptr())
+        torch.cuda.synchronize(local)
+        dev, e2e = [], []
+        for _ in range(reps):
+            l2.zero_()
+            torch.cuda.synchronize(local)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            m.run_device(b, xd.data_ptr())
+            e1.record(stream)
+            e1.synchronize()
+            dev.append(e0.elapsed_time(e1))
+        lg = np.empty((b, c.classes), np.float32)
+        ex = np.empty(b, np.int32)
+        for _ in range(reps):
+            l2.zero_()
+            torch.cuda.synchronize(local)
+            t0 = time.perf_counter()
+            m.run_into(xh.numpy(), lg, ex)
+            e2e.append((time.perf_counter() - t0) * 1e3)
+        layer_inst = sum(len(bt) for bt in r.batches())
+        H, F, S = c.hidden, c.ffn, c.seq
+        flops = layer_inst * S * 2 * (4 * H * H + 2 * H * F + 2 * S * H)  # GEMMs + the two attention products
+        ms = statistics.median(dev)
+        tensor = flops * 3 / (ms * 1e-3) / 1e12  # bf16x3: three tcgen05 products per contraction
+        out[f"b{b}"] = {
+            "ms_per_minibatch": ms, "ms_min": min(dev), "e2e_ms_per_minibatch": statistics.median(e2e),
+            "h2d_bytes": int(xh.numel() * 4), "d2h_bytes": int(b * (c.classes + 1 + c.layers) * 4),
+            "published_acrobat_ms": BERXIT_PUBLISHED_MS[b], "published_hw": "RTX 3070 (PAPER.md:846-847)",
+            "speedup_vs_published_e2e": BERXIT_PUBLISHED_MS[b] / statistics.median(e2e),
+            "layer_instances": layer_inst, "exits_per_layer": np.bincount(r.exit_layer, minlength=c.layers).tolist(),
+            "launches_per_minibatch": m.launches_per_batch(b),
+            "roofline": {"bound": "tensor", "achieved_algorithmic_tflops": flops / (ms * 1e-3) / 1e12,
+                         "achieved_tensor_tflops": tensor, "peak": pk["bf16_tflops_sustained"], "unit": "TFLOP/s",
+                         "frac": tensor / pk["bf16_tflops_sustained"],
+                         "def": "tensor = 3 split-bf16 products per algorithmic FMA; peak = measured sustained bf16"},
+            "parity": parity}
+        del m
+    cfg = mbx.berxit_config()
+    out["config"] = {"model": "Berxit (BERT-base, shared layers, LTE exit)", "hidden": cfg.hidden, "heads": cfg.heads,
+                     "ffn": cfg.ffn, "layers": cfg.layers, "seq": cfg.seq, "classes": cfg.classes,
+                     "exit_threshold": cfg.exit_threshold, "precision": "bf16x3", "l2": "flushed before each mini-batch"}
+    if cpu:
+        out["cpu_baseline"] = berxit_cpu(mbx, runs[64])
+    return out
+
+
+def berxit_cpu(mbx, run):
+    """The oracle restatement (oracle/berxit_oracle.cpp, the only CPU Berxit: the reference has none)
+    on one full-depth instance, one thread."""
+    from test_berxit import BerxitOracle
+    o = BerxitOracle()
+    c = mbx.berxit_config(**run["config"])
+    i = run["exit_layer"].index(c.layers - 1)
+    p = o.params(c, run["seed"])
+    x = o.inputs(c, run["seed"], [i])
+    t0 = time.perf_counter()
+    o.run(c, p, x, threads=1)
+    s = time.perf_counter() - t0
+    mean_layers = (np.mean(run["exit_layer"]) + 1) / c.layers
+    return {"kind": "port", "cores": 1, "s_per_instance_12_layers": s,
+            "ms_per_minibatch_b64_1core": s * 1e3 * 64 * mean_layers,
+            "sample": f"oracle, instance {i} (exits after layer {c.layers}), one thread"}
 
 
 def pinned_inputs(torch, toks, data):

@@ -788,6 +788,11 @@ class Berxit:
                                          _ptr(ex, ctypes.c_int32), _ptr(sc, ctypes.c_int32)))
         return BerxitResult(lg, ex, sc)
 
+    def run_into(self, x: np.ndarray, logits: np.ndarray, exit_layer: np.ndarray):
+        """``run`` into caller-owned output arrays, without the schedule (the e2e timing call)."""
+        self._check(lib().mbx_berxit_run(self.h, x.shape[0], _ptr(x, ctypes.c_float), _ptr(logits, ctypes.c_float),
+                                         _ptr(exit_layer, ctypes.c_int32), None))
+
     def run_device(self, batch: int, x_dev_ptr: int):
         """Enqueues one mini-batch whose inputs are at device address x_dev_ptr (asynchronous)."""
         self._check(lib().mbx_berxit_run_device(self.h, batch, ctypes.c_void_p(x_dev_ptr)))

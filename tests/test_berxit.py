@@ -222,3 +222,31 @@ def test_gpu_device_resident_run_matches_host_run():
     got = m.read(8)
     assert np.array_equal(got.logits.view(np.uint32), want.logits.view(np.uint32))
     assert np.array_equal(got.schedule, want.schedule)
+
+
+# ------------------------------------------------------------------------------ golden (oracle-made)
+def _golden_runs():
+    from conftest import load_golden
+    return load_golden("berxit")["runs"]
+
+
+def test_oracle_reproduces_golden(oracle):
+    """The restatement still produces the committed vectors (oracle/make_berxit_golden.py)."""
+    run = next(r for r in _golden_runs() if r["name"] == "small")
+    c = mbx.berxit_config(**{k: v for k, v in run["config"].items()})
+    lg, ex = oracle.run(c, oracle.params(c, run["seed"]), oracle.inputs(c, run["seed"], range(run["batch"])))
+    assert ex.tolist() == run["exit_layer"]
+    assert np.array_equal(lg, np.asarray(run["logits"], np.float32))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("idx", [0, 1, 2])
+def test_gpu_matches_golden_every_instance(idx):
+    run = _golden_runs()[idx]
+    c = mbx.berxit_config(**run["config"])
+    m = mbx.Berxit(0, "bf16x3", c, max_batch=run["batch"])
+    m.make_params(run["seed"])
+    r = m.run(mbx.berxit_make_inputs(c, run["seed"], run["batch"]))
+    want_ex = np.asarray(run["exit_layer"], np.int32)
+    st = _check(r, np.asarray(run["logits"], np.float32), want_ex, c.layers)
+    print("berxit golden", run["name"], run["batch"], st)
