@@ -58,7 +58,8 @@ constexpr int kNT = 256;        // MMA N per tile
 constexpr int kKC = 64;         // K chunk (elements)
 constexpr int kABlock = kSeq * kKC;  // bf16 elements of one A chunk part (16 KB)
 constexpr int kWBlock = kNT * kKC;   // bf16 elements of one W chunk part (32 KB)
-constexpr int kGemmThreads = 192;
+constexpr int kEpiWarps = 8;  // two per TMEM lane quarter, each draining half of a tile's columns
+constexpr int kGemmThreads = 64 + 32 * kEpiWarps;
 constexpr int kStageSmem = 192 * 1024;
 
 enum Epi { EPI_PLAIN = 0, EPI_RESID = 1, EPI_GELU = 2, EPI_QKV = 3 };
@@ -90,6 +91,13 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
                    smem_u32(dst)),
                "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
+}
+// Programmatic dependent launch: every kernel after the first of a mini-batch is launched while
+// its predecessor runs; it sets up shared memory / TMEM, then waits here for the predecessor's
+// completion (and memory) before touching anything in HBM, and lets its own successor launch.
+__device__ __forceinline__ void pdl_wait_and_release() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
@@ -190,6 +198,71 @@ struct GemmArgs {
   int H;
 };
 
+// Fused epilogue of one accumulator tile: row r of instance `inst`, columns n0 .. n0 + NT; tm is
+// the TMEM address of this warp's lane quarter at the tile's first column.
+template <int EPI>
+__device__ __forceinline__ void epilogue_tile(const GemmArgs& g, unsigned tm, int inst, int n0, int NT, int r,
+                                              int half) {
+  const int P = g.P;
+  const int ncc = NT / 64;  // 32-column groups per epilogue warp
+#pragma unroll 1
+  for (int cc = half * ncc; cc < (half + 1) * ncc; ++cc) {
+    float v[32];
+    tmem_ld32(tm + unsigned(cc * 32), v);
+    const int col0 = n0 + cc * 32;
+    const float4* b4 = reinterpret_cast<const float4*>(g.bias + col0);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float4 b = __ldg(b4 + j);
+      v[4 * j] += b.x;
+      v[4 * j + 1] += b.y;
+      v[4 * j + 2] += b.z;
+      v[4 * j + 3] += b.w;
+    }
+    const size_t row = ((size_t)inst * kSeq + r) * g.N + col0;
+    if (EPI == EPI_GELU) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = gelu(v[j]);
+      store_img_row<4>(g.out_img, g.N / kKC, P, inst, r, col0, v);
+    } else if (EPI == EPI_QKV) {
+      const int H = g.H, sec = col0 / H, c = col0 - sec * H;
+      if (sec == 0) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] *= 0.125f;  // 1 / sqrt(64), exact
+        store_img_row<4>(g.out_img, H / kKC, P, inst, r, c, v);
+      } else if (sec == 1) {
+        store_img_row<4>(g.k_img, H / kKC, P, inst, r, c, v);
+      } else {
+        const int h = c >> 6, d0 = c & 63;
+        bf16_t* vb = g.vt_img + (((size_t)inst * (H / 64) + h) * 2 + (r >> 6)) * P * 4096;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          unsigned short hi, lo;
+          split2(v[j], hi, lo);
+          const int e = canon(d0 + j, r & 63);
+          vb[e] = hi;
+          if (P > 1) vb[e + 4096] = lo;
+        }
+      }
+    } else {
+      if (EPI == EPI_RESID) {
+        const float4* r4 = reinterpret_cast<const float4*>(g.resid + row);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float4 x = r4[j];
+          v[4 * j] = x.x + v[4 * j];
+          v[4 * j + 1] = x.y + v[4 * j + 1];
+          v[4 * j + 2] = x.z + v[4 * j + 2];
+          v[4 * j + 3] = x.w + v[4 * j + 3];
+        }
+      }
+      float4* o4 = reinterpret_cast<float4*>(g.out + row);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) o4[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+    }
+  }
+}
+
 template <int EPI>
 __global__ void __launch_bounds__(kGemmThreads, 1) bx_gemm(GemmArgs g) {
   extern __shared__ __align__(1024) unsigned char smem[];
@@ -206,8 +279,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1) bx_gemm(GemmArgs g) {
   unsigned* tmem_slot = reinterpret_cast<unsigned*>(bars + 20);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int count = *g.count;
-  const int ntile_total = count * g.ntiles;
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
@@ -215,7 +286,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) bx_gemm(GemmArgs g) {
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&acc_full[a], 1);
-      mbar_init(&acc_empty[a], 128);
+      mbar_init(&acc_empty[a], 32 * kEpiWarps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -229,6 +300,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1) bx_gemm(GemmArgs g) {
   __syncthreads();
   tc_fence_after();
   const unsigned tmem = *tmem_slot;
+  pdl_wait_and_release();
+  const int count = *g.count;
+  const int ntile_total = count * g.ntiles;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -289,62 +363,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) bx_gemm(GemmArgs g) {
       const int inst = g.alive[t / g.ntiles], n0 = (t % g.ntiles) * NT;
       mbar_wait(&acc_full[acc], (tc >> 1) & 1);
       tc_fence_after();
-#pragma unroll 1
-      for (int cc = 0; cc < NT / 32; ++cc) {
-        float v[32];
-        tmem_ld32(tmem + (unsigned(32 * q) << 16) + unsigned(acc * kNT + cc * 32), v);
-        const int col0 = n0 + cc * 32;
-        const float4* b4 = reinterpret_cast<const float4*>(g.bias + col0);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const float4 b = __ldg(b4 + j);
-          v[4 * j] += b.x;
-          v[4 * j + 1] += b.y;
-          v[4 * j + 2] += b.z;
-          v[4 * j + 3] += b.w;
-        }
-        const size_t row = ((size_t)inst * kSeq + r) * g.N + col0;
-        if (EPI == EPI_GELU) {
-#pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] = gelu(v[j]);
-          store_img_row<4>(g.out_img, g.N / kKC, P, inst, r, col0, v);
-        } else if (EPI == EPI_QKV) {
-          const int H = g.H, sec = col0 / H, c = col0 - sec * H;
-          if (sec == 0) {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] *= 0.125f;  // 1 / sqrt(64), exact
-            store_img_row<4>(g.out_img, H / kKC, P, inst, r, c, v);
-          } else if (sec == 1) {
-            store_img_row<4>(g.k_img, H / kKC, P, inst, r, c, v);
-          } else {
-            const int h = c >> 6, d0 = c & 63;
-            bf16_t* vb = g.vt_img + (((size_t)inst * (H / 64) + h) * 2 + (r >> 6)) * P * 4096;
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              unsigned short hi, lo;
-              split2(v[j], hi, lo);
-              const int e = canon(d0 + j, r & 63);
-              vb[e] = hi;
-              if (P > 1) vb[e + 4096] = lo;
-            }
-          }
-        } else {
-          if (EPI == EPI_RESID) {
-            const float4* r4 = reinterpret_cast<const float4*>(g.resid + row);
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              const float4 x = r4[j];
-              v[4 * j] = x.x + v[4 * j];
-              v[4 * j + 1] = x.y + v[4 * j + 1];
-              v[4 * j + 2] = x.z + v[4 * j + 2];
-              v[4 * j + 3] = x.w + v[4 * j + 3];
-            }
-          }
-          float4* o4 = reinterpret_cast<float4*>(g.out + row);
-#pragma unroll
-          for (int j = 0; j < 8; ++j) o4[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-        }
-      }
+      epilogue_tile<EPI>(g, tmem + (unsigned(32 * q) << 16) + unsigned(acc * kNT), inst, n0, NT, r, (warp - 2) >> 2);
       tc_fence_before();
       mbar_arrive(&acc_empty[acc]);
     }
@@ -392,6 +411,7 @@ __global__ void __launch_bounds__(128, 2) bx_attention(const bf16_t* q_img, cons
   unsigned long long* bar = reinterpret_cast<unsigned long long*>(asmem + 98304);
   unsigned* tmem_slot = reinterpret_cast<unsigned*>(asmem + 98304 + 32);
   const int m = blockIdx.y, h = blockIdx.x;
+  pdl_wait_and_release();
   if (m >= *count) return;
   const int inst = alive[m];
   const int t = threadIdx.x, warp = t >> 5;
@@ -524,6 +544,7 @@ __global__ void __launch_bounds__(256) bx_layernorm(const float* y, float* x, bf
                                                     int P, float eps, ExitArgs ex) {
   const int row = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   const int m = row / kSeq, r = row % kSeq;
+  pdl_wait_and_release();
   const int n = *count;
   if (m < n) {
     const int inst = alive[m];
@@ -640,6 +661,7 @@ __global__ void bx_begin(int* alive, int* count, int* exit_layer, int* sched, in
 
 __global__ void __launch_bounds__(256) bx_to_image(const float* x, bf16_t* x_img, int H, int P, int b) {
   // one thread per (instance, row, 8-column group)
+  pdl_wait_and_release();
   const size_t g8 = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   const size_t per_inst = (size_t)kSeq * (H / 8);
   if (g8 >= per_inst * b) return;
@@ -732,6 +754,23 @@ T* dalloc(size_t n) {
   return static_cast<T*>(p);
 }
 
+// Launch with programmatic stream serialization (the kernel's pdl_wait_and_release orders it
+// after its predecessor); captured into the mini-batch graph as programmatic edges.
+template <class... KArgs, class... Args>
+void launch_pdl(void (*kernel)(KArgs...), dim3 grid, int threads, size_t smem, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  bx::check(cudaLaunchKernelEx(&cfg, kernel, args...), "berxit launch");
+}
+
 void launch_gemm(mbx_berxit* m, int b, int epi, const bx::bf16_t* a_img, const bx::bf16_t* w_img, int K, int N,
                  const float* bias, const float* resid, float* out, bx::bf16_t* out_img) {
   // Tile width: the smallest makespan ceil(tiles / SMs) x (width + fixed per-tile cost) for a
@@ -747,10 +786,10 @@ void launch_gemm(mbx_berxit* m, int b, int epi, const bx::bf16_t* a_img, const b
   const int grid = (int)std::min<long>(m->sms, (long)b * g.ntiles);
   const size_t smem = bx::kStageSmem + 256;
   switch (epi) {
-    case bx::EPI_PLAIN: bx::bx_gemm<bx::EPI_PLAIN><<<grid, bx::kGemmThreads, smem, m->stream>>>(g); break;
-    case bx::EPI_RESID: bx::bx_gemm<bx::EPI_RESID><<<grid, bx::kGemmThreads, smem, m->stream>>>(g); break;
-    case bx::EPI_GELU: bx::bx_gemm<bx::EPI_GELU><<<grid, bx::kGemmThreads, smem, m->stream>>>(g); break;
-    default: bx::bx_gemm<bx::EPI_QKV><<<grid, bx::kGemmThreads, smem, m->stream>>>(g); break;
+    case bx::EPI_PLAIN: launch_pdl(bx::bx_gemm<bx::EPI_PLAIN>, grid, bx::kGemmThreads, smem, m->stream, g); break;
+    case bx::EPI_RESID: launch_pdl(bx::bx_gemm<bx::EPI_RESID>, grid, bx::kGemmThreads, smem, m->stream, g); break;
+    case bx::EPI_GELU: launch_pdl(bx::bx_gemm<bx::EPI_GELU>, grid, bx::kGemmThreads, smem, m->stream, g); break;
+    default: launch_pdl(bx::bx_gemm<bx::EPI_QKV>, grid, bx::kGemmThreads, smem, m->stream, g); break;
   }
   bx::check(cudaGetLastError(), "bx_gemm launch");
 }
@@ -762,22 +801,24 @@ void enqueue(mbx_berxit* m, int b) {
   const size_t wp = 3 * (size_t)H * H;
   bx::bx_begin<<<1, 256, 0, m->stream>>>(m->alive, m->count, m->exit_layer, m->sched, b, m->bmax, L);
   const size_t groups = (size_t)b * bx::kSeq * (H / 8);
-  bx::bx_to_image<<<unsigned((groups + 255) / 256), 256, 0, m->stream>>>(m->x, m->x_img, H, P, b);
+  launch_pdl(bx::bx_to_image, dim3(unsigned((groups + 255) / 256)), 256, 0, m->stream, (const float*)m->x, m->x_img, H,
+             P, b);
   (void)wp;
   for (int l = 0; l < L; ++l) {
     launch_gemm(m, b, bx::EPI_QKV, m->x_img, m->wqkv, H, 3 * H, m->bqkv, nullptr, nullptr, m->q_img);
-    bx::bx_attention<<<dim3(c.heads, m->bmax), 128, bx::kAttSmem, m->stream>>>(
-        m->q_img, m->k_img, m->vt_img, m->ctx_img, m->alive, m->count, H, P);
+    launch_pdl(bx::bx_attention, dim3(c.heads, m->bmax), 128, bx::kAttSmem, m->stream, (const bx::bf16_t*)m->q_img,
+               (const bx::bf16_t*)m->k_img, (const bx::bf16_t*)m->vt_img, m->ctx_img, (const int*)m->alive,
+               (const int*)m->count, H, P);
     launch_gemm(m, b, bx::EPI_RESID, m->ctx_img, m->wo, H, H, m->bo, m->x, m->y, nullptr);
     bx::ExitArgs off{};
-    bx::bx_layernorm<<<m->bmax * bx::kSeq / 8, 256, 0, m->stream>>>(m->y, m->x, m->x_img, m->g1, m->be1, m->alive,
-                                                                    m->count, H, P, c.ln_eps, off);
+    launch_pdl(bx::bx_layernorm, dim3(m->bmax * bx::kSeq / 8), 256, 0, m->stream, (const float*)m->y, m->x, m->x_img,
+               m->g1, m->be1, (const int*)m->alive, (const int*)m->count, H, P, c.ln_eps, off);
     launch_gemm(m, b, bx::EPI_GELU, m->x_img, m->w1, H, F, m->b1, nullptr, nullptr, m->f_img);
     launch_gemm(m, b, bx::EPI_RESID, m->f_img, m->w2, F, H, m->b2, m->x, m->y, nullptr);
     bx::ExitArgs ex{1, m->wl, m->bl, m->wc, m->bc, m->logits, m->exit_layer, m->sched, m->keep, m->done,
                     m->alive, m->count, c.classes, l, L, m->bmax, c.exit_threshold};
-    bx::bx_layernorm<<<m->bmax * bx::kSeq / 8, 256, 0, m->stream>>>(m->y, m->x, m->x_img, m->g2, m->be2, m->alive,
-                                                                    m->count, H, P, c.ln_eps, ex);
+    launch_pdl(bx::bx_layernorm, dim3(m->bmax * bx::kSeq / 8), 256, 0, m->stream, (const float*)m->y, m->x, m->x_img,
+               m->g2, m->be2, (const int*)m->alive, (const int*)m->count, H, P, c.ln_eps, ex);
     bx::check(cudaGetLastError(), "berxit layer launch");
   }
 }
@@ -895,6 +936,7 @@ int mbx_berxit_create(int device, int precision, const mbx_berxit_config* c, int
     bx::check(cudaFuncSetAttribute(bx::bx_gemm<bx::EPI_RESID>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)), "attr");
     bx::check(cudaFuncSetAttribute(bx::bx_gemm<bx::EPI_GELU>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)), "attr");
     bx::check(cudaFuncSetAttribute(bx::bx_gemm<bx::EPI_QKV>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)), "attr");
+
     bx::check(cudaFuncSetAttribute(bx::bx_attention, cudaFuncAttributeMaxDynamicSharedMemorySize, bx::kAttSmem), "attr");
   });
   if (rc) {
