@@ -9,7 +9,7 @@ from parity_metrics import elementwise
 
 runs = {r["batch"]: r for r in json.load(gzip.open("tests/golden/berxit.json.gz", "rt"))["runs"] if r["name"] == "bert-base"}
 l2 = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
-for b in (64, 8):
+for b in [int(a) for a in sys.argv[1:]] or (64, 8):
     run = runs[b]
     c = mbx.berxit_config(**run["config"])
     m = mbx.Berxit(0, "bf16x3", c, max_batch=b)
