@@ -189,8 +189,8 @@ struct GemmArgs {
   bf16_t* out_img;      // EPI_GELU: [inst][N/64][P][128 x 64]
   const int* alive;
   const int* count;
-  int kch, ntiles, N, P;
-  int nt;  // tile width (MMA N): 256, 128 or 64 — a row range of the weight image's 256-row tiles
+  int kch, N, P;
+  int nt;  // tile width chosen on the host for the batch size (256, 128 or 64)
   // EPI_QKV: out_img = Q image (scaled by 1/8), k_img = K image ([inst][head][part][128 x 64],
   // i.e. A images with one chunk per head), vt_img = V^T image ([inst][head][key chunk][part][64 x 64])
   bf16_t* k_img;
@@ -267,20 +267,16 @@ template <int EPI>
 __global__ void __launch_bounds__(kGemmThreads, 1) bx_gemm(GemmArgs g) {
   extern __shared__ __align__(1024) unsigned char smem[];
   const int P = g.P;
-  const int NT = g.nt;
-  const unsigned a_bytes = unsigned(P) * kABlock * 2, w_part = unsigned(NT) * 128, w_bytes = unsigned(P) * w_part;
-  const unsigned stage_bytes = a_bytes + w_bytes;
-  const int S = kStageSmem / int(stage_bytes);
   unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem + kStageSmem);
-  unsigned long long* full = bars;          // [S]
-  unsigned long long* empty = bars + 8;     // [S]
+  unsigned long long* full = bars;          // [S <= 8]
+  unsigned long long* empty = bars + 8;     // [S <= 8]
   unsigned long long* acc_full = bars + 16; // [2]
   unsigned long long* acc_empty = bars + 18;  // [2]
   unsigned* tmem_slot = reinterpret_cast<unsigned*>(bars + 20);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < S; ++s) {
+    for (int s = 0; s < 8; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
@@ -302,13 +298,29 @@ __global__ void __launch_bounds__(kGemmThreads, 1) bx_gemm(GemmArgs g) {
   const unsigned tmem = *tmem_slot;
   pdl_wait_and_release();
   const int count = *g.count;
-  const int ntile_total = count * g.ntiles;
+  // Tile width (MMA N: 256, 128 or 64, a row range of the weight image's 256-row tiles) for THIS
+  // layer's running count, known only here: the smallest modelled makespan, ceil(tiles / CTAs) x
+  // (width + per-tile cost) + the last tile's exposed epilogue (~3/4 width).  The width never
+  // changes a column's accumulation order, only the parallelism.
+  int NT = g.nt;
+  if (count * (g.N / NT) < int(gridDim.x) / 2) {  // most CTAs idle at the host's width: narrow it
+    int best = -1;
+    for (int w = 256; w >= 64; w >>= 1) {
+      const int tiles = count * (g.N / w), rounds = (tiles + gridDim.x - 1) / gridDim.x, cost = rounds * (w + 48) + 3 * w / 4;
+      if (best < 0 || cost < best) best = cost, NT = w;
+    }
+  }
+  const int ntiles = g.N / NT;
+  const unsigned a_bytes = unsigned(P) * kABlock * 2, w_part = unsigned(NT) * 128, w_bytes = unsigned(P) * w_part;
+  const unsigned stage_bytes = a_bytes + w_bytes;
+  const int S = kStageSmem / int(stage_bytes);
+  const int ntile_total = count * ntiles;
 
   if (warp == 0) {
     if (lane == 0) {
       int it = 0;
       for (int t = blockIdx.x; t < ntile_total; t += gridDim.x) {
-        const int inst = g.alive[t / g.ntiles], n0 = (t % g.ntiles) * NT;
+        const int inst = g.alive[t / ntiles], n0 = (t % ntiles) * NT;
         const bf16_t* a = g.a_img + (size_t)inst * g.kch * P * kABlock;
         // rows n0 .. n0 + NT of the 256-row image tile: a contiguous range of each part block
         const bf16_t* w = g.w_img + (size_t)(n0 / kNT) * g.kch * P * kWBlock + (n0 % kNT) * kKC;
@@ -360,7 +372,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) bx_gemm(GemmArgs g) {
     int tc = 0;
     for (int t = blockIdx.x; t < ntile_total; t += gridDim.x, ++tc) {
       const int acc = tc & 1;
-      const int inst = g.alive[t / g.ntiles], n0 = (t % g.ntiles) * NT;
+      const int inst = g.alive[t / ntiles], n0 = (t % ntiles) * NT;
       mbar_wait(&acc_full[acc], (tc >> 1) & 1);
       tc_fence_after();
       epilogue_tile<EPI>(g, tmem + (unsigned(32 * q) << 16) + unsigned(acc * kNT), inst, n0, NT, r, (warp - 2) >> 2);
@@ -773,17 +785,18 @@ void launch_pdl(void (*kernel)(KArgs...), dim3 grid, int threads, size_t smem, c
 
 void launch_gemm(mbx_berxit* m, int b, int epi, const bx::bf16_t* a_img, const bx::bf16_t* w_img, int K, int N,
                  const float* bias, const float* resid, float* out, bx::bf16_t* out_img) {
-  // Tile width: the smallest makespan ceil(tiles / SMs) x (width + fixed per-tile cost) for a
-  // batch of b running instances (BERT-base b64: 256 for QKV / W1, 128 for Wo / W2).
+  // Tile width for a batch of b running instances: the smallest makespan ceil(tiles / SMs) x
+  // (width + fixed per-tile cost) (BERT-base b64: 256 for QKV / W1, 128 for Wo / W2).  The kernel
+  // narrows it when the layer's running count (known only on the device) leaves most CTAs idle.
   int nt = 256;
   long best = -1;
   for (int w : {256, 128, 64}) {
     const long tiles = (long)b * (N / w), rounds = (tiles + m->sms - 1) / m->sms, cost = rounds * (w + 48);
     if (best < 0 || cost < best) best = cost, nt = w;
   }
-  bx::GemmArgs g{a_img, w_img, bias, resid, out, out_img, m->alive, m->count, K / bx::kKC, N / nt, N, m->P, nt,
+  bx::GemmArgs g{a_img, w_img, bias, resid, out, out_img, m->alive, m->count, K / bx::kKC, N, m->P, nt,
                  m->k_img, m->vt_img, m->c.hidden};
-  const int grid = (int)std::min<long>(m->sms, (long)b * g.ntiles);
+  const int grid = (int)std::min<long>(m->sms, (long)b * (N / 64));
   const size_t smem = bx::kStageSmem + 256;
   switch (epi) {
     case bx::EPI_PLAIN: launch_pdl(bx::bx_gemm<bx::EPI_PLAIN>, grid, bx::kGemmThreads, smem, m->stream, g); break;
